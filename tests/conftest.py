@@ -1,0 +1,37 @@
+"""pytest configuration: markers, repo on sys.path, shared helpers."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA B200 (run with -m gpu on the GPU box)")
+    config.addinivalue_line("markers", "slow: long CPU test, opt-in with LOKA_SLOW=1")
+    config.addinivalue_line("markers", "dist: multi-process torch.distributed test (gloo on CPU)")
+
+
+def pytest_collection_modifyitems(config, items):
+    if os.environ.get("LOKA_SLOW") == "1":
+        return
+    skip = pytest.mark.skip(reason="slow test; set LOKA_SLOW=1")
+    for it in items:
+        if "slow" in it.keywords:
+            it.add_marker(skip)
+
+
+@pytest.fixture(scope="session")
+def fp8_host_cast(tmp_path_factory):
+    """Build the test-only cuda_fp8.hpp host-cast helper (tests/helpers/fp8_host_cast.cpp)."""
+    out = tmp_path_factory.mktemp("helpers") / "fp8_host_cast"
+    src = os.path.join(ROOT, "tests", "helpers", "fp8_host_cast.cpp")
+    cuda_inc = os.path.join(os.environ.get("CUDA_HOME", "/usr/local/cuda"), "include")
+    r = subprocess.run(["g++", "-O2", "-I", cuda_inc, src, "-o", str(out)], capture_output=True, text=True)
+    if r.returncode != 0:
+        pytest.skip("cannot build cuda_fp8 host helper: " + r.stderr[-300:])
+    return str(out)

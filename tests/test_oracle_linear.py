@@ -1,0 +1,108 @@
+"""Pins for oracle/linear.py (O7-O10): SPEC GEMM examples, a pure-Python triple loop with
+exactly-rounded sums, finite differences for the backward directions, an exact integer
+construction, and torch float64 LayerNorm/RMSNorm (library) plus the SPEC norm properties."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+from oracle import linear as L, quantize as Q
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def test_gemm_identity_and_1x1():
+    rng = np.random.default_rng(0)
+    w = rng.standard_normal((5, 6))
+    assert np.array_equal(L.fwd(np.eye(6), w), w.T)  # SPEC.md:127 (x = I_K -> w^T)
+    g = GOLD["gemm_1x1"]
+    assert L.fwd(np.array([[g["x"]]]), np.array([[g["w"]]]))[0, 0] == g["out"]
+
+
+def test_gemm_vs_python_triple_loop():
+    rng = np.random.default_rng(1)
+    x, w = rng.standard_normal((8, 8)), rng.standard_normal((8, 8))
+    ref = [[math.fsum(x[i, k] * w[n, k] for k in range(8)) for n in range(8)] for i in range(8)]
+    assert np.allclose(L.fwd(x, w), np.array(ref), rtol=1e-14, atol=1e-14)
+
+
+def test_directions_are_gradients_of_fwd():
+    """SPEC.md:148 direction consistency: dgrad/wgrad = finite-difference gradients of
+    L(X, W) = sum(G * fwd(X, W))."""
+    rng = np.random.default_rng(2)
+    x, w, g = rng.standard_normal((4, 3)), rng.standard_normal((5, 3)), rng.standard_normal((4, 5))
+    loss = lambda xx, ww: float(np.sum(g * L.fwd(xx, ww)))
+    h = 1e-5
+    fx = np.zeros_like(x)
+    for idx in np.ndindex(*x.shape):
+        e = np.zeros_like(x); e[idx] = h
+        fx[idx] = (loss(x + e, w) - loss(x - e, w)) / (2 * h)
+    fw = np.zeros_like(w)
+    for idx in np.ndindex(*w.shape):
+        e = np.zeros_like(w); e[idx] = h
+        fw[idx] = (loss(x, w + e) - loss(x, w - e)) / (2 * h)
+    assert np.abs(L.dgrad(g, w) - fx).max() < 1e-8
+    assert np.abs(L.wgrad(g, x) - fw).max() < 1e-8
+
+
+def test_representable_operands_exact():
+    """small-integer FP8 codes with power-of-two scales -> exact products; the
+    oracle result equals exact integer arithmetic."""
+    rng = np.random.default_rng(3)
+    M, N, K = 16, 12, 64
+    xi = rng.integers(-8, 9, (M, K)); wi = rng.integers(-8, 9, (N, K))
+    xc, xs = Q.quantize(xi.astype(float) * 2.0 ** -3, "e4m3", "row", "ue8m0")
+    wc, ws = Q.quantize(wi.astype(float) * 2.0 ** 2, "e4m3", "tensor", "ue8m0")
+    y = L.linear_norm(xc, xs, "e4m3", "row", wc, ws, "e4m3", "tensor")
+    exact = np.array([[sum(int(xi[m, k]) * int(wi[n, k]) for k in range(K)) for n in range(N)] for m in range(M)])
+    assert np.array_equal(y, exact * 2.0 ** -1)
+
+
+def test_layer_and_rms_norm_vs_torch_float64():
+    rng = np.random.default_rng(4)
+    y = rng.standard_normal((33, 96)) * 3 + 1
+    gam, bet = rng.standard_normal(96), rng.standard_normal(96)
+    t = torch.from_numpy(y)
+    assert np.allclose(L.layer_norm(y), F.layer_norm(t, (96,), eps=1e-5).numpy(), rtol=1e-13, atol=1e-13)
+    assert np.allclose(L.layer_norm(y, 1e-5, gam, bet),
+                       F.layer_norm(t, (96,), torch.from_numpy(gam), torch.from_numpy(bet), 1e-5).numpy(),
+                       rtol=1e-13, atol=1e-13)
+    assert np.allclose(L.rms_norm(y), F.rms_norm(t, (96,), eps=1e-6).numpy(), rtol=1e-13, atol=1e-13)
+    assert np.allclose(L.rms_norm(y, 1e-6, gam), F.rms_norm(t, (96,), torch.from_numpy(gam), 1e-6).numpy(),
+                       rtol=1e-13, atol=1e-13)
+
+
+def test_norm_closed_forms_and_blocknorm_properties():
+    c, eps = GOLD["rmsnorm_constant"]["c"], GOLD["rmsnorm_constant"]["eps"]
+    row = np.full((1, 512), c)
+    assert np.allclose(L.rms_norm(row, eps), c / math.sqrt(c * c + eps), rtol=1e-15)
+    assert np.all(L.layer_norm(row) == 0)
+    rng = np.random.default_rng(5)
+    y = rng.standard_normal((7, 512))
+    assert np.allclose(L.block_rms_norm(y, 512), L.rms_norm(y), rtol=1e-15, atol=0)
+    z = L.block_rms_norm(y, 256)
+    y2 = y.copy(); y2[:, 300] += 100.0   # perturb block 1 only -> block 0 bit-identical
+    z2 = L.block_rms_norm(y2, 256)
+    assert np.array_equal(z[:, :256], z2[:, :256]) and not np.array_equal(z[:, 256:], z2[:, 256:])
+    # a row [big block | small block] -> each block normalised to unit RMS
+    two = np.concatenate([rng.standard_normal((1, 256)) * 1e3, rng.standard_normal((1, 256)) * 1e-2], 1)
+    out = L.block_rms_norm(two, 256)
+    for b in range(2):  # mean(y^2) = rms^2 / (rms^2 + eps) per block
+        ms = np.mean(two[0, b * 256:(b + 1) * 256] ** 2)
+        assert abs(np.mean(out[0, b * 256:(b + 1) * 256] ** 2) - ms / (ms + 1e-6)) < 1e-12
+    with pytest.raises(L.IndivisibleFeatureDim):
+        L.block_rms_norm(np.zeros((2, 300)), 256)
+
+
+def test_bias_then_norm_and_round_bf16():
+    rng = np.random.default_rng(6)
+    y, b = rng.standard_normal((3, 8)), rng.standard_normal(8)
+    assert np.array_equal(L.add_bias(y, b), y + b[None, :])
+    v = np.concatenate([rng.standard_normal(4096).astype(np.float32).astype(np.float64),
+                        np.array([1.0 + 2 ** -8, 1.0 + 3 * 2 ** -8, -(1.0 + 2 ** -8), 2.0 ** -130])])
+    ref = torch.from_numpy(v.astype(np.float32)).to(torch.bfloat16).to(torch.float64).numpy()
+    assert np.array_equal(L.round_bf16(v), ref)  # fp32-exact inputs: torch's cast is a single RNE

@@ -1,0 +1,161 @@
+"""Pins for oracle/quantize.py (O3-O6): SPEC worked examples, a brute-force per-element
+re-derivation using float32 IEEE arithmetic (numpy float32 division/multiplication) and the
+torch CPU FP8 cast (independent of the oracle's table encoder and float64 rounding), and the
+SPEC's invariants (idempotence, monotonicity, granularity refinement)."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import fp8, quantize as Q, probe
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+TORCH_DT = {"e4m3": torch.float8_e4m3fn, "e5m2": torch.float8_e5m2}
+FMAX = {"e4m3": 448.0, "e5m2": 57344.0}
+
+
+def test_spec_rowwise_example():
+    g = GOLD["rowwise_scales"]
+    codes, s = Q.quantize(np.array(g["x"], float), "e4m3", "row")
+    exp = np.array([np.float32(n) / np.float32(g["fmax"]) for n in g["scales_num"]], np.float32)
+    assert np.array_equal(s, exp)
+    # the amax element of each row maps to the max code
+    assert codes[0, 1] == 0x7E and codes[1, 1] == 0x7E
+
+
+def test_spec_tensor_amax_is_max_and_zero_matrix():
+    x = np.array([[448.0, -3.0], [1.0, 0.5]])
+    _, s = Q.quantize(x, "e4m3", "tensor")
+    assert s[0] == GOLD["tensor_amax_equals_max"]["scale"]
+    codes, s = Q.quantize(np.zeros((3, 5)), "e4m3", "tensor")
+    assert s[0] == GOLD["zero_matrix"]["scale"] and (codes == GOLD["zero_matrix"]["code"]).all()
+    codes, s = Q.quantize(-np.zeros((2, 2)), "e4m3", "row")  # sign of zero kept (D2)
+    assert (codes == 0x80).all() and (s == 1).all()
+
+
+def test_identity_and_powers_of_two_roundtrip():
+    """exactly representable inputs roundtrip bit-exactly.  That holds when the
+    scale itself is exact (UE8M0, a power of two).  With FP32 scales s = fl32(amax/448) is a
+    rounded value (1/448 is not a binary fraction), so the roundtrip is exact up to the
+    scale's own rounding: |x_hat - x| <= 2^-24 |x| (D1)."""
+    rng = np.random.default_rng(0)
+    x = np.exp2(rng.integers(-6, 8, (16, 40))) * rng.choice([-1, 1], (16, 40))
+    for arr in (np.eye(7), x):
+        for gran in ("tensor", "row", "blk_1x128"):
+            codes, s = Q.quantize(arr, "e4m3", gran, "ue8m0")
+            assert np.array_equal(Q.dequantize(codes, s, "e4m3", gran), arr)
+            codes, s = Q.quantize(arr, "e4m3", gran, "f32")
+            d = Q.dequantize(codes, s, "e4m3", gran)
+            assert np.all(np.abs(d - arr) <= 2.0 ** -24 * np.abs(arr))
+
+
+def _brute(x, f, gran, scale_fmt="f32"):
+    """Independent per-element re-derivation: explicit granule loops, float32 IEEE ops, torch cast."""
+    rows, cols = x.shape
+    shp = Q.scale_shape(rows, cols, gran)
+    amax = np.zeros(shp)
+    for i in range(rows):
+        for j in range(cols):
+            idx = Q.granule_index(i, j, gran)
+            amax[idx] = max(amax[idx], abs(x[i, j]))
+    fm = np.float32(FMAX[f])
+    s = np.ones(shp, np.float32)
+    r = np.ones(shp, np.float32)
+    for idx in np.ndindex(*shp):
+        a = np.float32(amax[idx])
+        if a > 0:
+            if scale_fmt == "f32":
+                s[idx] = a / fm            # numpy float32 division is IEEE correctly rounded
+                r[idx] = fm / a
+            else:
+                e = -127
+                while np.float64(a) > np.float64(fm) * 2.0 ** e:
+                    e += 1
+                s[idx] = np.float32(2.0 ** e)
+                r[idx] = np.float32(2.0 ** -e)
+    v = np.empty((rows, cols), np.float32)
+    for i in range(rows):
+        for j in range(cols):
+            v[i, j] = np.float32(x[i, j]) * r[Q.granule_index(i, j, gran)]
+    t = torch.from_numpy(v).clamp(-FMAX[f], FMAX[f]).to(TORCH_DT[f]).view(torch.uint8).numpy()
+    return t, s
+
+
+@pytest.mark.parametrize("f", ["e4m3", "e5m2"])
+@pytest.mark.parametrize("gran", Q.GRANS)
+@pytest.mark.parametrize("scale_fmt", ["f32", "ue8m0"])
+def test_quantize_matches_bruteforce(f, gran, scale_fmt):
+    rng = np.random.default_rng(hash((f, gran, scale_fmt)) % 2**32)
+    rows, cols = (130, 260) if gran.startswith("blk_128") else (9, 300)
+    x = (rng.standard_normal((rows, cols)) * np.exp(rng.standard_normal((rows, 1)) * 3)).astype(np.float32)
+    x[0, :5] = 0.0
+    x[3, :] = 0.0  # an all-zero row / granule
+    x = x.astype(np.float64)
+    codes, s = Q.quantize(x, f, gran, scale_fmt)
+    bc, bs = _brute(x, f, gran, scale_fmt)
+    assert np.array_equal(s.view(np.uint32), bs.view(np.uint32))
+    assert np.array_equal(codes, bc)
+
+
+def test_ue8m0_definition_edges():
+    """s = smallest power of two (>= 2^-127) with a <= max*s; probed at max*2^j and neighbours."""
+    for f, fm in FMAX.items():
+        vals = []
+        for j in range(-120, 100):
+            c = np.float32(fm * 2.0 ** j)
+            vals += [c, np.nextafter(c, np.float32(0)), np.nextafter(c, np.float32(np.inf))]
+        vals += [np.float32(1e-45), np.float32(3e-38), np.float32(3.4e38)]
+        for a in vals:
+            a = float(a)
+            s = Q.ue8m0_scale(a, fm)
+            m, e = math.frexp(s)
+            assert m == 0.5 and a <= fm * s
+            assert s == 2.0 ** -127 or a > fm * s / 2
+
+
+def test_idempotence_and_monotonicity():
+    """SPEC.md:79-80."""
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((20, 256)) * 10
+    for gran in ("tensor", "row", "blk_1x128", "blk_128x128"):
+        c1, s1 = Q.quantize(x, "e4m3", gran)
+        c2, s2 = Q.quantize(Q.dequantize(c1, s1, "e4m3", gran), "e4m3", gran)
+        assert np.array_equal(c1, c2) and np.array_equal(s1, s2)
+    row = np.sort(rng.uniform(0, 5, 256))[None, :]
+    c, s = Q.quantize(row, "e4m3", "row")
+    d = Q.dequantize(c, s, "e4m3", "row")[0]
+    assert np.all(np.diff(d) >= 0)
+
+
+def test_rowwise_refines_tensorwise():
+    """rows with amax ratios >= 2^4 -> rowwise roundtrip MERE <= tensorwise."""
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal((16, 128)) * (2.0 ** (4 * np.arange(16)))[:, None] / 2 ** 30
+    errs = {}
+    for gran in ("tensor", "row"):
+        c, s = Q.quantize(x, "e4m3", gran)
+        errs[gran] = probe.mere(Q.dequantize(c, s, "e4m3", gran), x)
+    assert errs["row"] <= errs["tensor"]
+
+
+def test_nonfinite_raises_and_amax_override():
+    with pytest.raises(Q.NonFiniteInput):
+        Q.quantize(np.array([[1.0, np.nan]]), "e4m3", "row")
+    with pytest.raises(Q.NonFiniteInput):
+        Q.quantize(np.array([[1.0, np.inf]]), "e4m3", "tensor")
+    # split-phase tensorwise: a larger (global) amax gives the scale of the global tensor
+    x = np.array([[1.0, 2.0]])
+    c, s = Q.quantize(x, "e4m3", "tensor", amax=np.array([4.0]))
+    assert s[0] == np.float32(4.0) / np.float32(448.0)
+
+
+def test_mode_div_matches_float32_division():
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((4, 64)).astype(np.float32).astype(np.float64)
+    c, s = Q.quantize(x, "e4m3", "row", mode="div")
+    v = (x.astype(np.float32) / s[:, None]).astype(np.float32)
+    ref = torch.from_numpy(v).clamp(-448, 448).to(torch.float8_e4m3fn).view(torch.uint8).numpy()
+    assert np.array_equal(c, ref)
