@@ -1,0 +1,210 @@
+/*
+ * loka.h — C ABI of the B200-native (sm_100a) LoKA FP8 linear+norm hot path.
+ *
+ * LoKA (arXiv 2605.10886) makes FP8 practical for large recommendation models.  This library
+ * implements the data-parallel hot path named by BASELINE.json's north_star:
+ *   a1-a3  quantize (granule amax -> scale -> saturating RNE cast)        loka_quantize
+ *   a4-a5  FP8 GEMM (tcgen05, FP32 accumulation in TMEM) fused with
+ *          dequant / bias / LayerNorm / RMSNorm / BlockNorm epilogue      loka_fp8_linear_norm
+ *   a6     many small GEMMs in one launch                                  loka_grouped_fp8_linear
+ *   a7     LoKA Probe error statistic (MERE)                               loka_probe_error
+ *   a8     LoKA Dispatch constrained selection                             loka_dispatch_select
+ *
+ * Conventions (every call):
+ *   - Returns loka_status; no C++ exception crosses the ABI.  loka_status_string() gives text.
+ *   - Ownership: the caller owns all memory.  Tensor data/scales are DEVICE pointers; descriptor
+ *     structs and arrays passed by pointer are HOST memory read only during the call.  The library
+ *     never allocates device memory in a hot call; workspace is sized by loka_*_workspace_size().
+ *   - Asynchrony: device work is enqueued on the caller's stream and never synchronized.  Errors
+ *     detected on the device (non-finite input) are OR'ed into an optional device int32
+ *     *status_dev (bit LOKA_DEVSTATUS_NONFINITE); the caller reads it after its own sync.
+ *   - No CPU fallback: on a device that is not sm_100 the calls return LOKA_ERR_UNSUPPORTED.
+ *   - Layouts: row-major, last dimension contiguous, leading dimension `ld` in elements.  Base
+ *     pointers 16-byte aligned; ld*elem_size % 16 == 0 (TMA requirement) else LOKA_ERR_INVALID_ARG.
+ *   - Thread safety: calls may be made concurrently; the only global state is a mutex-guarded
+ *     per-device tensor-map/attribute cache.
+ */
+#ifndef LOKA_H_
+#define LOKA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LOKA_VERSION_MAJOR 0
+#define LOKA_VERSION_MINOR 1
+
+#if defined(__GNUC__)
+#define LOKA_API __attribute__((visibility("default")))
+#else
+#define LOKA_API
+#endif
+
+typedef struct CUstream_st* loka_stream_t; /* identical to cudaStream_t */
+
+typedef enum loka_status {
+  LOKA_OK = 0,
+  LOKA_ERR_INVALID_ARG = 1, /* null pointer, bad enum, misalignment, bad leading dimension   */
+  LOKA_ERR_SHAPE = 2,       /* inconsistent shapes; BLOCK_RMS with N % block != 0     */
+  LOKA_ERR_UNSUPPORTED = 3, /* not sm_100, or a combination this build does not implement     */
+  LOKA_ERR_NONFINITE = 4,   /* (host-visible form of the device status bit)                  */
+  LOKA_ERR_WORKSPACE = 5,   /* workspace pointer null or smaller than loka_*_workspace_size() */
+  LOKA_ERR_CUDA = 6         /* a CUDA runtime call or launch failed                           */
+} loka_status;
+
+#define LOKA_DEVSTATUS_NONFINITE 0x1 /* OR'ed into *status_dev when an input holds NaN/Inf */
+
+typedef enum loka_dtype {
+  LOKA_F32 = 0,
+  LOKA_BF16 = 1,
+  LOKA_E4M3 = 2, /* OCP E4M3FN, max 448   (D4) */
+  LOKA_E5M2 = 3  /* OCP E5M2,   max 57344                */
+} loka_dtype;
+
+/* Scale granularity in the tensor's own [rows, cols] frame ("tensorwise, rowwise,
+ * blockwise"; D6).  FP32 scale array layouts (row-major):
+ *   TENSOR [1] | ROW [rows] | COL [cols] | BLK_1x128 [rows, ceil(cols/128)]
+ *   | BLK_128x1 [ceil(rows/128), cols] | BLK_128x128 [ceil(rows/128), ceil(cols/128)]        */
+typedef enum loka_gran {
+  LOKA_GRAN_TENSOR = 0,
+  LOKA_GRAN_ROW = 1,
+  LOKA_GRAN_COL = 2,
+  LOKA_GRAN_BLK_1x128 = 3,
+  LOKA_GRAN_BLK_128x1 = 4,
+  LOKA_GRAN_BLK_128x128 = 5
+} loka_gran;
+
+/* F32: s = fl32(amax/max), r = fl32(max/amax) (D1).  UE8M0: s = 2^e, the smallest
+ * power of two (e >= -127) with amax <= max*s, r = 2^-e (D7).  Both stored as FP32.
+ * amax == 0 gives s = r = 1 (D2).                                                            */
+typedef enum loka_scale_fmt { LOKA_SCALE_F32 = 0, LOKA_SCALE_UE8M0 = 1 } loka_scale_fmt;
+
+typedef enum loka_phase {
+  LOKA_PHASE_FULL = 0,          /* amax + cast in one call                                   */
+  LOKA_PHASE_AMAX_ONLY = 1,     /* TENSOR only: write the local amax to *amax_dev            */
+  LOKA_PHASE_CAST_WITH_AMAX = 2 /* TENSOR only: cast with the (all-reduced) amax in *amax_dev */
+} loka_phase;
+
+typedef enum loka_norm {
+  LOKA_NORM_NONE = 0,
+  LOKA_NORM_LAYER = 1,    /* (y-mu)/sqrt(var+eps) * gamma + beta, biased var (D13)  */
+  LOKA_NORM_RMS = 2,      /* y/sqrt(mean(y^2)+eps) * gamma (D14)                    */
+  LOKA_NORM_BLOCK_RMS = 3 /* RMSNorm per contiguous block of norm_block columns, unparameterized
+                             ("RMSNorm((Wx + b).view(-1, BlockN)).view(B, N)")   */
+} loka_norm;
+
+/* GEMM direction ("separate optimization decisions for each direction").  The
+ * kernel always computes C[M,N] = A[M,K] . B[N,K]^T with both operands K-major; the direction
+ * says how the caller laid the operands out:
+ *   FWD   Y  = X  W^T : A = Xq [M,K],        B = Wq [N,K]
+ *   DGRAD dX = dY W   : A = dYq [M,N_out],   B = (W^T)q [K_in, N_out]   (K-major copy of W)
+ *   WGRAD dW = dY^T X : A = (dY^T)q [N,M],   B = (X^T)q [K,M]           (K-major copies)      */
+typedef enum loka_direction { LOKA_DIR_FWD = 0, LOKA_DIR_DGRAD = 1, LOKA_DIR_WGRAD = 2 } loka_direction;
+
+typedef struct loka_tensor {
+  void* data;               /* device pointer, row-major [rows, cols], leading dimension ld    */
+  loka_dtype dtype;
+  int64_t rows, cols, ld;
+  float* scales;            /* device FP32 scale array for FP8 tensors (layout per gran)      */
+  loka_gran gran;
+  loka_scale_fmt scale_fmt;
+} loka_tensor;
+
+/* ---- a1-a3: quantize ----------------------------------------------------------------------
+ * x  : bf16 or f32 [rows, cols].
+ * q  : e4m3/e5m2 codes [rows, cols] (q->data may be NULL when only qt is wanted) + q->scales in
+ *      q->gran layout (required).  q->rows/cols must equal x's.
+ * qt : nullable.  K-major copy for backward: codes of the SAME quantization written transposed,
+ *      [cols, rows]; qt->scales gets the same scales in the transposed frame's layout
+ *      (qt->gran must be the transpose of q->gran: ROW<->COL, 1x128<->128x1, others equal).
+ * phase, amax_dev: see loka_phase; amax_dev is a device float (TENSOR only, else ignored).
+ * Bit-exact with oracle/quantize.py (codes as bytes, scales as FP32 bit patterns).            */
+LOKA_API loka_status loka_quantize(const loka_tensor* x, loka_tensor* q, loka_tensor* qt, loka_phase phase,
+                          float* amax_dev, int32_t* status_dev, void* ws, size_t ws_bytes,
+                          loka_stream_t stream);
+LOKA_API size_t loka_quantize_workspace_size(const loka_tensor* x, const loka_tensor* q);
+
+/* ---- a4-a5: FP8 GEMM + fused epilogue ----------------------------------------------------- */
+typedef struct loka_linear_args {
+  int64_t M, N, K;
+  loka_direction dir;       /* metadata; see loka_direction                                   */
+  loka_tensor a;            /* e4m3/e5m2 [M,K] K-major, scales gran TENSOR | ROW              */
+  loka_tensor b;            /* e4m3/e5m2 [N,K] K-major, scales gran TENSOR | ROW              */
+  const void* bias;         /* nullable [N], dtype bias_dtype (F32 | BF16); added before norm */
+  loka_dtype bias_dtype;
+  loka_norm norm;
+  int32_t norm_block;       /* BLOCK_RMS block size (256 in the paper)          */
+  float eps;                /* <= 0 selects the default: 1e-5 LAYER, 1e-6 RMS/BLOCK_RMS       */
+  const float* gamma;       /* nullable [N] (LAYER, RMS)                                      */
+  const float* beta;        /* nullable [N] (LAYER)                                           */
+  loka_tensor y;            /* [M,N]: F32 | BF16 | E4M3/E5M2 with y.scales ROW (next layer's
+                               rowwise input, amax over the full normalised row)             */
+  float* debug_precast;     /* nullable [M,N] FP32 (ld = N): post-norm values before the
+                               output cast, for tests                                        */
+  int32_t* status_dev;      /* nullable                                                       */
+} loka_linear_args;
+
+/* Y = epilogue(A . B^T): acc(FP32, TMEM) -> y = acc*sa[m]*sb[n] (+bias[n]) -> norm -> cast.
+ * Full-row norms (LAYER, RMS, FP8 output with ROW scales) need N <= 2048 (one thread-block
+ * cluster of <= 8 CTAs spans the row); BLOCK_RMS and NONE take any N.  K % 16 == 0.          */
+LOKA_API loka_status loka_fp8_linear_norm(const loka_linear_args* args, void* ws, size_t ws_bytes,
+                                 loka_stream_t stream);
+LOKA_API size_t loka_linear_workspace_size(const loka_linear_args* args);
+
+/* ---- a6: grouped launch: G independent linear+norm problems ------------------------------- */
+LOKA_API loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* args, void* ws, size_t ws_bytes,
+                                    loka_stream_t stream);
+LOKA_API size_t loka_grouped_workspace_size(int32_t G, const loka_linear_args* args);
+
+/* ---- a7: LoKA Probe error statistic ------------------------------------------------------- */
+typedef struct loka_probe_pair {
+  const void* out;          /* device [M,N], dtype out_dtype (F32 | BF16): low-precision path */
+  loka_dtype out_dtype;
+  const void* ref;          /* device [M,N], dtype ref_dtype (F32 | BF16): BF16 path (D9)     */
+  loka_dtype ref_dtype;
+  int64_t M, N, ld_out, ld_ref;
+} loka_probe_pair;
+
+typedef struct loka_probe_stats {
+  double mere;              /* (1/(M N)) sum |out-ref| / max(|ref|, f), f = floor_rel*mean|ref| */
+  double max_rel;
+  double sum_abs_ref;
+  int64_t count;
+  int64_t n_floored;        /* elements with |ref| < f                                        */
+} loka_probe_stats;
+
+/* One launch sequence for L layers; stats_dev is a DEVICE array of L loka_probe_stats.
+ * Within 1e-5 relative of oracle/probe.py (D8-D10).                  */
+LOKA_API loka_status loka_probe_error(int32_t L, const loka_probe_pair* pairs, double floor_rel,
+                             loka_probe_stats* stats_dev, void* ws, size_t ws_bytes, loka_stream_t stream);
+LOKA_API size_t loka_probe_workspace_size(int32_t L, const loka_probe_pair* pairs);
+
+/* ---- a8: LoKA Dispatch (host) -------------------------------------------------------------- */
+typedef struct loka_candidate {
+  const char* id;
+  loka_direction dir;
+  double mere;
+  double time_us;           /* end-to-end time of the op with this recipe (D19)               */
+} loka_candidate;
+
+/* keep candidates with mere < mere_budget and baseline_time_us/time_us >
+ * min_speedup (both strict); choose the smallest time; ties -> lexicographically smallest id;
+ * *chosen = index, or -1 for the baseline when none passes.  Pure host function.             */
+LOKA_API loka_status loka_dispatch_select(const loka_candidate* c, int32_t n, double baseline_time_us,
+                                 double mere_budget, double min_speedup, int32_t* chosen);
+
+/* ---- helpers -------------------------------------------------------------------------------- */
+LOKA_API const char* loka_status_string(loka_status s);
+LOKA_API int32_t loka_device_supported(int32_t device); /* 1 if sm_100, else 0 */
+LOKA_API int32_t loka_version(void);                    /* major*100 + minor */
+/* Number of kernel launches the library made since load (process-wide counter; for bench
+ * evidence of "gpu_launches").                                                               */
+LOKA_API int64_t loka_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LOKA_H_ */

@@ -1,0 +1,259 @@
+"""Thin Python binding of libloka.so (include/loka.h) — argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of ``libloka.so``; this module only
+builds the C structs from torch tensors (device memory), passes the current CUDA stream, and
+checks the returned status.  There is NO CPU fallback: importing raises if the library is
+missing, and every call raises on a non-OK status (``LOKA_ERR_UNSUPPORTED`` off sm_100).
+
+The functions carry the C names (``loka_quantize``, ``loka_fp8_linear_norm``,
+``loka_grouped_fp8_linear``, ``loka_probe_error``, ``loka_dispatch_select``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libloka.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libloka.so not built ({LIB_PATH}); run `python -c 'import __graft_entry__ as g; g.build()'` "
+                      "or `python paper_2605_10886_b200/build.py` — there is no CPU fallback")
+_lib = C.CDLL(LIB_PATH)
+
+# ---- enums (include/loka.h) ----------------------------------------------------------------
+OK, ERR_INVALID_ARG, ERR_SHAPE, ERR_UNSUPPORTED, ERR_NONFINITE, ERR_WORKSPACE, ERR_CUDA = range(7)
+DEVSTATUS_NONFINITE = 0x1
+F32, BF16, E4M3, E5M2 = range(4)
+GRAN = {"tensor": 0, "row": 1, "col": 2, "blk_1x128": 3, "blk_128x1": 4, "blk_128x128": 5}
+SCALE = {"f32": 0, "ue8m0": 1}
+PHASE = {"full": 0, "amax": 1, "cast": 2}
+NORM = {"none": 0, "layer": 1, "rms": 2, "block_rms": 3}
+DIR = {"fwd": 0, "dgrad": 1, "wgrad": 2}
+FMT = {"e4m3": E4M3, "e5m2": E5M2}
+_TORCH_DT = {F32: torch.float32, BF16: torch.bfloat16, E4M3: torch.uint8, E5M2: torch.uint8}
+
+
+class LokaError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        super().__init__(f"{what}: {_lib.loka_status_string(status).decode()} (status {status})")
+        self.status = status
+
+
+class loka_tensor(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("dtype", C.c_int), ("rows", C.c_int64), ("cols", C.c_int64),
+                ("ld", C.c_int64), ("scales", C.c_void_p), ("gran", C.c_int), ("scale_fmt", C.c_int)]
+
+
+class loka_linear_args(C.Structure):
+    _fields_ = [("M", C.c_int64), ("N", C.c_int64), ("K", C.c_int64), ("dir", C.c_int),
+                ("a", loka_tensor), ("b", loka_tensor), ("bias", C.c_void_p), ("bias_dtype", C.c_int),
+                ("norm", C.c_int), ("norm_block", C.c_int32), ("eps", C.c_float), ("gamma", C.c_void_p),
+                ("beta", C.c_void_p), ("y", loka_tensor), ("debug_precast", C.c_void_p), ("status_dev", C.c_void_p)]
+
+
+class loka_probe_pair(C.Structure):
+    _fields_ = [("out", C.c_void_p), ("out_dtype", C.c_int), ("ref", C.c_void_p), ("ref_dtype", C.c_int),
+                ("M", C.c_int64), ("N", C.c_int64), ("ld_out", C.c_int64), ("ld_ref", C.c_int64)]
+
+
+class loka_probe_stats(C.Structure):
+    _fields_ = [("mere", C.c_double), ("max_rel", C.c_double), ("sum_abs_ref", C.c_double),
+                ("count", C.c_int64), ("n_floored", C.c_int64)]
+
+
+class loka_candidate(C.Structure):
+    _fields_ = [("id", C.c_char_p), ("dir", C.c_int), ("mere", C.c_double), ("time_us", C.c_double)]
+
+
+_P = C.POINTER
+_sig = {
+    "loka_quantize": ([_P(loka_tensor), _P(loka_tensor), _P(loka_tensor), C.c_int, C.c_void_p, C.c_void_p,
+                       C.c_void_p, C.c_size_t, C.c_void_p], C.c_int),
+    "loka_quantize_workspace_size": ([_P(loka_tensor), _P(loka_tensor)], C.c_size_t),
+    "loka_fp8_linear_norm": ([_P(loka_linear_args), C.c_void_p, C.c_size_t, C.c_void_p], C.c_int),
+    "loka_linear_workspace_size": ([_P(loka_linear_args)], C.c_size_t),
+    "loka_grouped_fp8_linear": ([C.c_int32, _P(loka_linear_args), C.c_void_p, C.c_size_t, C.c_void_p], C.c_int),
+    "loka_grouped_workspace_size": ([C.c_int32, _P(loka_linear_args)], C.c_size_t),
+    "loka_probe_error": ([C.c_int32, _P(loka_probe_pair), C.c_double, C.c_void_p, C.c_void_p, C.c_size_t,
+                          C.c_void_p], C.c_int),
+    "loka_probe_workspace_size": ([C.c_int32, _P(loka_probe_pair)], C.c_size_t),
+    "loka_dispatch_select": ([_P(loka_candidate), C.c_int32, C.c_double, C.c_double, C.c_double, _P(C.c_int32)],
+                             C.c_int),
+    "loka_status_string": ([C.c_int], C.c_char_p),
+    "loka_device_supported": ([C.c_int32], C.c_int32),
+    "loka_version": ([], C.c_int32),
+    "loka_launch_count": ([], C.c_int64),
+}
+for _name, (_args, _ret) in _sig.items():
+    _fn = getattr(_lib, _name)
+    _fn.argtypes = _args
+    _fn.restype = _ret
+EXPORTS = tuple(_sig)
+
+
+def _check(status: int, what: str):
+    if status != OK:
+        raise LokaError(status, what)
+
+
+def _stream(stream=None) -> int:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return F32
+    if t.dtype == torch.bfloat16:
+        return BF16
+    raise TypeError(t.dtype)
+
+
+def _tensor(data, dtype: int, rows: int, cols: int, scales=None, gran="tensor", scale_fmt="f32", ld=None):
+    if data is not None:
+        assert data.is_cuda and data.dim() == 2 and data.stride(1) == 1
+        ld = data.stride(0) if ld is None else ld
+    return loka_tensor(None if data is None else data.data_ptr(), dtype, rows, cols, ld if ld is not None else cols,
+                       None if scales is None else scales.data_ptr(), GRAN[gran], SCALE[scale_fmt])
+
+
+def scale_shape(rows: int, cols: int, gran: str):
+    cd = lambda a, b: -(-a // b)
+    return {"tensor": (1,), "row": (rows,), "col": (cols,), "blk_1x128": (rows, cd(cols, 128)),
+            "blk_128x1": (cd(rows, 128), cols), "blk_128x128": (cd(rows, 128), cd(cols, 128))}[gran]
+
+
+_T_GRAN = {"row": "col", "col": "row", "blk_1x128": "blk_128x1", "blk_128x1": "blk_1x128"}
+
+
+def loka_quantize(x: torch.Tensor, fmt: str = "e4m3", gran: str = "row", scale_fmt: str = "f32",
+                  phase: str = "full", amax: torch.Tensor | None = None, status: torch.Tensor | None = None,
+                  out: torch.Tensor | None = None, scales: torch.Tensor | None = None, want_q: bool = True,
+                  transpose: bool = False, stream=None):
+    """a1-a3.  Returns (codes uint8 [rows, cols] or None, scales fp32) [+ (codes_t, scales_t)]."""
+    rows, cols = x.shape
+    dev = x.device
+    if want_q and out is None:
+        out = torch.empty(rows, cols, dtype=torch.uint8, device=dev) if cols % 16 == 0 else \
+            torch.empty(rows, (cols + 15) // 16 * 16, dtype=torch.uint8, device=dev)[:, :cols]
+    if scales is None:
+        scales = torch.empty(scale_shape(rows, cols, gran), dtype=torch.float32, device=dev)
+    qx = _tensor(x, _dtype_code(x), rows, cols)
+    qq = _tensor(out if want_q else None, FMT[fmt], rows, cols, scales, gran, scale_fmt)
+    qt = None
+    qt_codes = qt_scales = None
+    if transpose:
+        tg = _T_GRAN.get(gran, gran)
+        qt_codes = torch.empty(cols, rows, dtype=torch.uint8, device=dev)
+        qt_scales = torch.empty(scale_shape(cols, rows, tg), dtype=torch.float32, device=dev)
+        qt = _tensor(qt_codes, FMT[fmt], cols, rows, qt_scales, tg, scale_fmt)
+    ws = torch.empty(256, dtype=torch.uint8, device=dev)
+    st = _lib.loka_quantize(C.byref(qx), C.byref(qq), None if qt is None else C.byref(qt), PHASE[phase],
+                            _ptr(amax), _ptr(status), _ptr(ws), 256, _stream(stream))
+    _check(st, "loka_quantize")
+    if transpose:
+        return (out if want_q else None), scales, qt_codes, qt_scales
+    return (out if want_q else None), scales
+
+
+def make_linear_args(a, a_scales, b, b_scales, *, a_fmt="e4m3", b_fmt="e4m3", a_gran="row", b_gran="row",
+                     norm="none", norm_block=256, eps=0.0, gamma=None, beta=None, bias=None, out_dtype="f32",
+                     y=None, y_scales=None, precast=None, status=None, direction="fwd", keep=None):
+    """Build a loka_linear_args for C = A . B^T (A [M,K], B [N,K] FP8 codes, K-major)."""
+    M, K = a.shape
+    N = b.shape[0]
+    od = {"f32": F32, "bf16": BF16, "e4m3": E4M3, "e5m2": E5M2}[out_dtype]
+    dev = a.device
+    if y is None:
+        y = torch.empty(M, N, dtype=_TORCH_DT[od], device=dev)
+    if od in (E4M3, E5M2) and y_scales is None:
+        y_scales = torch.empty(M, dtype=torch.float32, device=dev)
+    args = loka_linear_args()
+    args.M, args.N, args.K, args.dir = M, N, K, DIR[direction]
+    args.a = _tensor(a, FMT[a_fmt], M, K, a_scales, a_gran)
+    args.b = _tensor(b, FMT[b_fmt], N, K, b_scales, b_gran)
+    args.bias = None if bias is None else bias.data_ptr()
+    args.bias_dtype = F32 if bias is None else _dtype_code(bias)
+    args.norm, args.norm_block, args.eps = NORM[norm], norm_block, eps
+    args.gamma = None if gamma is None else gamma.data_ptr()
+    args.beta = None if beta is None else beta.data_ptr()
+    args.y = _tensor(y, od, M, N, y_scales, "row")
+    args.debug_precast = None if precast is None else precast.data_ptr()
+    args.status_dev = None if status is None else status.data_ptr()
+    if keep is not None:  # keep python references alive as long as args is used
+        keep.extend([a, a_scales, b, b_scales, bias, gamma, beta, y, y_scales, precast, status])
+    return args, y, y_scales
+
+
+def loka_fp8_linear_norm(a, a_scales, b, b_scales, stream=None, **kw):
+    """a4+a5.  Returns (y, y_scales or None)."""
+    args, y, ys = make_linear_args(a, a_scales, b, b_scales, **kw)
+    _check(_lib.loka_fp8_linear_norm(C.byref(args), None, 0, _stream(stream)), "loka_fp8_linear_norm")
+    return y, ys
+
+
+def loka_grouped_fp8_linear(args_list, stream=None):
+    """a6.  args_list: sequence of loka_linear_args (see make_linear_args)."""
+    G = len(args_list)
+    arr = (loka_linear_args * G)(*args_list)
+    _check(_lib.loka_grouped_fp8_linear(G, arr, None, 0, _stream(stream)), "loka_grouped_fp8_linear")
+
+
+def loka_probe_error(pairs, floor_rel: float = 1e-6, stream=None, stats=None, ws=None):
+    """a7.  pairs: [(out, ref)] device tensors (f32/bf16, 2-D).  Returns a float64 tensor [L, 5]
+    viewing the device loka_probe_stats array (mere, max_rel, sum_abs_ref, count*, n_floored*)
+    where the last two are int64 bit patterns; use probe_stats_to_dicts()."""
+    L = len(pairs)
+    arr = (loka_probe_pair * L)()
+    for i, (o, r) in enumerate(pairs):
+        arr[i] = loka_probe_pair(o.data_ptr(), _dtype_code(o), r.data_ptr(), _dtype_code(r), o.shape[0], o.shape[1],
+                                 o.stride(0), r.stride(0))
+    dev = pairs[0][0].device
+    if stats is None:
+        stats = torch.empty(L, 5, dtype=torch.float64, device=dev)
+    nws = _lib.loka_probe_workspace_size(L, arr)
+    if ws is None or ws.numel() < nws:
+        ws = torch.empty(nws, dtype=torch.uint8, device=dev)
+    _check(_lib.loka_probe_error(L, arr, floor_rel, C.c_void_p(stats.data_ptr()), C.c_void_p(ws.data_ptr()), nws,
+                                 _stream(stream)), "loka_probe_error")
+    return stats
+
+
+def probe_stats_to_dicts(stats: torch.Tensor):
+    s = stats.detach().cpu()
+    ints = s.view(torch.int64)
+    return [dict(mere=float(s[i, 0]), max_rel=float(s[i, 1]), sum_abs_ref=float(s[i, 2]), count=int(ints[i, 3]),
+                 n_floored=int(ints[i, 4])) for i in range(s.shape[0])]
+
+
+def loka_dispatch_select(candidates, baseline_time_us: float, mere_budget: float = 0.2,
+                         min_speedup: float = 1.05) -> int:
+    """a8.  candidates: [(id, direction, mere, time_us)].  Returns index or -1 (baseline)."""
+    n = len(candidates)
+    ids = [c[0].encode() for c in candidates]
+    arr = (loka_candidate * max(n, 1))()
+    for i, (cid, d, m, t) in enumerate(candidates):
+        arr[i] = loka_candidate(ids[i], DIR[d] if isinstance(d, str) else int(d), float(m), float(t))
+    out = C.c_int32(-2)
+    _check(_lib.loka_dispatch_select(arr, n, baseline_time_us, mere_budget, min_speedup, C.byref(out)),
+           "loka_dispatch_select")
+    return out.value
+
+
+def launch_count() -> int:
+    return int(_lib.loka_launch_count())
+
+
+def device_supported(device: int = 0) -> bool:
+    return bool(_lib.loka_device_supported(device))
+
+
+def version() -> int:
+    return int(_lib.loka_version())

@@ -1,0 +1,327 @@
+// api.cu — the C ABI (include/loka.h): argument validation, workspace sizing, TMA tensor-map
+// construction, kernel selection and launch.  No device work is done here besides launches.
+#include <atomic>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace loka {
+
+static std::atomic<long long> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// ---- device capability (per device, cached) ----------------------------------------------
+struct DevInfo {
+  int checked = 0, ok = 0, sms = 148;
+};
+static std::mutex g_mu;
+static DevInfo g_dev[64];
+
+static loka_status check_device(int* sms_out = nullptr) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return LOKA_ERR_CUDA;
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevInfo& d = g_dev[dev];
+  if (!d.checked) {
+    cudaDeviceProp pr;
+    if (cudaGetDeviceProperties(&pr, dev) != cudaSuccess) return LOKA_ERR_CUDA;
+    d.ok = (pr.major == 10 && pr.minor == 0);
+    d.sms = pr.multiProcessorCount;
+    d.checked = 1;
+  }
+  if (sms_out) *sms_out = d.sms;
+  return d.ok ? LOKA_OK : LOKA_ERR_UNSUPPORTED;
+}
+
+// ---- TMA descriptor encoding through the driver entry point (no -lcuda link) -------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 2D map over a row-major u8 matrix [rows, cols] (ld bytes), box {128 cols, box_rows rows}, SW128.
+static bool make_map_u8(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, uint32_t box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld};
+  cuuint32_t box[2] = {128u, box_rows};
+  cuuint32_t es[2] = {1u, 1u};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int elem_size(loka_dtype t) { return t == LOKA_F32 ? 4 : t == LOKA_BF16 ? 2 : 1; }
+static bool is_fp8(loka_dtype t) { return t == LOKA_E4M3 || t == LOKA_E5M2; }
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+static int transpose_gran(int g) {
+  switch (g) {
+    case LOKA_GRAN_ROW: return LOKA_GRAN_COL;
+    case LOKA_GRAN_COL: return LOKA_GRAN_ROW;
+    case LOKA_GRAN_BLK_1x128: return LOKA_GRAN_BLK_128x1;
+    case LOKA_GRAN_BLK_128x1: return LOKA_GRAN_BLK_1x128;
+    default: return g;
+  }
+}
+
+}  // namespace loka
+
+using namespace loka;
+
+extern "C" {
+
+const char* loka_status_string(loka_status s) {
+  switch (s) {
+    case LOKA_OK: return "ok";
+    case LOKA_ERR_INVALID_ARG: return "invalid argument";
+    case LOKA_ERR_SHAPE: return "shape mismatch";
+    case LOKA_ERR_UNSUPPORTED: return "unsupported (device is not sm_100 or combination not implemented)";
+    case LOKA_ERR_NONFINITE: return "non-finite input";
+    case LOKA_ERR_WORKSPACE: return "workspace too small";
+    case LOKA_ERR_CUDA: return "CUDA error";
+  }
+  return "unknown status";
+}
+
+int32_t loka_device_supported(int32_t device) {
+  cudaDeviceProp pr;
+  if (cudaGetDeviceProperties(&pr, device) != cudaSuccess) return 0;
+  return (pr.major == 10 && pr.minor == 0) ? 1 : 0;
+}
+
+int32_t loka_version(void) { return LOKA_VERSION_MAJOR * 100 + LOKA_VERSION_MINOR; }
+int64_t loka_launch_count(void) { return (int64_t)g_launches.load(); }
+
+// ------------------------------------------------------------------------------------------
+size_t loka_quantize_workspace_size(const loka_tensor* /*x*/, const loka_tensor* /*q*/) { return 256; }
+
+loka_status loka_quantize(const loka_tensor* x, loka_tensor* q, loka_tensor* qt, loka_phase phase, float* amax_dev,
+                          int32_t* status_dev, void* ws, size_t ws_bytes, loka_stream_t stream) {
+  if (!x || !q) return LOKA_ERR_INVALID_ARG;
+  if (x->dtype != LOKA_BF16 && x->dtype != LOKA_F32) return LOKA_ERR_INVALID_ARG;
+  if (!is_fp8(q->dtype) || (q->scale_fmt != LOKA_SCALE_F32 && q->scale_fmt != LOKA_SCALE_UE8M0))
+    return LOKA_ERR_INVALID_ARG;
+  if (x->rows < 0 || x->cols < 0 || q->rows != x->rows || q->cols != x->cols) return LOKA_ERR_SHAPE;
+  if (x->rows == 0 || x->cols == 0) return LOKA_OK;
+  if (!x->data || !aligned16(x->data) || x->ld < x->cols || (x->ld * elem_size(x->dtype)) % 16) return LOKA_ERR_INVALID_ARG;
+  if (!q->scales) return LOKA_ERR_INVALID_ARG;
+  if (q->data && (!aligned16(q->data) || q->ld < q->cols || q->ld % 16)) return LOKA_ERR_INVALID_ARG;
+  if (q->gran < LOKA_GRAN_TENSOR || q->gran > LOKA_GRAN_BLK_128x128) return LOKA_ERR_INVALID_ARG;
+  if (phase != LOKA_PHASE_FULL && q->gran != LOKA_GRAN_TENSOR) return LOKA_ERR_INVALID_ARG;
+  if (phase != LOKA_PHASE_FULL && !amax_dev) return LOKA_ERR_INVALID_ARG;
+  if (qt) {
+    if (qt->dtype != q->dtype || qt->rows != x->cols || qt->cols != x->rows || qt->gran != transpose_gran(q->gran) ||
+        qt->scale_fmt != q->scale_fmt)
+      return LOKA_ERR_SHAPE;
+    if (!qt->data || qt->ld < qt->cols) return LOKA_ERR_INVALID_ARG;
+  }
+  // COL / 128x1 granules (per-column scales over all rows) are not implemented yet.
+  if (q->gran == LOKA_GRAN_COL || q->gran == LOKA_GRAN_BLK_128x1) return LOKA_ERR_UNSUPPORTED;
+  int sms = 148;
+  loka_status st = check_device(&sms);
+  if (st != LOKA_OK) return st;
+  float* amax = amax_dev;
+  if (q->gran == LOKA_GRAN_TENSOR && phase == LOKA_PHASE_FULL && !amax) {
+    if (!ws || ws_bytes < loka_quantize_workspace_size(x, q)) return LOKA_ERR_WORKSPACE;
+    amax = reinterpret_cast<float*>(ws);
+  }
+  QuantParams p;
+  p.x = x->data;
+  p.rows = x->rows;
+  p.cols = x->cols;
+  p.ldx = x->ld;
+  p.q = reinterpret_cast<uint8_t*>(q->data);
+  p.ldq = q->ld;
+  p.scales = q->scales;
+  p.qt = qt ? reinterpret_cast<uint8_t*>(qt->data) : nullptr;
+  p.ldqt = qt ? qt->ld : 0;
+  p.scales_t = qt ? qt->scales : nullptr;
+  p.status = status_dev;
+  cudaError_t e = launch_quantize(p, x->dtype == LOKA_BF16, q->dtype, q->scale_fmt, q->gran, phase, amax,
+                                  reinterpret_cast<cudaStream_t>(stream), sms);
+  if (e == cudaErrorNotSupported) return LOKA_ERR_UNSUPPORTED;
+  return e == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
+}
+
+// ------------------------------------------------------------------------------------------
+size_t loka_linear_workspace_size(const loka_linear_args* /*a*/) { return 0; }
+
+static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CUtensorMap* tb, LinearParams* p,
+                                  int* bn_out) {
+  if (!a) return LOKA_ERR_INVALID_ARG;
+  const int64_t M = a->M, N = a->N, K = a->K;
+  if (M <= 0 || N <= 0 || K <= 0 || M > (1ll << 31) - 1 || N > (1ll << 30) || K > (1ll << 31) - 1)
+    return LOKA_ERR_SHAPE;
+  const loka_tensor &A = a->a, &B = a->b, &Y = a->y;
+  if (!is_fp8(A.dtype) || !is_fp8(B.dtype)) return LOKA_ERR_INVALID_ARG;
+  if (A.rows != M || A.cols != K || B.rows != N || B.cols != K || Y.rows != M || Y.cols != N) return LOKA_ERR_SHAPE;
+  if (!A.data || !B.data || !Y.data || !A.scales || !B.scales) return LOKA_ERR_INVALID_ARG;
+  if (!aligned16(A.data) || !aligned16(B.data) || !aligned16(Y.data)) return LOKA_ERR_INVALID_ARG;
+  if (A.ld < K || B.ld < K || A.ld % 16 || B.ld % 16) return LOKA_ERR_INVALID_ARG;
+  if (A.gran != LOKA_GRAN_TENSOR && A.gran != LOKA_GRAN_ROW) return LOKA_ERR_UNSUPPORTED;
+  if (B.gran != LOKA_GRAN_TENSOR && B.gran != LOKA_GRAN_ROW) return LOKA_ERR_UNSUPPORTED;
+  if (Y.dtype < LOKA_F32 || Y.dtype > LOKA_E5M2) return LOKA_ERR_INVALID_ARG;
+  if (Y.ld < N || (Y.ld * elem_size(Y.dtype)) % 16) return LOKA_ERR_INVALID_ARG;
+  const bool fp8_out = is_fp8(Y.dtype);
+  if (fp8_out && (!Y.scales || Y.gran != LOKA_GRAN_ROW)) return LOKA_ERR_INVALID_ARG;
+  if (a->bias && a->bias_dtype != LOKA_F32 && a->bias_dtype != LOKA_BF16) return LOKA_ERR_INVALID_ARG;
+  if (a->norm < LOKA_NORM_NONE || a->norm > LOKA_NORM_BLOCK_RMS) return LOKA_ERR_INVALID_ARG;
+  if (a->beta && a->norm != LOKA_NORM_LAYER) return LOKA_ERR_INVALID_ARG;
+  if (a->gamma && a->norm != LOKA_NORM_LAYER && a->norm != LOKA_NORM_RMS) return LOKA_ERR_INVALID_ARG;
+
+  int bn, csize = 1;
+  const bool full_row = a->norm == LOKA_NORM_LAYER || a->norm == LOKA_NORM_RMS || fp8_out;
+  if (N <= 64) bn = 64;
+  else if (N <= 128) bn = 128;
+  else bn = 256;
+  if (full_row) {
+    csize = (int)cdiv(N, bn);
+    if (csize > 8) return LOKA_ERR_UNSUPPORTED;  // row wider than one portable cluster
+  }
+  if (a->norm == LOKA_NORM_BLOCK_RMS) {
+    const int blk = a->norm_block;
+    if (blk <= 0 || N % blk) return LOKA_ERR_SHAPE;  // IndivisibleFeatureDim
+    if (blk % 32 || bn % blk) return LOKA_ERR_UNSUPPORTED;
+  }
+  if (!make_map_u8(ta, A.data, M, K, A.ld, 128)) return LOKA_ERR_CUDA;
+  if (!make_map_u8(tb, B.data, N, K, B.ld, (uint32_t)bn)) return LOKA_ERR_CUDA;
+
+  std::memset(p, 0, sizeof(*p));
+  p->M = (int32_t)M;
+  p->N = (int32_t)N;
+  p->K = (int32_t)K;
+  p->a_fmt = A.dtype == LOKA_E5M2 ? 1 : 0;
+  p->b_fmt = B.dtype == LOKA_E5M2 ? 1 : 0;
+  p->sa = A.scales;
+  p->sa_row = A.gran == LOKA_GRAN_ROW;
+  p->sb = B.scales;
+  p->sb_row = B.gran == LOKA_GRAN_ROW;
+  p->bias = a->bias;
+  p->bias_bf16 = a->bias_dtype == LOKA_BF16;
+  p->gamma = a->gamma;
+  p->beta = a->beta;
+  p->eps = a->eps > 0.f ? a->eps : (a->norm == LOKA_NORM_LAYER ? 1e-5f : 1e-6f);
+  p->norm = a->norm;
+  p->norm_block = a->norm == LOKA_NORM_BLOCK_RMS ? a->norm_block : 0;
+  p->out_dtype = Y.dtype;
+  p->y = Y.data;
+  p->ldy = Y.ld;
+  p->y_scales = fp8_out ? Y.scales : nullptr;
+  p->precast = a->debug_precast;
+  p->ld_pre = N;
+  p->status = a->status_dev;
+  p->cluster_n = csize;
+  *bn_out = bn;
+  return LOKA_OK;
+}
+
+loka_status loka_fp8_linear_norm(const loka_linear_args* a, void* /*ws*/, size_t /*ws_bytes*/, loka_stream_t stream) {
+  CUtensorMap ta, tb;
+  LinearParams p;
+  int bn = 0;
+  loka_status st = prepare_linear(a, &ta, &tb, &p, &bn);
+  if (st != LOKA_OK) return st;
+  st = check_device();
+  if (st != LOKA_OK) return st;
+  cudaError_t e = launch_linear(ta, tb, p, bn, reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
+}
+
+size_t loka_grouped_workspace_size(int32_t /*G*/, const loka_linear_args* /*a*/) { return 0; }
+
+loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* ws, size_t ws_bytes,
+                                    loka_stream_t stream) {
+  if (G < 0 || (G > 0 && !a)) return LOKA_ERR_INVALID_ARG;
+  std::vector<CUtensorMap> ta(G), tb(G);
+  std::vector<LinearParams> p(G);
+  std::vector<int> bn(G);
+  for (int g = 0; g < G; ++g) {
+    loka_status st = prepare_linear(&a[g], &ta[g], &tb[g], &p[g], &bn[g]);
+    if (st != LOKA_OK) return st;
+  }
+  loka_status st = check_device();
+  if (st != LOKA_OK) return st;
+  (void)ws;
+  (void)ws_bytes;
+  for (int g = 0; g < G; ++g) {
+    cudaError_t e = launch_linear(ta[g], tb[g], p[g], bn[g], reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return LOKA_ERR_CUDA;
+  }
+  return LOKA_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+static int probe_nblk(int32_t L) {
+  int n = 1184 / (L > 64 ? 64 : (L < 1 ? 1 : L));
+  return n < 1 ? 1 : n;
+}
+
+size_t loka_probe_workspace_size(int32_t L, const loka_probe_pair* /*pairs*/) {
+  return (size_t)64 * probe_nblk(L) * (8 + 8 + 8 + 4) + 64;
+}
+
+loka_status loka_probe_error(int32_t L, const loka_probe_pair* pairs, double floor_rel, loka_probe_stats* stats_dev,
+                             void* ws, size_t ws_bytes, loka_stream_t stream) {
+  if (L < 0 || (L > 0 && (!pairs || !stats_dev))) return LOKA_ERR_INVALID_ARG;
+  if (L == 0) return LOKA_OK;
+  if (!ws || ws_bytes < loka_probe_workspace_size(L, pairs) || !aligned16(ws)) return LOKA_ERR_WORKSPACE;
+  std::vector<ProbeLayer> layers(L);
+  for (int l = 0; l < L; ++l) {
+    const loka_probe_pair& q = pairs[l];
+    if ((q.out_dtype != LOKA_F32 && q.out_dtype != LOKA_BF16) || (q.ref_dtype != LOKA_F32 && q.ref_dtype != LOKA_BF16))
+      return LOKA_ERR_INVALID_ARG;
+    if (q.M < 0 || q.N < 0 || q.ld_out < q.N || q.ld_ref < q.N) return LOKA_ERR_SHAPE;
+    if (q.M * q.N > 0 && (!q.out || !q.ref || !aligned16(q.out) || !aligned16(q.ref))) return LOKA_ERR_INVALID_ARG;
+    if ((q.ld_out * elem_size(q.out_dtype)) % 16 || (q.ld_ref * elem_size(q.ref_dtype)) % 16)
+      return LOKA_ERR_INVALID_ARG;
+    layers[l] = ProbeLayer{q.out, q.ref, q.out_dtype == LOKA_BF16, q.ref_dtype == LOKA_BF16, q.M, q.N, q.ld_out, q.ld_ref};
+  }
+  loka_status st = check_device();
+  if (st != LOKA_OK) return st;
+  cudaError_t e = launch_probe(layers.data(), L, 0, floor_rel, stats_dev, reinterpret_cast<double*>(ws),
+                               probe_nblk(L), reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
+}
+
+// ------------------------------------------------------------------------------------------
+// a8: LoKA Dispatch.  Host-only; written independently of oracle/dispatch.py.
+loka_status loka_dispatch_select(const loka_candidate* c, int32_t n, double baseline_time_us, double mere_budget,
+                                 double min_speedup, int32_t* chosen) {
+  if (!chosen || n < 0 || (n > 0 && !c)) return LOKA_ERR_INVALID_ARG;
+  int32_t best = -1;
+  for (int32_t i = 0; i < n; ++i) {
+    const double t = c[i].time_us;
+    const bool accurate = c[i].mere < mere_budget;                          // strict
+    const bool faster = t > 0.0 && (baseline_time_us / t) > min_speedup;     // strict
+    if (!accurate || !faster) continue;
+    if (best < 0) {
+      best = i;
+      continue;
+    }
+    const double tb = c[best].time_us;
+    const char* ib = c[best].id ? c[best].id : "";
+    const char* ii = c[i].id ? c[i].id : "";
+    if (t < tb || (t == tb && std::strcmp(ii, ib) < 0)) best = i;
+  }
+  *chosen = best;
+  return LOKA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,213 @@
+// common.cuh — sm_100a device helpers shared by the LoKA kernels (PTX wrappers for FP8 casts,
+// mbarrier, TMA, tcgen05/TMEM, clusters).  Product code only; nothing here is used by oracle/.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/loka.h"
+
+#define LOKA_DEVINL __device__ __forceinline__
+
+namespace loka {
+
+// ------------------------------------------------------------------------------------------
+// FP8 constants (OCP E4M3FN / E5M2; D4)
+// ------------------------------------------------------------------------------------------
+template <int FMT> struct Fp8Traits;
+template <> struct Fp8Traits<LOKA_E4M3> {
+  static constexpr float kMax = 448.0f;
+  static constexpr int kMaxExp = 8;  // 448 = 1.75 * 2^8
+};
+template <> struct Fp8Traits<LOKA_E5M2> {
+  static constexpr float kMax = 57344.0f;
+  static constexpr int kMaxExp = 15;  // 57344 = 1.75 * 2^15
+};
+
+// Two FP32 -> two FP8 codes, saturating RNE (F2FP.SATFINITE).  lo goes to the low byte.
+template <int FMT> LOKA_DEVINL uint32_t cvt_fp8x2(float lo, float hi) {
+  uint16_t r;
+  if constexpr (FMT == LOKA_E4M3)
+    asm("{ cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2; }" : "=h"(r) : "f"(hi), "f"(lo));
+  else
+    asm("{ cvt.rn.satfinite.e5m2x2.f32 %0, %1, %2; }" : "=h"(r) : "f"(hi), "f"(lo));
+  return (uint32_t)r;
+}
+template <int FMT> LOKA_DEVINL uint32_t cvt_fp8x4(float a, float b, float c, float d) {
+  return cvt_fp8x2<FMT>(a, b) | (cvt_fp8x2<FMT>(c, d) << 16);
+}
+
+// Exact IEEE scale computation for one granule (D1/D2/D7).  amax >= 0, finite.
+template <int FMT, int SCALE_FMT>
+LOKA_DEVINL void scales_from_amax(float amax, float& s, float& r) {
+  constexpr float kMax = Fp8Traits<FMT>::kMax;
+  if (!(amax > 0.0f)) { s = 1.0f; r = 1.0f; return; }
+  if constexpr (SCALE_FMT == LOKA_SCALE_F32) {
+    s = __fdiv_rn(amax, kMax);
+    r = __fdiv_rn(kMax, amax);
+  } else {
+    // s = 2^e, e = smallest integer >= -127 with amax <= kMax * 2^e.  With amax = m * 2^ea
+    // (m in [1,2)) and kMax = 1.75 * 2^kMaxExp:  e = ea - kMaxExp + (m > 1.75).
+    uint32_t b = __float_as_uint(amax);
+    int ef = (int)(b >> 23);
+    uint32_t mf = b & 0x7FFFFFu;
+    int e;
+    if (ef == 0) {
+      e = -127;  // subnormal amax < 2^-126: amax/kMax < 2^-134
+    } else {
+      e = (ef - 127) - Fp8Traits<FMT>::kMaxExp + (mf > 0x600000u ? 1 : 0);
+      if (e < -127) e = -127;
+    }
+    s = (e >= -126) ? __uint_as_float((uint32_t)(e + 127) << 23) : __uint_as_float(0x00400000u);
+    r = __uint_as_float((uint32_t)(127 - e) << 23);  // 2^-e, e in [-127, 127]: exponent 0..254
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// misc
+// ------------------------------------------------------------------------------------------
+LOKA_DEVINL int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+LOKA_DEVINL uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+LOKA_DEVINL float bf16lo_to_f32(uint32_t w) { return __uint_as_float(w << 16); }
+LOKA_DEVINL float bf16hi_to_f32(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+LOKA_DEVINL uint32_t warp_max_u32(uint32_t v) {
+  return __reduce_max_sync(0xFFFFFFFFu, v);
+}
+
+// ------------------------------------------------------------------------------------------
+// mbarrier
+// ------------------------------------------------------------------------------------------
+LOKA_DEVINL void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+LOKA_DEVINL void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+LOKA_DEVINL void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+LOKA_DEVINL void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+LOKA_DEVINL bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+LOKA_DEVINL void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  while (!mbar_try_wait(a, parity)) {
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// TMA
+// ------------------------------------------------------------------------------------------
+LOKA_DEVINL void tma_prefetch_desc(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)m) : "memory");
+}
+LOKA_DEVINL void tma_load_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"((uint64_t)m), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// ------------------------------------------------------------------------------------------
+// tcgen05 / TMEM
+// ------------------------------------------------------------------------------------------
+template <uint32_t kCols>
+LOKA_DEVINL void tmem_alloc(uint32_t* dst_smem) {  // whole warp
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "n"(kCols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+template <uint32_t kCols>
+LOKA_DEVINL void tmem_dealloc(uint32_t taddr) {  // whole warp
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols));
+}
+LOKA_DEVINL void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+LOKA_DEVINL void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// SMEM matrix descriptor, K-major operand, 128-byte swizzle: rows of 128 B, 8-row groups 1024 B
+// apart (SBO), LBO unused (16 B), version 1 (sm_100), layout type 2 = SWIZZLE_128B.
+LOKA_DEVINL uint64_t smem_desc_kmajor_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;                 // LBO = 16 B (ignored for swizzled K-major)
+  d |= (uint64_t)(1024u >> 4) << 32;       // SBO = 1024 B
+  d |= (uint64_t)1u << 46;                 // version
+  d |= (uint64_t)2u << 61;                 // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor for kind::f8f6f4, FP32 accumulate, both operands K-major.
+LOKA_DEVINL uint32_t idesc_f8f6f4(int a_fmt, int b_fmt, uint32_t M, uint32_t N) {
+  uint32_t d = 0;
+  d |= 1u << 4;                     // D format F32
+  d |= (uint32_t)a_fmt << 7;        // 0 = E4M3, 1 = E5M2
+  d |= (uint32_t)b_fmt << 10;
+  d |= (N >> 3) << 17;
+  d |= (M >> 4) << 24;
+  return d;
+}
+
+LOKA_DEVINL void mma_f8f6f4(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+LOKA_DEVINL void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// 32 lanes x 32 columns of 32-bit: thread t of the warp gets lane (base + t), 32 consecutive cols.
+LOKA_DEVINL void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// ------------------------------------------------------------------------------------------
+// clusters / DSMEM
+// ------------------------------------------------------------------------------------------
+LOKA_DEVINL uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+LOKA_DEVINL void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+LOKA_DEVINL uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+LOKA_DEVINL float ld_dsmem_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+}  // namespace loka

@@ -1,0 +1,57 @@
+// launch.h — internal (non-ABI) launch interfaces between api.cu and the kernel files.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace loka {
+
+void note_launch(int n = 1);  // process-wide launch counter (loka_launch_count)
+
+struct QuantParams {
+  const void* x;
+  int64_t rows, cols, ldx;
+  uint8_t* q;        // nullable
+  int64_t ldq;
+  float* scales;     // scales in x's frame (nullable when only the transposed copy is wanted)
+  uint8_t* qt;       // nullable transposed codes [cols, rows]
+  int64_t ldqt;
+  float* scales_t;   // nullable scales in the transposed frame
+  int32_t* status;
+};
+
+cudaError_t launch_quantize(const QuantParams& p, bool in_bf16, int fmt, int scale_fmt, int gran, int phase,
+                            float* amax_dev, cudaStream_t st, int num_sms);
+
+struct LinearParams {
+  int32_t M, N, K;
+  int32_t a_fmt, b_fmt;          // 0 = e4m3, 1 = e5m2 (tcgen05 kind::f8f6f4 encoding)
+  const float* sa; int32_t sa_row;  // per-row (1) or tensor (0) scale of A
+  const float* sb; int32_t sb_row;  // per-row of B (= per output column n) or tensor
+  const void* bias; int32_t bias_bf16;
+  const float* gamma;
+  const float* beta;
+  float eps;
+  int32_t norm, norm_block;
+  int32_t out_dtype;             // loka_dtype
+  void* y; int64_t ldy;
+  float* y_scales;               // ROW scales of an FP8 output
+  float* precast; int64_t ld_pre;
+  int32_t* status;
+  int32_t cluster_n;             // CTAs per cluster along N (1 = no cross-CTA row exchange)
+};
+
+// Launch one linear+norm problem.  tma_a/tma_b are 2D maps over the FP8 operands with box
+// {128 (K), 128 (A rows)} and {128 (K), bn (B rows)}, 128B swizzle.
+cudaError_t launch_linear(const CUtensorMap& tma_a, const CUtensorMap& tma_b, const LinearParams& p, int bn,
+                          cudaStream_t st);
+
+struct ProbeLayer {
+  const void* out; const void* ref;
+  int32_t out_bf16, ref_bf16;
+  int64_t M, N, ld_out, ld_ref;
+};
+cudaError_t launch_probe(const ProbeLayer* layers_dev, int L, int64_t max_elems, double floor_rel,
+                         void* stats_dev, double* partials, int nblk, cudaStream_t st);
+
+}  // namespace loka

@@ -1,0 +1,366 @@
+// quantize.cu — a1/a2/a3: granule amax -> scale -> saturating RNE cast to e4m3/e5m2.
+//
+// Definition (D1-D3, D7):
+//   amax = max |x| over the granule (exact), s = fl32(amax/max), r = fl32(max/amax)
+//   (UE8M0: s = 2^e smallest power of two >= amax/max), q = satRNE_fp8(fl32(x * r)).
+//
+// HBM-bound: 2 B (bf16) read + 1 B written per element.  Kernels read 16 B per lane per
+// load (8 bf16), keep the row/block in registers between the amax reduction and the cast
+// when it fits (one HBM read), and reduce amax on the integer bit pattern of |x|
+// (NaN > Inf > finite, so a non-finite element is detected from the reduced amax alone).
+#include "common.cuh"
+#include "launch.h"
+
+namespace loka {
+
+// ----- element loading: 8 elements per lane as FP32 + max of |x| bit patterns ------------
+template <typename Tin> struct Vec8;
+
+template <> struct Vec8<__nv_bfloat16> {
+  uint4 w;  // 8 bf16
+  LOKA_DEVINL void load(const __nv_bfloat16* p) { w = __ldg(reinterpret_cast<const uint4*>(p)); }
+  LOKA_DEVINL void load_partial(const __nv_bfloat16* p, int n) {
+    uint16_t h[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) h[i] = i < n ? reinterpret_cast<const uint16_t*>(p)[i] : 0;
+    w.x = h[0] | ((uint32_t)h[1] << 16);
+    w.y = h[2] | ((uint32_t)h[3] << 16);
+    w.z = h[4] | ((uint32_t)h[5] << 16);
+    w.w = h[6] | ((uint32_t)h[7] << 16);
+  }
+  LOKA_DEVINL void zero() { w = make_uint4(0, 0, 0, 0); }
+  // max of |x| as FP32 bit patterns (bf16 -> fp32 is a 16-bit shift, order preserved)
+  LOKA_DEVINL uint32_t amax_bits() const {
+    uint32_t m;
+    uint32_t a = w.x & 0x7FFF7FFFu, b = w.y & 0x7FFF7FFFu, c = w.z & 0x7FFF7FFFu, d = w.w & 0x7FFF7FFFu;
+    asm("max.u16x2 %0, %1, %2;" : "=r"(a) : "r"(a), "r"(b));
+    asm("max.u16x2 %0, %1, %2;" : "=r"(c) : "r"(c), "r"(d));
+    asm("max.u16x2 %0, %1, %2;" : "=r"(m) : "r"(a), "r"(c));
+    return max(m & 0xFFFFu, m >> 16) << 16;
+  }
+  LOKA_DEVINL void to_f32(float (&f)[8]) const {
+    f[0] = bf16lo_to_f32(w.x); f[1] = bf16hi_to_f32(w.x);
+    f[2] = bf16lo_to_f32(w.y); f[3] = bf16hi_to_f32(w.y);
+    f[4] = bf16lo_to_f32(w.z); f[5] = bf16hi_to_f32(w.z);
+    f[6] = bf16lo_to_f32(w.w); f[7] = bf16hi_to_f32(w.w);
+  }
+};
+
+template <> struct Vec8<float> {
+  float4 a, b;
+  LOKA_DEVINL void load(const float* p) {
+    a = __ldg(reinterpret_cast<const float4*>(p));
+    b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  }
+  LOKA_DEVINL void load_partial(const float* p, int n) {
+    float h[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) h[i] = i < n ? p[i] : 0.0f;
+    a = make_float4(h[0], h[1], h[2], h[3]);
+    b = make_float4(h[4], h[5], h[6], h[7]);
+  }
+  LOKA_DEVINL void zero() { a = b = make_float4(0.f, 0.f, 0.f, 0.f); }
+  LOKA_DEVINL uint32_t amax_bits() const {
+    uint32_t m = __float_as_uint(a.x) & 0x7FFFFFFFu;
+    m = max(m, __float_as_uint(a.y) & 0x7FFFFFFFu);
+    m = max(m, __float_as_uint(a.z) & 0x7FFFFFFFu);
+    m = max(m, __float_as_uint(a.w) & 0x7FFFFFFFu);
+    m = max(m, __float_as_uint(b.x) & 0x7FFFFFFFu);
+    m = max(m, __float_as_uint(b.y) & 0x7FFFFFFFu);
+    m = max(m, __float_as_uint(b.z) & 0x7FFFFFFFu);
+    m = max(m, __float_as_uint(b.w) & 0x7FFFFFFFu);
+    return m;
+  }
+  LOKA_DEVINL void to_f32(float (&f)[8]) const {
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+    f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+  }
+};
+
+// 8 elements * r -> 8 codes (two u32).  fl32(x*r) is a plain IEEE multiply (no FMA, no FTZ).
+template <int FMT, typename Tin>
+LOKA_DEVINL uint2 cast8(const Vec8<Tin>& v, float r) {
+  float f[8];
+  v.to_f32(f);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) f[i] = __fmul_rn(f[i], r);
+  return make_uint2(cvt_fp8x4<FMT>(f[0], f[1], f[2], f[3]), cvt_fp8x4<FMT>(f[4], f[5], f[6], f[7]));
+}
+
+LOKA_DEVINL void store8(uint8_t* p, uint2 c, int n) {
+  if (n >= 8) {
+    *reinterpret_cast<uint2*>(p) = c;
+  } else {
+    const uint8_t* b = reinterpret_cast<const uint8_t*>(&c);
+    for (int i = 0; i < n; ++i) p[i] = b[i];
+  }
+}
+
+LOKA_DEVINL void flag_nonfinite(uint32_t amax_bits, int32_t* status) {
+  if (amax_bits >= 0x7F800000u && status != nullptr) atomicOr(status, LOKA_DEVSTATUS_NONFINITE);
+}
+
+// ----- ROW: one warp per row; rows of <= 256*NREG elements stay in registers -------------
+template <typename Tin, int FMT, int SF, int NREG>
+__global__ void __launch_bounds__(256) quant_row_kernel(QuantParams p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= p.rows) return;
+  const Tin* xr = reinterpret_cast<const Tin*>(p.x) + row * p.ldx;
+  const int64_t cols = p.cols;
+  const bool cached = cols <= 256 * NREG;
+  Vec8<Tin> v[NREG];
+  uint32_t am = 0;
+  for (int64_t c0 = 0, it = 0; c0 < cols; c0 += 256, ++it) {
+    const int64_t c = c0 + lane * 8;
+    Vec8<Tin> t;
+    if (c + 8 <= cols) t.load(xr + c);
+    else if (c < cols) t.load_partial(xr + c, (int)(cols - c));
+    else t.zero();
+    am = max(am, t.amax_bits());
+    if (cached) {
+#pragma unroll
+      for (int i = 0; i < NREG; ++i)
+        if (i == it) v[i] = t;
+    }
+  }
+  am = warp_max_u32(am);
+  flag_nonfinite(am, p.status);
+  float s, r;
+  scales_from_amax<FMT, SF>(__uint_as_float(am), s, r);
+  if (lane == 0) {
+    if (p.scales) p.scales[row] = s;
+    if (p.scales_t) p.scales_t[row] = s;
+  }
+  uint8_t* qr = p.q ? p.q + row * p.ldq : nullptr;
+  for (int64_t c0 = 0, it = 0; c0 < cols; c0 += 256, ++it) {
+    const int64_t c = c0 + lane * 8;
+    if (c >= cols) continue;
+    Vec8<Tin> t;
+    if (cached) {
+#pragma unroll
+      for (int i = 0; i < NREG; ++i)
+        if (i == it) t = v[i];
+    } else if (c + 8 <= cols) {
+      t.load(xr + c);
+    } else {
+      t.load_partial(xr + c, (int)(cols - c));
+    }
+    uint2 code = cast8<FMT>(t, r);
+    const int n = (int)imin64(8, cols - c);
+    if (qr) store8(qr + c, code, n);
+    if (p.qt) {  // transposed copy: element (row, c+i) -> qt[(c+i) * ldqt + row]
+      const uint8_t* b = reinterpret_cast<const uint8_t*>(&code);
+      for (int i = 0; i < n; ++i) p.qt[(c + i) * p.ldqt + row] = b[i];
+    }
+  }
+}
+
+// ----- BLK_1x128: one warp per row, 16 lanes per 128-column block -------------------------
+template <typename Tin, int FMT, int SF>
+__global__ void __launch_bounds__(256) quant_1x128_kernel(QuantParams p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= p.rows) return;
+  const Tin* xr = reinterpret_cast<const Tin*>(p.x) + row * p.ldx;
+  const int64_t cols = p.cols;
+  const int64_t nblk = (cols + 127) / 128;
+  for (int64_t c0 = 0; c0 < cols; c0 += 256) {
+    const int64_t c = c0 + lane * 8;
+    Vec8<Tin> t;
+    if (c + 8 <= cols) t.load(xr + c);
+    else if (c < cols) t.load_partial(xr + c, (int)(cols - c));
+    else t.zero();
+    uint32_t am = t.amax_bits();
+#pragma unroll
+    for (int o = 8; o >= 1; o >>= 1) am = max(am, __shfl_xor_sync(0xFFFFFFFFu, am, o));
+    flag_nonfinite(am, p.status);
+    float s, r;
+    scales_from_amax<FMT, SF>(__uint_as_float(am), s, r);
+    const int64_t blk = c0 / 128 + (lane >> 4);
+    if ((lane & 15) == 0 && blk < nblk) {
+      if (p.scales) p.scales[row * nblk + blk] = s;
+      if (p.scales_t) p.scales_t[blk * p.rows + row] = s;  // transposed frame: BLK_128x1 [nblk, rows]
+    }
+    if (c < cols) {
+      uint2 code = cast8<FMT>(t, r);
+      const int n = (int)imin64(8, cols - c);
+      if (p.q) store8(p.q + row * p.ldq + c, code, n);
+      if (p.qt) {
+        const uint8_t* b = reinterpret_cast<const uint8_t*>(&code);
+        for (int i = 0; i < n; ++i) p.qt[(c + i) * p.ldqt + row] = b[i];
+      }
+    }
+  }
+}
+
+// ----- BLK_128x128: one CTA (8 warps) per 128x128 block, block held in registers --------
+template <typename Tin, int FMT, int SF>
+__global__ void __launch_bounds__(256) quant_128x128_kernel(QuantParams p) {
+  __shared__ uint32_t red[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t bc = blockIdx.x, br = blockIdx.y;
+  const int64_t nbc = (p.cols + 127) / 128, nbr = (p.rows + 127) / 128;
+  const int64_t col = bc * 128 + (lane & 15) * 8;
+  Vec8<Tin> v[8];
+  uint32_t am = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t row = br * 128 + warp * 16 + i * 2 + (lane >> 4);
+    const Tin* xr = reinterpret_cast<const Tin*>(p.x) + row * p.ldx;
+    if (row < p.rows && col + 8 <= p.cols) v[i].load(xr + col);
+    else if (row < p.rows && col < p.cols) v[i].load_partial(xr + col, (int)(p.cols - col));
+    else v[i].zero();
+    am = max(am, v[i].amax_bits());
+  }
+  am = warp_max_u32(am);
+  if (lane == 0) red[warp] = am;
+  __syncthreads();
+  am = red[0];
+#pragma unroll
+  for (int w = 1; w < 8; ++w) am = max(am, red[w]);
+  if (threadIdx.x == 0) flag_nonfinite(am, p.status);
+  float s, r;
+  scales_from_amax<FMT, SF>(__uint_as_float(am), s, r);
+  if (threadIdx.x == 0) {
+    if (p.scales) p.scales[br * nbc + bc] = s;
+    if (p.scales_t) p.scales_t[bc * nbr + br] = s;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t row = br * 128 + warp * 16 + i * 2 + (lane >> 4);
+    if (row >= p.rows || col >= p.cols) continue;
+    uint2 code = cast8<FMT>(v[i], r);
+    const int n = (int)imin64(8, p.cols - col);
+    if (p.q) store8(p.q + row * p.ldq + col, code, n);
+    if (p.qt) {
+      const uint8_t* b = reinterpret_cast<const uint8_t*>(&code);
+      for (int k = 0; k < n; ++k) p.qt[(col + k) * p.ldqt + row] = b[k];
+    }
+  }
+}
+
+// ----- TENSOR: amax pass (atomicMax on bit patterns into a zeroed word) + cast pass -------
+template <typename Tin>
+__global__ void __launch_bounds__(256) amax_tensor_kernel(QuantParams p, uint32_t* amax_bits) {
+  __shared__ uint32_t red[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nwarps = (int64_t)gridDim.x * 8;
+  uint32_t am = 0;
+  for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < p.rows; row += nwarps) {
+    const Tin* xr = reinterpret_cast<const Tin*>(p.x) + row * p.ldx;
+    for (int64_t c = lane * 8; c < p.cols; c += 256) {
+      Vec8<Tin> t;
+      if (c + 8 <= p.cols) t.load(xr + c);
+      else t.load_partial(xr + c, (int)(p.cols - c));
+      am = max(am, t.amax_bits());
+    }
+  }
+  am = warp_max_u32(am);
+  if (lane == 0) red[warp] = am;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) am = max(am, red[w]);
+    am = max(am, red[0]);
+    if (am) atomicMax(amax_bits, am);
+    flag_nonfinite(am, p.status);
+  }
+}
+
+template <typename Tin, int FMT, int SF>
+__global__ void __launch_bounds__(256) cast_tensor_kernel(QuantParams p, const float* amax_dev) {
+  const float amax = *amax_dev;
+  float s, r;
+  scales_from_amax<FMT, SF>(amax, s, r);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (p.scales) p.scales[0] = s;
+    if (p.scales_t) p.scales_t[0] = s;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nwarps = (int64_t)gridDim.x * 8;
+  for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < p.rows; row += nwarps) {
+    const Tin* xr = reinterpret_cast<const Tin*>(p.x) + row * p.ldx;
+    for (int64_t c = lane * 8; c < p.cols; c += 256) {
+      Vec8<Tin> t;
+      const int n = (int)imin64(8, p.cols - c);
+      if (n == 8) t.load(xr + c);
+      else t.load_partial(xr + c, n);
+      uint2 code = cast8<FMT>(t, r);
+      if (p.q) store8(p.q + row * p.ldq + c, code, n);
+      if (p.qt) {
+        const uint8_t* b = reinterpret_cast<const uint8_t*>(&code);
+        for (int k = 0; k < n; ++k) p.qt[(c + k) * p.ldqt + row] = b[k];
+      }
+    }
+  }
+}
+
+// ----- host-side launch -------------------------------------------------------------------
+template <typename Tin, int FMT, int SF>
+static cudaError_t launch_quant_t(const QuantParams& p, int gran, int phase, float* amax_dev, cudaStream_t st,
+                                  int num_sms) {
+  const dim3 blk(256);
+  switch (gran) {
+    case LOKA_GRAN_ROW: {
+      const dim3 grd((unsigned)((p.rows + 7) / 8));
+      constexpr int kBig = sizeof(Tin) == 2 ? 16 : 8;  // <= 64 data registers per lane
+      if (p.cols <= 256 * 4) quant_row_kernel<Tin, FMT, SF, 4><<<grd, blk, 0, st>>>(p);
+      else quant_row_kernel<Tin, FMT, SF, kBig><<<grd, blk, 0, st>>>(p);
+      note_launch();
+      break;
+    }
+    case LOKA_GRAN_BLK_1x128: {
+      quant_1x128_kernel<Tin, FMT, SF><<<dim3((unsigned)((p.rows + 7) / 8)), blk, 0, st>>>(p);
+      note_launch();
+      break;
+    }
+    case LOKA_GRAN_BLK_128x128: {
+      quant_128x128_kernel<Tin, FMT, SF>
+          <<<dim3((unsigned)((p.cols + 127) / 128), (unsigned)((p.rows + 127) / 128)), blk, 0, st>>>(p);
+      note_launch();
+      break;
+    }
+    case LOKA_GRAN_TENSOR: {
+      int64_t nb = (p.rows + 7) / 8;
+      const int64_t cap = (int64_t)num_sms * 8;
+      if (nb > cap) nb = cap;
+      if (nb < 1) nb = 1;
+      if (phase == LOKA_PHASE_FULL || phase == LOKA_PHASE_AMAX_ONLY) {
+        cudaError_t e = cudaMemsetAsync(amax_dev, 0, sizeof(float), st);
+        if (e != cudaSuccess) return e;
+        amax_tensor_kernel<Tin><<<dim3((unsigned)nb), blk, 0, st>>>(p, reinterpret_cast<uint32_t*>(amax_dev));
+        note_launch();
+      }
+      if (phase == LOKA_PHASE_FULL || phase == LOKA_PHASE_CAST_WITH_AMAX) {
+        cast_tensor_kernel<Tin, FMT, SF><<<dim3((unsigned)nb), blk, 0, st>>>(p, amax_dev);
+        note_launch();
+      }
+      break;
+    }
+    default:
+      return cudaErrorNotSupported;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quantize(const QuantParams& p, bool in_bf16, int fmt, int scale_fmt, int gran, int phase,
+                            float* amax_dev, cudaStream_t st, int num_sms) {
+#define LOKA_Q(T, F, S)                                 \
+  if (fmt == F && scale_fmt == S)                       \
+    return launch_quant_t<T, F, S>(p, gran, phase, amax_dev, st, num_sms);
+  if (in_bf16) {
+    LOKA_Q(__nv_bfloat16, LOKA_E4M3, LOKA_SCALE_F32)
+    LOKA_Q(__nv_bfloat16, LOKA_E4M3, LOKA_SCALE_UE8M0)
+    LOKA_Q(__nv_bfloat16, LOKA_E5M2, LOKA_SCALE_F32)
+    LOKA_Q(__nv_bfloat16, LOKA_E5M2, LOKA_SCALE_UE8M0)
+  } else {
+    LOKA_Q(float, LOKA_E4M3, LOKA_SCALE_F32)
+    LOKA_Q(float, LOKA_E4M3, LOKA_SCALE_UE8M0)
+    LOKA_Q(float, LOKA_E5M2, LOKA_SCALE_F32)
+    LOKA_Q(float, LOKA_E5M2, LOKA_SCALE_UE8M0)
+  }
+#undef LOKA_Q
+  return cudaErrorNotSupported;
+}
+
+}  // namespace loka

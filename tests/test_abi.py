@@ -1,0 +1,94 @@
+"""C-ABI checks that need no GPU: libloka.so loads, exports every symbol include/loka.h declares,
+the ctypes structs match the header's sizes, host-only entry points work, and device entry
+points refuse to run without an sm_100 device (no CPU fallback)."""
+import ctypes as C
+import os
+import random
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "loka.h")
+
+
+@pytest.fixture(scope="module")
+def lk():
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2605_10886_b200 as lk
+    return lk
+
+
+def declared_symbols():
+    txt = open(HDR).read()
+    return sorted(set(re.findall(r"LOKA_API\s+[\w\s\*]+?\b(loka_\w+)\s*\(", txt)))
+
+
+def test_every_declared_symbol_is_exported(lk):
+    syms = declared_symbols()
+    assert len(syms) == 13, syms
+    out = subprocess.run(["nm", "-D", "--defined-only", lk.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (loka_\w+)", out))
+    assert set(syms) <= exported, set(syms) - exported
+    assert set(syms) == set(lk.EXPORTS)
+
+
+def test_struct_layouts_match_header(lk, tmp_path):
+    """Compile a tiny C program against include/loka.h and compare sizeof/offsetof with ctypes."""
+    src = tmp_path / "sz.c"
+    src.write_text('#include "loka.h"\n#include <stdio.h>\n#include <stddef.h>\nint main(){printf("%zu %zu %zu %zu %zu %zu %zu\\n",'
+                   'sizeof(loka_tensor), sizeof(loka_linear_args), sizeof(loka_probe_pair), sizeof(loka_probe_stats),'
+                   'sizeof(loka_candidate), offsetof(loka_linear_args, y), offsetof(loka_linear_args, status_dev));return 0;}\n')
+    exe = tmp_path / "sz"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    exp = [C.sizeof(lk.loka_tensor), C.sizeof(lk.loka_linear_args), C.sizeof(lk.loka_probe_pair),
+           C.sizeof(lk.loka_probe_stats), C.sizeof(lk.loka_candidate), lk.loka_linear_args.y.offset,
+           lk.loka_linear_args.status_dev.offset]
+    assert got == exp
+
+
+def test_host_helpers(lk):
+    assert lk.version() == 1
+    assert lk._lib.loka_status_string(0) == b"ok"
+    assert b"unsupported" in lk._lib.loka_status_string(3)
+
+
+def test_dispatch_select_matches_oracle_on_random_tables(lk):
+    """a8 is a pure host function: parity with oracle/dispatch.py needs no GPU."""
+    from oracle import dispatch
+    rnd = random.Random(11)
+    for _ in range(1000):
+        n = rnd.randint(0, 8)
+        ids = rnd.sample(list("abcdefghij"), n)
+        cands = [(ids[i], rnd.choice([0.05, 0.1, 0.2, 0.3, rnd.random() * 0.4]),
+                  rnd.choice([50.0, 80.0, 95.0, 100.0, rnd.uniform(40, 120)])) for i in range(n)]
+        ours = lk.loka_dispatch_select([(c, "fwd", m, t) for c, m, t in cands], 100.0, 0.2, 1.05)
+        assert ours == dispatch.select(cands, 100.0, 0.2, 1.05)
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="CPU-only check")
+def test_device_calls_refuse_without_gpu(lk):
+    """No CPU fallback: with no sm_100 device the compute entry points return an error status."""
+    assert lk.device_supported(0) is False
+    fake = 1 << 20  # a 16-byte aligned non-null pointer value; never dereferenced on the host
+    x = lk.loka_tensor(fake, lk.BF16, 4, 16, 16, None, 1, 0)
+    q = lk.loka_tensor(fake, lk.E4M3, 4, 16, 16, fake, 1, 0)
+    st = lk._lib.loka_quantize(C.byref(x), C.byref(q), None, 0, None, None, None, 0, None)
+    assert st in (lk.ERR_CUDA, lk.ERR_UNSUPPORTED)
+
+
+def test_shape_validation_is_host_side(lk):
+    """Invalid shapes are rejected before any device work (BLOCK_RMS with N % block != 0 -> ERR_SHAPE)."""
+    fake = 1 << 20
+    a = lk.loka_linear_args()
+    a.M, a.N, a.K = 128, 300, 128
+    a.a = lk.loka_tensor(fake, lk.E4M3, 128, 128, 128, fake, 1, 0)
+    a.b = lk.loka_tensor(fake, lk.E4M3, 300, 128, 128, fake, 1, 0)
+    a.y = lk.loka_tensor(fake, lk.F32, 128, 300, 304, None, 1, 0)
+    a.norm, a.norm_block = 3, 256
+    assert lk._lib.loka_fp8_linear_norm(C.byref(a), None, 0, None) == lk.ERR_SHAPE
+    a.b.rows = 299
+    assert lk._lib.loka_fp8_linear_norm(C.byref(a), None, 0, None) == lk.ERR_SHAPE

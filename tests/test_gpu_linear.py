@@ -1,0 +1,156 @@
+"""-m gpu: loka_fp8_linear_norm (a4+a5) against oracle/linear.py (FP64 on the dequantized
+operands the GPU consumed).  FP32 output: guarded max relative error <= 2e-3 (D17/D18);
+FP8 output: codes + row scales bit-exact vs the oracle's quantize of the GPU's own pre-cast
+values, and those values within 2e-3; BF16 output: 2e-3 plus one bf16 half-ulp."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from gpu_util import DEV, assert_bytes_equal, assert_scales_equal, f64, guarded_rel_err
+
+pytestmark = pytest.mark.gpu
+lk = pytest.importorskip("paper_2605_10886_b200") if torch.cuda.is_available() else None
+TOL = 2e-3
+
+
+def _operands(M, N, K, seed, xdist="gaussian", a_fmt="e4m3", b_fmt="e4m3", a_gran="row", b_gran="row"):
+    x = synth.heavy(M, K, seed) if xdist == "heavy" else synth.gaussian(M, K, seed)
+    w = synth.weight(N, K, seed + 1)
+    xq, xs = lk.loka_quantize(x.to(DEV), a_fmt, a_gran)
+    wq, ws = lk.loka_quantize(w.to(DEV), b_fmt, b_gran)
+    return xq, xs, wq, ws
+
+
+def _oracle(xq, xs, wq, ws, a_fmt="e4m3", b_fmt="e4m3", a_gran="row", b_gran="row", **kw):
+    return oracle.linear.linear_norm(xq.cpu().numpy(), xs.cpu().numpy(), a_fmt, a_gran, wq.cpu().numpy(),
+                                     ws.cpu().numpy(), b_fmt, b_gran, **kw)
+
+
+def test_cfg1_rowwise_layernorm():
+    """BJ configs[0]: X[256,256] x W[256,256], rowwise e4m3, LayerNorm, seed 0."""
+    M = N = K = 256
+    xq, xs, wq, ws = _operands(M, N, K, 0)
+    y, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm="layer", out_dtype="f32")
+    torch.cuda.synchronize()
+    yo = _oracle(xq, xs, wq, ws, norm="layer")
+    assert guarded_rel_err(f64(y), yo) <= TOL
+
+
+def test_accumulation_is_fp32_exact_on_representable_operands():
+    """D21: small-integer codes with power-of-two scales make every partial sum exact in FP32
+    (|sum| < 2^24), so any accumulation narrower than FP32 would show as a bit difference."""
+    g = torch.Generator().manual_seed(5)
+    for K in (128, 1024, 4096, 16384):
+        M, N = 128, 128
+        xi = torch.randint(-8, 9, (M, K), generator=g).float()
+        wi = torch.randint(-8, 9, (N, K), generator=g).float()
+        xq, xs = lk.loka_quantize(xi.to(DEV), "e4m3", "tensor", "ue8m0")
+        wq, ws = lk.loka_quantize(wi.to(DEV), "e4m3", "tensor", "ue8m0")
+        y, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, a_gran="tensor", b_gran="tensor", out_dtype="f32")
+        torch.cuda.synchronize()
+        yo = _oracle(xq, xs, wq, ws, a_gran="tensor", b_gran="tensor")
+        assert np.array_equal(f64(y), yo), (K, float(np.abs(f64(y) - yo).max()))
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 64, 128), (300, 128, 208), (256, 256, 1024), (200, 384, 512),
+                                   (4096 + 64, 1024, 1024), (256, 2048, 256), (130, 200, 96)])
+@pytest.mark.parametrize("norm", ["none", "layer", "rms"])
+def test_linear_norm_f32(M, N, K, norm):
+    xq, xs, wq, ws = _operands(M, N, K, M + N + K, xdist="heavy" if N % 3 else "gaussian")
+    y, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm=norm, out_dtype="f32")
+    torch.cuda.synchronize()
+    yo = _oracle(xq, xs, wq, ws, norm=norm)
+    assert guarded_rel_err(f64(y), yo) <= TOL
+
+
+@pytest.mark.parametrize("N,block", [(256, 256), (512, 256), (1024, 128), (768, 256), (128, 64)])
+def test_blocknorm(N, block):
+    M, K = 384, 512
+    xq, xs, wq, ws = _operands(M, N, K, 7)
+    y, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm="block_rms", norm_block=block, out_dtype="f32")
+    torch.cuda.synchronize()
+    yo = _oracle(xq, xs, wq, ws, norm="block_rms", block=block)
+    assert guarded_rel_err(f64(y), yo) <= TOL
+
+
+def test_blocknorm_indivisible_is_shape_error():
+    xq, xs, wq, ws = _operands(128, 300, 128, 1)
+    with pytest.raises(lk.LokaError) as e:
+        lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm="block_rms", norm_block=256)
+    assert e.value.status == lk.ERR_SHAPE
+
+
+@pytest.mark.parametrize("norm", ["layer", "rms"])
+def test_bias_gamma_beta_bf16_out(norm):
+    M, N, K = 256, 512, 256
+    xq, xs, wq, ws = _operands(M, N, K, 3)
+    g = torch.Generator().manual_seed(1)
+    bias = torch.randn(N, generator=g).to(torch.bfloat16)
+    gamma = (1 + 0.1 * torch.randn(N, generator=g)).float()
+    beta = (0.1 * torch.randn(N, generator=g)).float() if norm == "layer" else None
+    y, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm=norm, bias=bias.to(DEV), gamma=gamma.to(DEV),
+                                   beta=None if beta is None else beta.to(DEV), out_dtype="bf16")
+    torch.cuda.synchronize()
+    yo = _oracle(xq, xs, wq, ws, norm=norm, bias=bias.double().numpy(), gamma=gamma.double().numpy(),
+                 beta=None if beta is None else beta.double().numpy())
+    yg = f64(y)
+    rms = np.sqrt(np.mean(yo ** 2, axis=1, keepdims=True))
+    assert np.all(np.abs(yg - yo) <= TOL * np.maximum(np.abs(yo), rms) + 2.0 ** -8 * np.abs(yo))
+
+
+@pytest.mark.parametrize("norm,affine", [("layer", False), ("rms", False), ("none", False), ("block_rms", False),
+                                         ("layer", True)])
+@pytest.mark.parametrize("N", [256, 1024])
+def test_fp8_output_bit_exact(norm, affine, N):
+    """The epilogue's FP8 output (next layer's rowwise input): codes + row scales equal the
+    oracle's rowwise quantize of the GPU's own pre-cast FP32 values."""
+    M, K = 256, 512
+    xq, xs, wq, ws = _operands(M, N, K, 11, xdist="heavy")
+    pre = torch.empty(M, N, dtype=torch.float32, device=DEV)
+    gamma = torch.linspace(0.5, 1.5, N, device=DEV) if affine else None
+    y, ys = lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm=norm, out_dtype="e4m3", precast=pre, gamma=gamma)
+    torch.cuda.synchronize()
+    oq, os_ = oracle.quantize.quantize(f64(pre), "e4m3", "row")
+    assert_scales_equal(ys, os_)
+    assert_bytes_equal(y, oq)
+    yo = _oracle(xq, xs, wq, ws, norm=norm, gamma=None if gamma is None else f64(gamma))
+    assert guarded_rel_err(f64(pre), yo) <= TOL
+
+
+def test_tensorwise_e5m2_operands():
+    M, N, K = 256, 256, 384
+    xq, xs, wq, ws = _operands(M, N, K, 4, a_fmt="e5m2", b_fmt="e4m3", a_gran="tensor", b_gran="tensor")
+    y, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, a_fmt="e5m2", a_gran="tensor", b_gran="tensor", norm="rms")
+    torch.cuda.synchronize()
+    yo = _oracle(xq, xs, wq, ws, a_fmt="e5m2", a_gran="tensor", b_gran="tensor", norm="rms")
+    assert guarded_rel_err(f64(y), yo) <= TOL
+
+
+def test_cfg2_stack_full_size():
+    """BJ configs[1] in the bench's launch configuration: M=4096, 8 layers, rowwise e4m3, LayerNorm,
+    FP8 hand-off between layers; every layer checked on 64 sampled rows against the oracle run on
+    the GPU's own layer inputs."""
+    dims = synth.CFG2_DIMS
+    M = 4096
+    x = synth.gaussian(M, dims[0], 0, device=DEV)
+    hq, hs = lk.loka_quantize(x, "e4m3", "row")
+    rows = torch.randperm(M, generator=torch.Generator().manual_seed(1))[:64].sort().values.to(DEV)
+    for l in range(8):
+        K, N = dims[l], dims[l + 1]
+        w = synth.weight(N, K, 100 + l, device=DEV)
+        wq, ws = lk.loka_quantize(w, "e4m3", "row")
+        last = l == 7
+        pre = torch.empty(M, N, dtype=torch.float32, device=DEV)
+        y, ys = lk.loka_fp8_linear_norm(hq, hs, wq, ws, norm="layer", out_dtype="bf16" if last else "e4m3",
+                                        precast=pre)
+        torch.cuda.synchronize()
+        yo = oracle.linear.linear_norm(hq[rows].cpu().numpy(), hs[rows].cpu().numpy(), "e4m3", "row",
+                                       wq.cpu().numpy(), ws.cpu().numpy(), "e4m3", "row", norm="layer")
+        assert guarded_rel_err(f64(pre[rows]), yo) <= TOL, l
+        if not last:
+            oq, os_ = oracle.quantize.quantize(f64(pre[rows]), "e4m3", "row")
+            assert_bytes_equal(y[rows], oq)
+            assert_scales_equal(ys[rows], os_)
+            hq, hs = y, ys

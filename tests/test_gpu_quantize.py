@@ -1,0 +1,99 @@
+"""-m gpu: loka_quantize (a1-a3) bit-exact against oracle/quantize.py on the same input bytes."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from gpu_util import DEV, assert_bytes_equal, assert_scales_equal
+
+pytestmark = pytest.mark.gpu
+lk = pytest.importorskip("paper_2605_10886_b200") if torch.cuda.is_available() else None
+
+SHAPES = [(1, 16), (7, 300), (128, 128), (130, 260), (257, 1040), (64, 4096 + 16)]
+
+
+def _inputs(rows, cols, dtype, seed):
+    x = synth.heavy(rows, cols, seed) if seed % 2 else synth.gaussian(rows, cols, seed)
+    x = x.float() * 3.0 if dtype == torch.float32 else x
+    x = x.clone()
+    if rows > 3:
+        x[3] = 0.0           # all-zero row -> s = r = 1
+        x[2, : min(cols, 5)] = -0.0
+    return x
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("gran", ["row", "blk_1x128", "blk_128x128", "tensor"])
+@pytest.mark.parametrize("fmt", ["e4m3", "e5m2"])
+@pytest.mark.parametrize("scale_fmt", ["f32", "ue8m0"])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_quantize_bit_exact(shape, gran, fmt, scale_fmt, dtype):
+    rows, cols = shape
+    x = _inputs(rows, cols, dtype, seed=rows * 7 + cols)
+    q, s = lk.loka_quantize(x.to(DEV), fmt, gran, scale_fmt)
+    torch.cuda.synchronize()
+    oq, os_ = oracle.quantize.quantize(x.double().numpy(), fmt, gran, scale_fmt)
+    assert_scales_equal(s, os_, f"{gran}/{fmt}/{scale_fmt}")
+    assert_bytes_equal(q, oq, f"{gran}/{fmt}/{scale_fmt}")
+
+
+def test_tensorwise_split_phase_and_strided_input():
+    x = synth.heavy(300, 512, 5)
+    xd = torch.zeros(300, 640, dtype=torch.bfloat16, device=DEV)[:, :512]
+    xd.copy_(x.to(DEV))
+    amax = torch.empty(1, dtype=torch.float32, device=DEV)
+    lk.loka_quantize(xd, "e4m3", "tensor", phase="amax", amax=amax, want_q=False)
+    g = amax * 2.0  # as if another rank held a larger value
+    q, s = lk.loka_quantize(xd, "e4m3", "tensor", phase="cast", amax=g)
+    torch.cuda.synchronize()
+    assert float(amax) == float(x.float().abs().max())
+    oq, os_ = oracle.quantize.quantize(x.double().numpy(), "e4m3", "tensor", amax=np.array([float(g)]))
+    assert_scales_equal(s, os_)
+    assert_bytes_equal(q, oq)
+
+
+@pytest.mark.parametrize("gran", ["row", "blk_1x128", "blk_128x128", "tensor"])
+def test_transposed_copy(gran):
+    x = synth.gaussian(130, 272, 9)
+    q, s, qt, st = lk.loka_quantize(x.to(DEV), "e5m2", gran, transpose=True)
+    torch.cuda.synchronize()
+    oq, os_ = oracle.quantize.quantize(x.double().numpy(), "e5m2", gran)
+    assert_bytes_equal(q, oq)
+    assert_bytes_equal(qt, oq.T.copy())
+    tg = {"row": "col", "blk_1x128": "blk_128x1"}.get(gran, gran)
+    ts = os_.reshape(lk.scale_shape(130, 272, gran))
+    if gran in ("blk_1x128", "blk_128x128"):
+        ts = ts.T
+    assert_scales_equal(st, np.ascontiguousarray(ts).reshape(lk.scale_shape(272, 130, tg)))
+
+
+def test_nonfinite_sets_status():
+    x = synth.gaussian(8, 256, 1)
+    x[5, 17] = float("nan")
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    lk.loka_quantize(x.to(DEV), "e4m3", "row", status=st)
+    torch.cuda.synchronize()
+    assert int(st) & lk.DEVSTATUS_NONFINITE
+    x[5, 17] = float("inf")
+    st.zero_()
+    lk.loka_quantize(x.to(DEV), "e4m3", "tensor", status=st)
+    torch.cuda.synchronize()
+    assert int(st) & lk.DEVSTATUS_NONFINITE
+    st.zero_()
+    lk.loka_quantize(synth.gaussian(8, 256, 2).to(DEV), "e4m3", "row", status=st)
+    torch.cuda.synchronize()
+    assert int(st) == 0
+
+
+@pytest.mark.parametrize("rows,cols", [(4096, 1024), (32768, 4096)])
+def test_full_size_sampled(rows, cols):
+    """BASELINE sizes in the bench's launch config: device-generated input, rows sampled for the oracle."""
+    x = synth.heavy(rows, cols, 3, device=DEV)
+    q, s = lk.loka_quantize(x, "e4m3", "row")
+    torch.cuda.synchronize()
+    idx = torch.randperm(rows, generator=torch.Generator().manual_seed(0))[:64].sort().values
+    xs = x[idx.to(DEV)].cpu()
+    oq, os_ = oracle.quantize.quantize(xs.double().numpy(), "e4m3", "row")
+    assert_bytes_equal(q[idx.to(DEV)], oq)
+    assert_scales_equal(s[idx.to(DEV)], os_)
