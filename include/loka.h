@@ -203,6 +203,12 @@ LOKA_API int32_t loka_version(void);                    /* major*100 + minor */
 /* Number of kernel launches the library made since load (process-wide counter; for bench
  * evidence of "gpu_launches").                                                               */
 LOKA_API int64_t loka_launch_count(void);
+/* Pipeline watchdog (debug): every mbarrier wait in the GEMM kernels gives up after 4 s, records
+ * where it stalled and lets the kernel finish (with garbage output) instead of hanging the GPU.
+ * Returns the number of timed-out waits since the last reset (0 = healthy; -1 = CUDA error) and
+ * fills info3 = {tag (1 smem-empty, 2 smem-full, 3 accumulator-ready), block id,
+ * thread | parity << 32}.  reset != 0 clears the record.  Synchronous.                      */
+LOKA_API int64_t loka_debug_hang_info(uint64_t* info3, int32_t reset);
 
 #ifdef __cplusplus
 }

@@ -86,6 +86,7 @@ _sig = {
     "loka_device_supported": ([C.c_int32], C.c_int32),
     "loka_version": ([], C.c_int32),
     "loka_launch_count": ([], C.c_int64),
+    "loka_debug_hang_info": ([_P(C.c_uint64), C.c_int32], C.c_int64),
 }
 for _name, (_args, _ret) in _sig.items():
     _fn = getattr(_lib, _name)
@@ -257,3 +258,10 @@ def device_supported(device: int = 0) -> bool:
 
 def version() -> int:
     return int(_lib.loka_version())
+
+
+def debug_hang_info(reset: bool = True):
+    """(count, tag, block, thread|parity<<32) of pipeline-watchdog timeouts (0 count = healthy)."""
+    info = (C.c_uint64 * 3)()
+    n = _lib.loka_debug_hang_info(info, 1 if reset else 0)
+    return int(n), int(info[0]), int(info[1]), int(info[2])

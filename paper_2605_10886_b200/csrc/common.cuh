@@ -103,9 +103,34 @@ LOKA_DEVINL bool mbar_try_wait(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-LOKA_DEVINL void mbar_wait(uint64_t* bar, uint32_t parity) {
+LOKA_DEVINL uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Watchdog state (one copy per translation unit; linear.cu reads its own): a wait that exceeds kHangNs records where it hung,
+// raises g_loka_abort so every other wait returns at once, and returns — the kernel then
+// finishes with garbage output instead of hanging the GPU (read via loka_debug_hang_info).
+static __device__ unsigned long long g_loka_hang[4];  // per translation unit
+static __device__ int g_loka_abort;
+constexpr uint64_t kHangNs = 4000000000ull;
+
+LOKA_DEVINL void mbar_wait(uint64_t* bar, uint32_t parity, int tag = 0) {
   const uint32_t a = smem_u32(bar);
+  if (mbar_try_wait(a, parity)) return;
+  const uint64_t t0 = globaltimer_ns();
   while (!mbar_try_wait(a, parity)) {
+    if (*reinterpret_cast<volatile int*>(&g_loka_abort)) return;
+    if (globaltimer_ns() - t0 > kHangNs) {
+      if (atomicAdd(&g_loka_hang[0], 1ull) == 0) {
+        g_loka_hang[1] = (unsigned long long)tag;
+        g_loka_hang[2] = (unsigned long long)(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z));
+        g_loka_hang[3] = (unsigned long long)threadIdx.x | ((unsigned long long)parity << 32);
+      }
+      atomicExch(&g_loka_abort, 1);
+      return;
+    }
   }
 }
 

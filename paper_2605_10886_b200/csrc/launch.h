@@ -6,7 +6,8 @@
 
 namespace loka {
 
-void note_launch(int n = 1);  // process-wide launch counter (loka_launch_count)
+void note_launch(int n = 1);
+long long debug_hang_info(unsigned long long* info, int reset);  // process-wide launch counter (loka_launch_count)
 
 struct QuantParams {
   const void* x;

@@ -20,6 +20,7 @@
 
 namespace loka {
 
+
 constexpr int kThreads = 192;  // 6 warps
 constexpr int kBK = 128;       // FP8 elements of K per stage (128 B rows, SW128 atom)
 
@@ -121,7 +122,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kb = 0; kb < num_kb; ++kb) {
         const int s = kb % C::kStages;
         const uint32_t ph = (uint32_t)(kb / C::kStages) & 1u;
-        mbar_wait(&empty_bar[s], ph ^ 1u);
+        mbar_wait(&empty_bar[s], ph ^ 1u, 1);
         mbar_arrive_expect_tx(&full_bar[s], C::kStageBytes);
         tma_load_2d(sA + s * C::kStageA, &tma_a, &full_bar[s], kb * kBK, m0);
         tma_load_2d(sB + s * C::kStageB, &tma_b, &full_bar[s], kb * kBK, n0);
@@ -136,7 +137,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kb = 0; kb < num_kb; ++kb) {
         const int s = kb % C::kStages;
         const uint32_t ph = (uint32_t)(kb / C::kStages) & 1u;
-        mbar_wait(&full_bar[s], ph);
+        mbar_wait(&full_bar[s], ph, 2);
         tc_fence_after();
         const uint32_t a0 = smem_u32(sA + s * C::kStageA);
         const uint32_t b0 = smem_u32(sB + s * C::kStageB);
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int blk = norm == LOKA_NORM_BLOCK_RMS ? p.norm_block : BN;
     const int nblk_cta = (ncols + blk - 1) / blk;  // <= 8 (blk >= 32)
 
-    mbar_wait(tmem_full, 0);
+    mbar_wait(tmem_full, 0, 3);
     tc_fence_after();
 
     // y_j = acc_j * sa * sb_j + bias_j (identical in every pass)
@@ -428,6 +429,21 @@ static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const
   cudaError_t e = cudaLaunchKernelEx(&cfg, linear_norm_kernel<BN>, ta, tb, p);
   note_launch();
   return e;
+}
+
+// Host accessor for the watchdog: returns the number of timed-out waits since the last reset
+// and fills info[3] = {tag (1 empty, 2 full, 3 tmem_full), linear block id, thread | parity<<32}.
+long long debug_hang_info(unsigned long long* info, int reset) {
+  unsigned long long h[4] = {0, 0, 0, 0};
+  if (cudaMemcpyFromSymbol(h, g_loka_hang, sizeof(h)) != cudaSuccess) return -1;
+  if (info) info[0] = h[1], info[1] = h[2], info[2] = h[3];
+  if (reset) {
+    unsigned long long z[4] = {0, 0, 0, 0};
+    int zi = 0;
+    cudaMemcpyToSymbol(g_loka_hang, z, sizeof(z));
+    cudaMemcpyToSymbol(g_loka_abort, &zi, sizeof(zi));
+  }
+  return (long long)h[0];
 }
 
 cudaError_t launch_linear(const CUtensorMap& ta, const CUtensorMap& tb, const LinearParams& p, int bn,

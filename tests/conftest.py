@@ -35,3 +35,18 @@ def fp8_host_cast(tmp_path_factory):
     if r.returncode != 0:
         pytest.skip("cannot build cuda_fp8 host helper: " + r.stderr[-300:])
     return str(out)
+
+
+@pytest.fixture(autouse=True)
+def _gpu_watchdog(request):
+    """For GPU tests: fail loudly if a GEMM pipeline wait timed out (libloka's mbarrier watchdog)."""
+    yield
+    if "gpu" not in request.keywords:
+        return
+    import torch
+    if not torch.cuda.is_available():
+        return
+    import paper_2605_10886_b200 as lk
+    torch.cuda.synchronize()
+    n, tag, blk, thr = lk.debug_hang_info(reset=True)
+    assert n == 0, f"pipeline watchdog: {n} timed-out waits, tag={tag} block={blk} thread={thr & 0xffffffff} parity={thr >> 32}"

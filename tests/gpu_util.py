@@ -31,3 +31,13 @@ def guarded_rel_err(y: np.ndarray, yo: np.ndarray) -> float:
     guard = np.maximum(np.abs(yo), rms)
     guard = np.where(guard > 0, guard, 1.0)
     return float(np.max(np.abs(y - yo) / guard)) if y.size else 0.0
+
+
+def to_dev_padded(x: torch.Tensor, align_elems: int = 16) -> torch.Tensor:
+    """Copy a 2-D tensor to the GPU in storage whose leading dimension is a multiple of
+    ``align_elems`` (the C ABI requires ld * elem_size % 16 == 0)."""
+    rows, cols = x.shape
+    ld = -(-cols // align_elems) * align_elems
+    buf = torch.zeros(rows, ld, dtype=x.dtype, device=DEV)
+    buf[:, :cols].copy_(x.to(DEV))
+    return buf[:, :cols]

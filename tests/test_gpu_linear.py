@@ -8,7 +8,7 @@ import torch
 
 import oracle
 import synth
-from gpu_util import DEV, assert_bytes_equal, assert_scales_equal, f64, guarded_rel_err
+from gpu_util import DEV, assert_bytes_equal, assert_scales_equal, f64, guarded_rel_err, to_dev_padded
 
 pytestmark = pytest.mark.gpu
 lk = pytest.importorskip("paper_2605_10886_b200") if torch.cuda.is_available() else None
@@ -18,8 +18,8 @@ TOL = 2e-3
 def _operands(M, N, K, seed, xdist="gaussian", a_fmt="e4m3", b_fmt="e4m3", a_gran="row", b_gran="row"):
     x = synth.heavy(M, K, seed) if xdist == "heavy" else synth.gaussian(M, K, seed)
     w = synth.weight(N, K, seed + 1)
-    xq, xs = lk.loka_quantize(x.to(DEV), a_fmt, a_gran)
-    wq, ws = lk.loka_quantize(w.to(DEV), b_fmt, b_gran)
+    xq, xs = lk.loka_quantize(to_dev_padded(x), a_fmt, a_gran)
+    wq, ws = lk.loka_quantize(to_dev_padded(w), b_fmt, b_gran)
     return xq, xs, wq, ws
 
 

@@ -5,7 +5,7 @@ import torch
 
 import oracle
 import synth
-from gpu_util import DEV, assert_bytes_equal, assert_scales_equal
+from gpu_util import DEV, assert_bytes_equal, assert_scales_equal, to_dev_padded
 
 pytestmark = pytest.mark.gpu
 lk = pytest.importorskip("paper_2605_10886_b200") if torch.cuda.is_available() else None
@@ -31,7 +31,7 @@ def _inputs(rows, cols, dtype, seed):
 def test_quantize_bit_exact(shape, gran, fmt, scale_fmt, dtype):
     rows, cols = shape
     x = _inputs(rows, cols, dtype, seed=rows * 7 + cols)
-    q, s = lk.loka_quantize(x.to(DEV), fmt, gran, scale_fmt)
+    q, s = lk.loka_quantize(to_dev_padded(x), fmt, gran, scale_fmt)
     torch.cuda.synchronize()
     oq, os_ = oracle.quantize.quantize(x.double().numpy(), fmt, gran, scale_fmt)
     assert_scales_equal(s, os_, f"{gran}/{fmt}/{scale_fmt}")
@@ -56,7 +56,7 @@ def test_tensorwise_split_phase_and_strided_input():
 @pytest.mark.parametrize("gran", ["row", "blk_1x128", "blk_128x128", "tensor"])
 def test_transposed_copy(gran):
     x = synth.gaussian(130, 272, 9)
-    q, s, qt, st = lk.loka_quantize(x.to(DEV), "e5m2", gran, transpose=True)
+    q, s, qt, st = lk.loka_quantize(to_dev_padded(x), "e5m2", gran, transpose=True)
     torch.cuda.synchronize()
     oq, os_ = oracle.quantize.quantize(x.double().numpy(), "e5m2", gran)
     assert_bytes_equal(q, oq)
