@@ -328,11 +328,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 
     // ---- pass 2: normalise, cast, store ----
-    if (row_ok) {
+    {  // every lane executes the .sync.aligned TMEM loads; only rows < M store
       for (int c = 0; c < nchunks; ++c) {
         float v[32];
         load_y(c, v);
         norm_out(c, v);
+        if (!row_ok) continue;
         const int col0 = n0 + c * 32;
         const int nv = min(32, ncols - c * 32);
         if (p.precast) {
