@@ -177,6 +177,7 @@ typedef struct loka_probe_stats {
 } loka_probe_stats;
 
 /* One launch sequence for L layers; stats_dev is a DEVICE array of L loka_probe_stats.
+ * Any leading dimension is accepted (16-byte-aligned rows take the vector path).
  * Within 1e-5 relative of oracle/probe.py (D8-D10).                  */
 LOKA_API loka_status loka_probe_error(int32_t L, const loka_probe_pair* pairs, double floor_rel,
                              loka_probe_stats* stats_dev, void* ws, size_t ws_bytes, loka_stream_t stream);

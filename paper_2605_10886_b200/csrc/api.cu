@@ -292,10 +292,12 @@ loka_status loka_probe_error(int32_t L, const loka_probe_pair* pairs, double flo
     if ((q.out_dtype != LOKA_F32 && q.out_dtype != LOKA_BF16) || (q.ref_dtype != LOKA_F32 && q.ref_dtype != LOKA_BF16))
       return LOKA_ERR_INVALID_ARG;
     if (q.M < 0 || q.N < 0 || q.ld_out < q.N || q.ld_ref < q.N) return LOKA_ERR_SHAPE;
-    if (q.M * q.N > 0 && (!q.out || !q.ref || !aligned16(q.out) || !aligned16(q.ref))) return LOKA_ERR_INVALID_ARG;
-    if ((q.ld_out * elem_size(q.out_dtype)) % 16 || (q.ld_ref * elem_size(q.ref_dtype)) % 16)
-      return LOKA_ERR_INVALID_ARG;
-    layers[l] = ProbeLayer{q.out, q.ref, q.out_dtype == LOKA_BF16, q.ref_dtype == LOKA_BF16, q.M, q.N, q.ld_out, q.ld_ref};
+    if (q.M * q.N > 0 && (!q.out || !q.ref)) return LOKA_ERR_INVALID_ARG;
+    // any leading dimension is accepted; rows that are 16-byte aligned use vector loads
+    const int ov = aligned16(q.out) && (q.ld_out * elem_size(q.out_dtype)) % 16 == 0;
+    const int rv = aligned16(q.ref) && (q.ld_ref * elem_size(q.ref_dtype)) % 16 == 0;
+    layers[l] = ProbeLayer{q.out, q.ref, q.out_dtype == LOKA_BF16, q.ref_dtype == LOKA_BF16, q.M, q.N, q.ld_out, q.ld_ref,
+                           ov, rv};
   }
   loka_status st = check_device();
   if (st != LOKA_OK) return st;

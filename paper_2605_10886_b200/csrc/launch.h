@@ -51,6 +51,7 @@ struct ProbeLayer {
   const void* out; const void* ref;
   int32_t out_bf16, ref_bf16;
   int64_t M, N, ld_out, ld_ref;
+  int32_t out_vec, ref_vec;  // rows 16B-aligned: vector loads allowed
 };
 cudaError_t launch_probe(const ProbeLayer* layers_dev, int L, int64_t max_elems, double floor_rel,
                          void* stats_dev, double* partials, int nblk, cudaStream_t st);

@@ -25,8 +25,8 @@ struct ProbeStatsDev {  // == loka_probe_stats
   long long count, n_floored;
 };
 
-LOKA_DEVINL void load4(const void* base, int bf16, int64_t off, float (&v)[4], int n) {
-  if (n == 4) {
+LOKA_DEVINL void load4(const void* base, int bf16, int64_t off, float (&v)[4], int n, int vec) {
+  if (n == 4 && vec) {
     if (bf16) {
       const uint2 w = *reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(base) + off);
       v[0] = bf16lo_to_f32(w.x); v[1] = bf16hi_to_f32(w.x);
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(256) probe_p1(const __grid_constant__ ProbeBat
   for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < L.M; row += nw) {
     for (int64_t c = lane * 4; c < L.N; c += 128) {
       float v[4];
-      load4(L.ref, L.ref_bf16, row * L.ld_ref + c, v, (int)imin64(4, L.N - c));
+      load4(L.ref, L.ref_bf16, row * L.ld_ref + c, v, (int)imin64(4, L.N - c), L.ref_vec);
       acc += (double)(fabsf(v[0]) + fabsf(v[1])) + (double)(fabsf(v[2]) + fabsf(v[3]));
     }
   }
@@ -96,8 +96,8 @@ __global__ void __launch_bounds__(256) probe_p2(const __grid_constant__ ProbeBat
     for (int64_t c = lane * 4; c < L.N; c += 128) {
       const int n = (int)imin64(4, L.N - c);
       float o[4], r[4];
-      load4(L.out, L.out_bf16, row * L.ld_out + c, o, n);
-      load4(L.ref, L.ref_bf16, row * L.ld_ref + c, r, n);
+      load4(L.out, L.out_bf16, row * L.ld_out + c, o, n, L.out_vec);
+      load4(L.ref, L.ref_bf16, row * L.ld_ref + c, r, n, L.ref_vec);
       float part = 0.f;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {

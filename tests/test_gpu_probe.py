@@ -37,7 +37,9 @@ def test_probe_identical_and_scaled():
     ref = synth.gaussian(512, 512, 1).float().to(DEV) + 3.0
     st = lk.probe_stats_to_dicts(lk.loka_probe_error([(ref, ref), (ref * 1.1, ref)]))
     assert st[0]["mere"] == 0.0 and st[0]["max_rel"] == 0.0
-    assert abs(st[1]["mere"] - 0.1) < 1e-6
+    # 1.1*ref is itself rounded to FP32, so the exact value is the oracle's on the same arrays
+    _check(st[1], oracle.probe.mere_stats(f64(ref * 1.1), f64(ref)))
+    assert abs(st[1]["mere"] - 0.1) < 1e-4
 
 
 def test_probe_64_layers_one_call():
