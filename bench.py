@@ -334,6 +334,7 @@ def main():
         for _ in range(reps):
             flush.zero_()
             stack.quantize_all(sh)
+            torch.cuda._sleep(3_000_000)  # hold the stream while the host enqueues: events see GPU time only
             row = []
             for l in range(8):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

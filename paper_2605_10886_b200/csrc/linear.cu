@@ -9,35 +9,45 @@
 // B200 design:
 //   * CTA tile 128 x BN (BN in {64,128,256}), K staged 128 FP8 (= one 128B swizzle atom) per
 //     pipeline stage; warp 0 = TMA producer, warp 1 = tcgen05.mma issuer (one elected lane),
-//     warps 2-5 = epilogue (warp w reads TMEM lanes 32*(w%4)..+31, one row per thread).
+//     warps 2-9 = epilogue: warp w reads TMEM lanes 32*(w%4)..+31 (one row per thread) and the
+//     column half (w-2)/4 of the tile.
 //   * The 128 x BN FP32 accumulator lives in TMEM; it never goes to HBM (a5).
+//   * Epilogue arithmetic is packed FP32x2 (FMUL2/FFMA2/FADD2) with 3-input min/max; for norms
+//     without bias the per-row dequant scale s_a is folded into eps
+//     ((s z - s mu)/sqrt(s^2 var + eps) == (z - mu)/sqrt(var + eps/s^2)), and the normalised
+//     value is one FFMA: v = fma(y, rstd, -mu*rstd).
 //   * Case 2 (row wider than one CTA) is a thread-block cluster along N (<= 8 CTAs): per-row
-//     partial statistics (Chan's (n, mean, M2) for LayerNorm, sum of squares for RMSNorm, amax
-//     for an FP8 output) are exchanged through distributed shared memory and merged in
-//     cluster-rank order, so every CTA derives bit-identical row statistics.
+//     partial statistics (Chan's (n, mean, M2), sum of squares, y max/min) are exchanged through
+//     distributed shared memory and merged in cluster-rank order, so every CTA derives
+//     bit-identical row statistics.
+//   * Programmatic dependent launch: the prologue (barrier init, TMEM alloc, descriptor
+//     prefetch) overlaps the previous kernel's tail; global inputs are read after
+//     griddepcontrol.wait.
 #include "common.cuh"
 #include "launch.h"
 
 namespace loka {
 
-
-constexpr int kThreads = 192;  // 6 warps
-constexpr int kBK = 128;       // FP8 elements of K per stage (128 B rows, SW128 atom)
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;  // 10 warps
+constexpr int kBK = 128;                       // FP8 elements of K per stage (128 B rows, SW128 atom)
+constexpr int kRec = 16;                       // floats per row record in the half exchange
 
 template <int BN> struct LinCfg {
   static constexpr int kStageA = 128 * kBK;  // bytes
   static constexpr int kStageB = BN * kBK;
   static constexpr int kStageBytes = kStageA + kStageB;
-  static constexpr int kStages = (196 * 1024) / kStageBytes > 8 ? 8 : (196 * 1024) / kStageBytes;
+  static constexpr int kStages = (192 * 1024) / kStageBytes > 8 ? 8 : (192 * 1024) / kStageBytes;
   static constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
-  // smem: [stages A][stages B][barriers][tmem slot][column params 4*BN][stats 128*4]
   static constexpr int kOffB = kStages * kStageA;
   static constexpr int kOffBar = kOffB + kStages * kStageB;
   static constexpr int kOffTmem = kOffBar + (2 * kStages + 1) * 8;
-  static constexpr int kOffCol = (kOffTmem + 4 + 15) & ~15;
-  static constexpr int kOffStat = kOffCol + 4 * BN * 4;
-  static constexpr int kOffStat2 = kOffStat + 128 * 4 * 4;
-  static constexpr int kSmemBytes = kOffStat2 + 128 * 4 + 1024;  // + alignment slack
+  static constexpr int kOffCol = (kOffTmem + 4 + 15) & ~15;         // sb, bias, gamma, beta [BN]
+  static constexpr int kOffHx = kOffCol + 4 * BN * 4;                // [2][128][kRec]
+  static constexpr int kOffCs = kOffHx + 2 * 128 * kRec * 4;         // [128][8] cluster record
+  static constexpr int kOffCs2 = kOffCs + 128 * 8 * 4;               // [128] cluster amax
+  static constexpr int kSmemBytes = kOffCs2 + 128 * 4 + 1024;        // + alignment slack
+  static_assert(kSmemBytes <= 227 * 1024, "smem");
 };
 
 // Chan et al. pairwise merge of (n, mean, M2) — the same update as PAPER.md:293-299
@@ -52,6 +62,19 @@ LOKA_DEVINL void chan_merge(float& n, float& mean, float& m2, float nb, float me
   n = nt;
 }
 
+// Per-row record merged across the two column halves and across the cluster (non-BlockNorm):
+//   {n, mean, m2, ss, ymax, ymin}; BlockNorm: {ss_b[8], maxabs_b[8]} (blocks never span CTAs).
+struct RowRec {
+  float n, mean, m2, ss, ymax, ymin;
+  LOKA_DEVINL void init() { n = 0.f; mean = 0.f; m2 = 0.f; ss = 0.f; ymax = -INFINITY; ymin = INFINITY; }
+  LOKA_DEVINL void merge(const RowRec& o) {
+    chan_merge(n, mean, m2, o.n, o.mean, o.m2);
+    ss += o.ss;
+    ymax = fmaxf(ymax, o.ymax);
+    ymin = fminf(ymin, o.ymin);
+  }
+};
+
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     linear_norm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
@@ -65,12 +88,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty_bar = full_bar + C::kStages;
   uint64_t* tmem_full = empty_bar + C::kStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffTmem);
-  float* col_sb = reinterpret_cast<float*>(smem + C::kOffCol);
-  float* col_bias = col_sb + BN;
-  float* col_gamma = col_bias + BN;
-  float* col_beta = col_gamma + BN;
-  float* stat = reinterpret_cast<float*>(smem + C::kOffStat);    // [128][4]
-  float* stat2 = reinterpret_cast<float*>(smem + C::kOffStat2);  // [128]
+  float* col = reinterpret_cast<float*>(smem + C::kOffCol);  // [4][BN]: sb, bias, gamma, beta
+  float* hx = reinterpret_cast<float*>(smem + C::kOffHx);
+  float* cs = reinterpret_cast<float*>(smem + C::kOffCs);
+  float* cs2 = reinterpret_cast<float*>(smem + C::kOffCs2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * 128;
@@ -79,7 +100,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int num_kb = (p.K + kBK - 1) / kBK;
   const int csize = p.cluster_n;
 
-  // ---- one-time setup ----
+  // ---- one-time setup (overlaps the previous kernel under PDL) ----
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tma_a);
     tma_prefetch_desc(&tma_b);
@@ -91,17 +112,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
+  pdl_wait();  // inputs written by the previous kernel are visible from here on
   if (warp >= 2) {  // per-column epilogue parameters -> smem
-    for (int j = threadIdx.x - 64; j < BN; j += 128) {
+    for (int j = threadIdx.x - 64; j < BN; j += 32 * kEpiWarps) {
       const int n = n0 + j;
       const bool ok = n < p.N;
-      col_sb[j] = ok ? p.sb[p.sb_row ? n : 0] : 0.f;
+      col[j] = ok ? p.sb[p.sb_row ? n : 0] : 0.f;
       float b = 0.f;
       if (ok && p.bias) b = p.bias_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.bias)[n])
                                          : reinterpret_cast<const float*>(p.bias)[n];
-      col_bias[j] = b;
-      col_gamma[j] = (ok && p.gamma) ? p.gamma[n] : 1.f;
-      col_beta[j] = (ok && p.beta) ? p.beta[n] : 0.f;
+      col[BN + j] = b;
+      col[2 * BN + j] = (ok && p.gamma) ? p.gamma[n] : 1.f;
+      col[3 * BN + j] = (ok && p.beta) ? p.beta[n] : 0.f;
     }
   }
   tc_fence_before();
@@ -109,11 +131,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  // number of cluster-wide barriers every thread of the CTA executes (uniform)
+  const int norm = p.norm;
   const bool is_fp8_out = p.out_dtype == LOKA_E4M3 || p.out_dtype == LOKA_E5M2;
   const bool affine = p.gamma != nullptr || p.beta != nullptr;
-  const bool xchg_stats = csize > 1 && (p.norm == LOKA_NORM_LAYER || p.norm == LOKA_NORM_RMS);
-  const bool xchg_amax = csize > 1 && is_fp8_out;
+  const bool is_block = norm == LOKA_NORM_BLOCK_RMS;
+  // cluster-wide barriers: every thread of the CTA executes the same count (uniform)
+  const bool xchg_stats = csize > 1 && !is_block && (norm != LOKA_NORM_NONE || (is_fp8_out && !affine));
+  const bool xchg_amax = csize > 1 && is_fp8_out && (is_block || affine);
   const int n_cluster_bars = csize > 1 ? (int)xchg_stats + (int)xchg_amax + 1 : 0;
 
   if (warp == 0) {
@@ -153,137 +177,208 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
     for (int i = 0; i < n_cluster_bars; ++i) cluster_sync_all();
   } else {
-    // ===== epilogue: thread = one row of the 128 x BN tile =====
-    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    // ===== epilogue: thread = one row x one column half of the 128 x BN tile =====
+    const int q = warp & 3;              // TMEM lane quadrant this warp may access
+    const int h = (warp - 2) >> 2;       // column half
     const int r = q * 32 + lane;
     const int grow = m0 + r;
     const bool row_ok = grow < p.M;
+    constexpr int kHalf = BN / 2;
+    const int cb = h * kHalf;                          // first local column of this thread
+    const int nloc = max(0, min(kHalf, ncols - cb));   // valid columns of this thread
+    const int nchunks = (nloc + 31) / 32;
+    const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)cb;
     const float sa = row_ok ? p.sa[p.sa_row ? grow : 0] : 0.f;
-    const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16);
-    const int nchunks = (ncols + 31) / 32;
-    const int norm = p.norm;
-    const int blk = norm == LOKA_NORM_BLOCK_RMS ? p.norm_block : BN;
-    const int nblk_cta = (ncols + blk - 1) / blk;  // <= 8 (blk >= 32)
+    const bool has_bias = p.bias != nullptr;
+    const bool fold = !has_bias && norm != LOKA_NORM_NONE;  // s_a folded into eps
+    const float ys = fold ? 1.f : sa;
+    const int blk = is_block ? p.norm_block : BN;
+    const uint32_t col_s = smem_u32(col);
 
     mbar_wait(tmem_full, 0, 3);
     tc_fence_after();
+    pdl_launch_dependents();
 
-    // y_j = acc_j * sa * sb_j + bias_j (identical in every pass)
+    // y_j for the 32 columns of chunk c (local to this thread's half)
     auto load_y = [&](int c, float (&v)[32]) {
       tmem_ld32(taddr + (uint32_t)(c * 32), v);
+      const uint32_t o = (uint32_t)(cb + c * 32) * 4u;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int jj = c * 32 + j;
-        v[j] = __fadd_rn(__fmul_rn(__fmul_rn(v[j], sa), col_sb[jj]), col_bias[jj]);
+      for (int j = 0; j < 32; j += 4) {
+        float4 s4 = lds_f4(col_s + o + j * 4);
+        float2 s01 = make_float2(s4.x, s4.y), s23 = make_float2(s4.z, s4.w);
+        if (!fold) {
+          s01 = fmul2(s01, make_float2(ys, ys));
+          s23 = fmul2(s23, make_float2(ys, ys));
+        }
+        float2 a01 = make_float2(v[j], v[j + 1]), a23 = make_float2(v[j + 2], v[j + 3]);
+        if (has_bias) {
+          const float4 b4 = lds_f4(col_s + (uint32_t)BN * 4u + o + j * 4);
+          a01 = ffma2(a01, s01, make_float2(b4.x, b4.y));
+          a23 = ffma2(a23, s23, make_float2(b4.z, b4.w));
+        } else {
+          a01 = fmul2(a01, s01);
+          a23 = fmul2(a23, s23);
+        }
+        v[j] = a01.x; v[j + 1] = a01.y; v[j + 2] = a23.x; v[j + 3] = a23.y;
       }
     };
 
-    // ---- pass 1: row statistics over this CTA's columns ----
-    float st_n = 0.f, st_mean = 0.f, st_m2 = 0.f;  // LayerNorm (Chan)
-    float st_ss = 0.f;                              // RMSNorm
-    float blk_ss[8], blk_max[8];
+    // ---- pass 1: statistics over this thread's columns ----
+    RowRec rec;
+    rec.init();
+    float bss[8], bmax[8];  // BlockNorm: per block sum of squares and max |y|
 #pragma unroll
-    for (int b = 0; b < 8; ++b) blk_ss[b] = 0.f, blk_max[b] = 0.f;
-    float ymax = -INFINITY, ymin = INFINITY;
-    const bool need_pass1 = norm != LOKA_NORM_NONE || (is_fp8_out && !affine);
+    for (int b = 0; b < 8; ++b) bss[b] = 0.f, bmax[b] = 0.f;
+    const bool need_minmax = is_fp8_out && !affine;
+    const bool need_pass1 = norm != LOKA_NORM_NONE || need_minmax;
     if (need_pass1) {
       for (int c = 0; c < nchunks; ++c) {
         float v[32];
         load_y(c, v);
-        const int nv = min(32, ncols - c * 32);
-        if (norm == LOKA_NORM_LAYER) {
-          float s = 0.f;
+        const int nv = min(32, nloc - c * 32);
+        if (nv < 32) {  // ragged last chunk: replicate a valid value into the masked lanes so that
+                        // max/min are unaffected, and zero them for the sums
 #pragma unroll
-          for (int j = 0; j < 32; ++j) s += j < nv ? v[j] : 0.f;
-          const float mc = s / (float)nv;
-          float m2 = 0.f;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float d = j < nv ? v[j] - mc : 0.f;
-            m2 = fmaf(d, d, m2);
-          }
-          chan_merge(st_n, st_mean, st_m2, (float)nv, mc, m2);
-        } else if (norm == LOKA_NORM_RMS) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) st_ss = j < nv ? fmaf(v[j], v[j], st_ss) : st_ss;
-        } else if (norm == LOKA_NORM_BLOCK_RMS) {
-          const int b = (c * 32) / blk;
-          float ss = 0.f, mx = 0.f;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            if (j < nv) {
-              ss = fmaf(v[j], v[j], ss);
-              mx = fmaxf(mx, fabsf(v[j]));
-            }
-          }
-#pragma unroll
-          for (int bb = 0; bb < 8; ++bb)
-            if (bb == b) blk_ss[bb] += ss, blk_max[bb] = fmaxf(blk_max[bb], mx);
+          for (int j = 1; j < 32; ++j)
+            if (j >= nv) v[j] = v[0];
         }
+        float cmax = v[0], cmin = v[0];
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (j < nv) ymax = fmaxf(ymax, v[j]), ymin = fminf(ymin, v[j]);
+        for (int j = 0; j < 32; j += 2) cmax = fmax3(cmax, v[j], v[j + 1]), cmin = fmin3(cmin, v[j], v[j + 1]);
+        if (nv < 32) {
+#pragma unroll
+          for (int j = 1; j < 32; ++j)
+            if (j >= nv) v[j] = 0.f;
+        }
+        if (norm == LOKA_NORM_LAYER) {
+          float2 s0 = make_float2(0.f, 0.f), s1 = s0, s2 = s0, s3 = s0;
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) {
+            s0 = fadd2(s0, make_float2(v[j], v[j + 1]));
+            s1 = fadd2(s1, make_float2(v[j + 2], v[j + 3]));
+            s2 = fadd2(s2, make_float2(v[j + 4], v[j + 5]));
+            s3 = fadd2(s3, make_float2(v[j + 6], v[j + 7]));
+          }
+          s0 = fadd2(fadd2(s0, s1), fadd2(s2, s3));
+          const float mc = (s0.x + s0.y) / (float)nv;
+          const float2 nm = make_float2(-mc, -mc);
+          float2 q0 = make_float2(0.f, 0.f), q1 = q0;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const float2 d0 = fadd2(make_float2(v[j], v[j + 1]), nm);
+            const float2 d1 = fadd2(make_float2(v[j + 2], v[j + 3]), nm);
+            q0 = ffma2(d0, d0, q0);
+            q1 = ffma2(d1, d1, q1);
+          }
+          q0 = fadd2(q0, q1);
+          // masked lanes contributed (0 - mc)^2 each: remove them exactly as counted
+          float m2 = q0.x + q0.y;
+          if (nv < 32) m2 = fmaxf(0.f, m2 - (float)(32 - nv) * mc * mc);
+          chan_merge(rec.n, rec.mean, rec.m2, (float)nv, mc, m2);
+        } else if (norm == LOKA_NORM_RMS || is_block) {
+          float2 q0 = make_float2(0.f, 0.f), q1 = q0;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const float2 a = make_float2(v[j], v[j + 1]), b = make_float2(v[j + 2], v[j + 3]);
+            q0 = ffma2(a, a, q0);
+            q1 = ffma2(b, b, q1);
+          }
+          q0 = fadd2(q0, q1);
+          const float ss = q0.x + q0.y;
+          if (is_block) {
+            const int b = (cb + c * 32) / blk;
+            const float ma = fmaxf(cmax, -cmin);
+#pragma unroll
+            for (int bb = 0; bb < 8; ++bb)
+              if (bb == b) bss[bb] += ss, bmax[bb] = fmaxf(bmax[bb], ma);
+          } else {
+            rec.ss += ss;
+            rec.n += (float)nv;
+          }
+        } else {
+          rec.n += (float)nv;
+        }
+        rec.ymax = fmaxf(rec.ymax, cmax);
+        rec.ymin = fminf(rec.ymin, cmin);
+      }
+      // ---- combine the two column halves (fixed order h0, h1 -> identical in both) ----
+      float* my = hx + ((size_t)h * 128 + r) * kRec;
+      if (is_block) {
+#pragma unroll
+        for (int b = 0; b < 8; ++b) my[b] = bss[b], my[8 + b] = bmax[b];
+      } else {
+        my[0] = rec.n; my[1] = rec.mean; my[2] = rec.m2; my[3] = rec.ss; my[4] = rec.ymax; my[5] = rec.ymin;
+      }
+      named_bar_sync(1, 32 * kEpiWarps);
+      const float* r0 = hx + (size_t)r * kRec;
+      const float* r1 = hx + ((size_t)128 + r) * kRec;
+      if (is_block) {
+#pragma unroll
+        for (int b = 0; b < 8; ++b) bss[b] = r0[b] + r1[b], bmax[b] = fmaxf(r0[8 + b], r1[8 + b]);
+      } else {
+        rec.n = r0[0]; rec.mean = r0[1]; rec.m2 = r0[2]; rec.ss = r0[3]; rec.ymax = r0[4]; rec.ymin = r0[5];
+        RowRec o;
+        o.n = r1[0]; o.mean = r1[1]; o.m2 = r1[2]; o.ss = r1[3]; o.ymax = r1[4]; o.ymin = r1[5];
+        rec.merge(o);
       }
     }
 
     // ---- cross-CTA statistics (Case 2) ----
-    float mu = 0.f, rstd = 1.f;
-    if (norm == LOKA_NORM_LAYER || norm == LOKA_NORM_RMS) {
-      float n_tot = st_n, mean = st_mean, m2 = st_m2, ss = st_ss, mx = ymax, mn = ymin;
-      if (xchg_stats) {
-        stat[r * 4 + 0] = norm == LOKA_NORM_LAYER ? st_mean : st_ss;
-        stat[r * 4 + 1] = st_m2;
-        stat[r * 4 + 2] = ymax;
-        stat[r * 4 + 3] = ymin;
-        cluster_sync_all();
-        n_tot = 0.f; mean = 0.f; m2 = 0.f; ss = 0.f; mx = -INFINITY; mn = INFINITY;
-        const uint32_t la = smem_u32(&stat[r * 4]);
-        for (int rk = 0; rk < csize; ++rk) {
-          const uint32_t ra = mapa_shared(la, (uint32_t)rk);
-          const float a0 = ld_dsmem_f32(ra), a1 = ld_dsmem_f32(ra + 4);
-          const float a2 = ld_dsmem_f32(ra + 8), a3 = ld_dsmem_f32(ra + 12);
-          const float nk = (float)min(BN, p.N - rk * BN);
-          if (norm == LOKA_NORM_LAYER) chan_merge(n_tot, mean, m2, nk, a0, a1);
-          else ss += a0, n_tot += nk;
-          mx = fmaxf(mx, a2);
-          mn = fminf(mn, a3);
-        }
-      } else if (norm == LOKA_NORM_RMS) {
-        n_tot = (float)ncols;
+    if (xchg_stats) {
+      if (h == 0) {
+        float* d = cs + r * 8;
+        d[0] = rec.n; d[1] = rec.mean; d[2] = rec.m2; d[3] = rec.ss; d[4] = rec.ymax; d[5] = rec.ymin;
       }
-      ymax = mx;
-      ymin = mn;
-      if (norm == LOKA_NORM_LAYER) {
-        mu = mean;
-        rstd = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(m2, n_tot), p.eps)));
-      } else {
-        mu = 0.f;
-        rstd = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, n_tot), p.eps)));
+      cluster_sync_all();
+      rec.init();
+      const uint32_t la = smem_u32(cs + r * 8);
+      for (int rk = 0; rk < csize; ++rk) {
+        const uint32_t ra = mapa_shared(la, (uint32_t)rk);
+        RowRec o;
+        o.n = ld_dsmem_f32(ra); o.mean = ld_dsmem_f32(ra + 4); o.m2 = ld_dsmem_f32(ra + 8);
+        o.ss = ld_dsmem_f32(ra + 12); o.ymax = ld_dsmem_f32(ra + 16); o.ymin = ld_dsmem_f32(ra + 20);
+        rec.merge(o);
       }
     }
-    float blk_rstd[8];
+
+    // ---- finalize: v = fma(y, rstd, c0) per column (BlockNorm: per block) ----
+    const float eps_eff = fold ? __fdiv_rn(p.eps, __fmul_rn(sa, sa)) : p.eps;
+    float rstd = 1.f, c0 = 0.f;
+    if (norm == LOKA_NORM_LAYER) {
+      rstd = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(rec.m2, rec.n), eps_eff)));
+      c0 = -__fmul_rn(rec.mean, rstd);
+    } else if (norm == LOKA_NORM_RMS) {
+      rstd = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(rec.ss, rec.n), eps_eff)));
+    }
+    float brs[8];
 #pragma unroll
     for (int b = 0; b < 8; ++b)
-      blk_rstd[b] = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(blk_ss[b], (float)blk), p.eps)));
+      brs[b] = is_block ? __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(bss[b], (float)blk), eps_eff))) : 1.f;
 
-    // out_j = norm(y_j) (identical in every pass)
+    // out = norm(y) (identical in every pass)
     auto norm_out = [&](int c, float (&v)[32]) {
-      if (norm == LOKA_NORM_LAYER || norm == LOKA_NORM_RMS) {
+      if (norm == LOKA_NORM_NONE) return;
+      float rs = rstd;
+      if (is_block) {
+        const int b = (cb + c * 32) / blk;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int jj = c * 32 + j;
-          float o = __fmul_rn(__fsub_rn(v[j], mu), rstd);
-          if (affine) o = __fadd_rn(__fmul_rn(o, col_gamma[jj]), col_beta[jj]);
-          v[j] = o;
+        for (int bb = 0; bb < 8; ++bb)
+          if (bb == b) rs = brs[bb];
+      }
+      const float2 r2 = make_float2(rs, rs), c2 = make_float2(c0, c0);
+      const uint32_t o = (uint32_t)(cb + c * 32) * 4u;
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        float2 a = ffma2(make_float2(v[j], v[j + 1]), r2, c2);
+        float2 b = ffma2(make_float2(v[j + 2], v[j + 3]), r2, c2);
+        if (affine) {
+          const float4 g4 = lds_f4(col_s + 2u * BN * 4u + o + j * 4);
+          const float4 e4 = lds_f4(col_s + 3u * BN * 4u + o + j * 4);
+          a = ffma2(a, make_float2(g4.x, g4.y), make_float2(e4.x, e4.y));
+          b = ffma2(b, make_float2(g4.z, g4.w), make_float2(e4.z, e4.w));
         }
-      } else if (norm == LOKA_NORM_BLOCK_RMS) {
-        const int b = (c * 32) / blk;
-        float rs = blk_rstd[0];
-#pragma unroll
-        for (int bb = 1; bb < 8; ++bb)
-          if (bb == b) rs = blk_rstd[bb];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(v[j], rs);
+        v[j] = a.x; v[j + 1] = a.y; v[j + 2] = b.x; v[j + 3] = b.y;
       }
     };
 
@@ -291,110 +386,112 @@ __global__ void __launch_bounds__(kThreads, 1)
     float r_out = 1.f;
     if (is_fp8_out) {
       float amax = 0.f;
-      if (!affine) {  // out is monotone in y: the amax is attained at ymax or ymin exactly
-        if (norm == LOKA_NORM_LAYER || norm == LOKA_NORM_RMS) {
-          const float hi = __fmul_rn(__fsub_rn(ymax, mu), rstd);
-          const float lo = __fmul_rn(__fsub_rn(ymin, mu), rstd);
-          amax = fmaxf(fabsf(hi), fabsf(lo));
-        } else if (norm == LOKA_NORM_BLOCK_RMS) {
-          for (int b = 0; b < nblk_cta; ++b) amax = fmaxf(amax, __fmul_rn(blk_max[b], blk_rstd[b]));
+      if (!affine) {  // v is monotone in y: max |v| is attained at ymax or ymin, exactly
+        if (is_block) {
+          const int nb_cta = (ncols + blk - 1) / blk;
+#pragma unroll
+          for (int b = 0; b < 8; ++b)
+            if (b < nb_cta) amax = fmaxf(amax, __fmul_rn(bmax[b], brs[b]));
+        } else if (norm == LOKA_NORM_NONE) {
+          amax = fmaxf(fabsf(rec.ymax), fabsf(rec.ymin));
         } else {
-          amax = fmaxf(fabsf(ymax), fabsf(ymin));
+          amax = fmaxf(fabsf(fmaf(rec.ymax, rstd, c0)), fabsf(fmaf(rec.ymin, rstd, c0)));
         }
-      } else {  // affine: one more pass over TMEM
+      } else {  // affine: one more pass over TMEM, then combine halves
         for (int c = 0; c < nchunks; ++c) {
           float v[32];
           load_y(c, v);
           norm_out(c, v);
-          const int nv = min(32, ncols - c * 32);
+          const int nv = min(32, nloc - c * 32);
 #pragma unroll
           for (int j = 0; j < 32; ++j)
             if (j < nv) amax = fmaxf(amax, fabsf(v[j]));
         }
+        float* my = hx + ((size_t)h * 128 + r) * kRec;
+        named_bar_sync(1, 32 * kEpiWarps);  // everyone finished reading hx from pass 1
+        my[15] = amax;
+        named_bar_sync(1, 32 * kEpiWarps);
+        amax = fmaxf(hx[(size_t)r * kRec + 15], hx[((size_t)128 + r) * kRec + 15]);
       }
-      if (nchunks == 0) amax = 0.f;
       if (xchg_amax) {
-        stat2[r] = amax;
+        if (h == 0) cs2[r] = amax;
         cluster_sync_all();
         amax = 0.f;
-        const uint32_t la = smem_u32(&stat2[r]);
+        const uint32_t la = smem_u32(&cs2[r]);
         for (int rk = 0; rk < csize; ++rk) amax = fmaxf(amax, ld_dsmem_f32(mapa_shared(la, (uint32_t)rk)));
       }
       if (__float_as_uint(amax) >= 0x7F800000u && p.status) atomicOr(p.status, LOKA_DEVSTATUS_NONFINITE);
       float s_out;
       if (p.out_dtype == LOKA_E4M3) scales_from_amax<LOKA_E4M3, LOKA_SCALE_F32>(amax, s_out, r_out);
       else scales_from_amax<LOKA_E5M2, LOKA_SCALE_F32>(amax, s_out, r_out);
-      if (row_ok && blockIdx.y == 0 && p.y_scales) p.y_scales[grow] = s_out;
+      if (row_ok && blockIdx.y == 0 && h == 0 && p.y_scales) p.y_scales[grow] = s_out;
     }
 
-    // ---- pass 2: normalise, cast, store ----
-    {  // every lane executes the .sync.aligned TMEM loads; only rows < M store
-      for (int c = 0; c < nchunks; ++c) {
-        float v[32];
-        load_y(c, v);
-        norm_out(c, v);
-        if (!row_ok) continue;
-        const int col0 = n0 + c * 32;
-        const int nv = min(32, ncols - c * 32);
-        if (p.precast) {
-          float* dst = p.precast + (int64_t)grow * p.ld_pre + col0;
+    // ---- pass 2: normalise, cast, store (every lane runs the .sync.aligned TMEM loads) ----
+    for (int c = 0; c < nchunks; ++c) {
+      float v[32];
+      load_y(c, v);
+      norm_out(c, v);
+      if (!row_ok) continue;
+      const int lc = cb + c * 32;  // local column
+      const int nv = min(32, nloc - c * 32);
+      const int64_t gcol = (int64_t)n0 + lc;
+      if (p.precast) {
+        float* dst = p.precast + (int64_t)grow * p.ld_pre + gcol;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nv) dst[j] = v[j];
+      }
+      if (p.out_dtype == LOKA_F32) {
+        float* dst = reinterpret_cast<float*>(p.y) + (int64_t)grow * p.ldy + gcol;
+        if (nv == 32) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        } else {
 #pragma unroll
           for (int j = 0; j < 32; ++j)
             if (j < nv) dst[j] = v[j];
         }
-        if (p.out_dtype == LOKA_F32) {
-          float* dst = reinterpret_cast<float*>(p.y) + (int64_t)grow * p.ldy + col0;
-          if (nv == 32) {
+      } else if (p.out_dtype == LOKA_BF16) {
+        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.y) + (int64_t)grow * p.ldy + gcol;
+        uint32_t w[16];
 #pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-          } else {
+        for (int j = 0; j < 16; ++j) {
+          __nv_bfloat162 hh = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+          w[j] = *reinterpret_cast<uint32_t*>(&hh);
+        }
+        if (nv == 32) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (j < nv) dst[j] = v[j];
-          }
-        } else if (p.out_dtype == LOKA_BF16) {
-          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.y) + (int64_t)grow * p.ldy + col0;
-          if (nv == 32) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              uint4 w;
-              __nv_bfloat162 h0 = __floats2bfloat162_rn(v[j], v[j + 1]);
-              __nv_bfloat162 h1 = __floats2bfloat162_rn(v[j + 2], v[j + 3]);
-              __nv_bfloat162 h2 = __floats2bfloat162_rn(v[j + 4], v[j + 5]);
-              __nv_bfloat162 h3 = __floats2bfloat162_rn(v[j + 6], v[j + 7]);
-              w.x = *reinterpret_cast<uint32_t*>(&h0);
-              w.y = *reinterpret_cast<uint32_t*>(&h1);
-              w.z = *reinterpret_cast<uint32_t*>(&h2);
-              w.w = *reinterpret_cast<uint32_t*>(&h3);
-              *reinterpret_cast<uint4*>(dst + j) = w;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (j < nv) dst[j] = __float2bfloat16_rn(v[j]);
-          }
+          for (int j = 0; j < 16; j += 4)
+            *reinterpret_cast<uint4*>(dst + 2 * j) = make_uint4(w[j], w[j + 1], w[j + 2], w[j + 3]);
         } else {
-          uint8_t* dst = reinterpret_cast<uint8_t*>(p.y) + (int64_t)grow * p.ldy + col0;
-          uint32_t w[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float a = __fmul_rn(v[4 * j], r_out), b = __fmul_rn(v[4 * j + 1], r_out);
-            const float c2 = __fmul_rn(v[4 * j + 2], r_out), d = __fmul_rn(v[4 * j + 3], r_out);
-            w[j] = p.out_dtype == LOKA_E4M3 ? cvt_fp8x4<LOKA_E4M3>(a, b, c2, d) : cvt_fp8x4<LOKA_E5M2>(a, b, c2, d);
-          }
-          if (nv == 32) {
-            *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
-            *reinterpret_cast<uint4*>(dst + 16) = make_uint4(w[4], w[5], w[6], w[7]);
-          } else {
+          for (int j = 0; j < 32; ++j)
+            if (j < nv) dst[j] = __float2bfloat16_rn(v[j]);
+        }
+      } else {
+        uint8_t* dst = reinterpret_cast<uint8_t*>(p.y) + (int64_t)grow * p.ldy + gcol;
+        const float2 rr = make_float2(r_out, r_out);
+        uint32_t w[8];
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (j < nv) dst[j] = (uint8_t)(w[j >> 2] >> (8 * (j & 3)));
-          }
+        for (int j = 0; j < 8; ++j) {
+          const float2 a = fmul2(make_float2(v[4 * j], v[4 * j + 1]), rr);
+          const float2 b = fmul2(make_float2(v[4 * j + 2], v[4 * j + 3]), rr);
+          w[j] = p.out_dtype == LOKA_E4M3 ? cvt_fp8x4<LOKA_E4M3>(a.x, a.y, b.x, b.y)
+                                           : cvt_fp8x4<LOKA_E5M2>(a.x, a.y, b.x, b.y);
+        }
+        if (nv == 32) {
+          *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+          *reinterpret_cast<uint4*>(dst + 16) = make_uint4(w[4], w[5], w[6], w[7]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < nv) dst[j] = (uint8_t)(w[j >> 2] >> (8 * (j & 3)));
         }
       }
     }
-    if (csize > 1) cluster_sync_all();  // peers may still read our stats from DSMEM
+    if (csize > 1) cluster_sync_all();  // peers may still read our records from DSMEM
   }
 
   tc_fence_before();
@@ -403,6 +500,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc<C::kTmemCols>(tmem_base);
   }
+}
+
+// Host accessor for the watchdog: returns the number of timed-out waits since the last reset
+// and fills info[3] = {tag (1 empty, 2 full, 3 tmem_full), linear block id, thread | parity<<32}.
+long long debug_hang_info(unsigned long long* info, int reset) {
+  unsigned long long h[4] = {0, 0, 0, 0};
+  if (cudaMemcpyFromSymbol(h, g_loka_hang, sizeof(h)) != cudaSuccess) return -1;
+  if (info) info[0] = h[1], info[1] = h[2], info[2] = h[3];
+  if (reset) {
+    unsigned long long z[4] = {0, 0, 0, 0};
+    int zi = 0;
+    cudaMemcpyToSymbol(g_loka_hang, z, sizeof(z));
+    cudaMemcpyToSymbol(g_loka_abort, &zi, sizeof(zi));
+  }
+  return (long long)h[0];
 }
 
 template <int BN>
@@ -420,31 +532,18 @@ static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const
   cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.dynamicSmemBytes = C::kSmemBytes;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 1;
   attr[0].val.clusterDim.y = (unsigned)p.cluster_n;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   cudaError_t e = cudaLaunchKernelEx(&cfg, linear_norm_kernel<BN>, ta, tb, p);
   note_launch();
   return e;
-}
-
-// Host accessor for the watchdog: returns the number of timed-out waits since the last reset
-// and fills info[3] = {tag (1 empty, 2 full, 3 tmem_full), linear block id, thread | parity<<32}.
-long long debug_hang_info(unsigned long long* info, int reset) {
-  unsigned long long h[4] = {0, 0, 0, 0};
-  if (cudaMemcpyFromSymbol(h, g_loka_hang, sizeof(h)) != cudaSuccess) return -1;
-  if (info) info[0] = h[1], info[1] = h[2], info[2] = h[3];
-  if (reset) {
-    unsigned long long z[4] = {0, 0, 0, 0};
-    int zi = 0;
-    cudaMemcpyToSymbol(g_loka_hang, z, sizeof(z));
-    cudaMemcpyToSymbol(g_loka_abort, &zi, sizeof(zi));
-  }
-  return (long long)h[0];
 }
 
 cudaError_t launch_linear(const CUtensorMap& ta, const CUtensorMap& tb, const LinearParams& p, int bn,

@@ -103,6 +103,7 @@ LOKA_DEVINL void flag_nonfinite(uint32_t amax_bits, int32_t* status) {
 // ----- ROW: one warp per row; rows of <= 256*NREG elements stay in registers -------------
 template <typename Tin, int FMT, int SF, int NREG>
 __global__ void __launch_bounds__(256) quant_row_kernel(QuantParams p) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= p.rows) return;
@@ -159,6 +160,7 @@ __global__ void __launch_bounds__(256) quant_row_kernel(QuantParams p) {
 // ----- BLK_1x128: one warp per row, 16 lanes per 128-column block -------------------------
 template <typename Tin, int FMT, int SF>
 __global__ void __launch_bounds__(256) quant_1x128_kernel(QuantParams p) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= p.rows) return;
@@ -197,6 +199,7 @@ __global__ void __launch_bounds__(256) quant_1x128_kernel(QuantParams p) {
 // ----- BLK_128x128: one CTA (8 warps) per 128x128 block, block held in registers --------
 template <typename Tin, int FMT, int SF>
 __global__ void __launch_bounds__(256) quant_128x128_kernel(QuantParams p) {
+  pdl_wait();
   __shared__ uint32_t red[8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t bc = blockIdx.x, br = blockIdx.y;
@@ -243,6 +246,7 @@ __global__ void __launch_bounds__(256) quant_128x128_kernel(QuantParams p) {
 // ----- TENSOR: amax pass (atomicMax on bit patterns into a zeroed word) + cast pass -------
 template <typename Tin>
 __global__ void __launch_bounds__(256) amax_tensor_kernel(QuantParams p, uint32_t* amax_bits) {
+  pdl_wait();
   __shared__ uint32_t red[8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nwarps = (int64_t)gridDim.x * 8;
@@ -269,6 +273,7 @@ __global__ void __launch_bounds__(256) amax_tensor_kernel(QuantParams p, uint32_
 
 template <typename Tin, int FMT, int SF>
 __global__ void __launch_bounds__(256) cast_tensor_kernel(QuantParams p, const float* amax_dev) {
+  pdl_wait();
   const float amax = *amax_dev;
   float s, r;
   scales_from_amax<FMT, SF>(amax, s, r);
@@ -295,52 +300,62 @@ __global__ void __launch_bounds__(256) cast_tensor_kernel(QuantParams p, const f
   }
 }
 
-// ----- host-side launch -------------------------------------------------------------------
+// ----- host-side launch (programmatic dependent launch: prologue overlaps the previous kernel)
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  note_launch();
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <typename Tin, int FMT, int SF>
 static cudaError_t launch_quant_t(const QuantParams& p, int gran, int phase, float* amax_dev, cudaStream_t st,
                                   int num_sms) {
   const dim3 blk(256);
+  cudaError_t e = cudaSuccess;
   switch (gran) {
     case LOKA_GRAN_ROW: {
       const dim3 grd((unsigned)((p.rows + 7) / 8));
       constexpr int kBig = sizeof(Tin) == 2 ? 16 : 8;  // <= 64 data registers per lane
-      if (p.cols <= 256 * 4) quant_row_kernel<Tin, FMT, SF, 4><<<grd, blk, 0, st>>>(p);
-      else quant_row_kernel<Tin, FMT, SF, kBig><<<grd, blk, 0, st>>>(p);
-      note_launch();
+      if (p.cols <= 256 * 4) e = launch_pdl(quant_row_kernel<Tin, FMT, SF, 4>, grd, blk, st, p);
+      else e = launch_pdl(quant_row_kernel<Tin, FMT, SF, kBig>, grd, blk, st, p);
       break;
     }
-    case LOKA_GRAN_BLK_1x128: {
-      quant_1x128_kernel<Tin, FMT, SF><<<dim3((unsigned)((p.rows + 7) / 8)), blk, 0, st>>>(p);
-      note_launch();
+    case LOKA_GRAN_BLK_1x128:
+      e = launch_pdl(quant_1x128_kernel<Tin, FMT, SF>, dim3((unsigned)((p.rows + 7) / 8)), blk, st, p);
       break;
-    }
-    case LOKA_GRAN_BLK_128x128: {
-      quant_128x128_kernel<Tin, FMT, SF>
-          <<<dim3((unsigned)((p.cols + 127) / 128), (unsigned)((p.rows + 127) / 128)), blk, 0, st>>>(p);
-      note_launch();
+    case LOKA_GRAN_BLK_128x128:
+      e = launch_pdl(quant_128x128_kernel<Tin, FMT, SF>,
+                     dim3((unsigned)((p.cols + 127) / 128), (unsigned)((p.rows + 127) / 128)), blk, st, p);
       break;
-    }
     case LOKA_GRAN_TENSOR: {
       int64_t nb = (p.rows + 7) / 8;
       const int64_t cap = (int64_t)num_sms * 8;
       if (nb > cap) nb = cap;
       if (nb < 1) nb = 1;
       if (phase == LOKA_PHASE_FULL || phase == LOKA_PHASE_AMAX_ONLY) {
-        cudaError_t e = cudaMemsetAsync(amax_dev, 0, sizeof(float), st);
+        e = cudaMemsetAsync(amax_dev, 0, sizeof(float), st);
         if (e != cudaSuccess) return e;
-        amax_tensor_kernel<Tin><<<dim3((unsigned)nb), blk, 0, st>>>(p, reinterpret_cast<uint32_t*>(amax_dev));
-        note_launch();
+        e = launch_pdl(amax_tensor_kernel<Tin>, dim3((unsigned)nb), blk, st, p, reinterpret_cast<uint32_t*>(amax_dev));
+        if (e != cudaSuccess) return e;
       }
-      if (phase == LOKA_PHASE_FULL || phase == LOKA_PHASE_CAST_WITH_AMAX) {
-        cast_tensor_kernel<Tin, FMT, SF><<<dim3((unsigned)nb), blk, 0, st>>>(p, amax_dev);
-        note_launch();
-      }
+      if (phase == LOKA_PHASE_FULL || phase == LOKA_PHASE_CAST_WITH_AMAX)
+        e = launch_pdl(cast_tensor_kernel<Tin, FMT, SF>, dim3((unsigned)nb), blk, st, p, (const float*)amax_dev);
       break;
     }
     default:
       return cudaErrorNotSupported;
   }
-  return cudaGetLastError();
+  return e;
 }
 
 cudaError_t launch_quantize(const QuantParams& p, bool in_bf16, int fmt, int scale_fmt, int gran, int phase,
