@@ -168,10 +168,14 @@ constexpr uint64_t kHangNs = 4000000000ull;
 LOKA_DEVINL void mbar_wait(uint64_t* bar, uint32_t parity, int tag = 0) {
   const uint32_t a = smem_u32(bar);
   if (mbar_try_wait(a, parity)) return;
-  const uint64_t t0 = globaltimer_ns();
+  uint64_t t0 = 0;
+  uint32_t spins = 0;
   while (!mbar_try_wait(a, parity)) {
+    if ((++spins & 1023u) != 0) continue;  // the watchdog costs nothing on the normal path
+    const uint64_t t = globaltimer_ns();
+    if (t0 == 0) t0 = t;
     if (*reinterpret_cast<volatile int*>(&g_loka_abort)) return;
-    if (globaltimer_ns() - t0 > kHangNs) {
+    if (t - t0 > kHangNs) {
       if (atomicAdd(&g_loka_hang[0], 1ull) == 0) {
         g_loka_hang[1] = (unsigned long long)tag;
         g_loka_hang[2] = (unsigned long long)(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z));

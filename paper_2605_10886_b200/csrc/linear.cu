@@ -195,7 +195,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int blk = is_block ? p.norm_block : BN;
     const uint32_t col_s = smem_u32(col);
 
-    mbar_wait(tmem_full, 0, 3);
+    if (lane == 0) mbar_wait(tmem_full, 0, 3);  // one waiter per warp
+    __syncwarp();
     tc_fence_after();
     pdl_launch_dependents();
 
