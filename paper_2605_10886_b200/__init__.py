@@ -87,6 +87,7 @@ _sig = {
     "loka_version": ([], C.c_int32),
     "loka_launch_count": ([], C.c_int64),
     "loka_debug_hang_info": ([_P(C.c_uint64), C.c_int32], C.c_int64),
+    "loka_debug_trace": ([C.c_int32, _P(C.c_uint64), C.c_int64], C.c_int64),
 }
 for _name, (_args, _ret) in _sig.items():
     _fn = getattr(_lib, _name)
@@ -265,3 +266,10 @@ def debug_hang_info(reset: bool = True):
     info = (C.c_uint64 * 3)()
     n = _lib.loka_debug_hang_info(info, 1 if reset else 0)
     return int(n), int(info[0]), int(info[1]), int(info[2])
+
+
+def debug_trace(enable: int = -1, n: int = 0):
+    """Phase-trace control/readout (see include/loka.h loka_debug_trace). Returns a list of stamps."""
+    buf = (C.c_uint64 * max(n, 1))()
+    got = _lib.loka_debug_trace(enable, buf if n else None, n)
+    return [int(buf[i]) for i in range(max(got, 0))]

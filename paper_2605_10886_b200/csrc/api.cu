@@ -109,6 +109,10 @@ int32_t loka_device_supported(int32_t device) {
 int32_t loka_version(void) { return LOKA_VERSION_MAJOR * 100 + LOKA_VERSION_MINOR; }
 int64_t loka_launch_count(void) { return (int64_t)g_launches.load(); }
 
+int64_t loka_debug_trace(int32_t enable, uint64_t* out, int64_t n) {
+  return (int64_t)debug_trace(enable, reinterpret_cast<unsigned long long*>(out), n);
+}
+
 int64_t loka_debug_hang_info(uint64_t* info3, int32_t reset) {
   return (int64_t)debug_hang_info(reinterpret_cast<unsigned long long*>(info3), reset);
 }

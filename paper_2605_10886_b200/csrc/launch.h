@@ -7,7 +7,8 @@
 namespace loka {
 
 void note_launch(int n = 1);
-long long debug_hang_info(unsigned long long* info, int reset);  // process-wide launch counter (loka_launch_count)
+long long debug_hang_info(unsigned long long* info, int reset);
+long long debug_trace(int enable, unsigned long long* out, long long n);  // process-wide launch counter (loka_launch_count)
 
 struct QuantParams {
   const void* x;

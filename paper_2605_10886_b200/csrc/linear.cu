@@ -28,6 +28,17 @@
 
 namespace loka {
 
+// Opt-in phase trace (loka_debug_trace): per CTA, 8 globaltimer stamps
+//   0 entry | 1 after griddepcontrol.wait | 2 first TMA issued | 3 first stage landed (MMA)
+//   4 last MMA committed | 5 accumulator ready (epilogue) | 6 statistics done | 7 stores done
+constexpr int kTraceCtas = 4096;
+static __device__ unsigned long long g_trace[kTraceCtas * 8];
+static __device__ int g_trace_on;
+#define LOKA_TRACE(slot)                                                                   \
+  do {                                                                                     \
+    if (trace_on && cta_lin < kTraceCtas) g_trace[cta_lin * 8 + (slot)] = globaltimer_ns(); \
+  } while (0)
+
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + 32 * kEpiWarps;  // 10 warps
 constexpr int kBK = 128;                       // FP8 elements of K per stage (128 B rows, SW128 atom)
@@ -99,6 +110,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int ncols = min(BN, p.N - n0);  // valid columns of this CTA (> 0)
   const int num_kb = (p.K + kBK - 1) / kBK;
   const int csize = p.cluster_n;
+  const int trace_on = *reinterpret_cast<volatile int*>(&g_trace_on);
+  const int cta_lin = blockIdx.x + gridDim.x * blockIdx.y;
+  if (threadIdx.x == 0) LOKA_TRACE(0);
 
   // ---- one-time setup (overlaps the previous kernel under PDL) ----
   if (warp == 0 && lane == 0) {
@@ -113,6 +127,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
   pdl_wait();  // inputs written by the previous kernel are visible from here on
+  if (threadIdx.x == 0) LOKA_TRACE(1);
   if (warp >= 2) {  // per-column epilogue parameters -> smem
     for (int j = threadIdx.x - 64; j < BN; j += 32 * kEpiWarps) {
       const int n = n0 + j;
@@ -150,6 +165,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive_expect_tx(&full_bar[s], C::kStageBytes);
         tma_load_2d(sA + s * C::kStageA, &tma_a, &full_bar[s], kb * kBK, m0);
         tma_load_2d(sB + s * C::kStageB, &tma_b, &full_bar[s], kb * kBK, n0);
+        if (kb == 0) LOKA_TRACE(2);
       }
     }
     __syncwarp();
@@ -162,6 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int s = kb % C::kStages;
         const uint32_t ph = (uint32_t)(kb / C::kStages) & 1u;
         mbar_wait(&full_bar[s], ph, 2);
+        if (kb == 0) LOKA_TRACE(3);
         tc_fence_after();
         const uint32_t a0 = smem_u32(sA + s * C::kStageA);
         const uint32_t b0 = smem_u32(sB + s * C::kStageB);
@@ -173,6 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit(&empty_bar[s]);
       }
       mma_commit(tmem_full);
+      LOKA_TRACE(4);
     }
     __syncwarp();
     for (int i = 0; i < n_cluster_bars; ++i) cluster_sync_all();
@@ -199,6 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
     tc_fence_after();
     pdl_launch_dependents();
+    if (warp == 2 && lane == 0) LOKA_TRACE(5);
 
     // y_j for the 32 columns of chunk c (local to this thread's half)
     auto load_y = [&](int c, float (&v)[32]) {
@@ -429,6 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 
     // ---- pass 2: normalise, cast, store (every lane runs the .sync.aligned TMEM loads) ----
+    if (warp == 2 && lane == 0) LOKA_TRACE(6);
     for (int c = 0; c < nchunks; ++c) {
       float v[32];
       load_y(c, v);
@@ -492,6 +512,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+    if (warp == 2 && lane == 0) LOKA_TRACE(7);
     if (csize > 1) cluster_sync_all();  // peers may still read our records from DSMEM
   }
 
@@ -516,6 +537,22 @@ long long debug_hang_info(unsigned long long* info, int reset) {
     cudaMemcpyToSymbol(g_loka_abort, &zi, sizeof(zi));
   }
   return (long long)h[0];
+}
+
+long long debug_trace(int enable, unsigned long long* out, long long n) {
+  long long got = 0;
+  if (out && n > 0) {
+    got = n < (long long)kTraceCtas * 8 ? n : (long long)kTraceCtas * 8;
+    if (cudaMemcpyFromSymbol(out, g_trace, (size_t)got * 8) != cudaSuccess) return -1;
+  }
+  if (enable >= 0) {
+    if (enable) {
+      static unsigned long long zero[kTraceCtas * 8];
+      cudaMemcpyToSymbol(g_trace, zero, sizeof(zero));
+    }
+    cudaMemcpyToSymbol(g_trace_on, &enable, sizeof(int));
+  }
+  return got;
 }
 
 template <int BN>
