@@ -211,9 +211,10 @@ LOKA_API int64_t loka_launch_count(void);
  * thread | parity << 32}.  reset != 0 clears the record.  Synchronous.                      */
 LOKA_API int64_t loka_debug_hang_info(uint64_t* info3, int32_t reset);
 /* Phase trace (debug/profiling): enable = 1 clears the buffer and makes every later GEMM CTA
- * record 8 globaltimer stamps (entry, after grid-dependency wait, first TMA issued, first stage
- * landed, last MMA committed, accumulator ready, statistics done, stores done) at
- * out[(blockIdx.x + gridDim.x*blockIdx.y)*8 + slot] for the first 4096 CTAs of the LAST launch;
+ * record 16 globaltimer stamps (entry, after grid-dependency wait, first TMA issued, first stage
+ * landed, last MMA committed, accumulator ready, statistics done, stores done, pass-1 done,
+ * halves merged, cluster merged, finalized) at
+ * out[(blockIdx.x + gridDim.x*blockIdx.y)*16 + slot] for the first 4096 CTAs of the LAST launch;
  * enable = 0 turns it off, enable = -1 leaves it unchanged.  Copies up to n stamps into out
  * (host, may be NULL).  Returns the number copied, -1 on a CUDA error.  Synchronous.          */
 LOKA_API int64_t loka_debug_trace(int32_t enable, uint64_t* out, int64_t n);

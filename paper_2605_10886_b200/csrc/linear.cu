@@ -32,11 +32,11 @@ namespace loka {
 //   0 entry | 1 after griddepcontrol.wait | 2 first TMA issued | 3 first stage landed (MMA)
 //   4 last MMA committed | 5 accumulator ready (epilogue) | 6 statistics done | 7 stores done
 constexpr int kTraceCtas = 4096;
-static __device__ unsigned long long g_trace[kTraceCtas * 8];
+static __device__ unsigned long long g_trace[kTraceCtas * 16];
 static __device__ int g_trace_on;
 #define LOKA_TRACE(slot)                                                                   \
   do {                                                                                     \
-    if (trace_on && cta_lin < kTraceCtas) g_trace[cta_lin * 8 + (slot)] = globaltimer_ns(); \
+    if (trace_on && cta_lin < kTraceCtas) g_trace[cta_lin * 16 + (slot)] = globaltimer_ns(); \
   } while (0)
 
 constexpr int kEpiWarps = 8;
@@ -44,21 +44,27 @@ constexpr int kThreads = 64 + 32 * kEpiWarps;  // 10 warps
 constexpr int kBK = 128;                       // FP8 elements of K per stage (128 B rows, SW128 atom)
 constexpr int kRec = 16;                       // floats per row record in the half exchange
 
+constexpr int kMaxCluster = 8;
+
 template <int BN> struct LinCfg {
   static constexpr int kStageA = 128 * kBK;  // bytes
   static constexpr int kStageB = BN * kBK;
   static constexpr int kStageBytes = kStageA + kStageB;
-  static constexpr int kStages = (192 * 1024) / kStageBytes > 8 ? 8 : (192 * 1024) / kStageBytes;
+  // everything but the operand ring: column params, half exchange, pushed cluster records
+  static constexpr int kFixed = 4 * BN * 4 + 2 * 128 * kRec * 4 + kMaxCluster * 128 * 16 + kMaxCluster * 128 * 4 +
+                                512 + 1024;
+  static constexpr int kStagesFit = (227 * 1024 - kFixed) / kStageBytes;
+  static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
   static constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
   static constexpr int kOffB = kStages * kStageA;
   static constexpr int kOffBar = kOffB + kStages * kStageB;
   static constexpr int kOffTmem = kOffBar + (2 * kStages + 1) * 8;
   static constexpr int kOffCol = (kOffTmem + 4 + 15) & ~15;         // sb, bias, gamma, beta [BN]
   static constexpr int kOffHx = kOffCol + 4 * BN * 4;                // [2][128][kRec]
-  static constexpr int kOffCs = kOffHx + 2 * 128 * kRec * 4;         // [128][8] cluster record
-  static constexpr int kOffCs2 = kOffCs + 128 * 8 * 4;               // [128] cluster amax
-  static constexpr int kSmemBytes = kOffCs2 + 128 * 4 + 1024;        // + alignment slack
-  static_assert(kSmemBytes <= 227 * 1024, "smem");
+  static constexpr int kOffCs = kOffHx + 2 * 128 * kRec * 4;         // [kMaxCluster][128] float4 records
+  static constexpr int kOffCs2 = kOffCs + kMaxCluster * 128 * 16;    // [kMaxCluster][128] amax
+  static constexpr int kSmemBytes = kOffCs2 + kMaxCluster * 128 * 4 + 1024;  // + alignment slack
+  static_assert(kStages >= 2 && kSmemBytes <= 227 * 1024, "smem");
 };
 
 // Chan et al. pairwise merge of (n, mean, M2) — the same update as PAPER.md:293-299
@@ -322,46 +328,60 @@ __global__ void __launch_bounds__(kThreads, 1)
         rec.ymax = fmaxf(rec.ymax, cmax);
         rec.ymin = fminf(rec.ymin, cmin);
       }
+      if (warp == 2 && lane == 0) LOKA_TRACE(8);
       // ---- combine the two column halves (fixed order h0, h1 -> identical in both) ----
-      float* my = hx + ((size_t)h * 128 + r) * kRec;
+      // component-major [half][component][row]: consecutive lanes hit consecutive banks
+      float* my = hx + (size_t)h * kRec * 128 + r;
       if (is_block) {
 #pragma unroll
-        for (int b = 0; b < 8; ++b) my[b] = bss[b], my[8 + b] = bmax[b];
+        for (int b = 0; b < 8; ++b) my[b * 128] = bss[b], my[(8 + b) * 128] = bmax[b];
       } else {
-        my[0] = rec.n; my[1] = rec.mean; my[2] = rec.m2; my[3] = rec.ss; my[4] = rec.ymax; my[5] = rec.ymin;
+        my[0] = rec.n; my[128] = rec.mean; my[256] = rec.m2; my[384] = rec.ss; my[512] = rec.ymax;
+        my[640] = rec.ymin;
       }
       named_bar_sync(1, 32 * kEpiWarps);
-      const float* r0 = hx + (size_t)r * kRec;
-      const float* r1 = hx + ((size_t)128 + r) * kRec;
+      const float* r0 = hx + r;
+      const float* r1 = hx + (size_t)kRec * 128 + r;
       if (is_block) {
 #pragma unroll
-        for (int b = 0; b < 8; ++b) bss[b] = r0[b] + r1[b], bmax[b] = fmaxf(r0[8 + b], r1[8 + b]);
+        for (int b = 0; b < 8; ++b)
+          bss[b] = r0[b * 128] + r1[b * 128], bmax[b] = fmaxf(r0[(8 + b) * 128], r1[(8 + b) * 128]);
       } else {
-        rec.n = r0[0]; rec.mean = r0[1]; rec.m2 = r0[2]; rec.ss = r0[3]; rec.ymax = r0[4]; rec.ymin = r0[5];
+        rec.n = r0[0]; rec.mean = r0[128]; rec.m2 = r0[256]; rec.ss = r0[384]; rec.ymax = r0[512]; rec.ymin = r0[640];
         RowRec o;
-        o.n = r1[0]; o.mean = r1[1]; o.m2 = r1[2]; o.ss = r1[3]; o.ymax = r1[4]; o.ymin = r1[5];
+        o.n = r1[0]; o.mean = r1[128]; o.m2 = r1[256]; o.ss = r1[384]; o.ymax = r1[512]; o.ymin = r1[640];
         rec.merge(o);
       }
     }
+    if (warp == 2 && lane == 0) LOKA_TRACE(9);
 
     // ---- cross-CTA statistics (Case 2) ----
+    // Push: the h == 0 thread of row r stores this CTA's record (mean|ss, m2, ymax, ymin) into
+    // slot [my rank][r] of every cluster peer (one st.shared::cluster.v4 per peer); after the
+    // cluster barrier every thread merges slots 0..C-1 from local smem in rank order.
     if (xchg_stats) {
+      const uint32_t my_rank = cluster_ctarank();
       if (h == 0) {
-        float* d = cs + r * 8;
-        d[0] = rec.n; d[1] = rec.mean; d[2] = rec.m2; d[3] = rec.ss; d[4] = rec.ymax; d[5] = rec.ymin;
+        const float4 v = make_float4(norm == LOKA_NORM_LAYER ? rec.mean : rec.ss, rec.m2, rec.ymax, rec.ymin);
+        const uint32_t la = smem_u32(cs + ((size_t)my_rank * 128 + r) * 4);
+        for (int rk = 0; rk < csize; ++rk) st_dsmem_f4(mapa_shared(la, (uint32_t)rk), v);
       }
       cluster_sync_all();
       rec.init();
-      const uint32_t la = smem_u32(cs + r * 8);
       for (int rk = 0; rk < csize; ++rk) {
-        const uint32_t ra = mapa_shared(la, (uint32_t)rk);
+        const float4 v = lds_f4(smem_u32(cs + ((size_t)rk * 128 + r) * 4));
         RowRec o;
-        o.n = ld_dsmem_f32(ra); o.mean = ld_dsmem_f32(ra + 4); o.m2 = ld_dsmem_f32(ra + 8);
-        o.ss = ld_dsmem_f32(ra + 12); o.ymax = ld_dsmem_f32(ra + 16); o.ymin = ld_dsmem_f32(ra + 20);
+        o.n = (float)min(BN, p.N - rk * BN);
+        o.mean = norm == LOKA_NORM_LAYER ? v.x : 0.f;
+        o.m2 = v.y;
+        o.ss = norm == LOKA_NORM_LAYER ? 0.f : v.x;
+        o.ymax = v.z;
+        o.ymin = v.w;
         rec.merge(o);
       }
     }
 
+    if (warp == 2 && lane == 0) LOKA_TRACE(10);
     // ---- finalize: v = fma(y, rstd, c0) per column (BlockNorm: per block) ----
     const float eps_eff = fold ? __fdiv_rn(p.eps, __fmul_rn(sa, sa)) : p.eps;
     float rstd = 1.f, c0 = 0.f;
@@ -402,6 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
 
+    if (warp == 2 && lane == 0) LOKA_TRACE(11);
     // ---- FP8 output: row amax of the normalised values -> row scale ----
     float r_out = 1.f;
     if (is_fp8_out) {
@@ -427,18 +448,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 32; ++j)
             if (j < nv) amax = fmaxf(amax, fabsf(v[j]));
         }
-        float* my = hx + ((size_t)h * 128 + r) * kRec;
         named_bar_sync(1, 32 * kEpiWarps);  // everyone finished reading hx from pass 1
-        my[15] = amax;
+        hx[((size_t)h * kRec + 15) * 128 + r] = amax;
         named_bar_sync(1, 32 * kEpiWarps);
-        amax = fmaxf(hx[(size_t)r * kRec + 15], hx[((size_t)128 + r) * kRec + 15]);
+        amax = fmaxf(hx[(size_t)15 * 128 + r], hx[((size_t)kRec + 15) * 128 + r]);
       }
-      if (xchg_amax) {
-        if (h == 0) cs2[r] = amax;
+      if (xchg_amax) {  // push this CTA's row amax into slot [my rank] of every peer
+        const uint32_t my_rank = cluster_ctarank();
+        if (h == 0) {
+          const uint32_t la = smem_u32(&cs2[my_rank * 128 + r]);
+          for (int rk = 0; rk < csize; ++rk) st_dsmem_f32(mapa_shared(la, (uint32_t)rk), amax);
+        }
         cluster_sync_all();
         amax = 0.f;
-        const uint32_t la = smem_u32(&cs2[r]);
-        for (int rk = 0; rk < csize; ++rk) amax = fmaxf(amax, ld_dsmem_f32(mapa_shared(la, (uint32_t)rk)));
+        for (int rk = 0; rk < csize; ++rk) amax = fmaxf(amax, cs2[rk * 128 + r]);
       }
       if (__float_as_uint(amax) >= 0x7F800000u && p.status) atomicOr(p.status, LOKA_DEVSTATUS_NONFINITE);
       float s_out;
@@ -542,12 +565,12 @@ long long debug_hang_info(unsigned long long* info, int reset) {
 long long debug_trace(int enable, unsigned long long* out, long long n) {
   long long got = 0;
   if (out && n > 0) {
-    got = n < (long long)kTraceCtas * 8 ? n : (long long)kTraceCtas * 8;
+    got = n < (long long)kTraceCtas * 16 ? n : (long long)kTraceCtas * 16;
     if (cudaMemcpyFromSymbol(out, g_trace, (size_t)got * 8) != cudaSuccess) return -1;
   }
   if (enable >= 0) {
     if (enable) {
-      static unsigned long long zero[kTraceCtas * 8];
+      static unsigned long long zero[kTraceCtas * 16];
       cudaMemcpyToSymbol(g_trace, zero, sizeof(zero));
     }
     cudaMemcpyToSymbol(g_trace_on, &enable, sizeof(int));

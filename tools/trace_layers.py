@@ -15,7 +15,7 @@ dev = torch.device("cuda")
 M = 4096
 x = synth.gaussian(M, DIMS[0], 0, device=dev)
 hq, hs = lk.loka_quantize(x, "e4m3", "row")
-names = ["entry", "pdl_wait", "tma0", "stage0", "mma_done", "acc_ready", "stats", "stored"]
+names = ["entry", "pdl", "tma0", "stage0", "mma", "acc", "pre2", "stored", "p1", "halves", "clus", "fin"]
 for l in range(8):
     K, N = DIMS[l], DIMS[l + 1]
     wq, ws = lk.loka_quantize(synth.weight(N, K, 100 + l, device=dev), "e4m3", "row")
@@ -25,7 +25,7 @@ for l in range(8):
             lk.debug_trace(1)
         y, ys = lk.loka_fp8_linear_norm(hq, hs, wq, ws, norm="layer", out_dtype="bf16" if l == 7 else "e4m3")
         torch.cuda.synchronize()
-    t = np.array(lk.debug_trace(0, 4096 * 8), dtype=np.int64).reshape(-1, 8)
+    t = np.array(lk.debug_trace(0, 4096 * 16), dtype=np.int64).reshape(-1, 16)[:, :12]
     t = t[t[:, 0] > 0]
     base = t[:, 0].min()
     rel = (t - base) / 1000.0  # us
