@@ -127,6 +127,14 @@ LOKA_API loka_status loka_quantize(const loka_tensor* x, loka_tensor* q, loka_te
                           loka_stream_t stream);
 LOKA_API size_t loka_quantize_workspace_size(const loka_tensor* x, const loka_tensor* q);
 
+/* Grouped a1/a2: G (<= 64) independent ROW-granular quantizations in ONE launch (e.g. a layer
+ * stack's input activation plus every layer's weight).  x[g], q[g] as for loka_quantize with
+ * phase FULL and no transposed copy; all x[g] share one input dtype and all q[g] one FP8 format
+ * and scale format, q[g].gran == LOKA_GRAN_ROW.  Results are bit-identical to G separate
+ * loka_quantize calls.                                                                        */
+LOKA_API loka_status loka_quantize_grouped(int32_t G, const loka_tensor* x, loka_tensor* q, int32_t* status_dev,
+                                           loka_stream_t stream);
+
 /* ---- a4-a5: FP8 GEMM + fused epilogue ----------------------------------------------------- */
 typedef struct loka_linear_args {
   int64_t M, N, K;

@@ -73,6 +73,7 @@ _sig = {
     "loka_quantize": ([_P(loka_tensor), _P(loka_tensor), _P(loka_tensor), C.c_int, C.c_void_p, C.c_void_p,
                        C.c_void_p, C.c_size_t, C.c_void_p], C.c_int),
     "loka_quantize_workspace_size": ([_P(loka_tensor), _P(loka_tensor)], C.c_size_t),
+    "loka_quantize_grouped": ([C.c_int32, _P(loka_tensor), _P(loka_tensor), C.c_void_p, C.c_void_p], C.c_int),
     "loka_fp8_linear_norm": ([_P(loka_linear_args), C.c_void_p, C.c_size_t, C.c_void_p], C.c_int),
     "loka_linear_workspace_size": ([_P(loka_linear_args)], C.c_size_t),
     "loka_grouped_fp8_linear": ([C.c_int32, _P(loka_linear_args), C.c_void_p, C.c_size_t, C.c_void_p], C.c_int),
@@ -273,3 +274,22 @@ def debug_trace(enable: int = -1, n: int = 0):
     buf = (C.c_uint64 * max(n, 1))()
     got = _lib.loka_debug_trace(enable, buf if n else None, n)
     return [int(buf[i]) for i in range(max(got, 0))]
+
+
+def loka_quantize_grouped(xs, fmt: str = "e4m3", scale_fmt: str = "f32", outs=None, scales=None, status=None,
+                          stream=None):
+    """Grouped ROW quantize of several 2-D tensors in one launch.  Returns [(codes, scales)]."""
+    G = len(xs)
+    xa = (loka_tensor * G)()
+    qa = (loka_tensor * G)()
+    res = []
+    for g, x in enumerate(xs):
+        r, c = x.shape
+        o = outs[g] if outs is not None else torch.empty(r, (c + 15) // 16 * 16, dtype=torch.uint8,
+                                                         device=x.device)[:, :c]
+        s = scales[g] if scales is not None else torch.empty(r, dtype=torch.float32, device=x.device)
+        xa[g] = _tensor(x, _dtype_code(x), r, c)
+        qa[g] = _tensor(o, FMT[fmt], r, c, s, "row", scale_fmt)
+        res.append((o, s))
+    _check(_lib.loka_quantize_grouped(G, xa, qa, _ptr(status), _stream(stream)), "loka_quantize_grouped")
+    return res

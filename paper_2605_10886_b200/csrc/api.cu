@@ -168,6 +168,51 @@ loka_status loka_quantize(const loka_tensor* x, loka_tensor* q, loka_tensor* qt,
   return e == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
 }
 
+loka_status loka_quantize_grouped(int32_t G, const loka_tensor* x, loka_tensor* q, int32_t* status_dev,
+                                  loka_stream_t stream) {
+  if (G < 0 || G > kMaxQuantGroup || (G > 0 && (!x || !q))) return LOKA_ERR_INVALID_ARG;
+  if (G == 0) return LOKA_OK;
+  QuantGroup grp;
+  std::memset(&grp, 0, sizeof(grp));
+  grp.G = G;
+  int64_t max_cols = 0;
+  for (int g = 0; g < G; ++g) {
+    const loka_tensor &xg = x[g], &qg = q[g];
+    if (xg.dtype != x[0].dtype || qg.dtype != q[0].dtype || qg.scale_fmt != q[0].scale_fmt) return LOKA_ERR_INVALID_ARG;
+    if (xg.dtype != LOKA_BF16 && xg.dtype != LOKA_F32) return LOKA_ERR_INVALID_ARG;
+    if (!is_fp8(qg.dtype) || (qg.scale_fmt != LOKA_SCALE_F32 && qg.scale_fmt != LOKA_SCALE_UE8M0))
+      return LOKA_ERR_INVALID_ARG;
+    if (qg.gran != LOKA_GRAN_ROW) return LOKA_ERR_UNSUPPORTED;
+    if (xg.rows < 0 || xg.cols < 0 || qg.rows != xg.rows || qg.cols != xg.cols) return LOKA_ERR_SHAPE;
+    if (xg.rows && xg.cols) {
+      if (!xg.data || !aligned16(xg.data) || xg.ld < xg.cols || (xg.ld * elem_size(xg.dtype)) % 16)
+        return LOKA_ERR_INVALID_ARG;
+      if (!qg.scales || !qg.data || !aligned16(qg.data) || qg.ld < qg.cols || qg.ld % 16) return LOKA_ERR_INVALID_ARG;
+    }
+    QuantParams& p = grp.p[g];
+    p.x = xg.data;
+    p.rows = xg.cols ? xg.rows : 0;
+    p.cols = xg.cols;
+    p.ldx = xg.ld;
+    p.q = reinterpret_cast<uint8_t*>(qg.data);
+    p.ldq = qg.ld;
+    p.scales = qg.scales;
+    p.qt = nullptr;
+    p.ldqt = 0;
+    p.scales_t = nullptr;
+    p.status = status_dev;
+    grp.row_start[g + 1] = grp.row_start[g] + p.rows;
+    if (xg.cols > max_cols) max_cols = xg.cols;
+  }
+  if (grp.row_start[G] == 0) return LOKA_OK;
+  loka_status st = check_device();
+  if (st != LOKA_OK) return st;
+  cudaError_t e = launch_quantize_grouped(grp, x[0].dtype == LOKA_BF16, q[0].dtype, q[0].scale_fmt, max_cols,
+                                          reinterpret_cast<cudaStream_t>(stream));
+  if (e == cudaErrorNotSupported) return LOKA_ERR_UNSUPPORTED;
+  return e == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
+}
+
 // ------------------------------------------------------------------------------------------
 size_t loka_linear_workspace_size(const loka_linear_args* /*a*/) { return 0; }
 

@@ -25,6 +25,16 @@ struct QuantParams {
 cudaError_t launch_quantize(const QuantParams& p, bool in_bf16, int fmt, int scale_fmt, int gran, int phase,
                             float* amax_dev, cudaStream_t st, int num_sms);
 
+constexpr int kMaxQuantGroup = 64;
+struct QuantGroup {
+  int32_t G;
+  int64_t row_start[kMaxQuantGroup + 1];  // prefix sum of rows
+  QuantParams p[kMaxQuantGroup];
+};
+// ROW granularity, every tensor the same input dtype / FP8 format / scale format.
+cudaError_t launch_quantize_grouped(const QuantGroup& grp, bool in_bf16, int fmt, int scale_fmt, int64_t max_cols,
+                                    cudaStream_t st);
+
 struct LinearParams {
   int32_t M, N, K;
   int32_t a_fmt, b_fmt;          // 0 = e4m3, 1 = e5m2 (tcgen05 kind::f8f6f4 encoding)

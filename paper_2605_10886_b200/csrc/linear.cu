@@ -134,19 +134,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
   pdl_wait();  // inputs written by the previous kernel are visible from here on
   if (threadIdx.x == 0) LOKA_TRACE(1);
-  if (warp >= 2) {  // per-column epilogue parameters -> smem
-    for (int j = threadIdx.x - 64; j < BN; j += 32 * kEpiWarps) {
-      const int n = n0 + j;
-      const bool ok = n < p.N;
-      col[j] = ok ? p.sb[p.sb_row ? n : 0] : 0.f;
-      float b = 0.f;
-      if (ok && p.bias) b = p.bias_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.bias)[n])
-                                         : reinterpret_cast<const float*>(p.bias)[n];
-      col[BN + j] = b;
-      col[2 * BN + j] = (ok && p.gamma) ? p.gamma[n] : 1.f;
-      col[3 * BN + j] = (ok && p.beta) ? p.beta[n] : 0.f;
-    }
-  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -218,6 +205,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float ys = fold ? 1.f : sa;
     const int blk = is_block ? p.norm_block : BN;
     const uint32_t col_s = smem_u32(col);
+
+    // per-column epilogue parameters -> smem (while the producer / MMA warps run the mainloop)
+    for (int j = threadIdx.x - 64; j < BN; j += 32 * kEpiWarps) {
+      const int n = n0 + j;
+      const bool ok = n < p.N;
+      col[j] = ok ? p.sb[p.sb_row ? n : 0] : 0.f;
+      float b = 0.f;
+      if (ok && p.bias) b = p.bias_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.bias)[n])
+                                         : reinterpret_cast<const float*>(p.bias)[n];
+      col[BN + j] = b;
+      col[2 * BN + j] = (ok && p.gamma) ? p.gamma[n] : 1.f;
+      col[3 * BN + j] = (ok && p.beta) ? p.beta[n] : 0.f;
+    }
+    named_bar_sync(1, 32 * kEpiWarps);
 
     if (lane == 0) mbar_wait(tmem_full, 0, 3);  // one waiter per warp
     __syncwarp();

@@ -102,27 +102,30 @@ LOKA_DEVINL void flag_nonfinite(uint32_t amax_bits, int32_t* status) {
 
 // ----- ROW: one warp per row; rows of <= 256*NREG elements stay in registers -------------
 template <typename Tin, int FMT, int SF, int NREG>
-__global__ void __launch_bounds__(256) quant_row_kernel(QuantParams p) {
-  pdl_wait();
-  const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (row >= p.rows) return;
+LOKA_DEVINL void quant_row_body(const QuantParams& p, int64_t row, int lane) {
   const Tin* xr = reinterpret_cast<const Tin*>(p.x) + row * p.ldx;
   const int64_t cols = p.cols;
   const bool cached = cols <= 256 * NREG;
   Vec8<Tin> v[NREG];
   uint32_t am = 0;
-  for (int64_t c0 = 0, it = 0; c0 < cols; c0 += 256, ++it) {
-    const int64_t c = c0 + lane * 8;
-    Vec8<Tin> t;
-    if (c + 8 <= cols) t.load(xr + c);
-    else if (c < cols) t.load_partial(xr + c, (int)(cols - c));
-    else t.zero();
-    am = max(am, t.amax_bits());
-    if (cached) {
+  if (cached) {  // the whole row in registers: all loads in flight at once, one HBM read
 #pragma unroll
-      for (int i = 0; i < NREG; ++i)
-        if (i == it) v[i] = t;
+    for (int i = 0; i < NREG; ++i) {
+      const int64_t c = i * 256 + lane * 8;
+      if (c + 8 <= cols) v[i].load(xr + c);
+      else if (c < cols) v[i].load_partial(xr + c, (int)(cols - c));
+      else v[i].zero();
+    }
+#pragma unroll
+    for (int i = 0; i < NREG; ++i) am = max(am, v[i].amax_bits());
+  } else {
+    for (int64_t c0 = 0; c0 < cols; c0 += 256) {
+      const int64_t c = c0 + lane * 8;
+      Vec8<Tin> t;
+      if (c + 8 <= cols) t.load(xr + c);
+      else if (c < cols) t.load_partial(xr + c, (int)(cols - c));
+      else t.zero();
+      am = max(am, t.amax_bits());
     }
   }
   am = warp_max_u32(am);
@@ -134,27 +137,53 @@ __global__ void __launch_bounds__(256) quant_row_kernel(QuantParams p) {
     if (p.scales_t) p.scales_t[row] = s;
   }
   uint8_t* qr = p.q ? p.q + row * p.ldq : nullptr;
-  for (int64_t c0 = 0, it = 0; c0 < cols; c0 += 256, ++it) {
-    const int64_t c = c0 + lane * 8;
-    if (c >= cols) continue;
-    Vec8<Tin> t;
-    if (cached) {
-#pragma unroll
-      for (int i = 0; i < NREG; ++i)
-        if (i == it) t = v[i];
-    } else if (c + 8 <= cols) {
-      t.load(xr + c);
-    } else {
-      t.load_partial(xr + c, (int)(cols - c));
-    }
-    uint2 code = cast8<FMT>(t, r);
+  auto emit = [&](int64_t c, const Vec8<Tin>& t) {
+    const uint2 code = cast8<FMT>(t, r);
     const int n = (int)imin64(8, cols - c);
     if (qr) store8(qr + c, code, n);
     if (p.qt) {  // transposed copy: element (row, c+i) -> qt[(c+i) * ldqt + row]
       const uint8_t* b = reinterpret_cast<const uint8_t*>(&code);
       for (int i = 0; i < n; ++i) p.qt[(c + i) * p.ldqt + row] = b[i];
     }
+  };
+  if (cached) {
+#pragma unroll
+    for (int i = 0; i < NREG; ++i) {
+      const int64_t c = i * 256 + lane * 8;
+      if (c < cols) emit(c, v[i]);
+    }
+  } else {
+    for (int64_t c0 = 0; c0 < cols; c0 += 256) {
+      const int64_t c = c0 + lane * 8;
+      if (c >= cols) continue;
+      Vec8<Tin> t;
+      if (c + 8 <= cols) t.load(xr + c);
+      else t.load_partial(xr + c, (int)(cols - c));
+      emit(c, t);
+    }
   }
+}
+
+template <typename Tin, int FMT, int SF, int NREG>
+__global__ void __launch_bounds__(256) quant_row_kernel(QuantParams p) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= p.rows) return;
+  quant_row_body<Tin, FMT, SF, NREG>(p, row, lane);
+}
+
+// ----- grouped ROW quantize: many tensors (e.g. an activation + every layer's weight) in one
+// launch; warp w of the grid takes global row w, located in tensor g by a prefix sum of rows.
+template <typename Tin, int FMT, int SF, int NREG>
+__global__ void __launch_bounds__(256) quant_row_grouped_kernel(const __grid_constant__ QuantGroup grp) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t grow = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (grow >= grp.row_start[grp.G]) return;
+  int g = 0;
+  while (grow >= grp.row_start[g + 1]) ++g;
+  quant_row_body<Tin, FMT, SF, NREG>(grp.p[g], grow - grp.row_start[g], lane);
 }
 
 // ----- BLK_1x128: one warp per row, 16 lanes per 128-column block -------------------------
@@ -375,6 +404,38 @@ cudaError_t launch_quantize(const QuantParams& p, bool in_bf16, int fmt, int sca
     LOKA_Q(float, LOKA_E5M2, LOKA_SCALE_UE8M0)
   }
 #undef LOKA_Q
+  return cudaErrorNotSupported;
+}
+
+}  // namespace loka
+
+namespace loka {
+
+template <typename Tin, int FMT, int SF>
+static cudaError_t launch_grouped_t(const QuantGroup& grp, int64_t max_cols, cudaStream_t st) {
+  const int64_t rows = grp.row_start[grp.G];
+  const dim3 grd((unsigned)((rows + 7) / 8)), blk(256);
+  constexpr int kBig = sizeof(Tin) == 2 ? 16 : 8;
+  if (max_cols <= 256 * 4) return launch_pdl(quant_row_grouped_kernel<Tin, FMT, SF, 4>, grd, blk, st, grp);
+  return launch_pdl(quant_row_grouped_kernel<Tin, FMT, SF, kBig>, grd, blk, st, grp);
+}
+
+cudaError_t launch_quantize_grouped(const QuantGroup& grp, bool in_bf16, int fmt, int scale_fmt, int64_t max_cols,
+                                    cudaStream_t st) {
+#define LOKA_G(T, F, S) \
+  if (fmt == F && scale_fmt == S) return launch_grouped_t<T, F, S>(grp, max_cols, st);
+  if (in_bf16) {
+    LOKA_G(__nv_bfloat16, LOKA_E4M3, LOKA_SCALE_F32)
+    LOKA_G(__nv_bfloat16, LOKA_E4M3, LOKA_SCALE_UE8M0)
+    LOKA_G(__nv_bfloat16, LOKA_E5M2, LOKA_SCALE_F32)
+    LOKA_G(__nv_bfloat16, LOKA_E5M2, LOKA_SCALE_UE8M0)
+  } else {
+    LOKA_G(float, LOKA_E4M3, LOKA_SCALE_F32)
+    LOKA_G(float, LOKA_E4M3, LOKA_SCALE_UE8M0)
+    LOKA_G(float, LOKA_E5M2, LOKA_SCALE_F32)
+    LOKA_G(float, LOKA_E5M2, LOKA_SCALE_UE8M0)
+  }
+#undef LOKA_G
   return cudaErrorNotSupported;
 }
 

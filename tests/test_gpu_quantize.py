@@ -97,3 +97,16 @@ def test_full_size_sampled(rows, cols):
     oq, os_ = oracle.quantize.quantize(xs.double().numpy(), "e4m3", "row")
     assert_bytes_equal(q[idx.to(DEV)], oq)
     assert_scales_equal(s[idx.to(DEV)], os_)
+
+
+@pytest.mark.parametrize("fmt,scale_fmt", [("e4m3", "f32"), ("e5m2", "ue8m0")])
+def test_grouped_rowwise_matches_oracle(fmt, scale_fmt):
+    """loka_quantize_grouped: X + the 8 cfg2 weights (+ ragged shapes) in one launch, bit-exact."""
+    xs = [synth.heavy(300, 1024, 1)] + [synth.weight(synth.CFG2_DIMS[l + 1], synth.CFG2_DIMS[l], 100 + l)
+                                        for l in range(8)] + [synth.gaussian(5, 3000, 2), synth.gaussian(1, 40, 3)]
+    outs = lk.loka_quantize_grouped([to_dev_padded(x) for x in xs], fmt, scale_fmt)
+    torch.cuda.synchronize()
+    for x, (q, s) in zip(xs, outs):
+        oq, os_ = oracle.quantize.quantize(x.double().numpy(), fmt, "row", scale_fmt)
+        assert_scales_equal(s, os_)
+        assert_bytes_equal(q, oq)
