@@ -243,30 +243,28 @@ static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CU
   // 148 SMs) for this M, else the narrowest allowed.  Row-coupled epilogues (full-row norm or an
   // FP8 output with row scales) put the ceil(N/BN) CTAs of a row block in one cluster (<= 8).
   const bool full_row = a->norm == LOKA_NORM_LAYER || a->norm == LOKA_NORM_RMS || fp8_out;
+  const bool block = a->norm == LOKA_NORM_BLOCK_RMS;
+  const int blk = a->norm_block;
+  if (block && (blk <= 0 || N % blk)) return LOKA_ERR_SHAPE;  // IndivisibleFeatureDim
+  // a BlockNorm block must tile the CTA (BN % blk == 0) and cover whole epilogue quarters
+  // (blk % (BN/4) == 0, each thread's BN/4 columns lie in one block)
+  auto legal = [&](int c) {
+    if (full_row && cdiv(N, c) > 8) return false;
+    if (block && (c % blk || blk % (c / 4))) return false;
+    return true;
+  };
   const int64_t mb = cdiv(M, 128);
   int bn = 0, csize = 1;
   const int cands[3] = {256, 128, 64};
   for (int i = 0; i < 3 && !bn; ++i) {
     const int c = cands[i];
-    if (full_row && cdiv(N, c) > 8) continue;
-    if (a->norm == LOKA_NORM_BLOCK_RMS && (c % a->norm_block)) continue;
+    if (!legal(c)) continue;
     if (c > 64 && c / 2 >= N) continue;  // a narrower tile covers N as well
     if (mb * cdiv(N, c) >= 120 || c == 64) bn = c;
   }
-  if (!bn) {  // fall back to the narrowest legal tile
-    for (int i = 2; i >= 0 && !bn; --i) {
-      const int c = cands[i];
-      if (full_row && cdiv(N, c) > 8) continue;
-      if (a->norm == LOKA_NORM_BLOCK_RMS && (c % a->norm_block)) continue;
-      bn = c;
-    }
-  }
-  if (a->norm == LOKA_NORM_BLOCK_RMS) {
-    const int blk = a->norm_block;
-    if (blk <= 0 || N % blk) return LOKA_ERR_SHAPE;  // IndivisibleFeatureDim
-    if (blk % 32 || !bn) return LOKA_ERR_UNSUPPORTED;
-  }
-  if (!bn) return LOKA_ERR_UNSUPPORTED;  // row wider than one portable cluster (N > 2048)
+  for (int i = 2; i >= 0 && !bn; --i)  // fall back to the narrowest legal tile
+    if (legal(cands[i])) bn = cands[i];
+  if (!bn) return LOKA_ERR_UNSUPPORTED;  // row wider than one portable cluster (N > 2048) or odd block
   if (full_row) csize = (int)cdiv(N, bn);
   if (!make_map_u8(ta, A.data, M, K, A.ld, 128)) return LOKA_ERR_CUDA;
   if (!make_map_u8(tb, B.data, N, K, B.ld, (uint32_t)bn)) return LOKA_ERR_CUDA;

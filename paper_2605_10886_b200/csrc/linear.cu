@@ -9,17 +9,19 @@
 // B200 design:
 //   * CTA tile 128 x BN (BN in {64,128,256}), K staged 128 FP8 (= one 128B swizzle atom) per
 //     pipeline stage; warp 0 = TMA producer, warp 1 = tcgen05.mma issuer (one elected lane),
-//     warps 2-9 = epilogue: warp w reads TMEM lanes 32*(w%4)..+31 (one row per thread) and the
-//     column half (w-2)/4 of the tile.
+//     warps 2-17 = epilogue: warp w reads TMEM lanes 32*(w%4)..+31 (one row per thread) and the
+//     column quarter (w-2)/4 of the tile, i.e. BN/4 columns held entirely in registers: ONE
+//     batch of TMEM loads and one wait, statistics, exchange and output all from registers.
 //   * The 128 x BN FP32 accumulator lives in TMEM; it never goes to HBM (a5).
 //   * Epilogue arithmetic is packed FP32x2 (FMUL2/FFMA2/FADD2) with 3-input min/max; for norms
 //     without bias the per-row dequant scale s_a is folded into eps
 //     ((s z - s mu)/sqrt(s^2 var + eps) == (z - mu)/sqrt(var + eps/s^2)), and the normalised
 //     value is one FFMA: v = fma(y, rstd, -mu*rstd).
-//   * Case 2 (row wider than one CTA) is a thread-block cluster along N (<= 8 CTAs): per-row
-//     partial statistics (Chan's (n, mean, M2), sum of squares, y max/min) are exchanged through
-//     distributed shared memory and merged in cluster-rank order, so every CTA derives
-//     bit-identical row statistics.
+//   * The four column quarters of a row merge their statistics through shared memory (aliased on
+//     the drained operand ring); Case 2 (row wider than one CTA) is a thread-block cluster along
+//     N (<= 8 CTAs): every CTA pushes its per-row record (Chan (mean, M2) | sum of squares, y max,
+//     y min) into each peer with one st.shared::cluster.v4, and all CTAs merge the records in
+//     cluster-rank order, so every CTA derives bit-identical row statistics.
 //   * Programmatic dependent launch: the prologue (barrier init, TMEM alloc, descriptor
 //     prefetch) overlaps the previous kernel's tail; global inputs are read after
 //     griddepcontrol.wait.
@@ -28,31 +30,32 @@
 
 namespace loka {
 
-// Opt-in phase trace (loka_debug_trace): per CTA, 8 globaltimer stamps
+// Opt-in phase trace (loka_debug_trace): per CTA, 16 globaltimer stamps
 //   0 entry | 1 after griddepcontrol.wait | 2 first TMA issued | 3 first stage landed (MMA)
 //   4 last MMA committed | 5 accumulator ready (epilogue) | 6 statistics done | 7 stores done
+//   8 accumulator in registers | 9 quarters merged | 10 cluster merged | 11 finalized
 constexpr int kTraceCtas = 4096;
 static __device__ unsigned long long g_trace[kTraceCtas * 16];
 static __device__ int g_trace_on;
-#define LOKA_TRACE(slot)                                                                   \
-  do {                                                                                     \
+#define LOKA_TRACE(slot)                                                                    \
+  do {                                                                                      \
     if (trace_on && cta_lin < kTraceCtas) g_trace[cta_lin * 16 + (slot)] = globaltimer_ns(); \
   } while (0)
 
-constexpr int kEpiWarps = 8;
-constexpr int kThreads = 64 + 32 * kEpiWarps;  // 10 warps
-constexpr int kBK = 128;                       // FP8 elements of K per stage (128 B rows, SW128 atom)
-constexpr int kRec = 16;                       // floats per row record in the half exchange
-
+constexpr int kEpiWarps = 16;               // every warp runs the epilogue ...
+constexpr int kEpiThreads = 32 * kEpiWarps;
+constexpr int kThreads = kEpiThreads;       // ... after warp 0 lane 0 (TMA) / warp 1 lane 0 (MMA) roles
+constexpr int kBK = 128;                    // FP8 elements of K per stage (128 B rows, SW128 atom)
+constexpr int kRec = 6;                     // floats per (row, quarter) record: n, mean, m2, ss, ymax, ymin
 constexpr int kMaxCluster = 8;
 
 template <int BN> struct LinCfg {
+  static constexpr int kCPT = BN / 4;  // columns per epilogue thread
   static constexpr int kStageA = 128 * kBK;  // bytes
   static constexpr int kStageB = BN * kBK;
   static constexpr int kStageBytes = kStageA + kStageB;
-  // everything but the operand ring: column params, half exchange, pushed cluster records
-  static constexpr int kFixed = 4 * BN * 4 + 2 * 128 * kRec * 4 + kMaxCluster * 128 * 16 + kMaxCluster * 128 * 4 +
-                                512 + 1024;
+  // everything but the operand ring: column params, pushed cluster records (+ amax), barriers
+  static constexpr int kFixed = 4 * BN * 4 + kMaxCluster * 128 * 16 + kMaxCluster * 128 * 4 + 512 + 1024;
   static constexpr int kStagesFit = (227 * 1024 - kFixed) / kStageBytes;
   static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
   static constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
@@ -60,10 +63,11 @@ template <int BN> struct LinCfg {
   static constexpr int kOffBar = kOffB + kStages * kStageB;
   static constexpr int kOffTmem = kOffBar + (2 * kStages + 1) * 8;
   static constexpr int kOffCol = (kOffTmem + 4 + 15) & ~15;         // sb, bias, gamma, beta [BN]
-  static constexpr int kOffHx = kOffCol + 4 * BN * 4;                // [2][128][kRec]
-  static constexpr int kOffCs = kOffHx + 2 * 128 * kRec * 4;         // [kMaxCluster][128] float4 records
+  static constexpr int kOffCs = kOffCol + 4 * BN * 4;                // [kMaxCluster][128] float4 records
   static constexpr int kOffCs2 = kOffCs + kMaxCluster * 128 * 16;    // [kMaxCluster][128] amax
   static constexpr int kSmemBytes = kOffCs2 + kMaxCluster * 128 * 4 + 1024;  // + alignment slack
+  // the quarter exchange [4][kRec + 1][128] floats aliases the (drained) operand ring
+  static_assert(4 * (kRec + 1) * 128 * 4 <= kStages * kStageBytes, "hx alias");
   static_assert(kStages >= 2 && kSmemBytes <= 227 * 1024, "smem");
 };
 
@@ -79,8 +83,6 @@ LOKA_DEVINL void chan_merge(float& n, float& mean, float& m2, float nb, float me
   n = nt;
 }
 
-// Per-row record merged across the two column halves and across the cluster (non-BlockNorm):
-//   {n, mean, m2, ss, ymax, ymin}; BlockNorm: {ss_b[8], maxabs_b[8]} (blocks never span CTAs).
 struct RowRec {
   float n, mean, m2, ss, ymax, ymin;
   LOKA_DEVINL void init() { n = 0.f; mean = 0.f; m2 = 0.f; ss = 0.f; ymax = -INFINITY; ymin = INFINITY; }
@@ -97,6 +99,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     linear_norm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                        const LinearParams p) {
   using C = LinCfg<BN>;
+  constexpr int CPT = C::kCPT;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -106,7 +109,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tmem_full = empty_bar + C::kStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffTmem);
   float* col = reinterpret_cast<float*>(smem + C::kOffCol);  // [4][BN]: sb, bias, gamma, beta
-  float* hx = reinterpret_cast<float*>(smem + C::kOffHx);
+  float* hx = reinterpret_cast<float*>(smem);                // [4][kRec+1][128], valid after tmem_full
   float* cs = reinterpret_cast<float*>(smem + C::kOffCs);
   float* cs2 = reinterpret_cast<float*>(smem + C::kOffCs2);
 
@@ -146,7 +149,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   // cluster-wide barriers: every thread of the CTA executes the same count (uniform)
   const bool xchg_stats = csize > 1 && !is_block && (norm != LOKA_NORM_NONE || (is_fp8_out && !affine));
   const bool xchg_amax = csize > 1 && is_fp8_out && (is_block || affine);
-  const int n_cluster_bars = csize > 1 ? (int)xchg_stats + (int)xchg_amax + 1 : 0;
 
   if (warp == 0) {
     // ===== TMA producer =====
@@ -162,7 +164,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     __syncwarp();
-    for (int i = 0; i < n_cluster_bars; ++i) cluster_sync_all();
   } else if (warp == 1) {
     // ===== MMA issuer =====
     if (lane == 0) {
@@ -186,18 +187,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       LOKA_TRACE(4);
     }
     __syncwarp();
-    for (int i = 0; i < n_cluster_bars; ++i) cluster_sync_all();
-  } else {
-    // ===== epilogue: thread = one row x one column half of the 128 x BN tile =====
+  }
+  {
+    // ===== epilogue (all 16 warps): thread = one row x one column quarter (CPT cols, registers) =====
     const int q = warp & 3;              // TMEM lane quadrant this warp may access
-    const int h = (warp - 2) >> 2;       // column half
+    const int cq = warp >> 2;            // column quarter
     const int r = q * 32 + lane;
     const int grow = m0 + r;
     const bool row_ok = grow < p.M;
-    constexpr int kHalf = BN / 2;
-    const int cb = h * kHalf;                          // first local column of this thread
-    const int nloc = max(0, min(kHalf, ncols - cb));   // valid columns of this thread
-    const int nchunks = (nloc + 31) / 32;
+    const int cb = cq * CPT;                         // first local column of this thread
+    const int nv = max(0, min(CPT, ncols - cb));     // valid columns of this thread
     const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)cb;
     const float sa = row_ok ? p.sa[p.sa_row ? grow : 0] : 0.f;
     const bool has_bias = p.bias != nullptr;
@@ -207,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t col_s = smem_u32(col);
 
     // per-column epilogue parameters -> smem (while the producer / MMA warps run the mainloop)
-    for (int j = threadIdx.x - 64; j < BN; j += 32 * kEpiWarps) {
+    for (int j = threadIdx.x; j < BN; j += kEpiThreads) {
       const int n = n0 + j;
       const bool ok = n < p.N;
       col[j] = ok ? p.sb[p.sb_row ? n : 0] : 0.f;
@@ -218,151 +217,134 @@ __global__ void __launch_bounds__(kThreads, 1)
       col[2 * BN + j] = (ok && p.gamma) ? p.gamma[n] : 1.f;
       col[3 * BN + j] = (ok && p.beta) ? p.beta[n] : 0.f;
     }
-    named_bar_sync(1, 32 * kEpiWarps);
+    named_bar_sync(1, kEpiThreads);
 
     if (lane == 0) mbar_wait(tmem_full, 0, 3);  // one waiter per warp
     __syncwarp();
     tc_fence_after();
     pdl_launch_dependents();
-    if (warp == 2 && lane == 0) LOKA_TRACE(5);
+    if (threadIdx.x == 64) LOKA_TRACE(5);
 
-    // y_j for the 32 columns of chunk c (local to this thread's half)
-    auto load_y = [&](int c, float (&v)[32]) {
-      tmem_ld32(taddr + (uint32_t)(c * 32), v);
-      const uint32_t o = (uint32_t)(cb + c * 32) * 4u;
+    // ---- accumulator -> registers: all loads in flight, one wait ----
+    float y[CPT];
+    if constexpr (CPT >= 32) {
 #pragma unroll
-      for (int j = 0; j < 32; j += 4) {
-        float4 s4 = lds_f4(col_s + o + j * 4);
-        float2 s01 = make_float2(s4.x, s4.y), s23 = make_float2(s4.z, s4.w);
-        if (!fold) {
-          s01 = fmul2(s01, make_float2(ys, ys));
-          s23 = fmul2(s23, make_float2(ys, ys));
-        }
-        float2 a01 = make_float2(v[j], v[j + 1]), a23 = make_float2(v[j + 2], v[j + 3]);
-        if (has_bias) {
-          const float4 b4 = lds_f4(col_s + (uint32_t)BN * 4u + o + j * 4);
-          a01 = ffma2(a01, s01, make_float2(b4.x, b4.y));
-          a23 = ffma2(a23, s23, make_float2(b4.z, b4.w));
-        } else {
-          a01 = fmul2(a01, s01);
-          a23 = fmul2(a23, s23);
-        }
-        v[j] = a01.x; v[j + 1] = a01.y; v[j + 2] = a23.x; v[j + 3] = a23.y;
+      for (int i = 0; i < CPT / 32; ++i) tmem_ld32_nowait(taddr + (uint32_t)(32 * i), y + 32 * i);
+#pragma unroll
+      for (int i = 0; i < CPT / 16; ++i) tmem_wait16(y + 16 * i);
+    } else {
+      tmem_ld16_nowait(taddr, y);
+      tmem_wait16(y);
+    }
+    // y_j = acc_j * s_a * s_b[n] (+ bias[n]); with fold: acc_j * s_b[n]
+#pragma unroll
+    for (int j = 0; j < CPT; j += 4) {
+      const uint32_t o = (uint32_t)(cb + j) * 4u;
+      const float4 s4 = lds_f4(col_s + o);
+      float2 s01 = make_float2(s4.x, s4.y), s23 = make_float2(s4.z, s4.w);
+      if (!fold) {
+        s01 = fmul2(s01, make_float2(ys, ys));
+        s23 = fmul2(s23, make_float2(ys, ys));
       }
-    };
+      float2 a01 = make_float2(y[j], y[j + 1]), a23 = make_float2(y[j + 2], y[j + 3]);
+      if (has_bias) {
+        const float4 b4 = lds_f4(col_s + (uint32_t)BN * 4u + o);
+        a01 = ffma2(a01, s01, make_float2(b4.x, b4.y));
+        a23 = ffma2(a23, s23, make_float2(b4.z, b4.w));
+      } else {
+        a01 = fmul2(a01, s01);
+        a23 = fmul2(a23, s23);
+      }
+      y[j] = a01.x; y[j + 1] = a01.y; y[j + 2] = a23.x; y[j + 3] = a23.y;
+    }
+    if (threadIdx.x == 64) LOKA_TRACE(8);
 
-    // ---- pass 1: statistics over this thread's columns ----
+    // ---- per-thread statistics over its nv valid columns ----
     RowRec rec;
     rec.init();
-    float bss[8], bmax[8];  // BlockNorm: per block sum of squares and max |y|
-#pragma unroll
-    for (int b = 0; b < 8; ++b) bss[b] = 0.f, bmax[b] = 0.f;
     const bool need_minmax = is_fp8_out && !affine;
-    const bool need_pass1 = norm != LOKA_NORM_NONE || need_minmax;
-    if (need_pass1) {
-      for (int c = 0; c < nchunks; ++c) {
-        float v[32];
-        load_y(c, v);
-        const int nv = min(32, nloc - c * 32);
-        if (nv < 32) {  // ragged last chunk: replicate a valid value into the masked lanes so that
-                        // max/min are unaffected, and zero them for the sums
+    const bool need_stats = norm != LOKA_NORM_NONE || need_minmax;
+    if (need_stats && nv > 0) {
+      // Columns >= N of a ragged tile hold exact zeros (zero-filled B rows, s_b = bias = 0), so
+      // sums need no mask; only max/min must skip them.
+      const float* t = y;
+      float cmax = y[0], cmin = y[0];
+      if (nv == CPT) {
 #pragma unroll
-          for (int j = 1; j < 32; ++j)
-            if (j >= nv) v[j] = v[0];
-        }
-        float cmax = v[0], cmin = v[0];
-#pragma unroll
-        for (int j = 0; j < 32; j += 2) cmax = fmax3(cmax, v[j], v[j + 1]), cmin = fmin3(cmin, v[j], v[j + 1]);
-        if (nv < 32) {
-#pragma unroll
-          for (int j = 1; j < 32; ++j)
-            if (j >= nv) v[j] = 0.f;
-        }
-        if (norm == LOKA_NORM_LAYER) {
-          float2 s0 = make_float2(0.f, 0.f), s1 = s0, s2 = s0, s3 = s0;
-#pragma unroll
-          for (int j = 0; j < 32; j += 8) {
-            s0 = fadd2(s0, make_float2(v[j], v[j + 1]));
-            s1 = fadd2(s1, make_float2(v[j + 2], v[j + 3]));
-            s2 = fadd2(s2, make_float2(v[j + 4], v[j + 5]));
-            s3 = fadd2(s3, make_float2(v[j + 6], v[j + 7]));
-          }
-          s0 = fadd2(fadd2(s0, s1), fadd2(s2, s3));
-          const float mc = (s0.x + s0.y) / (float)nv;
-          const float2 nm = make_float2(-mc, -mc);
-          float2 q0 = make_float2(0.f, 0.f), q1 = q0;
-#pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            const float2 d0 = fadd2(make_float2(v[j], v[j + 1]), nm);
-            const float2 d1 = fadd2(make_float2(v[j + 2], v[j + 3]), nm);
-            q0 = ffma2(d0, d0, q0);
-            q1 = ffma2(d1, d1, q1);
-          }
-          q0 = fadd2(q0, q1);
-          // masked lanes contributed (0 - mc)^2 each: remove them exactly as counted
-          float m2 = q0.x + q0.y;
-          if (nv < 32) m2 = fmaxf(0.f, m2 - (float)(32 - nv) * mc * mc);
-          chan_merge(rec.n, rec.mean, rec.m2, (float)nv, mc, m2);
-        } else if (norm == LOKA_NORM_RMS || is_block) {
-          float2 q0 = make_float2(0.f, 0.f), q1 = q0;
-#pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            const float2 a = make_float2(v[j], v[j + 1]), b = make_float2(v[j + 2], v[j + 3]);
-            q0 = ffma2(a, a, q0);
-            q1 = ffma2(b, b, q1);
-          }
-          q0 = fadd2(q0, q1);
-          const float ss = q0.x + q0.y;
-          if (is_block) {
-            const int b = (cb + c * 32) / blk;
-            const float ma = fmaxf(cmax, -cmin);
-#pragma unroll
-            for (int bb = 0; bb < 8; ++bb)
-              if (bb == b) bss[bb] += ss, bmax[bb] = fmaxf(bmax[bb], ma);
-          } else {
-            rec.ss += ss;
-            rec.n += (float)nv;
-          }
-        } else {
-          rec.n += (float)nv;
-        }
-        rec.ymax = fmaxf(rec.ymax, cmax);
-        rec.ymin = fminf(rec.ymin, cmin);
-      }
-      if (warp == 2 && lane == 0) LOKA_TRACE(8);
-      // ---- combine the two column halves (fixed order h0, h1 -> identical in both) ----
-      // component-major [half][component][row]: consecutive lanes hit consecutive banks
-      float* my = hx + (size_t)h * kRec * 128 + r;
-      if (is_block) {
-#pragma unroll
-        for (int b = 0; b < 8; ++b) my[b * 128] = bss[b], my[(8 + b) * 128] = bmax[b];
+        for (int j = 0; j < CPT; j += 2) cmax = fmax3(cmax, y[j], y[j + 1]), cmin = fmin3(cmin, y[j], y[j + 1]);
       } else {
-        my[0] = rec.n; my[128] = rec.mean; my[256] = rec.m2; my[384] = rec.ss; my[512] = rec.ymax;
-        my[640] = rec.ymin;
-      }
-      named_bar_sync(1, 32 * kEpiWarps);
-      const float* r0 = hx + r;
-      const float* r1 = hx + (size_t)kRec * 128 + r;
-      if (is_block) {
 #pragma unroll
-        for (int b = 0; b < 8; ++b)
-          bss[b] = r0[b * 128] + r1[b * 128], bmax[b] = fmaxf(r0[(8 + b) * 128], r1[(8 + b) * 128]);
-      } else {
-        rec.n = r0[0]; rec.mean = r0[128]; rec.m2 = r0[256]; rec.ss = r0[384]; rec.ymax = r0[512]; rec.ymin = r0[640];
-        RowRec o;
-        o.n = r1[0]; o.mean = r1[128]; o.m2 = r1[256]; o.ss = r1[384]; o.ymax = r1[512]; o.ymin = r1[640];
-        rec.merge(o);
+        for (int j = 0; j < CPT; ++j)
+          if (j < nv) cmax = fmaxf(cmax, y[j]), cmin = fminf(cmin, y[j]);
+      }
+      rec.n = (float)nv;
+      rec.ymax = cmax;
+      rec.ymin = cmin;
+      if (norm == LOKA_NORM_LAYER) {
+        float2 s0 = make_float2(0.f, 0.f), s1 = s0, s2 = s0, s3 = s0;
+#pragma unroll
+        for (int j = 0; j < CPT; j += 8) {
+          s0 = fadd2(s0, make_float2(t[j], t[j + 1]));
+          s1 = fadd2(s1, make_float2(t[j + 2], t[j + 3]));
+          s2 = fadd2(s2, make_float2(t[j + 4], t[j + 5]));
+          s3 = fadd2(s3, make_float2(t[j + 6], t[j + 7]));
+        }
+        s0 = fadd2(fadd2(s0, s1), fadd2(s2, s3));
+        const float mc = (s0.x + s0.y) / (float)nv;
+        const float2 nm = make_float2(-mc, -mc);
+        float2 q0 = make_float2(0.f, 0.f), q1 = q0;
+#pragma unroll
+        for (int j = 0; j < CPT; j += 4) {
+          const float2 d0 = fadd2(make_float2(t[j], t[j + 1]), nm);
+          const float2 d1 = fadd2(make_float2(t[j + 2], t[j + 3]), nm);
+          q0 = ffma2(d0, d0, q0);
+          q1 = ffma2(d1, d1, q1);
+        }
+        q0 = fadd2(q0, q1);
+        float m2 = q0.x + q0.y;
+        if (nv < CPT) m2 = fmaxf(0.f, m2 - (float)(CPT - nv) * mc * mc);  // masked lanes added mc^2 each
+        rec.mean = mc;
+        rec.m2 = m2;
+      } else if (norm == LOKA_NORM_RMS || is_block) {
+        float2 q0 = make_float2(0.f, 0.f), q1 = q0;
+#pragma unroll
+        for (int j = 0; j < CPT; j += 4) {
+          const float2 a = make_float2(t[j], t[j + 1]), b = make_float2(t[j + 2], t[j + 3]);
+          q0 = ffma2(a, a, q0);
+          q1 = ffma2(b, b, q1);
+        }
+        q0 = fadd2(q0, q1);
+        rec.ss = q0.x + q0.y;
       }
     }
-    if (warp == 2 && lane == 0) LOKA_TRACE(9);
 
-    // ---- cross-CTA statistics (Case 2) ----
-    // Push: the h == 0 thread of row r stores this CTA's record (mean|ss, m2, ymax, ymin) into
-    // slot [my rank][r] of every cluster peer (one st.shared::cluster.v4 per peer); after the
-    // cluster barrier every thread merges slots 0..C-1 from local smem in rank order.
+    // ---- merge the four column quarters of each row (fixed order -> identical in all four) ----
+    // BlockNorm blocks cover whole quarters (blk % CPT == 0): a thread keeps its own block's sum
+    // and the per-quarter (ss, max|y|) needed for the row amax.
+    float q_ss[4], q_ma[4];
+    if (need_stats) {
+      float* my = hx + (size_t)cq * (kRec + 1) * 128 + r;  // component-major: conflict-free
+      my[0] = rec.n; my[128] = rec.mean; my[256] = rec.m2; my[384] = rec.ss; my[512] = rec.ymax; my[640] = rec.ymin;
+      named_bar_sync(1, kEpiThreads);
+      RowRec all;
+      all.init();
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float* o = hx + (size_t)k * (kRec + 1) * 128 + r;
+        RowRec t;
+        t.n = o[0]; t.mean = o[128]; t.m2 = o[256]; t.ss = o[384]; t.ymax = o[512]; t.ymin = o[640];
+        q_ss[k] = t.ss;
+        q_ma[k] = t.n > 0.f ? fmaxf(t.ymax, -t.ymin) : 0.f;
+        all.merge(t);
+      }
+      rec = all;
+    }
+    if (threadIdx.x == 64) LOKA_TRACE(9);
+
+    // ---- cross-CTA statistics (Case 2): push records, cluster barrier, merge in rank order ----
     if (xchg_stats) {
       const uint32_t my_rank = cluster_ctarank();
-      if (h == 0) {
+      if (cq == 0) {
         const float4 v = make_float4(norm == LOKA_NORM_LAYER ? rec.mean : rec.ss, rec.m2, rec.ymax, rec.ymin);
         const uint32_t la = smem_u32(cs + ((size_t)my_rank * 128 + r) * 4);
         for (int rk = 0; rk < csize; ++rk) st_dsmem_f4(mapa_shared(la, (uint32_t)rk), v);
@@ -381,9 +363,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         rec.merge(o);
       }
     }
+    if (threadIdx.x == 64) LOKA_TRACE(10);
 
-    if (warp == 2 && lane == 0) LOKA_TRACE(10);
-    // ---- finalize: v = fma(y, rstd, c0) per column (BlockNorm: per block) ----
+    // ---- finalize: v = fma(y, rstd, c0) (BlockNorm: rstd of the thread's block) ----
     const float eps_eff = fold ? __fdiv_rn(p.eps, __fmul_rn(sa, sa)) : p.eps;
     float rstd = 1.f, c0 = 0.f;
     if (norm == LOKA_NORM_LAYER) {
@@ -392,71 +374,68 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (norm == LOKA_NORM_RMS) {
       rstd = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(rec.ss, rec.n), eps_eff)));
     }
-    float brs[8];
+    float q_rs[4] = {1.f, 1.f, 1.f, 1.f};  // BlockNorm: rstd of each quarter's block
+    if (is_block) {
+      const int qpb = blk / CPT;  // quarters per block
 #pragma unroll
-    for (int b = 0; b < 8; ++b)
-      brs[b] = is_block ? __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(bss[b], (float)blk), eps_eff))) : 1.f;
-
-    // out = norm(y) (identical in every pass)
-    auto norm_out = [&](int c, float (&v)[32]) {
-      if (norm == LOKA_NORM_NONE) return;
-      float rs = rstd;
-      if (is_block) {
-        const int b = (cb + c * 32) / blk;
+      for (int k = 0; k < 4; ++k) {
+        const int kb0 = (k / qpb) * qpb;
+        float ss = 0.f;
 #pragma unroll
-        for (int bb = 0; bb < 8; ++bb)
-          if (bb == b) rs = brs[bb];
+        for (int k2 = 0; k2 < 4; ++k2)
+          if (k2 >= kb0 && k2 < kb0 + qpb) ss += q_ss[k2];
+        q_rs[k] = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, (float)blk), eps_eff)));
       }
-      const float2 r2 = make_float2(rs, rs), c2 = make_float2(c0, c0);
-      const uint32_t o = (uint32_t)(cb + c * 32) * 4u;
 #pragma unroll
-      for (int j = 0; j < 32; j += 4) {
-        float2 a = ffma2(make_float2(v[j], v[j + 1]), r2, c2);
-        float2 b = ffma2(make_float2(v[j + 2], v[j + 3]), r2, c2);
+      for (int k = 0; k < 4; ++k)
+        if (k == cq) rstd = q_rs[k];
+    }
+    if (threadIdx.x == 64) LOKA_TRACE(11);
+
+    // normalised values in place (registers)
+    if (norm != LOKA_NORM_NONE) {
+      const float2 r2 = make_float2(rstd, rstd), c2 = make_float2(c0, c0);
+#pragma unroll
+      for (int j = 0; j < CPT; j += 4) {
+        float2 a = ffma2(make_float2(y[j], y[j + 1]), r2, c2);
+        float2 b = ffma2(make_float2(y[j + 2], y[j + 3]), r2, c2);
         if (affine) {
-          const float4 g4 = lds_f4(col_s + 2u * BN * 4u + o + j * 4);
-          const float4 e4 = lds_f4(col_s + 3u * BN * 4u + o + j * 4);
+          const uint32_t o = (uint32_t)(cb + j) * 4u;
+          const float4 g4 = lds_f4(col_s + 2u * BN * 4u + o);
+          const float4 e4 = lds_f4(col_s + 3u * BN * 4u + o);
           a = ffma2(a, make_float2(g4.x, g4.y), make_float2(e4.x, e4.y));
           b = ffma2(b, make_float2(g4.z, g4.w), make_float2(e4.z, e4.w));
         }
-        v[j] = a.x; v[j + 1] = a.y; v[j + 2] = b.x; v[j + 3] = b.y;
+        y[j] = a.x; y[j + 1] = a.y; y[j + 2] = b.x; y[j + 3] = b.y;
       }
-    };
+    }
 
-    if (warp == 2 && lane == 0) LOKA_TRACE(11);
     // ---- FP8 output: row amax of the normalised values -> row scale ----
     float r_out = 1.f;
     if (is_fp8_out) {
       float amax = 0.f;
       if (!affine) {  // v is monotone in y: max |v| is attained at ymax or ymin, exactly
         if (is_block) {
-          const int nb_cta = (ncols + blk - 1) / blk;
 #pragma unroll
-          for (int b = 0; b < 8; ++b)
-            if (b < nb_cta) amax = fmaxf(amax, __fmul_rn(bmax[b], brs[b]));
+          for (int k = 0; k < 4; ++k) amax = fmaxf(amax, __fmul_rn(q_ma[k], q_rs[k]));
         } else if (norm == LOKA_NORM_NONE) {
           amax = fmaxf(fabsf(rec.ymax), fabsf(rec.ymin));
         } else {
           amax = fmaxf(fabsf(fmaf(rec.ymax, rstd, c0)), fabsf(fmaf(rec.ymin, rstd, c0)));
         }
-      } else {  // affine: one more pass over TMEM, then combine halves
-        for (int c = 0; c < nchunks; ++c) {
-          float v[32];
-          load_y(c, v);
-          norm_out(c, v);
-          const int nv = min(32, nloc - c * 32);
+      } else {  // affine: max over this thread's values, then over the four quarters
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < nv) amax = fmaxf(amax, fabsf(v[j]));
-        }
-        named_bar_sync(1, 32 * kEpiWarps);  // everyone finished reading hx from pass 1
-        hx[((size_t)h * kRec + 15) * 128 + r] = amax;
-        named_bar_sync(1, 32 * kEpiWarps);
-        amax = fmaxf(hx[(size_t)15 * 128 + r], hx[((size_t)kRec + 15) * 128 + r]);
+        for (int j = 0; j < CPT; ++j)
+          if (j < nv) amax = fmaxf(amax, fabsf(y[j]));
+        hx[((size_t)cq * (kRec + 1) + kRec) * 128 + r] = amax;  // slot kRec: not read by the stats merge
+        named_bar_sync(1, kEpiThreads);
+        amax = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) amax = fmaxf(amax, hx[((size_t)k * (kRec + 1) + kRec) * 128 + r]);
       }
       if (xchg_amax) {  // push this CTA's row amax into slot [my rank] of every peer
         const uint32_t my_rank = cluster_ctarank();
-        if (h == 0) {
+        if (cq == 0) {
           const uint32_t la = smem_u32(&cs2[my_rank * 128 + r]);
           for (int rk = 0; rk < csize; ++rk) st_dsmem_f32(mapa_shared(la, (uint32_t)rk), amax);
         }
@@ -468,76 +447,72 @@ __global__ void __launch_bounds__(kThreads, 1)
       float s_out;
       if (p.out_dtype == LOKA_E4M3) scales_from_amax<LOKA_E4M3, LOKA_SCALE_F32>(amax, s_out, r_out);
       else scales_from_amax<LOKA_E5M2, LOKA_SCALE_F32>(amax, s_out, r_out);
-      if (row_ok && blockIdx.y == 0 && h == 0 && p.y_scales) p.y_scales[grow] = s_out;
+      if (row_ok && blockIdx.y == 0 && cq == 0 && p.y_scales) p.y_scales[grow] = s_out;
     }
+    if (threadIdx.x == 64) LOKA_TRACE(6);
 
-    // ---- pass 2: normalise, cast, store (every lane runs the .sync.aligned TMEM loads) ----
-    if (warp == 2 && lane == 0) LOKA_TRACE(6);
-    for (int c = 0; c < nchunks; ++c) {
-      float v[32];
-      load_y(c, v);
-      norm_out(c, v);
-      if (!row_ok) continue;
-      const int lc = cb + c * 32;  // local column
-      const int nv = min(32, nloc - c * 32);
-      const int64_t gcol = (int64_t)n0 + lc;
+    // ---- cast + store from registers ----
+    if (row_ok && nv > 0) {
+      const int64_t gcol = (int64_t)n0 + cb;
       if (p.precast) {
         float* dst = p.precast + (int64_t)grow * p.ld_pre + gcol;
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (j < nv) dst[j] = v[j];
+        for (int j = 0; j < CPT; ++j)
+          if (j < nv) dst[j] = y[j];
       }
       if (p.out_dtype == LOKA_F32) {
         float* dst = reinterpret_cast<float*>(p.y) + (int64_t)grow * p.ldy + gcol;
-        if (nv == 32) {
+        if (nv == CPT) {
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          for (int j = 0; j < CPT; j += 4)
+            *reinterpret_cast<float4*>(dst + j) = make_float4(y[j], y[j + 1], y[j + 2], y[j + 3]);
         } else {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < nv) dst[j] = v[j];
+          for (int j = 0; j < CPT; ++j)
+            if (j < nv) dst[j] = y[j];
         }
       } else if (p.out_dtype == LOKA_BF16) {
         __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.y) + (int64_t)grow * p.ldy + gcol;
-        uint32_t w[16];
+        if (nv == CPT) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          __nv_bfloat162 hh = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
-          w[j] = *reinterpret_cast<uint32_t*>(&hh);
-        }
-        if (nv == 32) {
+          for (int j = 0; j < CPT; j += 8) {
+            uint32_t w[4];
 #pragma unroll
-          for (int j = 0; j < 16; j += 4)
-            *reinterpret_cast<uint4*>(dst + 2 * j) = make_uint4(w[j], w[j + 1], w[j + 2], w[j + 3]);
+            for (int k = 0; k < 4; ++k) {
+              __nv_bfloat162 hh = __floats2bfloat162_rn(y[j + 2 * k], y[j + 2 * k + 1]);
+              w[k] = *reinterpret_cast<uint32_t*>(&hh);
+            }
+            *reinterpret_cast<uint4*>(dst + j) = make_uint4(w[0], w[1], w[2], w[3]);
+          }
         } else {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < nv) dst[j] = __float2bfloat16_rn(v[j]);
+          for (int j = 0; j < CPT; ++j)
+            if (j < nv) dst[j] = __float2bfloat16_rn(y[j]);
         }
       } else {
         uint8_t* dst = reinterpret_cast<uint8_t*>(p.y) + (int64_t)grow * p.ldy + gcol;
         const float2 rr = make_float2(r_out, r_out);
-        uint32_t w[8];
+        uint32_t w[CPT / 4];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float2 a = fmul2(make_float2(v[4 * j], v[4 * j + 1]), rr);
-          const float2 b = fmul2(make_float2(v[4 * j + 2], v[4 * j + 3]), rr);
+        for (int j = 0; j < CPT / 4; ++j) {
+          const float2 a = fmul2(make_float2(y[4 * j], y[4 * j + 1]), rr);
+          const float2 b = fmul2(make_float2(y[4 * j + 2], y[4 * j + 3]), rr);
           w[j] = p.out_dtype == LOKA_E4M3 ? cvt_fp8x4<LOKA_E4M3>(a.x, a.y, b.x, b.y)
                                            : cvt_fp8x4<LOKA_E5M2>(a.x, a.y, b.x, b.y);
         }
-        if (nv == 32) {
-          *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
-          *reinterpret_cast<uint4*>(dst + 16) = make_uint4(w[4], w[5], w[6], w[7]);
+        if (nv == CPT) {
+#pragma unroll
+          for (int j = 0; j < CPT / 16; ++j)
+            *reinterpret_cast<uint4*>(dst + 16 * j) = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
         } else {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
+          for (int j = 0; j < CPT; ++j)
             if (j < nv) dst[j] = (uint8_t)(w[j >> 2] >> (8 * (j & 3)));
         }
       }
     }
-    if (warp == 2 && lane == 0) LOKA_TRACE(7);
-    if (csize > 1) cluster_sync_all();  // peers may still read our records from DSMEM
+    if (threadIdx.x == 64) LOKA_TRACE(7);
+    if (csize > 1) cluster_sync_all();  // peers may still be pushing into / reading our smem
   }
 
   tc_fence_before();
