@@ -325,27 +325,12 @@ def main():
         t_fp8 = time_steps(g8.replay, args.steps, args.warmup, flush, stream, barrier)
     clocks = clk.summary()
 
-    # per-kernel timing of the dominant kernel (the fused linear+norm launches), eager, same stream
-    lin_ms = [0.0] * 8
-    reps = max(3, min(args.steps, 20))
-    evs = []
-    with torch.cuda.stream(stream):
-        for _ in range(reps):
-            flush.zero_()
-            stack.quantize_all(sh)
-            torch.cuda._sleep(3_000_000)  # hold the stream while the host enqueues: events see GPU time only
-            row = []
-            for l in range(8):
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                stack.linear_only(l, sh)
-                e1.record(stream)
-                row.append((e0, e1))
-            evs.append(row)
-    torch.cuda.synchronize()
-    for row in evs:
-        for l, (e0, e1) in enumerate(row):
-            lin_ms[l] += e0.elapsed_time(e1) / reps
+    # The dominant kernel (the fused linear+norm launches): a graph of its 8 launches, replayed with
+    # the L2 flushed before each replay, timed with events on the launching stream; the per-launch
+    # duration is the replay time / 8 (launch gaps included, host enqueue excluded).
+    glin = capture(lambda: [stack.linear_only(l, sh) for l in range(8)], stream)
+    t_lin = time_steps(glin.replay, args.steps, args.warmup, flush, stream, None)
+    lin_ms_per_launch = (sum(t_lin) / len(t_lin)) / 8.0
 
     # BF16 baseline (torch F.linear + F.layer_norm, graph-captured) on the same inputs
     out_bf = torch.empty(M_PER_GPU, DIMS[8], dtype=torch.bfloat16, device=dev)
@@ -381,7 +366,7 @@ def main():
     bf16_peak, hbm_peak, src = peaks()
     fp8_peak = 2.0 * bf16_peak  # nominal dense fp8/bf16 ratio 4500/2250
     lin_fl = [2.0 * M_PER_GPU * DIMS[l] * DIMS[l + 1] for l in range(8)]
-    achieved = sum(lin_fl) / (sum(lin_ms) * 1e-3) / 1e12
+    achieved = (sum(lin_fl) / 8.0) / (lin_ms_per_launch * 1e-3) / 1e12  # mean FLOPs per launch / mean launch time
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
@@ -407,7 +392,9 @@ def main():
                          "bound": "tensor", "achieved": round(achieved, 2), "peak": round(fp8_peak, 1),
                          "unit": "TFLOP/s", "frac": round(achieved / fp8_peak, 4), "traffic": traffic,
                          "peak_source": f"{src}: 2 x bf16 {bf16_peak} TF/s (nominal fp8/bf16 ratio)",
-                         "per_launch_us": [round(1e3 * t, 2) for t in lin_ms]},
+                         "flop_per_launch": sum(lin_fl) / 8.0,
+                         "mean_launch_us": round(1e3 * lin_ms_per_launch, 3),
+                         "timing": "graph of the 8 launches, L2 flushed before each replay, CUDA events"},
             "e2e": {"value": round(e2e_value, 3), "unit": "TFLOP/s", "ms_per_step": round(ms_e2e, 5),
                     "h2d_bytes_per_step": int(x.numel() * 2), "d2h_bytes_per_step": int(stack.y.numel() * 2)},
             "gpu_launches": int(launches_per_step * args.steps),

@@ -68,6 +68,23 @@ static bool make_map_u8(CUtensorMap* m, const void* ptr, int64_t rows, int64_t c
 }
 
 static int elem_size(loka_dtype t) { return t == LOKA_F32 ? 4 : t == LOKA_BF16 ? 2 : 1; }
+
+// 2D map over the GEMM output [rows, cols] of dtype t (ld elements), box {128 bytes, 128 rows},
+// SW128 — the layout of the epilogue's staging tile.
+static bool make_map_out(CUtensorMap* m, void* ptr, int64_t rows, int64_t cols, int64_t ld, loka_dtype t) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  const int e = elem_size(t);
+  const CUtensorMapDataType dt = t == LOKA_F32    ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : t == LOKA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                  : CU_TENSOR_MAP_DATA_TYPE_UINT8;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * e)};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / e), 128u};
+  cuuint32_t es[2] = {1u, 1u};
+  return enc(m, dt, 2, ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 static bool is_fp8(loka_dtype t) { return t == LOKA_E4M3 || t == LOKA_E5M2; }
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -216,8 +233,8 @@ loka_status loka_quantize_grouped(int32_t G, const loka_tensor* x, loka_tensor* 
 // ------------------------------------------------------------------------------------------
 size_t loka_linear_workspace_size(const loka_linear_args* /*a*/) { return 0; }
 
-static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CUtensorMap* tb, LinearParams* p,
-                                  int* bn_out) {
+static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CUtensorMap* tb, CUtensorMap* ty,
+                                  LinearParams* p, int* bn_out) {
   if (!a) return LOKA_ERR_INVALID_ARG;
   const int64_t M = a->M, N = a->N, K = a->K;
   if (M <= 0 || N <= 0 || K <= 0 || M > (1ll << 31) - 1 || N > (1ll << 30) || K > (1ll << 31) - 1)
@@ -268,6 +285,7 @@ static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CU
   if (full_row) csize = (int)cdiv(N, bn);
   if (!make_map_u8(ta, A.data, M, K, A.ld, 128)) return LOKA_ERR_CUDA;
   if (!make_map_u8(tb, B.data, N, K, B.ld, (uint32_t)bn)) return LOKA_ERR_CUDA;
+  if (!make_map_out(ty, Y.data, M, N, Y.ld, Y.dtype)) return LOKA_ERR_CUDA;
 
   std::memset(p, 0, sizeof(*p));
   p->M = (int32_t)M;
@@ -299,14 +317,14 @@ static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CU
 }
 
 loka_status loka_fp8_linear_norm(const loka_linear_args* a, void* /*ws*/, size_t /*ws_bytes*/, loka_stream_t stream) {
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, ty;
   LinearParams p;
   int bn = 0;
-  loka_status st = prepare_linear(a, &ta, &tb, &p, &bn);
+  loka_status st = prepare_linear(a, &ta, &tb, &ty, &p, &bn);
   if (st != LOKA_OK) return st;
   st = check_device();
   if (st != LOKA_OK) return st;
-  cudaError_t e = launch_linear(ta, tb, p, bn, reinterpret_cast<cudaStream_t>(stream));
+  cudaError_t e = launch_linear(ta, tb, ty, p, bn, reinterpret_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
 }
 
@@ -315,11 +333,11 @@ size_t loka_grouped_workspace_size(int32_t /*G*/, const loka_linear_args* /*a*/)
 loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* ws, size_t ws_bytes,
                                     loka_stream_t stream) {
   if (G < 0 || (G > 0 && !a)) return LOKA_ERR_INVALID_ARG;
-  std::vector<CUtensorMap> ta(G), tb(G);
+  std::vector<CUtensorMap> ta(G), tb(G), ty(G);
   std::vector<LinearParams> p(G);
   std::vector<int> bn(G);
   for (int g = 0; g < G; ++g) {
-    loka_status st = prepare_linear(&a[g], &ta[g], &tb[g], &p[g], &bn[g]);
+    loka_status st = prepare_linear(&a[g], &ta[g], &tb[g], &ty[g], &p[g], &bn[g]);
     if (st != LOKA_OK) return st;
   }
   loka_status st = check_device();
@@ -327,7 +345,7 @@ loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* 
   (void)ws;
   (void)ws_bytes;
   for (int g = 0; g < G; ++g) {
-    cudaError_t e = launch_linear(ta[g], tb[g], p[g], bn[g], reinterpret_cast<cudaStream_t>(stream));
+    cudaError_t e = launch_linear(ta[g], tb[g], ty[g], p[g], bn[g], reinterpret_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return LOKA_ERR_CUDA;
   }
   return LOKA_OK;

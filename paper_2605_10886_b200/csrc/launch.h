@@ -55,8 +55,9 @@ struct LinearParams {
 
 // Launch one linear+norm problem.  tma_a/tma_b are 2D maps over the FP8 operands with box
 // {128 (K), 128 (A rows)} and {128 (K), bn (B rows)}, 128B swizzle.
-cudaError_t launch_linear(const CUtensorMap& tma_a, const CUtensorMap& tma_b, const LinearParams& p, int bn,
-                          cudaStream_t st);
+// tma_y: 2D map over the output [M, N] (element type of y), box {128 bytes, 128 rows}, SW128.
+cudaError_t launch_linear(const CUtensorMap& tma_a, const CUtensorMap& tma_b, const CUtensorMap& tma_y,
+                          const LinearParams& p, int bn, cudaStream_t st);
 
 struct ProbeLayer {
   const void* out; const void* ref;

@@ -66,38 +66,53 @@ template <int BN> struct LinCfg {
   static constexpr int kOffCs = kOffCol + 4 * BN * 4;                // [kMaxCluster][128] float4 records
   static constexpr int kOffCs2 = kOffCs + kMaxCluster * 128 * 16;    // [kMaxCluster][128] amax
   static constexpr int kSmemBytes = kOffCs2 + kMaxCluster * 128 * 4 + 1024;  // + alignment slack
-  // the quarter exchange [4][kRec + 1][128] floats aliases the (drained) operand ring
-  static_assert(4 * (kRec + 1) * 128 * 4 <= kStages * kStageBytes, "hx alias");
+  // after the mainloop the (drained) operand ring holds the quarter exchange [4][kRec + 1][128]
+  // floats at offset 0 and the output staging tile (128 rows x BN x <= 4 bytes) at kOffStage
+  static constexpr int kOffStage = 16384;
+  static_assert(4 * (kRec + 1) * 128 * 4 <= kOffStage, "hx alias");
+  static_assert(kOffStage + 128 * BN * 4 <= kStages * kStageBytes, "staging alias");
   static_assert(kStages >= 2 && kSmemBytes <= 227 * 1024, "smem");
 };
 
-// Chan et al. pairwise merge of (n, mean, M2) — the same update as PAPER.md:293-299
-// (batched Welford merge) applied to column partitions of one row.
-LOKA_DEVINL void chan_merge(float& n, float& mean, float& m2, float nb, float meanb, float m2b) {
-  if (nb <= 0.f) return;
-  if (n <= 0.f) { n = nb; mean = meanb; m2 = m2b; return; }
-  const float nt = n + nb;
-  const float d = meanb - mean;
-  mean = mean + d * (nb / nt);
-  m2 = m2 + m2b + d * d * (n * nb / nt);
-  n = nt;
-}
-
+// Row statistics of a column partition: (n, mean, M2) for LayerNorm (merged with the batched
+// Welford / Chan update of PAPER.md:293-299 applied to column partitions), sum of squares for
+// RMS/BlockNorm, y max / min for the FP8 output's row amax.
 struct RowRec {
   float n, mean, m2, ss, ymax, ymin;
   LOKA_DEVINL void init() { n = 0.f; mean = 0.f; m2 = 0.f; ss = 0.f; ymax = -INFINITY; ymin = INFINITY; }
-  LOKA_DEVINL void merge(const RowRec& o) {
-    chan_merge(n, mean, m2, o.n, o.mean, o.m2);
-    ss += o.ss;
-    ymax = fmaxf(ymax, o.ymax);
-    ymin = fminf(ymin, o.ymin);
-  }
 };
+
+// n-way parallel merge of K partial records (fixed order -> bit-identical wherever it runs):
+//   n = sum n_k, mean = sum n_k mean_k / n, M2 = sum M2_k + sum n_k (mean_k - mean)^2
+// (Chan et al.'s pairwise update applied to all parts at once: one division).
+template <int K>
+LOKA_DEVINL RowRec merge_recs(const RowRec (&r)[K]) {
+  RowRec o;
+  o.init();
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    o.n += r[k].n;
+    s = fmaf(r[k].n, r[k].mean, s);
+    o.ss += r[k].ss;
+    o.ymax = fmaxf(o.ymax, r[k].ymax);
+    o.ymin = fminf(o.ymin, r[k].ymin);
+  }
+  o.mean = o.n > 0.f ? __fdiv_rn(s, o.n) : 0.f;
+  float m2 = 0.f;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const float d = r[k].mean - o.mean;
+    m2 += r[k].m2 + r[k].n * d * d;
+  }
+  o.m2 = m2;
+  return o;
+}
 
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     linear_norm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-                       const LinearParams p) {
+                       const __grid_constant__ CUtensorMap tma_y, const LinearParams p) {
   using C = LinCfg<BN>;
   constexpr int CPT = C::kCPT;
   extern __shared__ uint8_t smem_raw[];
@@ -127,6 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tma_a);
     tma_prefetch_desc(&tma_b);
+    tma_prefetch_desc(&tma_y);
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
@@ -326,18 +342,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       float* my = hx + (size_t)cq * (kRec + 1) * 128 + r;  // component-major: conflict-free
       my[0] = rec.n; my[128] = rec.mean; my[256] = rec.m2; my[384] = rec.ss; my[512] = rec.ymax; my[640] = rec.ymin;
       named_bar_sync(1, kEpiThreads);
-      RowRec all;
-      all.init();
+      RowRec parts[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const float* o = hx + (size_t)k * (kRec + 1) * 128 + r;
-        RowRec t;
+        RowRec& t = parts[k];
         t.n = o[0]; t.mean = o[128]; t.m2 = o[256]; t.ss = o[384]; t.ymax = o[512]; t.ymin = o[640];
         q_ss[k] = t.ss;
         q_ma[k] = t.n > 0.f ? fmaxf(t.ymax, -t.ymin) : 0.f;
-        all.merge(t);
       }
-      rec = all;
+      rec = merge_recs(parts);
     }
     if (threadIdx.x == 64) LOKA_TRACE(9);
 
@@ -350,18 +364,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int rk = 0; rk < csize; ++rk) st_dsmem_f4(mapa_shared(la, (uint32_t)rk), v);
       }
       cluster_sync_all();
-      rec.init();
-      for (int rk = 0; rk < csize; ++rk) {
-        const float4 v = lds_f4(smem_u32(cs + ((size_t)rk * 128 + r) * 4));
-        RowRec o;
-        o.n = (float)min(BN, p.N - rk * BN);
-        o.mean = norm == LOKA_NORM_LAYER ? v.x : 0.f;
-        o.m2 = v.y;
-        o.ss = norm == LOKA_NORM_LAYER ? 0.f : v.x;
-        o.ymax = v.z;
-        o.ymin = v.w;
-        rec.merge(o);
+      RowRec parts[kMaxCluster];  // ranks >= csize stay empty (n = 0) and merge as no-ops
+#pragma unroll
+      for (int rk = 0; rk < kMaxCluster; ++rk) {
+        RowRec& o = parts[rk];
+        o.init();
+        if (rk < csize) {
+          const float4 v = lds_f4(smem_u32(cs + ((size_t)rk * 128 + r) * 4));
+          o.n = (float)min(BN, p.N - rk * BN);
+          o.mean = norm == LOKA_NORM_LAYER ? v.x : 0.f;
+          o.m2 = v.y;
+          o.ss = norm == LOKA_NORM_LAYER ? 0.f : v.x;
+          o.ymax = v.z;
+          o.ymin = v.w;
+        }
       }
+      rec = merge_recs(parts);
     }
     if (threadIdx.x == 64) LOKA_TRACE(10);
 
@@ -451,65 +469,68 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (threadIdx.x == 64) LOKA_TRACE(6);
 
-    // ---- cast + store from registers ----
-    if (row_ok && nv > 0) {
-      const int64_t gcol = (int64_t)n0 + cb;
-      if (p.precast) {
-        float* dst = p.precast + (int64_t)grow * p.ld_pre + gcol;
+    // ---- cast into a 128B-swizzled smem tile (aliasing the drained ring), then TMA store ----
+    // Box b of the tile holds output bytes [128 b, 128 b + 128) of every row; 16-byte chunk c of
+    // row r lives at b*16K + r*128 + ((c ^ (r & 7)) << 4), the TMA SWIZZLE_128B pattern, so the
+    // 8 rows a quarter-warp writes land in 8 different bank groups (conflict-free) and the global
+    // writes are whole 128-byte lines (OOB rows / columns are clipped by the TMA unit).
+    if (p.precast && row_ok) {
+      float* dst = p.precast + (int64_t)grow * p.ld_pre + n0 + cb;
 #pragma unroll
-        for (int j = 0; j < CPT; ++j)
-          if (j < nv) dst[j] = y[j];
+      for (int j = 0; j < CPT; ++j)
+        if (j < nv) dst[j] = y[j];
+    }
+    const int esz = p.out_dtype == LOKA_F32 ? 4 : p.out_dtype == LOKA_BF16 ? 2 : 1;
+    const uint32_t stage_s = smem_u32(smem) + (uint32_t)C::kOffStage;
+    auto put16 = [&](int chunk, uint4 v) {  // chunk = 16-byte chunk index within this thread's bytes
+      const uint32_t bofs = (uint32_t)(cb * esz + 16 * chunk);
+      const uint32_t a = stage_s + (bofs >> 7) * 16384u + (uint32_t)r * 128u +
+                         ((((bofs >> 4) & 7u) ^ ((uint32_t)r & 7u)) << 4);
+      sts_u4(a, v);
+    };
+    if (p.out_dtype == LOKA_F32) {
+#pragma unroll
+      for (int k = 0; k < CPT / 4; ++k)
+        put16(k, make_uint4(__float_as_uint(y[4 * k]), __float_as_uint(y[4 * k + 1]), __float_as_uint(y[4 * k + 2]),
+                            __float_as_uint(y[4 * k + 3])));
+    } else if (p.out_dtype == LOKA_BF16) {
+#pragma unroll
+      for (int k = 0; k < CPT / 8; ++k) {
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          __nv_bfloat162 hh = __floats2bfloat162_rn(y[8 * k + 2 * i], y[8 * k + 2 * i + 1]);
+          w[i] = *reinterpret_cast<uint32_t*>(&hh);
+        }
+        put16(k, make_uint4(w[0], w[1], w[2], w[3]));
       }
-      if (p.out_dtype == LOKA_F32) {
-        float* dst = reinterpret_cast<float*>(p.y) + (int64_t)grow * p.ldy + gcol;
-        if (nv == CPT) {
+    } else {
+      const float2 rr = make_float2(r_out, r_out);
 #pragma unroll
-          for (int j = 0; j < CPT; j += 4)
-            *reinterpret_cast<float4*>(dst + j) = make_float4(y[j], y[j + 1], y[j + 2], y[j + 3]);
-        } else {
+      for (int k = 0; k < CPT / 16; ++k) {
+        uint32_t w[4];
 #pragma unroll
-          for (int j = 0; j < CPT; ++j)
-            if (j < nv) dst[j] = y[j];
-        }
-      } else if (p.out_dtype == LOKA_BF16) {
-        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.y) + (int64_t)grow * p.ldy + gcol;
-        if (nv == CPT) {
-#pragma unroll
-          for (int j = 0; j < CPT; j += 8) {
-            uint32_t w[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              __nv_bfloat162 hh = __floats2bfloat162_rn(y[j + 2 * k], y[j + 2 * k + 1]);
-              w[k] = *reinterpret_cast<uint32_t*>(&hh);
-            }
-            *reinterpret_cast<uint4*>(dst + j) = make_uint4(w[0], w[1], w[2], w[3]);
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < CPT; ++j)
-            if (j < nv) dst[j] = __float2bfloat16_rn(y[j]);
-        }
-      } else {
-        uint8_t* dst = reinterpret_cast<uint8_t*>(p.y) + (int64_t)grow * p.ldy + gcol;
-        const float2 rr = make_float2(r_out, r_out);
-        uint32_t w[CPT / 4];
-#pragma unroll
-        for (int j = 0; j < CPT / 4; ++j) {
-          const float2 a = fmul2(make_float2(y[4 * j], y[4 * j + 1]), rr);
-          const float2 b = fmul2(make_float2(y[4 * j + 2], y[4 * j + 3]), rr);
-          w[j] = p.out_dtype == LOKA_E4M3 ? cvt_fp8x4<LOKA_E4M3>(a.x, a.y, b.x, b.y)
+        for (int i = 0; i < 4; ++i) {
+          const int j = 16 * k + 4 * i;
+          const float2 a = fmul2(make_float2(y[j], y[j + 1]), rr);
+          const float2 b = fmul2(make_float2(y[j + 2], y[j + 3]), rr);
+          w[i] = p.out_dtype == LOKA_E4M3 ? cvt_fp8x4<LOKA_E4M3>(a.x, a.y, b.x, b.y)
                                            : cvt_fp8x4<LOKA_E5M2>(a.x, a.y, b.x, b.y);
         }
-        if (nv == CPT) {
-#pragma unroll
-          for (int j = 0; j < CPT / 16; ++j)
-            *reinterpret_cast<uint4*>(dst + 16 * j) = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
-        } else {
-#pragma unroll
-          for (int j = 0; j < CPT; ++j)
-            if (j < nv) dst[j] = (uint8_t)(w[j >> 2] >> (8 * (j & 3)));
-        }
+        put16(k, make_uint4(w[0], w[1], w[2], w[3]));
       }
+    }
+    fence_proxy_async_smem();
+    named_bar_sync(1, kEpiThreads);
+    if (threadIdx.x == 0) {
+      const int per_box = 128 / esz;  // output elements per 128-byte box row
+      const int nbox = BN * esz / 128;
+      for (int b = 0; b < nbox; ++b) {
+        const int c0 = n0 + b * per_box;
+        if (c0 < p.N) tma_store_2d(&tma_y, reinterpret_cast<const uint8_t*>(smem) + C::kOffStage + b * 16384, c0, m0);
+      }
+      bulk_commit();
+      bulk_wait_read0();  // the tile must stay in smem until the TMA unit has read it
     }
     if (threadIdx.x == 64) LOKA_TRACE(7);
     if (csize > 1) cluster_sync_all();  // peers may still be pushing into / reading our smem
@@ -555,7 +576,8 @@ long long debug_trace(int enable, unsigned long long* out, long long n) {
 }
 
 template <int BN>
-static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const LinearParams& p, cudaStream_t st) {
+static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, const LinearParams& p,
+                             cudaStream_t st) {
   using C = LinCfg<BN>;
   static bool attr_done = false;  // idempotent; racing threads set the same value
   if (!attr_done) {
@@ -578,17 +600,17 @@ static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, linear_norm_kernel<BN>, ta, tb, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, linear_norm_kernel<BN>, ta, tb, ty, p);
   note_launch();
   return e;
 }
 
-cudaError_t launch_linear(const CUtensorMap& ta, const CUtensorMap& tb, const LinearParams& p, int bn,
-                          cudaStream_t st) {
+cudaError_t launch_linear(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, const LinearParams& p,
+                          int bn, cudaStream_t st) {
   switch (bn) {
-    case 64: return launch_bn<64>(ta, tb, p, st);
-    case 128: return launch_bn<128>(ta, tb, p, st);
-    case 256: return launch_bn<256>(ta, tb, p, st);
+    case 64: return launch_bn<64>(ta, tb, ty, p, st);
+    case 128: return launch_bn<128>(ta, tb, ty, p, st);
+    case 256: return launch_bn<256>(ta, tb, ty, p, st);
     default: return cudaErrorInvalidValue;
   }
 }
