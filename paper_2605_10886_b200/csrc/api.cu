@@ -69,20 +69,22 @@ static bool make_map_u8(CUtensorMap* m, const void* ptr, int64_t rows, int64_t c
 
 static int elem_size(loka_dtype t) { return t == LOKA_F32 ? 4 : t == LOKA_BF16 ? 2 : 1; }
 
-// 2D map over the GEMM output [rows, cols] of dtype t (ld elements), box {128 bytes, 128 rows},
-// SW128 — the layout of the epilogue's staging tile.
-static bool make_map_out(CUtensorMap* m, void* ptr, int64_t rows, int64_t cols, int64_t ld, loka_dtype t) {
+// 2D map over the GEMM output [rows, cols] of dtype t (ld elements), box {min(128, bn*e) bytes,
+// 128 rows} with the matching 128B / 64B swizzle — the layout of the epilogue's staging tile.
+static bool make_map_out(CUtensorMap* m, void* ptr, int64_t rows, int64_t cols, int64_t ld, loka_dtype t, int bn) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
   const int e = elem_size(t);
+  const int box_bytes = bn * e < 128 ? bn * e : 128;
   const CUtensorMapDataType dt = t == LOKA_F32    ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                  : t == LOKA_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                                   : CU_TENSOR_MAP_DATA_TYPE_UINT8;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)(ld * e)};
-  cuuint32_t box[2] = {(cuuint32_t)(128 / e), 128u};
+  cuuint32_t box[2] = {(cuuint32_t)(box_bytes / e), 128u};
   cuuint32_t es[2] = {1u, 1u};
-  return enc(m, dt, 2, ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  return enc(m, dt, 2, ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             box_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 static bool is_fp8(loka_dtype t) { return t == LOKA_E4M3 || t == LOKA_E5M2; }
@@ -285,7 +287,7 @@ static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CU
   if (full_row) csize = (int)cdiv(N, bn);
   if (!make_map_u8(ta, A.data, M, K, A.ld, 128)) return LOKA_ERR_CUDA;
   if (!make_map_u8(tb, B.data, N, K, B.ld, (uint32_t)bn)) return LOKA_ERR_CUDA;
-  if (!make_map_out(ty, Y.data, M, N, Y.ld, Y.dtype)) return LOKA_ERR_CUDA;
+  if (!make_map_out(ty, Y.data, M, N, Y.ld, Y.dtype, bn)) return LOKA_ERR_CUDA;
 
   std::memset(p, 0, sizeof(*p));
   p->M = (int32_t)M;

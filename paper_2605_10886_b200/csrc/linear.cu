@@ -481,11 +481,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (j < nv) dst[j] = y[j];
     }
     const int esz = p.out_dtype == LOKA_F32 ? 4 : p.out_dtype == LOKA_BF16 ? 2 : 1;
+    // box row width: 128 B (SWIZZLE_128B, chunk ^= r & 7) or, when a CTA row is only 64 B
+    // (FP8 output, BN = 64), 64 B (SWIZZLE_64B, chunk ^= (r >> 1) & 3); must match make_map_out
+    const uint32_t box_bytes = (uint32_t)min(128, BN * esz);
     const uint32_t stage_s = smem_u32(smem) + (uint32_t)C::kOffStage;
     auto put16 = [&](int chunk, uint4 v) {  // chunk = 16-byte chunk index within this thread's bytes
       const uint32_t bofs = (uint32_t)(cb * esz + 16 * chunk);
-      const uint32_t a = stage_s + (bofs >> 7) * 16384u + (uint32_t)r * 128u +
-                         ((((bofs >> 4) & 7u) ^ ((uint32_t)r & 7u)) << 4);
+      const uint32_t c16 = (bofs % box_bytes) >> 4;
+      const uint32_t sw = box_bytes == 128u ? (c16 ^ ((uint32_t)r & 7u)) : (c16 ^ (((uint32_t)r >> 1) & 3u));
+      const uint32_t a = stage_s + (bofs / box_bytes) * (128u * box_bytes) + (uint32_t)r * box_bytes + (sw << 4);
       sts_u4(a, v);
     };
     if (p.out_dtype == LOKA_F32) {
@@ -523,11 +527,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_proxy_async_smem();
     named_bar_sync(1, kEpiThreads);
     if (threadIdx.x == 0) {
-      const int per_box = 128 / esz;  // output elements per 128-byte box row
-      const int nbox = BN * esz / 128;
+      const int per_box = (int)box_bytes / esz;  // output elements per box row
+      const int nbox = BN * esz / (int)box_bytes;
       for (int b = 0; b < nbox; ++b) {
         const int c0 = n0 + b * per_box;
-        if (c0 < p.N) tma_store_2d(&tma_y, reinterpret_cast<const uint8_t*>(smem) + C::kOffStage + b * 16384, c0, m0);
+        if (c0 < p.N)
+          tma_store_2d(&tma_y, reinterpret_cast<const uint8_t*>(smem) + C::kOffStage + b * 128 * (int)box_bytes, c0, m0);
       }
       bulk_commit();
       bulk_wait_read0();  // the tile must stay in smem until the TMA unit has read it
