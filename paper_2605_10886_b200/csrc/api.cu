@@ -1,5 +1,6 @@
 // api.cu — the C ABI (include/loka.h): argument validation, workspace sizing, TMA tensor-map
 // construction, kernel selection and launch.  No device work is done here besides launches.
+#include <algorithm>
 #include <atomic>
 #include <cstring>
 #include <mutex>
@@ -338,16 +339,55 @@ loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* 
   std::vector<CUtensorMap> ta(G), tb(G), ty(G);
   std::vector<LinearParams> p(G);
   std::vector<int> bn(G);
-  for (int g = 0; g < G; ++g) {
+  for (int g = 0; g < G; ++g) {  // full validation of every problem before any launch
     loka_status st = prepare_linear(&a[g], &ta[g], &tb[g], &ty[g], &p[g], &bn[g]);
     if (st != LOKA_OK) return st;
   }
-  loka_status st = check_device();
+  int sms = 148;
+  loka_status st = check_device(&sms);
   if (st != LOKA_OK) return st;
   (void)ws;
   (void)ws_bytes;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // Problems with a plain dequant(+bias) epilogue and bf16 output run in persistent grouped
+  // launches (<= kMaxGroups problems each, longest K first); row-coupled epilogues (norms, FP8
+  // output) keep their own fused linear_norm launches.
+  std::vector<int> grouped, single;
   for (int g = 0; g < G; ++g) {
-    cudaError_t e = launch_linear(ta[g], tb[g], ty[g], p[g], bn[g], reinterpret_cast<cudaStream_t>(stream));
+    const bool ok = a[g].norm == LOKA_NORM_NONE && a[g].y.dtype == LOKA_BF16 && !a[g].debug_precast;
+    (ok ? grouped : single).push_back(g);
+  }
+  std::stable_sort(grouped.begin(), grouped.end(), [&](int x, int y) { return a[x].K > a[y].K; });
+  for (size_t i0 = 0; i0 < grouped.size(); i0 += kMaxGroups) {
+    GroupedParams gp;
+    std::memset(&gp, 0, sizeof(gp));
+    const int n = (int)std::min<size_t>(kMaxGroups, grouped.size() - i0);
+    gp.G = n;
+    for (int k = 0; k < n; ++k) {
+      const loka_linear_args& q = a[grouped[i0 + k]];
+      if (!make_map_u8(&gp.ta[k], q.a.data, q.M, q.K, q.a.ld, 128)) return LOKA_ERR_CUDA;
+      if (!make_map_u8(&gp.tb[k], q.b.data, q.N, q.K, q.b.ld, 128)) return LOKA_ERR_CUDA;
+      if (!make_map_out(&gp.ty[k], q.y.data, q.M, q.N, q.y.ld, q.y.dtype, 128)) return LOKA_ERR_CUDA;
+      GroupDesc& d = gp.g[k];
+      d.M = (int32_t)q.M;
+      d.N = (int32_t)q.N;
+      d.K = (int32_t)q.K;
+      d.tiles_n = (int32_t)cdiv(q.N, 128);
+      d.a_fmt = q.a.dtype == LOKA_E5M2 ? 1 : 0;
+      d.b_fmt = q.b.dtype == LOKA_E5M2 ? 1 : 0;
+      d.sa = q.a.scales;
+      d.sa_row = q.a.gran == LOKA_GRAN_ROW;
+      d.sb = q.b.scales;
+      d.sb_row = q.b.gran == LOKA_GRAN_ROW;
+      d.bias = q.bias;
+      d.bias_bf16 = q.bias_dtype == LOKA_BF16;
+      d.out_dtype = q.y.dtype;
+      gp.tile_start[k + 1] = gp.tile_start[k] + (int32_t)(cdiv(q.M, 128) * d.tiles_n);
+    }
+    if (launch_grouped(gp, sms, s) != cudaSuccess) return LOKA_ERR_CUDA;
+  }
+  for (int g : single) {
+    cudaError_t e = launch_linear(ta[g], tb[g], ty[g], p[g], bn[g], s);
     if (e != cudaSuccess) return LOKA_ERR_CUDA;
   }
   return LOKA_OK;

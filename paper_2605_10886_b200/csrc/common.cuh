@@ -209,6 +209,7 @@ LOKA_DEVINL void tma_store_2d(const CUtensorMap* m, const void* src, int32_t c0,
 }
 LOKA_DEVINL void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 LOKA_DEVINL void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+LOKA_DEVINL void bulk_wait_read_le1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 // make generic-proxy shared-memory writes visible to the async (TMA) proxy
 LOKA_DEVINL void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 LOKA_DEVINL void sts_u4(uint32_t saddr, uint4 v) {

@@ -59,6 +59,24 @@ struct LinearParams {
 cudaError_t launch_linear(const CUtensorMap& tma_a, const CUtensorMap& tma_b, const CUtensorMap& tma_y,
                           const LinearParams& p, int bn, cudaStream_t st);
 
+// ---- grouped persistent launch (grouped.cu) ----
+constexpr int kMaxGroups = 32;  // per launch (kernel-parameter space: 3 tensor maps per group)
+struct GroupDesc {
+  int32_t M, N, K, tiles_n;
+  int32_t a_fmt, b_fmt;
+  const float* sa; int32_t sa_row;
+  const float* sb; int32_t sb_row;
+  const void* bias; int32_t bias_bf16;
+  int32_t out_dtype;
+};
+struct GroupedParams {
+  CUtensorMap ta[kMaxGroups], tb[kMaxGroups], ty[kMaxGroups];  // A box {128,128}, B box {128,128}, Y out
+  GroupDesc g[kMaxGroups];
+  int32_t G;
+  int32_t tile_start[kMaxGroups + 1];  // prefix sum of 128x128 tiles
+};
+cudaError_t launch_grouped(const GroupedParams& gp, int num_sms, cudaStream_t st);
+
 struct ProbeLayer {
   const void* out; const void* ref;
   int32_t out_bf16, ref_bf16;

@@ -1,0 +1,82 @@
+"""-m gpu: loka_grouped_fp8_linear (a6) against oracle/linear.py: the cfg3 DHEN-style ensemble
+(64 heterogeneous GEMMs over 8 shared inputs, one persistent launch per <= 32 problems) and a
+mixed list that also routes norm / FP8-output problems through their own fused launches."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from gpu_util import DEV, f64, to_dev_padded
+
+pytestmark = pytest.mark.gpu
+lk = pytest.importorskip("paper_2605_10886_b200") if torch.cuda.is_available() else None
+TOL = 2e-3
+
+
+def _check_bf16(y, yo):
+    yg = f64(y)
+    rms = np.sqrt(np.mean(yo ** 2, axis=1, keepdims=True))
+    bound = TOL * np.maximum(np.abs(yo), rms) + 2.0 ** -8 * np.abs(yo)
+    bad = np.abs(yg - yo) > bound
+    assert not bad.any(), (int(bad.sum()), float(np.abs(yg - yo).max()))
+
+
+def _quant(x):
+    return lk.loka_quantize(to_dev_padded(x) if x.device.type == "cpu" else x, "e4m3", "row")
+
+
+def test_cfg3_ensemble_64_gemms_sampled():
+    S = synth.CFG3_DIMS
+    M = 2048
+    xs = [(synth.heavy(M, k, i, device=DEV) if i % 2 else synth.gaussian(M, k, i, device=DEV)) for i, k in enumerate(S)]
+    xq = [_quant(x) for x in xs]
+    args, keep, outs = [], [], []
+    for i, k in enumerate(S):
+        for j, n in enumerate(S):
+            wq, ws = _quant(synth.weight(n, k, 1000 + 8 * i + j, device=DEV))
+            a, y, _ = lk.make_linear_args(xq[i][0], xq[i][1], wq, ws, out_dtype="bf16", keep=keep)
+            args.append(a)
+            outs.append((i, wq, ws, y))
+    lk.loka_grouped_fp8_linear(args)
+    torch.cuda.synchronize()
+    rows = torch.randperm(M, generator=torch.Generator().manual_seed(3))[:48].sort().values.to(DEV)
+    for i, wq, ws, y in outs:
+        q, s = xq[i]
+        yo = oracle.linear.linear_norm(q[rows].cpu().numpy(), s[rows].cpu().numpy(), "e4m3", "row",
+                                       wq.cpu().numpy(), ws.cpu().numpy(), "e4m3", "row")
+        _check_bf16(y[rows], yo)
+
+
+def test_grouped_mixed_epilogues_and_ragged_shapes():
+    """Ragged M/N/K, bias, tensorwise scales, plus problems that need their own fused launch
+    (LayerNorm, FP8 output) in the same call."""
+    specs = [(300, 200, 208, "none", "bf16", True), (130, 64, 96, "none", "bf16", False),
+             (256, 512, 384, "layer", "f32", False), (128, 256, 128, "none", "e4m3", False),
+             (1000, 384, 1024, "none", "bf16", True), (64, 136, 16, "none", "bf16", False)]
+    args, keep, res = [], [], []
+    for t, (M, N, K, norm, od, bias) in enumerate(specs):
+        x, w = synth.heavy(M, K, t), synth.weight(N, K, 50 + t)
+        gran = "tensor" if t == 1 else "row"
+        xq, xs = lk.loka_quantize(to_dev_padded(x), "e4m3", gran)
+        wq, ws = lk.loka_quantize(to_dev_padded(w), "e4m3", gran)
+        b = torch.randn(N, generator=torch.Generator().manual_seed(t)).to(torch.bfloat16).to(DEV) if bias else None
+        a, y, ys = lk.make_linear_args(xq, xs, wq, ws, a_gran=gran, b_gran=gran, norm=norm, out_dtype=od, bias=b,
+                                       keep=keep)
+        args.append(a)
+        res.append((xq, xs, wq, ws, gran, norm, od, b, y, ys))
+    lk.loka_grouped_fp8_linear(args)
+    torch.cuda.synchronize()
+    for xq, xs, wq, ws, gran, norm, od, b, y, ys in res:
+        yo = oracle.linear.linear_norm(xq.cpu().numpy(), xs.cpu().numpy(), "e4m3", gran, wq.cpu().numpy(),
+                                       ws.cpu().numpy(), "e4m3", gran, norm=norm,
+                                       bias=None if b is None else f64(b))
+        if od == "bf16":
+            _check_bf16(y, yo)
+        elif od == "f32":
+            rms = np.sqrt(np.mean(yo ** 2, axis=1, keepdims=True))
+            assert np.max(np.abs(f64(y) - yo) / np.maximum(np.abs(yo), rms)) <= TOL
+        else:
+            deq = oracle.quantize.dequantize(y.cpu().numpy(), ys.cpu().numpy(), "e4m3", "row")
+            rms = np.sqrt(np.mean(yo ** 2, axis=1, keepdims=True))
+            assert np.all(np.abs(deq - yo) <= 2.0 ** -4 * np.abs(yo) + TOL * np.maximum(np.abs(yo), rms) + 1e-30)
