@@ -1,0 +1,81 @@
+"""a9 multi-rank protocol on CPU (gloo, world_size 2 and 3): row sharding, the split-phase
+tensorwise quantize with an all_reduce(MAX) between the phases, and per-rank probe-statistics
+reduction.  The device kernels are replaced by oracle functions here (no GPU); the GPU path of
+the same protocol is tests/test_gpu_dist.py."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+from paper_2605_10886_b200 import dist as ldist
+
+pytestmark = pytest.mark.dist
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _oracle_amax(x, fmt):
+    return torch.tensor([float(np.abs(x.double().numpy()).max())], dtype=torch.float32)
+
+
+def _oracle_cast(x, fmt, amax, scale_fmt):
+    q, s = oracle.quantize.quantize(x.double().numpy(), fmt, "tensor", scale_fmt, amax=np.array([float(amax[0])]))
+    return torch.from_numpy(q), torch.from_numpy(s)
+
+
+def _worker(rank, world, port, total, cols, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    r0, r1 = ldist.shard_rows(total, world, rank)
+    x = synth.heavy(r1 - r0, cols, 3, row0=r0, total_rows=total)
+    q, s, amax = ldist.quantize_tensorwise_sharded(x, "e4m3", amax_fn=_oracle_amax, cast_fn=_oracle_cast)
+    # probe statistics of the shard (oracle), then the cross-rank reduction
+    ref = x.double().numpy()
+    out = oracle.quantize.dequantize(q.numpy(), s.numpy(), "e4m3", "tensor")
+    st = ldist.reduce_probe_stats([oracle.probe.mere_stats(out, ref)])[0]
+    np.save(os.path.join(out_dir, f"q{rank}.npy"), q.numpy())
+    np.save(os.path.join(out_dir, f"s{rank}.npy"), s.numpy())
+    if rank == 0:
+        np.save(os.path.join(out_dir, "probe.npy"), np.array([st["mere"], st["max_rel"], st["count"]]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,total", [(2, 300), (3, 257)])
+def test_sharded_tensorwise_equals_single_device(world, total, tmp_path):
+    cols = 96
+    mp.spawn(_worker, args=(world, _free_port(), total, cols, str(tmp_path)), nprocs=world, join=True)
+    x = synth.heavy(total, cols, 3)
+    # the shard generator reproduces the global tensor's rows exactly
+    parts = [synth.heavy(r1 - r0, cols, 3, row0=r0, total_rows=total)
+             for r0, r1 in (ldist.shard_rows(total, world, r) for r in range(world))]
+    assert torch.equal(torch.cat(parts), x)
+    qg, sg = oracle.quantize.quantize(x.double().numpy(), "e4m3", "tensor")
+    qs = np.concatenate([np.load(tmp_path / f"q{r}.npy") for r in range(world)])
+    for r in range(world):
+        assert np.load(tmp_path / f"s{r}.npy").view(np.uint32)[0] == sg.view(np.uint32)[0]
+    assert np.array_equal(qs, qg)  # bit-identical to the single-device quantization
+    # the reduced probe statistics equal the statistics of the whole tensor
+    st = oracle.probe.mere_stats(oracle.quantize.dequantize(qg, sg, "e4m3", "tensor"), x.double().numpy())
+    pr = np.load(tmp_path / "probe.npy")
+    assert int(pr[2]) == st["count"] and abs(pr[1] - st["max_rel"]) <= 1e-12 * st["max_rel"]
+
+
+def test_shard_rows_partition():
+    for total in (0, 1, 7, 4096, 262144):
+        for world in (1, 2, 3, 4, 8):
+            spans = [ldist.shard_rows(total, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == total
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            assert max(b - a for a, b in spans) - min(b - a for a, b in spans) <= 1

@@ -1,0 +1,86 @@
+"""Multi-GPU check of the sharded tensorwise quantize (a9) over NCCL (one process per GPU):
+
+  torchrun --nproc-per-node N --master-addr 127.0.0.1 --master-port P tools/dist_check.py [rows cols]
+
+Every rank generates its row shard of one global heavy-tailed tensor (synth.heavy with row0 /
+total_rows), runs loka_quantize(AMAX_ONLY) -> NCCL all_reduce(MAX) -> loka_quantize(CAST) on its
+GPU, and the codes are gathered to rank 0, which requires them to be bit-identical to the single-
+GPU loka_quantize of the whole tensor and to the oracle on sampled rows.  Prints one JSON line.
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import synth  # noqa: E402
+import paper_2605_10886_b200 as lk  # noqa: E402
+from paper_2605_10886_b200 import dist as ldist  # noqa: E402
+
+
+def main():
+    rows = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
+    cols = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    r0, r1 = ldist.shard_rows(rows, world, rank)
+    x = synth.heavy(r1 - r0, cols, 3, device=dev, row0=r0, total_rows=rows)
+    # time the exchange step: amax kernel + all_reduce + cast kernel, CUDA events, max over ranks
+    for _ in range(3):
+        q, s, amax = ldist.quantize_tensorwise_sharded(x, "e4m3")
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+    e0.record()
+    reps = 20
+    for _ in range(reps):
+        q, s, amax = ldist.quantize_tensorwise_sharded(x, "e4m3")
+    e1.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1) / reps], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        gathered = [torch.empty(ldist.shard_rows(rows, world, r)[1] - ldist.shard_rows(rows, world, r)[0], cols,
+                                dtype=torch.uint8, device=dev) for r in range(world)]
+        dist.all_gather(gathered, q.contiguous())
+        scales = [torch.empty(1, dtype=torch.float32, device=dev) for _ in range(world)]
+        dist.all_gather(scales, s)
+    else:
+        gathered, scales = [q], [s]
+    ok = True
+    if rank == 0:
+        xg = synth.heavy(rows, cols, 3, device=dev)
+        qg, sg = lk.loka_quantize(xg, "e4m3", "tensor")
+        torch.cuda.synchronize()
+        ok &= all(int(sc.view(torch.int32)) == int(sg.view(torch.int32)) for sc in scales)
+        ok &= bool(torch.equal(torch.cat(gathered), qg))
+        import oracle  # test infrastructure: the oracle check on sampled rows
+        idx = torch.randperm(rows, generator=torch.Generator().manual_seed(0))[:32].sort().values
+        oq, os_ = oracle.quantize.quantize(xg[idx.to(dev)].cpu().double().numpy(), "e4m3", "tensor",
+                                           amax=np.array([float(amax)]))
+        ok &= bool(np.array_equal(qg[idx.to(dev)].cpu().numpy(), oq))
+        ok &= os_.view(np.uint32)[0] == sg.cpu().numpy().view(np.uint32)[0]
+        print(json.dumps({"world": world, "rows": rows, "cols": cols, "bit_identical": bool(ok),
+                          "sharded_tensorwise_quantize_ms": round(float(ms), 4),
+                          "gbps_per_gpu": round((r1 - r0) * cols * 3 * 2 / (float(ms) * 1e-3) / 1e9, 1),
+                          "note": "2 reads of x (amax + cast) + 1 write per element, max over ranks"}))
+    if world > 1:
+        dist.destroy_process_group()
+    if not ok:
+        sys.exit(1)
+
+
+if __name__ == "__main__":
+    main()
