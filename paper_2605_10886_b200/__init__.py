@@ -157,9 +157,10 @@ def loka_quantize(x: torch.Tensor, fmt: str = "e4m3", gran: str = "row", scale_f
         qt_codes = torch.empty(cols, rows, dtype=torch.uint8, device=dev)
         qt_scales = torch.empty(scale_shape(cols, rows, tg), dtype=torch.float32, device=dev)
         qt = _tensor(qt_codes, FMT[fmt], cols, rows, qt_scales, tg, scale_fmt)
-    ws = torch.empty(256, dtype=torch.uint8, device=dev)
+    nws = _lib.loka_quantize_workspace_size(C.byref(qx), C.byref(qq))
+    ws = torch.empty(nws, dtype=torch.uint8, device=dev)
     st = _lib.loka_quantize(C.byref(qx), C.byref(qq), None if qt is None else C.byref(qt), PHASE[phase],
-                            _ptr(amax), _ptr(status), _ptr(ws), 256, _stream(stream))
+                            _ptr(amax), _ptr(status), _ptr(ws), nws, _stream(stream))
     _check(st, "loka_quantize")
     if transpose:
         return (out if want_q else None), scales, qt_codes, qt_scales

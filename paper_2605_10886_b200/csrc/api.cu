@@ -138,7 +138,11 @@ int64_t loka_debug_hang_info(uint64_t* info3, int32_t reset) {
 }
 
 // ------------------------------------------------------------------------------------------
-size_t loka_quantize_workspace_size(const loka_tensor* /*x*/, const loka_tensor* /*q*/) { return 256; }
+size_t loka_quantize_workspace_size(const loka_tensor* x, const loka_tensor* /*q*/) {
+  // 256 B (tensorwise amax word) + the ROW / COL amax pre-pass array of the tiled path
+  const int64_t n = x ? (x->rows > x->cols ? x->rows : x->cols) : 0;
+  return 256 + (size_t)(n > 0 ? n : 0) * 4;
+}
 
 loka_status loka_quantize(const loka_tensor* x, loka_tensor* q, loka_tensor* qt, loka_phase phase, float* amax_dev,
                           int32_t* status_dev, void* ws, size_t ws_bytes, loka_stream_t stream) {
@@ -160,15 +164,21 @@ loka_status loka_quantize(const loka_tensor* x, loka_tensor* q, loka_tensor* qt,
       return LOKA_ERR_SHAPE;
     if (!qt->data || qt->ld < qt->cols) return LOKA_ERR_INVALID_ARG;
   }
-  // COL / 128x1 granules (per-column scales over all rows) are not implemented yet.
-  if (q->gran == LOKA_GRAN_COL || q->gran == LOKA_GRAN_BLK_128x1) return LOKA_ERR_UNSUPPORTED;
+  // the tiled cast(-transpose) path serves column-spanning granules and transposed copies
+  const bool tiled = (qt != nullptr || q->gran == LOKA_GRAN_COL || q->gran == LOKA_GRAN_BLK_128x1) &&
+                     phase != LOKA_PHASE_AMAX_ONLY;
   int sms = 148;
   loka_status st = check_device(&sms);
   if (st != LOKA_OK) return st;
   float* amax = amax_dev;
   if (q->gran == LOKA_GRAN_TENSOR && phase == LOKA_PHASE_FULL && !amax) {
-    if (!ws || ws_bytes < loka_quantize_workspace_size(x, q)) return LOKA_ERR_WORKSPACE;
+    if (!ws || ws_bytes < 256) return LOKA_ERR_WORKSPACE;
     amax = reinterpret_cast<float*>(ws);
+  }
+  void* pre = nullptr;  // ROW / COL amax pre-pass array of the tiled path
+  if (tiled && (q->gran == LOKA_GRAN_ROW || q->gran == LOKA_GRAN_COL)) {
+    if (!ws || ws_bytes < loka_quantize_workspace_size(x, q) || !aligned16(ws)) return LOKA_ERR_WORKSPACE;
+    pre = reinterpret_cast<uint8_t*>(ws) + 256;
   }
   QuantParams p;
   p.x = x->data;
@@ -182,8 +192,11 @@ loka_status loka_quantize(const loka_tensor* x, loka_tensor* q, loka_tensor* qt,
   p.ldqt = qt ? qt->ld : 0;
   p.scales_t = qt ? qt->scales : nullptr;
   p.status = status_dev;
-  cudaError_t e = launch_quantize(p, x->dtype == LOKA_BF16, q->dtype, q->scale_fmt, q->gran, phase, amax,
-                                  reinterpret_cast<cudaStream_t>(stream), sms);
+  cudaError_t e =
+      tiled ? launch_quantize_tiled(p, x->dtype == LOKA_BF16, q->dtype, q->scale_fmt, q->gran, phase, amax, pre,
+                                    reinterpret_cast<cudaStream_t>(stream))
+            : launch_quantize(p, x->dtype == LOKA_BF16, q->dtype, q->scale_fmt, q->gran, phase, amax,
+                              reinterpret_cast<cudaStream_t>(stream), sms);
   if (e == cudaErrorNotSupported) return LOKA_ERR_UNSUPPORTED;
   return e == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
 }

@@ -25,6 +25,11 @@ struct QuantParams {
 cudaError_t launch_quantize(const QuantParams& p, bool in_bf16, int fmt, int scale_fmt, int gran, int phase,
                             float* amax_dev, cudaStream_t st, int num_sms);
 
+// Tiled quantize (quantize_t.cu): any granularity incl. COL / BLK_128x1, optional transposed
+// copy; ws holds the ROW / COL amax pre-pass array (4 * max(rows, cols) bytes).
+cudaError_t launch_quantize_tiled(const QuantParams& p, bool in_bf16, int fmt, int scale_fmt, int gran, int phase,
+                                  float* amax_dev, void* ws, cudaStream_t st);
+
 constexpr int kMaxQuantGroup = 64;
 struct QuantGroup {
   int32_t G;

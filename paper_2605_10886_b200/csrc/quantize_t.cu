@@ -1,0 +1,318 @@
+// quantize_t.cu — a3: quantize with a K-major transposed copy (cast-transpose) and the column-
+// spanning granularities (COL, BLK_128x1) the backward directions need ("separate
+// optimization decisions for each direction", "RW GW HP"; D6):
+//   dgrad dX = dY W    : B operand = W^T (K-major over N) -> W quantized per COLUMN, written transposed
+//   wgrad dW = dY^T X  : A = dY^T, B = X^T (K-major over M) -> per COLUMN / 128x1, written transposed
+//
+// One CTA (256 threads) per 128 x 128 input tile: the tile is loaded with 16-byte loads into
+// registers (64 elements per thread), granule amax is reduced within the tile (1x128: half warp,
+// 128x1: per column across the tile, 128x128: whole CTA) or read from a pre-pass array
+// (TENSOR / ROW / COL span beyond one tile), codes are written row-major directly and the
+// transposed copy goes through a padded shared-memory tile so both layouts are written with
+// coalesced 128-byte rows.  Same arithmetic as quantize.cu (bit-identical codes and scales).
+#include "common.cuh"
+#include "launch.h"
+
+namespace loka {
+
+template <typename Tin> struct In8;
+template <> struct In8<__nv_bfloat16> {
+  static LOKA_DEVINL void load(const __nv_bfloat16* p, int n, float (&f)[8]) {
+    if (n == 8) {
+      const uint4 w = __ldg(reinterpret_cast<const uint4*>(p));
+      f[0] = bf16lo_to_f32(w.x); f[1] = bf16hi_to_f32(w.x); f[2] = bf16lo_to_f32(w.y); f[3] = bf16hi_to_f32(w.y);
+      f[4] = bf16lo_to_f32(w.z); f[5] = bf16hi_to_f32(w.z); f[6] = bf16lo_to_f32(w.w); f[7] = bf16hi_to_f32(w.w);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) f[i] = i < n ? __bfloat162float(p[i]) : 0.f;
+    }
+  }
+};
+template <> struct In8<float> {
+  static LOKA_DEVINL void load(const float* p, int n, float (&f)[8]) {
+    if (n == 8) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(p)), b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+      f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) f[i] = i < n ? p[i] : 0.f;
+    }
+  }
+};
+
+LOKA_DEVINL uint32_t absbits(float v) { return __float_as_uint(v) & 0x7FFFFFFFu; }
+
+// ---- pre-pass: per-row amax (bit patterns) ------------------------------------------------
+template <typename Tin>
+__global__ void __launch_bounds__(256) row_amax_kernel(QuantParams p, uint32_t* amax_row) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= p.rows) return;
+  const Tin* xr = reinterpret_cast<const Tin*>(p.x) + row * p.ldx;
+  uint32_t am = 0;
+  for (int64_t c = lane * 8; c < p.cols; c += 256) {
+    float f[8];
+    In8<Tin>::load(xr + c, (int)imin64(8, p.cols - c), f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) am = max(am, absbits(f[i]));
+  }
+  am = warp_max_u32(am);
+  if (lane == 0) amax_row[row] = am;
+  if (am >= 0x7F800000u && lane == 0 && p.status) atomicOr(p.status, LOKA_DEVSTATUS_NONFINITE);
+}
+
+// ---- pre-pass: per-column amax over all rows (atomicMax into a zeroed array) ---------------
+template <typename Tin>
+__global__ void __launch_bounds__(256) col_amax_kernel(QuantParams p, uint32_t* amax_col) {
+  pdl_wait();
+  __shared__ uint32_t red[8][128];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t c0 = (int64_t)blockIdx.x * 128, r0 = (int64_t)blockIdx.y * 128;
+  const int cl = (lane & 15) * 8;
+  uint32_t cm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t row = r0 + warp * 16 + i * 2 + (lane >> 4);
+    const int64_t c = c0 + cl;
+    if (row < p.rows && c < p.cols) {
+      float f[8];
+      In8<Tin>::load(reinterpret_cast<const Tin*>(p.x) + row * p.ldx + c, (int)imin64(8, p.cols - c), f);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) cm[k] = max(cm[k], absbits(f[k]));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) cm[k] = max(cm[k], __shfl_xor_sync(0xFFFFFFFFu, cm[k], 16));
+  if (lane < 16) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) red[warp][cl + k] = cm[k];
+  }
+  __syncthreads();
+  if (threadIdx.x < 128 && c0 + threadIdx.x < p.cols) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) m = max(m, red[w][threadIdx.x]);
+    if (m) atomicMax(&amax_col[c0 + threadIdx.x], m);
+    if (m >= 0x7F800000u && p.status) atomicOr(p.status, LOKA_DEVSTATUS_NONFINITE);
+  }
+}
+
+// ---- tile kernel: granule scales + cast + row-major and/or transposed codes ----------------
+// amax_g: pre-pass array for TENSOR ([1], float bits) / ROW ([rows]) / COL ([cols]); else null.
+template <typename Tin, int FMT, int SF>
+__global__ void __launch_bounds__(256) quant_tile_kernel(QuantParams p, int gran, const uint32_t* amax_g) {
+  pdl_wait();
+  __shared__ uint32_t red[8][128];
+  __shared__ uint8_t tq[128][128 + 8];  // codes tile for the transposed write (+8 B pad: <= 2-way conflicts)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t c0 = (int64_t)blockIdx.x * 128, r0 = (int64_t)blockIdx.y * 128;
+  const int64_t nbc = (p.cols + 127) / 128, nbr = (p.rows + 127) / 128;
+  const int cl = (lane & 15) * 8;  // local column of this lane's 8 elements
+  const int64_t c = c0 + cl;
+  const int nc = (int)max((int64_t)0, imin64(8, p.cols - c));
+  float v[8][8];  // [row iteration][element]
+  uint32_t rowm[8], colm[8] = {0, 0, 0, 0, 0, 0, 0, 0}, all = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t row = r0 + warp * 16 + i * 2 + (lane >> 4);
+    if (row < p.rows && nc > 0) In8<Tin>::load(reinterpret_cast<const Tin*>(p.x) + row * p.ldx + c, nc, v[i]);
+    else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[i][k] = 0.f;
+    }
+    uint32_t m = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t b = absbits(v[i][k]);
+      m = max(m, b);
+      colm[k] = max(colm[k], b);
+    }
+    rowm[i] = m;
+    all = max(all, m);
+  }
+  // ---- granule amax ----
+  // cast multiplier r per element = rrow[i] (row-like granules) or rcol[k] (column-like granules)
+  float rrow[8] = {1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f}, rcol[8] = {1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f};
+  const bool colwise = gran == LOKA_GRAN_BLK_128x1 || gran == LOKA_GRAN_COL;
+  if (gran == LOKA_GRAN_BLK_1x128) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      uint32_t m = rowm[i];
+#pragma unroll
+      for (int o = 8; o >= 1; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+      if (m >= 0x7F800000u && (lane & 15) == 0 && p.status) atomicOr(p.status, LOKA_DEVSTATUS_NONFINITE);
+      float s, r;
+      scales_from_amax<FMT, SF>(__uint_as_float(m), s, r);
+      const int64_t row = r0 + warp * 16 + i * 2 + (lane >> 4);
+      if ((lane & 15) == 0 && row < p.rows) {
+        if (p.scales) p.scales[row * nbc + blockIdx.x] = s;
+        if (p.scales_t) p.scales_t[(int64_t)blockIdx.x * p.rows + row] = s;  // t-frame BLK_128x1 [nbc, rows]
+      }
+      rrow[i] = r;
+    }
+  } else if (gran == LOKA_GRAN_BLK_128x1 || gran == LOKA_GRAN_BLK_128x128) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) colm[k] = max(colm[k], __shfl_xor_sync(0xFFFFFFFFu, colm[k], 16));
+    if (lane < 16) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) red[warp][cl + k] = colm[k];
+    }
+    __syncthreads();
+    if (gran == LOKA_GRAN_BLK_128x1) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        uint32_t m = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) m = max(m, red[w][cl + k]);
+        float s, r;
+        scales_from_amax<FMT, SF>(__uint_as_float(m), s, r);
+        rcol[k] = r;
+        if (warp == 0 && lane < 16 && k < nc) {
+          if (m >= 0x7F800000u && p.status) atomicOr(p.status, LOKA_DEVSTATUS_NONFINITE);
+          if (p.scales) p.scales[(int64_t)blockIdx.y * p.cols + c + k] = s;     // [nbr, cols]
+          if (p.scales_t) p.scales_t[(c + k) * nbr + blockIdx.y] = s;           // t-frame 1x128 [cols, nbr]
+        }
+      }
+    } else {
+      uint32_t m = 0;
+      for (int j = 0; j < 128; ++j) {
+#pragma unroll
+        for (int w = 0; w < 8; ++w) m = max(m, red[w][j]);
+      }
+      float s, r;
+      scales_from_amax<FMT, SF>(__uint_as_float(m), s, r);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) rrow[i] = r;
+      if (threadIdx.x == 0) {
+        if (m >= 0x7F800000u && p.status) atomicOr(p.status, LOKA_DEVSTATUS_NONFINITE);
+        if (p.scales) p.scales[(int64_t)blockIdx.y * nbc + blockIdx.x] = s;
+        if (p.scales_t) p.scales_t[(int64_t)blockIdx.x * nbr + blockIdx.y] = s;
+      }
+    }
+  } else {  // TENSOR / ROW / COL from the pre-pass array
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int64_t row = r0 + warp * 16 + i * 2 + (lane >> 4);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        uint32_t m;
+        if (gran == LOKA_GRAN_TENSOR) m = amax_g[0];
+        else if (gran == LOKA_GRAN_ROW) m = row < p.rows ? amax_g[row] : 0u;
+        else m = (k < nc) ? amax_g[c + k] : 0u;
+        float s, r;
+        scales_from_amax<FMT, SF>(__uint_as_float(m), s, r);
+        if (gran == LOKA_GRAN_COL) rcol[k] = r;
+        else rrow[i] = r;
+        // scales: ROW by the lane holding column 0 of the tile row; COL by row-block 0; TENSOR once
+        if (gran == LOKA_GRAN_ROW && k == 0 && cl == 0 && blockIdx.x == 0 && row < p.rows) {
+          if (p.scales) p.scales[row] = s;
+          if (p.scales_t) p.scales_t[row] = s;
+        } else if (gran == LOKA_GRAN_COL && i == 0 && warp == 0 && lane < 16 && blockIdx.y == 0 && k < nc) {
+          if (p.scales) p.scales[c + k] = s;
+          if (p.scales_t) p.scales_t[c + k] = s;
+        } else if (gran == LOKA_GRAN_TENSOR && threadIdx.x == 0 && i == 0 && k == 0 && blockIdx.x == 0 &&
+                   blockIdx.y == 0) {
+          if (p.scales) p.scales[0] = s;
+          if (p.scales_t) p.scales_t[0] = s;
+        }
+      }
+    }
+  }
+  // ---- cast; row-major codes straight to global, transposed through smem ----
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    float f[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) f[k] = __fmul_rn(v[i][k], colwise ? rcol[k] : rrow[i]);
+    const uint32_t lo = cvt_fp8x4<FMT>(f[0], f[1], f[2], f[3]), hi = cvt_fp8x4<FMT>(f[4], f[5], f[6], f[7]);
+    const int lr = warp * 16 + i * 2 + (lane >> 4);
+    const int64_t row = r0 + lr;
+    if (p.q && row < p.rows && nc > 0) {
+      uint8_t* dst = p.q + row * p.ldq + c;
+      if (nc == 8) *reinterpret_cast<uint2*>(dst) = make_uint2(lo, hi);
+      else
+        for (int k = 0; k < nc; ++k) dst[k] = (uint8_t)((k < 4 ? lo : hi) >> (8 * (k & 3)));
+    }
+    if (p.qt) *reinterpret_cast<uint2*>(&tq[lr][cl]) = make_uint2(lo, hi);
+  }
+  if (p.qt) {
+    __syncthreads();
+    // qt row (c0 + j) = column j of the tile: 128 codes from tq[0..127][j]; thread t writes 8
+    // consecutive codes (rows 8*(t&15) .. +7) of transposed row j = t >> 4 (+16 per pass)
+    const int t = threadIdx.x;
+    for (int j = t >> 4; j < 128; j += 16) {
+      const int64_t orow = c0 + j;
+      const int rb = (t & 15) * 8;
+      if (orow >= p.cols || r0 + rb >= p.rows) continue;
+      uint32_t w0 = 0, w1 = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) w0 |= (uint32_t)tq[rb + k][j] << (8 * k);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) w1 |= (uint32_t)tq[rb + 4 + k][j] << (8 * k);
+      uint8_t* dst = p.qt + orow * p.ldqt + r0 + rb;
+      const int nr = (int)imin64(8, p.rows - (r0 + rb));
+      if (nr == 8 && ((reinterpret_cast<uintptr_t>(dst) & 7) == 0)) *reinterpret_cast<uint2*>(dst) = make_uint2(w0, w1);
+      else
+        for (int k = 0; k < nr; ++k) dst[k] = (uint8_t)((k < 4 ? w0 : w1) >> (8 * (k & 3)));
+    }
+  }
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl_t(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  note_launch();
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+template <typename Tin, int FMT, int SF>
+static cudaError_t launch_tiled_t(const QuantParams& p, int gran, int phase, float* amax_dev, void* ws,
+                                  cudaStream_t st) {
+  const dim3 tiles((unsigned)((p.cols + 127) / 128), (unsigned)((p.rows + 127) / 128));
+  uint32_t* amax = nullptr;
+  cudaError_t e = cudaSuccess;
+  if (gran == LOKA_GRAN_TENSOR) {
+    amax = reinterpret_cast<uint32_t*>(amax_dev);
+    if (phase != LOKA_PHASE_CAST_WITH_AMAX)  // FULL (AMAX_ONLY is handled by quantize.cu alone)
+      e = launch_quantize(p, sizeof(Tin) == 2, FMT, SF, LOKA_GRAN_TENSOR, LOKA_PHASE_AMAX_ONLY, amax_dev, st, 148);
+  } else if (gran == LOKA_GRAN_ROW) {
+    amax = reinterpret_cast<uint32_t*>(ws);
+    e = launch_pdl_t(row_amax_kernel<Tin>, dim3((unsigned)((p.rows + 7) / 8)), dim3(256), st, p, amax);
+  } else if (gran == LOKA_GRAN_COL) {
+    amax = reinterpret_cast<uint32_t*>(ws);
+    e = cudaMemsetAsync(amax, 0, (size_t)p.cols * 4, st);
+    if (e == cudaSuccess) e = launch_pdl_t(col_amax_kernel<Tin>, tiles, dim3(256), st, p, amax);
+  }
+  if (e != cudaSuccess) return e;
+  return launch_pdl_t(quant_tile_kernel<Tin, FMT, SF>, tiles, dim3(256), st, p, gran, (const uint32_t*)amax);
+}
+
+cudaError_t launch_quantize_tiled(const QuantParams& p, bool in_bf16, int fmt, int scale_fmt, int gran, int phase,
+                                  float* amax_dev, void* ws, cudaStream_t st) {
+#define LOKA_T(T, F, S) \
+  if (fmt == F && scale_fmt == S) return launch_tiled_t<T, F, S>(p, gran, phase, amax_dev, ws, st);
+  if (in_bf16) {
+    LOKA_T(__nv_bfloat16, LOKA_E4M3, LOKA_SCALE_F32)
+    LOKA_T(__nv_bfloat16, LOKA_E4M3, LOKA_SCALE_UE8M0)
+    LOKA_T(__nv_bfloat16, LOKA_E5M2, LOKA_SCALE_F32)
+    LOKA_T(__nv_bfloat16, LOKA_E5M2, LOKA_SCALE_UE8M0)
+  } else {
+    LOKA_T(float, LOKA_E4M3, LOKA_SCALE_F32)
+    LOKA_T(float, LOKA_E4M3, LOKA_SCALE_UE8M0)
+    LOKA_T(float, LOKA_E5M2, LOKA_SCALE_F32)
+    LOKA_T(float, LOKA_E5M2, LOKA_SCALE_UE8M0)
+  }
+#undef LOKA_T
+  return cudaErrorNotSupported;
+}
+
+}  // namespace loka

@@ -24,7 +24,7 @@ def _inputs(rows, cols, dtype, seed):
 
 
 @pytest.mark.parametrize("shape", SHAPES)
-@pytest.mark.parametrize("gran", ["row", "blk_1x128", "blk_128x128", "tensor"])
+@pytest.mark.parametrize("gran", ["row", "col", "blk_1x128", "blk_128x1", "blk_128x128", "tensor"])
 @pytest.mark.parametrize("fmt", ["e4m3", "e5m2"])
 @pytest.mark.parametrize("scale_fmt", ["f32", "ue8m0"])
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
@@ -53,19 +53,25 @@ def test_tensorwise_split_phase_and_strided_input():
     assert_bytes_equal(q, oq)
 
 
-@pytest.mark.parametrize("gran", ["row", "blk_1x128", "blk_128x128", "tensor"])
-def test_transposed_copy(gran):
-    x = synth.gaussian(130, 272, 9)
+@pytest.mark.parametrize("gran", ["row", "col", "blk_1x128", "blk_128x1", "blk_128x128", "tensor"])
+@pytest.mark.parametrize("shape", [(130, 272), (256, 384), (300, 100)])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_transposed_copy(gran, shape, dtype):
+    """a3 cast-transpose: the K-major copy for dgrad / wgrad holds the same codes transposed and the
+    scales in the transposed frame (ROW<->COL, 1x128<->128x1)."""
+    rows, cols = shape
+    x = synth.heavy(rows, cols, 9).to(dtype)
     q, s, qt, st = lk.loka_quantize(to_dev_padded(x), "e5m2", gran, transpose=True)
     torch.cuda.synchronize()
     oq, os_ = oracle.quantize.quantize(x.double().numpy(), "e5m2", gran)
+    assert_scales_equal(s, os_)
     assert_bytes_equal(q, oq)
     assert_bytes_equal(qt, oq.T.copy())
-    tg = {"row": "col", "blk_1x128": "blk_128x1"}.get(gran, gran)
-    ts = os_.reshape(lk.scale_shape(130, 272, gran))
-    if gran in ("blk_1x128", "blk_128x128"):
+    tg = {"row": "col", "col": "row", "blk_1x128": "blk_128x1", "blk_128x1": "blk_1x128"}.get(gran, gran)
+    ts = os_.reshape(lk.scale_shape(rows, cols, gran))
+    if gran in ("blk_1x128", "blk_128x1", "blk_128x128"):
         ts = ts.T
-    assert_scales_equal(st, np.ascontiguousarray(ts).reshape(lk.scale_shape(272, 130, tg)))
+    assert_scales_equal(st, np.ascontiguousarray(ts).reshape(lk.scale_shape(cols, rows, tg)))
 
 
 def test_nonfinite_sets_status():
