@@ -139,8 +139,11 @@ LOKA_API loka_status loka_quantize_grouped(int32_t G, const loka_tensor* x, loka
 typedef struct loka_linear_args {
   int64_t M, N, K;
   loka_direction dir;       /* metadata; see loka_direction                                   */
-  loka_tensor a;            /* e4m3/e5m2 [M,K] K-major, scales gran TENSOR | ROW              */
-  loka_tensor b;            /* e4m3/e5m2 [N,K] K-major, scales gran TENSOR | ROW              */
+  loka_tensor a;            /* e4m3/e5m2 [M,K] K-major, scales gran TENSOR | ROW | BLK_1x128  */
+  loka_tensor b;            /* e4m3/e5m2 [N,K] K-major, scales gran TENSOR | ROW, or with a
+                               BLK_1x128 A: BLK_128x128 | BLK_1x128 (blockwise recipe, FP32
+                               promotion per 128-K block; epilogue NONE (+bias), FP8 output
+                               only for N <= 128)                                             */
   const void* bias;         /* nullable [N], dtype bias_dtype (F32 | BF16); added before norm */
   loka_dtype bias_dtype;
   loka_norm norm;

@@ -332,7 +332,64 @@ static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CU
   return LOKA_OK;
 }
 
+// Blockwise recipe (BW-F32, D6/D7): A scales 1x128, B scales 128x128 (or 1x128 for the
+// K-major copies of wgrad); FP32 promotion per 128-K block (blockwise.cu).  Epilogue: (+bias),
+// f32 / bf16 output, or FP8 with row scales when N <= 128.
+static bool is_blockwise(const loka_linear_args* a) { return a && a->a.gran == LOKA_GRAN_BLK_1x128; }
+
+static loka_status prepare_bw(const loka_linear_args* a, CUtensorMap* ta, CUtensorMap* tb, CUtensorMap* ty,
+                              BwParams* p) {
+  const int64_t M = a->M, N = a->N, K = a->K;
+  if (M <= 0 || N <= 0 || K <= 0 || M > (1ll << 31) - 1 || N > (1ll << 30) || K > (1ll << 31) - 1)
+    return LOKA_ERR_SHAPE;
+  const loka_tensor &A = a->a, &B = a->b, &Y = a->y;
+  if (!is_fp8(A.dtype) || !is_fp8(B.dtype)) return LOKA_ERR_INVALID_ARG;
+  if (A.rows != M || A.cols != K || B.rows != N || B.cols != K || Y.rows != M || Y.cols != N) return LOKA_ERR_SHAPE;
+  if (!A.data || !B.data || !Y.data || !A.scales || !B.scales) return LOKA_ERR_INVALID_ARG;
+  if (!aligned16(A.data) || !aligned16(B.data) || !aligned16(Y.data)) return LOKA_ERR_INVALID_ARG;
+  if (A.ld < K || B.ld < K || A.ld % 16 || B.ld % 16) return LOKA_ERR_INVALID_ARG;
+  if (B.gran != LOKA_GRAN_BLK_128x128 && B.gran != LOKA_GRAN_BLK_1x128) return LOKA_ERR_UNSUPPORTED;
+  if (Y.dtype < LOKA_F32 || Y.dtype > LOKA_E5M2) return LOKA_ERR_INVALID_ARG;
+  if (Y.ld < N || (Y.ld * elem_size(Y.dtype)) % 16) return LOKA_ERR_INVALID_ARG;
+  const bool fp8_out = is_fp8(Y.dtype);
+  if (fp8_out && (!Y.scales || Y.gran != LOKA_GRAN_ROW || N > 128)) return LOKA_ERR_UNSUPPORTED;
+  if (a->norm != LOKA_NORM_NONE || a->gamma || a->beta) return LOKA_ERR_UNSUPPORTED;
+  if (a->bias && a->bias_dtype != LOKA_F32 && a->bias_dtype != LOKA_BF16) return LOKA_ERR_INVALID_ARG;
+  if (!make_map_u8(ta, A.data, M, K, A.ld, 128)) return LOKA_ERR_CUDA;
+  if (!make_map_u8(tb, B.data, N, K, B.ld, 128)) return LOKA_ERR_CUDA;
+  if (!make_map_out(ty, Y.data, M, N, Y.ld, Y.dtype, 128)) return LOKA_ERR_CUDA;
+  std::memset(p, 0, sizeof(*p));
+  p->M = (int32_t)M;
+  p->N = (int32_t)N;
+  p->K = (int32_t)K;
+  p->a_fmt = A.dtype == LOKA_E5M2 ? 1 : 0;
+  p->b_fmt = B.dtype == LOKA_E5M2 ? 1 : 0;
+  p->sa = A.scales;
+  p->sa_ld = (int32_t)cdiv(K, 128);
+  p->sb = B.scales;
+  p->sb_ld = (int32_t)cdiv(K, 128);
+  p->sb_rows = B.gran == LOKA_GRAN_BLK_1x128;
+  p->bias = a->bias;
+  p->bias_bf16 = a->bias_dtype == LOKA_BF16;
+  p->out_dtype = Y.dtype;
+  p->y_scales = fp8_out ? Y.scales : nullptr;
+  p->precast = a->debug_precast;
+  p->ld_pre = N;
+  return LOKA_OK;
+}
+
+static loka_status run_bw(const loka_linear_args* a, cudaStream_t s) {
+  CUtensorMap ta, tb, ty;
+  BwParams p;
+  loka_status st = prepare_bw(a, &ta, &tb, &ty, &p);
+  if (st != LOKA_OK) return st;
+  st = check_device();
+  if (st != LOKA_OK) return st;
+  return launch_linear_bw(ta, tb, ty, p, s) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
+}
+
 loka_status loka_fp8_linear_norm(const loka_linear_args* a, void* /*ws*/, size_t /*ws_bytes*/, loka_stream_t stream) {
+  if (is_blockwise(a)) return run_bw(a, reinterpret_cast<cudaStream_t>(stream));
   CUtensorMap ta, tb, ty;
   LinearParams p;
   int bn = 0;
@@ -353,7 +410,9 @@ loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* 
   std::vector<LinearParams> p(G);
   std::vector<int> bn(G);
   for (int g = 0; g < G; ++g) {  // full validation of every problem before any launch
-    loka_status st = prepare_linear(&a[g], &ta[g], &tb[g], &ty[g], &p[g], &bn[g]);
+    BwParams bw;
+    loka_status st = is_blockwise(&a[g]) ? prepare_bw(&a[g], &ta[g], &tb[g], &ty[g], &bw)
+                                          : prepare_linear(&a[g], &ta[g], &tb[g], &ty[g], &p[g], &bn[g]);
     if (st != LOKA_OK) return st;
   }
   int sms = 148;
@@ -367,7 +426,8 @@ loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* 
   // output) keep their own fused linear_norm launches.
   std::vector<int> grouped, single;
   for (int g = 0; g < G; ++g) {
-    const bool ok = a[g].norm == LOKA_NORM_NONE && a[g].y.dtype == LOKA_BF16 && !a[g].debug_precast;
+    const bool ok = a[g].norm == LOKA_NORM_NONE && a[g].y.dtype == LOKA_BF16 && !a[g].debug_precast &&
+                    !is_blockwise(&a[g]);
     (ok ? grouped : single).push_back(g);
   }
   std::stable_sort(grouped.begin(), grouped.end(), [&](int x, int y) { return a[x].K > a[y].K; });
@@ -400,6 +460,11 @@ loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* 
     if (launch_grouped(gp, sms, s) != cudaSuccess) return LOKA_ERR_CUDA;
   }
   for (int g : single) {
+    if (is_blockwise(&a[g])) {
+      loka_status sb = run_bw(&a[g], s);
+      if (sb != LOKA_OK) return sb;
+      continue;
+    }
     cudaError_t e = launch_linear(ta[g], tb[g], ty[g], p[g], bn[g], s);
     if (e != cudaSuccess) return LOKA_ERR_CUDA;
   }

@@ -64,6 +64,21 @@ struct LinearParams {
 cudaError_t launch_linear(const CUtensorMap& tma_a, const CUtensorMap& tma_b, const CUtensorMap& tma_y,
                           const LinearParams& p, int bn, cudaStream_t st);
 
+// ---- blockwise-scaled GEMM with FP32 promotion (blockwise.cu) ----
+struct BwParams {
+  int32_t M, N, K;
+  int32_t a_fmt, b_fmt;
+  const float* sa; int32_t sa_ld;   // A: 1x128 scales [M, ceil(K/128)]
+  const float* sb; int32_t sb_ld;   // B: 128x128 [ceil(N/128), ceil(K/128)] or 1x128 [N, ceil(K/128)]
+  int32_t sb_rows;                  // 1: B scales are 1x128 (per row of B)
+  const void* bias; int32_t bias_bf16;
+  int32_t out_dtype;
+  float* y_scales;                  // FP8 output ROW scales (N <= 128)
+  float* precast; int64_t ld_pre;
+};
+cudaError_t launch_linear_bw(const CUtensorMap& tma_a, const CUtensorMap& tma_b, const CUtensorMap& tma_y,
+                             const BwParams& p, cudaStream_t st);
+
 // ---- grouped persistent launch (grouped.cu) ----
 constexpr int kMaxGroups = 32;  // per launch (kernel-parameter space: 3 tensor maps per group)
 struct GroupDesc {
