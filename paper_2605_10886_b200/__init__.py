@@ -154,7 +154,8 @@ def loka_quantize(x: torch.Tensor, fmt: str = "e4m3", gran: str = "row", scale_f
     qt_codes = qt_scales = None
     if transpose:
         tg = _T_GRAN.get(gran, gran)
-        qt_codes = torch.empty(cols, rows, dtype=torch.uint8, device=dev)
+        # K-major copy for the backward GEMMs: leading dimension padded to 16 bytes (TMA)
+        qt_codes = torch.empty(cols, (rows + 15) // 16 * 16, dtype=torch.uint8, device=dev)[:, :rows]
         qt_scales = torch.empty(scale_shape(cols, rows, tg), dtype=torch.float32, device=dev)
         qt = _tensor(qt_codes, FMT[fmt], cols, rows, qt_scales, tg, scale_fmt)
     nws = _lib.loka_quantize_workspace_size(C.byref(qx), C.byref(qq))
