@@ -139,7 +139,8 @@ _T_GRAN = {"row": "col", "col": "row", "blk_1x128": "blk_128x1", "blk_128x1": "b
 def loka_quantize(x: torch.Tensor, fmt: str = "e4m3", gran: str = "row", scale_fmt: str = "f32",
                   phase: str = "full", amax: torch.Tensor | None = None, status: torch.Tensor | None = None,
                   out: torch.Tensor | None = None, scales: torch.Tensor | None = None, want_q: bool = True,
-                  transpose: bool = False, stream=None):
+                  transpose: bool = False, out_t: torch.Tensor | None = None, scales_t: torch.Tensor | None = None,
+                  stream=None):
     """a1-a3.  Returns (codes uint8 [rows, cols] or None, scales fp32) [+ (codes_t, scales_t)]."""
     rows, cols = x.shape
     dev = x.device
@@ -155,8 +156,10 @@ def loka_quantize(x: torch.Tensor, fmt: str = "e4m3", gran: str = "row", scale_f
     if transpose:
         tg = _T_GRAN.get(gran, gran)
         # K-major copy for the backward GEMMs: leading dimension padded to 16 bytes (TMA)
-        qt_codes = torch.empty(cols, (rows + 15) // 16 * 16, dtype=torch.uint8, device=dev)[:, :rows]
-        qt_scales = torch.empty(scale_shape(cols, rows, tg), dtype=torch.float32, device=dev)
+        qt_codes = out_t if out_t is not None else \
+            torch.empty(cols, (rows + 15) // 16 * 16, dtype=torch.uint8, device=dev)[:, :rows]
+        qt_scales = scales_t if scales_t is not None else \
+            torch.empty(scale_shape(cols, rows, tg), dtype=torch.float32, device=dev)
         qt = _tensor(qt_codes, FMT[fmt], cols, rows, qt_scales, tg, scale_fmt)
     nws = _lib.loka_quantize_workspace_size(C.byref(qx), C.byref(qq))
     ws = torch.empty(nws, dtype=torch.uint8, device=dev)

@@ -22,8 +22,8 @@ constexpr int kWCPT = kWBN / 2;
 constexpr int kWStageBytes = 128 * 128 + kWBN * 128;
 constexpr int kWStages = 5;
 constexpr int kWOffOut = kWStages * kWStageBytes;            // staging tile (<= 128 x 128 f32 = 64 KB)
-constexpr int kWOffRed = kWOffOut + 128 * kWBN * 4;          // [2][128] row amax halves
-constexpr int kWOffBar = kWOffRed + 2 * 128 * 4;
+constexpr int kWOffRed = kWOffOut + 128 * kWBN * 4;          // [3][128]: B row scales / row amax halves
+constexpr int kWOffBar = kWOffRed + 3 * 128 * 4;
 constexpr int kWSmem = kWOffBar + 256 + 1024;
 static_assert(kWSmem <= 227 * 1024, "blockwise smem");
 
@@ -103,8 +103,23 @@ __global__ void __launch_bounds__(kWThreads, 1)
     float y[kWCPT];
 #pragma unroll
     for (int j = 0; j < kWCPT; ++j) y[j] = 0.f;
+    // per-row B scales (1x128 K-major copies): the CTA's 128 scales of k-block kb are staged in
+    // smem (triple-buffered, one k-block ahead) instead of 64 strided global loads per thread
+    float* sbs = red;  // [3][128] (red is reused for the FP8 row amax only after the loop)
+    const int te = threadIdx.x - 64;
+    auto stage_sb = [&](int kb) {
+      if (te < 128) {
+        const int n = n0 + te;
+        sbs[(kb % 3) * 128 + te] = n < p.N ? __ldg(p.sb + (int64_t)n * p.sb_ld + kb) : 0.f;
+      }
+    };
+    if (p.sb_rows) stage_sb(0);
     for (int kb = 0; kb < nkb; ++kb) {
       const int buf = kb & 1;
+      if (p.sb_rows) {
+        if (kb + 1 < nkb) stage_sb(kb + 1);
+        named_bar_sync(1, 32 * kWEpiWarps);  // kb's scales visible; kb-2's buffer no longer read
+      }
       // scales of this k-block (issued before the wait to hide their latency)
       const float sa = row_ok ? __ldg(p.sa + (int64_t)grow * p.sa_ld + kb) : 0.f;
       float sbk = 0.f;
@@ -130,20 +145,21 @@ __global__ void __launch_bounds__(kWThreads, 1)
           y[j] = t.x;
           y[j + 1] = t.y;
         }
-      } else {  // per-row scales of B (1x128 K-major copy): s_b[n, kb]
+      } else {  // per-row scales of B (1x128 K-major copy): s_b[n, kb] from the staged smem copy
+        const uint32_t sbase = smem_u32(sbs + (kb % 3) * 128 + cb);
+        const float2 sa2 = make_float2(sa, sa);
 #pragma unroll
-        for (int j = 0; j < kWCPT; j += 2) {
-          const int n = n0 + cb + j;
-          const float b0 = n < p.N ? __ldg(p.sb + (int64_t)n * p.sb_ld + kb) : 0.f;
-          const float b1 = n + 1 < p.N ? __ldg(p.sb + (int64_t)(n + 1) * p.sb_ld + kb) : 0.f;
-          const float2 t = ffma2(make_float2(part[j], part[j + 1]), make_float2(sa * b0, sa * b1),
-                                 make_float2(y[j], y[j + 1]));
-          y[j] = t.x;
-          y[j + 1] = t.y;
+        for (int j = 0; j < kWCPT; j += 4) {
+          const float4 b4 = lds_f4(sbase + j * 4);
+          const float2 s01 = fmul2(sa2, make_float2(b4.x, b4.y)), s23 = fmul2(sa2, make_float2(b4.z, b4.w));
+          const float2 t0 = ffma2(make_float2(part[j], part[j + 1]), s01, make_float2(y[j], y[j + 1]));
+          const float2 t1 = ffma2(make_float2(part[j + 2], part[j + 3]), s23, make_float2(y[j + 2], y[j + 3]));
+          y[j] = t0.x; y[j + 1] = t0.y; y[j + 2] = t1.x; y[j + 3] = t1.y;
         }
       }
     }
     (void)nblk_b;
+    if (p.sb_rows) named_bar_sync(1, 32 * kWEpiWarps);  // sbs (aliasing red) fully consumed
     // ---- bias, optional FP8 cast with row scale, TMA store ----
     const int nv = max(0, min(kWCPT, p.N - (n0 + cb)));
     if (p.bias) {

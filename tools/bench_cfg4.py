@@ -78,13 +78,18 @@ def main():
             one = lambda ar: (lambda: lk._lib.loka_fp8_linear_norm(ctypes.byref(ar), None, 0, sh))
             t_f, t_d, t_w = tmean(one(fa)), tmean(one(da)), tmean(one(wa))
 
-            def step():  # every quantize (+ transposed copies) and the three GEMMs
-                lk.loka_quantize(x, "e4m3", g["fx"], out=xq, scales=xs)
-                lk.loka_quantize(w, "e4m3", g["fw"], out=wq, scales=ws)
-                lk.loka_quantize(dy, "e5m2", g["gdy"], out=gq, scales=gs)
-                lk.loka_quantize(w, "e4m3", g["gw"], want_q=False, transpose=True)
-                lk.loka_quantize(dy, "e5m2", g["wdy"], want_q=False, transpose=True)
-                lk.loka_quantize(x, "e4m3", g["wx"], want_q=False, transpose=True)
+            def quant(src, fmt, g_plain, g_t, q, s, qt, st):
+                # one pass writes both layouts when the two directions share the granules
+                if g_plain == g_t:
+                    lk.loka_quantize(src, fmt, g_plain, out=q, scales=s, transpose=True, out_t=qt, scales_t=st)
+                else:
+                    lk.loka_quantize(src, fmt, g_plain, out=q, scales=s)
+                    lk.loka_quantize(src, fmt, g_t, want_q=False, transpose=True, out_t=qt, scales_t=st)
+
+            def step():  # every quantize (incl. the K-major copies) and the three GEMMs
+                quant(x, "e4m3", g["fx"], g["wx"], xq, xs, xtq, xts)
+                quant(w, "e4m3", g["fw"], g["gw"], wq, ws, wtq, wts)
+                quant(dy, "e5m2", g["gdy"], g["wdy"], gq, gs, gtq, gts)
                 for ar in (fa, da, wa):
                     assert lk._lib.loka_fp8_linear_norm(ctypes.byref(ar), None, 0, sh) == 0
 
