@@ -42,6 +42,36 @@ template <> struct In8<float> {
 
 LOKA_DEVINL uint32_t absbits(float v) { return __float_as_uint(v) & 0x7FFFFFFFu; }
 
+// 8 input elements kept in their storage form (bf16: 4 registers) until the cast.
+template <typename Tin> struct Raw8;
+template <> struct Raw8<__nv_bfloat16> {
+  uint32_t w[4];
+  LOKA_DEVINL void load(const __nv_bfloat16* p, int n) {
+    if (n == 8) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+      w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+    } else {
+      const uint16_t* h = reinterpret_cast<const uint16_t*>(p);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        w[i] = (2 * i < n ? h[2 * i] : 0u) | ((2 * i + 1 < n ? (uint32_t)h[2 * i + 1] : 0u) << 16);
+    }
+  }
+  LOKA_DEVINL void zero() { w[0] = w[1] = w[2] = w[3] = 0u; }
+  LOKA_DEVINL float f(int k) const { return (k & 1) ? bf16hi_to_f32(w[k >> 1]) : bf16lo_to_f32(w[k >> 1]); }
+  LOKA_DEVINL uint32_t abits(int k) const { return absbits(f(k)); }
+};
+template <> struct Raw8<float> {
+  float v[8];
+  LOKA_DEVINL void load(const float* p, int n) { In8<float>::load(p, n, v); }
+  LOKA_DEVINL void zero() {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = 0.f;
+  }
+  LOKA_DEVINL float f(int k) const { return v[k]; }
+  LOKA_DEVINL uint32_t abits(int k) const { return absbits(v[k]); }
+};
+
 // ---- pre-pass: per-row amax (bit patterns) ------------------------------------------------
 template <typename Tin>
 __global__ void __launch_bounds__(256) row_amax_kernel(QuantParams p, uint32_t* amax_row) {
@@ -101,7 +131,7 @@ __global__ void __launch_bounds__(256) col_amax_kernel(QuantParams p, uint32_t* 
 // ---- tile kernel: granule scales + cast + row-major and/or transposed codes ----------------
 // amax_g: pre-pass array for TENSOR ([1], float bits) / ROW ([rows]) / COL ([cols]); else null.
 template <typename Tin, int FMT, int SF>
-__global__ void __launch_bounds__(256) quant_tile_kernel(QuantParams p, int gran, const uint32_t* amax_g) {
+__global__ void __launch_bounds__(256, 2) quant_tile_kernel(QuantParams p, int gran, const uint32_t* amax_g) {
   pdl_wait();
   __shared__ uint32_t red[8][128];
   __shared__ uint8_t tq[128][128 + 8];  // codes tile for the transposed write (+8 B pad: <= 2-way conflicts)
@@ -111,25 +141,24 @@ __global__ void __launch_bounds__(256) quant_tile_kernel(QuantParams p, int gran
   const int cl = (lane & 15) * 8;  // local column of this lane's 8 elements
   const int64_t c = c0 + cl;
   const int nc = (int)max((int64_t)0, imin64(8, p.cols - c));
-  float v[8][8];  // [row iteration][element]
-  uint32_t rowm[8], colm[8] = {0, 0, 0, 0, 0, 0, 0, 0}, all = 0;
+  Raw8<Tin> v[8];  // [row iteration], 8 elements each, storage form
+  uint32_t rowm[8], colm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int64_t row = r0 + warp * 16 + i * 2 + (lane >> 4);
-    if (row < p.rows && nc > 0) In8<Tin>::load(reinterpret_cast<const Tin*>(p.x) + row * p.ldx + c, nc, v[i]);
-    else {
+    if (row < p.rows && nc > 0) v[i].load(reinterpret_cast<const Tin*>(p.x) + row * p.ldx + c, nc);
+    else v[i].zero();
+  }
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v[i][k] = 0.f;
-    }
+  for (int i = 0; i < 8; ++i) {
     uint32_t m = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const uint32_t b = absbits(v[i][k]);
+      const uint32_t b = v[i].abits(k);
       m = max(m, b);
       colm[k] = max(colm[k], b);
     }
     rowm[i] = m;
-    all = max(all, m);
   }
   // ---- granule amax ----
   // cast multiplier r per element = rrow[i] (row-like granules) or rcol[k] (column-like granules)
@@ -190,32 +219,36 @@ __global__ void __launch_bounds__(256) quant_tile_kernel(QuantParams p, int gran
         if (p.scales_t) p.scales_t[(int64_t)blockIdx.x * nbr + blockIdx.y] = s;
       }
     }
-  } else {  // TENSOR / ROW / COL from the pre-pass array
+  } else if (gran == LOKA_GRAN_TENSOR) {  // from the pre-pass amax word
+    float s, r;
+    scales_from_amax<FMT, SF>(__uint_as_float(amax_g[0]), s, r);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) rrow[i] = r;
+    if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
+      if (p.scales) p.scales[0] = s;
+      if (p.scales_t) p.scales_t[0] = s;
+    }
+  } else if (gran == LOKA_GRAN_ROW) {  // from the pre-pass row amax array
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int64_t row = r0 + warp * 16 + i * 2 + (lane >> 4);
+      float s, r;
+      scales_from_amax<FMT, SF>(__uint_as_float(row < p.rows ? amax_g[row] : 0u), s, r);
+      rrow[i] = r;
+      if (cl == 0 && blockIdx.x == 0 && row < p.rows) {
+        if (p.scales) p.scales[row] = s;
+        if (p.scales_t) p.scales_t[row] = s;
+      }
+    }
+  } else {  // COL from the pre-pass column amax array
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        uint32_t m;
-        if (gran == LOKA_GRAN_TENSOR) m = amax_g[0];
-        else if (gran == LOKA_GRAN_ROW) m = row < p.rows ? amax_g[row] : 0u;
-        else m = (k < nc) ? amax_g[c + k] : 0u;
-        float s, r;
-        scales_from_amax<FMT, SF>(__uint_as_float(m), s, r);
-        if (gran == LOKA_GRAN_COL) rcol[k] = r;
-        else rrow[i] = r;
-        // scales: ROW by the lane holding column 0 of the tile row; COL by row-block 0; TENSOR once
-        if (gran == LOKA_GRAN_ROW && k == 0 && cl == 0 && blockIdx.x == 0 && row < p.rows) {
-          if (p.scales) p.scales[row] = s;
-          if (p.scales_t) p.scales_t[row] = s;
-        } else if (gran == LOKA_GRAN_COL && i == 0 && warp == 0 && lane < 16 && blockIdx.y == 0 && k < nc) {
-          if (p.scales) p.scales[c + k] = s;
-          if (p.scales_t) p.scales_t[c + k] = s;
-        } else if (gran == LOKA_GRAN_TENSOR && threadIdx.x == 0 && i == 0 && k == 0 && blockIdx.x == 0 &&
-                   blockIdx.y == 0) {
-          if (p.scales) p.scales[0] = s;
-          if (p.scales_t) p.scales_t[0] = s;
-        }
+    for (int k = 0; k < 8; ++k) {
+      float s, r;
+      scales_from_amax<FMT, SF>(__uint_as_float(k < nc ? amax_g[c + k] : 0u), s, r);
+      rcol[k] = r;
+      if (warp == 0 && lane < 16 && blockIdx.y == 0 && k < nc) {
+        if (p.scales) p.scales[c + k] = s;
+        if (p.scales_t) p.scales_t[c + k] = s;
       }
     }
   }
@@ -224,7 +257,7 @@ __global__ void __launch_bounds__(256) quant_tile_kernel(QuantParams p, int gran
   for (int i = 0; i < 8; ++i) {
     float f[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) f[k] = __fmul_rn(v[i][k], colwise ? rcol[k] : rrow[i]);
+    for (int k = 0; k < 8; ++k) f[k] = __fmul_rn(v[i].f(k), colwise ? rcol[k] : rrow[i]);
     const uint32_t lo = cvt_fp8x4<FMT>(f[0], f[1], f[2], f[3]), hi = cvt_fp8x4<FMT>(f[4], f[5], f[6], f[7]);
     const int lr = warp * 16 + i * 2 + (lane >> 4);
     const int64_t row = r0 + lr;
