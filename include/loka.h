@@ -165,6 +165,28 @@ LOKA_API loka_status loka_fp8_linear_norm(const loka_linear_args* args, void* ws
                                  loka_stream_t stream);
 LOKA_API size_t loka_linear_workspace_size(const loka_linear_args* args);
 
+/* ---- a4+a5 for a whole LRM MLP stack in ONE launch (BASELINE.json configs[1]) --------------
+ * Layer l: h_{l+1} = norm_l(h_l . W_l^T) with h_0 = x (e4m3 + ROW scales) and W_l e4m3 + ROW
+ * scales (No Bias, unparameterized norm: PAPER.md:443, 483).  Every intermediate h_l (l = 1..L-1)
+ * is quantized rowwise to e4m3 exactly as loka_fp8_linear_norm with an E4M3/ROW output would,
+ * but never leaves the chip: a cluster of C CTAs keeps a 128-row block's activation in shared
+ * memory (the next layer's A operand) and streams only the weights.  Only y (the last layer's
+ * output) is written.  The result is bit-identical to the chain of L loka_fp8_linear_norm calls.
+ * Limits: L <= 8, dims[l] <= 1024 for l < L (K of each layer), with C = ceil(max N / 256), every
+ * N = dims[l+1] in {64C, 128C, 256C} (C <= 8); norm in {NONE, LAYER, RMS}.                     */
+typedef struct loka_stack_args {
+  int32_t L;
+  int64_t M;
+  int64_t dims[9];          /* dims[0] = K of layer 0, dims[l+1] = N of layer l                 */
+  loka_tensor x;            /* e4m3 [M, dims[0]] + ROW scales                                    */
+  loka_tensor w[8];         /* e4m3 [dims[l+1], dims[l]] + ROW scales                           */
+  loka_norm norm[8];
+  float eps[8];             /* <= 0: default (1e-5 LAYER, 1e-6 RMS)                              */
+  loka_tensor y;            /* [M, dims[L]]: F32 | BF16 | E4M3/E5M2 with ROW scales             */
+  int32_t* status_dev;      /* nullable                                                          */
+} loka_stack_args;
+LOKA_API loka_status loka_fp8_mlp_stack(const loka_stack_args* args, loka_stream_t stream);
+
 /* ---- a6: grouped launch: G independent linear+norm problems ------------------------------- */
 LOKA_API loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* args, void* ws, size_t ws_bytes,
                                     loka_stream_t stream);

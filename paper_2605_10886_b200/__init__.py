@@ -54,6 +54,12 @@ class loka_linear_args(C.Structure):
                 ("beta", C.c_void_p), ("y", loka_tensor), ("debug_precast", C.c_void_p), ("status_dev", C.c_void_p)]
 
 
+class loka_stack_args(C.Structure):
+    _fields_ = [("L", C.c_int32), ("M", C.c_int64), ("dims", C.c_int64 * 9), ("x", loka_tensor),
+                ("w", loka_tensor * 8), ("norm", C.c_int * 8), ("eps", C.c_float * 8), ("y", loka_tensor),
+                ("status_dev", C.c_void_p)]
+
+
 class loka_probe_pair(C.Structure):
     _fields_ = [("out", C.c_void_p), ("out_dtype", C.c_int), ("ref", C.c_void_p), ("ref_dtype", C.c_int),
                 ("M", C.c_int64), ("N", C.c_int64), ("ld_out", C.c_int64), ("ld_ref", C.c_int64)]
@@ -76,6 +82,7 @@ _sig = {
     "loka_quantize_grouped": ([C.c_int32, _P(loka_tensor), _P(loka_tensor), C.c_void_p, C.c_void_p], C.c_int),
     "loka_fp8_linear_norm": ([_P(loka_linear_args), C.c_void_p, C.c_size_t, C.c_void_p], C.c_int),
     "loka_linear_workspace_size": ([_P(loka_linear_args)], C.c_size_t),
+    "loka_fp8_mlp_stack": ([_P(loka_stack_args), C.c_void_p], C.c_int),
     "loka_grouped_fp8_linear": ([C.c_int32, _P(loka_linear_args), C.c_void_p, C.c_size_t, C.c_void_p], C.c_int),
     "loka_grouped_workspace_size": ([C.c_int32, _P(loka_linear_args)], C.c_size_t),
     "loka_probe_error": ([C.c_int32, _P(loka_probe_pair), C.c_double, C.c_void_p, C.c_void_p, C.c_size_t,
@@ -298,3 +305,36 @@ def loka_quantize_grouped(xs, fmt: str = "e4m3", scale_fmt: str = "f32", outs=No
         res.append((o, s))
     _check(_lib.loka_quantize_grouped(G, xa, qa, _ptr(status), _stream(stream)), "loka_quantize_grouped")
     return res
+
+
+def make_stack_args(xq, xs, ws, norms="layer", out_dtype="bf16", y=None, y_scales=None, eps=None, status=None):
+    """loka_stack_args for h_{l+1} = norm_l(h_l W_l^T): xq/xs = e4m3 codes + row scales of the input,
+    ws = [(codes [N_l, K_l], row scales [N_l])].  Returns (args, y, y_scales)."""
+    L = len(ws)
+    M, K0 = xq.shape
+    a = loka_stack_args()
+    a.L, a.M = L, M
+    dims = [K0] + [w.shape[0] for w, _ in ws]
+    for i, d in enumerate(dims):
+        a.dims[i] = d
+    a.x = _tensor(xq, E4M3, M, K0, xs, "row")
+    for l, (wq, wsc) in enumerate(ws):
+        a.w[l] = _tensor(wq, E4M3, wq.shape[0], wq.shape[1], wsc, "row")
+        a.norm[l] = NORM[norms if isinstance(norms, str) else norms[l]]
+        a.eps[l] = 0.0 if eps is None else float(eps)
+    od = {"f32": F32, "bf16": BF16, "e4m3": E4M3, "e5m2": E5M2}[out_dtype]
+    N = dims[-1]
+    if y is None:
+        y = torch.empty(M, N, dtype=_TORCH_DT[od], device=xq.device)
+    if od in (E4M3, E5M2) and y_scales is None:
+        y_scales = torch.empty(M, dtype=torch.float32, device=xq.device)
+    a.y = _tensor(y, od, M, N, y_scales, "row")
+    a.status_dev = None if status is None else status.data_ptr()
+    return a, y, y_scales
+
+
+def loka_fp8_mlp_stack(xq, xs, ws, stream=None, **kw):
+    """Whole layer stack in one launch (intermediate activations stay on chip)."""
+    a, y, ys = make_stack_args(xq, xs, ws, **kw)
+    _check(_lib.loka_fp8_mlp_stack(C.byref(a), _stream(stream)), "loka_fp8_mlp_stack")
+    return y, ys

@@ -401,6 +401,62 @@ loka_status loka_fp8_linear_norm(const loka_linear_args* a, void* /*ws*/, size_t
   return e == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
 }
 
+loka_status loka_fp8_mlp_stack(const loka_stack_args* a, loka_stream_t stream) {
+  if (!a) return LOKA_ERR_INVALID_ARG;
+  const int L = a->L;
+  if (L < 1 || L > kMaxStackLayers || a->M <= 0 || a->M > (1ll << 31) - 1) return LOKA_ERR_SHAPE;
+  int64_t maxN = 0;
+  for (int l = 0; l < L; ++l) {
+    if (a->dims[l] <= 0 || a->dims[l + 1] <= 0) return LOKA_ERR_SHAPE;
+    if (a->dims[l] > 1024) return LOKA_ERR_UNSUPPORTED;  // A operand of a layer held in 128 KB of smem
+    maxN = std::max<int64_t>(maxN, a->dims[l + 1]);
+  }
+  const int C = (int)cdiv(maxN, 256);
+  if (C > 8) return LOKA_ERR_UNSUPPORTED;
+  StackParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.L = L;
+  p.M = (int32_t)a->M;
+  p.C = C;
+  const loka_tensor& X = a->x;
+  if (X.dtype != LOKA_E4M3 || X.gran != LOKA_GRAN_ROW || !X.data || !X.scales || X.rows != a->M ||
+      X.cols != a->dims[0] || !aligned16(X.data) || X.ld < X.cols || X.ld % 16)
+    return LOKA_ERR_INVALID_ARG;
+  if (!make_map_u8(&p.tx, X.data, a->M, X.cols, X.ld, 128)) return LOKA_ERR_CUDA;
+  p.xs = X.scales;
+  for (int l = 0; l < L; ++l) {
+    const int64_t K = a->dims[l], N = a->dims[l + 1];
+    const int64_t bn = N / C;
+    if (N % C || (bn != 64 && bn != 128 && bn != 256)) return LOKA_ERR_UNSUPPORTED;
+    if (l > 0 && K % 128) return LOKA_ERR_UNSUPPORTED;
+    const loka_tensor& W = a->w[l];
+    if (W.dtype != LOKA_E4M3 || W.gran != LOKA_GRAN_ROW || !W.data || !W.scales || W.rows != N || W.cols != K ||
+        !aligned16(W.data) || W.ld < K || W.ld % 16)
+      return LOKA_ERR_INVALID_ARG;
+    const int nm = a->norm[l];
+    if (nm != LOKA_NORM_NONE && nm != LOKA_NORM_LAYER && nm != LOKA_NORM_RMS) return LOKA_ERR_UNSUPPORTED;
+    if (!make_map_u8(&p.tw[l], W.data, N, K, W.ld, (uint32_t)bn)) return LOKA_ERR_CUDA;
+    p.ws[l] = W.scales;
+    p.K[l] = (int32_t)K;
+    p.N[l] = (int32_t)N;
+    p.BN[l] = (int32_t)bn;
+    p.norm[l] = nm;
+    p.eps[l] = a->eps[l] > 0.f ? a->eps[l] : (nm == LOKA_NORM_LAYER ? 1e-5f : 1e-6f);
+  }
+  const loka_tensor& Y = a->y;
+  if (Y.dtype < LOKA_F32 || Y.dtype > LOKA_E5M2 || !Y.data || !aligned16(Y.data) || Y.rows != a->M ||
+      Y.cols != a->dims[L] || Y.ld < Y.cols || (Y.ld * elem_size(Y.dtype)) % 16)
+    return LOKA_ERR_INVALID_ARG;
+  if (is_fp8(Y.dtype) && (!Y.scales || Y.gran != LOKA_GRAN_ROW)) return LOKA_ERR_INVALID_ARG;
+  if (!make_map_out(&p.ty, Y.data, a->M, Y.cols, Y.ld, Y.dtype, p.BN[L - 1])) return LOKA_ERR_CUDA;
+  p.out_dtype = Y.dtype;
+  p.y_scales = is_fp8(Y.dtype) ? Y.scales : nullptr;
+  p.status = a->status_dev;
+  loka_status st = check_device();
+  if (st != LOKA_OK) return st;
+  return launch_stack(p, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
+}
+
 size_t loka_grouped_workspace_size(int32_t /*G*/, const loka_linear_args* /*a*/) { return 0; }
 
 loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* ws, size_t ws_bytes,

@@ -64,6 +64,24 @@ struct LinearParams {
 cudaError_t launch_linear(const CUtensorMap& tma_a, const CUtensorMap& tma_b, const CUtensorMap& tma_y,
                           const LinearParams& p, int bn, cudaStream_t st);
 
+// ---- fused layer stack (stack.cu) ----
+constexpr int kMaxStackLayers = 8;
+struct StackParams {
+  CUtensorMap tx;                    // X codes [M, K0], box {128, 128}
+  CUtensorMap tw[kMaxStackLayers];   // W_l codes [N_l, K_l], box {128, BN_l}
+  CUtensorMap ty;                    // output [M, N_last], box {min(128, BN*e) bytes, 128}
+  const float* xs;                   // X row scales
+  const float* ws[kMaxStackLayers];  // W_l row scales (per output column)
+  int32_t L, M, C;
+  int32_t K[kMaxStackLayers], N[kMaxStackLayers], BN[kMaxStackLayers];
+  int32_t norm[kMaxStackLayers];
+  float eps[kMaxStackLayers];
+  int32_t out_dtype;
+  float* y_scales;
+  int32_t* status;
+};
+cudaError_t launch_stack(const StackParams& p, cudaStream_t st);
+
 // ---- blockwise-scaled GEMM with FP32 promotion (blockwise.cu) ----
 struct BwParams {
   int32_t M, N, K;

@@ -1,0 +1,440 @@
+// stack.cu — a whole LRM MLP stack (BASELINE.json configs[1]: L layers of rowwise-e4m3 FP8 linear
+// + LayerNorm, "many small GEMMs followed immediately by normalization") in ONE launch.
+//
+// A thread-block cluster of C CTAs owns a 128-row block of the batch; CTA `rank` owns the column
+// slice [rank*BN_l, (rank+1)*BN_l) of every layer (BN_l = N_l / C).  Per layer:
+//   * the layer input h_l (the MMA's A operand, 128 x K_l FP8) is already in every CTA's shared
+//     memory, in the 128B-swizzled K-major layout tcgen05 reads; only the weight slice streams
+//     (TMA ring, prefetched across layers);
+//   * tcgen05.mma accumulates the 128 x BN_l tile in TMEM;
+//   * the epilogue (same arithmetic as linear.cu: s_a folded into eps, packed FP32x2 statistics,
+//     quarter merge in smem, cluster exchange of (mean, M2, ymax, ymin) pushed with DSMEM stores,
+//     one-FFMA normalisation, row amax from ymax/ymin) produces the next layer's e4m3 codes and
+//     row scale, and writes the codes straight into EVERY cluster CTA's A buffer with
+//     st.shared::cluster.v4 (then fence.proxy.async + cluster barrier before the next MMA);
+//   * only the last layer's output goes to HBM (swizzled staging tile + TMA store).
+// The codes and scales are bit-identical to the per-layer chain of linear_norm_kernel launches.
+#include "common.cuh"
+#include "launch.h"
+
+namespace loka {
+
+constexpr int kSThreads = 512;  // 16 warps: warp 0 lane 0 = TMA producer, warp 1 lane 0 = MMA issuer,
+                                // then all 16 warps run each layer's epilogue
+constexpr int kSStages = 2;
+constexpr int kSBNMax = 256, kSKMax = 1024;
+constexpr int kSRec = 6;
+constexpr int kSOffA = 0;                                // [kb][128 rows][128 B] (<= 128 KB)
+constexpr int kSOffW = 128 * kSKMax;                     // weight ring
+constexpr int kSStageW = kSBNMax * 128;
+constexpr int kSOffCs = kSOffW + kSStages * kSStageW;    // [8][128] float4 cluster records
+constexpr int kSOffCol = kSOffCs + 8 * 128 * 16;         // [kSBNMax] W row scales of this slice
+constexpr int kSOffBar = kSOffCol + kSBNMax * 4;
+constexpr int kSSmem = kSOffBar + 128 + 1024;
+static_assert(kSSmem <= 227 * 1024, "stack smem");
+
+struct SRow {
+  float n, mean, m2, ss, ymax, ymin;
+  LOKA_DEVINL void init() { n = 0.f; mean = 0.f; m2 = 0.f; ss = 0.f; ymax = -INFINITY; ymin = INFINITY; }
+};
+template <int K>
+LOKA_DEVINL SRow merge_rows(const SRow (&r)[K]) {
+  SRow o;
+  o.init();
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    o.n += r[k].n;
+    s = fmaf(r[k].n, r[k].mean, s);
+    o.ss += r[k].ss;
+    o.ymax = fmaxf(o.ymax, r[k].ymax);
+    o.ymin = fminf(o.ymin, r[k].ymin);
+  }
+  o.mean = o.n > 0.f ? __fdiv_rn(s, o.n) : 0.f;
+  float m2 = 0.f;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const float d = r[k].mean - o.mean;
+    m2 += r[k].m2 + r[k].n * d * d;
+  }
+  o.m2 = m2;
+  return o;
+}
+
+struct SCtx {
+  uint8_t* smem;
+  uint32_t tmem_base;
+  int warp, lane, q, cq, r, grow, m0, rank, C;
+  bool row_ok;
+};
+
+// One layer's epilogue for CPT = BN/4 columns per thread.  `sa` is the layer input's row scale;
+// returns the next layer's row scale (or 1 for the last layer).
+template <int CPT>
+LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, float sa) {
+  constexpr int BN = 4 * CPT;
+  const int norm = p.norm[l];
+  const int N = p.N[l];
+  const int n0 = c.rank * BN;
+  const bool last = l + 1 == p.L;
+  const bool fold = norm != LOKA_NORM_NONE;  // no bias in the stack: s_a goes into eps
+  float* col = reinterpret_cast<float*>(c.smem + kSOffCol);
+  float* cs = reinterpret_cast<float*>(c.smem + kSOffCs);
+  float* hx = reinterpret_cast<float*>(c.smem + kSOffA);  // A is drained once our MMAs completed
+  const int cb = c.cq * CPT;
+  const uint32_t col_s = smem_u32(col);
+
+  // ---- accumulator -> registers, dequant ----
+  float y[CPT];
+  const uint32_t taddr = c.tmem_base + ((uint32_t)(c.q * 32) << 16) + (uint32_t)cb;
+  if constexpr (CPT >= 32) {
+#pragma unroll
+    for (int i = 0; i < CPT / 32; ++i) tmem_ld32_nowait(taddr + (uint32_t)(32 * i), y + 32 * i);
+  } else {
+    tmem_ld16_nowait(taddr, y);
+  }
+#pragma unroll
+  for (int i = 0; i < CPT / 16; ++i) tmem_wait16(y + 16 * i);
+  const float ys = fold ? 1.f : sa;
+#pragma unroll
+  for (int j = 0; j < CPT; j += 4) {
+    const float4 s4 = lds_f4(col_s + (uint32_t)(cb + j) * 4u);
+    const float2 a = fmul2(make_float2(y[j], y[j + 1]), fmul2(make_float2(s4.x, s4.y), make_float2(ys, ys)));
+    const float2 b = fmul2(make_float2(y[j + 2], y[j + 3]), fmul2(make_float2(s4.z, s4.w), make_float2(ys, ys)));
+    y[j] = a.x; y[j + 1] = a.y; y[j + 2] = b.x; y[j + 3] = b.y;
+  }
+
+  // ---- statistics over this thread's CPT columns (all valid: N = C*BN exactly) ----
+  SRow rec;
+  rec.init();
+  rec.n = (float)CPT;
+  float cmax = y[0], cmin = y[0];
+#pragma unroll
+  for (int j = 0; j < CPT; j += 2) cmax = fmax3(cmax, y[j], y[j + 1]), cmin = fmin3(cmin, y[j], y[j + 1]);
+  rec.ymax = cmax;
+  rec.ymin = cmin;
+  if (norm == LOKA_NORM_LAYER) {
+    float2 s0 = make_float2(0.f, 0.f), s1 = s0, s2 = s0, s3 = s0;
+#pragma unroll
+    for (int j = 0; j < CPT; j += 8) {
+      s0 = fadd2(s0, make_float2(y[j], y[j + 1]));
+      s1 = fadd2(s1, make_float2(y[j + 2], y[j + 3]));
+      s2 = fadd2(s2, make_float2(y[j + 4], y[j + 5]));
+      s3 = fadd2(s3, make_float2(y[j + 6], y[j + 7]));
+    }
+    s0 = fadd2(fadd2(s0, s1), fadd2(s2, s3));
+    const float mc = (s0.x + s0.y) / (float)CPT;
+    const float2 nm = make_float2(-mc, -mc);
+    float2 q0 = make_float2(0.f, 0.f), q1 = q0;
+#pragma unroll
+    for (int j = 0; j < CPT; j += 4) {
+      const float2 d0 = fadd2(make_float2(y[j], y[j + 1]), nm);
+      const float2 d1 = fadd2(make_float2(y[j + 2], y[j + 3]), nm);
+      q0 = ffma2(d0, d0, q0);
+      q1 = ffma2(d1, d1, q1);
+    }
+    q0 = fadd2(q0, q1);
+    rec.mean = mc;
+    rec.m2 = q0.x + q0.y;
+  } else if (norm == LOKA_NORM_RMS) {
+    float2 q0 = make_float2(0.f, 0.f), q1 = q0;
+#pragma unroll
+    for (int j = 0; j < CPT; j += 4) {
+      const float2 a = make_float2(y[j], y[j + 1]), b = make_float2(y[j + 2], y[j + 3]);
+      q0 = ffma2(a, a, q0);
+      q1 = ffma2(b, b, q1);
+    }
+    q0 = fadd2(q0, q1);
+    rec.ss = q0.x + q0.y;
+  }
+  // ---- merge the four column quarters (component-major records in smem) ----
+  {
+    float* my = hx + (size_t)c.cq * kSRec * 128 + c.r;
+    my[0] = rec.n; my[128] = rec.mean; my[256] = rec.m2; my[384] = rec.ss; my[512] = rec.ymax; my[640] = rec.ymin;
+    named_bar_sync(1, kSThreads);
+    SRow parts[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float* o = hx + (size_t)k * kSRec * 128 + c.r;
+      parts[k].n = o[0]; parts[k].mean = o[128]; parts[k].m2 = o[256]; parts[k].ss = o[384];
+      parts[k].ymax = o[512]; parts[k].ymin = o[640];
+    }
+    rec = merge_rows(parts);
+    if (c.C == 1) named_bar_sync(1, kSThreads);  // hx (aliasing A) read by all before A is rewritten
+  }
+  // ---- cluster exchange: push (mean|ss, m2, ymax, ymin) to every peer, barrier, merge ----
+  if (c.C > 1) {
+    if (c.cq == 0) {
+      const float4 v = make_float4(norm == LOKA_NORM_LAYER ? rec.mean : rec.ss, rec.m2, rec.ymax, rec.ymin);
+      const uint32_t la = smem_u32(cs + ((size_t)c.rank * 128 + c.r) * 4);
+      for (int rk = 0; rk < c.C; ++rk) st_dsmem_f4(mapa_shared(la, (uint32_t)rk), v);
+    }
+    cluster_sync_all();  // barrier 1: also proves every cluster CTA finished this layer's MMAs
+    SRow parts[8];
+#pragma unroll
+    for (int rk = 0; rk < 8; ++rk) {
+      parts[rk].init();
+      if (rk < c.C) {
+        const float4 v = lds_f4(smem_u32(cs + ((size_t)rk * 128 + c.r) * 4));
+        parts[rk].n = (float)BN;
+        parts[rk].mean = norm == LOKA_NORM_LAYER ? v.x : 0.f;
+        parts[rk].m2 = v.y;
+        parts[rk].ss = norm == LOKA_NORM_LAYER ? 0.f : v.x;
+        parts[rk].ymax = v.z;
+        parts[rk].ymin = v.w;
+      }
+    }
+    rec = merge_rows(parts);
+  }
+  // ---- normalise (one FFMA) ----
+  const float eps = p.eps[l];
+  const float eps_eff = fold ? __fdiv_rn(eps, __fmul_rn(sa, sa)) : eps;
+  float rstd = 1.f, c0 = 0.f;
+  if (norm == LOKA_NORM_LAYER) {
+    rstd = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(rec.m2, rec.n), eps_eff)));
+    c0 = -__fmul_rn(rec.mean, rstd);
+  } else if (norm == LOKA_NORM_RMS) {
+    rstd = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(rec.ss, rec.n), eps_eff)));
+  }
+  if (norm != LOKA_NORM_NONE) {
+    const float2 r2 = make_float2(rstd, rstd), c2 = make_float2(c0, c0);
+#pragma unroll
+    for (int j = 0; j < CPT; j += 2) {
+      const float2 a = ffma2(make_float2(y[j], y[j + 1]), r2, c2);
+      y[j] = a.x;
+      y[j + 1] = a.y;
+    }
+  }
+  const bool fp8_next = !last || p.out_dtype == LOKA_E4M3 || p.out_dtype == LOKA_E5M2;
+  const int ofmt = last ? p.out_dtype : LOKA_E4M3;
+  float s_out = 1.f, r_out = 1.f;
+  if (fp8_next) {  // row amax of the normalised row (monotone in y: from ymax / ymin, exact)
+    const float amax = norm == LOKA_NORM_NONE ? fmaxf(fabsf(rec.ymax), fabsf(rec.ymin))
+                                              : fmaxf(fabsf(fmaf(rec.ymax, rstd, c0)), fabsf(fmaf(rec.ymin, rstd, c0)));
+    if (__float_as_uint(amax) >= 0x7F800000u && p.status) atomicOr(p.status, LOKA_DEVSTATUS_NONFINITE);
+    if (ofmt == LOKA_E5M2) scales_from_amax<LOKA_E5M2, LOKA_SCALE_F32>(amax, s_out, r_out);
+    else scales_from_amax<LOKA_E4M3, LOKA_SCALE_F32>(amax, s_out, r_out);
+  }
+  if (!last) {
+    // ---- next layer's A operand: codes into every cluster CTA's swizzled A tile ----
+    const float2 rr = make_float2(r_out, r_out);
+    const uint32_t a_local = smem_u32(c.smem + kSOffA);
+#pragma unroll
+    for (int ch = 0; ch < CPT / 16; ++ch) {
+      uint32_t w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int j = 16 * ch + 4 * i;
+        const float2 a = fmul2(make_float2(y[j], y[j + 1]), rr);
+        const float2 b = fmul2(make_float2(y[j + 2], y[j + 3]), rr);
+        w[i] = cvt_fp8x4<LOKA_E4M3>(a.x, a.y, b.x, b.y);
+      }
+      const int k = n0 + cb + 16 * ch;  // K index of the next layer
+      const uint32_t off = (uint32_t)(k >> 7) * 16384u + (uint32_t)c.r * 128u +
+                           ((((uint32_t)(k & 127) >> 4) ^ ((uint32_t)c.r & 7u)) << 4);
+      const float4 v = make_float4(__uint_as_float(w[0]), __uint_as_float(w[1]), __uint_as_float(w[2]),
+                                   __uint_as_float(w[3]));
+      for (int rk = 0; rk < c.C; ++rk) st_dsmem_f4(mapa_shared(a_local + off, (uint32_t)rk), v);
+    }
+    asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");  // generic writes -> tensor-core reads
+    if (c.C > 1) cluster_sync_all();  // barrier 2: h_{l+1} complete in every CTA
+    else named_bar_sync(1, kSThreads);
+    return s_out;
+  }
+  // ---- last layer: output tile -> swizzled staging (reuses A) -> TMA store ----
+  if (fp8_next && c.row_ok && c.rank == 0 && c.cq == 0 && p.y_scales) p.y_scales[c.grow] = s_out;
+  const int esz = p.out_dtype == LOKA_F32 ? 4 : p.out_dtype == LOKA_BF16 ? 2 : 1;
+  const uint32_t box_bytes = (uint32_t)min(128, BN * esz);
+  const uint32_t stage_s = smem_u32(c.smem + kSOffA);
+  auto put16 = [&](int chunk, uint4 v) {
+    const uint32_t bofs = (uint32_t)(cb * esz + 16 * chunk);
+    const uint32_t c16 = (bofs % box_bytes) >> 4;
+    const uint32_t sw = box_bytes == 128u ? (c16 ^ ((uint32_t)c.r & 7u)) : (c16 ^ (((uint32_t)c.r >> 1) & 3u));
+    sts_u4(stage_s + (bofs / box_bytes) * (128u * box_bytes) + (uint32_t)c.r * box_bytes + (sw << 4), v);
+  };
+  if (esz == 4) {
+#pragma unroll
+    for (int k = 0; k < CPT / 4; ++k)
+      put16(k, make_uint4(__float_as_uint(y[4 * k]), __float_as_uint(y[4 * k + 1]), __float_as_uint(y[4 * k + 2]),
+                          __float_as_uint(y[4 * k + 3])));
+  } else if (esz == 2) {
+#pragma unroll
+    for (int k = 0; k < CPT / 8; ++k) {
+      uint32_t w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        __nv_bfloat162 hh = __floats2bfloat162_rn(y[8 * k + 2 * i], y[8 * k + 2 * i + 1]);
+        w[i] = *reinterpret_cast<uint32_t*>(&hh);
+      }
+      put16(k, make_uint4(w[0], w[1], w[2], w[3]));
+    }
+  } else {
+    const float2 rr = make_float2(r_out, r_out);
+#pragma unroll
+    for (int k = 0; k < CPT / 16; ++k) {
+      uint32_t w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int j = 16 * k + 4 * i;
+        const float2 a = fmul2(make_float2(y[j], y[j + 1]), rr);
+        const float2 b = fmul2(make_float2(y[j + 2], y[j + 3]), rr);
+        w[i] = ofmt == LOKA_E5M2 ? cvt_fp8x4<LOKA_E5M2>(a.x, a.y, b.x, b.y) : cvt_fp8x4<LOKA_E4M3>(a.x, a.y, b.x, b.y);
+      }
+      put16(k, make_uint4(w[0], w[1], w[2], w[3]));
+    }
+  }
+  fence_proxy_async_smem();
+  named_bar_sync(1, kSThreads);
+  if (threadIdx.x == 0) {
+    const int per_box = (int)box_bytes / esz, nbox = BN * esz / (int)box_bytes;
+    for (int b = 0; b < nbox; ++b) {
+      const int c0b = n0 + b * per_box;
+      if (c0b < N) tma_store_2d(&p.ty, c.smem + kSOffA + b * 128 * (int)box_bytes, c0b, c.m0);
+    }
+    bulk_commit();
+    bulk_wait_read0();
+  }
+  return 1.f;
+}
+
+__global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_constant__ StackParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem + kSOffA;
+  uint8_t* sW = smem + kSOffW;
+  float* col = reinterpret_cast<float*>(smem + kSOffCol);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kSOffBar);
+  uint64_t* empty_bar = full_bar + kSStages;
+  uint64_t* a_full = empty_bar + kSStages;
+  uint64_t* tmem_full = a_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  SCtx c;
+  c.smem = smem;
+  c.warp = threadIdx.x >> 5;
+  c.lane = threadIdx.x & 31;
+  c.q = c.warp & 3;
+  c.cq = c.warp >> 2;
+  c.r = c.q * 32 + c.lane;
+  c.m0 = blockIdx.x * 128;
+  c.grow = c.m0 + c.r;
+  c.row_ok = c.grow < p.M;
+  c.C = p.C;
+  c.rank = p.C > 1 ? (int)cluster_ctarank() : 0;
+
+  if (c.warp == 0 && c.lane == 0) {
+    tma_prefetch_desc(&p.tx);
+    tma_prefetch_desc(&p.ty);
+    for (int l = 0; l < p.L; ++l) tma_prefetch_desc(&p.tw[l]);
+    for (int s = 0; s < kSStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(a_full, 1);
+    mbar_init(tmem_full, 1);
+    fence_barrier_init();
+  }
+  if (c.warp == 1) tmem_alloc<kSBNMax>(tmem_slot);
+  pdl_wait();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  c.tmem_base = *tmem_slot;
+  if (p.C > 1) cluster_sync_all();  // every cluster CTA is running before any DSMEM traffic
+
+  float sa = c.row_ok ? p.xs[c.grow] : 0.f;  // row scale of the current layer input
+  int prod_it = 0, mma_it = 0;
+  auto produce = [&](int l, int kb) {
+    const int s = prod_it % kSStages;
+    mbar_wait(&empty_bar[s], ((uint32_t)(prod_it / kSStages) & 1u) ^ 1u, 1);
+    mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(p.BN[l] * 128));
+    tma_load_2d(sW + s * kSStageW, &p.tw[l], &full_bar[s], kb * 128, c.rank * p.BN[l]);
+    ++prod_it;
+  };
+  int prefetched = 0;  // k-blocks of the current layer already issued during the previous layer
+  for (int l = 0; l < p.L; ++l) {
+    const int nkb = (p.K[l] + 127) / 128;
+    if (c.warp == 0 && c.lane == 0) {  // ===== producer =====
+      if (l == 0) {
+        mbar_arrive_expect_tx(a_full, (uint32_t)(nkb * 128 * 128));
+        for (int kb = 0; kb < nkb; ++kb) tma_load_2d(sA + kb * 16384, &p.tx, a_full, kb * 128, c.m0);
+      }
+      for (int kb = prefetched; kb < nkb; ++kb) produce(l, kb);
+      prefetched = 0;
+      if (l + 1 < p.L) {  // run ahead into the next layer's weights while this layer finishes
+        const int nn = min(kSStages, (p.K[l + 1] + 127) / 128);
+        for (int kb = 0; kb < nn; ++kb) produce(l + 1, kb);
+        prefetched = nn;
+      }
+    }
+    if (c.warp == 1 && c.lane == 0) {  // ===== MMA issuer =====
+      if (l == 0) mbar_wait(a_full, 0, 5);
+      else asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // DSMEM-written A -> tensor core
+      tc_fence_after();
+      const uint32_t idesc = idesc_f8f6f4(0, 0, 128, (uint32_t)p.BN[l]);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = mma_it % kSStages;
+        mbar_wait(&full_bar[s], (uint32_t)(mma_it / kSStages) & 1u, 2);
+        tc_fence_after();
+        const uint32_t a0 = smem_u32(sA + kb * 16384), b0 = smem_u32(sW + s * kSStageW);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          mma_f8f6f4(c.tmem_base, smem_desc_kmajor_sw128(a0 + k * 32), smem_desc_kmajor_sw128(b0 + k * 32), idesc,
+                     (kb | k) != 0);
+        mma_commit(&empty_bar[s]);
+        ++mma_it;
+      }
+      mma_commit(tmem_full);
+    }
+    __syncwarp();
+    // ===== epilogue (all warps) =====
+    const float* ws = p.ws[l];
+    for (int j = threadIdx.x; j < p.BN[l]; j += kSThreads) col[j] = ws[c.rank * p.BN[l] + j];
+    named_bar_sync(1, kSThreads);
+    if (c.lane == 0) mbar_wait(tmem_full, (uint32_t)l & 1u, 3);
+    __syncwarp();
+    tc_fence_after();
+    float s_next;
+    switch (p.BN[l]) {
+      case 64: s_next = stack_epilogue<16>(p, c, l, sa); break;
+      case 128: s_next = stack_epilogue<32>(p, c, l, sa); break;
+      default: s_next = stack_epilogue<64>(p, c, l, sa); break;
+    }
+    sa = c.row_ok ? s_next : 0.f;
+    tc_fence_before();  // this layer's tcgen05.ld done before the next layer's MMAs overwrite TMEM
+  }
+  if (p.C > 1) cluster_sync_all();
+  __syncthreads();
+  if (c.warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<kSBNMax>(c.tmem_base);
+  }
+}
+
+cudaError_t launch_stack(const StackParams& p, cudaStream_t st) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(stack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSSmem);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((p.M + 127) / 128), (unsigned)p.C, 1);
+  cfg.blockDim = dim3(kSThreads, 1, 1);
+  cfg.dynamicSmemBytes = kSSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = (unsigned)p.C;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, stack_kernel, p);
+  note_launch();
+  return e;
+}
+
+}  // namespace loka
