@@ -139,13 +139,27 @@ class Fp8Stack:
                                              y=self.y if last else self.hq[l], y_scales=None if last else self.hs[l],
                                              keep=self.keep)
             self.largs.append(args)
+        # the fused stack: all 8 layers in one launch, same output bits as the per-layer chain
+        self.sargs, _, _ = lk.make_stack_args(self.xq, self.xs, list(zip(self.wq, self.wsc)), norms="layer",
+                                              out_dtype="bf16", y=self.y)
 
     def quantize_all(self, stream_handle):
         st = self.lk._lib.loka_quantize_grouped(self.G, self.qx, self.qq, None, stream_handle)
         if st:
             raise self.lk.LokaError(st, "loka_quantize_grouped")
 
+    def stack_only(self, stream_handle):
+        st = self.lk._lib.loka_fp8_mlp_stack(self.C.byref(self.sargs), stream_handle)
+        if st:
+            raise self.lk.LokaError(st, "loka_fp8_mlp_stack")
+
     def step(self, stream_handle):
+        """The bench step: 1 grouped quantize launch + 1 fused stack launch."""
+        self.quantize_all(stream_handle)
+        self.stack_only(stream_handle)
+
+    def step_per_layer(self, stream_handle):
+        """Reference path: the same step with one fused linear+norm launch per layer."""
         lib, C = self.lk._lib, self.C
         self.quantize_all(stream_handle)
         for a in self.largs:
@@ -325,12 +339,15 @@ def main():
         t_fp8 = time_steps(g8.replay, args.steps, args.warmup, flush, stream, barrier)
     clocks = clk.summary()
 
-    # The dominant kernel (the fused linear+norm launches): a graph of its 8 launches, replayed with
-    # the L2 flushed before each replay, timed with events on the launching stream; the per-launch
-    # duration is the replay time / 8 (launch gaps included, host enqueue excluded).
-    glin = capture(lambda: [stack.linear_only(l, sh) for l in range(8)], stream)
-    t_lin = time_steps(glin.replay, args.steps, args.warmup, flush, stream, None)
-    lin_ms_per_launch = (sum(t_lin) / len(t_lin)) / 8.0
+    # The dominant kernel (the fused stack launch): a graph of that one launch, replayed with the L2
+    # flushed before each replay, timed with events on the launching stream.
+    gst = capture(lambda: stack.stack_only(sh), stream)
+    t_st = time_steps(gst.replay, args.steps, args.warmup, flush, stream, None)
+    stack_ms = sum(t_st) / len(t_st)
+    # the per-layer path (one linear_norm launch per layer) for comparison
+    gpl = capture(lambda: stack.step_per_layer(sh), stream)
+    t_pl = time_steps(gpl.replay, args.steps, args.warmup, flush, stream, None)
+    per_layer_ms = sum(t_pl) / len(t_pl)
 
     # BF16 baseline (torch F.linear + F.layer_norm, graph-captured) on the same inputs
     out_bf = torch.empty(M_PER_GPU, DIMS[8], dtype=torch.bfloat16, device=dev)
@@ -365,13 +382,13 @@ def main():
 
     bf16_peak, hbm_peak, src = peaks()
     fp8_peak = 2.0 * bf16_peak  # nominal dense fp8/bf16 ratio 4500/2250
-    lin_fl = [2.0 * M_PER_GPU * DIMS[l] * DIMS[l + 1] for l in range(8)]
-    achieved = (sum(lin_fl) / 8.0) / (lin_ms_per_launch * 1e-3) / 1e12  # mean FLOPs per launch / mean launch time
+    stack_fl = flops_per_step()  # one stack launch = the 8 layers' 2 M K N
+    achieved = stack_fl / (stack_ms * 1e-3) / 1e12
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get("linear_norm_bytes_per_launch")
+            traffic = json.load(open(tf)).get("stack_bytes_per_launch")
         except Exception:  # noqa: BLE001
             traffic = None
 
@@ -383,18 +400,21 @@ def main():
             "config": {"workload": WORKLOAD, "model": "cfg2", "global_batch": M_PER_GPU * world,
                        "seq_len": None, "parallelism": f"dp{world}",
                        "l2": "flushed before every timed step (256 MiB write)",
-                       "step": "1 grouped quantize launch (X + 8 W, rowwise e4m3) + 8 fused FP8 linear+LayerNorm launches, CUDA-graph replay"},
+                       "step": "1 grouped quantize launch (X + 8 W, rowwise e4m3) + 1 fused 8-layer FP8 "
+                               "linear+LayerNorm stack launch, CUDA-graph replay"},
             "pct_of_4500_tflops": round(100.0 * value / world / 4500.0, 2),
             "bf16_baseline": {"value": round(bf_value, 3), "unit": "TFLOP/s", "ms_per_step": round(ms_bf, 5),
                               "impl": "torch F.linear + F.layer_norm (bf16, cuBLAS), CUDA-graph replay"},
             "speedup_vs_bf16": round(ms_bf / ms_fp8, 3),
-            "roofline": {"kernel": "linear_norm_kernel (fused FP8 GEMM + LayerNorm), 8 launches/step",
+            "roofline": {"kernel": "stack_kernel (8 fused FP8 GEMM + LayerNorm layers), 1 launch/step",
                          "bound": "tensor", "achieved": round(achieved, 2), "peak": round(fp8_peak, 1),
                          "unit": "TFLOP/s", "frac": round(achieved / fp8_peak, 4), "traffic": traffic,
                          "peak_source": f"{src}: 2 x bf16 {bf16_peak} TF/s (nominal fp8/bf16 ratio)",
-                         "flop_per_launch": sum(lin_fl) / 8.0,
-                         "mean_launch_us": round(1e3 * lin_ms_per_launch, 3),
-                         "timing": "graph of the 8 launches, L2 flushed before each replay, CUDA events"},
+                         "flop_per_launch": stack_fl, "launch_us": round(1e3 * stack_ms, 3),
+                         "timing": "graph of the launch, L2 flushed before each replay, CUDA events"},
+            "per_layer_path": {"ms_per_step": round(per_layer_ms, 5),
+                               "value": round(flops_per_step() / (per_layer_ms * 1e-3) / 1e12, 3),
+                               "impl": "grouped quantize + 8 linear_norm launches (same output bits)"},
             "e2e": {"value": round(e2e_value, 3), "unit": "TFLOP/s", "ms_per_step": round(ms_e2e, 5),
                     "h2d_bytes_per_step": int(x.numel() * 2), "d2h_bytes_per_step": int(stack.y.numel() * 2)},
             "gpu_launches": int(launches_per_step * args.steps),
