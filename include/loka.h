@@ -248,6 +248,8 @@ LOKA_API int64_t loka_debug_hang_info(uint64_t* info3, int32_t reset);
  * landed, last MMA committed, accumulator ready, statistics done, stores done, pass-1 done,
  * halves merged, cluster merged, finalized) at
  * out[(blockIdx.x + gridDim.x*blockIdx.y)*16 + slot] for the first 4096 CTAs of the LAST launch;
+ * the fused stack kernel records 64 stamps per CTA (2 + 7 per layer, see stack.cu) at
+ * out[65536 + (blockIdx.x + gridDim.x*blockIdx.y)*64 + slot] for its first 512 CTAs.
  * enable = 0 turns it off, enable = -1 leaves it unchanged.  Copies up to n stamps into out
  * (host, may be NULL).  Returns the number copied, -1 on a CUDA error.  Synchronous.          */
 LOKA_API int64_t loka_debug_trace(int32_t enable, uint64_t* out, int64_t n);

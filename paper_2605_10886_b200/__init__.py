@@ -179,7 +179,7 @@ def loka_quantize(x: torch.Tensor, fmt: str = "e4m3", gran: str = "row", scale_f
 
 
 def make_linear_args(a, a_scales, b, b_scales, *, a_fmt="e4m3", b_fmt="e4m3", a_gran="row", b_gran="row",
-                     norm="none", norm_block=256, eps=0.0, gamma=None, beta=None, bias=None, out_dtype="f32",
+                     a_scale_fmt="f32", b_scale_fmt="f32", norm="none", norm_block=256, eps=0.0, gamma=None, beta=None, bias=None, out_dtype="f32",
                      y=None, y_scales=None, precast=None, status=None, direction="fwd", keep=None):
     """Build a loka_linear_args for C = A . B^T (A [M,K], B [N,K] FP8 codes, K-major)."""
     M, K = a.shape
@@ -192,8 +192,8 @@ def make_linear_args(a, a_scales, b, b_scales, *, a_fmt="e4m3", b_fmt="e4m3", a_
         y_scales = torch.empty(M, dtype=torch.float32, device=dev)
     args = loka_linear_args()
     args.M, args.N, args.K, args.dir = M, N, K, DIR[direction]
-    args.a = _tensor(a, FMT[a_fmt], M, K, a_scales, a_gran)
-    args.b = _tensor(b, FMT[b_fmt], N, K, b_scales, b_gran)
+    args.a = _tensor(a, FMT[a_fmt], M, K, a_scales, a_gran, a_scale_fmt)
+    args.b = _tensor(b, FMT[b_fmt], N, K, b_scales, b_gran, b_scale_fmt)
     args.bias = None if bias is None else bias.data_ptr()
     args.bias_dtype = F32 if bias is None else _dtype_code(bias)
     args.norm, args.norm_block, args.eps = NORM[norm], norm_block, eps
@@ -207,18 +207,36 @@ def make_linear_args(a, a_scales, b, b_scales, *, a_fmt="e4m3", b_fmt="e4m3", a_
     return args, y, y_scales
 
 
-def loka_fp8_linear_norm(a, a_scales, b, b_scales, stream=None, **kw):
-    """a4+a5.  Returns (y, y_scales or None)."""
+def _workspace(nbytes: int, device, ws=None):
+    if nbytes == 0:
+        return None, 0
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    return ws, ws.numel()
+
+
+def linear_workspace(args) -> int:
+    """Workspace bytes loka_fp8_linear_norm needs for args (UE8M0 blockwise scale packs; else 0)."""
+    return int(_lib.loka_linear_workspace_size(C.byref(args)))
+
+
+def loka_fp8_linear_norm(a, a_scales, b, b_scales, stream=None, ws=None, **kw):
+    """a4+a5.  Returns (y, y_scales or None).  ws: optional preallocated uint8 workspace."""
     args, y, ys = make_linear_args(a, a_scales, b, b_scales, **kw)
-    _check(_lib.loka_fp8_linear_norm(C.byref(args), None, 0, _stream(stream)), "loka_fp8_linear_norm")
+    ws, nws = _workspace(linear_workspace(args), a.device, ws)
+    _check(_lib.loka_fp8_linear_norm(C.byref(args), None if ws is None else C.c_void_p(ws.data_ptr()), nws,
+                                     _stream(stream)), "loka_fp8_linear_norm")
     return y, ys
 
 
-def loka_grouped_fp8_linear(args_list, stream=None):
+def loka_grouped_fp8_linear(args_list, stream=None, ws=None):
     """a6.  args_list: sequence of loka_linear_args (see make_linear_args)."""
     G = len(args_list)
     arr = (loka_linear_args * G)(*args_list)
-    _check(_lib.loka_grouped_fp8_linear(G, arr, None, 0, _stream(stream)), "loka_grouped_fp8_linear")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ws, nws = _workspace(int(_lib.loka_grouped_workspace_size(G, arr)), dev, ws)
+    _check(_lib.loka_grouped_fp8_linear(G, arr, None if ws is None else C.c_void_p(ws.data_ptr()), nws,
+                                        _stream(stream)), "loka_grouped_fp8_linear")
 
 
 def loka_probe_error(pairs, floor_rel: float = 1e-6, stream=None, stats=None, ws=None):

@@ -247,7 +247,47 @@ loka_status loka_quantize_grouped(int32_t G, const loka_tensor* x, loka_tensor* 
 }
 
 // ------------------------------------------------------------------------------------------
-size_t loka_linear_workspace_size(const loka_linear_args* /*a*/) { return 0; }
+// Native block-scaled (MX) recipe: blockwise UE8M0 scales on both operands (A 1x128, B 128x128
+// or 1x128).  A power-of-two block scale is four identical 1x32 MX scales, so the tensor core
+// applies them exactly (kind::mxf8f6f4.block_scale) and the accumulator is the dequantized
+// product: the full epilogue (bias, every norm, FP8 output) works as for rowwise.  The scales
+// are repacked into the MMA's 512-byte UE8M0 atoms in the workspace (sfpack.cu) first.
+static bool is_mx(const loka_linear_args* a) {
+  return a && a->a.gran == LOKA_GRAN_BLK_1x128 &&
+         (a->b.gran == LOKA_GRAN_BLK_128x128 || a->b.gran == LOKA_GRAN_BLK_1x128) &&
+         a->a.scale_fmt == LOKA_SCALE_UE8M0 && a->b.scale_fmt == LOKA_SCALE_UE8M0;
+}
+static size_t mx_pack_a_bytes(const loka_linear_args* a) {
+  return (size_t)cdiv(a->M, 128) * (size_t)cdiv(a->K, 128) * 512;
+}
+static size_t mx_pack_b_bytes(const loka_linear_args* a) {
+  return (size_t)cdiv(a->N, 256) * 2 * (size_t)cdiv(a->K, 128) * 512;
+}
+static size_t mx_ws_bytes(const loka_linear_args* a) {
+  if (!is_mx(a) || a->M <= 0 || a->N <= 0 || a->K <= 0) return 0;
+  return ((mx_pack_a_bytes(a) + 255) & ~size_t(255)) + mx_pack_b_bytes(a);
+}
+size_t loka_linear_workspace_size(const loka_linear_args* a) { return mx_ws_bytes(a); }
+
+// Pack the UE8M0 scales of an MX problem into ws and point p at the packs.
+static loka_status mx_pack(const loka_linear_args* a, LinearParams* p, void* ws, size_t ws_bytes, cudaStream_t s) {
+  const size_t need = mx_ws_bytes(a);
+  if (!ws || ws_bytes < need || !aligned16(ws)) return LOKA_ERR_WORKSPACE;
+  const int64_t kbs = cdiv(a->K, 128);
+  uint8_t* wa = static_cast<uint8_t*>(ws);
+  uint8_t* wb = wa + ((mx_pack_a_bytes(a) + 255) & ~size_t(255));
+  SfPackParams sp;
+  std::memset(&sp, 0, sizeof(sp));
+  sp.kblocks = (int32_t)kbs;
+  sp.seg[0] = {a->a.scales, kbs, a->M, 1, (int32_t)cdiv(a->M, 128), wa};
+  sp.seg[1] = {a->b.scales, kbs, a->N, a->b.gran == LOKA_GRAN_BLK_128x128 ? 128 : 1, (int32_t)(cdiv(a->N, 256) * 2),
+               wb};
+  if (launch_sf_pack(sp, s) != cudaSuccess) return LOKA_ERR_CUDA;
+  p->sfa_pack = wa;
+  p->sfb_pack = wb;
+  p->sf_kblocks = (int32_t)kbs;
+  return LOKA_OK;
+}
 
 static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CUtensorMap* tb, CUtensorMap* ty,
                                   LinearParams* p, int* bn_out) {
@@ -261,8 +301,9 @@ static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CU
   if (!A.data || !B.data || !Y.data || !A.scales || !B.scales) return LOKA_ERR_INVALID_ARG;
   if (!aligned16(A.data) || !aligned16(B.data) || !aligned16(Y.data)) return LOKA_ERR_INVALID_ARG;
   if (A.ld < K || B.ld < K || A.ld % 16 || B.ld % 16) return LOKA_ERR_INVALID_ARG;
-  if (A.gran != LOKA_GRAN_TENSOR && A.gran != LOKA_GRAN_ROW) return LOKA_ERR_UNSUPPORTED;
-  if (B.gran != LOKA_GRAN_TENSOR && B.gran != LOKA_GRAN_ROW) return LOKA_ERR_UNSUPPORTED;
+  const bool mx = is_mx(a);
+  if (!mx && A.gran != LOKA_GRAN_TENSOR && A.gran != LOKA_GRAN_ROW) return LOKA_ERR_UNSUPPORTED;
+  if (!mx && B.gran != LOKA_GRAN_TENSOR && B.gran != LOKA_GRAN_ROW) return LOKA_ERR_UNSUPPORTED;
   if (Y.dtype < LOKA_F32 || Y.dtype > LOKA_E5M2) return LOKA_ERR_INVALID_ARG;
   if (Y.ld < N || (Y.ld * elem_size(Y.dtype)) % 16) return LOKA_ERR_INVALID_ARG;
   const bool fp8_out = is_fp8(Y.dtype);
@@ -282,6 +323,7 @@ static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CU
   // a BlockNorm block must tile the CTA (BN % blk == 0) and cover whole epilogue quarters
   // (blk % (BN/4) == 0, each thread's BN/4 columns lie in one block)
   auto legal = [&](int c) {
+    if (mx && c < 128) return false;  // MX scale atoms cover 128 rows of B
     if (full_row && cdiv(N, c) > 8) return false;
     if (block && (c % blk || blk % (c / 4))) return false;
     return true;
@@ -292,7 +334,7 @@ static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CU
   for (int i = 0; i < 3 && !bn; ++i) {
     const int c = cands[i];
     if (!legal(c)) continue;
-    if (c > 64 && c / 2 >= N) continue;  // a narrower tile covers N as well
+    if (c > 64 && c / 2 >= N && !(mx && c == 128)) continue;  // a narrower tile covers N as well
     if (mb * cdiv(N, c) >= 120 || c == 64) bn = c;
   }
   for (int i = 2; i >= 0 && !bn; --i)  // fall back to the narrowest legal tile
@@ -328,6 +370,7 @@ static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CU
   p->ld_pre = N;
   p->status = a->status_dev;
   p->cluster_n = csize;
+  p->mx = mx ? 1 : 0;
   *bn_out = bn;
   return LOKA_OK;
 }
@@ -335,7 +378,7 @@ static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CU
 // Blockwise recipe (BW-F32, D6/D7): A scales 1x128, B scales 128x128 (or 1x128 for the
 // K-major copies of wgrad); FP32 promotion per 128-K block (blockwise.cu).  Epilogue: (+bias),
 // f32 / bf16 output, or FP8 with row scales when N <= 128.
-static bool is_blockwise(const loka_linear_args* a) { return a && a->a.gran == LOKA_GRAN_BLK_1x128; }
+static bool is_blockwise(const loka_linear_args* a) { return a && a->a.gran == LOKA_GRAN_BLK_1x128 && !is_mx(a); }
 
 static loka_status prepare_bw(const loka_linear_args* a, CUtensorMap* ta, CUtensorMap* tb, CUtensorMap* ty,
                               BwParams* p) {
@@ -388,15 +431,20 @@ static loka_status run_bw(const loka_linear_args* a, cudaStream_t s) {
   return launch_linear_bw(ta, tb, ty, p, s) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
 }
 
-loka_status loka_fp8_linear_norm(const loka_linear_args* a, void* /*ws*/, size_t /*ws_bytes*/, loka_stream_t stream) {
+loka_status loka_fp8_linear_norm(const loka_linear_args* a, void* ws, size_t ws_bytes, loka_stream_t stream) {
   if (is_blockwise(a)) return run_bw(a, reinterpret_cast<cudaStream_t>(stream));
   CUtensorMap ta, tb, ty;
   LinearParams p;
   int bn = 0;
   loka_status st = prepare_linear(a, &ta, &tb, &ty, &p, &bn);
   if (st != LOKA_OK) return st;
+  if (p.mx && (!ws || ws_bytes < mx_ws_bytes(a) || !aligned16(ws))) return LOKA_ERR_WORKSPACE;
   st = check_device();
   if (st != LOKA_OK) return st;
+  if (p.mx) {
+    st = mx_pack(a, &p, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+    if (st != LOKA_OK) return st;
+  }
   cudaError_t e = launch_linear(ta, tb, ty, p, bn, reinterpret_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
 }
@@ -457,7 +505,12 @@ loka_status loka_fp8_mlp_stack(const loka_stack_args* a, loka_stream_t stream) {
   return launch_stack(p, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
 }
 
-size_t loka_grouped_workspace_size(int32_t /*G*/, const loka_linear_args* /*a*/) { return 0; }
+// MX problems need their scale packs (each 256-byte aligned, back to back); everything else none.
+size_t loka_grouped_workspace_size(int32_t G, const loka_linear_args* a) {
+  size_t n = 0;
+  for (int g = 0; g < G && a; ++g) n += (mx_ws_bytes(&a[g]) + 255) & ~size_t(255);
+  return n;
+}
 
 loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* ws, size_t ws_bytes,
                                     loka_stream_t stream) {
@@ -474,8 +527,9 @@ loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* 
   int sms = 148;
   loka_status st = check_device(&sms);
   if (st != LOKA_OK) return st;
-  (void)ws;
-  (void)ws_bytes;
+  if (loka_grouped_workspace_size(G, a) > 0 &&
+      (!ws || ws_bytes < loka_grouped_workspace_size(G, a) || !aligned16(ws)))
+    return LOKA_ERR_WORKSPACE;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   // Problems with a plain dequant(+bias) epilogue and bf16 output run in persistent grouped
   // launches (<= kMaxGroups problems each, longest K first); row-coupled epilogues (norms, FP8
@@ -483,7 +537,7 @@ loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* 
   std::vector<int> grouped, single;
   for (int g = 0; g < G; ++g) {
     const bool ok = a[g].norm == LOKA_NORM_NONE && a[g].y.dtype == LOKA_BF16 && !a[g].debug_precast &&
-                    !is_blockwise(&a[g]);
+                    !is_blockwise(&a[g]) && !is_mx(&a[g]);
     (ok ? grouped : single).push_back(g);
   }
   std::stable_sort(grouped.begin(), grouped.end(), [&](int x, int y) { return a[x].K > a[y].K; });
@@ -515,7 +569,14 @@ loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* 
     }
     if (launch_grouped(gp, sms, s) != cudaSuccess) return LOKA_ERR_CUDA;
   }
+  size_t ws_off = 0;
   for (int g : single) {
+    if (is_mx(&a[g])) {
+      const size_t nb = (mx_ws_bytes(&a[g]) + 255) & ~size_t(255);
+      loka_status sm = mx_pack(&a[g], &p[g], static_cast<uint8_t*>(ws) + ws_off, nb, s);
+      if (sm != LOKA_OK) return sm;
+      ws_off += nb;
+    }
     if (is_blockwise(&a[g])) {
       loka_status sb = run_bw(&a[g], s);
       if (sb != LOKA_OK) return sb;

@@ -263,6 +263,47 @@ LOKA_DEVINL void mma_f8f6f4(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t 
       "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// ---- block-scaled (MX) MMA: kind::mxf8f6f4.block_scale, UE8M0 scale per 32 K, scales in TMEM ----
+// Instruction descriptor (block-scaled form): b_sf_id [4,6), a/b format [7,10)/[10,13), N>>3
+// [17,23), scale format [23] (1 = UE8M0), M>>4 [24,29), a_sf_id [29,31).
+LOKA_DEVINL uint32_t idesc_mxf8f6f4(int a_fmt, int b_fmt, uint32_t M, uint32_t N) {
+  uint32_t d = 0;
+  d |= (uint32_t)a_fmt << 7;
+  d |= (uint32_t)b_fmt << 10;
+  d |= (N >> 3) << 17;
+  d |= 1u << 23;  // UE8M0 scales
+  d |= (M >> 4) << 24;
+  return d;
+}
+// sf_id k selects byte k of the 32-bit TMEM scale word (the k-th 32-wide K block of a 128-K
+// group); it is carried both in the descriptor and in the top two bits of the TMEM addresses.
+LOKA_DEVINL void mma_mxf8f6f4(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t tsfa, uint32_t tsfb,
+                              uint32_t k, uint32_t accumulate) {
+  const uint32_t id = idesc | (k << 29) | (k << 4);
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %6, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%4], [%5], p;\n}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(id), "r"(tsfa | (k << 30)), "r"(tsfb | (k << 30)), "r"(accumulate)
+      : "memory");
+}
+// smem -> TMEM copy of one 32 x 16 B scale-factor atom, broadcast to the four 32-lane groups
+// (lane i of every group gets row i: 4 TMEM columns).  Source: no-swizzle K-major descriptor,
+// 8-row core matrices 128 B apart (SBO).
+LOKA_DEVINL void utccp_32x128b_warpx4(uint32_t tmem_dst, uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)(128u >> 4) << 16;  // LBO (single 16 B column: unused)
+  d |= (uint64_t)(128u >> 4) << 32;  // SBO = 128 B
+  d |= (uint64_t)1u << 46;           // version; layout type 0 = no swizzle
+  asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(tmem_dst), "l"(d) : "memory");
+}
+// 1-D bulk copy global -> own shared memory, completing as transaction bytes on `bar`.
+LOKA_DEVINL void bulk_load_g2s(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst_smem)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 LOKA_DEVINL void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -329,6 +370,14 @@ LOKA_DEVINL uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
 }
 LOKA_DEVINL void st_dsmem_f4(uint32_t addr, float4 v) {
   asm volatile("st.shared::cluster.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+// Bulk (TMA-engine) copy of `bytes` (multiple of 16) from this CTA's shared memory to a cluster
+// peer's; completes as transaction bytes on the peer's mbarrier (both cluster addresses, mapa).
+LOKA_DEVINL void bulk_copy_s2cluster(uint32_t dst_cluster, uint32_t src_cta, uint32_t bytes, uint32_t mbar_cluster) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   dst_cluster),
+               "r"(src_cta), "r"(bytes), "r"(mbar_cluster)
                : "memory");
 }
 LOKA_DEVINL void st_dsmem_f32(uint32_t addr, float v) {

@@ -56,7 +56,27 @@ struct LinearParams {
   float* precast; int64_t ld_pre;
   int32_t* status;
   int32_t cluster_n;             // CTAs per cluster along N (1 = no cross-CTA row exchange)
+  // native block-scaled (MX) mode: UE8M0 blockwise scales applied by the tensor core; sa/sb unused
+  int32_t mx;
+  const uint8_t* sfa_pack;       // [ceil(M/128)][kblocks][512] (sfpack.cu layout)
+  const uint8_t* sfb_pack;       // [ceil(N/256)*2][kblocks][512]
+  int32_t sf_kblocks;            // ceil(K/128)
 };
+
+// ---- UE8M0 scale packing for the MX mode (sfpack.cu) ----
+struct SfPackSeg {
+  const float* scales;  // FP32 powers of two, [rows / row_div, ld] row-major
+  int64_t ld;
+  int64_t rows;         // operand rows
+  int32_t row_div;      // 1 (1x128 scales) or 128 (128x128 scales)
+  int32_t row_blocks;   // 128-row atoms to write (>= ceil(rows/128))
+  uint8_t* out;         // [row_blocks][kblocks][512]
+};
+struct SfPackParams {
+  SfPackSeg seg[2];
+  int32_t kblocks;
+};
+cudaError_t launch_sf_pack(const SfPackParams& p, cudaStream_t st);
 
 // Launch one linear+norm problem.  tma_a/tma_b are 2D maps over the FP8 operands with box
 // {128 (K), 128 (A rows)} and {128 (K), bn (B rows)}, 128B swizzle.
@@ -81,6 +101,7 @@ struct StackParams {
   int32_t* status;
 };
 cudaError_t launch_stack(const StackParams& p, cudaStream_t st);
+long long stack_debug_trace(int enable, unsigned long long* out, long long n);  // see loka_debug_trace
 
 // ---- blockwise-scaled GEMM with FP32 promotion (blockwise.cu) ----
 struct BwParams {

@@ -49,29 +49,37 @@ constexpr int kBK = 128;                    // FP8 elements of K per stage (128 
 constexpr int kRec = 6;                     // floats per (row, quarter) record: n, mean, m2, ss, ymax, ymin
 constexpr int kMaxCluster = 8;
 
-template <int BN> struct LinCfg {
+constexpr uint32_t pow2_cols(uint32_t c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
+
+template <int BN, bool MX = false> struct LinCfg {
   static constexpr int kCPT = BN / 4;  // columns per epilogue thread
   static constexpr int kStageA = 128 * kBK;  // bytes
   static constexpr int kStageB = BN * kBK;
   static constexpr int kStageBytes = kStageA + kStageB;
+  // MX mode: per stage one 512 B UE8M0 atom for A and BN/128 for B (bulk-copied with the stage),
+  // copied to TMEM columns [BN + s*kSfCols, ...) by tcgen05.cp
+  static constexpr int kSf = MX ? 512 * (1 + BN / 128) : 0;
+  static constexpr int kSfCols = 4 * (1 + BN / 128);
   // everything but the operand ring: column params, pushed cluster records (+ amax), barriers
   static constexpr int kFixed = 4 * BN * 4 + kMaxCluster * 128 * 16 + kMaxCluster * 128 * 4 + 512 + 1024;
-  static constexpr int kStagesFit = (227 * 1024 - kFixed) / kStageBytes;
+  static constexpr int kStagesFit = (227 * 1024 - kFixed) / (kStageBytes + kSf);
   static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
-  static constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
+  static constexpr uint32_t kTmemCols = pow2_cols(MX ? BN + kStages * kSfCols : BN);
   static constexpr int kOffB = kStages * kStageA;
   static constexpr int kOffBar = kOffB + kStages * kStageB;
   static constexpr int kOffTmem = kOffBar + (2 * kStages + 1) * 8;
   static constexpr int kOffCol = (kOffTmem + 4 + 15) & ~15;         // sb, bias, gamma, beta [BN]
   static constexpr int kOffCs = kOffCol + 4 * BN * 4;                // [kMaxCluster][128] float4 records
   static constexpr int kOffCs2 = kOffCs + kMaxCluster * 128 * 16;    // [kMaxCluster][128] amax
-  static constexpr int kSmemBytes = kOffCs2 + kMaxCluster * 128 * 4 + 1024;  // + alignment slack
+  static constexpr int kOffSf = kOffCs2 + kMaxCluster * 128 * 4;         // [kStages][kSf] (MX)
+  static constexpr int kSmemBytes = kOffSf + kStages * kSf + 1024;       // + alignment slack
   // after the mainloop the (drained) operand ring holds the quarter exchange [4][kRec + 1][128]
   // floats at offset 0 and the output staging tile (128 rows x BN x <= 4 bytes) at kOffStage
   static constexpr int kOffStage = 16384;
   static_assert(4 * (kRec + 1) * 128 * 4 <= kOffStage, "hx alias");
   static_assert(kOffStage + 128 * BN * 4 <= kStages * kStageBytes, "staging alias");
   static_assert(kStages >= 2 && kSmemBytes <= 227 * 1024, "smem");
+  static_assert(!MX || BN % 128 == 0, "MX scale atoms cover 128 rows of B");
 };
 
 // Row statistics of a column partition: (n, mean, M2) for LayerNorm (merged with the batched
@@ -109,11 +117,11 @@ LOKA_DEVINL RowRec merge_recs(const RowRec (&r)[K]) {
   return o;
 }
 
-template <int BN>
+template <int BN, bool MX>
 __global__ void __launch_bounds__(kThreads, 1)
     linear_norm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                        const __grid_constant__ CUtensorMap tma_y, const LinearParams p) {
-  using C = LinCfg<BN>;
+  using C = LinCfg<BN, MX>;
   constexpr int CPT = C::kCPT;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -173,9 +181,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int s = kb % C::kStages;
         const uint32_t ph = (uint32_t)(kb / C::kStages) & 1u;
         mbar_wait(&empty_bar[s], ph ^ 1u, 1);
-        mbar_arrive_expect_tx(&full_bar[s], C::kStageBytes);
+        mbar_arrive_expect_tx(&full_bar[s], C::kStageBytes + C::kSf);
         tma_load_2d(sA + s * C::kStageA, &tma_a, &full_bar[s], kb * kBK, m0);
         tma_load_2d(sB + s * C::kStageB, &tma_b, &full_bar[s], kb * kBK, n0);
+        if constexpr (MX) {  // the stage's UE8M0 atoms: A rows m0.., B rows n0.. (BN/128 atoms)
+          uint8_t* sf = smem + C::kOffSf + s * C::kSf;
+          bulk_load_g2s(sf, p.sfa_pack + ((size_t)(m0 >> 7) * p.sf_kblocks + kb) * 512, 512, &full_bar[s]);
+#pragma unroll
+          for (int j = 0; j < BN / 128; ++j)
+            bulk_load_g2s(sf + 512 * (j + 1), p.sfb_pack + ((size_t)((n0 >> 7) + j) * p.sf_kblocks + kb) * 512, 512,
+                          &full_bar[s]);
+        }
         if (kb == 0) LOKA_TRACE(2);
       }
     }
@@ -183,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ===== MMA issuer =====
     if (lane == 0) {
-      const uint32_t idesc = idesc_f8f6f4(p.a_fmt, p.b_fmt, 128, BN);
+      const uint32_t idesc = MX ? idesc_mxf8f6f4(p.a_fmt, p.b_fmt, 128, BN) : idesc_f8f6f4(p.a_fmt, p.b_fmt, 128, BN);
       for (int kb = 0; kb < num_kb; ++kb) {
         const int s = kb % C::kStages;
         const uint32_t ph = (uint32_t)(kb / C::kStages) & 1u;
@@ -192,10 +208,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t a0 = smem_u32(sA + s * C::kStageA);
         const uint32_t b0 = smem_u32(sB + s * C::kStageB);
+        if constexpr (MX) {
+          // scales smem -> TMEM (executes in order with the MMAs issued by this thread)
+          const uint32_t sft = tmem_base + (uint32_t)(BN + s * C::kSfCols);
+          const uint32_t sfs = smem_u32(smem + C::kOffSf + s * C::kSf);
 #pragma unroll
-        for (int k = 0; k < kBK / 32; ++k) {
-          mma_f8f6f4(tmem_base, smem_desc_kmajor_sw128(a0 + k * 32), smem_desc_kmajor_sw128(b0 + k * 32), idesc,
-                     (kb | k) != 0);
+          for (int j = 0; j <= BN / 128; ++j) utccp_32x128b_warpx4(sft + 4u * j, sfs + 512u * j);
+#pragma unroll
+          for (int k = 0; k < kBK / 32; ++k)
+            mma_mxf8f6f4(tmem_base, smem_desc_kmajor_sw128(a0 + k * 32), smem_desc_kmajor_sw128(b0 + k * 32), idesc,
+                         sft, sft + 4u, (uint32_t)k, (kb | k) != 0);
+        } else {
+#pragma unroll
+          for (int k = 0; k < kBK / 32; ++k) {
+            mma_f8f6f4(tmem_base, smem_desc_kmajor_sw128(a0 + k * 32), smem_desc_kmajor_sw128(b0 + k * 32), idesc,
+                       (kb | k) != 0);
+          }
         }
         mma_commit(&empty_bar[s]);
       }
@@ -214,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int cb = cq * CPT;                         // first local column of this thread
     const int nv = max(0, min(CPT, ncols - cb));     // valid columns of this thread
     const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)cb;
-    const float sa = row_ok ? p.sa[p.sa_row ? grow : 0] : 0.f;
+    const float sa = row_ok ? (MX ? 1.f : p.sa[p.sa_row ? grow : 0]) : 0.f;  // MX: scales applied by the MMA
     const bool has_bias = p.bias != nullptr;
     const bool fold = !has_bias && norm != LOKA_NORM_NONE;  // s_a folded into eps
     const float ys = fold ? 1.f : sa;
@@ -225,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = threadIdx.x; j < BN; j += kEpiThreads) {
       const int n = n0 + j;
       const bool ok = n < p.N;
-      col[j] = ok ? p.sb[p.sb_row ? n : 0] : 0.f;
+      col[j] = ok ? (MX ? 1.f : p.sb[p.sb_row ? n : 0]) : 0.f;
       float b = 0.f;
       if (ok && p.bias) b = p.bias_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.bias)[n])
                                          : reinterpret_cast<const float*>(p.bias)[n];
@@ -570,6 +598,13 @@ long long debug_trace(int enable, unsigned long long* out, long long n) {
     got = n < (long long)kTraceCtas * 16 ? n : (long long)kTraceCtas * 16;
     if (cudaMemcpyFromSymbol(out, g_trace, (size_t)got * 8) != cudaSuccess) return -1;
   }
+  if (n > (long long)kTraceCtas * 16) {
+    const long long g2 = stack_debug_trace(enable, out + (size_t)kTraceCtas * 16, n - (long long)kTraceCtas * 16);
+    if (g2 < 0) return -1;
+    got += g2;
+  } else if (stack_debug_trace(enable, nullptr, 0) < 0) {
+    return -1;
+  }
   if (enable >= 0) {
     if (enable) {
       static unsigned long long zero[kTraceCtas * 16];
@@ -580,13 +615,13 @@ long long debug_trace(int enable, unsigned long long* out, long long n) {
   return got;
 }
 
-template <int BN>
+template <int BN, bool MX>
 static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, const LinearParams& p,
                              cudaStream_t st) {
-  using C = LinCfg<BN>;
+  using C = LinCfg<BN, MX>;
   static bool attr_done = false;  // idempotent; racing threads set the same value
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(linear_norm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(linear_norm_kernel<BN, MX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr_done = true;
@@ -605,17 +640,24 @@ static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, linear_norm_kernel<BN>, ta, tb, ty, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, linear_norm_kernel<BN, MX>, ta, tb, ty, p);
   note_launch();
   return e;
 }
 
 cudaError_t launch_linear(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, const LinearParams& p,
                           int bn, cudaStream_t st) {
+  if (p.mx) {
+    switch (bn) {
+      case 128: return launch_bn<128, true>(ta, tb, ty, p, st);
+      case 256: return launch_bn<256, true>(ta, tb, ty, p, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (bn) {
-    case 64: return launch_bn<64>(ta, tb, ty, p, st);
-    case 128: return launch_bn<128>(ta, tb, ty, p, st);
-    case 256: return launch_bn<256>(ta, tb, ty, p, st);
+    case 64: return launch_bn<64, false>(ta, tb, ty, p, st);
+    case 128: return launch_bn<128, false>(ta, tb, ty, p, st);
+    case 256: return launch_bn<256, false>(ta, tb, ty, p, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -10,8 +10,10 @@
 //   * the epilogue (same arithmetic as linear.cu: s_a folded into eps, packed FP32x2 statistics,
 //     quarter merge in smem, cluster exchange of (mean, M2, ymax, ymin) pushed with DSMEM stores,
 //     one-FFMA normalisation, row amax from ymax/ymin) produces the next layer's e4m3 codes and
-//     row scale, and writes the codes straight into EVERY cluster CTA's A buffer with
-//     st.shared::cluster.v4 (then fence.proxy.async + cluster barrier before the next MMA);
+//     row scale, writes its codes into its own A tile and sends that slice to every peer's A tile
+//     with one bulk (TMA-engine) shared::cta -> shared::cluster copy per peer, completing on the
+//     peer's a_full mbarrier (slices narrower than a 128-wide K block: per-thread DSMEM stores +
+//     cluster barrier); the next layer's MMAs start when a_full flips;
 //   * only the last layer's output goes to HBM (swizzled staging tile + TMA store).
 // The codes and scales are bit-identical to the per-layer chain of linear_norm_kernel launches.
 #include "common.cuh"
@@ -32,6 +34,18 @@ constexpr int kSOffCol = kSOffCs + 8 * 128 * 16;         // [kSBNMax] W row scal
 constexpr int kSOffBar = kSOffCol + kSBNMax * 4;
 constexpr int kSSmem = kSOffBar + 128 + 1024;
 static_assert(kSSmem <= 227 * 1024, "stack smem");
+
+// Opt-in phase trace (loka_debug_trace): per CTA 64 globaltimer stamps — 0 entry, 1 setup done,
+// then per layer l at 2 + 7 l: +0 first weight stage landed (MMA), +1 last MMA committed,
+// +2 accumulator ready (epilogue), +3 quarters merged, +4 cluster merged, +5 codes pushed,
+// +6 next-layer A complete (MMA issuer saw a_full).
+constexpr int kSTraceCtas = 512;
+static __device__ unsigned long long g_strace[kSTraceCtas * 64];
+static __device__ int g_strace_on;
+#define LOKA_STRACE(c, slot)                                                                    \
+  do {                                                                                          \
+    if ((c).trace && (c).cta < kSTraceCtas) g_strace[(c).cta * 64 + (slot)] = globaltimer_ns(); \
+  } while (0)
 
 struct SRow {
   float n, mean, m2, ss, ymax, ymin;
@@ -65,6 +79,8 @@ struct SCtx {
   uint8_t* smem;
   uint32_t tmem_base;
   int warp, lane, q, cq, r, grow, m0, rank, C;
+  int trace, cta;
+  uint64_t* a_full;  // layer-input-complete barrier (TMA X load, then peers' bulk copies)
   bool row_ok;
 };
 
@@ -160,6 +176,7 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
       parts[k].ymax = o[512]; parts[k].ymin = o[640];
     }
     rec = merge_rows(parts);
+    if (threadIdx.x == 0) LOKA_STRACE(c, 2 + 7 * l + 3);
     if (c.C == 1) named_bar_sync(1, kSThreads);  // hx (aliasing A) read by all before A is rewritten
   }
   // ---- cluster exchange: push (mean|ss, m2, ymax, ymin) to every peer, barrier, merge ----
@@ -170,6 +187,7 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
       for (int rk = 0; rk < c.C; ++rk) st_dsmem_f4(mapa_shared(la, (uint32_t)rk), v);
     }
     cluster_sync_all();  // barrier 1: also proves every cluster CTA finished this layer's MMAs
+    if (threadIdx.x == 0) LOKA_STRACE(c, 2 + 7 * l + 4);
     SRow parts[8];
 #pragma unroll
     for (int rk = 0; rk < 8; ++rk) {
@@ -234,11 +252,32 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
                            ((((uint32_t)(k & 127) >> 4) ^ ((uint32_t)c.r & 7u)) << 4);
       const float4 v = make_float4(__uint_as_float(w[0]), __uint_as_float(w[1]), __uint_as_float(w[2]),
                                    __uint_as_float(w[3]));
-      for (int rk = 0; rk < c.C; ++rk) st_dsmem_f4(mapa_shared(a_local + off, (uint32_t)rk), v);
+      sts_u4(a_local + off, make_uint4(w[0], w[1], w[2], w[3]));
+      if constexpr (BN < 128) {  // slice not contiguous in the swizzled tile: per-thread DSMEM stores
+        for (int rk = 0; rk < c.C; ++rk)
+          if (rk != c.rank) st_dsmem_f4(mapa_shared(a_local + off, (uint32_t)rk), v);
+      }
     }
-    asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");  // generic writes -> tensor-core reads
-    if (c.C > 1) cluster_sync_all();  // barrier 2: h_{l+1} complete in every CTA
-    else named_bar_sync(1, kSThreads);
+    if (BN >= 128 || c.C == 1) {
+      // The slice [n0, n0 + BN) of h_{l+1} is BN/128 whole 16 KB K-blocks of the A tile: one bulk
+      // (TMA-engine) copy per peer, completing on the peer's a_full barrier.  Peers' A tiles are free:
+      // barrier 1 above proved every cluster CTA's layer-l MMAs (and its hx reads) completed.
+      fence_proxy_async_smem();  // generic writes -> async proxy (bulk-copy source, own MMA)
+      named_bar_sync(1, kSThreads);
+      if (threadIdx.x == 0) {
+        const uint32_t src = a_local + (uint32_t)(n0 >> 7) * 16384u, bytes = (uint32_t)BN * 128u;
+        for (int rk = 0; rk < c.C; ++rk)
+          if (rk != c.rank)
+            bulk_copy_s2cluster(mapa_shared(src, (uint32_t)rk), src, bytes, mapa_shared(smem_u32(c.a_full), (uint32_t)rk));
+        mbar_arrive_expect_tx(c.a_full, (uint32_t)(c.C - 1) * bytes);
+        LOKA_STRACE(c, 2 + 7 * l + 5);
+      }
+    } else {
+      asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");  // generic writes -> tensor-core reads
+      if (threadIdx.x == 0) LOKA_STRACE(c, 2 + 7 * l + 5);
+      cluster_sync_all();  // barrier 2: h_{l+1} complete in every CTA
+      if (threadIdx.x == 0) mbar_arrive_expect_tx(c.a_full, 0u);
+    }
     return s_out;
   }
   // ---- last layer: output tile -> swizzled staging (reuses A) -> TMA store ----
@@ -321,6 +360,10 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
   c.row_ok = c.grow < p.M;
   c.C = p.C;
   c.rank = p.C > 1 ? (int)cluster_ctarank() : 0;
+  c.a_full = a_full;
+  c.trace = *reinterpret_cast<volatile int*>(&g_strace_on);
+  c.cta = blockIdx.x + gridDim.x * blockIdx.y;
+  if (threadIdx.x == 0) LOKA_STRACE(c, 0);
 
   if (c.warp == 0 && c.lane == 0) {
     tma_prefetch_desc(&p.tx);
@@ -341,6 +384,7 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
   tc_fence_after();
   c.tmem_base = *tmem_slot;
   if (p.C > 1) cluster_sync_all();  // every cluster CTA is running before any DSMEM traffic
+  if (threadIdx.x == 0) LOKA_STRACE(c, 1);
 
   float sa = c.row_ok ? p.xs[c.grow] : 0.f;  // row scale of the current layer input
   int prod_it = 0, mma_it = 0;
@@ -368,14 +412,15 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
       }
     }
     if (c.warp == 1 && c.lane == 0) {  // ===== MMA issuer =====
-      if (l == 0) mbar_wait(a_full, 0, 5);
-      else asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // DSMEM-written A -> tensor core
+      mbar_wait(a_full, (uint32_t)l & 1u, 5);  // h_l complete: X by TMA, then own slice + peers' bulk copies
       tc_fence_after();
+      if (l > 0) LOKA_STRACE(c, 2 + 7 * (l - 1) + 6);
       const uint32_t idesc = idesc_f8f6f4(0, 0, 128, (uint32_t)p.BN[l]);
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = mma_it % kSStages;
         mbar_wait(&full_bar[s], (uint32_t)(mma_it / kSStages) & 1u, 2);
         tc_fence_after();
+        if (kb == 0) LOKA_STRACE(c, 2 + 7 * l);
         const uint32_t a0 = smem_u32(sA + kb * 16384), b0 = smem_u32(sW + s * kSStageW);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
@@ -385,6 +430,7 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
         ++mma_it;
       }
       mma_commit(tmem_full);
+      LOKA_STRACE(c, 2 + 7 * l + 1);
     }
     __syncwarp();
     // ===== epilogue (all warps) =====
@@ -394,6 +440,7 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
     if (c.lane == 0) mbar_wait(tmem_full, (uint32_t)l & 1u, 3);
     __syncwarp();
     tc_fence_after();
+    if (threadIdx.x == 0) LOKA_STRACE(c, 2 + 7 * l + 2);
     float s_next;
     switch (p.BN[l]) {
       case 64: s_next = stack_epilogue<16>(p, c, l, sa); break;
@@ -409,6 +456,22 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
     tc_fence_after();
     tmem_dealloc<kSBNMax>(c.tmem_base);
   }
+}
+
+long long stack_debug_trace(int enable, unsigned long long* out, long long n) {
+  long long got = 0;
+  if (out && n > 0) {
+    got = n < (long long)kSTraceCtas * 64 ? n : (long long)kSTraceCtas * 64;
+    if (cudaMemcpyFromSymbol(out, g_strace, (size_t)got * 8) != cudaSuccess) return -1;
+  }
+  if (enable >= 0) {
+    if (enable) {
+      static unsigned long long zero[kSTraceCtas * 64];
+      if (cudaMemcpyToSymbol(g_strace, zero, sizeof(zero)) != cudaSuccess) return -1;
+    }
+    if (cudaMemcpyToSymbol(g_strace_on, &enable, sizeof(int)) != cudaSuccess) return -1;
+  }
+  return got;
 }
 
 cudaError_t launch_stack(const StackParams& p, cudaStream_t st) {

@@ -1,0 +1,35 @@
+"""Per-CTA phase timeline of the fused cfg2 stack launch (loka_debug_trace, stack slots)."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+import paper_2605_10886_b200 as lk  # noqa: E402
+
+DIMS = synth.CFG2_DIMS
+dev = torch.device("cuda")
+M = int(os.environ.get("M", "4096"))
+x = synth.gaussian(M, DIMS[0], 0, device=dev)
+xq, xs = lk.loka_quantize(x, "e4m3", "row")
+ws = [lk.loka_quantize(synth.weight(DIMS[l + 1], DIMS[l], 100 + l, device=dev), "e4m3", "row") for l in range(8)]
+for rep in range(4):
+    torch.cuda.synchronize()
+    if rep == 3:
+        lk.debug_trace(1)
+    y, _ = lk.loka_fp8_mlp_stack(xq, xs, ws, norms="layer", out_dtype="bf16")
+    torch.cuda.synchronize()
+t = np.array(lk.debug_trace(0, 65536 + 512 * 64), dtype=np.int64)[65536:].reshape(-1, 64)[:, :58]
+t = t[t[:, 0] > 0]
+base = t[:, 0].min()
+rel = np.where(t > 0, (t - base) / 1000.0, np.nan)
+med = np.nanmedian(rel, axis=0)
+mx = np.nanmax(rel, axis=0)
+print(f"ctas={len(t)} entry {med[0]:.2f}/{mx[0]:.2f} setup {med[1]:.2f}/{mx[1]:.2f} end(max last stamp) {np.nanmax(rel):.2f} us")
+names = ["w_landed", "mma_done", "acc_ready", "q_merged", "cl_merged", "pushed", "A_ready"]
+for l in range(8):
+    b = 2 + 7 * l
+    print(f"L{l} K={DIMS[l]} N={DIMS[l + 1]}: " + " ".join(f"{n}={med[b + i]:.2f}/{mx[b + i]:.2f}" for i, n in enumerate(names)))
