@@ -27,6 +27,9 @@ RECIPES = {
     "tensorwise": dict(fx="tensor", fw="tensor", gdy="tensor", gw="tensor", wdy="tensor", wx="tensor"),
     "blockwise": dict(fx="blk_1x128", fw="blk_128x128", gdy="blk_1x128", gw="blk_128x128", wdy="blk_128x1",
                       wx="blk_128x1"),
+    # same granules with UE8M0 scales: native block-scaled MMA (kind::mxf8f6f4.block_scale)
+    "blockwise_ue8m0": dict(fx="blk_1x128", fw="blk_128x128", gdy="blk_1x128", gw="blk_128x128", wdy="blk_128x1",
+                            wx="blk_128x1", sf="ue8m0"),
 }
 T = {"row": "col", "col": "row", "blk_1x128": "blk_128x1", "blk_128x1": "blk_1x128"}
 
@@ -60,38 +63,43 @@ def main():
     with torch.cuda.stream(stream):
         for name, g in RECIPES.items():
             # quantized operands (and their K-major transposed copies)
-            xq, xs = lk.loka_quantize(x, "e4m3", g["fx"])
-            wq, ws = lk.loka_quantize(w, "e4m3", g["fw"])
-            gq, gs = lk.loka_quantize(dy, "e5m2", g["gdy"])
-            _, _, wtq, wts = lk.loka_quantize(w, "e4m3", g["gw"], want_q=False, transpose=True)
-            _, _, gtq, gts = lk.loka_quantize(dy, "e5m2", g["wdy"], want_q=False, transpose=True)
-            _, _, xtq, xts = lk.loka_quantize(x, "e4m3", g["wx"], want_q=False, transpose=True)
+            sf = g.get("sf", "f32")
+            xq, xs = lk.loka_quantize(x, "e4m3", g["fx"], sf)
+            wq, ws = lk.loka_quantize(w, "e4m3", g["fw"], sf)
+            gq, gs = lk.loka_quantize(dy, "e5m2", g["gdy"], sf)
+            _, _, wtq, wts = lk.loka_quantize(w, "e4m3", g["gw"], sf, want_q=False, transpose=True)
+            _, _, gtq, gts = lk.loka_quantize(dy, "e5m2", g["wdy"], sf, want_q=False, transpose=True)
+            _, _, xtq, xts = lk.loka_quantize(x, "e4m3", g["wx"], sf, want_q=False, transpose=True)
             keep = []
-            fa, yy, _ = lk.make_linear_args(xq, xs, wq, ws, a_gran=g["fx"], b_gran=g["fw"], out_dtype="bf16", keep=keep)
+            kw = dict(a_scale_fmt=sf, b_scale_fmt=sf, keep=keep)
+            fa, yy, _ = lk.make_linear_args(xq, xs, wq, ws, a_gran=g["fx"], b_gran=g["fw"], out_dtype="bf16", **kw)
             da, dx, _ = lk.make_linear_args(gq, gs, wtq, wts, a_fmt="e5m2", a_gran=g["gdy"],
-                                            b_gran=T.get(g["gw"], g["gw"]), out_dtype="bf16", keep=keep)
+                                            b_gran=T.get(g["gw"], g["gw"]), out_dtype="bf16", **kw)
             wa, dw, _ = lk.make_linear_args(gtq, gts, xtq, xts, a_fmt="e5m2", a_gran=T.get(g["wdy"], g["wdy"]),
-                                            b_gran=T.get(g["wx"], g["wx"]), out_dtype="f32", keep=keep)
+                                            b_gran=T.get(g["wx"], g["wx"]), out_dtype="f32", **kw)
             sh = stream.cuda_stream
-            run = lambda ar: lk._lib.loka_fp8_linear_norm(lk.C.byref(ar) if hasattr(lk, "C") else None, None, 0, sh)
             import ctypes
-            one = lambda ar: (lambda: lk._lib.loka_fp8_linear_norm(ctypes.byref(ar), None, 0, sh))
+            wsb = {id(ar): torch.empty(max(1, lk.linear_workspace(ar)), dtype=torch.uint8, device=dev)
+                   for ar in (fa, da, wa)}
+            call = lambda ar: lk._lib.loka_fp8_linear_norm(ctypes.byref(ar), ctypes.c_void_p(wsb[id(ar)].data_ptr()),
+                                                           wsb[id(ar)].numel(), sh)
+            one = lambda ar: (lambda: call(ar))
             t_f, t_d, t_w = tmean(one(fa)), tmean(one(da)), tmean(one(wa))
 
             def quant(src, fmt, g_plain, g_t, q, s, qt, st):
                 # one pass writes both layouts when the two directions share the granules
                 if g_plain == g_t:
-                    lk.loka_quantize(src, fmt, g_plain, out=q, scales=s, transpose=True, out_t=qt, scales_t=st)
+                    lk.loka_quantize(src, fmt, g_plain, sf, out=q, scales=s, transpose=True, out_t=qt, scales_t=st)
                 else:
-                    lk.loka_quantize(src, fmt, g_plain, out=q, scales=s)
-                    lk.loka_quantize(src, fmt, g_t, want_q=False, transpose=True, out_t=qt, scales_t=st)
+                    lk.loka_quantize(src, fmt, g_plain, sf, out=q, scales=s)
+                    lk.loka_quantize(src, fmt, g_t, sf, want_q=False, transpose=True, out_t=qt, scales_t=st)
 
             def step():  # every quantize (incl. the K-major copies) and the three GEMMs
                 quant(x, "e4m3", g["fx"], g["wx"], xq, xs, xtq, xts)
                 quant(w, "e4m3", g["fw"], g["gw"], wq, ws, wtq, wts)
                 quant(dy, "e5m2", g["gdy"], g["wdy"], gq, gs, gtq, gts)
                 for ar in (fa, da, wa):
-                    assert lk._lib.loka_fp8_linear_norm(ctypes.byref(ar), None, 0, sh) == 0
+                    assert call(ar) == 0
 
             t_s = tmean(step, max(5, a.steps // 2))
             res[name] = {
