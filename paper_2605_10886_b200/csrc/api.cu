@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -72,7 +73,8 @@ static int elem_size(loka_dtype t) { return t == LOKA_F32 ? 4 : t == LOKA_BF16 ?
 
 // 2D map over the GEMM output [rows, cols] of dtype t (ld elements), box {min(128, bn*e) bytes,
 // 128 rows} with the matching 128B / 64B swizzle — the layout of the epilogue's staging tile.
-static bool make_map_out(CUtensorMap* m, void* ptr, int64_t rows, int64_t cols, int64_t ld, loka_dtype t, int bn) {
+static bool make_map_out(CUtensorMap* m, void* ptr, int64_t rows, int64_t cols, int64_t ld, loka_dtype t, int bn,
+                         uint32_t box_rows = 128) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
   const int e = elem_size(t);
@@ -82,7 +84,7 @@ static bool make_map_out(CUtensorMap* m, void* ptr, int64_t rows, int64_t cols, 
                                                   : CU_TENSOR_MAP_DATA_TYPE_UINT8;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)(ld * e)};
-  cuuint32_t box[2] = {(cuuint32_t)(box_bytes / e), 128u};
+  cuuint32_t box[2] = {(cuuint32_t)(box_bytes / e), box_rows};
   cuuint32_t es[2] = {1u, 1u};
   return enc(m, dt, 2, ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
              box_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
@@ -505,6 +507,16 @@ loka_status loka_fp8_mlp_stack(const loka_stack_args* a, loka_stream_t stream) {
   return launch_stack(p, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
 }
 
+// Grouped GEMM engine: the CTA-pair kernel (gemm2.cu) unless LOKA_GROUPED_1CTA=1 selects the
+// single-CTA 128 x 128 kernel (grouped.cu; kept for A/B measurement).
+static bool use_pair_kernel() {
+  static const bool one = [] {
+    const char* e = std::getenv("LOKA_GROUPED_1CTA");
+    return e && e[0] == '1';
+  }();
+  return !one;
+}
+
 // MX problems need their scale packs (each 256-byte aligned, back to back); everything else none.
 size_t loka_grouped_workspace_size(int32_t G, const loka_linear_args* a) {
   size_t n = 0;
@@ -531,13 +543,14 @@ loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* 
       (!ws || ws_bytes < loka_grouped_workspace_size(G, a) || !aligned16(ws)))
     return LOKA_ERR_WORKSPACE;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  // Problems with a plain dequant(+bias) epilogue and bf16 output run in persistent grouped
-  // launches (<= kMaxGroups problems each, longest K first); row-coupled epilogues (norms, FP8
-  // output) keep their own fused linear_norm launches.
+  // Problems with a plain dequant(+bias) epilogue and bf16 (pair kernel: also f32) output run in
+  // persistent grouped launches (<= kMaxGroups problems each, longest K first); row-coupled
+  // epilogues (norms, FP8 output) keep their own fused linear_norm launches.
+  const bool pair = use_pair_kernel();
   std::vector<int> grouped, single;
   for (int g = 0; g < G; ++g) {
-    const bool ok = a[g].norm == LOKA_NORM_NONE && a[g].y.dtype == LOKA_BF16 && !a[g].debug_precast &&
-                    !is_blockwise(&a[g]) && !is_mx(&a[g]);
+    const bool ok = a[g].norm == LOKA_NORM_NONE && !a[g].debug_precast && !is_blockwise(&a[g]) && !is_mx(&a[g]) &&
+                    (a[g].y.dtype == LOKA_BF16 || (pair && a[g].y.dtype == LOKA_F32));
     (ok ? grouped : single).push_back(g);
   }
   std::stable_sort(grouped.begin(), grouped.end(), [&](int x, int y) { return a[x].K > a[y].K; });
@@ -550,12 +563,14 @@ loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* 
       const loka_linear_args& q = a[grouped[i0 + k]];
       if (!make_map_u8(&gp.ta[k], q.a.data, q.M, q.K, q.a.ld, 128)) return LOKA_ERR_CUDA;
       if (!make_map_u8(&gp.tb[k], q.b.data, q.N, q.K, q.b.ld, 128)) return LOKA_ERR_CUDA;
-      if (!make_map_out(&gp.ty[k], q.y.data, q.M, q.N, q.y.ld, q.y.dtype, 128)) return LOKA_ERR_CUDA;
+      if (!make_map_out(&gp.ty[k], q.y.data, q.M, q.N, q.y.ld, q.y.dtype, 128, pair ? 32u : 128u))
+        return LOKA_ERR_CUDA;
       GroupDesc& d = gp.g[k];
       d.M = (int32_t)q.M;
       d.N = (int32_t)q.N;
       d.K = (int32_t)q.K;
-      d.tiles_n = (int32_t)cdiv(q.N, 128);
+      const int tile = pair ? 256 : 128;  // CTA-pair tiles are 256 x 256
+      d.tiles_n = (int32_t)cdiv(q.N, tile);
       d.a_fmt = q.a.dtype == LOKA_E5M2 ? 1 : 0;
       d.b_fmt = q.b.dtype == LOKA_E5M2 ? 1 : 0;
       d.sa = q.a.scales;
@@ -565,9 +580,9 @@ loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* 
       d.bias = q.bias;
       d.bias_bf16 = q.bias_dtype == LOKA_BF16;
       d.out_dtype = q.y.dtype;
-      gp.tile_start[k + 1] = gp.tile_start[k] + (int32_t)(cdiv(q.M, 128) * d.tiles_n);
+      gp.tile_start[k + 1] = gp.tile_start[k] + (int32_t)(cdiv(q.M, tile) * d.tiles_n);
     }
-    if (launch_grouped(gp, sms, s) != cudaSuccess) return LOKA_ERR_CUDA;
+    if ((pair ? launch_grouped2(gp, sms, s) : launch_grouped(gp, sms, s)) != cudaSuccess) return LOKA_ERR_CUDA;
   }
   size_t ws_off = 0;
   for (int g : single) {

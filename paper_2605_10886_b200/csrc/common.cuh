@@ -297,6 +297,47 @@ LOKA_DEVINL void utccp_32x128b_warpx4(uint32_t tmem_dst, uint32_t saddr) {
   d |= (uint64_t)1u << 46;           // version; layout type 0 = no swizzle
   asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(tmem_dst), "l"(d) : "memory");
 }
+// ---- CTA pair (cta_group::2): one MMA spans the two SMs of a 2-CTA cluster ----
+template <uint32_t kCols>
+LOKA_DEVINL void tmem_alloc_cg2(uint32_t* dst_smem) {  // one warp in EACH CTA of the pair (same warp id)
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "n"(kCols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+}
+template <uint32_t kCols>
+LOKA_DEVINL void tmem_dealloc_cg2(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols));
+}
+// D[256 x N] (+)= A[256 x 32] . B[N x 32]^T: rows 0-127 of A / D and B rows 0..N/2-1 live in the
+// leader CTA, the rest at the same shared-memory / TMEM offsets in the peer.  Leader issues.
+LOKA_DEVINL void mma_f8f6f4_cg2(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// arrive on `bar` (same offset) in every CTA of cta_mask once the issued MMAs complete
+LOKA_DEVINL void mma_commit_cg2_mc(uint64_t* bar, uint16_t cta_mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(cta_mask)
+      : "memory");
+}
+// TMA 2-D load into this CTA's shared memory whose completion is counted on the LEADER's
+// barrier (bar_cluster: a shared::cluster address, e.g. mapa(bar, 0)).
+LOKA_DEVINL void tma_load_2d_cg2(void* dst, const CUtensorMap* m, uint32_t bar_cluster, int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)m), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+LOKA_DEVINL void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+LOKA_DEVINL void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 // 1-D bulk copy global -> own shared memory, completing as transaction bytes on `bar`.
 LOKA_DEVINL void bulk_load_g2s(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(

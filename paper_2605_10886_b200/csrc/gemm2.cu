@@ -1,0 +1,274 @@
+// gemm2.cu — a4/a6 on CTA pairs: persistent FP8 GEMM with 256 x 256 tiles computed by ONE
+// tcgen05.mma.cta_group::2 per 32-wide K step across the two SMs of a 2-CTA cluster.
+//
+// Why: a 128 x 128 (or 128 x 256) single-CTA tile needs 32 KB (48 KB) of
+// operands per 128-K stage for 4.2 (8.4) MFLOP, i.e. ~19-25 TB/s of L2 -> SM traffic chip-wide at
+// the tensor-core rate — more than L2 delivers, so the many-small-GEMM mix (BJ configs[2])
+// and the big training GEMMs (configs[3]) were L2-bound.  A CTA pair computes a 256 x 256 tile:
+// each CTA stages its 128 rows of A and HALF of the 256 rows of B (32 KB per stage per SM for
+// 16.8 MFLOP per pair), halving the traffic per FLOP of the 128 x 256 tile.
+//
+//   * cluster (2,1,1); rank 0 is the leader.  Both CTAs' producers (warp 0 lane 0) TMA-load their
+//     halves with .cta_group::2 loads whose transaction bytes land on the LEADER's full barrier;
+//     the leader's MMA thread (warp 1 lane 0) issues the M=256, N=256 MMAs and commits with
+//     .multicast::cluster to the empty barriers of both CTAs (stage free in both).
+//   * Each CTA's TMEM holds its 128 rows x 256 columns; two accumulator buffers (all 512 columns)
+//     let the MMAs of tile j+1 run while the epilogue drains tile j.  The 8 epilogue warps of both
+//     CTAs (16 arrivals) release a buffer on the leader's acc_empty barrier.
+//   * Epilogue per warp: 32 rows (its TMEM lane quadrant) x 128 columns in 32-column chunks:
+//     y = acc * s_a[m] * s_b[n] (+ bias[n]) -> bf16 / f32 into a per-warp double-buffered
+//     32-row x 128-byte swizzled box -> TMA store (no CTA-wide barrier in the epilogue).
+//   * Persistent: pair c walks tiles c, c + #pairs, ... of the concatenated tile list of up to
+//     kMaxGroups GEMMs (longest K first, host order), tile = (256-row block, 256-col block).
+#include "common.cuh"
+#include "launch.h"
+
+namespace loka {
+
+constexpr int k2Stages = 4;
+constexpr int k2EpiWarps = 8;
+constexpr int k2Threads = 64 + 32 * k2EpiWarps;
+constexpr int k2StageA = 128 * 128, k2StageB = 128 * 128;  // per CTA: 128 rows x 128 K each
+constexpr int k2OffB = k2Stages * k2StageA;
+constexpr int k2OffOut = k2OffB + k2Stages * k2StageB;       // [8 warps][2][32 rows x 128 B]
+constexpr int k2OffCol = k2OffOut + k2EpiWarps * 2 * 4096;  // [2 tiles][s_b | bias][256] FP32
+constexpr int k2OffBar = k2OffCol + 2 * 2 * 256 * 4;
+constexpr int k2Smem = k2OffBar + 256 + 1024;
+static_assert(k2Smem <= 227 * 1024, "gemm2 smem");
+
+__global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_constant__ GroupedParams gp) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + k2OffB;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + k2OffBar);
+  uint64_t* empty_bar = full_bar + k2Stages;
+  uint64_t* acc_full = empty_bar + k2Stages;  // [2]
+  uint64_t* acc_empty = acc_full + 2;          // [2] (leader's is the one used)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = (int)cluster_ctarank();
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int T = gp.tile_start[gp.G];
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < k2Stages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 2 * k2EpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_cg2<512>(tmem_slot);
+  pdl_wait();
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive / TMA
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto locate = [&](int t, int& g, int& mb, int& nb) {  // binary search of the tile prefix sum
+    int lo = 0, hi = gp.G - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (t >= gp.tile_start[mid]) lo = mid;
+      else hi = mid - 1;
+    }
+    g = lo;
+    const int local = t - gp.tile_start[g];
+    const int tn = gp.g[g].tiles_n;
+    mb = local / tn;
+    nb = local - mb * tn;
+  };
+
+  if (warp == 0) {
+    // ===== TMA producer (both CTAs): this CTA's A rows and half of the tile's B rows =====
+    if (lane == 0) {
+      const uint32_t full0 = mapa_shared(smem_u32(full_bar), 0);  // leader's full_bar[0]
+      int it = 0;
+      for (int t = cid; t < T; t += ncl) {
+        int g, mb, nb;
+        locate(t, g, mb, nb);
+        const int nkb = (gp.g[g].K + 127) / 128;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % k2Stages;
+          const uint32_t ph = (uint32_t)(it / k2Stages) & 1u;
+          mbar_wait(&empty_bar[s], ph ^ 1u, 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[s], 2u * (k2StageA + k2StageB));
+          tma_load_2d_cg2(sA + s * k2StageA, &gp.ta[g], full0 + 8u * s, kb * 128, mb * 256 + rank * 128);
+          tma_load_2d_cg2(sB + s * k2StageB, &gp.tb[g], full0 + 8u * s, kb * 128, nb * 256 + rank * 128);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ===== MMA issuer (leader only): tile j -> accumulator buffer j & 1 of both CTAs =====
+    if (lane == 0 && rank == 0) {
+      int it = 0, j = 0;
+      for (int t = cid; t < T; t += ncl, ++j) {
+        int g, mb, nb;
+        locate(t, g, mb, nb);
+        const int nkb = (gp.g[g].K + 127) / 128;
+        const int buf = j & 1;
+        mbar_wait(&acc_empty[buf], ((uint32_t)(j >> 1) & 1u) ^ 1u, 4);  // both CTAs drained it
+        tc_fence_after();
+        const uint32_t idesc = idesc_f8f6f4(gp.g[g].a_fmt, gp.g[g].b_fmt, 256, 256);
+        const uint32_t dacc = tmem_base + (uint32_t)(buf * 256);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % k2Stages;
+          const uint32_t ph = (uint32_t)(it / k2Stages) & 1u;
+          mbar_wait(&full_bar[s], ph, 2);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + s * k2StageA);
+          const uint32_t b0 = smem_u32(sB + s * k2StageB);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            mma_f8f6f4_cg2(dacc, smem_desc_kmajor_sw128(a0 + k * 32), smem_desc_kmajor_sw128(b0 + k * 32), idesc,
+                           (kb | k) != 0);
+          mma_commit_cg2_mc(&empty_bar[s], 3);
+        }
+        mma_commit_cg2_mc(&acc_full[buf], 3);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===== epilogue (both CTAs): warp = TMEM lane quadrant q x column half h =====
+    const int q = warp & 3;
+    const int h = (warp - 2) >> 2;
+    const int r = q * 32 + lane;
+    uint8_t* stg = smem + k2OffOut + (warp - 2) * 8192;
+    const uint32_t acc_empty0 = mapa_shared(smem_u32(acc_empty), 0);
+    int nbox = 0;
+    int j = 0;
+    for (int t = cid; t < T; t += ncl, ++j) {
+      int g, mb, nb;
+      locate(t, g, mb, nb);
+      const GroupDesc& d = gp.g[g];
+      const int buf = j & 1;
+      // this tile's 256 column parameters -> smem (while the MMAs run); buffer j & 1 was last read
+      // in tile j - 2, which every epilogue warp finished before the barrier of tile j - 1
+      float* colp = reinterpret_cast<float*>(smem + k2OffCol) + buf * 512;
+      {
+        const int e = threadIdx.x - 64;
+        const int n = nb * 256 + e;
+        const bool ok = n < d.N;
+        colp[e] = ok ? __ldg(d.sb + (d.sb_row ? n : 0)) : 0.f;
+        float b = 0.f;
+        if (ok && d.bias) b = d.bias_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(d.bias)[n])
+                                          : reinterpret_cast<const float*>(d.bias)[n];
+        colp[256 + e] = b;
+      }
+      named_bar_sync(2, 32 * k2EpiWarps);
+      if (lane == 0) mbar_wait(&acc_full[buf], (uint32_t)(j >> 1) & 1u, 3);
+      __syncwarp();
+      tc_fence_after();
+      const int row0 = mb * 256 + rank * 128 + q * 32;  // first row of this warp's box
+      const int grow = row0 + lane;
+      const float sa = grow < d.M ? d.sa[d.sa_row ? grow : 0] : 0.f;
+      const int esz = d.out_dtype == LOKA_F32 ? 4 : 2;
+      const int cpb = 128 / esz;  // columns per 128-byte box row
+      const int col0 = nb * 256 + h * 128;
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * 256 + h * 128);
+#pragma unroll 1
+      for (int cb = 0; cb < 128; cb += 32) {
+        float y[32];
+        tmem_ld32(tbase + (uint32_t)cb, y);
+        if (cb == 96) {  // accumulator fully in registers: hand the buffer back to the MMA
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(acc_empty0 + 8u * buf);
+        }
+        const uint32_t cs = smem_u32(colp + h * 128 + cb);
+        const float2 sa2 = make_float2(sa, sa);
+#pragma unroll
+        for (int c = 0; c < 32; c += 4) {  // y = acc * (s_a s_b) + bias, column params broadcast from smem
+          const float4 s4 = lds_f4(cs + 4u * c), b4 = lds_f4(cs + 1024u + 4u * c);
+          const float2 a = fadd2(fmul2(make_float2(y[c], y[c + 1]), fmul2(sa2, make_float2(s4.x, s4.y))),
+                                 make_float2(b4.x, b4.y));
+          const float2 b = fadd2(fmul2(make_float2(y[c + 2], y[c + 3]), fmul2(sa2, make_float2(s4.z, s4.w))),
+                                 make_float2(b4.z, b4.w));
+          y[c] = a.x; y[c + 1] = a.y; y[c + 2] = b.x; y[c + 3] = b.y;
+        }
+        const int in_box = cb % cpb;  // first column of this chunk inside its box
+        uint8_t* box = stg + (nbox & 1) * 4096;
+        if (in_box == 0) {  // the buffer's previous store (two boxes ago) must have been read
+          if (lane == 0) bulk_wait_read_le1();
+          __syncwarp();
+        }
+        const uint32_t rowa = smem_u32(box) + (uint32_t)lane * 128u;
+        if (esz == 4) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            sts_u4(rowa + ((((uint32_t)k) ^ ((uint32_t)lane & 7u)) << 4),
+                   make_uint4(__float_as_uint(y[4 * k]), __float_as_uint(y[4 * k + 1]), __float_as_uint(y[4 * k + 2]),
+                              __float_as_uint(y[4 * k + 3])));
+        } else {
+          const uint32_t p0 = (uint32_t)(in_box * 2) >> 4;  // first 16-byte piece (0 or 4)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            uint32_t w[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              __nv_bfloat162 hh = __floats2bfloat162_rn(y[8 * k + 2 * i], y[8 * k + 2 * i + 1]);
+              w[i] = *reinterpret_cast<uint32_t*>(&hh);
+            }
+            sts_u4(rowa + (((p0 + (uint32_t)k) ^ ((uint32_t)lane & 7u)) << 4), make_uint4(w[0], w[1], w[2], w[3]));
+          }
+        }
+        if (in_box + 32 == cpb) {  // box complete: store it
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const int c0 = col0 + cb + 32 - cpb;
+            if (c0 < d.N && row0 < d.M) tma_store_2d(&gp.ty[g], box, c0, row0);
+            bulk_commit();
+          }
+          ++nbox;
+        }
+      }
+    }
+    if (lane == 0) bulk_wait0();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the peer's TMEM is written by the leader's MMAs until the very end
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_cg2<512>(tmem_base);
+  }
+}
+
+cudaError_t launch_grouped2(const GroupedParams& gp, int num_sms, cudaStream_t st) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(grouped2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, k2Smem);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  const int T = gp.tile_start[gp.G];
+  const int pairs = T < num_sms / 2 ? T : num_sms / 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * pairs), 1, 1);
+  cfg.blockDim = dim3(k2Threads, 1, 1);
+  cfg.dynamicSmemBytes = k2Smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, grouped2_kernel, gp);
+  note_launch();
+  return e;
+}
+
+}  // namespace loka

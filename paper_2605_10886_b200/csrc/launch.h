@@ -135,6 +135,9 @@ struct GroupedParams {
   int32_t tile_start[kMaxGroups + 1];  // prefix sum of 128x128 tiles
 };
 cudaError_t launch_grouped(const GroupedParams& gp, int num_sms, cudaStream_t st);
+// CTA-pair variant (gemm2.cu): tiles 256 x 256 (tiles_n = ceil(N/256), tile_start counts them);
+// ta/tb boxes {128, 128}; ty box {128 bytes, 32 rows}, SW128; bf16 / f32 output.
+cudaError_t launch_grouped2(const GroupedParams& gp, int num_sms, cudaStream_t st);
 
 struct ProbeLayer {
   const void* out; const void* ref;

@@ -80,3 +80,45 @@ def test_grouped_mixed_epilogues_and_ragged_shapes():
             deq = oracle.quantize.dequantize(y.cpu().numpy(), ys.cpu().numpy(), "e4m3", "row")
             rms = np.sqrt(np.mean(yo ** 2, axis=1, keepdims=True))
             assert np.all(np.abs(deq - yo) <= 2.0 ** -4 * np.abs(yo) + TOL * np.maximum(np.abs(yo), rms) + 1e-30)
+
+
+@pytest.mark.parametrize("od", ["f32", "bf16"])
+def test_pair_kernel_ragged_formats_and_many_tiles(od):
+    """CTA-pair (256 x 256 tile) grouped engine: ragged M/N/K, e5m2 x e4m3, more tiles than SM
+    pairs (persistent walk, both accumulator buffers reused), bias, f32 and bf16 outputs."""
+    specs = [(700, 520, 1000, "e5m2", True), (2304, 2048, 256, "e4m3", False), (256, 256, 16, "e4m3", True),
+             (130, 1096, 4096, "e4m3", False)]
+    args, keep, res = [], [], []
+    for t, (M, N, K, af, bias) in enumerate(specs):
+        x, w = synth.heavy(M, K, 60 + t), synth.weight(N, K, 70 + t)
+        xq, xs = lk.loka_quantize(to_dev_padded(x), af, "row")
+        wq, ws = lk.loka_quantize(to_dev_padded(w), "e4m3", "row")
+        b = torch.randn(N, generator=torch.Generator().manual_seed(t)).to(DEV) if bias else None
+        a, y, _ = lk.make_linear_args(xq, xs, wq, ws, a_fmt=af, out_dtype=od, bias=b, keep=keep)
+        args.append(a)
+        res.append((xq, xs, wq, ws, af, b, y))
+    lk.loka_grouped_fp8_linear(args)
+    torch.cuda.synchronize()
+    for xq, xs, wq, ws, af, b, y in res:
+        M = xq.shape[0]
+        rows = torch.randperm(M, generator=torch.Generator().manual_seed(M))[:64].sort().values.to(DEV)
+        yo = oracle.linear.linear_norm(xq[rows].cpu().numpy(), xs[rows].cpu().numpy(), af, "row", wq.cpu().numpy(),
+                                       ws.cpu().numpy(), "e4m3", "row", bias=None if b is None else f64(b))
+        if od == "bf16":
+            _check_bf16(y[rows], yo)
+        else:
+            rms = np.sqrt(np.mean(yo ** 2, axis=1, keepdims=True))
+            assert np.max(np.abs(f64(y[rows]) - yo) / np.maximum(np.abs(yo), rms)) <= TOL
+
+
+def test_single_cta_grouped_engine_still_correct():
+    """LOKA_GROUPED_1CTA=1 selects the single-CTA 128 x 128 grouped kernel (kept for A/B runs)."""
+    import subprocess
+    import sys
+    import os
+    code = ("import sys; sys.path.insert(0, 'tests'); import test_gpu_grouped as t; "
+            "t.test_grouped_mixed_epilogues_and_ragged_shapes(); print('ok')")
+    env = dict(os.environ, LOKA_GROUPED_1CTA="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
