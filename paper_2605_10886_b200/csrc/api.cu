@@ -433,8 +433,29 @@ static loka_status run_bw(const loka_linear_args* a, cudaStream_t s) {
   return launch_linear_bw(ta, tb, ty, p, s) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
 }
 
+// Grouped GEMM engine: the CTA-pair kernel (gemm2.cu) unless LOKA_GROUPED_1CTA=1 selects the
+// single-CTA 128 x 128 kernel (grouped.cu; kept for A/B measurement).
+static bool use_pair_kernel() {
+  static const bool one = [] {
+    const char* e = std::getenv("LOKA_GROUPED_1CTA");
+    return e && e[0] == '1';
+  }();
+  return !one;
+}
+
+// A plain dequant(+bias) problem big enough to fill every SM pair with 256 x 256 tiles runs on
+// the CTA-pair persistent engine (gemm2.cu) as a one-problem group.
+static bool pair_eligible(const loka_linear_args* a) {
+  if (!a || !use_pair_kernel() || a->norm != LOKA_NORM_NONE || a->debug_precast || is_mx(a)) return false;
+  if (a->a.gran != LOKA_GRAN_TENSOR && a->a.gran != LOKA_GRAN_ROW) return false;
+  if (a->b.gran != LOKA_GRAN_TENSOR && a->b.gran != LOKA_GRAN_ROW) return false;
+  if (a->y.dtype != LOKA_BF16 && a->y.dtype != LOKA_F32) return false;
+  return cdiv(a->M, 256) * cdiv(a->N, 256) >= 74;
+}
+
 loka_status loka_fp8_linear_norm(const loka_linear_args* a, void* ws, size_t ws_bytes, loka_stream_t stream) {
   if (is_blockwise(a)) return run_bw(a, reinterpret_cast<cudaStream_t>(stream));
+  if (pair_eligible(a)) return loka_grouped_fp8_linear(1, a, ws, ws_bytes, stream);
   CUtensorMap ta, tb, ty;
   LinearParams p;
   int bn = 0;
@@ -507,15 +528,6 @@ loka_status loka_fp8_mlp_stack(const loka_stack_args* a, loka_stream_t stream) {
   return launch_stack(p, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
 }
 
-// Grouped GEMM engine: the CTA-pair kernel (gemm2.cu) unless LOKA_GROUPED_1CTA=1 selects the
-// single-CTA 128 x 128 kernel (grouped.cu; kept for A/B measurement).
-static bool use_pair_kernel() {
-  static const bool one = [] {
-    const char* e = std::getenv("LOKA_GROUPED_1CTA");
-    return e && e[0] == '1';
-  }();
-  return !one;
-}
 
 // MX problems need their scale packs (each 256-byte aligned, back to back); everything else none.
 size_t loka_grouped_workspace_size(int32_t G, const loka_linear_args* a) {
