@@ -54,6 +54,7 @@ def main():
     ap.add_argument("--out", required=True)
     ap.add_argument("--traffic-json")
     ap.add_argument("--title", default="")
+    ap.add_argument("--traffic-key", default="stack_bytes_per_launch")
     a = ap.parse_args()
     lines = [f"# ncu summary {a.title}".rstrip(), ""]
     if a.launches:
@@ -85,9 +86,14 @@ def main():
             rb = to_bytes(*d["dram__bytes_read.sum"])
             wb = to_bytes(*d.get("dram__bytes_write.sum", ("0", "byte")))
             lines += ["", f"DRAM traffic per launch: {rb + wb:.0f} bytes (read {rb:.0f} + write {wb:.0f})."]
-            if a.traffic_json:
-                json.dump({"linear_norm_bytes_per_launch": rb + wb, "source": a.full, "kernel": name},
-                          open(a.traffic_json, "w"), indent=1)
+            if a.traffic_json:  # merge: one entry per kernel key
+                try:
+                    tj = json.load(open(a.traffic_json))
+                except (OSError, ValueError):
+                    tj = {}
+                tj[a.traffic_key] = rb + wb
+                tj[a.traffic_key + "_source"] = f"{a.full}: {name}"
+                json.dump(tj, open(a.traffic_json, "w"), indent=1)
         lines.append("")
     open(a.out, "w").write("\n".join(lines))
     print("\n".join(lines))
