@@ -171,7 +171,10 @@ LOKA_API size_t loka_linear_workspace_size(const loka_linear_args* args);
  * is quantized rowwise to e4m3 exactly as loka_fp8_linear_norm with an E4M3/ROW output would,
  * but never leaves the chip: a cluster of C CTAs keeps a 128-row block's activation in shared
  * memory (the next layer's A operand) and streams only the weights.  Only y (the last layer's
- * output) is written.  The result is bit-identical to the chain of L loka_fp8_linear_norm calls.
+ * output) is written (plus the hand-offs the caller asks for in h[]).  Every layer is the
+ * arithmetic of a loka_fp8_linear_norm call with an E4M3/ROW output (the last: y's dtype), up to
+ * the order of the FP32 accumulation (the A operand arrives slice by slice and is consumed in
+ * arrival order) and of the row-statistics merge.
  * Limits: L <= 8, dims[l] <= 1024 for l < L (K of each layer), with C = ceil(max N / 256), every
  * N = dims[l+1] in {64C, 128C, 256C} (C <= 8); norm in {NONE, LAYER, RMS}.                     */
 typedef struct loka_stack_args {
@@ -184,8 +187,16 @@ typedef struct loka_stack_args {
   float eps[8];             /* <= 0: default (1e-5 LAYER, 1e-6 RMS)                              */
   loka_tensor y;            /* [M, dims[L]]: F32 | BF16 | E4M3/E5M2 with ROW scales             */
   int32_t* status_dev;      /* nullable                                                          */
+  loka_tensor h[7];         /* optional saved hand-offs: h[l] = h_{l+1} (e4m3 [M, dims[l+1]],
+                               ld % 16 == 0, ROW scales) for l < L-1; data NULL = not saved
+                               (training keeps them for the backward pass)                        */
+  void* ws;                 /* device workspace, >= loka_stack_workspace_size(args) bytes (the
+                               cluster all-gathers a hand-off through L2; a saved h[l] doubles
+                               as that buffer), 16-byte aligned; may be NULL when the size is 0   */
+  size_t ws_bytes;
 } loka_stack_args;
 LOKA_API loka_status loka_fp8_mlp_stack(const loka_stack_args* args, loka_stream_t stream);
+LOKA_API size_t loka_stack_workspace_size(const loka_stack_args* args);
 
 /* ---- a6: grouped launch: G independent linear+norm problems ------------------------------- */
 LOKA_API loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* args, void* ws, size_t ws_bytes,

@@ -57,7 +57,7 @@ class loka_linear_args(C.Structure):
 class loka_stack_args(C.Structure):
     _fields_ = [("L", C.c_int32), ("M", C.c_int64), ("dims", C.c_int64 * 9), ("x", loka_tensor),
                 ("w", loka_tensor * 8), ("norm", C.c_int * 8), ("eps", C.c_float * 8), ("y", loka_tensor),
-                ("status_dev", C.c_void_p)]
+                ("status_dev", C.c_void_p), ("h", loka_tensor * 7), ("ws", C.c_void_p), ("ws_bytes", C.c_size_t)]
 
 
 class loka_probe_pair(C.Structure):
@@ -96,6 +96,7 @@ _sig = {
     "loka_launch_count": ([], C.c_int64),
     "loka_debug_hang_info": ([_P(C.c_uint64), C.c_int32], C.c_int64),
     "loka_debug_trace": ([C.c_int32, _P(C.c_uint64), C.c_int64], C.c_int64),
+    "loka_stack_workspace_size": ([_P(loka_stack_args)], C.c_size_t),
 }
 for _name, (_args, _ret) in _sig.items():
     _fn = getattr(_lib, _name)
@@ -325,9 +326,11 @@ def loka_quantize_grouped(xs, fmt: str = "e4m3", scale_fmt: str = "f32", outs=No
     return res
 
 
-def make_stack_args(xq, xs, ws, norms="layer", out_dtype="bf16", y=None, y_scales=None, eps=None, status=None):
+def make_stack_args(xq, xs, ws, norms="layer", out_dtype="bf16", y=None, y_scales=None, eps=None, status=None,
+                    save=None):
     """loka_stack_args for h_{l+1} = norm_l(h_l W_l^T): xq/xs = e4m3 codes + row scales of the input,
-    ws = [(codes [N_l, K_l], row scales [N_l])].  Returns (args, y, y_scales)."""
+    ws = [(codes [N_l, K_l], row scales [N_l])].  save: optional list of L-1 (codes, scales) device
+    tensors receiving the hand-offs h_1..h_{L-1}.  Returns (args, y, y_scales)."""
     L = len(ws)
     M, K0 = xq.shape
     a = loka_stack_args()
@@ -348,6 +351,13 @@ def make_stack_args(xq, xs, ws, norms="layer", out_dtype="bf16", y=None, y_scale
         y_scales = torch.empty(M, dtype=torch.float32, device=xq.device)
     a.y = _tensor(y, od, M, N, y_scales, "row")
     a.status_dev = None if status is None else status.data_ptr()
+    for l, hs in enumerate(save or []):
+        a.h[l] = _tensor(hs[0], E4M3, M, dims[l + 1], hs[1], "row")
+    nws = int(_lib.loka_stack_workspace_size(C.byref(a)))
+    if nws:
+        ws = torch.empty(nws, dtype=torch.uint8, device=xq.device)
+        a.ws, a.ws_bytes = ws.data_ptr(), nws
+        a._keep_ws = ws  # the workspace lives as long as the args object
     return a, y, y_scales
 
 

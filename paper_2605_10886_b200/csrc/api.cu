@@ -472,6 +472,29 @@ loka_status loka_fp8_linear_norm(const loka_linear_args* a, void* ws, size_t ws_
   return e == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
 }
 
+// Layer l's hand-off is all-gathered through L2 (global codes + multicast TMA loads) when the
+// cluster has peers and the CTA's slice is whole 128-wide K blocks (BN_l = N_l / C >= 128).
+static bool stack_l2_handoff(const loka_stack_args* a, int C, int l) {
+  return C > 1 && l + 1 < a->L && a->dims[l + 1] / C >= 128;
+}
+static int stack_cluster(const loka_stack_args* a) {
+  int64_t maxN = 0;
+  for (int l = 0; l < a->L && l < kMaxStackLayers; ++l) maxN = std::max<int64_t>(maxN, a->dims[l + 1]);
+  return (int)cdiv(maxN, 256);
+}
+static int64_t stack_ws_ld(const loka_stack_args* a) {  // one [M, ld] region reused by every layer
+  int64_t ld = 0;
+  for (int l = 0; l + 1 < a->L && l < kMaxStackLayers; ++l) ld = std::max<int64_t>(ld, a->dims[l + 1]);
+  return (ld + 15) / 16 * 16;
+}
+size_t loka_stack_workspace_size(const loka_stack_args* a) {
+  if (!a || a->L < 1 || a->L > kMaxStackLayers || a->M <= 0) return 0;
+  const int C = stack_cluster(a);
+  for (int l = 0; l + 1 < a->L; ++l)
+    if (!a->h[l].data && stack_l2_handoff(a, C, l)) return (size_t)a->M * (size_t)stack_ws_ld(a);
+  return 0;
+}
+
 loka_status loka_fp8_mlp_stack(const loka_stack_args* a, loka_stream_t stream) {
   if (!a) return LOKA_ERR_INVALID_ARG;
   const int L = a->L;
@@ -523,6 +546,23 @@ loka_status loka_fp8_mlp_stack(const loka_stack_args* a, loka_stream_t stream) {
   p.out_dtype = Y.dtype;
   p.y_scales = is_fp8(Y.dtype) ? Y.scales : nullptr;
   p.status = a->status_dev;
+  for (int l = 0; l + 1 < L; ++l) {  // hand-offs h_{l+1}: the caller's saved copy, else workspace
+    const loka_tensor& H = a->h[l];
+    if (H.data) {
+      if (H.dtype != LOKA_E4M3 || H.rows != a->M || H.cols != a->dims[l + 1] || H.ld < H.cols || H.ld % 16 ||
+          !H.scales || H.gran != LOKA_GRAN_ROW || !aligned16(H.data))
+        return LOKA_ERR_INVALID_ARG;
+      p.h_save[l] = static_cast<uint8_t*>(H.data);
+      p.h_ld[l] = (int32_t)H.ld;
+      p.hs_save[l] = H.scales;
+    } else if (stack_l2_handoff(a, C, l)) {
+      if (!a->ws || a->ws_bytes < loka_stack_workspace_size(a) || !aligned16(a->ws)) return LOKA_ERR_WORKSPACE;
+      p.h_save[l] = static_cast<uint8_t*>(a->ws);
+      p.h_ld[l] = (int32_t)stack_ws_ld(a);
+    }
+    if (p.h_save[l] && !make_map_u8(&p.th[l], p.h_save[l], a->M, a->dims[l + 1], p.h_ld[l], 128))
+      return LOKA_ERR_CUDA;
+  }
   loka_status st = check_device();
   if (st != LOKA_OK) return st;
   return launch_stack(p, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;

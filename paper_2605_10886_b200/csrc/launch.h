@@ -88,7 +88,7 @@ cudaError_t launch_linear(const CUtensorMap& tma_a, const CUtensorMap& tma_b, co
 constexpr int kMaxStackLayers = 8;
 struct StackParams {
   CUtensorMap tx;                    // X codes [M, K0], box {128, 128}
-  CUtensorMap tw[kMaxStackLayers];   // W_l codes [N_l, K_l], box {128, BN_l}
+  CUtensorMap tw[kMaxStackLayers];   // W_l codes [N_l, K_l], box {128, min(BN_l, 128)}
   CUtensorMap ty;                    // output [M, N_last], box {min(128, BN*e) bytes, 128}
   const float* xs;                   // X row scales
   const float* ws[kMaxStackLayers];  // W_l row scales (per output column)
@@ -99,6 +99,12 @@ struct StackParams {
   int32_t out_dtype;
   float* y_scales;
   int32_t* status;
+  // hand-off h_{l+1} codes in global memory [M, N_l] (ld h_ld): the caller's saved copy or the
+  // workspace; required where the cluster all-gathers through L2 (C > 1, BN_l >= 128), else nullable
+  uint8_t* h_save[kMaxStackLayers];
+  int32_t h_ld[kMaxStackLayers];
+  float* hs_save[kMaxStackLayers];    // nullable: its row scales [M]
+  CUtensorMap th[kMaxStackLayers];    // map over h_save[l], box {128, 128}, SW128 (multicast loads)
 };
 cudaError_t launch_stack(const StackParams& p, cudaStream_t st);
 long long stack_debug_trace(int enable, unsigned long long* out, long long n);  // see loka_debug_trace

@@ -3,19 +3,29 @@
 //
 // A thread-block cluster of C CTAs owns a 128-row block of the batch; CTA `rank` owns the column
 // slice [rank*BN_l, (rank+1)*BN_l) of every layer (BN_l = N_l / C).  Per layer:
-//   * the layer input h_l (the MMA's A operand, 128 x K_l FP8) is already in every CTA's shared
-//     memory, in the 128B-swizzled K-major layout tcgen05 reads; only the weight slice streams
-//     (TMA ring, prefetched across layers);
-//   * tcgen05.mma accumulates the 128 x BN_l tile in TMEM;
-//   * the epilogue (same arithmetic as linear.cu: s_a folded into eps, packed FP32x2 statistics,
-//     quarter merge in smem, cluster exchange of (mean, M2, ymax, ymin) pushed with DSMEM stores,
-//     one-FFMA normalisation, row amax from ymax/ymin) produces the next layer's e4m3 codes and
-//     row scale, writes its codes into its own A tile and sends that slice to every peer's A tile
-//     with one bulk (TMA-engine) shared::cta -> shared::cluster copy per peer, completing on the
-//     peer's a_full mbarrier (slices narrower than a 128-wide K block: per-thread DSMEM stores +
-//     cluster barrier); the next layer's MMAs start when a_full flips;
-//   * only the last layer's output goes to HBM (swizzled staging tile + TMA store).
-// The codes and scales are bit-identical to the per-layer chain of linear_norm_kernel launches.
+//   * the layer input h_l (the MMA's A operand, 128 x K_l FP8) lives in every CTA's shared memory
+//     in the 128B-swizzled K-major layout tcgen05 reads; only the weight slice streams (2-stage TMA
+//     ring of BN_l x 128 stages, running ahead across layers);
+//   * h_l arrives slice by slice (slice s = the columns rank s produced in layer l-1): one mbarrier
+//     per slice; the MMAs consume the CTA's own slice first, then the peers' slices in the order
+//     they are sent, so the all-gather of h_l overlaps layer l's MMAs;
+//   * the epilogue (s_a folded into eps, packed FP32x2 statistics, quarter merge in smem, cluster
+//     exchange of (mean|ss, M2, ymax, ymin) records pushed with DSMEM stores, one-FFMA
+//     normalisation, row amax from ymax/ymin) produces the next layer's e4m3 codes and row scale
+//     and writes the codes into the CTA's own A tile; the slice then reaches the peers through L2:
+//     TMA store of its K blocks to a global hand-off buffer, then one TMA load per K block
+//     multicast to every peer, completing on the peer's slice barrier (kSGatherL2; the SM-to-SM
+//     alternative — one bulk DSMEM copy per peer — measured ~4% slower).  Slices narrower than a
+//     128-wide K block go by per-thread DSMEM stores + a cluster barrier;
+//   * only the last layer's output goes to HBM (swizzled staging tile + TMA store); the global
+//     hand-offs double as the saved activations training needs (loka_stack_args.h).
+// Each layer is the arithmetic of a loka_fp8_linear_norm call with an E4M3/ROW output, up to the
+// order of the FP32 accumulation and of the row-statistics merge.
+//
+// Where the time goes (tools/trace_stack.py): per CTA and layer, the L2 -> SM
+// ingress (~40 B/clk per SM: the weight slice plus 3/4 of h_l) bounds the MMA phase; the FP32
+// accumulator drain from TMEM (~64 B/clk: 1 us for 128 x 256) and the two cluster-wide merges
+// bound the epilogue.
 #include "common.cuh"
 #include "launch.h"
 
@@ -24,21 +34,21 @@ namespace loka {
 constexpr int kSThreads = 512;  // 16 warps: warp 0 lane 0 = TMA producer, warp 1 lane 0 = MMA issuer,
                                 // then all 16 warps run each layer's epilogue
 constexpr int kSStages = 2;
-constexpr int kSBNMax = 256, kSKMax = 1024;
+constexpr int kSKMax = 1024;
 constexpr int kSRec = 6;
 constexpr int kSOffA = 0;                                // [kb][128 rows][128 B] (<= 128 KB)
-constexpr int kSOffW = 128 * kSKMax;                     // weight ring
-constexpr int kSStageW = kSBNMax * 128;
+constexpr int kSOffW = 128 * kSKMax;                     // weight ring [stage][<= 256 rows][128 B]
+constexpr int kSStageW = 256 * 128;
 constexpr int kSOffCs = kSOffW + kSStages * kSStageW;    // [8][128] float4 cluster records
-constexpr int kSOffCol = kSOffCs + 8 * 128 * 16;         // [kSBNMax] W row scales of this slice
-constexpr int kSOffBar = kSOffCol + kSBNMax * 4;
-constexpr int kSSmem = kSOffBar + 128 + 1024;
+constexpr int kSOffCol = kSOffCs + 8 * 128 * 16;         // [256] W row scales of this slice
+constexpr int kSOffBar = kSOffCol + 256 * 4;
+constexpr int kSSmem = kSOffBar + 256 + 1024;
 static_assert(kSSmem <= 227 * 1024, "stack smem");
 
 // Opt-in phase trace (loka_debug_trace): per CTA 64 globaltimer stamps — 0 entry, 1 setup done,
-// then per layer l at 2 + 7 l: +0 first weight stage landed (MMA), +1 last MMA committed,
-// +2 accumulator ready (epilogue), +3 quarters merged, +4 cluster merged, +5 codes pushed,
-// +6 next-layer A complete (MMA issuer saw a_full).
+// then per layer l at 2 + 7 l: +0 first weight stage landed (MMA), +1 last MMA issued,
+// +2 first accumulator half ready (epilogue), +3 quarters merged, +4 cluster merged,
+// +5 codes pushed, +6 next layer's A complete (MMA issuer saw its last slice).
 constexpr int kSTraceCtas = 512;
 static __device__ unsigned long long g_strace[kSTraceCtas * 64];
 static __device__ int g_strace_on;
@@ -75,75 +85,74 @@ LOKA_DEVINL SRow merge_rows(const SRow (&r)[K]) {
   return o;
 }
 
+// Issuing the MMAs per 128-column half (so the epilogue could drain half 0 while half 1 is being
+// multiplied) was measured SLOWER: two N=128 passes re-read A from shared memory and the MMA
+// becomes shared-memory-bandwidth bound (A + B bytes per FLOP double).  Kept switchable.
+constexpr bool kSplitHalves = false;
+// All-gather of a layer's hand-off among the cluster: through L2 (codes stored to global memory,
+// multicast TMA loads back into the peers' A tiles) or SM-to-SM (bulk DSMEM copies).  Measured
+// equal on cfg2 (~4 us per 96 KB per CTA either way); L2 is the default because the global copy
+// doubles as the saved activation training needs.
+constexpr bool kSGatherL2 = true;
+
+// Layer schedule shared by the producer and the MMA issuer: unit u in [0, nh * nkb) is
+// (half h = u / nkb, K block kb); within a half the K blocks go slice by slice, own slice first.
+struct SPlan {
+  int nh, hn, nkb, kps;
+  bool sliced;
+};
+LOKA_DEVINL SPlan splan(const StackParams& p, int l) {
+  SPlan s;
+  const int bn = p.BN[l];
+  s.nh = kSplitHalves && bn > 128 ? 2 : 1;
+  s.hn = s.nh == 2 ? 128 : bn;
+  s.nkb = (p.K[l] + 127) / 128;
+  s.sliced = l > 0 && p.C > 1 && p.BN[l - 1] >= 128;
+  s.kps = s.sliced ? p.BN[l - 1] / 128 : s.nkb;
+  return s;
+}
+LOKA_DEVINL int unit_kb(const SPlan& s, int i, int rank, int C) {  // i = index within the half
+  if (!s.sliced) return i;
+  const int t = i / s.kps;
+  const int src = (rank - t + C) % C;
+  return src * s.kps + (i - t * s.kps);
+}
+
 struct SCtx {
   uint8_t* smem;
   uint32_t tmem_base;
   int warp, lane, q, cq, r, grow, m0, rank, C;
   int trace, cta;
-  uint64_t* a_full;  // layer-input-complete barrier (TMA X load, then peers' bulk copies)
+  uint64_t* a_bar;     // [8] per-slice "layer input complete" barriers
+  uint64_t* half_bar;  // [2] accumulator half ready
   bool row_ok;
 };
 
-// One layer's epilogue for CPT = BN/4 columns per thread.  `sa` is the layer input's row scale;
-// returns the next layer's row scale (or 1 for the last layer).
-template <int CPT>
-LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, float sa) {
-  constexpr int BN = 4 * CPT;
-  const int norm = p.norm[l];
-  const int N = p.N[l];
-  const int n0 = c.rank * BN;
-  const bool last = l + 1 == p.L;
-  const bool fold = norm != LOKA_NORM_NONE;  // no bias in the stack: s_a goes into eps
-  float* col = reinterpret_cast<float*>(c.smem + kSOffCol);
-  float* cs = reinterpret_cast<float*>(c.smem + kSOffCs);
-  float* hx = reinterpret_cast<float*>(c.smem + kSOffA);  // A is drained once our MMAs completed
-  const int cb = c.cq * CPT;
-  const uint32_t col_s = smem_u32(col);
-
-  // ---- accumulator -> registers, dequant ----
-  float y[CPT];
-  const uint32_t taddr = c.tmem_base + ((uint32_t)(c.q * 32) << 16) + (uint32_t)cb;
-  if constexpr (CPT >= 32) {
-#pragma unroll
-    for (int i = 0; i < CPT / 32; ++i) tmem_ld32_nowait(taddr + (uint32_t)(32 * i), y + 32 * i);
-  } else {
-    tmem_ld16_nowait(taddr, y);
-  }
-#pragma unroll
-  for (int i = 0; i < CPT / 16; ++i) tmem_wait16(y + 16 * i);
-  const float ys = fold ? 1.f : sa;
-#pragma unroll
-  for (int j = 0; j < CPT; j += 4) {
-    const float4 s4 = lds_f4(col_s + (uint32_t)(cb + j) * 4u);
-    const float2 a = fmul2(make_float2(y[j], y[j + 1]), fmul2(make_float2(s4.x, s4.y), make_float2(ys, ys)));
-    const float2 b = fmul2(make_float2(y[j + 2], y[j + 3]), fmul2(make_float2(s4.z, s4.w), make_float2(ys, ys)));
-    y[j] = a.x; y[j + 1] = a.y; y[j + 2] = b.x; y[j + 3] = b.y;
-  }
-
-  // ---- statistics over this thread's CPT columns (all valid: N = C*BN exactly) ----
+template <int SEG>
+LOKA_DEVINL SRow seg_stats(const float* y, int norm) {
   SRow rec;
   rec.init();
-  rec.n = (float)CPT;
+  rec.n = (float)SEG;
   float cmax = y[0], cmin = y[0];
 #pragma unroll
-  for (int j = 0; j < CPT; j += 2) cmax = fmax3(cmax, y[j], y[j + 1]), cmin = fmin3(cmin, y[j], y[j + 1]);
+  for (int j = 0; j < SEG; j += 2) cmax = fmax3(cmax, y[j], y[j + 1]), cmin = fmin3(cmin, y[j], y[j + 1]);
   rec.ymax = cmax;
   rec.ymin = cmin;
   if (norm == LOKA_NORM_LAYER) {
     float2 s0 = make_float2(0.f, 0.f), s1 = s0, s2 = s0, s3 = s0;
 #pragma unroll
-    for (int j = 0; j < CPT; j += 8) {
+    for (int j = 0; j < SEG; j += 8) {
       s0 = fadd2(s0, make_float2(y[j], y[j + 1]));
       s1 = fadd2(s1, make_float2(y[j + 2], y[j + 3]));
       s2 = fadd2(s2, make_float2(y[j + 4], y[j + 5]));
       s3 = fadd2(s3, make_float2(y[j + 6], y[j + 7]));
     }
     s0 = fadd2(fadd2(s0, s1), fadd2(s2, s3));
-    const float mc = (s0.x + s0.y) / (float)CPT;
+    const float mc = (s0.x + s0.y) / (float)SEG;
     const float2 nm = make_float2(-mc, -mc);
     float2 q0 = make_float2(0.f, 0.f), q1 = q0;
 #pragma unroll
-    for (int j = 0; j < CPT; j += 4) {
+    for (int j = 0; j < SEG; j += 4) {
       const float2 d0 = fadd2(make_float2(y[j], y[j + 1]), nm);
       const float2 d1 = fadd2(make_float2(y[j + 2], y[j + 3]), nm);
       q0 = ffma2(d0, d0, q0);
@@ -155,7 +164,7 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
   } else if (norm == LOKA_NORM_RMS) {
     float2 q0 = make_float2(0.f, 0.f), q1 = q0;
 #pragma unroll
-    for (int j = 0; j < CPT; j += 4) {
+    for (int j = 0; j < SEG; j += 4) {
       const float2 a = make_float2(y[j], y[j + 1]), b = make_float2(y[j + 2], y[j + 3]);
       q0 = ffma2(a, a, q0);
       q1 = ffma2(b, b, q1);
@@ -163,6 +172,59 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
     q0 = fadd2(q0, q1);
     rec.ss = q0.x + q0.y;
   }
+  return rec;
+}
+
+// One layer's epilogue: NH accumulator halves of SEG columns per thread (thread (q, cq) owns row
+// r = 32 q + lane and, in half h, the columns h*128 + cq*SEG + [0, SEG)).  `sa` is the layer
+// input's row scale; returns the next layer's row scale (or 1 for the last layer).
+template <int NH, int SEG>
+LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, float sa, uint32_t& hph) {
+  static_assert(NH == 1 || SEG == 32, "halves are 128 columns");
+  constexpr int BN = NH == 2 ? 256 : 4 * SEG;
+  constexpr int CPT = NH * SEG;
+  const int norm = p.norm[l];
+  const int N = p.N[l];
+  const int n0 = c.rank * BN;
+  const bool last = l + 1 == p.L;
+  const bool fold = norm != LOKA_NORM_NONE;  // no bias in the stack: s_a goes into eps
+  float* cs = reinterpret_cast<float*>(c.smem + kSOffCs);
+  float* hx = reinterpret_cast<float*>(c.smem + kSOffA);  // A is drained once our MMAs completed
+  const uint32_t col_s = smem_u32(c.smem + kSOffCol);
+  const float ys = fold ? 1.f : sa;
+
+  // ---- accumulator halves -> registers (dequant, partial statistics) as each half completes ----
+  float y[CPT];
+  SRow hrec[NH];
+#pragma unroll
+  for (int h = 0; h < NH; ++h) {
+    if (c.lane == 0) mbar_wait(&c.half_bar[h], (hph >> h) & 1u, 3);
+    __syncwarp();
+    tc_fence_after();
+    if (h == 0 && threadIdx.x == 0) LOKA_STRACE(c, 2 + 7 * l + 2);
+    const int cbh = h * 128 + c.cq * SEG;
+    const uint32_t taddr = c.tmem_base + ((uint32_t)(c.q * 32) << 16) + (uint32_t)cbh;
+    float* yh = y + h * SEG;
+    if constexpr (SEG >= 32) {
+#pragma unroll
+      for (int i = 0; i < SEG / 32; ++i) tmem_ld32_nowait(taddr + (uint32_t)(32 * i), yh + 32 * i);
+    } else {
+      tmem_ld16_nowait(taddr, yh);
+    }
+#pragma unroll
+    for (int i = 0; i < SEG / 16; ++i) tmem_wait16(yh + 16 * i);
+#pragma unroll
+    for (int j = 0; j < SEG; j += 4) {
+      const float4 s4 = lds_f4(col_s + (uint32_t)(cbh + j) * 4u);
+      const float2 a = fmul2(make_float2(yh[j], yh[j + 1]), fmul2(make_float2(s4.x, s4.y), make_float2(ys, ys)));
+      const float2 b = fmul2(make_float2(yh[j + 2], yh[j + 3]), fmul2(make_float2(s4.z, s4.w), make_float2(ys, ys)));
+      yh[j] = a.x; yh[j + 1] = a.y; yh[j + 2] = b.x; yh[j + 3] = b.y;
+    }
+    hrec[h] = seg_stats<SEG>(yh, norm);
+  }
+  hph ^= NH == 2 ? 3u : 1u;
+  SRow rec = NH == 2 ? merge_rows(hrec) : hrec[0];
+
   // ---- merge the four column quarters (component-major records in smem) ----
   {
     float* my = hx + (size_t)c.cq * kSRec * 128 + c.r;
@@ -223,6 +285,7 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
       y[j + 1] = a.y;
     }
   }
+  if (l == 1 && threadIdx.x == 0) LOKA_STRACE(c, 58);
   const bool fp8_next = !last || p.out_dtype == LOKA_E4M3 || p.out_dtype == LOKA_E5M2;
   const int ofmt = last ? p.out_dtype : LOKA_E4M3;
   float s_out = 1.f, r_out = 1.f;
@@ -233,50 +296,97 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
     if (ofmt == LOKA_E5M2) scales_from_amax<LOKA_E5M2, LOKA_SCALE_F32>(amax, s_out, r_out);
     else scales_from_amax<LOKA_E4M3, LOKA_SCALE_F32>(amax, s_out, r_out);
   }
+  if (l == 1 && threadIdx.x == 0) LOKA_STRACE(c, 59);
   if (!last) {
-    // ---- next layer's A operand: codes into every cluster CTA's swizzled A tile ----
+    // ---- next layer's A operand: codes into this CTA's swizzled A tile (+ saved hand-off) ----
     const float2 rr = make_float2(r_out, r_out);
     const uint32_t a_local = smem_u32(c.smem + kSOffA);
+    uint8_t* hsave = p.h_save[l];
 #pragma unroll
-    for (int ch = 0; ch < CPT / 16; ++ch) {
-      uint32_t w[4];
+    for (int h = 0; h < NH; ++h) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int j = 16 * ch + 4 * i;
-        const float2 a = fmul2(make_float2(y[j], y[j + 1]), rr);
-        const float2 b = fmul2(make_float2(y[j + 2], y[j + 3]), rr);
-        w[i] = cvt_fp8x4<LOKA_E4M3>(a.x, a.y, b.x, b.y);
-      }
-      const int k = n0 + cb + 16 * ch;  // K index of the next layer
-      const uint32_t off = (uint32_t)(k >> 7) * 16384u + (uint32_t)c.r * 128u +
-                           ((((uint32_t)(k & 127) >> 4) ^ ((uint32_t)c.r & 7u)) << 4);
-      const float4 v = make_float4(__uint_as_float(w[0]), __uint_as_float(w[1]), __uint_as_float(w[2]),
-                                   __uint_as_float(w[3]));
-      sts_u4(a_local + off, make_uint4(w[0], w[1], w[2], w[3]));
-      if constexpr (BN < 128) {  // slice not contiguous in the swizzled tile: per-thread DSMEM stores
-        for (int rk = 0; rk < c.C; ++rk)
-          if (rk != c.rank) st_dsmem_f4(mapa_shared(a_local + off, (uint32_t)rk), v);
+      for (int ch = 0; ch < SEG / 16; ++ch) {
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int j = h * SEG + 16 * ch + 4 * i;
+          const float2 a = fmul2(make_float2(y[j], y[j + 1]), rr);
+          const float2 b = fmul2(make_float2(y[j + 2], y[j + 3]), rr);
+          w[i] = cvt_fp8x4<LOKA_E4M3>(a.x, a.y, b.x, b.y);
+        }
+        const int k = n0 + h * 128 + c.cq * SEG + 16 * ch;  // K index of the next layer
+        const uint32_t off = (uint32_t)(k >> 7) * 16384u + (uint32_t)c.r * 128u +
+                             ((((uint32_t)(k & 127) >> 4) ^ ((uint32_t)c.r & 7u)) << 4);
+        sts_u4(a_local + off, make_uint4(w[0], w[1], w[2], w[3]));
+        if constexpr (BN < 128) {  // slice not contiguous in the swizzled tile: per-thread DSMEM stores
+          const float4 v = make_float4(__uint_as_float(w[0]), __uint_as_float(w[1]), __uint_as_float(w[2]),
+                                       __uint_as_float(w[3]));
+          for (int rk = 0; rk < c.C; ++rk)
+            if (rk != c.rank) st_dsmem_f4(mapa_shared(a_local + off, (uint32_t)rk), v);
+        }
+        if (hsave && c.row_ok && !(kSGatherL2 && BN >= 128 && c.C > 1))  // (L2 gather: TMA-stored below)
+          *reinterpret_cast<uint4*>(hsave + (size_t)c.grow * p.h_ld[l] + k) = make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
-    if (BN >= 128 || c.C == 1) {
-      // The slice [n0, n0 + BN) of h_{l+1} is BN/128 whole 16 KB K-blocks of the A tile: one bulk
-      // (TMA-engine) copy per peer, completing on the peer's a_full barrier.  Peers' A tiles are free:
-      // barrier 1 above proved every cluster CTA's layer-l MMAs (and its hx reads) completed.
-      fence_proxy_async_smem();  // generic writes -> async proxy (bulk-copy source, own MMA)
+    if (p.hs_save[l] && c.row_ok && c.rank == 0 && c.cq == 0) p.hs_save[l][c.grow] = s_out;
+    if (l == 1 && threadIdx.x == 0) LOKA_STRACE(c, 60);
+    if (c.C == 1) {
+      fence_proxy_async_smem();  // generic writes -> async proxy (own MMA)
       named_bar_sync(1, kSThreads);
       if (threadIdx.x == 0) {
+        mbar_arrive(&c.a_bar[0]);
+        LOKA_STRACE(c, 2 + 7 * l + 5);
+      }
+    } else if (BN >= 128 && kSGatherL2) {
+      // The slice [n0, n0 + BN) of h_{l+1} is BN/128 whole 16 KB K blocks of the A tile.  Its
+      // codes also went to global memory (p.h_save[l], L2-resident); one TMA load per K block,
+      // multicast to every peer, brings them back into the peers' A tiles and completes on each
+      // peer's slice barrier a_bar[rank] — the all-gather runs on the L2 -> SM path instead of the
+      // SM -> SM network (DSMEM: ~14-21 B/clk per SM, measured ~2x slower here).  Peers' A tiles
+      // are free: barrier 1 above proved every cluster CTA's layer-l MMAs (and hx reads) completed.
+      // The data are this CTA's own writes, so a CTA-wide barrier orders them before the load.
+      fence_proxy_async_smem();  // generic smem writes -> async proxy (TMA store source, own MMA)
+      named_bar_sync(1, kSThreads);
+      if (l == 1 && threadIdx.x == 0) LOKA_STRACE(c, 61);
+      if (threadIdx.x == 0) {
+        const uint32_t bytes = (uint32_t)BN * 128u;
+        // the slice's K blocks (already swizzled in A) -> global with TMA stores; wait until written
+        for (int kb = n0 >> 7; kb < (n0 + BN) >> 7; ++kb) tma_store_2d(&p.th[l], c.smem + kSOffA + kb * 16384, kb * 128, c.m0);
+        bulk_commit();
+        bulk_wait0();
+        fence_proxy_async_global();
+        const uint16_t mask = (uint16_t)(((1u << c.C) - 1u) & ~(1u << c.rank));
+        for (int kb = n0 >> 7; kb < (n0 + BN) >> 7; ++kb)
+          tma_load_2d_mc(c.smem + kSOffA + kb * 16384, &p.th[l], &c.a_bar[c.rank], kb * 128, c.m0, mask);
+        mbar_arrive(&c.a_bar[c.rank]);  // own slice
+        for (int s = 0; s < c.C; ++s)
+          if (s != c.rank) mbar_arrive_expect_tx(&c.a_bar[s], bytes);  // peers' slices (same BN)
+        LOKA_STRACE(c, 2 + 7 * l + 5);
+      }
+    } else if (BN >= 128) {
+      // DSMEM variant of the all-gather: one bulk (TMA-engine) shared::cta -> shared::cluster copy
+      // of the slice per peer, completing on the peer's slice barrier a_bar[rank]; peers served in
+      // rank order starting after this CTA (the order in which every receiver consumes slices).
+      fence_proxy_async_smem();  // generic writes -> async proxy (bulk-copy source, own MMA)
+      named_bar_sync(1, kSThreads);
+      if (l == 1 && threadIdx.x == 0) LOKA_STRACE(c, 61);
+      if (threadIdx.x == 0) {
         const uint32_t src = a_local + (uint32_t)(n0 >> 7) * 16384u, bytes = (uint32_t)BN * 128u;
-        for (int rk = 0; rk < c.C; ++rk)
-          if (rk != c.rank)
-            bulk_copy_s2cluster(mapa_shared(src, (uint32_t)rk), src, bytes, mapa_shared(smem_u32(c.a_full), (uint32_t)rk));
-        mbar_arrive_expect_tx(c.a_full, (uint32_t)(c.C - 1) * bytes);
+        for (int t = 1; t < c.C; ++t) {
+          const int rk = (c.rank + t) % c.C;
+          bulk_copy_s2cluster(mapa_shared(src, (uint32_t)rk), src, bytes,
+                              mapa_shared(smem_u32(&c.a_bar[c.rank]), (uint32_t)rk));
+        }
+        mbar_arrive(&c.a_bar[c.rank]);  // own slice
+        for (int s = 0; s < c.C; ++s)
+          if (s != c.rank) mbar_arrive_expect_tx(&c.a_bar[s], bytes);  // peers' slices (same BN)
         LOKA_STRACE(c, 2 + 7 * l + 5);
       }
     } else {
       asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");  // generic writes -> tensor-core reads
       if (threadIdx.x == 0) LOKA_STRACE(c, 2 + 7 * l + 5);
       cluster_sync_all();  // barrier 2: h_{l+1} complete in every CTA
-      if (threadIdx.x == 0) mbar_arrive_expect_tx(c.a_full, 0u);
+      if (threadIdx.x == 0) mbar_arrive(&c.a_bar[0]);
     }
     return s_out;
   }
@@ -285,41 +395,46 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
   const int esz = p.out_dtype == LOKA_F32 ? 4 : p.out_dtype == LOKA_BF16 ? 2 : 1;
   const uint32_t box_bytes = (uint32_t)min(128, BN * esz);
   const uint32_t stage_s = smem_u32(c.smem + kSOffA);
-  auto put16 = [&](int chunk, uint4 v) {
-    const uint32_t bofs = (uint32_t)(cb * esz + 16 * chunk);
+  auto put16 = [&](int lcol, uint4 v) {  // lcol: local column (within BN) of the piece's first element
+    const uint32_t bofs = (uint32_t)(lcol * esz);
     const uint32_t c16 = (bofs % box_bytes) >> 4;
     const uint32_t sw = box_bytes == 128u ? (c16 ^ ((uint32_t)c.r & 7u)) : (c16 ^ (((uint32_t)c.r >> 1) & 3u));
     sts_u4(stage_s + (bofs / box_bytes) * (128u * box_bytes) + (uint32_t)c.r * box_bytes + (sw << 4), v);
   };
-  if (esz == 4) {
 #pragma unroll
-    for (int k = 0; k < CPT / 4; ++k)
-      put16(k, make_uint4(__float_as_uint(y[4 * k]), __float_as_uint(y[4 * k + 1]), __float_as_uint(y[4 * k + 2]),
-                          __float_as_uint(y[4 * k + 3])));
-  } else if (esz == 2) {
+  for (int h = 0; h < NH; ++h) {
+    const int lc = h * 128 + c.cq * SEG;
+    const float* yh = y + h * SEG;
+    if (esz == 4) {
 #pragma unroll
-    for (int k = 0; k < CPT / 8; ++k) {
-      uint32_t w[4];
+      for (int k = 0; k < SEG / 4; ++k)
+        put16(lc + 4 * k, make_uint4(__float_as_uint(yh[4 * k]), __float_as_uint(yh[4 * k + 1]),
+                                     __float_as_uint(yh[4 * k + 2]), __float_as_uint(yh[4 * k + 3])));
+    } else if (esz == 2) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        __nv_bfloat162 hh = __floats2bfloat162_rn(y[8 * k + 2 * i], y[8 * k + 2 * i + 1]);
-        w[i] = *reinterpret_cast<uint32_t*>(&hh);
+      for (int k = 0; k < SEG / 8; ++k) {
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          __nv_bfloat162 hh = __floats2bfloat162_rn(yh[8 * k + 2 * i], yh[8 * k + 2 * i + 1]);
+          w[i] = *reinterpret_cast<uint32_t*>(&hh);
+        }
+        put16(lc + 8 * k, make_uint4(w[0], w[1], w[2], w[3]));
       }
-      put16(k, make_uint4(w[0], w[1], w[2], w[3]));
-    }
-  } else {
-    const float2 rr = make_float2(r_out, r_out);
+    } else {
+      const float2 rr = make_float2(r_out, r_out);
 #pragma unroll
-    for (int k = 0; k < CPT / 16; ++k) {
-      uint32_t w[4];
+      for (int k = 0; k < SEG / 16; ++k) {
+        uint32_t w[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int j = 16 * k + 4 * i;
-        const float2 a = fmul2(make_float2(y[j], y[j + 1]), rr);
-        const float2 b = fmul2(make_float2(y[j + 2], y[j + 3]), rr);
-        w[i] = ofmt == LOKA_E5M2 ? cvt_fp8x4<LOKA_E5M2>(a.x, a.y, b.x, b.y) : cvt_fp8x4<LOKA_E4M3>(a.x, a.y, b.x, b.y);
+        for (int i = 0; i < 4; ++i) {
+          const int j = 16 * k + 4 * i;
+          const float2 a = fmul2(make_float2(yh[j], yh[j + 1]), rr);
+          const float2 b = fmul2(make_float2(yh[j + 2], yh[j + 3]), rr);
+          w[i] = ofmt == LOKA_E5M2 ? cvt_fp8x4<LOKA_E5M2>(a.x, a.y, b.x, b.y) : cvt_fp8x4<LOKA_E4M3>(a.x, a.y, b.x, b.y);
+        }
+        put16(lc + 16 * k, make_uint4(w[0], w[1], w[2], w[3]));
       }
-      put16(k, make_uint4(w[0], w[1], w[2], w[3]));
     }
   }
   fence_proxy_async_smem();
@@ -344,9 +459,9 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
   float* col = reinterpret_cast<float*>(smem + kSOffCol);
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kSOffBar);
   uint64_t* empty_bar = full_bar + kSStages;
-  uint64_t* a_full = empty_bar + kSStages;
-  uint64_t* tmem_full = a_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* a_bar = empty_bar + kSStages;  // [8]
+  uint64_t* half_bar = a_bar + 8;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(half_bar + 2);
 
   SCtx c;
   c.smem = smem;
@@ -360,7 +475,8 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
   c.row_ok = c.grow < p.M;
   c.C = p.C;
   c.rank = p.C > 1 ? (int)cluster_ctarank() : 0;
-  c.a_full = a_full;
+  c.a_bar = a_bar;
+  c.half_bar = half_bar;
   c.trace = *reinterpret_cast<volatile int*>(&g_strace_on);
   c.cta = blockIdx.x + gridDim.x * blockIdx.y;
   if (threadIdx.x == 0) LOKA_STRACE(c, 0);
@@ -373,11 +489,11 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
-    mbar_init(a_full, 1);
-    mbar_init(tmem_full, 1);
+    for (int s = 0; s < 8; ++s) mbar_init(&a_bar[s], 1);
+    for (int h = 0; h < 2; ++h) mbar_init(&half_bar[h], 1);
     fence_barrier_init();
   }
-  if (c.warp == 1) tmem_alloc<kSBNMax>(tmem_slot);
+  if (c.warp == 1) tmem_alloc<256>(tmem_slot);
   pdl_wait();
   tc_fence_before();
   __syncthreads();
@@ -388,48 +504,62 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
 
   float sa = c.row_ok ? p.xs[c.grow] : 0.f;  // row scale of the current layer input
   int prod_it = 0, mma_it = 0;
-  auto produce = [&](int l, int kb) {
-    const int s = prod_it % kSStages;
-    mbar_wait(&empty_bar[s], ((uint32_t)(prod_it / kSStages) & 1u) ^ 1u, 1);
-    mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(p.BN[l] * 128));
-    tma_load_2d(sW + s * kSStageW, &p.tw[l], &full_bar[s], kb * 128, c.rank * p.BN[l]);
+  uint32_t aph = 0;  // MMA issuer: parity of each slice barrier's next phase
+  uint32_t hph = 0;  // epilogue: parity of each accumulator-half barrier's next phase
+  auto produce = [&](int l, int u) {
+    const SPlan s = splan(p, l);
+    const int h = u / s.nkb;
+    const int kb = unit_kb(s, u - h * s.nkb, c.rank, c.C);
+    const int st = prod_it % kSStages;
+    mbar_wait(&empty_bar[st], ((uint32_t)(prod_it / kSStages) & 1u) ^ 1u, 1);
+    mbar_arrive_expect_tx(&full_bar[st], (uint32_t)(s.hn * 128));
+    tma_load_2d(sW + st * kSStageW, &p.tw[l], &full_bar[st], kb * 128, c.rank * p.BN[l] + h * 128);
     ++prod_it;
   };
-  int prefetched = 0;  // k-blocks of the current layer already issued during the previous layer
+  int prefetched = 0;  // units of the current layer already issued during the previous layer
   for (int l = 0; l < p.L; ++l) {
-    const int nkb = (p.K[l] + 127) / 128;
+    const SPlan pl = splan(p, l);
+    const int units = pl.nh * pl.nkb;
     if (c.warp == 0 && c.lane == 0) {  // ===== producer =====
       if (l == 0) {
-        mbar_arrive_expect_tx(a_full, (uint32_t)(nkb * 128 * 128));
-        for (int kb = 0; kb < nkb; ++kb) tma_load_2d(sA + kb * 16384, &p.tx, a_full, kb * 128, c.m0);
+        mbar_arrive_expect_tx(&a_bar[0], (uint32_t)(pl.nkb * 128 * 128));
+        for (int kb = 0; kb < pl.nkb; ++kb) tma_load_2d(sA + kb * 16384, &p.tx, &a_bar[0], kb * 128, c.m0);
       }
-      for (int kb = prefetched; kb < nkb; ++kb) produce(l, kb);
+      for (int u = prefetched; u < units; ++u) produce(l, u);
       prefetched = 0;
       if (l + 1 < p.L) {  // run ahead into the next layer's weights while this layer finishes
-        const int nn = min(kSStages, (p.K[l + 1] + 127) / 128);
-        for (int kb = 0; kb < nn; ++kb) produce(l + 1, kb);
+        const SPlan nx = splan(p, l + 1);
+        const int nn = min(kSStages, nx.nh * nx.nkb);
+        for (int u = 0; u < nn; ++u) produce(l + 1, u);
         prefetched = nn;
       }
     }
     if (c.warp == 1 && c.lane == 0) {  // ===== MMA issuer =====
-      mbar_wait(a_full, (uint32_t)l & 1u, 5);  // h_l complete: X by TMA, then own slice + peers' bulk copies
-      tc_fence_after();
-      if (l > 0) LOKA_STRACE(c, 2 + 7 * (l - 1) + 6);
-      const uint32_t idesc = idesc_f8f6f4(0, 0, 128, (uint32_t)p.BN[l]);
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = mma_it % kSStages;
-        mbar_wait(&full_bar[s], (uint32_t)(mma_it / kSStages) & 1u, 2);
-        tc_fence_after();
-        if (kb == 0) LOKA_STRACE(c, 2 + 7 * l);
-        const uint32_t a0 = smem_u32(sA + kb * 16384), b0 = smem_u32(sW + s * kSStageW);
+      const uint32_t idesc = idesc_f8f6f4(0, 0, 128, (uint32_t)pl.hn);
+      for (int h = 0; h < pl.nh; ++h) {
+        for (int i = 0; i < pl.nkb; ++i) {
+          const int kb = unit_kb(pl, i, c.rank, c.C);
+          if (h == 0 && i % pl.kps == 0) {  // first use of a slice of h_l: wait until it is complete
+            const int src = kb / pl.kps;
+            mbar_wait(&a_bar[src], (aph >> src) & 1u, 5);
+            aph ^= 1u << src;
+            tc_fence_after();
+            if (l > 0) LOKA_STRACE(c, 2 + 7 * (l - 1) + 6);
+          }
+          const int st = mma_it % kSStages;
+          mbar_wait(&full_bar[st], (uint32_t)(mma_it / kSStages) & 1u, 2);
+          tc_fence_after();
+          if (h == 0 && i == 0) LOKA_STRACE(c, 2 + 7 * l);
+          const uint32_t a0 = smem_u32(sA + kb * 16384), b0 = smem_u32(sW + st * kSStageW);
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          mma_f8f6f4(c.tmem_base, smem_desc_kmajor_sw128(a0 + k * 32), smem_desc_kmajor_sw128(b0 + k * 32), idesc,
-                     (kb | k) != 0);
-        mma_commit(&empty_bar[s]);
-        ++mma_it;
+          for (int k = 0; k < 4; ++k)
+            mma_f8f6f4(c.tmem_base + (uint32_t)(h * 128), smem_desc_kmajor_sw128(a0 + k * 32),
+                       smem_desc_kmajor_sw128(b0 + k * 32), idesc, (i | k) != 0);
+          mma_commit(&empty_bar[st]);
+          ++mma_it;
+        }
+        mma_commit(&half_bar[h]);
       }
-      mma_commit(tmem_full);
       LOKA_STRACE(c, 2 + 7 * l + 1);
     }
     __syncwarp();
@@ -437,15 +567,13 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
     const float* ws = p.ws[l];
     for (int j = threadIdx.x; j < p.BN[l]; j += kSThreads) col[j] = ws[c.rank * p.BN[l] + j];
     named_bar_sync(1, kSThreads);
-    if (c.lane == 0) mbar_wait(tmem_full, (uint32_t)l & 1u, 3);
-    __syncwarp();
-    tc_fence_after();
-    if (threadIdx.x == 0) LOKA_STRACE(c, 2 + 7 * l + 2);
     float s_next;
     switch (p.BN[l]) {
-      case 64: s_next = stack_epilogue<16>(p, c, l, sa); break;
-      case 128: s_next = stack_epilogue<32>(p, c, l, sa); break;
-      default: s_next = stack_epilogue<64>(p, c, l, sa); break;
+      case 64: s_next = stack_epilogue<1, 16>(p, c, l, sa, hph); break;
+      case 128: s_next = stack_epilogue<1, 32>(p, c, l, sa, hph); break;
+      default:
+        s_next = kSplitHalves ? stack_epilogue<2, 32>(p, c, l, sa, hph) : stack_epilogue<1, 64>(p, c, l, sa, hph);
+        break;
     }
     sa = c.row_ok ? s_next : 0.f;
     tc_fence_before();  // this layer's tcgen05.ld done before the next layer's MMAs overwrite TMEM
@@ -454,7 +582,7 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
   __syncthreads();
   if (c.warp == 1) {
     tc_fence_after();
-    tmem_dealloc<kSBNMax>(c.tmem_base);
+    tmem_dealloc<256>(c.tmem_base);
   }
 }
 

@@ -1,17 +1,21 @@
 """-m gpu: loka_fp8_mlp_stack (a4+a5 for a whole LRM MLP stack in one launch, BJ configs[1]).
-At the cfg2 shape the result must be bit-identical to the chain of per-layer loka_fp8_linear_norm
-calls (same tiling, same arithmetic); every case is also checked against the oracle run layer by
-layer on the GPU's own FP8 hand-offs."""
+Every layer is checked against oracle/linear.py run on the stack's OWN input to that layer (the
+hand-offs h_1..h_{L-1} the kernel writes out on request): the next hand-off's row scale must match
+the oracle's to FP32 rounding and every code must decode to within e4m3 rounding (+ the FP32
+accumulation tolerance) of the oracle's FP64 result; the last layer's output within 2e-3 (+ one
+bf16 half-ulp).  Shapes cover the cfg2 stack (C = 4 clusters, both slice widths), ragged M, a
+single-CTA cluster (C = 1) and every output dtype."""
 import numpy as np
 import pytest
 import torch
 
 import oracle
 import synth
-from gpu_util import DEV, f64, guarded_rel_err
+from gpu_util import DEV, f64
 
 pytestmark = pytest.mark.gpu
 lk = pytest.importorskip("paper_2605_10886_b200") if torch.cuda.is_available() else None
+TOL = 2e-3
 
 
 def _inputs(M, dims, xdist="gaussian"):
@@ -22,56 +26,102 @@ def _inputs(M, dims, xdist="gaussian"):
     return xq, xs, ws
 
 
-def _chain(xq, xs, ws, norm, out_dtype):
-    hq, hs = xq, xs
-    outs = []
-    for l, (wq, wsc) in enumerate(ws):
-        last = l == len(ws) - 1
-        y, ys = lk.loka_fp8_linear_norm(hq, hs, wq, wsc, norm=norm, out_dtype=out_dtype if last else "e4m3")
-        outs.append((y, ys))
-        hq, hs = y, ys
-    return outs
-
-
-def test_cfg2_stack_bit_identical_to_layer_chain():
-    dims, M = synth.CFG2_DIMS, 4096
-    xq, xs, ws = _inputs(M, dims)
-    y, _ = lk.loka_fp8_mlp_stack(xq, xs, ws, norms="layer", out_dtype="bf16")
-    chain = _chain(xq, xs, ws, "layer", "bf16")
+def _run(M, dims, norm, out_dtype, xdist="gaussian", keep_handoffs=True):
+    xq, xs, ws = _inputs(M, dims, xdist)
+    save = [(torch.empty(M, n, dtype=torch.uint8, device=DEV), torch.empty(M, dtype=torch.float32, device=DEV))
+            for n in dims[1:-1]] if keep_handoffs else None
+    a, y, ys = lk.make_stack_args(xq, xs, ws, norms=norm, out_dtype=out_dtype, save=save)
+    import ctypes as C
+    assert lk._lib.loka_fp8_mlp_stack(C.byref(a), None) == 0
     torch.cuda.synchronize()
-    assert torch.equal(y.view(torch.int16), chain[-1][0].view(torch.int16))
+    return xq, xs, ws, save, y, ys
+
+
+def _layer_oracle(hq, hs, wq, wsc, norm, rows=None):
+    hq, hs = hq.cpu().numpy(), hs.cpu().numpy()
+    if rows is not None:
+        hq, hs = hq[rows], hs[rows]
+    return oracle.linear.linear_norm(hq, hs, "e4m3", "row", wq.cpu().numpy(), wsc.cpu().numpy(), "e4m3", "row",
+                                     norm=norm)
+
+
+def _check_handoff(codes, scales, yo, rows=None):
+    """codes/scales: the stack's e4m3 hand-off; yo: the oracle's FP64 layer output."""
+    c = codes.cpu().numpy()
+    s = scales.cpu().numpy().astype(np.float64)
+    if rows is not None:
+        c, s = c[rows], s[rows]
+    oq, os_ = oracle.quantize.quantize(yo, "e4m3", "row")
+    assert np.all(np.abs(s - os_) <= 1e-5 * os_), float(np.max(np.abs(s - os_) / os_))
+    got = oracle.quantize.dequantize(c, s.astype(np.float32), "e4m3", "row")
+    rms = np.sqrt(np.mean(yo ** 2, axis=1, keepdims=True))
+    bound = 2.0 ** -4 * np.abs(yo) + 1.1 * TOL * np.maximum(np.abs(yo), rms) + 2.0 ** -10 * s[:, None]
+    bad = np.abs(got - yo) > bound
+    assert not bad.any(), (int(bad.sum()), float(np.max(np.abs(got - yo) - bound)))
+
+
+def _check_out(y, ys, yo, out_dtype, rows=None):
+    if rows is not None:
+        y = y[rows]
+        ys = None if ys is None else ys[rows]
+    rms = np.sqrt(np.mean(yo ** 2, axis=1, keepdims=True))
+    if out_dtype in ("e4m3", "e5m2"):
+        _check_handoff(y, ys, yo) if out_dtype == "e4m3" else None
+        return
+    extra = 2.0 ** -8 * np.abs(yo) if out_dtype == "bf16" else 0.0
+    bad = np.abs(f64(y) - yo) > TOL * np.maximum(np.abs(yo), rms) + extra
+    assert not bad.any(), (int(bad.sum()), float(np.max(np.abs(f64(y) - yo))))
+
+
+def test_cfg2_stack_every_layer_vs_oracle():
+    """BJ configs[1] at full size (M = 4096, 8 layers, C = 4): layers checked on 96 sampled rows."""
+    dims, M = synth.CFG2_DIMS, 4096
+    xq, xs, ws, save, y, _ = _run(M, dims, "layer", "bf16")
+    rows = np.sort(np.random.default_rng(1).choice(M, 96, replace=False))
+    ins = [(xq, xs)] + save
+    for l in range(len(dims) - 1):
+        yo = _layer_oracle(ins[l][0], ins[l][1], ws[l][0], ws[l][1], "layer", rows)
+        if l + 1 < len(dims) - 1:
+            _check_handoff(save[l][0], save[l][1], yo, rows)
+        else:
+            _check_out(y, None, yo, "bf16", rows)
 
 
 @pytest.mark.parametrize("norm,out_dtype", [("layer", "e4m3"), ("rms", "f32"), ("none", "bf16")])
-def test_stack_vs_oracle(norm, out_dtype):
-    dims, M = [512, 1024, 256, 512], 300  # C = 4 (BN 256 / 64 / 128), ragged M
-    xq, xs, ws = _inputs(M, dims, "heavy")
-    y, ys = lk.loka_fp8_mlp_stack(xq, xs, ws, norms=norm, out_dtype=out_dtype)
-    chain = _chain(xq, xs, ws, norm, out_dtype)
-    torch.cuda.synchronize()
-    # oracle on the chain's own hand-offs: the stack's inputs of every layer equal the chain's
-    # up to rounding order of the statistics, so compare the final layer with the tolerance
-    hq, hs = (xq, xs) if len(ws) == 1 else chain[-2]
-    yo = oracle.linear.linear_norm(hq.cpu().numpy(), hs.cpu().numpy(), "e4m3", "row", ws[-1][0].cpu().numpy(),
-                                   ws[-1][1].cpu().numpy(), "e4m3", "row", norm=norm)
-    if out_dtype == "e4m3":
-        got = oracle.quantize.dequantize(y.cpu().numpy(), ys.cpu().numpy(), "e4m3", "row")
-        rms = np.sqrt(np.mean(yo ** 2, axis=1, keepdims=True))
-        assert np.mean(np.abs(got - yo) <= 2.0 ** -3 * np.abs(yo) + 2e-3 * np.maximum(np.abs(yo), rms)) > 0.999
-    else:
-        got = f64(y)
-        tol = 2e-3 if out_dtype == "f32" else 6e-3
-        assert guarded_rel_err(got, yo) <= tol or np.mean(
-            np.abs(got - yo) <= tol * np.maximum(np.abs(yo), np.sqrt(np.mean(yo ** 2, 1, keepdims=True)))) > 0.999
+def test_stack_ragged_all_slice_widths(norm, out_dtype):
+    dims, M = [512, 1024, 256, 512, 1024], 300  # C = 4: BN 256 / 64 / 128 / 256, ragged M
+    xq, xs, ws, save, y, ys = _run(M, dims, norm, out_dtype, "heavy")
+    ins = [(xq, xs)] + save
+    for l in range(len(dims) - 1):
+        yo = _layer_oracle(ins[l][0], ins[l][1], ws[l][0], ws[l][1], norm)
+        if l + 1 < len(dims) - 1:
+            _check_handoff(save[l][0], save[l][1], yo)
+        else:
+            _check_out(y, ys, yo, out_dtype)
 
 
 def test_stack_single_cta_cluster_and_short():
     dims, M = [256, 256, 128, 256], 520  # max N 256 -> C = 1
-    xq, xs, ws = _inputs(M, dims)
-    y, _ = lk.loka_fp8_mlp_stack(xq, xs, ws, norms="layer", out_dtype="f32")
-    chain = _chain(xq, xs, ws, "layer", "f32")
+    xq, xs, ws, save, y, _ = _run(M, dims, "layer", "f32")
+    ins = [(xq, xs)] + save
+    for l in range(len(dims) - 1):
+        yo = _layer_oracle(ins[l][0], ins[l][1], ws[l][0], ws[l][1], "layer")
+        if l + 1 < len(dims) - 1:
+            _check_handoff(save[l][0], save[l][1], yo)
+        else:
+            _check_out(y, None, yo, "f32")
+
+
+def test_stack_matches_layer_chain_closely():
+    """The fused stack and the chain of per-layer launches compute the same function; they differ
+    only in FP32 summation order, so the final outputs agree to accumulation noise except where an
+    e4m3 hand-off code flipped at a rounding midpoint (rare)."""
+    dims, M = synth.CFG2_DIMS, 1024
+    xq, xs, ws, _, y, _ = _run(M, dims, "layer", "f32", keep_handoffs=False)  # hand-offs via the workspace
+    hq, hs = xq, xs
+    for l, (wq, wsc) in enumerate(ws):
+        last = l == len(ws) - 1
+        hq, hs = lk.loka_fp8_linear_norm(hq, hs, wq, wsc, norm="layer", out_dtype="f32" if last else "e4m3")
     torch.cuda.synchronize()
-    hq, hs = chain[-2]
-    yo = oracle.linear.linear_norm(hq.cpu().numpy(), hs.cpu().numpy(), "e4m3", "row", ws[-1][0].cpu().numpy(),
-                                   ws[-1][1].cpu().numpy(), "e4m3", "row", norm="layer")
-    assert np.mean(np.abs(f64(y) - yo) <= 2e-3 * np.maximum(np.abs(yo), np.sqrt(np.mean(yo ** 2, 1, keepdims=True)))) > 0.999
+    d = (y - hq).abs()
+    assert float((d <= 2e-2 * hq.abs().clamp_min(1.0)).float().mean()) > 0.99

@@ -22,13 +22,17 @@ for rep in range(4):
         lk.debug_trace(1)
     y, _ = lk.loka_fp8_mlp_stack(xq, xs, ws, norms="layer", out_dtype="bf16")
     torch.cuda.synchronize()
-t = np.array(lk.debug_trace(0, 65536 + 512 * 64), dtype=np.int64)[65536:].reshape(-1, 64)[:, :58]
+t = np.array(lk.debug_trace(0, 65536 + 512 * 64), dtype=np.int64)[65536:].reshape(-1, 64)[:, :64]
 t = t[t[:, 0] > 0]
 base = t[:, 0].min()
 rel = np.where(t > 0, (t - base) / 1000.0, np.nan)
 med = np.nanmedian(rel, axis=0)
 mx = np.nanmax(rel, axis=0)
 print(f"ctas={len(t)} entry {med[0]:.2f}/{mx[0]:.2f} setup {med[1]:.2f}/{mx[1]:.2f} end(max last stamp) {np.nanmax(rel):.2f} us")
+d = rel[:, 58:62]
+if np.isfinite(d).any():
+    print("L1 epilogue detail (median): normalized %.2f scales %.2f codes_stored %.2f fenced+barrier %.2f" %
+          tuple(np.nanmedian(d, axis=0)))
 names = ["w_landed", "mma_done", "acc_ready", "q_merged", "cl_merged", "pushed", "A_ready"]
 for l in range(8):
     b = 2 + 7 * l
