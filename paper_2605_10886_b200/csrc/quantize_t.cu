@@ -8,8 +8,8 @@
 // registers (64 elements per thread), granule amax is reduced within the tile (1x128: half warp,
 // 128x1: per column across the tile, 128x128: whole CTA) or read from a pre-pass array
 // (TENSOR / ROW / COL span beyond one tile), codes are written row-major directly and the
-// transposed copy goes through a padded shared-memory tile so both layouts are written with
-// coalesced 128-byte rows.  Same arithmetic as quantize.cu (bit-identical codes and scales).
+// transposed copy goes through a swizzled shared-memory tile and an in-register byte transpose so
+// both layouts are written with coalesced 128-byte rows.  Same arithmetic as quantize.cu (bit-identical codes and scales).
 #include "common.cuh"
 #include "launch.h"
 
@@ -129,12 +129,42 @@ __global__ void __launch_bounds__(256) col_amax_kernel(QuantParams p, uint32_t* 
 }
 
 // ---- tile kernel: granule scales + cast + row-major and/or transposed codes ----------------
-// amax_g: pre-pass array for TENSOR ([1], float bits) / ROW ([rows]) / COL ([cols]); else null.
-template <typename Tin, int FMT, int SF>
-__global__ void __launch_bounds__(256, 2) quant_tile_kernel(QuantParams p, int gran, const uint32_t* amax_g) {
+// GRAN is a template parameter so the granularities whose scales come from a pre-pass (TENSOR /
+// ROW / COL) carry no reduction state and run at 3 CTAs per SM.  amax_g: pre-pass array for
+// TENSOR ([1], float bits) / ROW ([rows]) / COL ([cols]); else null.
+//
+// Transposed copy: the 128 x 128 code tile goes to shared memory row-major with its 16-byte chunks
+// XOR-swizzled by (row / 8) & 7; each thread then reads an 8-row x 4-column block as eight 32-bit
+// words (2-way bank conflicts at most), transposes it in registers with byte permutes (PRMT) and
+// writes 4 transposed rows x 8 bytes; 16 lanes cover 128 contiguous bytes of a transposed row.
+template <typename Tin, int GRAN> struct TileOcc {
+  static constexpr int kBlocks =
+      sizeof(Tin) == 2 && (GRAN == LOKA_GRAN_TENSOR || GRAN == LOKA_GRAN_ROW || GRAN == LOKA_GRAN_COL) ? 3 : 2;
+};
+
+LOKA_DEVINL uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+// 4 x 4 byte transpose: in[i] holds row i (bytes = columns 0..3); out[k] = column k (bytes = rows)
+LOKA_DEVINL void transpose4x4(const uint32_t (&in)[4], uint32_t (&out)[4]) {
+  const uint32_t t0 = prmt(in[0], in[1], 0x5140u), t1 = prmt(in[2], in[3], 0x5140u);
+  const uint32_t t2 = prmt(in[0], in[1], 0x7362u), t3 = prmt(in[2], in[3], 0x7362u);
+  out[0] = prmt(t0, t1, 0x5410u);
+  out[1] = prmt(t0, t1, 0x7632u);
+  out[2] = prmt(t2, t3, 0x5410u);
+  out[3] = prmt(t2, t3, 0x7632u);
+}
+LOKA_DEVINL uint32_t tq_off(int row, int col) {  // byte offset of (row, col) in the swizzled code tile
+  return (uint32_t)row * 128u + ((((uint32_t)col >> 4) ^ (((uint32_t)row >> 3) & 7u)) << 4) + ((uint32_t)col & 15u);
+}
+
+template <typename Tin, int FMT, int SF, int GRAN>
+__global__ void __launch_bounds__(256, TileOcc<Tin, GRAN>::kBlocks) quant_tile_kernel(QuantParams p, const uint32_t* amax_g) {
   pdl_wait();
   __shared__ uint32_t red[8][128];
-  __shared__ uint8_t tq[128][128 + 8];  // codes tile for the transposed write (+8 B pad: <= 2-way conflicts)
+  __shared__ __align__(16) uint8_t tq[128 * 128];  // codes tile for the transposed write (swizzled)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t c0 = (int64_t)blockIdx.x * 128, r0 = (int64_t)blockIdx.y * 128;
   const int64_t nbc = (p.cols + 127) / 128, nbr = (p.rows + 127) / 128;
@@ -142,32 +172,23 @@ __global__ void __launch_bounds__(256, 2) quant_tile_kernel(QuantParams p, int g
   const int64_t c = c0 + cl;
   const int nc = (int)max((int64_t)0, imin64(8, p.cols - c));
   Raw8<Tin> v[8];  // [row iteration], 8 elements each, storage form
-  uint32_t rowm[8], colm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int64_t row = r0 + warp * 16 + i * 2 + (lane >> 4);
     if (row < p.rows && nc > 0) v[i].load(reinterpret_cast<const Tin*>(p.x) + row * p.ldx + c, nc);
     else v[i].zero();
   }
+  // ---- granule amax -> cast multiplier per element: rrow[i] (row-like) or rcol[k] (column-like) ----
+  constexpr bool kColwise = GRAN == LOKA_GRAN_BLK_128x1 || GRAN == LOKA_GRAN_COL;
+  float rrow[8], rcol[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    uint32_t m = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint32_t b = v[i].abits(k);
-      m = max(m, b);
-      colm[k] = max(colm[k], b);
-    }
-    rowm[i] = m;
-  }
-  // ---- granule amax ----
-  // cast multiplier r per element = rrow[i] (row-like granules) or rcol[k] (column-like granules)
-  float rrow[8] = {1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f}, rcol[8] = {1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f};
-  const bool colwise = gran == LOKA_GRAN_BLK_128x1 || gran == LOKA_GRAN_COL;
-  if (gran == LOKA_GRAN_BLK_1x128) {
+  for (int i = 0; i < 8; ++i) rrow[i] = rcol[i] = 1.f;
+  if constexpr (GRAN == LOKA_GRAN_BLK_1x128) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      uint32_t m = rowm[i];
+      uint32_t m = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) m = max(m, v[i].abits(k));
 #pragma unroll
       for (int o = 8; o >= 1; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
       if (m >= 0x7F800000u && (lane & 15) == 0 && p.status) atomicOr(p.status, LOKA_DEVSTATUS_NONFINITE);
@@ -180,7 +201,12 @@ __global__ void __launch_bounds__(256, 2) quant_tile_kernel(QuantParams p, int g
       }
       rrow[i] = r;
     }
-  } else if (gran == LOKA_GRAN_BLK_128x1 || gran == LOKA_GRAN_BLK_128x128) {
+  } else if constexpr (GRAN == LOKA_GRAN_BLK_128x1 || GRAN == LOKA_GRAN_BLK_128x128) {
+    uint32_t colm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) colm[k] = max(colm[k], v[i].abits(k));
 #pragma unroll
     for (int k = 0; k < 8; ++k) colm[k] = max(colm[k], __shfl_xor_sync(0xFFFFFFFFu, colm[k], 16));
     if (lane < 16) {
@@ -188,7 +214,7 @@ __global__ void __launch_bounds__(256, 2) quant_tile_kernel(QuantParams p, int g
       for (int k = 0; k < 8; ++k) red[warp][cl + k] = colm[k];
     }
     __syncthreads();
-    if (gran == LOKA_GRAN_BLK_128x1) {
+    if constexpr (GRAN == LOKA_GRAN_BLK_128x1) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         uint32_t m = 0;
@@ -204,11 +230,16 @@ __global__ void __launch_bounds__(256, 2) quant_tile_kernel(QuantParams p, int g
         }
       }
     } else {
+      __shared__ uint32_t red2[8];
       uint32_t m = 0;
-      for (int j = 0; j < 128; ++j) {
+      if (threadIdx.x < 128) {
 #pragma unroll
-        for (int w = 0; w < 8; ++w) m = max(m, red[w][j]);
+        for (int w = 0; w < 8; ++w) m = max(m, red[w][threadIdx.x]);
       }
+      m = warp_max_u32(m);
+      if (lane == 0) red2[warp] = m;
+      __syncthreads();
+      m = max(max(red2[0], red2[1]), max(red2[2], red2[3]));
       float s, r;
       scales_from_amax<FMT, SF>(__uint_as_float(m), s, r);
 #pragma unroll
@@ -219,7 +250,7 @@ __global__ void __launch_bounds__(256, 2) quant_tile_kernel(QuantParams p, int g
         if (p.scales_t) p.scales_t[(int64_t)blockIdx.x * nbr + blockIdx.y] = s;
       }
     }
-  } else if (gran == LOKA_GRAN_TENSOR) {  // from the pre-pass amax word
+  } else if constexpr (GRAN == LOKA_GRAN_TENSOR) {  // from the pre-pass amax word
     float s, r;
     scales_from_amax<FMT, SF>(__uint_as_float(amax_g[0]), s, r);
 #pragma unroll
@@ -228,7 +259,7 @@ __global__ void __launch_bounds__(256, 2) quant_tile_kernel(QuantParams p, int g
       if (p.scales) p.scales[0] = s;
       if (p.scales_t) p.scales_t[0] = s;
     }
-  } else if (gran == LOKA_GRAN_ROW) {  // from the pre-pass row amax array
+  } else if constexpr (GRAN == LOKA_GRAN_ROW) {  // from the pre-pass row amax array
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int64_t row = r0 + warp * 16 + i * 2 + (lane >> 4);
@@ -252,12 +283,12 @@ __global__ void __launch_bounds__(256, 2) quant_tile_kernel(QuantParams p, int g
       }
     }
   }
-  // ---- cast; row-major codes straight to global, transposed through smem ----
+  // ---- cast; row-major codes straight to global, the transposed copy through smem ----
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     float f[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) f[k] = __fmul_rn(v[i].f(k), colwise ? rcol[k] : rrow[i]);
+    for (int k = 0; k < 8; ++k) f[k] = __fmul_rn(v[i].f(k), kColwise ? rcol[k] : rrow[i]);
     const uint32_t lo = cvt_fp8x4<FMT>(f[0], f[1], f[2], f[3]), hi = cvt_fp8x4<FMT>(f[4], f[5], f[6], f[7]);
     const int lr = warp * 16 + i * 2 + (lane >> 4);
     const int64_t row = r0 + lr;
@@ -267,27 +298,32 @@ __global__ void __launch_bounds__(256, 2) quant_tile_kernel(QuantParams p, int g
       else
         for (int k = 0; k < nc; ++k) dst[k] = (uint8_t)((k < 4 ? lo : hi) >> (8 * (k & 3)));
     }
-    if (p.qt) *reinterpret_cast<uint2*>(&tq[lr][cl]) = make_uint2(lo, hi);
+    if (p.qt) *reinterpret_cast<uint2*>(&tq[tq_off(lr, cl)]) = make_uint2(lo, hi);
   }
   if (p.qt) {
     __syncthreads();
-    // qt row (c0 + j) = column j of the tile: 128 codes from tq[0..127][j]; thread t writes 8
-    // consecutive codes (rows 8*(t&15) .. +7) of transposed row j = t >> 4 (+16 per pass)
-    const int t = threadIdx.x;
-    for (int j = t >> 4; j < 128; j += 16) {
-      const int64_t orow = c0 + j;
-      const int rb = (t & 15) * 8;
-      if (orow >= p.cols || r0 + rb >= p.rows) continue;
-      uint32_t w0 = 0, w1 = 0;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) w0 |= (uint32_t)tq[rb + k][j] << (8 * k);
+    for (int it = 0; it < 2; ++it) {
+      const int item = threadIdx.x + 256 * it;
+      const int rg = item & 15, cg = item >> 4;  // rows 8rg..8rg+7, columns 4cg..4cg+3 of the tile
+      uint32_t w[8];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) w1 |= (uint32_t)tq[rb + 4 + k][j] << (8 * k);
-      uint8_t* dst = p.qt + orow * p.ldqt + r0 + rb;
-      const int nr = (int)imin64(8, p.rows - (r0 + rb));
-      if (nr == 8 && ((reinterpret_cast<uintptr_t>(dst) & 7) == 0)) *reinterpret_cast<uint2*>(dst) = make_uint2(w0, w1);
-      else
-        for (int k = 0; k < nr; ++k) dst[k] = (uint8_t)((k < 4 ? w0 : w1) >> (8 * (k & 3)));
+      for (int i = 0; i < 8; ++i) w[i] = *reinterpret_cast<const uint32_t*>(&tq[tq_off(8 * rg + i, 4 * cg)]);
+      uint32_t lo[4], hi[4];
+      transpose4x4({w[0], w[1], w[2], w[3]}, lo);
+      transpose4x4({w[4], w[5], w[6], w[7]}, hi);
+      const int64_t rb = r0 + 8 * rg;
+      if (rb >= p.rows) continue;
+      const int nr = (int)imin64(8, p.rows - rb);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t orow = c0 + 4 * cg + k;
+        if (orow >= p.cols) break;
+        uint8_t* dst = p.qt + orow * p.ldqt + rb;
+        if (nr == 8) *reinterpret_cast<uint2*>(dst) = make_uint2(lo[k], hi[k]);
+        else
+          for (int j = 0; j < nr; ++j) dst[j] = (uint8_t)((j < 4 ? lo[k] : hi[k]) >> (8 * (j & 3)));
+      }
     }
   }
 }
@@ -326,7 +362,19 @@ static cudaError_t launch_tiled_t(const QuantParams& p, int gran, int phase, flo
     if (e == cudaSuccess) e = launch_pdl_t(col_amax_kernel<Tin>, tiles, dim3(256), st, p, amax);
   }
   if (e != cudaSuccess) return e;
-  return launch_pdl_t(quant_tile_kernel<Tin, FMT, SF>, tiles, dim3(256), st, p, gran, (const uint32_t*)amax);
+  const uint32_t* ag = amax;
+  switch (gran) {
+    case LOKA_GRAN_TENSOR: return launch_pdl_t(quant_tile_kernel<Tin, FMT, SF, LOKA_GRAN_TENSOR>, tiles, dim3(256), st, p, ag);
+    case LOKA_GRAN_ROW: return launch_pdl_t(quant_tile_kernel<Tin, FMT, SF, LOKA_GRAN_ROW>, tiles, dim3(256), st, p, ag);
+    case LOKA_GRAN_COL: return launch_pdl_t(quant_tile_kernel<Tin, FMT, SF, LOKA_GRAN_COL>, tiles, dim3(256), st, p, ag);
+    case LOKA_GRAN_BLK_1x128:
+      return launch_pdl_t(quant_tile_kernel<Tin, FMT, SF, LOKA_GRAN_BLK_1x128>, tiles, dim3(256), st, p, ag);
+    case LOKA_GRAN_BLK_128x1:
+      return launch_pdl_t(quant_tile_kernel<Tin, FMT, SF, LOKA_GRAN_BLK_128x1>, tiles, dim3(256), st, p, ag);
+    case LOKA_GRAN_BLK_128x128:
+      return launch_pdl_t(quant_tile_kernel<Tin, FMT, SF, LOKA_GRAN_BLK_128x128>, tiles, dim3(256), st, p, ag);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_quantize_tiled(const QuantParams& p, bool in_bf16, int fmt, int scale_fmt, int gran, int phase,
