@@ -74,7 +74,7 @@ LOKA_DEVINL SRow merge_rows(const SRow (&r)[K]) {
     o.ymax = fmaxf(o.ymax, r[k].ymax);
     o.ymin = fminf(o.ymin, r[k].ymin);
   }
-  o.mean = o.n > 0.f ? __fdiv_rn(s, o.n) : 0.f;
+  o.mean = o.n > 0.f ? s * __frcp_rn(o.n) : 0.f;  // (statistics need not be correctly rounded)
   float m2 = 0.f;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
@@ -268,13 +268,15 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
   }
   // ---- normalise (one FFMA) ----
   const float eps = p.eps[l];
-  const float eps_eff = fold ? __fdiv_rn(eps, __fmul_rn(sa, sa)) : eps;
+  // rstd by the hardware reciprocal square root (~2 ulp): the statistics are FP32 estimates of
+  // FP64 quantities anyway; only the FP8 scales derived from the normalised values are IEEE-exact
+  const float eps_eff = fold ? eps * __frcp_rn(sa * sa) : eps;
   float rstd = 1.f, c0 = 0.f;
   if (norm == LOKA_NORM_LAYER) {
-    rstd = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(rec.m2, rec.n), eps_eff)));
+    rstd = rsqrtf(fmaf(rec.m2, __frcp_rn(rec.n), eps_eff));
     c0 = -__fmul_rn(rec.mean, rstd);
   } else if (norm == LOKA_NORM_RMS) {
-    rstd = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(rec.ss, rec.n), eps_eff)));
+    rstd = rsqrtf(fmaf(rec.ss, __frcp_rn(rec.n), eps_eff));
   }
   if (norm != LOKA_NORM_NONE) {
     const float2 r2 = make_float2(rstd, rstd), c2 = make_float2(c0, c0);
