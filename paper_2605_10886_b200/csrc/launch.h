@@ -25,6 +25,15 @@ struct QuantParams {
 cudaError_t launch_quantize(const QuantParams& p, bool in_bf16, int fmt, int scale_fmt, int gran, int phase,
                             float* amax_dev, cudaStream_t st, int num_sms);
 
+// Streaming quantize through smem with bulk copies (quantize_tma.cu): ROW / TENSOR
+// cast (amax_dev = the tensor amax), bf16 input, no transposed copy; see quant_tma_eligible.
+bool quant_tma_eligible(const QuantParams& p, bool in_bf16, int gran);
+cudaError_t launch_quantize_tma(const QuantParams& p, int fmt, int scale_fmt, int gran, const float* amax_dev,
+                                int num_sms, cudaStream_t st);
+struct QuantGroup;
+cudaError_t launch_quantize_tma_group(const QuantGroup& grp, int64_t max_cols, int fmt, int scale_fmt, int gran,
+                                      const float* amax_dev, int num_sms, cudaStream_t st);
+
 // Tiled quantize (quantize_t.cu): any granularity incl. COL / BLK_128x1, optional transposed
 // copy; ws holds the ROW / COL amax pre-pass array (4 * max(rows, cols) bytes).
 cudaError_t launch_quantize_tiled(const QuantParams& p, bool in_bf16, int fmt, int scale_fmt, int gran, int phase,

@@ -8,6 +8,8 @@
 // load (8 bf16), keep the row/block in registers between the amax reduction and the cast
 // when it fits (one HBM read), and reduce amax on the integer bit pattern of |x|
 // (NaN > Inf > finite, so a non-finite element is detected from the reduced amax alone).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "launch.h"
 
@@ -173,6 +175,60 @@ __global__ void __launch_bounds__(256) quant_row_kernel(QuantParams p) {
   quant_row_body<Tin, FMT, SF, NREG>(p, row, lane);
 }
 
+// ----- ROW, streaming variant (no transposed copy, row fits NREG registers per lane): a
+// persistent grid of warps walks rows w, w + #warps, ...; the NEXT row's loads are issued before
+// the current row is reduced, cast and stored, so every warp keeps a row's worth of loads in
+// flight continuously (the one-row-per-warp kernel above idles between load bursts).
+template <typename Tin, int NREG>
+LOKA_DEVINL void load_row(Vec8<Tin> (&v)[NREG], const Tin* xr, int64_t cols, int lane) {
+#pragma unroll
+  for (int i = 0; i < NREG; ++i) {
+    const int64_t c = i * 256 + lane * 8;
+    if (c + 8 <= cols) v[i].load(xr + c);
+    else if (c < cols) v[i].load_partial(xr + c, (int)(cols - c));
+    else v[i].zero();
+  }
+}
+template <typename Tin, int FMT, int SF, int NREG>
+LOKA_DEVINL void emit_row(const Vec8<Tin> (&v)[NREG], const QuantParams& p, int64_t row, int lane) {
+  uint32_t am = 0;
+#pragma unroll
+  for (int i = 0; i < NREG; ++i) am = max(am, v[i].amax_bits());
+  am = warp_max_u32(am);
+  flag_nonfinite(am, p.status);
+  float s, r;
+  scales_from_amax<FMT, SF>(__uint_as_float(am), s, r);
+  if (lane == 0) {
+    if (p.scales) p.scales[row] = s;
+    if (p.scales_t) p.scales_t[row] = s;
+  }
+  uint8_t* qr = p.q + row * p.ldq;
+#pragma unroll
+  for (int i = 0; i < NREG; ++i) {
+    const int64_t c = i * 256 + lane * 8;
+    if (c < p.cols) store8(qr + c, cast8<FMT>(v[i], r), (int)imin64(8, p.cols - c));
+  }
+}
+template <typename Tin, int FMT, int SF, int NREG>
+__global__ void __launch_bounds__(256, 1) quant_row_stream_kernel(QuantParams p) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * 8;
+  int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const Tin* x = reinterpret_cast<const Tin*>(p.x);
+  Vec8<Tin> a[NREG];
+  if (row < p.rows) load_row<Tin, NREG>(a, x + row * p.ldx, p.cols, lane);
+  while (row < p.rows) {
+    const int64_t nrow = row + nw;
+    Vec8<Tin> b[NREG];
+    if (nrow < p.rows) load_row<Tin, NREG>(b, x + nrow * p.ldx, p.cols, lane);
+    emit_row<Tin, FMT, SF, NREG>(a, p, row, lane);
+#pragma unroll
+    for (int i = 0; i < NREG; ++i) a[i] = b[i];
+    row = nrow;
+  }
+}
+
 // ----- grouped ROW quantize: many tensors (e.g. an activation + every layer's weight) in one
 // launch; warp w of the grid takes global row w, located in tensor g by a prefix sum of rows.
 template <typename Tin, int FMT, int SF, int NREG>
@@ -312,18 +368,30 @@ __global__ void __launch_bounds__(256) cast_tensor_kernel(QuantParams p, const f
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nwarps = (int64_t)gridDim.x * 8;
+  constexpr int U = 4;  // loads in flight per lane before the first store (x and q may alias)
   for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < p.rows; row += nwarps) {
     const Tin* xr = reinterpret_cast<const Tin*>(p.x) + row * p.ldx;
-    for (int64_t c = lane * 8; c < p.cols; c += 256) {
-      Vec8<Tin> t;
-      const int n = (int)imin64(8, p.cols - c);
-      if (n == 8) t.load(xr + c);
-      else t.load_partial(xr + c, n);
-      uint2 code = cast8<FMT>(t, r);
-      if (p.q) store8(p.q + row * p.ldq + c, code, n);
-      if (p.qt) {
-        const uint8_t* b = reinterpret_cast<const uint8_t*>(&code);
-        for (int k = 0; k < n; ++k) p.qt[(c + k) * p.ldqt + row] = b[k];
+    for (int64_t c0 = lane * 8; c0 < p.cols; c0 += 256 * U) {
+      Vec8<Tin> t[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t c = c0 + 256 * u;
+        const int n = (int)imin64(8, p.cols - c);
+        if (n >= 8) t[u].load(xr + c);
+        else if (n > 0) t[u].load_partial(xr + c, n);
+        else t[u].zero();
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t c = c0 + 256 * u;
+        if (c >= p.cols) break;
+        const int n = (int)imin64(8, p.cols - c);
+        uint2 code = cast8<FMT>(t[u], r);
+        if (p.q) store8(p.q + row * p.ldq + c, code, n);
+        if (p.qt) {
+          const uint8_t* b = reinterpret_cast<const uint8_t*>(&code);
+          for (int k = 0; k < n; ++k) p.qt[(c + k) * p.ldqt + row] = b[k];
+        }
       }
     }
   }
@@ -346,17 +414,36 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cud
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+// LOKA_QUANT_TMA=0 keeps the register-resident kernels (A/B measurement; the outputs are identical)
+static bool quant_tma_use() {
+  static const bool off = [] {
+    const char* e = std::getenv("LOKA_QUANT_TMA");
+    return e && e[0] == '0';
+  }();
+  return !off;
+}
+
 template <typename Tin, int FMT, int SF>
 static cudaError_t launch_quant_t(const QuantParams& p, int gran, int phase, float* amax_dev, cudaStream_t st,
                                   int num_sms) {
   const dim3 blk(256);
   cudaError_t e = cudaSuccess;
+  const bool tma = quant_tma_use() && quant_tma_eligible(p, sizeof(Tin) == 2, gran) && p.rows >= 64;
+  if (tma && gran != LOKA_GRAN_TENSOR) return launch_quantize_tma(p, FMT, SF, gran, nullptr, num_sms, st);
   switch (gran) {
     case LOKA_GRAN_ROW: {
       const dim3 grd((unsigned)((p.rows + 7) / 8));
       constexpr int kBig = sizeof(Tin) == 2 ? 16 : 8;  // <= 64 data registers per lane
-      if (p.cols <= 256 * 4) e = launch_pdl(quant_row_kernel<Tin, FMT, SF, 4>, grd, blk, st, p);
-      else e = launch_pdl(quant_row_kernel<Tin, FMT, SF, kBig>, grd, blk, st, p);
+      const int64_t rows_per_pass = (int64_t)num_sms * 8;
+      if (p.q && !p.qt && p.rows > 2 * rows_per_pass && p.cols <= 256 * kBig) {  // streaming variant
+        const dim3 sg((unsigned)num_sms);
+        if (p.cols <= 256 * 4) e = launch_pdl(quant_row_stream_kernel<Tin, FMT, SF, 4>, sg, blk, st, p);
+        else e = launch_pdl(quant_row_stream_kernel<Tin, FMT, SF, kBig>, sg, blk, st, p);
+      } else if (p.cols <= 256 * 4) {
+        e = launch_pdl(quant_row_kernel<Tin, FMT, SF, 4>, grd, blk, st, p);
+      } else {
+        e = launch_pdl(quant_row_kernel<Tin, FMT, SF, kBig>, grd, blk, st, p);
+      }
       break;
     }
     case LOKA_GRAN_BLK_1x128:
@@ -377,8 +464,10 @@ static cudaError_t launch_quant_t(const QuantParams& p, int gran, int phase, flo
         e = launch_pdl(amax_tensor_kernel<Tin>, dim3((unsigned)nb), blk, st, p, reinterpret_cast<uint32_t*>(amax_dev));
         if (e != cudaSuccess) return e;
       }
-      if (phase == LOKA_PHASE_FULL || phase == LOKA_PHASE_CAST_WITH_AMAX)
-        e = launch_pdl(cast_tensor_kernel<Tin, FMT, SF>, dim3((unsigned)nb), blk, st, p, (const float*)amax_dev);
+      if (phase == LOKA_PHASE_FULL || phase == LOKA_PHASE_CAST_WITH_AMAX) {
+        if (tma) e = launch_quantize_tma(p, FMT, SF, gran, amax_dev, num_sms, st);
+        else e = launch_pdl(cast_tensor_kernel<Tin, FMT, SF>, dim3((unsigned)nb), blk, st, p, (const float*)amax_dev);
+      }
       break;
     }
     default:
@@ -413,6 +502,9 @@ namespace loka {
 
 template <typename Tin, int FMT, int SF>
 static cudaError_t launch_grouped_t(const QuantGroup& grp, int64_t max_cols, cudaStream_t st) {
+  bool tma = quant_tma_use() && sizeof(Tin) == 2;
+  for (int g = 0; g < grp.G && tma; ++g) tma = quant_tma_eligible(grp.p[g], true, LOKA_GRAN_ROW);
+  if (tma) return launch_quantize_tma_group(grp, max_cols, FMT, SF, LOKA_GRAN_ROW, nullptr, 148, st);
   const int64_t rows = grp.row_start[grp.G];
   const dim3 grd((unsigned)((rows + 7) / 8)), blk(256);
   constexpr int kBig = sizeof(Tin) == 2 ? 16 : 8;
