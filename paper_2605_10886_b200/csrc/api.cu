@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstring>
+#include <cmath>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -269,7 +270,11 @@ static size_t mx_ws_bytes(const loka_linear_args* a) {
   if (!is_mx(a) || a->M <= 0 || a->N <= 0 || a->K <= 0) return 0;
   return ((mx_pack_a_bytes(a) + 255) & ~size_t(255)) + mx_pack_b_bytes(a);
 }
-size_t loka_linear_workspace_size(const loka_linear_args* a) { return mx_ws_bytes(a); }
+static bool pair_eligible(const loka_linear_args* a);
+static size_t split_ws_bytes(const loka_linear_args* a);
+size_t loka_linear_workspace_size(const loka_linear_args* a) {
+  return mx_ws_bytes(a) + (pair_eligible(a) ? split_ws_bytes(a) : 0);
+}
 
 // Pack the UE8M0 scales of an MX problem into ws and point p at the packs.
 static loka_status mx_pack(const loka_linear_args* a, LinearParams* p, void* ws, size_t ws_bytes, cudaStream_t s) {
@@ -443,14 +448,53 @@ static bool use_pair_kernel() {
   return !one;
 }
 
-// A plain dequant(+bias) problem big enough to fill every SM pair with 256 x 256 tiles runs on
-// the CTA-pair persistent engine (gemm2.cu) as a one-problem group.
-static bool pair_eligible(const loka_linear_args* a) {
+// A plain dequant(+bias) problem (tensorwise / rowwise scales, bf16 / f32 out) the CTA-pair engine
+// can run.
+static bool plain_pair_ok(const loka_linear_args* a) {
   if (!a || !use_pair_kernel() || a->norm != LOKA_NORM_NONE || a->debug_precast || is_mx(a)) return false;
   if (a->a.gran != LOKA_GRAN_TENSOR && a->a.gran != LOKA_GRAN_ROW) return false;
   if (a->b.gran != LOKA_GRAN_TENSOR && a->b.gran != LOKA_GRAN_ROW) return false;
-  if (a->y.dtype != LOKA_BF16 && a->y.dtype != LOKA_F32) return false;
-  return cdiv(a->M, 256) * cdiv(a->N, 256) >= 74;
+  return a->y.dtype == LOKA_BF16 || a->y.dtype == LOKA_F32;
+}
+
+// Split-K for a lone problem with fewer 256 x 256 tiles than SM pairs and a long K (the paper's
+// 2048 x 123200 x 1024 layer): ks slices of kbps 128-K blocks; each slice's raw FP32
+// partial goes to the workspace and one reduction kernel applies the scales.  ks minimises
+// waves(ks) * kbps (in 128-K MMA-step units) + the partials' HBM round trip.
+static int split_k_for(const loka_linear_args* a, int* kbps_out = nullptr) {
+  constexpr int kPairs = 74;
+  if (kbps_out) *kbps_out = 0;
+  if (!plain_pair_ok(a) || a->M % 32 || a->N % 4 || a->M <= 0 || a->N <= 0 || a->K <= 0) return 1;
+  const int64_t tiles = cdiv(a->M, 256) * cdiv(a->N, 256), nkb = cdiv(a->K, 128);
+  if (tiles >= kPairs || nkb < 16) return 1;
+  double best = (double)nkb;  // one wave, no split
+  int bks = 1, bkbps = (int)nkb;
+  for (int ks = 2; ks <= 32; ++ks) {
+    const int64_t kbps = cdiv(nkb, ks);
+    if (kbps < 4) break;
+    const int64_t eks = cdiv(nkb, kbps);  // slices actually formed
+    const double waves = std::ceil((double)(tiles * eks) / kPairs);
+    const double part_steps = 2.0 * eks * (double)a->M * a->N * 4 / 6.5e12 / 0.376e-6;
+    const double cost = waves * (double)kbps + part_steps;
+    if (cost < best - 1e-9) {
+      best = cost;
+      bks = (int)eks;
+      bkbps = (int)kbps;
+    }
+  }
+  if (kbps_out) *kbps_out = bkbps;
+  return bks;
+}
+static size_t split_ws_bytes(const loka_linear_args* a) {
+  const int ks = split_k_for(a);
+  return ks > 1 ? (size_t)ks * (size_t)a->M * (size_t)a->N * 4 : 0;
+}
+
+// Large enough to fill every SM pair (directly or by split-K): runs on the CTA-pair persistent
+// engine (gemm2.cu) as a one-problem group.
+static bool pair_eligible(const loka_linear_args* a) {
+  if (!plain_pair_ok(a)) return false;
+  return cdiv(a->M, 256) * cdiv(a->N, 256) >= 74 || split_k_for(a) > 1;
 }
 
 loka_status loka_fp8_linear_norm(const loka_linear_args* a, void* ws, size_t ws_bytes, loka_stream_t stream) {
@@ -570,9 +614,11 @@ loka_status loka_fp8_mlp_stack(const loka_stack_args* a, loka_stream_t stream) {
 
 
 // MX problems need their scale packs (each 256-byte aligned, back to back); everything else none.
+// (a lone plain problem may also split K: its FP32 partials follow the MX packs)
 size_t loka_grouped_workspace_size(int32_t G, const loka_linear_args* a) {
   size_t n = 0;
   for (int g = 0; g < G && a; ++g) n += (mx_ws_bytes(&a[g]) + 255) & ~size_t(255);
+  if (G == 1 && a) n += split_ws_bytes(a);
   return n;
 }
 
@@ -606,6 +652,11 @@ loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* 
     (ok ? grouped : single).push_back(g);
   }
   std::stable_sort(grouped.begin(), grouped.end(), [&](int x, int y) { return a[x].K > a[y].K; });
+  int kbps = 0;
+  const int ksplit = (G == 1 && pair && grouped.size() == 1) ? split_k_for(&a[0], &kbps) : 1;
+  size_t mx_bytes = 0;
+  for (int g = 0; g < G; ++g) mx_bytes += (mx_ws_bytes(&a[g]) + 255) & ~size_t(255);
+  float* part = ksplit > 1 ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + mx_bytes) : nullptr;
   for (size_t i0 = 0; i0 < grouped.size(); i0 += kMaxGroups) {
     GroupedParams gp;
     std::memset(&gp, 0, sizeof(gp));
@@ -632,9 +683,17 @@ loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* 
       d.bias = q.bias;
       d.bias_bf16 = q.bias_dtype == LOKA_BF16;
       d.out_dtype = q.y.dtype;
-      gp.tile_start[k + 1] = gp.tile_start[k] + (int32_t)(cdiv(q.M, tile) * d.tiles_n);
+      d.ksplit = 1;
+      if (ksplit > 1) {  // G == 1
+        d.ksplit = ksplit;
+        d.kb_per_split = kbps;
+        if (!make_map_out(&gp.tp[k], part, (int64_t)ksplit * q.M, q.N, q.N, LOKA_F32, 128, 32u)) return LOKA_ERR_CUDA;
+      }
+      gp.tile_start[k + 1] = gp.tile_start[k] + (int32_t)(cdiv(q.M, tile) * d.tiles_n * d.ksplit);
     }
     if ((pair ? launch_grouped2(gp, sms, s) : launch_grouped(gp, sms, s)) != cudaSuccess) return LOKA_ERR_CUDA;
+    if (ksplit > 1 && launch_splitk_reduce(gp.g[0], part, a[0].y.data, a[0].y.ld, s) != cudaSuccess)
+      return LOKA_ERR_CUDA;
   }
   size_t ws_off = 0;
   for (int g : single) {

@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  int ks = 0;
   auto locate = [&](int t, int& g, int& mb, int& nb) {  // binary search of the tile prefix sum
     int lo = 0, hi = gp.G - 1;
     while (lo < hi) {
@@ -79,10 +80,23 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
       else hi = mid - 1;
     }
     g = lo;
-    const int local = t - gp.tile_start[g];
+    int local = t - gp.tile_start[g];
     const int tn = gp.g[g].tiles_n;
+    const int per = ((gp.g[g].M + 255) / 256) * tn;  // tiles of one K slice
+    ks = local / per;                                   // split-K slice (0 without split)
+    local -= ks * per;
     mb = local / tn;
     nb = local - mb * tn;
+  };
+  auto krange = [&](int g, int ks, int& kb0, int& kb1) {
+    const int nkb = (gp.g[g].K + 127) / 128;
+    if (gp.g[g].ksplit > 1) {
+      kb0 = ks * gp.g[g].kb_per_split;
+      kb1 = min(nkb, kb0 + gp.g[g].kb_per_split);
+    } else {
+      kb0 = 0;
+      kb1 = nkb;
+    }
   };
 
   if (warp == 0) {
@@ -93,8 +107,9 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
       for (int t = cid; t < T; t += ncl) {
         int g, mb, nb;
         locate(t, g, mb, nb);
-        const int nkb = (gp.g[g].K + 127) / 128;
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
+        int kb0, kb1;
+        krange(g, ks, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % k2Stages;
           const uint32_t ph = (uint32_t)(it / k2Stages) & 1u;
           mbar_wait(&empty_bar[s], ph ^ 1u, 1);
@@ -112,13 +127,14 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
       for (int t = cid; t < T; t += ncl, ++j) {
         int g, mb, nb;
         locate(t, g, mb, nb);
-        const int nkb = (gp.g[g].K + 127) / 128;
+        int kb0, kb1;
+        krange(g, ks, kb0, kb1);
         const int buf = j & 1;
         mbar_wait(&acc_empty[buf], ((uint32_t)(j >> 1) & 1u) ^ 1u, 4);  // both CTAs drained it
         tc_fence_after();
         const uint32_t idesc = idesc_f8f6f4(gp.g[g].a_fmt, gp.g[g].b_fmt, 256, 256);
         const uint32_t dacc = tmem_base + (uint32_t)(buf * 256);
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % k2Stages;
           const uint32_t ph = (uint32_t)(it / k2Stages) & 1u;
           mbar_wait(&full_bar[s], ph, 2);
@@ -128,7 +144,7 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             mma_f8f6f4_cg2(dacc, smem_desc_kmajor_sw128(a0 + k * 32), smem_desc_kmajor_sw128(b0 + k * 32), idesc,
-                           (kb | k) != 0);
+                           (kb > kb0 || k) ? 1u : 0u);
           mma_commit_cg2_mc(&empty_bar[s], 3);
         }
         mma_commit_cg2_mc(&acc_full[buf], 3);
@@ -168,8 +184,9 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
       tc_fence_after();
       const int row0 = mb * 256 + rank * 128 + q * 32;  // first row of this warp's box
       const int grow = row0 + lane;
-      const float sa = grow < d.M ? d.sa[d.sa_row ? grow : 0] : 0.f;
-      const int esz = d.out_dtype == LOKA_F32 ? 4 : 2;
+      const bool split = d.ksplit > 1;  // raw FP32 partial of K slice ks -> partial buffer
+      const float sa = grow < d.M ? (split ? 1.f : d.sa[d.sa_row ? grow : 0]) : 0.f;
+      const int esz = (split || d.out_dtype == LOKA_F32) ? 4 : 2;
       const int cpb = 128 / esz;  // columns per 128-byte box row
       const int col0 = nb * 256 + h * 128;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * 256 + h * 128);
@@ -185,7 +202,7 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
         const uint32_t cs = smem_u32(colp + h * 128 + cb);
         const float2 sa2 = make_float2(sa, sa);
 #pragma unroll
-        for (int c = 0; c < 32; c += 4) {  // y = acc * (s_a s_b) + bias, column params broadcast from smem
+        for (int c = 0; c < 32 && !split; c += 4) {  // y = acc * (s_a s_b) + bias, column params from smem
           const float4 s4 = lds_f4(cs + 4u * c), b4 = lds_f4(cs + 1024u + 4u * c);
           const float2 a = fadd2(fmul2(make_float2(y[c], y[c + 1]), fmul2(sa2, make_float2(s4.x, s4.y))),
                                  make_float2(b4.x, b4.y));
@@ -224,7 +241,10 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
           __syncwarp();
           if (lane == 0) {
             const int c0 = col0 + cb + 32 - cpb;
-            if (c0 < d.N && row0 < d.M) tma_store_2d(&gp.ty[g], box, c0, row0);
+            if (c0 < d.N && row0 < d.M) {
+              if (split) tma_store_2d(&gp.tp[g], box, c0, ks * d.M + row0);  // (M % 32 == 0 for split)
+              else tma_store_2d(&gp.ty[g], box, c0, row0);
+            }
             bulk_commit();
           }
           ++nbox;
@@ -241,6 +261,55 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
     tc_fence_after();
     tmem_dealloc_cg2<512>(tmem_base);
   }
+}
+
+// ---- split-K reduction: y = (sum over slices) * s_a[m] * s_b[n] (+ bias[n]), fixed slice order ----
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const GroupDesc d, const float* __restrict__ part,
+                                                            void* y, int64_t ldy) {
+  pdl_wait();
+  const int64_t n4 = d.N / 4, total = (int64_t)d.M * n4, slice = (int64_t)d.M * d.N;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / n4;
+    const int n = (int)(i - m * n4) * 4;
+    float4 acc = __ldg(reinterpret_cast<const float4*>(part + m * d.N + n));
+    for (int s = 1; s < d.ksplit; ++s) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(part + s * slice + m * d.N + n));
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    const float sa = d.sa[d.sa_row ? m : 0];
+    float o[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      o[k] = o[k] * (sa * d.sb[d.sb_row ? n + k : 0]);
+      if (d.bias)
+        o[k] += d.bias_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(d.bias)[n + k])
+                            : reinterpret_cast<const float*>(d.bias)[n + k];
+    }
+    if (d.out_dtype == LOKA_F32) {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + m * ldy + n) = make_float4(o[0], o[1], o[2], o[3]);
+    } else {
+      __nv_bfloat162 a = __floats2bfloat162_rn(o[0], o[1]), b = __floats2bfloat162_rn(o[2], o[3]);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(y) + m * ldy + n) =
+          make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+    }
+  }
+}
+
+cudaError_t launch_splitk_reduce(const GroupDesc& d, const float* part, void* y, int64_t ldy, cudaStream_t st) {
+  const int64_t total = (int64_t)d.M * (d.N / 4);
+  int64_t nb = (total + 255) / 256;
+  if (nb > 148 * 8) nb = 148 * 8;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)nb);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  note_launch();
+  return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel, d, part, y, ldy);
 }
 
 cudaError_t launch_grouped2(const GroupedParams& gp, int num_sms, cudaStream_t st) {

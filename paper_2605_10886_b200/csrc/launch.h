@@ -142,9 +142,13 @@ struct GroupDesc {
   const float* sb; int32_t sb_row;
   const void* bias; int32_t bias_bf16;
   int32_t out_dtype;
+  // split-K (CTA-pair engine only): ksplit slices of kb_per_split 128-K blocks; each writes its raw
+  // FP32 accumulator to the [ksplit][M][N] partial buffer (map tp), reduced by splitk_reduce
+  int32_t ksplit, kb_per_split;
 };
 struct GroupedParams {
   CUtensorMap ta[kMaxGroups], tb[kMaxGroups], ty[kMaxGroups];  // A box {128,128}, B box {128,128}, Y out
+  CUtensorMap tp[kMaxGroups];                                    // split-K partials [ksplit*M, N] f32
   GroupDesc g[kMaxGroups];
   int32_t G;
   int32_t tile_start[kMaxGroups + 1];  // prefix sum of 128x128 tiles
@@ -153,6 +157,8 @@ cudaError_t launch_grouped(const GroupedParams& gp, int num_sms, cudaStream_t st
 // CTA-pair variant (gemm2.cu): tiles 256 x 256 (tiles_n = ceil(N/256), tile_start counts them);
 // ta/tb boxes {128, 128}; ty box {128 bytes, 32 rows}, SW128; bf16 / f32 output.
 cudaError_t launch_grouped2(const GroupedParams& gp, int num_sms, cudaStream_t st);
+// y[m,n] = (sum_s part[s][m][n]) * s_a[m] * s_b[n] (+ bias[n]) -> y (bf16 / f32)
+cudaError_t launch_splitk_reduce(const GroupDesc& d, const float* part, void* y, int64_t ldy, cudaStream_t st);
 
 struct ProbeLayer {
   const void* out; const void* ref;

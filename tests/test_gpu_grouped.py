@@ -122,3 +122,28 @@ def test_single_cta_grouped_engine_still_correct():
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
                          cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("M,N,K,od,bias", [(512, 512, 8192, "f32", True), (2048, 1024, 16384, "bf16", False),
+                                           (256, 200, 4000, "bf16", True), (96, 1000, 2048, "f32", False)])
+def test_split_k_lone_gemm(M, N, K, od, bias):
+    """Few 256x256 tiles and a long K (the paper's 2048 x 123200 x 1024 layer, scaled down): the
+    CTA-pair engine splits K, writes FP32 partials to the workspace and reduces them in one kernel."""
+    x, w = synth.heavy(M, K, 80), synth.weight(N, K, 81)
+    xq, xs = lk.loka_quantize(to_dev_padded(x), "e4m3", "row")
+    wq, ws = lk.loka_quantize(to_dev_padded(w), "e4m3", "row")
+    b = torch.randn(N, generator=torch.Generator().manual_seed(5)).to(DEV) if bias else None
+    keep = []
+    args, y, _ = lk.make_linear_args(xq, xs, wq, ws, out_dtype=od, bias=b, keep=keep)
+    if M % 32 == 0 and N % 4 == 0:
+        assert lk.linear_workspace(args) > 0  # split chosen
+    y, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, out_dtype=od, bias=b)
+    torch.cuda.synchronize()
+    rows = torch.randperm(M, generator=torch.Generator().manual_seed(M))[:48].sort().values.to(DEV)
+    yo = oracle.linear.linear_norm(xq[rows].cpu().numpy(), xs[rows].cpu().numpy(), "e4m3", "row", wq.cpu().numpy(),
+                                   ws.cpu().numpy(), "e4m3", "row", bias=None if b is None else f64(b))
+    if od == "bf16":
+        _check_bf16(y[rows], yo)
+    else:
+        rms = np.sqrt(np.mean(yo ** 2, axis=1, keepdims=True))
+        assert np.max(np.abs(f64(y[rows]) - yo) / np.maximum(np.abs(yo), rms)) <= TOL
