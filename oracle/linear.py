@@ -19,6 +19,9 @@ DESIGN.md D15) and the norm that follows:
     PAPER.md:473 block 256; "unparameterized Grouped RMSNorm"):
     RMSNorm over each contiguous block of B columns, no gamma; N % B != 0 is an
     error (SPEC.md:399 IndivisibleFeatureDim).
+  * Hard Swish, applied to the norm's output
+    ("integrates seamlessly with BlockNorm, allowing both operations to be fused"):
+    h-swish(x) = x * ReLU6(x + 3) / 6, ReLU6(t) = min(max(t, 0), 6) (PAPER.md:502).
 """
 from __future__ import annotations
 
@@ -101,14 +104,29 @@ def apply_norm(y, norm="none", eps=None, gamma=None, beta=None, block=256):
     raise ValueError(norm)
 
 
+def hard_swish(x):
+    """PAPER.md:502: h-swish(x) = x * ReLU6(x + 3) / 6."""
+    x = np.asarray(x, np.float64)
+    return x * np.minimum(np.maximum(x + 3.0, 0.0), 6.0) / 6.0
+
+
+def apply_act(y, act="none"):
+    if act == "none":
+        return y
+    if act == "hardswish":
+        return hard_swish(y)
+    raise ValueError(act)
+
+
 def linear_norm(a_codes, a_scales, a_fmt, a_gran, b_codes, b_scales, b_fmt, b_gran,
-                bias=None, norm="none", eps=None, gamma=None, beta=None, block=256):
+                bias=None, norm="none", eps=None, gamma=None, beta=None, block=256, act="none"):
     """O6-O9 chain for C = A B^T with K-major operands A[M,K], B[N,K] (every direction
-    is this product once its operands are laid out K-major)."""
+    is this product once its operands are laid out K-major),
+    then the optional activation after the norm (NEXT-1)."""
     a_hat = Q.dequantize(a_codes, a_scales, a_fmt, a_gran)
     b_hat = Q.dequantize(b_codes, b_scales, b_fmt, b_gran)
     y = add_bias(matmul_nt(a_hat, b_hat), bias)
-    return apply_norm(y, norm, eps, gamma, beta, block)
+    return apply_act(apply_norm(y, norm, eps, gamma, beta, block), act)
 
 
 def round_bf16(v) -> np.ndarray:

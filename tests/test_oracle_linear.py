@@ -106,3 +106,29 @@ def test_bias_then_norm_and_round_bf16():
                         np.array([1.0 + 2 ** -8, 1.0 + 3 * 2 ** -8, -(1.0 + 2 ** -8), 2.0 ** -130])])
     ref = torch.from_numpy(v.astype(np.float32)).to(torch.bfloat16).to(torch.float64).numpy()
     assert np.array_equal(L.round_bf16(v), ref)  # fp32-exact inputs: torch's cast is a single RNE
+
+
+def test_hard_swish_closed_forms_and_torch():
+    """PAPER.md:502 h-swish(x) = x * ReLU6(x + 3) / 6: the piecewise closed form (0 below -3,
+    x above 3, x(x+3)/6 between; minimum -3/8 at x = -3/2), and torch's float64 hardswish."""
+    hs = L.hard_swish
+    assert hs(-3.0) == 0.0 and hs(-10.0) == 0.0 and hs(0.0) == 0.0
+    assert hs(3.0) == 3.0 and hs(7.5) == 7.5
+    assert hs(-1.5) == -0.375 and hs(1.0) == 1.0 * 4.0 / 6.0
+    x = np.linspace(-6, 6, 2401)
+    mid = (x > -3) & (x < 3)
+    assert np.allclose(hs(x)[mid], x[mid] * (x[mid] + 3) / 6, rtol=0, atol=1e-15)
+    assert hs(x).min() == -0.375
+    t = torch.from_numpy(np.random.default_rng(4).normal(0, 3, 10000))
+    assert np.allclose(hs(t.numpy()), torch.nn.functional.hardswish(t).numpy(), rtol=1e-15, atol=1e-15)
+
+
+def test_linear_norm_act_is_applied_after_the_norm():
+    rng = np.random.default_rng(7)
+    a, sa = Q.quantize(rng.normal(size=(6, 256)), "e4m3", "row")
+    b, sb = Q.quantize(rng.normal(size=(512, 256)), "e4m3", "row")
+    base = L.linear_norm(a, sa, "e4m3", "row", b, sb, "e4m3", "row", norm="block_rms", block=256)
+    act = L.linear_norm(a, sa, "e4m3", "row", b, sb, "e4m3", "row", norm="block_rms", block=256, act="hardswish")
+    assert np.array_equal(act, L.hard_swish(base))
+    assert np.array_equal(L.linear_norm(a, sa, "e4m3", "row", b, sb, "e4m3", "row", act="hardswish"),
+                          L.hard_swish(L.linear_norm(a, sa, "e4m3", "row", b, sb, "e4m3", "row")))
