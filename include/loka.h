@@ -96,6 +96,13 @@ typedef enum loka_norm {
                              ("RMSNorm((Wx + b).view(-1, BlockN)).view(B, N)")   */
 } loka_norm;
 
+/* Activation applied after the norm (PAPER.md:497-518 Hard Swish, "integrates seamlessly with
+ * BlockNorm, allowing both operations to be fused").                 */
+typedef enum loka_act {
+  LOKA_ACT_NONE = 0,
+  LOKA_ACT_HARDSWISH = 1 /* x * ReLU6(x + 3) / 6                              */
+} loka_act;
+
 /* GEMM direction ("separate optimization decisions for each direction").  The
  * kernel always computes C[M,N] = A[M,K] . B[N,K]^T with both operands K-major; the direction
  * says how the caller laid the operands out:
@@ -156,6 +163,8 @@ typedef struct loka_linear_args {
   float* debug_precast;     /* nullable [M,N] FP32 (ld = N): post-norm values before the
                                output cast, for tests                                        */
   int32_t* status_dev;      /* nullable                                                       */
+  loka_act act;             /* applied after the norm (and gamma/beta); NONE by default.  The
+                               FP8 output's row amax is then taken over the activated values  */
 } loka_linear_args;
 
 /* Y = epilogue(A . B^T): acc(FP32, TMEM) -> y = acc*sa[m]*sb[n] (+bias[n]) -> norm -> cast.

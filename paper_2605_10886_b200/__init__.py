@@ -31,6 +31,7 @@ GRAN = {"tensor": 0, "row": 1, "col": 2, "blk_1x128": 3, "blk_128x1": 4, "blk_12
 SCALE = {"f32": 0, "ue8m0": 1}
 PHASE = {"full": 0, "amax": 1, "cast": 2}
 NORM = {"none": 0, "layer": 1, "rms": 2, "block_rms": 3}
+ACT = {"none": 0, "hardswish": 1}
 DIR = {"fwd": 0, "dgrad": 1, "wgrad": 2}
 FMT = {"e4m3": E4M3, "e5m2": E5M2}
 _TORCH_DT = {F32: torch.float32, BF16: torch.bfloat16, E4M3: torch.uint8, E5M2: torch.uint8}
@@ -51,7 +52,8 @@ class loka_linear_args(C.Structure):
     _fields_ = [("M", C.c_int64), ("N", C.c_int64), ("K", C.c_int64), ("dir", C.c_int),
                 ("a", loka_tensor), ("b", loka_tensor), ("bias", C.c_void_p), ("bias_dtype", C.c_int),
                 ("norm", C.c_int), ("norm_block", C.c_int32), ("eps", C.c_float), ("gamma", C.c_void_p),
-                ("beta", C.c_void_p), ("y", loka_tensor), ("debug_precast", C.c_void_p), ("status_dev", C.c_void_p)]
+                ("beta", C.c_void_p), ("y", loka_tensor), ("debug_precast", C.c_void_p), ("status_dev", C.c_void_p),
+                ("act", C.c_int)]
 
 
 class loka_stack_args(C.Structure):
@@ -180,7 +182,7 @@ def loka_quantize(x: torch.Tensor, fmt: str = "e4m3", gran: str = "row", scale_f
 
 
 def make_linear_args(a, a_scales, b, b_scales, *, a_fmt="e4m3", b_fmt="e4m3", a_gran="row", b_gran="row",
-                     a_scale_fmt="f32", b_scale_fmt="f32", norm="none", norm_block=256, eps=0.0, gamma=None, beta=None, bias=None, out_dtype="f32",
+                     a_scale_fmt="f32", b_scale_fmt="f32", norm="none", act="none", norm_block=256, eps=0.0, gamma=None, beta=None, bias=None, out_dtype="f32",
                      y=None, y_scales=None, precast=None, status=None, direction="fwd", keep=None):
     """Build a loka_linear_args for C = A . B^T (A [M,K], B [N,K] FP8 codes, K-major)."""
     M, K = a.shape
@@ -203,6 +205,7 @@ def make_linear_args(a, a_scales, b, b_scales, *, a_fmt="e4m3", b_fmt="e4m3", a_
     args.y = _tensor(y, od, M, N, y_scales, "row")
     args.debug_precast = None if precast is None else precast.data_ptr()
     args.status_dev = None if status is None else status.data_ptr()
+    args.act = ACT[act]
     if keep is not None:  # keep python references alive as long as args is used
         keep.extend([a, a_scales, b, b_scales, bias, gamma, beta, y, y_scales, precast, status])
     return args, y, y_scales

@@ -319,6 +319,7 @@ static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CU
   if (a->norm < LOKA_NORM_NONE || a->norm > LOKA_NORM_BLOCK_RMS) return LOKA_ERR_INVALID_ARG;
   if (a->beta && a->norm != LOKA_NORM_LAYER) return LOKA_ERR_INVALID_ARG;
   if (a->gamma && a->norm != LOKA_NORM_LAYER && a->norm != LOKA_NORM_RMS) return LOKA_ERR_INVALID_ARG;
+  if (a->act != LOKA_ACT_NONE && a->act != LOKA_ACT_HARDSWISH) return LOKA_ERR_INVALID_ARG;
 
   // Tile width BN in {64,128,256}: the widest tile that still gives >= ~120 CTAs (most of the
   // 148 SMs) for this M, else the narrowest allowed.  Row-coupled epilogues (full-row norm or an
@@ -377,6 +378,7 @@ static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CU
   p->ld_pre = N;
   p->status = a->status_dev;
   p->cluster_n = csize;
+  p->act = a->act;
   p->mx = mx ? 1 : 0;
   *bn_out = bn;
   return LOKA_OK;
@@ -403,7 +405,7 @@ static loka_status prepare_bw(const loka_linear_args* a, CUtensorMap* ta, CUtens
   if (Y.ld < N || (Y.ld * elem_size(Y.dtype)) % 16) return LOKA_ERR_INVALID_ARG;
   const bool fp8_out = is_fp8(Y.dtype);
   if (fp8_out && (!Y.scales || Y.gran != LOKA_GRAN_ROW || N > 128)) return LOKA_ERR_UNSUPPORTED;
-  if (a->norm != LOKA_NORM_NONE || a->gamma || a->beta) return LOKA_ERR_UNSUPPORTED;
+  if (a->norm != LOKA_NORM_NONE || a->gamma || a->beta || a->act != LOKA_ACT_NONE) return LOKA_ERR_UNSUPPORTED;
   if (a->bias && a->bias_dtype != LOKA_F32 && a->bias_dtype != LOKA_BF16) return LOKA_ERR_INVALID_ARG;
   if (!make_map_u8(ta, A.data, M, K, A.ld, 128)) return LOKA_ERR_CUDA;
   if (!make_map_u8(tb, B.data, N, K, B.ld, 128)) return LOKA_ERR_CUDA;
@@ -451,7 +453,9 @@ static bool use_pair_kernel() {
 // A plain dequant(+bias) problem (tensorwise / rowwise scales, bf16 / f32 out) the CTA-pair engine
 // can run.
 static bool plain_pair_ok(const loka_linear_args* a) {
-  if (!a || !use_pair_kernel() || a->norm != LOKA_NORM_NONE || a->debug_precast || is_mx(a)) return false;
+  if (!a || !use_pair_kernel() || a->norm != LOKA_NORM_NONE || a->act != LOKA_ACT_NONE || a->debug_precast ||
+      is_mx(a))
+    return false;
   if (a->a.gran != LOKA_GRAN_TENSOR && a->a.gran != LOKA_GRAN_ROW) return false;
   if (a->b.gran != LOKA_GRAN_TENSOR && a->b.gran != LOKA_GRAN_ROW) return false;
   return a->y.dtype == LOKA_BF16 || a->y.dtype == LOKA_F32;
@@ -647,7 +651,8 @@ loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* 
   const bool pair = use_pair_kernel();
   std::vector<int> grouped, single;
   for (int g = 0; g < G; ++g) {
-    const bool ok = a[g].norm == LOKA_NORM_NONE && !a[g].debug_precast && !is_blockwise(&a[g]) && !is_mx(&a[g]) &&
+    const bool ok = a[g].norm == LOKA_NORM_NONE && a[g].act == LOKA_ACT_NONE && !a[g].debug_precast &&
+                    !is_blockwise(&a[g]) && !is_mx(&a[g]) &&
                     (a[g].y.dtype == LOKA_BF16 || (pair && a[g].y.dtype == LOKA_F32));
     (ok ? grouped : single).push_back(g);
   }

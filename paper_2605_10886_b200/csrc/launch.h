@@ -65,6 +65,7 @@ struct LinearParams {
   float* precast; int64_t ld_pre;
   int32_t* status;
   int32_t cluster_n;             // CTAs per cluster along N (1 = no cross-CTA row exchange)
+  int32_t act;                   // loka_act, applied after the norm (and gamma / beta)
   // native block-scaled (MX) mode: UE8M0 blockwise scales applied by the tensor core; sa/sb unused
   int32_t mx;
   const uint8_t* sfa_pack;       // [ceil(M/128)][kblocks][512] (sfpack.cu layout)

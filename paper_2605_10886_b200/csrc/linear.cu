@@ -168,7 +168,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int norm = p.norm;
   const bool is_fp8_out = p.out_dtype == LOKA_E4M3 || p.out_dtype == LOKA_E5M2;
-  const bool affine = p.gamma != nullptr || p.beta != nullptr;
+  // affine (gamma/beta) and the activation make the output non-monotone in y: the FP8 row amax
+  // is then reduced over the final values instead of derived from y max / min
+  const bool affine = p.gamma != nullptr || p.beta != nullptr || p.act != LOKA_ACT_NONE;
+  const bool has_gb = p.gamma != nullptr || p.beta != nullptr;
   const bool is_block = norm == LOKA_NORM_BLOCK_RMS;
   // cluster-wide barriers: every thread of the CTA executes the same count (uniform)
   const bool xchg_stats = csize > 1 && !is_block && (norm != LOKA_NORM_NONE || (is_fp8_out && !affine));
@@ -445,7 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < CPT; j += 4) {
         float2 a = ffma2(make_float2(y[j], y[j + 1]), r2, c2);
         float2 b = ffma2(make_float2(y[j + 2], y[j + 3]), r2, c2);
-        if (affine) {
+        if (has_gb) {
           const uint32_t o = (uint32_t)(cb + j) * 4u;
           const float4 g4 = lds_f4(col_s + 2u * BN * 4u + o);
           const float4 e4 = lds_f4(col_s + 3u * BN * 4u + o);
@@ -453,6 +456,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           b = ffma2(b, make_float2(g4.z, g4.w), make_float2(e4.z, e4.w));
         }
         y[j] = a.x; y[j + 1] = a.y; y[j + 2] = b.x; y[j + 3] = b.y;
+      }
+    }
+
+    // ---- activation (PAPER.md:502 Hard Swish): x * ReLU6(x + 3) / 6 ----
+    if (p.act == LOKA_ACT_HARDSWISH) {
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) {
+        const float t = fminf(fmaxf(y[j] + 3.f, 0.f), 6.f);
+        y[j] = __fdiv_rn(__fmul_rn(y[j], t), 6.f);
       }
     }
 

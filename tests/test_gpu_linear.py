@@ -154,3 +154,51 @@ def test_cfg2_stack_full_size():
             assert_bytes_equal(y[rows], oq)
             assert_scales_equal(ys[rows], os_)
             hq, hs = y, ys
+
+
+@pytest.mark.parametrize("norm,N", [("block_rms", 1024), ("block_rms", 256), ("layer", 512), ("rms", 2048),
+                                    ("none", 384)])
+def test_hardswish_after_norm_f32(norm, N):
+    """NEXT-1: Hard Swish fused after the norm in the same epilogue."""
+    M, K = 300, 512
+    xq, xs, wq, ws = _operands(M, N, K, 31, xdist="heavy")
+    y, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm=norm, act="hardswish", out_dtype="f32")
+    torch.cuda.synchronize()
+    yo = _oracle(xq, xs, wq, ws, norm=norm, act="hardswish")
+    # guard from the pre-activation scale: h-swish shrinks values near zero but its slope is <= 1.5
+    pre = _oracle(xq, xs, wq, ws, norm=norm)
+    rms = np.sqrt(np.mean(pre ** 2, axis=1, keepdims=True))
+    assert np.max(np.abs(f64(y) - yo) / np.maximum(np.abs(pre), rms)) <= 1.5 * TOL
+
+
+@pytest.mark.parametrize("norm,N", [("block_rms", 1024), ("layer", 256)])
+def test_hardswish_fp8_output_bit_exact(norm, N):
+    """The row amax of an activated row is reduced over the activated values (h-swish is not
+    monotone): codes + scales equal the oracle's rowwise quantize of the GPU's pre-cast values."""
+    M, K = 256, 384
+    xq, xs, wq, ws = _operands(M, N, K, 33, xdist="heavy")
+    pre = torch.empty(M, N, dtype=torch.float32, device=DEV)
+    y, ys = lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm=norm, act="hardswish", out_dtype="e4m3", precast=pre)
+    torch.cuda.synchronize()
+    oq, os_ = oracle.quantize.quantize(f64(pre), "e4m3", "row")
+    assert_scales_equal(ys, os_)
+    assert_bytes_equal(y, oq)
+    yo = _oracle(xq, xs, wq, ws, norm=norm, act="hardswish")
+    rms = np.sqrt(np.mean(_oracle(xq, xs, wq, ws, norm=norm) ** 2, axis=1, keepdims=True))
+    assert np.max(np.abs(f64(pre) - yo) / np.maximum(np.abs(yo), rms)) <= 1.5 * TOL
+
+
+def test_hardswish_with_gamma_beta_bf16():
+    M, N, K = 256, 512, 256
+    xq, xs, wq, ws = _operands(M, N, K, 35)
+    g = torch.Generator().manual_seed(2)
+    gamma = (1 + 0.2 * torch.randn(N, generator=g)).float()
+    beta = (0.5 * torch.randn(N, generator=g)).float()
+    y, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm="layer", gamma=gamma.to(DEV), beta=beta.to(DEV),
+                                   act="hardswish", out_dtype="bf16")
+    torch.cuda.synchronize()
+    yo = _oracle(xq, xs, wq, ws, norm="layer", gamma=gamma.double().numpy(), beta=beta.double().numpy(),
+                 act="hardswish")
+    pre = _oracle(xq, xs, wq, ws, norm="layer", gamma=gamma.double().numpy(), beta=beta.double().numpy())
+    rms = np.sqrt(np.mean(pre ** 2, axis=1, keepdims=True))
+    assert np.all(np.abs(f64(y) - yo) <= 1.5 * TOL * np.maximum(np.abs(pre), rms) + 2.0 ** -8 * np.abs(yo))
