@@ -414,7 +414,7 @@ def main():
                          "timing": "graph of the launch, L2 flushed before each replay, CUDA events"},
             "per_layer_path": {"ms_per_step": round(per_layer_ms, 5),
                                "value": round(flops_per_step() / (per_layer_ms * 1e-3) / 1e12, 3),
-                               "impl": "grouped quantize + 8 linear_norm launches (same output bits)"},
+                               "impl": "grouped quantize + 8 linear_norm launches (same layers, per-layer kernels)"},
             "e2e": {"value": round(e2e_value, 3), "unit": "TFLOP/s", "ms_per_step": round(ms_e2e, 5),
                     "h2d_bytes_per_step": int(x.numel() * 2), "d2h_bytes_per_step": int(stack.y.numel() * 2)},
             "gpu_launches": int(launches_per_step * args.steps),
