@@ -45,6 +45,27 @@ LOKA_DEVINL void load4(const void* base, int bf16, int64_t off, float (&v)[4], i
   }
 }
 
+// 8 consecutive elements (16 B of bf16 / 32 B of f32 when the row is 16-byte aligned)
+LOKA_DEVINL void load8(const void* base, int bf16, int64_t off, float (&v)[8], int n, int vec) {
+  if (n == 8 && vec) {
+    if (bf16) {
+      const uint4 w = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(base) + off));
+      v[0] = bf16lo_to_f32(w.x); v[1] = bf16hi_to_f32(w.x); v[2] = bf16lo_to_f32(w.y); v[3] = bf16hi_to_f32(w.y);
+      v[4] = bf16lo_to_f32(w.z); v[5] = bf16hi_to_f32(w.z); v[6] = bf16lo_to_f32(w.w); v[7] = bf16hi_to_f32(w.w);
+    } else {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(base) + off));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(base) + off) + 1);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    }
+  } else {
+    float t[4];
+    load4(base, bf16, off, t, n < 4 ? n : 4, 0);
+    v[0] = t[0]; v[1] = t[1]; v[2] = t[2]; v[3] = t[3];
+    load4(base, bf16, off + 4, t, n > 4 ? n - 4 : 0, 0);
+    v[4] = t[0]; v[5] = t[1]; v[6] = t[2]; v[7] = t[3];
+  }
+}
+
 template <typename T>
 LOKA_DEVINL T block_sum(T v, T* red) {
 #pragma unroll
@@ -65,10 +86,15 @@ __global__ void __launch_bounds__(256) probe_p1(const __grid_constant__ ProbeBat
   const int64_t nw = (int64_t)nblk * 8;
   double acc = 0.0;
   for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < L.M; row += nw) {
-    for (int64_t c = lane * 4; c < L.N; c += 128) {
-      float v[4];
-      load4(L.ref, L.ref_bf16, row * L.ld_ref + c, v, (int)imin64(4, L.N - c), L.ref_vec);
-      acc += (double)(fabsf(v[0]) + fabsf(v[1])) + (double)(fabsf(v[2]) + fabsf(v[3]));
+    for (int64_t c0 = lane * 8; c0 < L.N; c0 += 512) {  // two independent 16-B loads per lane in flight
+      float v[8], u[8];
+      load8(L.ref, L.ref_bf16, row * L.ld_ref + c0, v, (int)max((int64_t)0, imin64(8, L.N - c0)), L.ref_vec);
+      load8(L.ref, L.ref_bf16, row * L.ld_ref + c0 + 256, u, (int)max((int64_t)0, imin64(8, L.N - c0 - 256)),
+            L.ref_vec);
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s += fabsf(v[i]) + fabsf(u[i]);
+      acc += (double)s;
     }
   }
   const double t = block_sum(acc, red);
@@ -82,33 +108,91 @@ __global__ void __launch_bounds__(256) probe_p2(const __grid_constant__ ProbeBat
   __shared__ long long redl[8];
   __shared__ float redf[8];
   const ProbeLayer& L = b.layer[blockIdx.y];
+  // f from the P1 partials: a fixed-shape parallel reduction (every block derives the same value)
   double sabs = 0.0;
-  for (int i = 0; i < nblk; ++i) sabs += part1[(int64_t)blockIdx.y * nblk + i];
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) sabs += part1[(int64_t)blockIdx.y * nblk + i];
+  sabs = block_sum(sabs, red);
   const int64_t count = L.M * L.N;
   const double f = count > 0 ? floor_rel * (sabs / (double)count) : 0.0;
-  const float f32 = (float)f;  // used only as the denominator; the floored decision is in FP64
+  const float f32 = (float)f;  // used only as the denominator
+  // floored <=> |r| < f (FP64).  For an FP32 |r| that is |r| < t with t = f rounded UP to FP32
+  // (no FP32 value lies in [f, t)), so the decision stays exact with an FP32 compare.
+  const float ft = __double2float_ru(f);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nw = (int64_t)nblk * 8;
   double acc = 0.0;
   float mx = 0.f;
-  long long nfl = 0;
+  unsigned nfl32 = 0;
   for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < L.M; row += nw) {
-    for (int64_t c = lane * 4; c < L.N; c += 128) {
-      const int n = (int)imin64(4, L.N - c);
-      float o[4], r[4];
-      load4(L.out, L.out_bf16, row * L.ld_out + c, o, n, L.out_vec);
-      load4(L.ref, L.ref_bf16, row * L.ld_ref + c, r, n, L.ref_vec);
-      float part = 0.f;
+    // fast path for whole 512-column spans of aligned rows: two independent 16-B loads of each
+    // operand per lane in flight
+    const bool fast = L.out_vec && L.ref_vec && L.out_bf16 && L.ref_bf16 && f32 > 0.f;
+    int64_t cstart = lane * 8;
+    if (fast) {
+      constexpr int U = 4;  // 16-B loads of each operand per lane in flight
+      for (; (cstart - lane * 8) + 256 * U <= L.N; cstart += 256 * U) {  // warp-uniform span test
+        const __nv_bfloat16* op = reinterpret_cast<const __nv_bfloat16*>(L.out) + row * L.ld_out + cstart;
+        const __nv_bfloat16* rp = reinterpret_cast<const __nv_bfloat16*>(L.ref) + row * L.ld_ref + cstart;
+        uint4 ov4[U], rv4[U];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+        for (int u = 0; u < U; ++u) {
+          ov4[u] = __ldg(reinterpret_cast<const uint4*>(op + 256 * u));
+          rv4[u] = __ldg(reinterpret_cast<const uint4*>(rp + 256 * u));
+        }
+        uint32_t ow[4 * U], rw[4 * U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          ow[4 * u] = ov4[u].x; ow[4 * u + 1] = ov4[u].y; ow[4 * u + 2] = ov4[u].z; ow[4 * u + 3] = ov4[u].w;
+          rw[4 * u] = rv4[u].x; rw[4 * u + 1] = rv4[u].y; rw[4 * u + 2] = rv4[u].z; rw[4 * u + 3] = rv4[u].w;
+        }
+        float part = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8 * U; ++i) {
+          const float ov = (i & 1) ? bf16hi_to_f32(ow[i >> 1]) : bf16lo_to_f32(ow[i >> 1]);
+          const float rv = (i & 1) ? bf16hi_to_f32(rw[i >> 1]) : bf16lo_to_f32(rw[i >> 1]);
+          const float ar = fabsf(rv);
+          nfl32 += ar < ft ? 1u : 0u;
+          // den = max(|r|, f32) equals the floored select exactly (the only FP32 value in
+          // [f32, ft) is f32 itself); the fast division (<= 2 ulp) is far inside the 1e-5 bar
+          const float rel = __fdividef(fabsf(__fsub_rn(ov, rv)), fmaxf(ar, f32));
+          part += rel;
+          mx = fmaxf(mx, rel);
+        }
+        acc += (double)part;
+      }
+    }
+    for (int64_t c = cstart; c < L.N; c += 256) {
+      const int n = (int)imin64(8, L.N - c);
+      float o[8], r[8];
+      load8(L.out, L.out_bf16, row * L.ld_out + c, o, n, L.out_vec);
+      load8(L.ref, L.ref_bf16, row * L.ld_ref + c, r, n, L.ref_vec);
+      float part = 0.f;
+      if (n == 8 && f32 > 0.f) {
+        // fast path: den = max(|r|, f32) equals the floored select exactly (the only FP32 value in
+        // [f32, ft) is f32 itself), so no branches; ~10 instructions per element
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float ar = fabsf(r[i]);
+          nfl32 += ar < ft ? 1u : 0u;
+          const float rel = __fdividef(fabsf(__fsub_rn(o[i], r[i])), fmaxf(ar, f32));
+          part += rel;
+          mx = fmaxf(mx, rel);
+        }
+        acc += (double)part;
+        continue;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
         if (i < n) {
           const float ar = fabsf(r[i]);
-          const bool floored = (double)ar < f;
-          nfl += floored ? 1 : 0;
+          const bool floored = ar < ft;  // == (double)ar < f (D10)
+          nfl32 += floored ? 1u : 0u;
           const float den = floored ? f32 : ar;
           const float d = fabsf(__fsub_rn(o[i], r[i]));
+          // den >= f is a normal FP32 number: the fast division (<= 2 ulp) is far inside the
+          // statistic's 1e-5 tolerance (SV §8(c) parity matrix)
           float rel;
-          if (den > 0.f) rel = __fdiv_rn(d, den);
+          if (den > 0.f) rel = __fdividef(d, den);
           else rel = d > 0.f ? INFINITY : 0.f;
           part += rel;
           mx = fmaxf(mx, rel);
@@ -118,7 +202,7 @@ __global__ void __launch_bounds__(256) probe_p2(const __grid_constant__ ProbeBat
     }
   }
   const double t = block_sum(acc, red);
-  const long long tf = block_sum(nfl, redl);
+  const long long tf = block_sum((long long)nfl32, redl);
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
   __syncthreads();
