@@ -72,6 +72,20 @@ static bool make_map_u8(CUtensorMap* m, const void* ptr, int64_t rows, int64_t c
 
 static int elem_size(loka_dtype t) { return t == LOKA_F32 ? 4 : t == LOKA_BF16 ? 2 : 1; }
 
+// 2D map over a UE8M0 scale pack ([atoms][kblocks][512 B]) viewed as rows of 256 bytes; one box
+// {256, 2} is one atom, no swizzle (the tcgen05.cp source layout is the plain 512-byte atom).
+static bool make_map_pack(CUtensorMap* m, const void* ptr, int64_t rows256) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {256, (cuuint64_t)rows256};
+  cuuint64_t strides[1] = {256};
+  cuuint32_t box[2] = {256u, 2u};
+  cuuint32_t es[2] = {1u, 1u};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // 2D map over the GEMM output [rows, cols] of dtype t (ld elements), box {min(128, bn*e) bytes,
 // 128 rows} with the matching 128B / 64B swizzle — the layout of the epilogue's staging tile.
 static bool make_map_out(CUtensorMap* m, void* ptr, int64_t rows, int64_t cols, int64_t ld, loka_dtype t, int bn,
@@ -501,8 +515,56 @@ static bool pair_eligible(const loka_linear_args* a) {
   return cdiv(a->M, 256) * cdiv(a->N, 256) >= 74 || split_k_for(a) > 1;
 }
 
+// A UE8M0 blockwise problem with the plain epilogue that fills the SM pairs runs on the CTA-pair
+// block-scaled kernel (gemm2.cu mx_pair_kernel); others on linear_norm's MX mode.
+static bool mx_pair_ok(const loka_linear_args* a) {
+  if (!is_mx(a) || !use_pair_kernel() || a->norm != LOKA_NORM_NONE || a->act != LOKA_ACT_NONE || a->debug_precast)
+    return false;
+  if (a->y.dtype != LOKA_BF16 && a->y.dtype != LOKA_F32) return false;
+  return cdiv(a->M, 256) * cdiv(a->N, 256) >= 74;
+}
+static loka_status run_mx_pair(const loka_linear_args* a, void* ws, size_t ws_bytes, cudaStream_t s, int sms) {
+  CUtensorMap ta, tb, ty;
+  LinearParams lp;
+  int bn = 0;
+  loka_status st = prepare_linear(a, &ta, &tb, &ty, &lp, &bn);  // validation (maps rebuilt below)
+  if (st != LOKA_OK) return st;
+  st = mx_pack(a, &lp, ws, ws_bytes, s);
+  if (st != LOKA_OK) return st;
+  MxPairParams mp;
+  std::memset(&mp, 0, sizeof(mp));
+  const loka_tensor &A = a->a, &B = a->b, &Y = a->y;
+  if (!make_map_u8(&mp.ta, A.data, a->M, a->K, A.ld, 128)) return LOKA_ERR_CUDA;
+  if (!make_map_u8(&mp.tb, B.data, a->N, a->K, B.ld, 128)) return LOKA_ERR_CUDA;
+  if (!make_map_out(&mp.ty, Y.data, a->M, a->N, Y.ld, Y.dtype, 128, 32u)) return LOKA_ERR_CUDA;
+  const int64_t kbs = cdiv(a->K, 128);
+  if (!make_map_pack(&mp.tsa, lp.sfa_pack, cdiv(a->M, 128) * kbs * 2)) return LOKA_ERR_CUDA;
+  if (!make_map_pack(&mp.tsb, lp.sfb_pack, cdiv(a->N, 256) * 2 * kbs * 2)) return LOKA_ERR_CUDA;
+  GroupDesc& d = mp.d;
+  d.M = (int32_t)a->M;
+  d.N = (int32_t)a->N;
+  d.K = (int32_t)a->K;
+  d.tiles_n = (int32_t)cdiv(a->N, 256);
+  d.a_fmt = A.dtype == LOKA_E5M2 ? 1 : 0;
+  d.b_fmt = B.dtype == LOKA_E5M2 ? 1 : 0;
+  d.bias = a->bias;
+  d.bias_bf16 = a->bias_dtype == LOKA_BF16;
+  d.out_dtype = Y.dtype;
+  d.ksplit = 1;
+  mp.sf_kbs = (int32_t)kbs;
+  mp.tiles = (int32_t)(cdiv(a->M, 256) * d.tiles_n);
+  return launch_mx_pair(mp, sms, s) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
+}
+
 loka_status loka_fp8_linear_norm(const loka_linear_args* a, void* ws, size_t ws_bytes, loka_stream_t stream) {
   if (is_blockwise(a)) return run_bw(a, reinterpret_cast<cudaStream_t>(stream));
+  if (mx_pair_ok(a)) {
+    if (!ws || ws_bytes < mx_ws_bytes(a) || !aligned16(ws)) return LOKA_ERR_WORKSPACE;
+    int sms = 148;
+    loka_status st = check_device(&sms);
+    if (st != LOKA_OK) return st;
+    return run_mx_pair(a, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream), sms);
+  }
   if (pair_eligible(a)) return loka_grouped_fp8_linear(1, a, ws, ws_bytes, stream);
   CUtensorMap ta, tb, ty;
   LinearParams p;
@@ -702,6 +764,13 @@ loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* 
   }
   size_t ws_off = 0;
   for (int g : single) {
+    if (mx_pair_ok(&a[g])) {
+      const size_t nb = (mx_ws_bytes(&a[g]) + 255) & ~size_t(255);
+      loka_status sm = run_mx_pair(&a[g], static_cast<uint8_t*>(ws) + ws_off, nb, s, sms);
+      if (sm != LOKA_OK) return sm;
+      ws_off += nb;
+      continue;
+    }
     if (is_mx(&a[g])) {
       const size_t nb = (mx_ws_bytes(&a[g]) + 255) & ~size_t(255);
       loka_status sm = mx_pack(&a[g], &p[g], static_cast<uint8_t*>(ws) + ws_off, nb, s);

@@ -317,6 +317,25 @@ LOKA_DEVINL void mma_f8f6f4_cg2(uint32_t tmem_d, uint64_t da, uint64_t db, uint3
       "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// block-scaled (UE8M0 per 32-K) variant of the pair MMA; scale factors in each CTA's TMEM
+LOKA_DEVINL void mma_mxf8f6f4_cg2(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t tsfa,
+                                  uint32_t tsfb, uint32_t k, uint32_t accumulate) {
+  const uint32_t id = idesc | (k << 29) | (k << 4);
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %6, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%4], [%5], p;\n}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(id), "r"(tsfa | (k << 30)), "r"(tsfb | (k << 30)), "r"(accumulate)
+      : "memory");
+}
+// smem -> TMEM scale-factor atom copy in both CTAs of the pair (each from its own smem)
+LOKA_DEVINL void utccp_32x128b_warpx4_cg2(uint32_t tmem_dst, uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)(128u >> 4) << 16;
+  d |= (uint64_t)(128u >> 4) << 32;
+  d |= (uint64_t)1u << 46;
+  asm volatile("tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;" ::"r"(tmem_dst), "l"(d) : "memory");
+}
 // arrive on `bar` (same offset) in every CTA of cta_mask once the issued MMAs complete
 LOKA_DEVINL void mma_commit_cg2_mc(uint64_t* bar, uint16_t cta_mask) {
   asm volatile(

@@ -263,6 +263,243 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
   }
 }
 
+// ---- native block-scaled (UE8M0, MX) GEMM on the CTA pair --------------------------------------
+// One problem, 256 x 256 tiles, tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale.  Per 128-K stage
+// each CTA stages, next to its A rows and half of B, the UE8M0 atoms the MMA needs in ITS TMEM:
+// SFA for its 128 rows (512 B) and SFB for all 256 columns of the tile (2 x 512 B; CUTLASS's 2-SM
+// block-scaled layout); the leader copies them smem -> TMEM in both CTAs with
+// tcgen05.cp.cta_group::2 right before the stage's MMAs (same pipeline, issue order).  TMEM: one
+// 256-column accumulator + a 4-stage ring of 12 scale columns, so the accumulator is single-
+// buffered: the epilogue warps pull their 128 columns into registers first and release it at once.
+constexpr int kMxStages = 4;
+constexpr int kMxSf = 512 * 3;                                   // SFA + 2 SFB atoms per stage
+constexpr int kMxOffB = kMxStages * k2StageA;
+constexpr int kMxOffSf = kMxOffB + kMxStages * k2StageB;
+constexpr int kMxOffOut = kMxOffSf + kMxStages * kMxSf;          // [8 warps][2][4096]
+constexpr int kMxOffCol = kMxOffOut + k2EpiWarps * 2 * 4096;     // bias [256]
+constexpr int kMxOffBar = kMxOffCol + 256 * 4;
+constexpr int kMxSmem = kMxOffBar + 256 + 1024;
+static_assert(kMxSmem <= 227 * 1024, "mx pair smem");
+
+__global__ void __launch_bounds__(k2Threads, 1) mx_pair_kernel(const __grid_constant__ MxPairParams mp) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kMxOffB;
+  uint8_t* sSf = smem + kMxOffSf;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kMxOffBar);
+  uint64_t* empty_bar = full_bar + kMxStages;
+  uint64_t* acc_full = empty_bar + kMxStages;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  const GroupDesc& d = mp.d;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = (int)cluster_ctarank();
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int T = mp.tiles;
+  const int nkb = (d.K + 127) / 128;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&mp.ta);
+    tma_prefetch_desc(&mp.tb);
+    tma_prefetch_desc(&mp.tsa);
+    tma_prefetch_desc(&mp.tsb);
+    for (int s = 0; s < kMxStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 2 * k2EpiWarps);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_cg2<512>(tmem_slot);
+  pdl_wait();
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===== TMA producer (both CTAs) =====
+    if (lane == 0) {
+      const uint32_t full0 = mapa_shared(smem_u32(full_bar), 0);
+      int it = 0;
+      for (int t = cid; t < T; t += ncl) {
+        const int mb = t / d.tiles_n, nb = t - (t / d.tiles_n) * d.tiles_n;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % kMxStages;
+          const uint32_t ph = (uint32_t)(it / kMxStages) & 1u;
+          mbar_wait(&empty_bar[s], ph ^ 1u, 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[s], 2u * (k2StageA + k2StageB + kMxSf));
+          tma_load_2d_cg2(sA + s * k2StageA, &mp.ta, full0 + 8u * s, kb * 128, mb * 256 + rank * 128);
+          tma_load_2d_cg2(sB + s * k2StageB, &mp.tb, full0 + 8u * s, kb * 128, nb * 256 + rank * 128);
+          // scale atoms: (atom, kb) starts at 256-byte row (atom * kbs + kb) * 2 of the pack
+          uint8_t* sf = sSf + s * kMxSf;
+          tma_load_2d_cg2(sf, &mp.tsa, full0 + 8u * s, 0, ((mb * 2 + rank) * mp.sf_kbs + kb) * 2);
+          tma_load_2d_cg2(sf + 512, &mp.tsb, full0 + 8u * s, 0, ((nb * 2) * mp.sf_kbs + kb) * 2);
+          tma_load_2d_cg2(sf + 1024, &mp.tsb, full0 + 8u * s, 0, ((nb * 2 + 1) * mp.sf_kbs + kb) * 2);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ===== MMA issuer (leader only) =====
+    if (lane == 0 && rank == 0) {
+      int it = 0, j = 0;
+      const uint32_t idesc = idesc_mxf8f6f4(d.a_fmt, d.b_fmt, 256, 256);
+      for (int t = cid; t < T; t += ncl, ++j) {
+        mbar_wait(acc_empty, ((uint32_t)j & 1u) ^ 1u, 4);  // both CTAs drained the accumulator
+        tc_fence_after();
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % kMxStages;
+          const uint32_t ph = (uint32_t)(it / kMxStages) & 1u;
+          mbar_wait(&full_bar[s], ph, 2);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + s * k2StageA);
+          const uint32_t b0 = smem_u32(sB + s * k2StageB);
+          const uint32_t sft = tmem_base + 256u + 12u * (uint32_t)s;
+          const uint32_t sfs = smem_u32(sSf + s * kMxSf);
+          utccp_32x128b_warpx4_cg2(sft, sfs);               // SFA (this CTA's 128 rows)
+          utccp_32x128b_warpx4_cg2(sft + 4u, sfs + 512u);   // SFB columns 0..127
+          utccp_32x128b_warpx4_cg2(sft + 8u, sfs + 1024u);  // SFB columns 128..255
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            mma_mxf8f6f4_cg2(tmem_base, smem_desc_kmajor_sw128(a0 + k * 32), smem_desc_kmajor_sw128(b0 + k * 32),
+                             idesc, sft, sft + 4u, (uint32_t)k, (kb | k) != 0);
+          mma_commit_cg2_mc(&empty_bar[s], 3);
+        }
+        mma_commit_cg2_mc(acc_full, 3);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===== epilogue (both CTAs): warp = TMEM lane quadrant q x column half h =====
+    const int q = warp & 3;
+    const int h = (warp - 2) >> 2;
+    uint8_t* stg = smem + kMxOffOut + (warp - 2) * 8192;
+    float* colb = reinterpret_cast<float*>(smem + kMxOffCol);
+    const uint32_t acc_empty0 = mapa_shared(smem_u32(acc_empty), 0);
+    const int esz = d.out_dtype == LOKA_F32 ? 4 : 2;
+    const int cpb = 128 / esz;
+    int nbox = 0, j = 0;
+    for (int t = cid; t < T; t += ncl, ++j) {
+      const int mb = t / d.tiles_n, nb = t - (t / d.tiles_n) * d.tiles_n;
+      named_bar_sync(2, 32 * k2EpiWarps);  // the previous tile's bias reads are done
+      {
+        const int e = threadIdx.x - 64, n = nb * 256 + e;
+        float b = 0.f;
+        if (n < d.N && d.bias) b = d.bias_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(d.bias)[n])
+                                               : reinterpret_cast<const float*>(d.bias)[n];
+        colb[e] = b;
+      }
+      named_bar_sync(2, 32 * k2EpiWarps);
+      if (lane == 0) mbar_wait(acc_full, (uint32_t)j & 1u, 3);
+      __syncwarp();
+      tc_fence_after();
+      // the whole 128-column half into registers, then the accumulator goes back to the MMA
+      float y[128];
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * 128);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32_nowait(tbase + 32u * c, y + 32 * c);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) tmem_wait16(y + 16 * c);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(acc_empty0);
+      const int row0 = mb * 256 + rank * 128 + q * 32;
+      const int col0 = nb * 256 + h * 128;
+#pragma unroll
+      for (int cb = 0; cb < 128; cb += 32) {
+        float* yc = y + cb;
+        if (d.bias) {
+          const uint32_t cs = smem_u32(colb + h * 128 + cb);
+#pragma unroll
+          for (int c = 0; c < 32; c += 4) {
+            const float4 b4 = lds_f4(cs + 4u * c);
+            const float2 a = fadd2(make_float2(yc[c], yc[c + 1]), make_float2(b4.x, b4.y));
+            const float2 b = fadd2(make_float2(yc[c + 2], yc[c + 3]), make_float2(b4.z, b4.w));
+            yc[c] = a.x; yc[c + 1] = a.y; yc[c + 2] = b.x; yc[c + 3] = b.y;
+          }
+        }
+        const int in_box = cb % cpb;
+        uint8_t* box = stg + (nbox & 1) * 4096;
+        if (in_box == 0) {
+          if (lane == 0) bulk_wait_read_le1();
+          __syncwarp();
+        }
+        const uint32_t rowa = smem_u32(box) + (uint32_t)lane * 128u;
+        if (esz == 4) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            sts_u4(rowa + ((((uint32_t)k) ^ ((uint32_t)lane & 7u)) << 4),
+                   make_uint4(__float_as_uint(yc[4 * k]), __float_as_uint(yc[4 * k + 1]),
+                              __float_as_uint(yc[4 * k + 2]), __float_as_uint(yc[4 * k + 3])));
+        } else {
+          const uint32_t p0 = (uint32_t)(in_box * 2) >> 4;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            uint32_t w[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              __nv_bfloat162 hh = __floats2bfloat162_rn(yc[8 * k + 2 * i], yc[8 * k + 2 * i + 1]);
+              w[i] = *reinterpret_cast<uint32_t*>(&hh);
+            }
+            sts_u4(rowa + (((p0 + (uint32_t)k) ^ ((uint32_t)lane & 7u)) << 4), make_uint4(w[0], w[1], w[2], w[3]));
+          }
+        }
+        if (in_box + 32 == cpb) {
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const int c0 = col0 + cb + 32 - cpb;
+            if (c0 < d.N && row0 < d.M) tma_store_2d(&mp.ty, box, c0, row0);
+            bulk_commit();
+          }
+          ++nbox;
+        }
+      }
+    }
+    if (lane == 0) bulk_wait0();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_cg2<512>(tmem_base);
+  }
+}
+
+cudaError_t launch_mx_pair(const MxPairParams& mp, int num_sms, cudaStream_t st) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(mx_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMxSmem);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  const int pairs = mp.tiles < num_sms / 2 ? mp.tiles : num_sms / 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * pairs), 1, 1);
+  cfg.blockDim = dim3(k2Threads, 1, 1);
+  cfg.dynamicSmemBytes = kMxSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, mx_pair_kernel, mp);
+  note_launch();
+  return e;
+}
+
 // ---- split-K reduction: y = (sum over slices) * s_a[m] * s_b[n] (+ bias[n]), fixed slice order ----
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const GroupDesc d, const float* __restrict__ part,
                                                             void* y, int64_t ldy) {

@@ -158,6 +158,17 @@ cudaError_t launch_grouped(const GroupedParams& gp, int num_sms, cudaStream_t st
 // CTA-pair variant (gemm2.cu): tiles 256 x 256 (tiles_n = ceil(N/256), tile_start counts them);
 // ta/tb boxes {128, 128}; ty box {128 bytes, 32 rows}, SW128; bf16 / f32 output.
 cudaError_t launch_grouped2(const GroupedParams& gp, int num_sms, cudaStream_t st);
+// Native block-scaled (UE8M0 blockwise, MX) problem on the CTA pair (gemm2.cu): 256 x 256 tiles,
+// kind::mxf8f6f4.block_scale with cta_group::2; scale atoms TMA-loaded from the sfpack layout
+// viewed as rows of 256 B (maps tsa / tsb, box {256, 2} = one 512 B atom).  Plain epilogue
+// (+ bias), bf16 / f32 output.
+struct MxPairParams {
+  CUtensorMap ta, tb, ty, tsa, tsb;
+  GroupDesc d;     // sa / sb unused (the MMA applies the scales)
+  int32_t sf_kbs;  // 128-K blocks (atoms per operand row block)
+  int32_t tiles;
+};
+cudaError_t launch_mx_pair(const MxPairParams& mp, int num_sms, cudaStream_t st);
 // y[m,n] = (sum_s part[s][m][n]) * s_a[m] * s_b[n] (+ bias[n]) -> y (bf16 / f32)
 cudaError_t launch_splitk_reduce(const GroupDesc& d, const float* part, void* y, int64_t ldy, cudaStream_t st);
 

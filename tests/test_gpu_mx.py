@@ -152,3 +152,38 @@ def test_mx_workspace_required_and_grouped():
                                    wrs.cpu().numpy(), "e4m3", "row")
     rms = np.sqrt(np.mean(yr ** 2, axis=1, keepdims=True))
     assert np.all(np.abs(f64(y3) - yr) <= TOL * np.maximum(np.abs(yr), rms) + 2.0 ** -8 * np.abs(yr))
+
+
+def test_mx_pair_engine_exact_block_scales():
+    """>= 74 tiles of 256 x 256: the CTA-pair block-scaled kernel (cta_group::2, scale atoms copied
+    to both CTAs' TMEM).  Integer blocks x per-block powers of two -> exact in FP32; a ragged last
+    row tile (rows past M) and several tiles per pair."""
+    g = torch.Generator().manual_seed(11)
+    M, N, K = 2176, 2560, 384
+    xi = torch.randint(-8, 9, (M, K), generator=g).float()
+    wi = torch.randint(-8, 9, (N, K), generator=g).float()
+    ea = torch.randint(-1, 2, (M, K // 128), generator=g).float()
+    eb = torch.randint(-1, 2, (N // 128, K // 128), generator=g).float()
+    xv = xi * torch.repeat_interleave(2.0 ** ea, 128, dim=1)
+    wv = wi * torch.repeat_interleave(torch.repeat_interleave(2.0 ** eb, 128, dim=0), 128, dim=1)
+    xq, xs = lk.loka_quantize(xv.to(DEV), "e4m3", "blk_1x128", "ue8m0")
+    wq, ws = lk.loka_quantize(wv.to(DEV), "e4m3", "blk_128x128", "ue8m0")
+    y, _ = _mx(xq, xs, wq, ws, out_dtype="f32")
+    torch.cuda.synchronize()
+    assert np.array_equal(f64(y), xv.double().numpy() @ wv.double().numpy().T)
+
+
+@pytest.mark.parametrize("b_gran,a_fmt,od", [("blk_128x128", "e4m3", "bf16"), ("blk_1x128", "e5m2", "f32")])
+def test_mx_pair_engine_vs_oracle(b_gran, a_fmt, od):
+    M, N, K = 2048, 2816, 1000
+    xq, xs, wq, ws = _operands(M, N, K, 17, a_fmt=a_fmt, b_gran=b_gran)
+    bias = torch.randn(N, generator=torch.Generator().manual_seed(4))
+    y, _ = _mx(xq, xs, wq, ws, a_fmt=a_fmt, b_gran=b_gran, bias=bias.to(DEV), out_dtype=od)
+    torch.cuda.synchronize()
+    rows = np.sort(np.random.default_rng(2).choice(M, 64, replace=False))
+    yo = oracle.linear.linear_norm(xq.cpu().numpy()[rows], xs.cpu().numpy()[rows], a_fmt, "blk_1x128",
+                                   wq.cpu().numpy(), ws.cpu().numpy(), "e4m3", b_gran, bias=bias.double().numpy())
+    yg = f64(y)[rows]
+    rms = np.sqrt(np.mean(yo ** 2, axis=1, keepdims=True))
+    extra = 2.0 ** -8 * np.abs(yo) if od == "bf16" else 0.0
+    assert np.all(np.abs(yg - yo) <= TOL * np.maximum(np.abs(yo), rms) + extra)
