@@ -167,9 +167,10 @@ typedef struct loka_linear_args {
                                FP8 output's row amax is then taken over the activated values  */
 } loka_linear_args;
 
-/* Y = epilogue(A . B^T): acc(FP32, TMEM) -> y = acc*sa[m]*sb[n] (+bias[n]) -> norm -> cast.
- * Full-row norms (LAYER, RMS, FP8 output with ROW scales) need N <= 2048 (one thread-block
- * cluster of <= 8 CTAs spans the row); BLOCK_RMS and NONE take any N.  K % 16 == 0.          */
+/* Y = epilogue(A . B^T): acc(FP32, TMEM) -> y = acc*sa[m]*sb[n] (+bias[n]) -> norm -> act -> cast.
+ * Full-row norms (LAYER, RMS, FP8 output with ROW scales) need N <= 4096 (one thread-block
+ * cluster spans the row: <= 8 CTAs, or 16 CTAs of 256 columns via the non-portable cluster
+ * size for N > 2048); BLOCK_RMS and NONE take any N.  K % 16 == 0.                          */
 LOKA_API loka_status loka_fp8_linear_norm(const loka_linear_args* args, void* ws, size_t ws_bytes,
                                  loka_stream_t stream);
 LOKA_API size_t loka_linear_workspace_size(const loka_linear_args* args);

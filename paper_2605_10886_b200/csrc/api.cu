@@ -346,7 +346,8 @@ static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CU
   // (blk % (BN/4) == 0, each thread's BN/4 columns lie in one block)
   auto legal = [&](int c) {
     if (mx && c < 128) return false;  // MX scale atoms cover 128 rows of B
-    if (full_row && cdiv(N, c) > 8) return false;
+    // a full row spans one cluster: <= 8 CTAs (portable), or 16 of BN = 256 (opt-in, N <= 4096)
+    if (full_row && cdiv(N, c) > 8 && !(c == 256 && !mx && cdiv(N, c) <= 16)) return false;
     if (block && (c % blk || blk % (c / 4))) return false;
     return true;
   };

@@ -47,11 +47,12 @@ constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kThreads = kEpiThreads;       // ... after warp 0 lane 0 (TMA) / warp 1 lane 0 (MMA) roles
 constexpr int kBK = 128;                    // FP8 elements of K per stage (128 B rows, SW128 atom)
 constexpr int kRec = 6;                     // floats per (row, quarter) record: n, mean, m2, ss, ymax, ymin
-constexpr int kMaxCluster = 8;
+constexpr int kMaxCluster = 8;   // portable cluster size
+constexpr int kBigCluster = 16;  // non-portable (opt-in): rows up to 16 x 256 = 4096 columns
 
 constexpr uint32_t pow2_cols(uint32_t c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
 
-template <int BN, bool MX = false> struct LinCfg {
+template <int BN, bool MX = false, int MAXC = kMaxCluster> struct LinCfg {
   static constexpr int kCPT = BN / 4;  // columns per epilogue thread
   static constexpr int kStageA = 128 * kBK;  // bytes
   static constexpr int kStageB = BN * kBK;
@@ -61,7 +62,7 @@ template <int BN, bool MX = false> struct LinCfg {
   static constexpr int kSf = MX ? 512 * (1 + BN / 128) : 0;
   static constexpr int kSfCols = 4 * (1 + BN / 128);
   // everything but the operand ring: column params, pushed cluster records (+ amax), barriers
-  static constexpr int kFixed = 4 * BN * 4 + kMaxCluster * 128 * 16 + kMaxCluster * 128 * 4 + 512 + 1024;
+  static constexpr int kFixed = 4 * BN * 4 + MAXC * 128 * 16 + MAXC * 128 * 4 + 512 + 1024;
   static constexpr int kStagesFit = (227 * 1024 - kFixed) / (kStageBytes + kSf);
   static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
   static constexpr uint32_t kTmemCols = pow2_cols(MX ? BN + kStages * kSfCols : BN);
@@ -69,9 +70,9 @@ template <int BN, bool MX = false> struct LinCfg {
   static constexpr int kOffBar = kOffB + kStages * kStageB;
   static constexpr int kOffTmem = kOffBar + (2 * kStages + 1) * 8;
   static constexpr int kOffCol = (kOffTmem + 4 + 15) & ~15;         // sb, bias, gamma, beta [BN]
-  static constexpr int kOffCs = kOffCol + 4 * BN * 4;                // [kMaxCluster][128] float4 records
-  static constexpr int kOffCs2 = kOffCs + kMaxCluster * 128 * 16;    // [kMaxCluster][128] amax
-  static constexpr int kOffSf = kOffCs2 + kMaxCluster * 128 * 4;         // [kStages][kSf] (MX)
+  static constexpr int kOffCs = kOffCol + 4 * BN * 4;                // [MAXC][128] float4 records
+  static constexpr int kOffCs2 = kOffCs + MAXC * 128 * 16;           // [MAXC][128] amax
+  static constexpr int kOffSf = kOffCs2 + MAXC * 128 * 4;            // [kStages][kSf] (MX)
   static constexpr int kSmemBytes = kOffSf + kStages * kSf + 1024;       // + alignment slack
   // after the mainloop the (drained) operand ring holds the quarter exchange [4][kRec + 1][128]
   // floats at offset 0 and the output staging tile (128 rows x BN x <= 4 bytes) at kOffStage
@@ -117,11 +118,11 @@ LOKA_DEVINL RowRec merge_recs(const RowRec (&r)[K]) {
   return o;
 }
 
-template <int BN, bool MX>
+template <int BN, bool MX, int MAXC>
 __global__ void __launch_bounds__(kThreads, 1)
     linear_norm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                        const __grid_constant__ CUtensorMap tma_y, const LinearParams p) {
-  using C = LinCfg<BN, MX>;
+  using C = LinCfg<BN, MX, MAXC>;
   constexpr int CPT = C::kCPT;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -395,22 +396,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int rk = 0; rk < csize; ++rk) st_dsmem_f4(mapa_shared(la, (uint32_t)rk), v);
       }
       cluster_sync_all();
-      RowRec parts[kMaxCluster];  // ranks >= csize stay empty (n = 0) and merge as no-ops
-#pragma unroll
-      for (int rk = 0; rk < kMaxCluster; ++rk) {
-        RowRec& o = parts[rk];
-        o.init();
-        if (rk < csize) {
-          const float4 v = lds_f4(smem_u32(cs + ((size_t)rk * 128 + r) * 4));
-          o.n = (float)min(BN, p.N - rk * BN);
-          o.mean = norm == LOKA_NORM_LAYER ? v.x : 0.f;
-          o.m2 = v.y;
-          o.ss = norm == LOKA_NORM_LAYER ? 0.f : v.x;
-          o.ymax = v.z;
-          o.ymin = v.w;
-        }
+      // n-way merge in rank order straight from the pushed records (two passes over smem: the
+      // same sums as merge_recs over the ranks, without a register array per rank)
+      RowRec o;
+      o.init();
+      float sm = 0.f;
+      for (int rk = 0; rk < csize; ++rk) {
+        const float4 v = lds_f4(smem_u32(cs + ((size_t)rk * 128 + r) * 4));
+        const float nk = (float)min(BN, p.N - rk * BN);
+        o.n += nk;
+        sm = fmaf(nk, norm == LOKA_NORM_LAYER ? v.x : 0.f, sm);
+        o.ss += norm == LOKA_NORM_LAYER ? 0.f : v.x;
+        o.ymax = fmaxf(o.ymax, v.z);
+        o.ymin = fminf(o.ymin, v.w);
       }
-      rec = merge_recs(parts);
+      o.mean = o.n > 0.f ? __fdiv_rn(sm, o.n) : 0.f;
+      float m2 = 0.f;
+      for (int rk = 0; rk < csize; ++rk) {
+        const float4 v = lds_f4(smem_u32(cs + ((size_t)rk * 128 + r) * 4));
+        const float nk = (float)min(BN, p.N - rk * BN);
+        const float dk = (norm == LOKA_NORM_LAYER ? v.x : 0.f) - o.mean;
+        m2 += v.y + nk * dk * dk;
+      }
+      o.m2 = m2;
+      rec = o;
     }
     if (threadIdx.x == 64) LOKA_TRACE(10);
 
@@ -627,13 +636,18 @@ long long debug_trace(int enable, unsigned long long* out, long long n) {
   return got;
 }
 
-template <int BN, bool MX>
+template <int BN, bool MX, int MAXC = kMaxCluster>
 static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, const LinearParams& p,
                              cudaStream_t st) {
-  using C = LinCfg<BN, MX>;
+  using C = LinCfg<BN, MX, MAXC>;
   static bool attr_done = false;  // idempotent; racing threads set the same value
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(linear_norm_kernel<BN, MX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (MAXC > 8) {
+      cudaError_t e = cudaFuncSetAttribute(linear_norm_kernel<BN, MX, MAXC>,
+                                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = cudaFuncSetAttribute(linear_norm_kernel<BN, MX, MAXC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr_done = true;
@@ -652,13 +666,17 @@ static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, linear_norm_kernel<BN, MX>, ta, tb, ty, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, linear_norm_kernel<BN, MX, MAXC>, ta, tb, ty, p);
   note_launch();
   return e;
 }
 
 cudaError_t launch_linear(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, const LinearParams& p,
                           int bn, cudaStream_t st) {
+  if (p.cluster_n > kMaxCluster) {  // rows of 2304..4096 columns: 16-CTA cluster, BN = 256
+    if (bn != 256 || p.mx || p.cluster_n > kBigCluster) return cudaErrorInvalidValue;
+    return launch_bn<256, false, kBigCluster>(ta, tb, ty, p, st);
+  }
   if (p.mx) {
     switch (bn) {
       case 128: return launch_bn<128, true>(ta, tb, ty, p, st);

@@ -202,3 +202,23 @@ def test_hardswish_with_gamma_beta_bf16():
     pre = _oracle(xq, xs, wq, ws, norm="layer", gamma=gamma.double().numpy(), beta=beta.double().numpy())
     rms = np.sqrt(np.mean(pre ** 2, axis=1, keepdims=True))
     assert np.all(np.abs(f64(y) - yo) <= 1.5 * TOL * np.maximum(np.abs(pre), rms) + 2.0 ** -8 * np.abs(yo))
+
+
+@pytest.mark.parametrize("N,norm,od", [(4096, "layer", "f32"), (3000, "rms", "f32"), (4096, "layer", "e4m3"),
+                                       (2560, "none", "e4m3")])
+def test_full_row_norm_wide_rows_16_cta_cluster(N, norm, od):
+    """BJ configs[4] (cfg5) layer: LayerNorm over N = 4096 needs a 16-CTA (non-portable) cluster."""
+    M, K = 300, 384
+    xq, xs, wq, ws = _operands(M, N, K, 41, xdist="heavy")
+    if od == "f32":
+        y, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm=norm, out_dtype="f32")
+        torch.cuda.synchronize()
+        assert guarded_rel_err(f64(y), _oracle(xq, xs, wq, ws, norm=norm)) <= TOL
+    else:
+        pre = torch.empty(M, N, dtype=torch.float32, device=DEV)
+        y, ys = lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm=norm, out_dtype="e4m3", precast=pre)
+        torch.cuda.synchronize()
+        oq, os_ = oracle.quantize.quantize(f64(pre), "e4m3", "row")
+        assert_scales_equal(ys, os_)
+        assert_bytes_equal(y, oq)
+        assert guarded_rel_err(f64(pre), _oracle(xq, xs, wq, ws, norm=norm)) <= TOL
