@@ -286,7 +286,9 @@ static size_t mx_ws_bytes(const loka_linear_args* a) {
 }
 static bool pair_eligible(const loka_linear_args* a);
 static size_t split_ws_bytes(const loka_linear_args* a);
+static bool wide_norm_unfused(const loka_linear_args* a);
 size_t loka_linear_workspace_size(const loka_linear_args* a) {
+  if (wide_norm_unfused(a)) return (size_t)a->M * (size_t)a->N * 4;
   return mx_ws_bytes(a) + (pair_eligible(a) ? split_ws_bytes(a) : 0);
 }
 
@@ -557,8 +559,63 @@ static loka_status run_mx_pair(const loka_linear_args* a, void* ws, size_t ws_by
   return launch_mx_pair(mp, sms, s) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
 }
 
+// Full-row norms over rows wider than a portable cluster (N > 2048): when the CTA-pair engine has
+// enough tiles, GEMM (FP32 out, workspace) + one row-wise norm pass beats the 16-CTA-cluster fused
+// epilogue ("cross-block synchronization ... negates most of the performance gains";
+// measured).  Tensorwise / rowwise scales only.
+static bool wide_norm_unfused(const loka_linear_args* a) {
+  if (!a || !use_pair_kernel() || (a->norm != LOKA_NORM_LAYER && a->norm != LOKA_NORM_RMS)) return false;
+  if (a->N <= 2048 || a->N > 4096 || a->N % 8 || a->M <= 0 || a->K <= 0) return false;
+  if (a->a.gran != LOKA_GRAN_TENSOR && a->a.gran != LOKA_GRAN_ROW) return false;
+  if (a->b.gran != LOKA_GRAN_TENSOR && a->b.gran != LOKA_GRAN_ROW) return false;
+  return cdiv(a->M, 256) * cdiv(a->N, 256) >= 74;
+}
+static loka_status run_wide_norm(const loka_linear_args* a, void* ws, size_t ws_bytes, cudaStream_t s) {
+  const size_t need = (size_t)a->M * (size_t)a->N * 4;
+  if (!ws || ws_bytes < need || !aligned16(ws)) return LOKA_ERR_WORKSPACE;
+  if (a->y.ld < a->N || (a->y.ld * elem_size(a->y.dtype)) % 16 || !a->y.data) return LOKA_ERR_INVALID_ARG;
+  if (is_fp8(a->y.dtype) && (!a->y.scales || a->y.gran != LOKA_GRAN_ROW)) return LOKA_ERR_INVALID_ARG;
+  if (a->beta && a->norm != LOKA_NORM_LAYER) return LOKA_ERR_INVALID_ARG;
+  if (a->act != LOKA_ACT_NONE && a->act != LOKA_ACT_HARDSWISH) return LOKA_ERR_INVALID_ARG;
+  loka_linear_args g = *a;  // the GEMM: plain epilogue, FP32 into the workspace
+  g.norm = LOKA_NORM_NONE;
+  g.act = LOKA_ACT_NONE;
+  g.gamma = nullptr;
+  g.beta = nullptr;
+  g.debug_precast = nullptr;
+  g.y.data = ws;
+  g.y.dtype = LOKA_F32;
+  g.y.ld = a->N;
+  g.y.scales = nullptr;
+  loka_status st = loka_grouped_fp8_linear(1, &g, nullptr, 0, reinterpret_cast<loka_stream_t>(s));
+  if (st != LOKA_OK) return st;
+  int sms = 148;
+  st = check_device(&sms);
+  if (st != LOKA_OK) return st;
+  RowNormParams rp;
+  std::memset(&rp, 0, sizeof(rp));
+  rp.y32 = static_cast<const float*>(ws);
+  rp.ld32 = a->N;
+  rp.M = a->M;
+  rp.N = a->N;
+  rp.norm = a->norm;
+  rp.act = a->act;
+  rp.out_dtype = a->y.dtype;
+  rp.eps = a->eps > 0.f ? a->eps : (a->norm == LOKA_NORM_LAYER ? 1e-5f : 1e-6f);
+  rp.gamma = a->gamma;
+  rp.beta = a->beta;
+  rp.y = a->y.data;
+  rp.ldy = a->y.ld;
+  rp.y_scales = is_fp8(a->y.dtype) ? a->y.scales : nullptr;
+  rp.precast = a->debug_precast;
+  rp.ld_pre = a->N;
+  rp.status = a->status_dev;
+  return launch_rownorm(rp, sms, s) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
+}
+
 loka_status loka_fp8_linear_norm(const loka_linear_args* a, void* ws, size_t ws_bytes, loka_stream_t stream) {
   if (is_blockwise(a)) return run_bw(a, reinterpret_cast<cudaStream_t>(stream));
+  if (wide_norm_unfused(a)) return run_wide_norm(a, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
   if (mx_pair_ok(a)) {
     if (!ws || ws_bytes < mx_ws_bytes(a) || !aligned16(ws)) return LOKA_ERR_WORKSPACE;
     int sms = 148;

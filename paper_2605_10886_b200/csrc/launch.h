@@ -169,6 +169,19 @@ struct MxPairParams {
   int32_t tiles;
 };
 cudaError_t launch_mx_pair(const MxPairParams& mp, int num_sms, cudaStream_t st);
+// Row-wise norm / act / cast over an FP32 GEMM output (rownorm.cu; the unfused form for wide rows)
+struct RowNormParams {
+  const float* y32; int64_t ld32;
+  int64_t M, N;
+  int32_t norm, act, out_dtype;
+  float eps;
+  const float* gamma; const float* beta;
+  void* y; int64_t ldy;
+  float* y_scales;
+  float* precast; int64_t ld_pre;
+  int32_t* status;
+};
+cudaError_t launch_rownorm(const RowNormParams& p, int num_sms, cudaStream_t st);
 // y[m,n] = (sum_s part[s][m][n]) * s_a[m] * s_b[n] (+ bias[n]) -> y (bf16 / f32)
 cudaError_t launch_splitk_reduce(const GroupDesc& d, const float* part, void* y, int64_t ldy, cudaStream_t st);
 

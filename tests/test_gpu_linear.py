@@ -222,3 +222,36 @@ def test_full_row_norm_wide_rows_16_cta_cluster(N, norm, od):
         assert_scales_equal(ys, os_)
         assert_bytes_equal(y, oq)
         assert guarded_rel_err(f64(pre), _oracle(xq, xs, wq, ws, norm=norm)) <= TOL
+
+
+@pytest.mark.parametrize("norm,od,act,affine", [("layer", "f32", "none", False), ("rms", "bf16", "hardswish", True),
+                                                ("layer", "e4m3", "hardswish", False)])
+def test_wide_rows_unfused_pair_plus_rownorm(norm, od, act, affine):
+    """N > 2048 with enough rows: CTA-pair GEMM (FP32, workspace) + the row-wise norm pass
+    (rownorm.cu).  Sampled rows vs the oracle; FP8 codes bit-exact vs the GPU's pre-cast values."""
+    M, N, K = 1300, 4096, 512
+    xq, xs, wq, ws = _operands(M, N, K, 43, xdist="heavy")
+    g = torch.Generator().manual_seed(3)
+    gamma = (1 + 0.2 * torch.randn(N, generator=g)).float() if affine else None
+    pre = torch.empty(M, N, dtype=torch.float32, device=DEV)
+    y, ys = lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm=norm, act=act, out_dtype=od, precast=pre,
+                                   gamma=None if gamma is None else gamma.to(DEV))
+    torch.cuda.synchronize()
+    rows = np.sort(np.random.default_rng(5).choice(M, 48, replace=False))
+    kw = dict(norm=norm, act=act, gamma=None if gamma is None else gamma.double().numpy())
+    yo = oracle.linear.linear_norm(xq.cpu().numpy()[rows], xs.cpu().numpy()[rows], "e4m3", "row", wq.cpu().numpy(),
+                                   ws.cpu().numpy(), "e4m3", "row", **kw)
+    kw0 = dict(kw, act="none")
+    base = oracle.linear.linear_norm(xq.cpu().numpy()[rows], xs.cpu().numpy()[rows], "e4m3", "row",
+                                     wq.cpu().numpy(), ws.cpu().numpy(), "e4m3", "row", **kw0)
+    rms = np.sqrt(np.mean(base ** 2, axis=1, keepdims=True))
+    guard = np.maximum(np.abs(base), rms)
+    assert np.max(np.abs(f64(pre)[rows] - yo) / guard) <= 1.5 * TOL
+    if od == "e4m3":
+        oq, os_ = oracle.quantize.quantize(f64(pre), "e4m3", "row")
+        assert_scales_equal(ys, os_)
+        assert_bytes_equal(y, oq)
+    elif od == "bf16":
+        assert np.all(np.abs(f64(y)[rows] - yo) <= 1.5 * TOL * guard + 2.0 ** -8 * np.abs(yo))
+    else:
+        assert np.max(np.abs(f64(y)[rows] - yo) / guard) <= 1.5 * TOL
