@@ -129,6 +129,65 @@ def linear_norm(a_codes, a_scales, a_fmt, a_gran, b_codes, b_scales, b_fmt, b_gr
     return apply_act(apply_norm(y, norm, eps, gamma, beta, block), act)
 
 
+def norm_stats(y, norm="layer", eps=None, block=256):
+    """The forward quantities the backward needs: xhat (normalised, before gamma/beta/act) and rstd
+    (per row; BlockNorm: per row and block, [M, N/block])."""
+    y = np.asarray(y, np.float64)
+    if norm == "layer":
+        eps = 1e-5 if eps is None else eps
+        mu = y.mean(axis=1, keepdims=True)
+        rstd = 1.0 / np.sqrt(((y - mu) ** 2).mean(axis=1, keepdims=True) + eps)
+        return (y - mu) * rstd, rstd[:, 0]
+    if norm == "rms":
+        eps = 1e-6 if eps is None else eps
+        rstd = 1.0 / np.sqrt((y ** 2).mean(axis=1, keepdims=True) + eps)
+        return y * rstd, rstd[:, 0]
+    if norm == "block_rms":
+        eps = 1e-6 if eps is None else eps
+        m, n = y.shape
+        yb = y.reshape(m, n // block, block)
+        rstd = 1.0 / np.sqrt((yb ** 2).mean(axis=2) + eps)
+        return (yb * rstd[:, :, None]).reshape(m, n), rstd
+    raise ValueError(norm)
+
+
+def hard_swish_grad(x):
+    """d h-swish / dx = 0 (x < -3), (2x + 3)/6 (-3 <= x <= 3), 1 (x > 3) (PyTorch's convention at
+    the kinks)."""
+    x = np.asarray(x, np.float64)
+    return np.where(x < -3.0, 0.0, np.where(x <= 3.0, (2.0 * x + 3.0) / 6.0, 1.0))
+
+
+def norm_backward(dh, xhat, rstd, norm="layer", gamma=None, beta=None, act="none", block=256):
+    """NEXT-1: gradient wrt the norm's input z of h = act(xhat*gamma + beta),
+    given dh = dL/dh and the saved xhat, rstd (norm_stats).  With g = dh * act'(y_pre) * gamma:
+      LayerNorm (xhat = (z - mu) rstd):  dz = rstd (g - mean(g) - xhat mean(g xhat))
+      RMSNorm   (xhat = z rstd):         dz = rstd (g - xhat mean(g xhat))
+      BlockNorm: RMSNorm's formula per block (rstd [M, N/block])."""
+    dh = np.asarray(dh, np.float64)
+    xhat = np.asarray(xhat, np.float64)
+    g = dh
+    gam = np.ones(xhat.shape[1]) if gamma is None else np.asarray(gamma, np.float64)
+    if act == "hardswish":
+        ypre = xhat * gam[None, :] + (0.0 if beta is None else np.asarray(beta, np.float64)[None, :])
+        g = g * hard_swish_grad(ypre)
+    elif act != "none":
+        raise ValueError(act)
+    g = g * gam[None, :]
+    if norm == "layer":
+        r = np.asarray(rstd, np.float64)[:, None]
+        return r * (g - g.mean(axis=1, keepdims=True) - xhat * (g * xhat).mean(axis=1, keepdims=True))
+    if norm == "rms":
+        r = np.asarray(rstd, np.float64)[:, None]
+        return r * (g - xhat * (g * xhat).mean(axis=1, keepdims=True))
+    if norm == "block_rms":
+        m, n = xhat.shape
+        gb, xb = g.reshape(m, n // block, block), xhat.reshape(m, n // block, block)
+        r = np.asarray(rstd, np.float64).reshape(m, n // block, 1)
+        return (r * (gb - xb * (gb * xb).mean(axis=2, keepdims=True))).reshape(m, n)
+    raise ValueError(norm)
+
+
 def round_bf16(v) -> np.ndarray:
     """O10: round float64 values to the nearest bf16 value, ties to even (8 significant
     bits; bf16 subnormal spacing 2^-133).  |v| = f 2^p with f in [0.5, 1) -> the bf16

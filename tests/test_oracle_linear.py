@@ -132,3 +132,49 @@ def test_linear_norm_act_is_applied_after_the_norm():
     assert np.array_equal(act, L.hard_swish(base))
     assert np.array_equal(L.linear_norm(a, sa, "e4m3", "row", b, sb, "e4m3", "row", act="hardswish"),
                           L.hard_swish(L.linear_norm(a, sa, "e4m3", "row", b, sb, "e4m3", "row")))
+
+
+@pytest.mark.parametrize("norm,act,affine", [("layer", "none", False), ("layer", "hardswish", True),
+                                             ("rms", "none", True), ("rms", "hardswish", False),
+                                             ("block_rms", "none", False), ("block_rms", "hardswish", False)])
+def test_norm_backward_vs_torch_autograd_float64(norm, act, affine):
+    """NEXT-1 norm backward (oracle.linear.norm_backward) against torch autograd in float64 of the
+    forward definitions (F.layer_norm / F.rms_norm / grouped rms_norm, F.hardswish)."""
+    rng = np.random.default_rng(11)
+    M, N = 5, 512
+    z = rng.normal(0.3, 2.0, (M, N))
+    dh = rng.normal(size=(M, N))
+    gamma = 1 + 0.2 * rng.normal(size=N) if affine else None
+    beta = 0.3 * rng.normal(size=N) if (affine and norm == "layer") else None
+    zt = torch.tensor(z, requires_grad=True)
+    if norm == "layer":
+        y = F.layer_norm(zt, (N,), weight=None if gamma is None else torch.tensor(gamma),
+                         bias=None if beta is None else torch.tensor(beta), eps=1e-5)
+    elif norm == "rms":
+        y = F.rms_norm(zt, (N,), weight=None if gamma is None else torch.tensor(gamma), eps=1e-6)
+    else:
+        y = F.rms_norm(zt.view(M, N // 256, 256), (256,), eps=1e-6).view(M, N)
+    if act == "hardswish":
+        y = F.hardswish(y)
+    y.backward(torch.tensor(dh))
+    xhat, rstd = L.norm_stats(z, norm)
+    dz = L.norm_backward(dh, xhat, rstd, norm, gamma=gamma, beta=beta, act=act)
+    assert np.allclose(dz, zt.grad.numpy(), rtol=1e-11, atol=1e-12)
+
+
+def test_norm_backward_finite_differences():
+    """Independent of torch: central differences of L = sum(dh * hswish(LayerNorm(z)))."""
+    rng = np.random.default_rng(2)
+    z = rng.normal(size=(2, 16))
+    dh = rng.normal(size=(2, 16))
+
+    def loss(zz):
+        return float((dh * L.hard_swish(L.layer_norm(zz))).sum())
+    xhat, rstd = L.norm_stats(z, "layer")
+    dz = L.norm_backward(dh, xhat, rstd, "layer", act="hardswish")
+    h = 1e-6
+    for i, j in [(0, 0), (1, 7), (0, 15)]:
+        e = np.zeros_like(z)
+        e[i, j] = h
+        fd = (loss(z + e) - loss(z - e)) / (2 * h)
+        assert abs(fd - dz[i, j]) < 1e-6
