@@ -165,6 +165,21 @@ typedef struct loka_linear_args {
   int32_t* status_dev;      /* nullable                                                       */
   loka_act act;             /* applied after the norm (and gamma/beta); NONE by default.  The
                                FP8 output's row amax is then taken over the activated values  */
+  /* NEXT-1 norm backward fused into the (dgrad) GEMM epilogue: when bwd_xhat is
+     set, A.B^T (dequantized) is dL/dh for a forward h = act(norm(z)*gamma + beta) with this args'
+     norm / norm_block / gamma / beta / act, and y receives dL/dz:
+       g = dh * act'(xhat*gamma + beta) * gamma,
+       LAYER: dz = rstd (g - mean(g) - xhat mean(g xhat));  RMS: dz = rstd (g - xhat mean(g xhat));
+       BLOCK_RMS: RMS per block.  bwd_xhat: the forward's normalised values (bf16 [M, N], ld
+       bwd_xhat_ld, ld*2 % 16 == 0); bwd_rstd: [M] (LAYER/RMS) or [M, N/norm_block].  No bias;
+       the fused-epilogue row limits of the forward apply (N <= 4096 for LAYER/RMS).               */
+  const void* bwd_xhat;
+  int64_t bwd_xhat_ld;
+  const float* bwd_rstd;
+  /* forward saves for that backward (nullable): xhat (bf16, ld save_xhat_ld) and rstd of z        */
+  void* save_xhat;
+  int64_t save_xhat_ld;
+  float* save_rstd;
 } loka_linear_args;
 
 /* Y = epilogue(A . B^T): acc(FP32, TMEM) -> y = acc*sa[m]*sb[n] (+bias[n]) -> norm -> act -> cast.

@@ -336,6 +336,15 @@ static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CU
   if (a->beta && a->norm != LOKA_NORM_LAYER) return LOKA_ERR_INVALID_ARG;
   if (a->gamma && a->norm != LOKA_NORM_LAYER && a->norm != LOKA_NORM_RMS) return LOKA_ERR_INVALID_ARG;
   if (a->act != LOKA_ACT_NONE && a->act != LOKA_ACT_HARDSWISH) return LOKA_ERR_INVALID_ARG;
+  const bool bwd = a->bwd_xhat != nullptr;
+  if (bwd) {  // NEXT-1 norm backward epilogue
+    if (a->norm == LOKA_NORM_NONE || a->bias || !a->bwd_rstd || (a->bwd_xhat_ld * 2) % 16 || a->bwd_xhat_ld < N ||
+        !aligned16(a->bwd_xhat) || a->save_xhat || a->save_rstd)
+      return LOKA_ERR_INVALID_ARG;
+  }
+  if (a->save_xhat && ((a->save_xhat_ld * 2) % 16 || a->save_xhat_ld < N || !aligned16(a->save_xhat)))
+    return LOKA_ERR_INVALID_ARG;
+  if ((a->save_xhat || a->save_rstd) && a->norm == LOKA_NORM_NONE) return LOKA_ERR_INVALID_ARG;
 
   // Tile width BN in {64,128,256}: the widest tile that still gives >= ~120 CTAs (most of the
   // 148 SMs) for this M, else the narrowest allowed.  Row-coupled epilogues (full-row norm or an
@@ -397,6 +406,13 @@ static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CU
   p->cluster_n = csize;
   p->act = a->act;
   p->mx = mx ? 1 : 0;
+  p->bwd = bwd ? 1 : 0;
+  p->xhat = static_cast<const __nv_bfloat16*>(a->bwd_xhat);
+  p->ld_xhat = a->bwd_xhat_ld;
+  p->rstd_in = a->bwd_rstd;
+  p->save_xhat = static_cast<__nv_bfloat16*>(a->save_xhat);
+  p->ld_save_xhat = a->save_xhat_ld;
+  p->save_rstd = a->save_rstd;
   *bn_out = bn;
   return LOKA_OK;
 }
@@ -422,7 +438,9 @@ static loka_status prepare_bw(const loka_linear_args* a, CUtensorMap* ta, CUtens
   if (Y.ld < N || (Y.ld * elem_size(Y.dtype)) % 16) return LOKA_ERR_INVALID_ARG;
   const bool fp8_out = is_fp8(Y.dtype);
   if (fp8_out && (!Y.scales || Y.gran != LOKA_GRAN_ROW || N > 128)) return LOKA_ERR_UNSUPPORTED;
-  if (a->norm != LOKA_NORM_NONE || a->gamma || a->beta || a->act != LOKA_ACT_NONE) return LOKA_ERR_UNSUPPORTED;
+  if (a->norm != LOKA_NORM_NONE || a->gamma || a->beta || a->act != LOKA_ACT_NONE || a->bwd_xhat || a->save_xhat ||
+      a->save_rstd)
+    return LOKA_ERR_UNSUPPORTED;
   if (a->bias && a->bias_dtype != LOKA_F32 && a->bias_dtype != LOKA_BF16) return LOKA_ERR_INVALID_ARG;
   if (!make_map_u8(ta, A.data, M, K, A.ld, 128)) return LOKA_ERR_CUDA;
   if (!make_map_u8(tb, B.data, N, K, B.ld, 128)) return LOKA_ERR_CUDA;
@@ -564,8 +582,15 @@ static loka_status run_mx_pair(const loka_linear_args* a, void* ws, size_t ws_by
 // epilogue ("cross-block synchronization ... negates most of the performance gains";
 // measured).  Tensorwise / rowwise scales only.
 static bool wide_norm_unfused(const loka_linear_args* a) {
-  if (!a || !use_pair_kernel() || (a->norm != LOKA_NORM_LAYER && a->norm != LOKA_NORM_RMS)) return false;
-  if (a->N <= 2048 || a->N > 4096 || a->N % 8 || a->M <= 0 || a->K <= 0) return false;
+  if (!a || !use_pair_kernel() || a->save_xhat || a->save_rstd || a->M <= 0 || a->K <= 0) return false;
+  if (a->bwd_xhat) {  // NEXT-1 backward: the pass after the pair GEMM beats the fused epilogue at scale
+    const bool blk256 = a->norm == LOKA_NORM_BLOCK_RMS && a->norm_block == 256 && a->N % 256 == 0;
+    if (a->norm != LOKA_NORM_LAYER && a->norm != LOKA_NORM_RMS && !blk256) return false;
+    if (a->N % 8 || a->N > 4096 || a->bias) return false;
+  } else {
+    if (a->norm != LOKA_NORM_LAYER && a->norm != LOKA_NORM_RMS) return false;
+    if (a->N <= 2048 || a->N > 4096 || a->N % 8) return false;
+  }
   if (a->a.gran != LOKA_GRAN_TENSOR && a->a.gran != LOKA_GRAN_ROW) return false;
   if (a->b.gran != LOKA_GRAN_TENSOR && a->b.gran != LOKA_GRAN_ROW) return false;
   return cdiv(a->M, 256) * cdiv(a->N, 256) >= 74;
@@ -578,6 +603,8 @@ static loka_status run_wide_norm(const loka_linear_args* a, void* ws, size_t ws_
   if (a->beta && a->norm != LOKA_NORM_LAYER) return LOKA_ERR_INVALID_ARG;
   if (a->act != LOKA_ACT_NONE && a->act != LOKA_ACT_HARDSWISH) return LOKA_ERR_INVALID_ARG;
   loka_linear_args g = *a;  // the GEMM: plain epilogue, FP32 into the workspace
+  g.bwd_xhat = nullptr;
+  g.bwd_rstd = nullptr;
   g.norm = LOKA_NORM_NONE;
   g.act = LOKA_ACT_NONE;
   g.gamma = nullptr;
@@ -610,6 +637,15 @@ static loka_status run_wide_norm(const loka_linear_args* a, void* ws, size_t ws_
   rp.precast = a->debug_precast;
   rp.ld_pre = a->N;
   rp.status = a->status_dev;
+  if (a->bwd_xhat) {
+    if (!a->bwd_rstd || (a->bwd_xhat_ld * 2) % 16 || a->bwd_xhat_ld < a->N || !aligned16(a->bwd_xhat))
+      return LOKA_ERR_INVALID_ARG;
+    rp.bwd = 1;
+    rp.block = a->norm == LOKA_NORM_BLOCK_RMS ? a->norm_block : 0;
+    rp.xhat = static_cast<const __nv_bfloat16*>(a->bwd_xhat);
+    rp.ld_xhat = a->bwd_xhat_ld;
+    rp.rstd_in = a->bwd_rstd;
+  }
   return launch_rownorm(rp, sms, s) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
 }
 

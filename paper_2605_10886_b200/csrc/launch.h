@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cuda_bf16.h>
 #include <stdint.h>
 
 namespace loka {
@@ -66,6 +67,14 @@ struct LinearParams {
   int32_t* status;
   int32_t cluster_n;             // CTAs per cluster along N (1 = no cross-CTA row exchange)
   int32_t act;                   // loka_act, applied after the norm (and gamma / beta)
+  // NEXT-1 norm backward (bwd): the accumulator is dL/dh of a forward h = act(norm(z)*gamma+beta)
+  // whose saved xhat (bf16 [M, N], ld_xhat) and rstd (rstd_in: [M], BLOCK_RMS [M, N/block]) are
+  // given; the epilogue emits dL/dz.  Forward saves (nullable): save_xhat (bf16) / save_rstd.
+  int32_t bwd;
+  const __nv_bfloat16* xhat; int64_t ld_xhat;
+  const float* rstd_in;
+  __nv_bfloat16* save_xhat; int64_t ld_save_xhat;
+  float* save_rstd;
   // native block-scaled (MX) mode: UE8M0 blockwise scales applied by the tensor core; sa/sb unused
   int32_t mx;
   const uint8_t* sfa_pack;       // [ceil(M/128)][kblocks][512] (sfpack.cu layout)
@@ -180,6 +189,10 @@ struct RowNormParams {
   float* y_scales;
   float* precast; int64_t ld_pre;
   int32_t* status;
+  // NEXT-1 backward mode (bwd): y32 holds dL/dh; xhat / rstd_in are the forward's saves
+  int32_t bwd, block;
+  const __nv_bfloat16* xhat; int64_t ld_xhat;
+  const float* rstd_in;
 };
 cudaError_t launch_rownorm(const RowNormParams& p, int num_sms, cudaStream_t st);
 // y[m,n] = (sum_s part[s][m][n]) * s_a[m] * s_b[n] (+ bias[n]) -> y (bf16 / f32)

@@ -171,7 +171,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool is_fp8_out = p.out_dtype == LOKA_E4M3 || p.out_dtype == LOKA_E5M2;
   // affine (gamma/beta) and the activation make the output non-monotone in y: the FP8 row amax
   // is then reduced over the final values instead of derived from y max / min
-  const bool affine = p.gamma != nullptr || p.beta != nullptr || p.act != LOKA_ACT_NONE;
+  const bool bwd = p.bwd != 0;  // NEXT-1 norm backward epilogue (y = dL/dz: not monotone in acc)
+  const bool affine = p.gamma != nullptr || p.beta != nullptr || p.act != LOKA_ACT_NONE || bwd;
   const bool has_gb = p.gamma != nullptr || p.beta != nullptr;
   const bool is_block = norm == LOKA_NORM_BLOCK_RMS;
   // cluster-wide barriers: every thread of the CTA executes the same count (uniform)
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)cb;
     const float sa = row_ok ? (MX ? 1.f : p.sa[p.sa_row ? grow : 0]) : 0.f;  // MX: scales applied by the MMA
     const bool has_bias = p.bias != nullptr;
-    const bool fold = !has_bias && norm != LOKA_NORM_NONE;  // s_a folded into eps
+    const bool fold = !has_bias && norm != LOKA_NORM_NONE && !bwd;  // s_a folded into eps
     const float ys = fold ? 1.f : sa;
     const int blk = is_block ? p.norm_block : BN;
     const uint32_t col_s = smem_u32(col);
@@ -267,6 +268,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     named_bar_sync(1, kEpiThreads);
 
+    if (bwd && row_ok) {  // NEXT-1: pull this thread's x-hat row segment into L2 while the MMAs run
+      const __nv_bfloat16* xr = p.xhat + (int64_t)grow * p.ld_xhat + n0 + cb;
+      for (int j = 0; j < CPT; j += 64) asm volatile("prefetch.global.L2 [%0];" ::"l"(xr + j));
+    }
     if (lane == 0) mbar_wait(tmem_full, 0, 3);  // one waiter per warp
     __syncwarp();
     tc_fence_after();
@@ -312,7 +317,52 @@ __global__ void __launch_bounds__(kThreads, 1)
     rec.init();
     const bool need_minmax = is_fp8_out && !affine;
     const bool need_stats = norm != LOKA_NORM_NONE || need_minmax;
-    if (need_stats && nv > 0) {
+    // ---- NEXT-1 backward: g = dh * act'(xhat*gamma + beta) * gamma; per-row sums of g and g*xhat
+    //      (the LayerNorm / RMSNorm backward's two reductions) in the forward's record slots:
+    //      rec.mean = mean(g) over the thread's columns, rec.ss = sum(g * xhat) ----
+    // x-hat of this thread's 8 columns j..j+7 (bf16, one 16-byte load; re-read in the finalize pass
+    // instead of being held next to dh, so the backward fits every tile width)
+    auto load_xh8 = [&](int j, float (&xv)[8]) {
+      const __nv_bfloat16* xr = p.xhat + (int64_t)(row_ok ? grow : 0) * p.ld_xhat + n0 + cb + j;
+      if (row_ok && cb + j + 8 <= ncols) {
+        const uint4 w = __ldg(reinterpret_cast<const uint4*>(xr));
+        xv[0] = bf16lo_to_f32(w.x); xv[1] = bf16hi_to_f32(w.x); xv[2] = bf16lo_to_f32(w.y); xv[3] = bf16hi_to_f32(w.y);
+        xv[4] = bf16lo_to_f32(w.z); xv[5] = bf16hi_to_f32(w.z); xv[6] = bf16lo_to_f32(w.w); xv[7] = bf16hi_to_f32(w.w);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) xv[k] = (row_ok && cb + j + k < ncols) ? __bfloat162float(xr[k]) : 0.f;
+      }
+    };
+    if (bwd) {
+      float sg = 0.f, sgx = 0.f;
+#pragma unroll
+      for (int j = 0; j < CPT; j += 8) {
+        float xv[8];
+        load_xh8(j, xv);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t o = (uint32_t)(cb + j + k) * 4u;
+          const float gam = col[2 * BN + cb + j + k], bet = col[3 * BN + cb + j + k];
+          (void)o;
+          float g = y[j + k];
+          if (p.act == LOKA_ACT_HARDSWISH) {  // PyTorch's hardswish' convention at the kinks
+            const float yp = fmaf(xv[k], gam, bet);
+            g *= yp < -3.f ? 0.f : (yp <= 3.f ? fmaf(yp, 1.f / 3.f, 0.5f) : 1.f);
+          }
+          g = (cb + j + k < ncols) ? g * gam : 0.f;
+          y[j + k] = g;
+          sg += g;
+          sgx = fmaf(g, xv[k], sgx);
+        }
+      }
+      rec.init();
+      rec.n = (float)nv;
+      rec.mean = nv > 0 ? sg / (float)nv : 0.f;
+      rec.m2 = 0.f;
+      rec.ss = sgx;
+      rec.ymax = rec.ymin = 0.f;
+    }
+    if (need_stats && nv > 0 && !bwd) {
       // Columns >= N of a ragged tile hold exact zeros (zero-filled B rows, s_b = bias = 0), so
       // sums need no mask; only max/min must skip them.
       const float* t = y;
@@ -391,7 +441,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (xchg_stats) {
       const uint32_t my_rank = cluster_ctarank();
       if (cq == 0) {
-        const float4 v = make_float4(norm == LOKA_NORM_LAYER ? rec.mean : rec.ss, rec.m2, rec.ymax, rec.ymin);
+        const float4 v = bwd ? make_float4(rec.mean, rec.ss, 0.f, 0.f)
+                             : make_float4(norm == LOKA_NORM_LAYER ? rec.mean : rec.ss, rec.m2, rec.ymax, rec.ymin);
         const uint32_t la = smem_u32(cs + ((size_t)my_rank * 128 + r) * 4);
         for (int rk = 0; rk < csize; ++rk) st_dsmem_f4(mapa_shared(la, (uint32_t)rk), v);
       }
@@ -405,14 +456,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float4 v = lds_f4(smem_u32(cs + ((size_t)rk * 128 + r) * 4));
         const float nk = (float)min(BN, p.N - rk * BN);
         o.n += nk;
-        sm = fmaf(nk, norm == LOKA_NORM_LAYER ? v.x : 0.f, sm);
-        o.ss += norm == LOKA_NORM_LAYER ? 0.f : v.x;
+        sm = fmaf(nk, (norm == LOKA_NORM_LAYER || bwd) ? v.x : 0.f, sm);
+        o.ss += bwd ? v.y : (norm == LOKA_NORM_LAYER ? 0.f : v.x);
         o.ymax = fmaxf(o.ymax, v.z);
         o.ymin = fminf(o.ymin, v.w);
       }
       o.mean = o.n > 0.f ? __fdiv_rn(sm, o.n) : 0.f;
       float m2 = 0.f;
-      for (int rk = 0; rk < csize; ++rk) {
+      for (int rk = 0; rk < csize && !bwd; ++rk) {
         const float4 v = lds_f4(smem_u32(cs + ((size_t)rk * 128 + r) * 4));
         const float nk = (float)min(BN, p.N - rk * BN);
         const float dk = (norm == LOKA_NORM_LAYER ? v.x : 0.f) - o.mean;
@@ -450,13 +501,53 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (threadIdx.x == 64) LOKA_TRACE(11);
 
+    // ---- NEXT-1 backward finalize: dz = rstd (g - mean(g) - xhat mean(g xhat)) (LayerNorm),
+    //      rstd (g - xhat mean(g xhat)) (RMSNorm; BlockNorm per block with the block's sums) ----
+    {
+      if (bwd) {
+        float mg = 0.f, mgx = 0.f, rs = 0.f;
+        if (is_block) {
+          const int qpb = blk / CPT;
+          const int kb0 = (cq / qpb) * qpb;
+          float ss = 0.f;
+#pragma unroll
+          for (int k2 = 0; k2 < 4; ++k2)
+            if (k2 >= kb0 && k2 < kb0 + qpb) ss += q_ss[k2];
+          mgx = ss / (float)blk;
+          rs = row_ok ? p.rstd_in[(int64_t)grow * (p.N / blk) + (n0 + cb) / blk] : 0.f;
+        } else {
+          mg = norm == LOKA_NORM_LAYER ? rec.mean : 0.f;
+          mgx = rec.ss / rec.n;
+          rs = row_ok ? p.rstd_in[grow] : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < CPT; j += 8) {
+          float xv[8];
+          load_xh8(j, xv);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) y[j + k] = rs * (y[j + k] - mg - xv[k] * mgx);
+        }
+      }
+    }
     // normalised values in place (registers)
-    if (norm != LOKA_NORM_NONE) {
+    if (norm != LOKA_NORM_NONE && !bwd) {
       const float2 r2 = make_float2(rstd, rstd), c2 = make_float2(c0, c0);
+      const bool save = p.save_xhat != nullptr && row_ok;
 #pragma unroll
       for (int j = 0; j < CPT; j += 4) {
         float2 a = ffma2(make_float2(y[j], y[j + 1]), r2, c2);
         float2 b = ffma2(make_float2(y[j + 2], y[j + 3]), r2, c2);
+        if (save) {  // NEXT-1: the normalised values (before gamma / beta / act) for the backward
+          __nv_bfloat162 h0 = __floats2bfloat162_rn(a.x, a.y), h1 = __floats2bfloat162_rn(b.x, b.y);
+          __nv_bfloat16* d = p.save_xhat + (int64_t)grow * p.ld_save_xhat + n0 + cb + j;
+          if (cb + j + 4 <= ncols) {
+            *reinterpret_cast<uint2*>(d) = make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+          } else {
+            const __nv_bfloat16 hv[4] = {h0.x, h0.y, h1.x, h1.y};
+            for (int k = 0; k < 4; ++k)
+              if (cb + j + k < ncols) d[k] = hv[k];
+          }
+        }
         if (has_gb) {
           const uint32_t o = (uint32_t)(cb + j) * 4u;
           const float4 g4 = lds_f4(col_s + 2u * BN * 4u + o);
@@ -468,8 +559,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
 
+    if (p.save_rstd && row_ok && !bwd && norm != LOKA_NORM_NONE) {  // rstd of z = acc * s_a * s_b (+ bias)
+      const float rz = fold ? __fdiv_rn(rstd, sa) : rstd;
+      if (is_block) {
+        if (cb % blk == 0 && nv > 0) p.save_rstd[(int64_t)grow * (p.N / blk) + (n0 + cb) / blk] = rz;
+      } else if (cq == 0 && blockIdx.y == 0) {
+        p.save_rstd[grow] = rz;
+      }
+    }
+
     // ---- activation (PAPER.md:502 Hard Swish): x * ReLU6(x + 3) / 6 ----
-    if (p.act == LOKA_ACT_HARDSWISH) {
+    if (p.act == LOKA_ACT_HARDSWISH && !bwd) {
 #pragma unroll
       for (int j = 0; j < CPT; ++j) {
         const float t = fminf(fmaxf(y[j] + 3.f, 0.f), 6.f);

@@ -36,6 +36,64 @@ __global__ void __launch_bounds__(256) rownorm_kernel(const RowNormParams p) {
     for (int w = 0; w < 8; ++w) r += red[w];
     return r;
   };
+  auto rowout = [&](int64_t row, float (&v)[8 * V], const bool (&ok)[V], float amax) {
+      const bool fp8 = p.out_dtype == LOKA_E4M3 || p.out_dtype == LOKA_E5M2;
+      float r_out = 1.f;
+      if (fp8) {
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xFFFFFFFFu, amax, o));
+        __syncthreads();
+        if (lane == 0) red[warp] = amax;
+        __syncthreads();
+        if (t == 0) {
+          float m = red[0];
+          for (int w = 1; w < 8; ++w) m = fmaxf(m, red[w]);
+          if (__float_as_uint(m) >= 0x7F800000u && p.status) atomicOr(p.status, LOKA_DEVSTATUS_NONFINITE);
+          float s_out, r;
+          if (p.out_dtype == LOKA_E4M3) scales_from_amax<LOKA_E4M3, LOKA_SCALE_F32>(m, s_out, r);
+          else scales_from_amax<LOKA_E5M2, LOKA_SCALE_F32>(m, s_out, r);
+          if (p.y_scales) p.y_scales[row] = s_out;
+          bc = r;
+        }
+        __syncthreads();
+        r_out = bc;
+      }
+#pragma unroll
+      for (int u = 0; u < V; ++u) {
+        if (!ok[u]) continue;
+        const int c = (u * 256 + t) * 8;
+        const float* x = v + 8 * u;
+        if (p.precast) {
+          float* d = p.precast + row * p.ld_pre + c;
+          *reinterpret_cast<float4*>(d) = make_float4(x[0], x[1], x[2], x[3]);
+          *reinterpret_cast<float4*>(d + 4) = make_float4(x[4], x[5], x[6], x[7]);
+        }
+        if (p.out_dtype == LOKA_F32) {
+          float* d = reinterpret_cast<float*>(p.y) + row * p.ldy + c;
+          *reinterpret_cast<float4*>(d) = make_float4(x[0], x[1], x[2], x[3]);
+          *reinterpret_cast<float4*>(d + 4) = make_float4(x[4], x[5], x[6], x[7]);
+        } else if (p.out_dtype == LOKA_BF16) {
+          uint32_t w[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            __nv_bfloat162 hh = __floats2bfloat162_rn(x[2 * k], x[2 * k + 1]);
+            w[k] = *reinterpret_cast<uint32_t*>(&hh);
+          }
+          *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.y) + row * p.ldy + c) =
+              make_uint4(w[0], w[1], w[2], w[3]);
+        } else {
+          float f[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) f[k] = __fmul_rn(x[k], r_out);
+          const uint2 code = p.out_dtype == LOKA_E4M3
+                                 ? make_uint2(cvt_fp8x4<LOKA_E4M3>(f[0], f[1], f[2], f[3]),
+                                              cvt_fp8x4<LOKA_E4M3>(f[4], f[5], f[6], f[7]))
+                                 : make_uint2(cvt_fp8x4<LOKA_E5M2>(f[0], f[1], f[2], f[3]),
+                                              cvt_fp8x4<LOKA_E5M2>(f[4], f[5], f[6], f[7]));
+          *reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(p.y) + row * p.ldy + c) = code;
+        }
+      }
+  };
   for (int64_t row = blockIdx.x; row < p.M; row += gridDim.x) {
     const float* xr = p.y32 + row * p.ld32;
     float v[8 * V];
@@ -55,6 +113,77 @@ __global__ void __launch_bounds__(256) rownorm_kernel(const RowNormParams p) {
       }
     }
     float rstd = 1.f, c0 = 0.f;
+    if (p.bwd) {
+      // NEXT-1 norm backward: g = dh * act'(xhat*gamma + beta) * gamma,
+      // dz = rstd (g - mean(g) - xhat mean(g xhat)) (LayerNorm; RMS / BlockNorm without mean(g))
+      float xv[8 * V];
+#pragma unroll
+      for (int u = 0; u < V; ++u) {
+        const int c = (u * 256 + t) * 8;
+        if (ok[u]) {
+          const uint4 w = __ldg(reinterpret_cast<const uint4*>(p.xhat + row * p.ld_xhat + c));
+          xv[8 * u] = bf16lo_to_f32(w.x); xv[8 * u + 1] = bf16hi_to_f32(w.x); xv[8 * u + 2] = bf16lo_to_f32(w.y);
+          xv[8 * u + 3] = bf16hi_to_f32(w.y); xv[8 * u + 4] = bf16lo_to_f32(w.z); xv[8 * u + 5] = bf16hi_to_f32(w.z);
+          xv[8 * u + 6] = bf16lo_to_f32(w.w); xv[8 * u + 7] = bf16hi_to_f32(w.w);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) xv[8 * u + k] = 0.f;
+        }
+      }
+      float sg[V], sgx[V];
+#pragma unroll
+      for (int u = 0; u < V; ++u) {
+        const int c = (u * 256 + t) * 8;
+        sg[u] = sgx[u] = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float gam = (ok[u] && p.gamma) ? __ldg(p.gamma + c + k) : 1.f;
+          const float bet = (ok[u] && p.beta) ? __ldg(p.beta + c + k) : 0.f;
+          float g = v[8 * u + k];
+          if (p.act == LOKA_ACT_HARDSWISH) {
+            const float yp = fmaf(xv[8 * u + k], gam, bet);
+            g *= yp < -3.f ? 0.f : (yp <= 3.f ? fmaf(yp, 1.f / 3.f, 0.5f) : 1.f);
+          }
+          g = ok[u] ? g * gam : 0.f;
+          v[8 * u + k] = g;
+          sg[u] += g;
+          sgx[u] = fmaf(g, xv[8 * u + k], sgx[u]);
+        }
+      }
+      float amax = 0.f;
+      if (p.norm == LOKA_NORM_BLOCK_RMS) {  // blocks of 256 columns = one warp's span per u
+#pragma unroll
+        for (int u = 0; u < V; ++u) {
+          float s2 = sgx[u];
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) s2 += __shfl_xor_sync(0xFFFFFFFFu, s2, o);
+          const int c = (u * 256 + t) * 8;
+          const float rs = ok[u] ? p.rstd_in[row * (p.N / 256) + c / 256] : 0.f;
+          const float mgx = s2 / 256.f;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            v[8 * u + k] = rs * (v[8 * u + k] - xv[8 * u + k] * mgx);
+            if (ok[u]) amax = fmaxf(amax, fabsf(v[8 * u + k]));
+          }
+        }
+      } else {
+        float a1 = 0.f, a2 = 0.f;
+#pragma unroll
+        for (int u = 0; u < V; ++u) a1 += sg[u], a2 += sgx[u];
+        const float mg = p.norm == LOKA_NORM_LAYER ? __fdiv_rn(bsum(a1), n) : 0.f;
+        const float mgx = __fdiv_rn(bsum(a2), n);
+        const float rs = p.rstd_in[row];
+#pragma unroll
+        for (int u = 0; u < V; ++u)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            v[8 * u + k] = rs * (v[8 * u + k] - mg - xv[8 * u + k] * mgx);
+            if (ok[u]) amax = fmaxf(amax, fabsf(v[8 * u + k]));
+          }
+      }
+      rowout(row, v, ok, amax);
+      continue;
+    }
     if (p.norm == LOKA_NORM_LAYER) {
       float s = 0.f;
 #pragma unroll
@@ -91,62 +220,7 @@ __global__ void __launch_bounds__(256) rownorm_kernel(const RowNormParams p) {
         if (ok[u]) amax = fmaxf(amax, fabsf(x));
       }
     }
-    const bool fp8 = p.out_dtype == LOKA_E4M3 || p.out_dtype == LOKA_E5M2;
-    float r_out = 1.f;
-    if (fp8) {
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xFFFFFFFFu, amax, o));
-      __syncthreads();
-      if (lane == 0) red[warp] = amax;
-      __syncthreads();
-      if (t == 0) {
-        float m = red[0];
-        for (int w = 1; w < 8; ++w) m = fmaxf(m, red[w]);
-        if (__float_as_uint(m) >= 0x7F800000u && p.status) atomicOr(p.status, LOKA_DEVSTATUS_NONFINITE);
-        float s_out, r;
-        if (p.out_dtype == LOKA_E4M3) scales_from_amax<LOKA_E4M3, LOKA_SCALE_F32>(m, s_out, r);
-        else scales_from_amax<LOKA_E5M2, LOKA_SCALE_F32>(m, s_out, r);
-        if (p.y_scales) p.y_scales[row] = s_out;
-        bc = r;
-      }
-      __syncthreads();
-      r_out = bc;
-    }
-#pragma unroll
-    for (int u = 0; u < V; ++u) {
-      if (!ok[u]) continue;
-      const int c = (u * 256 + t) * 8;
-      const float* x = v + 8 * u;
-      if (p.precast) {
-        float* d = p.precast + row * p.ld_pre + c;
-        *reinterpret_cast<float4*>(d) = make_float4(x[0], x[1], x[2], x[3]);
-        *reinterpret_cast<float4*>(d + 4) = make_float4(x[4], x[5], x[6], x[7]);
-      }
-      if (p.out_dtype == LOKA_F32) {
-        float* d = reinterpret_cast<float*>(p.y) + row * p.ldy + c;
-        *reinterpret_cast<float4*>(d) = make_float4(x[0], x[1], x[2], x[3]);
-        *reinterpret_cast<float4*>(d + 4) = make_float4(x[4], x[5], x[6], x[7]);
-      } else if (p.out_dtype == LOKA_BF16) {
-        uint32_t w[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          __nv_bfloat162 hh = __floats2bfloat162_rn(x[2 * k], x[2 * k + 1]);
-          w[k] = *reinterpret_cast<uint32_t*>(&hh);
-        }
-        *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.y) + row * p.ldy + c) =
-            make_uint4(w[0], w[1], w[2], w[3]);
-      } else {
-        float f[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) f[k] = __fmul_rn(x[k], r_out);
-        const uint2 code = p.out_dtype == LOKA_E4M3
-                               ? make_uint2(cvt_fp8x4<LOKA_E4M3>(f[0], f[1], f[2], f[3]),
-                                            cvt_fp8x4<LOKA_E4M3>(f[4], f[5], f[6], f[7]))
-                               : make_uint2(cvt_fp8x4<LOKA_E5M2>(f[0], f[1], f[2], f[3]),
-                                            cvt_fp8x4<LOKA_E5M2>(f[4], f[5], f[6], f[7]));
-        *reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(p.y) + row * p.ldy + c) = code;
-      }
-    }
+    rowout(row, v, ok, amax);
   }
 }
 
