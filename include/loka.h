@@ -252,6 +252,25 @@ LOKA_API loka_status loka_probe_error(int32_t L, const loka_probe_pair* pairs, d
                              loka_probe_stats* stats_dev, void* ws, size_t ws_bytes, loka_stream_t stream);
 LOKA_API size_t loka_probe_workspace_size(int32_t L, const loka_probe_pair* pairs);
 
+/* ---- NEXT-2: LoKA Probe online input tracker (batched Welford) ------------
+ * Running summaries of one layer's input distribution, feature dimension only (the batch rows are
+ * independent): n (host), mean [K] and the unnormalised scatter Sigma [K, K]
+ * (row-major, ld K), both FP32 device arrays owned by the caller (zero them for n = 0).
+ * loka_probe_track_input merges one batch X [B, K] (bf16, ld*2 % 16 == 0, K % 8 == 0):
+ *   delta = mu_b - mean, mean += (B / n_new) delta,
+ *   Sigma += S_b + (n B / n_new) delta delta^T with S_b = (X - mu_b)^T (X - mu_b)
+ * (S_b on the tensor cores from a centred bf16 transpose, FP32 accumulation) and sets n += B.
+ * The unbiased covariance is Sigma / (n - 1).  Async on the stream; ws >= the workspace size.   */
+typedef struct loka_welford_state {
+  int64_t n;
+  int64_t K;
+  float* mean;
+  float* scatter;
+} loka_welford_state;
+LOKA_API size_t loka_probe_track_workspace_size(const loka_welford_state* st, int64_t B);
+LOKA_API loka_status loka_probe_track_input(loka_welford_state* st, const loka_tensor* x, void* ws, size_t ws_bytes,
+                                           loka_stream_t stream);
+
 /* ---- a8: LoKA Dispatch (host) -------------------------------------------------------------- */
 typedef struct loka_candidate {
   const char* id;

@@ -63,6 +63,10 @@ class loka_stack_args(C.Structure):
                 ("status_dev", C.c_void_p), ("h", loka_tensor * 7), ("ws", C.c_void_p), ("ws_bytes", C.c_size_t)]
 
 
+class loka_welford_state(C.Structure):
+    _fields_ = [("n", C.c_int64), ("K", C.c_int64), ("mean", C.c_void_p), ("scatter", C.c_void_p)]
+
+
 class loka_probe_pair(C.Structure):
     _fields_ = [("out", C.c_void_p), ("out_dtype", C.c_int), ("ref", C.c_void_p), ("ref_dtype", C.c_int),
                 ("M", C.c_int64), ("N", C.c_int64), ("ld_out", C.c_int64), ("ld_ref", C.c_int64)]
@@ -100,6 +104,8 @@ _sig = {
     "loka_debug_hang_info": ([_P(C.c_uint64), C.c_int32], C.c_int64),
     "loka_debug_trace": ([C.c_int32, _P(C.c_uint64), C.c_int64], C.c_int64),
     "loka_stack_workspace_size": ([_P(loka_stack_args)], C.c_size_t),
+    "loka_probe_track_workspace_size": ([_P(loka_welford_state), C.c_int64], C.c_size_t),
+    "loka_probe_track_input": ([_P(loka_welford_state), _P(loka_tensor), C.c_void_p, C.c_size_t, C.c_void_p], C.c_int),
 }
 for _name, (_args, _ret) in _sig.items():
     _fn = getattr(_lib, _name)
@@ -378,3 +384,31 @@ def loka_fp8_mlp_stack(xq, xs, ws, stream=None, **kw):
     a, y, ys = make_stack_args(xq, xs, ws, **kw)
     _check(_lib.loka_fp8_mlp_stack(C.byref(a), _stream(stream)), "loka_fp8_mlp_stack")
     return y, ys
+
+
+class InputTracker:
+    """NEXT-2: batched Welford tracker of one layer's input distribution
+    (feature mean + K x K scatter in FP32 on the device), wrapping loka_probe_track_input."""
+
+    def __init__(self, k: int, device=None):
+        dev = torch.device("cuda") if device is None else device
+        self.mean = torch.zeros(k, dtype=torch.float32, device=dev)
+        self.scatter = torch.zeros(k, k, dtype=torch.float32, device=dev)
+        self.state = loka_welford_state(0, k, self.mean.data_ptr(), self.scatter.data_ptr())
+        self._ws = None
+
+    @property
+    def n(self) -> int:
+        return int(self.state.n)
+
+    def update(self, x: torch.Tensor, stream=None):
+        assert x.dtype == torch.bfloat16 and x.dim() == 2 and x.stride(1) == 1
+        t = _tensor(x, BF16, x.shape[0], x.shape[1])
+        nws = int(_lib.loka_probe_track_workspace_size(C.byref(self.state), x.shape[0]))
+        if self._ws is None or self._ws.numel() < nws:
+            self._ws = torch.empty(max(nws, 1), dtype=torch.uint8, device=x.device)
+        _check(_lib.loka_probe_track_input(C.byref(self.state), C.byref(t), C.c_void_p(self._ws.data_ptr()),
+                                           self._ws.numel(), _stream(stream)), "loka_probe_track_input")
+
+    def covariance(self) -> torch.Tensor:
+        return self.scatter / (self.n - 1)

@@ -500,12 +500,18 @@ static bool plain_pair_ok(const loka_linear_args* a) {
 // 2048 x 123200 x 1024 layer): ks slices of kbps 128-K blocks; each slice's raw FP32
 // partial goes to the workspace and one reduction kernel applies the scales.  ks minimises
 // waves(ks) * kbps (in 128-K MMA-step units) + the partials' HBM round trip.
+static int split_k_shape(int64_t M, int64_t N, int64_t nkb, int* kbps_out);
 static int split_k_for(const loka_linear_args* a, int* kbps_out = nullptr) {
-  constexpr int kPairs = 74;
   if (kbps_out) *kbps_out = 0;
   if (!plain_pair_ok(a) || a->M % 32 || a->N % 4 || a->M <= 0 || a->N <= 0 || a->K <= 0) return 1;
-  const int64_t tiles = cdiv(a->M, 256) * cdiv(a->N, 256), nkb = cdiv(a->K, 128);
-  if (tiles >= kPairs || nkb < 16) return 1;
+  return split_k_shape(a->M, a->N, cdiv(a->K, 128), kbps_out);
+}
+// ks for an M x N output with nkb K-stages on the CTA-pair engine (1 = no split)
+static int split_k_shape(int64_t M, int64_t N, int64_t nkb, int* kbps_out) {
+  constexpr int kPairs = 74;
+  if (kbps_out) *kbps_out = 0;
+  const int64_t tiles = cdiv(M, 256) * cdiv(N, 256);
+  if (tiles >= kPairs || nkb < 16 || M % 32 || N % 4) return 1;
   double best = (double)nkb;  // one wave, no split
   int bks = 1, bkbps = (int)nkb;
   for (int ks = 2; ks <= 32; ++ks) {
@@ -513,7 +519,7 @@ static int split_k_for(const loka_linear_args* a, int* kbps_out = nullptr) {
     if (kbps < 4) break;
     const int64_t eks = cdiv(nkb, kbps);  // slices actually formed
     const double waves = std::ceil((double)(tiles * eks) / kPairs);
-    const double part_steps = 2.0 * eks * (double)a->M * a->N * 4 / 6.5e12 / 0.376e-6;
+    const double part_steps = 2.0 * eks * (double)M * N * 4 / 6.5e12 / 0.376e-6;
     const double cost = waves * (double)kbps + part_steps;
     if (cost < best - 1e-9) {
       best = cost;
@@ -890,6 +896,112 @@ static int probe_nblk(int32_t L) {
 
 size_t loka_probe_workspace_size(int32_t L, const loka_probe_pair* /*pairs*/) {
   return (size_t)64 * probe_nblk(L) * (8 + 8 + 8 + 4) + 64;
+}
+
+// ---- NEXT-2: batched Welford input tracker ----------------------------------------------------
+namespace {
+struct TrackWs {
+  size_t colpart, delta, one, xct, sb, part, total;
+  int64_t ldxct;
+  int nchunk, ksplit, kbps;
+};
+TrackWs track_ws(int64_t K, int64_t B) {
+  TrackWs w{};
+  w.ksplit = split_k_shape(K, K, cdiv(B, 64), &w.kbps);  // few K x K tiles, long B: split the batch
+  auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
+  w.nchunk = (int)std::max<int64_t>(1, std::min<int64_t>(128, cdiv(B, 64)));
+  w.ldxct = (B + 7) / 8 * 8;
+  size_t o = 0;
+  w.colpart = o; o += al((size_t)w.nchunk * K * 4);
+  w.delta = o;   o += al((size_t)K * 4);
+  w.one = o;     o += 256;
+  w.xct = o;     o += al((size_t)K * w.ldxct * 2);
+  w.sb = o;      o += al((size_t)K * K * 4);
+  w.part = o;    o += w.ksplit > 1 ? al((size_t)w.ksplit * K * K * 4) : 0;
+  w.total = o;
+  return w;
+}
+}  // namespace
+
+size_t loka_probe_track_workspace_size(const loka_welford_state* st, int64_t B) {
+  if (!st || st->K <= 0 || B <= 0) return 0;
+  return track_ws(st->K, B).total;
+}
+
+loka_status loka_probe_track_input(loka_welford_state* st, const loka_tensor* x, void* ws, size_t ws_bytes,
+                                   loka_stream_t stream) {
+  if (!st || !x || !st->mean || !st->scatter || st->K <= 0 || st->n < 0) return LOKA_ERR_INVALID_ARG;
+  const int64_t K = st->K, B = x->rows;
+  if (x->dtype != LOKA_BF16 || !x->data || x->cols != K || x->ld < K || (x->ld * 2) % 16 || K % 8 ||
+      !aligned16(x->data))
+    return LOKA_ERR_INVALID_ARG;
+  if (B < 0 || B > (1ll << 31) - 1 || K > (1 << 20)) return LOKA_ERR_SHAPE;
+  if (B == 0) return LOKA_OK;
+  const TrackWs w = track_ws(K, B);
+  if (!ws || ws_bytes < w.total || !aligned16(ws)) return LOKA_ERR_WORKSPACE;
+  int sms = 148;
+  loka_status stt = check_device(&sms);
+  if (stt != LOKA_OK) return stt;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  TrackParams tp;
+  std::memset(&tp, 0, sizeof(tp));
+  tp.x = static_cast<const __nv_bfloat16*>(x->data);
+  tp.ldx = x->ld;
+  tp.B = B;
+  tp.K = K;
+  tp.mean = st->mean;
+  tp.scatter = st->scatter;
+  tp.n_old = st->n;
+  tp.colpart = reinterpret_cast<float*>(base + w.colpart);
+  tp.delta = reinterpret_cast<float*>(base + w.delta);
+  tp.one = reinterpret_cast<float*>(base + w.one);
+  tp.xct = reinterpret_cast<__nv_bfloat16*>(base + w.xct);
+  tp.ldxct = w.ldxct;
+  tp.sb = reinterpret_cast<float*>(base + w.sb);
+  tp.nchunk = w.nchunk;
+  if (launch_track_prep(tp, s) != cudaSuccess) return LOKA_ERR_CUDA;
+  // S_b = Xc^T (Xc^T)^T on the CTA-pair engine, BF16 operands, FP32 out
+  GroupedParams gp;
+  std::memset(&gp, 0, sizeof(gp));
+  gp.G = 1;
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return LOKA_ERR_CUDA;
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)B, (cuuint64_t)K};
+    cuuint64_t strides[1] = {(cuuint64_t)(w.ldxct * 2)};
+    cuuint32_t box[2] = {64u, 128u};
+    cuuint32_t es[2] = {1u, 1u};
+    if (enc(&gp.ta[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, tp.xct, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return LOKA_ERR_CUDA;
+    gp.tb[0] = gp.ta[0];
+  }
+  if (!make_map_out(&gp.ty[0], tp.sb, K, K, K, LOKA_F32, 128, 32u)) return LOKA_ERR_CUDA;
+  GroupDesc& d = gp.g[0];
+  d.M = (int32_t)K;
+  d.N = (int32_t)K;
+  d.K = (int32_t)B;
+  d.tiles_n = (int32_t)cdiv(K, 256);
+  d.sa = tp.one;
+  d.sa_row = 0;
+  d.sb = tp.one;
+  d.sb_row = 0;
+  d.out_dtype = LOKA_F32;
+  d.ksplit = 1;
+  float* part = reinterpret_cast<float*>(base + w.part);
+  if (w.ksplit > 1) {
+    d.ksplit = w.ksplit;
+    d.kb_per_split = w.kbps;
+    if (!make_map_out(&gp.tp[0], part, (int64_t)w.ksplit * K, K, K, LOKA_F32, 128, 32u)) return LOKA_ERR_CUDA;
+  }
+  gp.tile_start[1] = (int32_t)(cdiv(K, 256) * d.tiles_n * d.ksplit);
+  if (launch_grouped2_bf16(gp, sms, s) != cudaSuccess) return LOKA_ERR_CUDA;
+  if (w.ksplit > 1 && launch_splitk_reduce(d, part, tp.sb, K, s) != cudaSuccess) return LOKA_ERR_CUDA;
+  if (launch_track_merge(tp, s) != cudaSuccess) return LOKA_ERR_CUDA;
+  st->n += B;
+  return LOKA_OK;
 }
 
 loka_status loka_probe_error(int32_t L, const loka_probe_pair* pairs, double floor_rel, loka_probe_stats* stats_dev,

@@ -317,6 +317,23 @@ LOKA_DEVINL void mma_f8f6f4_cg2(uint32_t tmem_d, uint64_t da, uint64_t db, uint3
       "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// BF16 x BF16 -> FP32 pair MMA (kind::f16, K = 16 per instruction = 32 bytes of a 128-byte row)
+LOKA_DEVINL uint32_t idesc_bf16(uint32_t M, uint32_t N) {
+  uint32_t d = 0;
+  d |= 1u << 4;   // D format F32
+  d |= 1u << 7;   // A format BF16
+  d |= 1u << 10;  // B format BF16
+  d |= (N >> 3) << 17;
+  d |= (M >> 4) << 24;
+  return d;
+}
+LOKA_DEVINL void mma_bf16_cg2(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 // block-scaled (UE8M0 per 32-K) variant of the pair MMA; scale factors in each CTA's TMEM
 LOKA_DEVINL void mma_mxf8f6f4_cg2(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t tsfa,
                                   uint32_t tsfb, uint32_t k, uint32_t accumulate) {

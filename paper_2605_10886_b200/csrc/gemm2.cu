@@ -36,7 +36,11 @@ constexpr int k2OffBar = k2OffCol + 2 * 2 * 256 * 4;
 constexpr int k2Smem = k2OffBar + 256 + 1024;
 static_assert(k2Smem <= 227 * 1024, "gemm2 smem");
 
+// BF16IN: BF16 operands (kind::f16; a 128-byte stage row holds 64 K elements) — the probe
+// tracker's scatter GEMM (NEXT-2); otherwise FP8 (kind::f8f6f4, 128 K elements per row).
+template <bool BF16IN>
 __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_constant__ GroupedParams gp) {
+  constexpr int kKE = BF16IN ? 64 : 128;  // K elements per 128-byte stage row
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -89,7 +93,7 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
     nb = local - mb * tn;
   };
   auto krange = [&](int g, int ks, int& kb0, int& kb1) {
-    const int nkb = (gp.g[g].K + 127) / 128;
+    const int nkb = (gp.g[g].K + kKE - 1) / kKE;
     if (gp.g[g].ksplit > 1) {
       kb0 = ks * gp.g[g].kb_per_split;
       kb1 = min(nkb, kb0 + gp.g[g].kb_per_split);
@@ -114,8 +118,8 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
           const uint32_t ph = (uint32_t)(it / k2Stages) & 1u;
           mbar_wait(&empty_bar[s], ph ^ 1u, 1);
           if (rank == 0) mbar_arrive_expect_tx(&full_bar[s], 2u * (k2StageA + k2StageB));
-          tma_load_2d_cg2(sA + s * k2StageA, &gp.ta[g], full0 + 8u * s, kb * 128, mb * 256 + rank * 128);
-          tma_load_2d_cg2(sB + s * k2StageB, &gp.tb[g], full0 + 8u * s, kb * 128, nb * 256 + rank * 128);
+          tma_load_2d_cg2(sA + s * k2StageA, &gp.ta[g], full0 + 8u * s, kb * kKE, mb * 256 + rank * 128);
+          tma_load_2d_cg2(sB + s * k2StageB, &gp.tb[g], full0 + 8u * s, kb * kKE, nb * 256 + rank * 128);
         }
       }
     }
@@ -132,7 +136,7 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
         const int buf = j & 1;
         mbar_wait(&acc_empty[buf], ((uint32_t)(j >> 1) & 1u) ^ 1u, 4);  // both CTAs drained it
         tc_fence_after();
-        const uint32_t idesc = idesc_f8f6f4(gp.g[g].a_fmt, gp.g[g].b_fmt, 256, 256);
+        const uint32_t idesc = BF16IN ? idesc_bf16(256, 256) : idesc_f8f6f4(gp.g[g].a_fmt, gp.g[g].b_fmt, 256, 256);
         const uint32_t dacc = tmem_base + (uint32_t)(buf * 256);
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % k2Stages;
@@ -143,8 +147,12 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
           const uint32_t b0 = smem_u32(sB + s * k2StageB);
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            mma_f8f6f4_cg2(dacc, smem_desc_kmajor_sw128(a0 + k * 32), smem_desc_kmajor_sw128(b0 + k * 32), idesc,
+            if constexpr (BF16IN)
+              mma_bf16_cg2(dacc, smem_desc_kmajor_sw128(a0 + k * 32), smem_desc_kmajor_sw128(b0 + k * 32), idesc,
                            (kb > kb0 || k) ? 1u : 0u);
+            else
+              mma_f8f6f4_cg2(dacc, smem_desc_kmajor_sw128(a0 + k * 32), smem_desc_kmajor_sw128(b0 + k * 32), idesc,
+                             (kb > kb0 || k) ? 1u : 0u);
           mma_commit_cg2_mc(&empty_bar[s], 3);
         }
         mma_commit_cg2_mc(&acc_full[buf], 3);
@@ -549,10 +557,11 @@ cudaError_t launch_splitk_reduce(const GroupDesc& d, const float* part, void* y,
   return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel, d, part, y, ldy);
 }
 
-cudaError_t launch_grouped2(const GroupedParams& gp, int num_sms, cudaStream_t st) {
+template <bool BF16IN>
+static cudaError_t launch_grouped2_t(const GroupedParams& gp, int num_sms, cudaStream_t st) {
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(grouped2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, k2Smem);
+    cudaError_t e = cudaFuncSetAttribute(grouped2_kernel<BF16IN>, cudaFuncAttributeMaxDynamicSharedMemorySize, k2Smem);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
@@ -572,9 +581,15 @@ cudaError_t launch_grouped2(const GroupedParams& gp, int num_sms, cudaStream_t s
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, grouped2_kernel, gp);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, grouped2_kernel<BF16IN>, gp);
   note_launch();
   return e;
+}
+cudaError_t launch_grouped2(const GroupedParams& gp, int num_sms, cudaStream_t st) {
+  return launch_grouped2_t<false>(gp, num_sms, st);
+}
+cudaError_t launch_grouped2_bf16(const GroupedParams& gp, int num_sms, cudaStream_t st) {
+  return launch_grouped2_t<true>(gp, num_sms, st);
 }
 
 }  // namespace loka

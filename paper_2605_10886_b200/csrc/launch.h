@@ -167,6 +167,27 @@ cudaError_t launch_grouped(const GroupedParams& gp, int num_sms, cudaStream_t st
 // CTA-pair variant (gemm2.cu): tiles 256 x 256 (tiles_n = ceil(N/256), tile_start counts them);
 // ta/tb boxes {128, 128}; ty box {128 bytes, 32 rows}, SW128; bf16 / f32 output.
 cudaError_t launch_grouped2(const GroupedParams& gp, int num_sms, cudaStream_t st);
+// the same engine on BF16 operands (K-major, 64 elements per stage row): FP32 C = A . B^T (sa = sb =
+// pointers to 1.0f, tensor scales), bf16 / f32 output
+cudaError_t launch_grouped2_bf16(const GroupedParams& gp, int num_sms, cudaStream_t st);
+
+// ---- NEXT-2 input tracker (track.cu): batched Welford merge of one bf16 batch X [B, K] ----
+struct TrackParams {
+  const __nv_bfloat16* x; int64_t ldx;
+  int64_t B, K;
+  float* mean;             // [K] tracked mean (updated in place)
+  float* scatter;          // [K, K] tracked unnormalised scatter (updated in place)
+  int64_t n_old;
+  float* colpart;          // ws [nchunk][K] column partial sums
+  float* delta;            // ws [K]
+  float* one;              // ws [1] = 1.0f (GEMM tensor scales)
+  __nv_bfloat16* xct;      // ws [K, ldxct] centred transpose
+  int64_t ldxct;
+  float* sb;               // ws [K, K] batch scatter
+  int32_t nchunk;
+};
+cudaError_t launch_track_prep(const TrackParams& p, cudaStream_t st);   // column means, delta, mean update, Xc^T
+cudaError_t launch_track_merge(const TrackParams& p, cudaStream_t st);  // scatter += S_b + c delta delta^T
 // Native block-scaled (UE8M0 blockwise, MX) problem on the CTA pair (gemm2.cu): 256 x 256 tiles,
 // kind::mxf8f6f4.block_scale with cta_group::2; scale atoms TMA-loaded from the sfpack layout
 // viewed as rows of 256 B (maps tsa / tsb, box {256, 2} = one 512 B atom).  Plain epilogue
