@@ -180,6 +180,12 @@ typedef struct loka_linear_args {
   void* save_xhat;
   int64_t save_xhat_ld;
   float* save_rstd;
+  /* NEXT-4: producer-side tensor amax.  Nullable device float, zeroed by the
+     caller: the epilogue folds max |y| over the values it stores (after their rounding to the
+     output dtype; F32 / BF16 outputs) into it (atomicMax on the IEEE bit pattern), so the next
+     layer's tensorwise quantize can skip its amax pass (LOKA_PHASE_CAST_WITH_AMAX), and a data-
+     parallel job all-reduces this word instead (a9).  Non-finite outputs raise it to Inf/NaN.    */
+  float* amax_out;
 } loka_linear_args;
 
 /* Y = epilogue(A . B^T): acc(FP32, TMEM) -> y = acc*sa[m]*sb[n] (+bias[n]) -> norm -> act -> cast.

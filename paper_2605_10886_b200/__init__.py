@@ -54,7 +54,8 @@ class loka_linear_args(C.Structure):
                 ("norm", C.c_int), ("norm_block", C.c_int32), ("eps", C.c_float), ("gamma", C.c_void_p),
                 ("beta", C.c_void_p), ("y", loka_tensor), ("debug_precast", C.c_void_p), ("status_dev", C.c_void_p),
                 ("act", C.c_int), ("bwd_xhat", C.c_void_p), ("bwd_xhat_ld", C.c_int64), ("bwd_rstd", C.c_void_p),
-                ("save_xhat", C.c_void_p), ("save_xhat_ld", C.c_int64), ("save_rstd", C.c_void_p)]
+                ("save_xhat", C.c_void_p), ("save_xhat_ld", C.c_int64), ("save_rstd", C.c_void_p),
+                ("amax_out", C.c_void_p)]
 
 
 class loka_stack_args(C.Structure):
@@ -190,7 +191,7 @@ def loka_quantize(x: torch.Tensor, fmt: str = "e4m3", gran: str = "row", scale_f
 
 def make_linear_args(a, a_scales, b, b_scales, *, a_fmt="e4m3", b_fmt="e4m3", a_gran="row", b_gran="row",
                      a_scale_fmt="f32", b_scale_fmt="f32", norm="none", act="none", bwd_xhat=None, bwd_rstd=None,
-                     save_xhat=None, save_rstd=None, norm_block=256, eps=0.0, gamma=None, beta=None, bias=None, out_dtype="f32",
+                     save_xhat=None, save_rstd=None, amax_out=None, norm_block=256, eps=0.0, gamma=None, beta=None, bias=None, out_dtype="f32",
                      y=None, y_scales=None, precast=None, status=None, direction="fwd", keep=None):
     """Build a loka_linear_args for C = A . B^T (A [M,K], B [N,K] FP8 codes, K-major)."""
     M, K = a.shape
@@ -220,9 +221,11 @@ def make_linear_args(a, a_scales, b, b_scales, *, a_fmt="e4m3", b_fmt="e4m3", a_
         args.save_xhat, args.save_xhat_ld = save_xhat.data_ptr(), save_xhat.stride(0)
     if save_rstd is not None:
         args.save_rstd = save_rstd.data_ptr()
+    if amax_out is not None:
+        args.amax_out = amax_out.data_ptr()
     if keep is not None:  # keep python references alive as long as args is used
         keep.extend([a, a_scales, b, b_scales, bias, gamma, beta, y, y_scales, precast, status, bwd_xhat, bwd_rstd,
-                     save_xhat, save_rstd])
+                     save_xhat, save_rstd, amax_out])
     return args, y, y_scales
 
 

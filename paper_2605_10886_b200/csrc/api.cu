@@ -345,6 +345,7 @@ static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CU
   if (a->save_xhat && ((a->save_xhat_ld * 2) % 16 || a->save_xhat_ld < N || !aligned16(a->save_xhat)))
     return LOKA_ERR_INVALID_ARG;
   if ((a->save_xhat || a->save_rstd) && a->norm == LOKA_NORM_NONE) return LOKA_ERR_INVALID_ARG;
+  if (a->amax_out && (fp8_out || (reinterpret_cast<uintptr_t>(a->amax_out) & 3))) return LOKA_ERR_INVALID_ARG;
 
   // Tile width BN in {64,128,256}: the widest tile that still gives >= ~120 CTAs (most of the
   // 148 SMs) for this M, else the narrowest allowed.  Row-coupled epilogues (full-row norm or an
@@ -413,6 +414,7 @@ static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CU
   p->save_xhat = static_cast<__nv_bfloat16*>(a->save_xhat);
   p->ld_save_xhat = a->save_xhat_ld;
   p->save_rstd = a->save_rstd;
+  p->amax_out = a->amax_out;
   *bn_out = bn;
   return LOKA_OK;
 }
@@ -439,7 +441,7 @@ static loka_status prepare_bw(const loka_linear_args* a, CUtensorMap* ta, CUtens
   const bool fp8_out = is_fp8(Y.dtype);
   if (fp8_out && (!Y.scales || Y.gran != LOKA_GRAN_ROW || N > 128)) return LOKA_ERR_UNSUPPORTED;
   if (a->norm != LOKA_NORM_NONE || a->gamma || a->beta || a->act != LOKA_ACT_NONE || a->bwd_xhat || a->save_xhat ||
-      a->save_rstd)
+      a->save_rstd || a->amax_out)
     return LOKA_ERR_UNSUPPORTED;
   if (a->bias && a->bias_dtype != LOKA_F32 && a->bias_dtype != LOKA_BF16) return LOKA_ERR_INVALID_ARG;
   if (!make_map_u8(ta, A.data, M, K, A.ld, 128)) return LOKA_ERR_CUDA;
@@ -577,6 +579,7 @@ static loka_status run_mx_pair(const loka_linear_args* a, void* ws, size_t ws_by
   d.bias = a->bias;
   d.bias_bf16 = a->bias_dtype == LOKA_BF16;
   d.out_dtype = Y.dtype;
+  d.amax_out = a->amax_out;
   d.ksplit = 1;
   mp.sf_kbs = (int32_t)kbs;
   mp.tiles = (int32_t)(cdiv(a->M, 256) * d.tiles_n);
@@ -620,6 +623,7 @@ static loka_status run_wide_norm(const loka_linear_args* a, void* ws, size_t ws_
   g.y.dtype = LOKA_F32;
   g.y.ld = a->N;
   g.y.scales = nullptr;
+  g.amax_out = nullptr;  // (the amax is of the normalised output: the row pass folds it)
   loka_status st = loka_grouped_fp8_linear(1, &g, nullptr, 0, reinterpret_cast<loka_stream_t>(s));
   if (st != LOKA_OK) return st;
   int sms = 148;
@@ -643,6 +647,7 @@ static loka_status run_wide_norm(const loka_linear_args* a, void* ws, size_t ws_
   rp.precast = a->debug_precast;
   rp.ld_pre = a->N;
   rp.status = a->status_dev;
+  rp.amax_out = a->amax_out;
   if (a->bwd_xhat) {
     if (!a->bwd_rstd || (a->bwd_xhat_ld * 2) % 16 || a->bwd_xhat_ld < a->N || !aligned16(a->bwd_xhat))
       return LOKA_ERR_INVALID_ARG;
@@ -850,6 +855,7 @@ loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* 
       d.bias = q.bias;
       d.bias_bf16 = q.bias_dtype == LOKA_BF16;
       d.out_dtype = q.y.dtype;
+      d.amax_out = q.amax_out;
       d.ksplit = 1;
       if (ksplit > 1) {  // G == 1
         d.ksplit = ksplit;

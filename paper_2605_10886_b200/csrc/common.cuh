@@ -119,6 +119,15 @@ LOKA_DEVINL float4 lds_f4(uint32_t saddr) {
   asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(saddr));
   return v;
 }
+// NEXT-4: fold a thread's max |v| into a device float by warp reduction + one atomicMax of the
+// IEEE bit pattern (non-negative floats order like their bits; NaN > Inf > finite).  Whole warp.
+LOKA_DEVINL void warp_amax_to(float* dst, float m) {
+  uint32_t b = __float_as_uint(m) & 0x7FFFFFFFu;
+  b = __reduce_max_sync(0xFFFFFFFFu, b);
+  if ((threadIdx.x & 31) == 0 && b) atomicMax(reinterpret_cast<unsigned int*>(dst), b);
+}
+// value as stored in the output dtype (bf16 rounding) for the producer amax
+LOKA_DEVINL float stored_bf16(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
 // named barrier among `n` threads (id 1..15; id 0 is __syncthreads)
 LOKA_DEVINL void named_bar_sync(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");

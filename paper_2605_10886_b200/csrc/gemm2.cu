@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
       const int cpb = 128 / esz;  // columns per 128-byte box row
       const int col0 = nb * 256 + h * 128;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * 256 + h * 128);
+      float amx = 0.f;  // NEXT-4 producer amax of this warp's stored values
 #pragma unroll 1
       for (int cb = 0; cb < 128; cb += 32) {
         float y[32];
@@ -217,6 +218,11 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
           const float2 b = fadd2(fmul2(make_float2(y[c + 2], y[c + 3]), fmul2(sa2, make_float2(s4.z, s4.w))),
                                  make_float2(b4.z, b4.w));
           y[c] = a.x; y[c + 1] = a.y; y[c + 2] = b.x; y[c + 3] = b.y;
+        }
+        if (d.amax_out && !split && grow < d.M) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (col0 + cb + c < d.N) amx = fmaxf(amx, fabsf(esz == 2 ? stored_bf16(y[c]) : y[c]));
         }
         const int in_box = cb % cpb;  // first column of this chunk inside its box
         uint8_t* box = stg + (nbox & 1) * 4096;
@@ -258,6 +264,7 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
           ++nbox;
         }
       }
+      if (d.amax_out && !split) warp_amax_to(d.amax_out, amx);
     }
     if (lane == 0) bulk_wait0();
   }
@@ -418,6 +425,7 @@ __global__ void __launch_bounds__(k2Threads, 1) mx_pair_kernel(const __grid_cons
       if (lane == 0) mbar_arrive_cluster(acc_empty0);
       const int row0 = mb * 256 + rank * 128 + q * 32;
       const int col0 = nb * 256 + h * 128;
+      float amx = 0.f;
 #pragma unroll
       for (int cb = 0; cb < 128; cb += 32) {
         float* yc = y + cb;
@@ -430,6 +438,11 @@ __global__ void __launch_bounds__(k2Threads, 1) mx_pair_kernel(const __grid_cons
             const float2 b = fadd2(make_float2(yc[c + 2], yc[c + 3]), make_float2(b4.z, b4.w));
             yc[c] = a.x; yc[c + 1] = a.y; yc[c + 2] = b.x; yc[c + 3] = b.y;
           }
+        }
+        if (d.amax_out && row0 + lane < d.M) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (col0 + cb + c < d.N) amx = fmaxf(amx, fabsf(esz == 2 ? stored_bf16(yc[c]) : yc[c]));
         }
         const int in_box = cb % cpb;
         uint8_t* box = stg + (nbox & 1) * 4096;
@@ -468,6 +481,7 @@ __global__ void __launch_bounds__(k2Threads, 1) mx_pair_kernel(const __grid_cons
           ++nbox;
         }
       }
+      if (d.amax_out) warp_amax_to(d.amax_out, amx);
     }
     if (lane == 0) bulk_wait0();
   }
@@ -513,6 +527,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const GroupDesc d, c
                                                             void* y, int64_t ldy) {
   pdl_wait();
   const int64_t n4 = d.N / 4, total = (int64_t)d.M * n4, slice = (int64_t)d.M * d.N;
+  float amx = 0.f;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t m = i / n4;
     const int n = (int)(i - m * n4) * 4;
@@ -530,6 +545,8 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const GroupDesc d, c
         o[k] += d.bias_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(d.bias)[n + k])
                             : reinterpret_cast<const float*>(d.bias)[n + k];
     }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) amx = fmaxf(amx, fabsf(d.out_dtype == LOKA_F32 ? o[k] : stored_bf16(o[k])));
     if (d.out_dtype == LOKA_F32) {
       *reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + m * ldy + n) = make_float4(o[0], o[1], o[2], o[3]);
     } else {
@@ -538,6 +555,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const GroupDesc d, c
           make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
     }
   }
+  if (d.amax_out) warp_amax_to(d.amax_out, amx);
 }
 
 cudaError_t launch_splitk_reduce(const GroupDesc& d, const float* part, void* y, int64_t ldy, cudaStream_t st) {

@@ -75,6 +75,7 @@ struct LinearParams {
   const float* rstd_in;
   __nv_bfloat16* save_xhat; int64_t ld_save_xhat;
   float* save_rstd;
+  float* amax_out;               // NEXT-4: atomicMax of |stored y| (bit pattern), nullable
   // native block-scaled (MX) mode: UE8M0 blockwise scales applied by the tensor core; sa/sb unused
   int32_t mx;
   const uint8_t* sfa_pack;       // [ceil(M/128)][kblocks][512] (sfpack.cu layout)
@@ -155,6 +156,7 @@ struct GroupDesc {
   // split-K (CTA-pair engine only): ksplit slices of kb_per_split 128-K blocks; each writes its raw
   // FP32 accumulator to the [ksplit][M][N] partial buffer (map tp), reduced by splitk_reduce
   int32_t ksplit, kb_per_split;
+  float* amax_out;  // NEXT-4: atomicMax of |stored y| (bit pattern), nullable
 };
 struct GroupedParams {
   CUtensorMap ta[kMaxGroups], tb[kMaxGroups], ty[kMaxGroups];  // A box {128,128}, B box {128,128}, Y out
@@ -214,6 +216,7 @@ struct RowNormParams {
   int32_t bwd, block;
   const __nv_bfloat16* xhat; int64_t ld_xhat;
   const float* rstd_in;
+  float* amax_out;  // NEXT-4, nullable
 };
 cudaError_t launch_rownorm(const RowNormParams& p, int num_sms, cudaStream_t st);
 // y[m,n] = (sum_s part[s][m][n]) * s_a[m] * s_b[n] (+ bias[n]) -> y (bf16 / f32)

@@ -623,6 +623,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     // row r lives at b*16K + r*128 + ((c ^ (r & 7)) << 4), the TMA SWIZZLE_128B pattern, so the
     // 8 rows a quarter-warp writes land in 8 different bank groups (conflict-free) and the global
     // writes are whole 128-byte lines (OOB rows / columns are clipped by the TMA unit).
+    if (p.amax_out) {  // NEXT-4: producer-side tensor amax over the stored values
+      float m = 0.f;
+#pragma unroll
+      for (int j = 0; j < CPT; ++j)
+        if (j < nv && row_ok) m = fmaxf(m, fabsf(p.out_dtype == LOKA_BF16 ? stored_bf16(y[j]) : y[j]));
+      warp_amax_to(p.amax_out, m);
+    }
     if (p.precast && row_ok) {
       float* dst = p.precast + (int64_t)grow * p.ld_pre + n0 + cb;
 #pragma unroll

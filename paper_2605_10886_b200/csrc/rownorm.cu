@@ -36,7 +36,16 @@ __global__ void __launch_bounds__(256) rownorm_kernel(const RowNormParams p) {
     for (int w = 0; w < 8; ++w) r += red[w];
     return r;
   };
+  float amx_out = 0.f;  // NEXT-4 producer amax over the stored values of this thread's rows
   auto rowout = [&](int64_t row, float (&v)[8 * V], const bool (&ok)[V], float amax) {
+      if (p.amax_out) {
+#pragma unroll
+        for (int u = 0; u < V; ++u)
+          if (ok[u])
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              amx_out = fmaxf(amx_out, fabsf(p.out_dtype == LOKA_BF16 ? stored_bf16(v[8 * u + k]) : v[8 * u + k]));
+      }
       const bool fp8 = p.out_dtype == LOKA_E4M3 || p.out_dtype == LOKA_E5M2;
       float r_out = 1.f;
       if (fp8) {
@@ -222,6 +231,7 @@ __global__ void __launch_bounds__(256) rownorm_kernel(const RowNormParams p) {
     }
     rowout(row, v, ok, amax);
   }
+  if (p.amax_out) warp_amax_to(p.amax_out, amx_out);
 }
 
 cudaError_t launch_rownorm(const RowNormParams& p, int num_sms, cudaStream_t st) {
