@@ -52,7 +52,8 @@ typedef enum loka_status {
   LOKA_ERR_UNSUPPORTED = 3, /* not sm_100, or a combination this build does not implement     */
   LOKA_ERR_NONFINITE = 4,   /* (host-visible form of the device status bit)                  */
   LOKA_ERR_WORKSPACE = 5,   /* workspace pointer null or smaller than loka_*_workspace_size() */
-  LOKA_ERR_CUDA = 6         /* a CUDA runtime call or launch failed                           */
+  LOKA_ERR_CUDA = 6,        /* a CUDA runtime call or launch failed                           */
+  LOKA_ERR_NOT_PD = 7       /* Cholesky: not positive definite after the jitter escalation    */
 } loka_status;
 
 #define LOKA_DEVSTATUS_NONFINITE 0x1 /* OR'ed into *status_dev when an input holds NaN/Inf */
@@ -276,6 +277,67 @@ typedef struct loka_welford_state {
 LOKA_API size_t loka_probe_track_workspace_size(const loka_welford_state* st, int64_t B);
 LOKA_API loka_status loka_probe_track_input(loka_welford_state* st, const loka_tensor* x, void* ws, size_t ws_bytes,
                                            loka_stream_t stream);
+
+/* ---- NEXT-3: LoKA Probe weight tracker and learned-distribution sampling ----
+ * All matrices are FP32, row-major and dense (ld = number of columns unless an ld is passed),
+ * device pointers owned by the caller; calls are asynchronous on
+ * the stream unless stated.  Readings of the paper: DESIGN.md D30-D34.
+ *
+ * loka_philox_normal: out[e] = standard normal number (offset + e) of the stream keyed by seed:
+ * Philox4x64-10 (counter (b, 0, 0, 0), key (seed, 0)) for block b = (offset + e) / 4, Box-Muller on
+ * the top 24 bits of the word pairs (x0, x1) and (x2, x3) (D31); FP32.  n >= 0.        */
+LOKA_API loka_status loka_philox_normal(uint64_t seed, uint64_t offset, int64_t n, float* out, loka_stream_t stream);
+
+/* loka_cholesky_jittered (PAPER.md:377-381 and its footnote): l = lower Cholesky factor of
+ * a_scale * (a + a^T)/2 + eps I, eps = eps_rel * trace(a_scale * a) / n (a non-positive trace
+ * uses scale 1, D30), escalated x10 up to `escalations` times while a pivot is not positive
+ * (SPEC.md:262).  a [n, n] (lda), l [n, n] (ldl, strict upper part zeroed) must not overlap.
+ * *eps_used (host) receives the eps of the successful factorisation.  SYNCHRONOUS: it reads the
+ * trace and the pivot status back (the factorisation itself runs on the device: 64-column
+ * panels, FP32).  LOKA_ERR_NOT_PD after the escalations.  ws >= loka_cholesky_workspace_size(). */
+LOKA_API size_t loka_cholesky_workspace_size(int64_t n);
+LOKA_API loka_status loka_cholesky_jittered(const float* a, int64_t lda, int64_t n, float a_scale, float eps_rel,
+                                            int32_t escalations, float* l, int64_t ldl, float* eps_used, void* ws,
+                                            size_t ws_bytes, loka_stream_t stream);
+
+/* Matrix-normal weight tracker: W [M, N] ~ MN(mean, U, V).  mean [M, N],
+ * U [M, M], V [N, N] are the caller's device arrays (ld = M / N); count, momentum m and eps_rel
+ * are host fields.  loka_probe_track_weight_init sets mean = W, U = I, V = I, count = 0
+ * (SPEC.md:216).  loka_probe_track_weight applies one update in the paper's order
+ * (PAPER.md:319-348): eps_U = eps_rel tr(U)/M, eps_V = eps_rel tr(V)/N; W_c = W - mean;
+ * L_V L_V^T = V + eps_V I, W~ = W_c L_V^{-T}, U' = W~ W~^T / N; L_U L_U^T = U + eps_U I,
+ * W^ = L_U^{-1} W_c, V' = W^^T W^ / M; U = sym(m U + (1-m) U') + eps_U I, V likewise;
+ * s = tr(U)/M, U /= s, V *= s; mean = m mean + (1-m) W (D32-D34); count += 1.  W is F32 or BF16
+ * (any ld >= N).  No host synchronisation: a non-positive pivot sets bit 0 of *status_dev
+ * (nullable).  ws >= loka_probe_track_weight_workspace_size().                                 */
+typedef struct loka_matnorm_state {
+  int64_t M, N;
+  int64_t count;
+  float momentum;
+  float eps_rel;
+  float* mean;
+  float* U;
+  float* V;
+} loka_matnorm_state;
+LOKA_API loka_status loka_probe_track_weight_init(loka_matnorm_state* st, const loka_tensor* w, loka_stream_t stream);
+LOKA_API size_t loka_probe_track_weight_workspace_size(const loka_matnorm_state* st);
+LOKA_API loka_status loka_probe_track_weight(loka_matnorm_state* st, const loka_tensor* w, int32_t* status_dev,
+                                             void* ws, size_t ws_bytes, loka_stream_t stream);
+
+/* Sampling learned distributions, Z from loka_philox_normal's stream:
+ *   loka_probe_sample_input:  out [B, K] = 1 mean^T + Z L_Sigma^T, Z [B, K] row-major (elements
+ *                             offset .. offset + B K - 1 of the stream);
+ *   loka_probe_sample_weight: out [M, N] = mean + L_U (Z L_V^T), Z [M, N] row-major.
+ * L_* are lower-triangular factors with a ZERO strict upper part (as loka_cholesky_jittered
+ * writes them; the GEMMs skip the zero tiles but read inside the diagonal tiles).  out: F32 or BF16, rows x cols = B x K / M x N, any ld >= cols.
+ * ws >= loka_probe_sample_workspace_size(rows, cols, is_weight).                               */
+LOKA_API size_t loka_probe_sample_workspace_size(int64_t rows, int64_t cols, int32_t is_weight);
+LOKA_API loka_status loka_probe_sample_input(const float* mean, const float* l_sigma, int64_t K, int64_t B,
+                                             uint64_t seed, uint64_t offset, loka_tensor* out, void* ws,
+                                             size_t ws_bytes, loka_stream_t stream);
+LOKA_API loka_status loka_probe_sample_weight(const float* mean, const float* l_u, const float* l_v, int64_t M,
+                                              int64_t N, uint64_t seed, uint64_t offset, loka_tensor* out, void* ws,
+                                              size_t ws_bytes, loka_stream_t stream);
 
 /* ---- a8: LoKA Dispatch (host) -------------------------------------------------------------- */
 typedef struct loka_candidate {

@@ -68,6 +68,11 @@ class loka_welford_state(C.Structure):
     _fields_ = [("n", C.c_int64), ("K", C.c_int64), ("mean", C.c_void_p), ("scatter", C.c_void_p)]
 
 
+class loka_matnorm_state(C.Structure):
+    _fields_ = [("M", C.c_int64), ("N", C.c_int64), ("count", C.c_int64), ("momentum", C.c_float),
+                ("eps_rel", C.c_float), ("mean", C.c_void_p), ("U", C.c_void_p), ("V", C.c_void_p)]
+
+
 class loka_probe_pair(C.Structure):
     _fields_ = [("out", C.c_void_p), ("out_dtype", C.c_int), ("ref", C.c_void_p), ("ref_dtype", C.c_int),
                 ("M", C.c_int64), ("N", C.c_int64), ("ld_out", C.c_int64), ("ld_ref", C.c_int64)]
@@ -107,6 +112,19 @@ _sig = {
     "loka_stack_workspace_size": ([_P(loka_stack_args)], C.c_size_t),
     "loka_probe_track_workspace_size": ([_P(loka_welford_state), C.c_int64], C.c_size_t),
     "loka_probe_track_input": ([_P(loka_welford_state), _P(loka_tensor), C.c_void_p, C.c_size_t, C.c_void_p], C.c_int),
+    "loka_philox_normal": ([C.c_uint64, C.c_uint64, C.c_int64, C.c_void_p, C.c_void_p], C.c_int),
+    "loka_cholesky_workspace_size": ([C.c_int64], C.c_size_t),
+    "loka_cholesky_jittered": ([C.c_void_p, C.c_int64, C.c_int64, C.c_float, C.c_float, C.c_int32, C.c_void_p,
+                                C.c_int64, _P(C.c_float), C.c_void_p, C.c_size_t, C.c_void_p], C.c_int),
+    "loka_probe_track_weight_init": ([_P(loka_matnorm_state), _P(loka_tensor), C.c_void_p], C.c_int),
+    "loka_probe_track_weight_workspace_size": ([_P(loka_matnorm_state)], C.c_size_t),
+    "loka_probe_track_weight": ([_P(loka_matnorm_state), _P(loka_tensor), C.c_void_p, C.c_void_p, C.c_size_t,
+                                 C.c_void_p], C.c_int),
+    "loka_probe_sample_workspace_size": ([C.c_int64, C.c_int64, C.c_int32], C.c_size_t),
+    "loka_probe_sample_input": ([C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_uint64, C.c_uint64,
+                                 _P(loka_tensor), C.c_void_p, C.c_size_t, C.c_void_p], C.c_int),
+    "loka_probe_sample_weight": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_uint64, C.c_uint64,
+                                  _P(loka_tensor), C.c_void_p, C.c_size_t, C.c_void_p], C.c_int),
 }
 for _name, (_args, _ret) in _sig.items():
     _fn = getattr(_lib, _name)
@@ -415,3 +433,122 @@ class InputTracker:
 
     def covariance(self) -> torch.Tensor:
         return self.scatter / (self.n - 1)
+
+    def factor(self, eps_rel: float = 1e-6, escalations: int = 4, stream=None):
+        """(L_Sigma, eps): jittered Cholesky of the unbiased covariance Sigma / (n - 1),
+        the 1/(n-1) applied inside the factorisation kernel.  Synchronous (reads the pivot status)."""
+        if self.n < 2:
+            raise ValueError("the covariance needs n > 1 (PAPER.md:301)")
+        return cholesky_jittered(self.scatter, eps_rel, escalations, a_scale=1.0 / (self.n - 1), stream=stream)
+
+    def sample(self, b: int, seed: int, offset: int = 0, eps_rel: float = 1e-6, out_dtype=torch.float32, stream=None):
+        """T' = 1 mu^T + Z L_Sigma^T from the tracked statistics."""
+        l_sigma, _ = self.factor(eps_rel, stream=stream)
+        return sample_input(self.mean, l_sigma, b, seed, offset, out_dtype, stream)
+
+
+# ---- NEXT-3: weight tracker and learned-distribution sampling (PAPER.md:307-393) ----------------
+_ws_cache = {}
+
+
+def _scratch(nbytes: int, device, tag: str):
+    key = (tag, str(device))
+    t = _ws_cache.get(key)
+    if t is None or t.numel() < nbytes:
+        t = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=device)
+        _ws_cache[key] = t
+    return t
+
+
+def philox_normal(n: int, seed: int, offset: int = 0, device=None, out=None, stream=None) -> torch.Tensor:
+    """n standard normals of the Philox4x64-10 stream (seed, offset) (loka_philox_normal, D31)."""
+    dev = torch.device("cuda") if device is None else torch.device(device)
+    if out is None:
+        out = torch.empty(n, dtype=torch.float32, device=dev)
+    _check(_lib.loka_philox_normal(seed & (2**64 - 1), offset, n, _ptr(out), _stream(stream)), "loka_philox_normal")
+    return out
+
+
+def cholesky_jittered(a: torch.Tensor, eps_rel: float = 1e-6, escalations: int = 4, a_scale: float = 1.0,
+                      out=None, stream=None):
+    """(L, eps_used) with L L^T = a_scale sym(a) + eps I (loka_cholesky_jittered; synchronous)."""
+    assert a.dtype == torch.float32 and a.dim() == 2 and a.shape[0] == a.shape[1] and a.stride(1) == 1
+    n = a.shape[0]
+    if out is None:
+        out = torch.empty(n, n, dtype=torch.float32, device=a.device)
+    ws = _scratch(int(_lib.loka_cholesky_workspace_size(n)), a.device, "chol")
+    eps = C.c_float(0.0)
+    _check(_lib.loka_cholesky_jittered(_ptr(a), a.stride(0), n, a_scale, eps_rel, escalations, _ptr(out),
+                                       out.stride(0), C.byref(eps), _ptr(ws), ws.numel(), _stream(stream)),
+           "loka_cholesky_jittered")
+    return out, float(eps.value)
+
+
+def _sample_out(rows, cols, out_dtype, device, out):
+    if out is None:
+        out = torch.empty(rows, cols, dtype=out_dtype, device=device)
+    assert out.dim() == 2 and out.stride(1) == 1 and tuple(out.shape) == (rows, cols)
+    return out, _tensor(out, _dtype_code(out), rows, cols, ld=out.stride(0))
+
+
+def sample_input(mean: torch.Tensor, l_sigma: torch.Tensor, b: int, seed: int, offset: int = 0,
+                 out_dtype=torch.float32, stream=None, out=None) -> torch.Tensor:
+    """T' = 1 mean^T + Z L_Sigma^T (loka_probe_sample_input)."""
+    k = mean.numel()
+    assert mean.is_contiguous() and l_sigma.is_contiguous() and tuple(l_sigma.shape) == (k, k)
+    out, t = _sample_out(b, k, out_dtype, mean.device, out)
+    ws = _scratch(int(_lib.loka_probe_sample_workspace_size(b, k, 0)), mean.device, "sample")
+    _check(_lib.loka_probe_sample_input(_ptr(mean), _ptr(l_sigma), k, b, seed & (2**64 - 1), offset, C.byref(t),
+                                        _ptr(ws), ws.numel(), _stream(stream)), "loka_probe_sample_input")
+    return out
+
+
+def sample_weight(mean: torch.Tensor, l_u: torch.Tensor, l_v: torch.Tensor, seed: int, offset: int = 0,
+                  out_dtype=torch.float32, stream=None, out=None) -> torch.Tensor:
+    """W' = mean + L_U Z L_V^T (loka_probe_sample_weight)."""
+    m, n = mean.shape
+    assert mean.is_contiguous() and l_u.is_contiguous() and l_v.is_contiguous()
+    assert tuple(l_u.shape) == (m, m) and tuple(l_v.shape) == (n, n)
+    out, t = _sample_out(m, n, out_dtype, mean.device, out)
+    ws = _scratch(int(_lib.loka_probe_sample_workspace_size(m, n, 1)), mean.device, "sample")
+    _check(_lib.loka_probe_sample_weight(_ptr(mean), _ptr(l_u), _ptr(l_v), m, n, seed & (2**64 - 1), offset,
+                                         C.byref(t), _ptr(ws), ws.numel(), _stream(stream)), "loka_probe_sample_weight")
+    return out
+
+
+class WeightTracker:
+    """NEXT-3: matrix-normal tracker of one weight W [M, N] ~ MN(mean, U, V) on the
+    device (FP32), wrapping loka_probe_track_weight_init / loka_probe_track_weight."""
+
+    def __init__(self, w0: torch.Tensor, momentum: float = 0.95, eps_rel: float = 1e-6, stream=None):
+        assert w0.dim() == 2 and w0.stride(1) == 1 and w0.dtype in (torch.float32, torch.bfloat16)
+        m, n = w0.shape
+        dev = w0.device
+        self.mean = torch.empty(m, n, dtype=torch.float32, device=dev)
+        self.U = torch.empty(m, m, dtype=torch.float32, device=dev)
+        self.V = torch.empty(n, n, dtype=torch.float32, device=dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.state = loka_matnorm_state(m, n, 0, momentum, eps_rel, self.mean.data_ptr(), self.U.data_ptr(),
+                                        self.V.data_ptr())
+        t = _tensor(w0, _dtype_code(w0), m, n, ld=w0.stride(0))
+        _check(_lib.loka_probe_track_weight_init(C.byref(self.state), C.byref(t), _stream(stream)),
+               "loka_probe_track_weight_init")
+        self._ws = torch.empty(int(_lib.loka_probe_track_weight_workspace_size(C.byref(self.state))),
+                               dtype=torch.uint8, device=dev)
+
+    @property
+    def count(self) -> int:
+        return int(self.state.count)
+
+    def update(self, w: torch.Tensor, stream=None):
+        assert w.dim() == 2 and w.stride(1) == 1 and tuple(w.shape) == (self.state.M, self.state.N)
+        t = _tensor(w, _dtype_code(w), w.shape[0], w.shape[1], ld=w.stride(0))
+        _check(_lib.loka_probe_track_weight(C.byref(self.state), C.byref(t), _ptr(self.status),
+                                            C.c_void_p(self._ws.data_ptr()), self._ws.numel(), _stream(stream)),
+               "loka_probe_track_weight")
+
+    def sample(self, seed: int, offset: int = 0, eps_rel: float = 1e-6, out_dtype=torch.float32, stream=None):
+        """W' = mean + L_U Z L_V^T with L_U L_U^T = U + eps I, L_V L_V^T = V + eps I."""
+        l_u, _ = cholesky_jittered(self.U, eps_rel, stream=stream)
+        l_v, _ = cholesky_jittered(self.V, eps_rel, stream=stream)
+        return sample_weight(self.mean, l_u, l_v, seed, offset, out_dtype, stream)

@@ -133,6 +133,7 @@ const char* loka_status_string(loka_status s) {
     case LOKA_ERR_NONFINITE: return "non-finite input";
     case LOKA_ERR_WORKSPACE: return "workspace too small";
     case LOKA_ERR_CUDA: return "CUDA error";
+    case LOKA_ERR_NOT_PD: return "not positive definite after the jitter escalation";
   }
   return "unknown status";
 }
@@ -1008,6 +1009,198 @@ loka_status loka_probe_track_input(loka_welford_state* st, const loka_tensor* x,
   if (launch_track_merge(tp, s) != cudaSuccess) return LOKA_ERR_CUDA;
   st->n += B;
   return LOKA_OK;
+}
+
+// ---- NEXT-3: weight tracker and sampling (linalg.cu) -----------------------------------------
+loka_status loka_philox_normal(uint64_t seed, uint64_t offset, int64_t n, float* out, loka_stream_t stream) {
+  if (n < 0 || (n > 0 && !out)) return LOKA_ERR_INVALID_ARG;
+  if (n == 0) return LOKA_OK;
+  loka_status stt = check_device();
+  if (stt != LOKA_OK) return stt;
+  return launch_philox_normal(seed, offset, n, out, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? LOKA_OK : LOKA_ERR_CUDA;
+}
+
+size_t loka_cholesky_workspace_size(int64_t) { return 256; }
+
+loka_status loka_cholesky_jittered(const float* a, int64_t lda, int64_t n, float a_scale, float eps_rel,
+                                   int32_t escalations, float* l, int64_t ldl, float* eps_used, void* ws,
+                                   size_t ws_bytes, loka_stream_t stream) {
+  if (n < 0 || (n > 0 && (!a || !l || lda < n || ldl < n)) || escalations < 0 || !(eps_rel >= 0.f) ||
+      !(a_scale > 0.f) || !(a_scale < INFINITY))
+    return LOKA_ERR_INVALID_ARG;
+  if (n == 0) return LOKA_OK;
+  {  // a and l must not overlap
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(a), a1 = a0 + (size_t)((n - 1) * lda + n) * 4;
+    const uintptr_t l0 = reinterpret_cast<uintptr_t>(l), l1 = l0 + (size_t)((n - 1) * ldl + n) * 4;
+    if (a0 < l1 && l0 < a1) return LOKA_ERR_INVALID_ARG;
+  }
+  if (!ws || ws_bytes < loka_cholesky_workspace_size(n) || (reinterpret_cast<uintptr_t>(ws) & 7)) return LOKA_ERR_WORKSPACE;
+  loka_status stt = check_device();
+  if (stt != LOKA_OK) return stt;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  double* tr = static_cast<double*>(ws);
+  int32_t* status = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws) + 64);
+  if (launch_trace2(a, n, lda, nullptr, 0, 0, tr, s) != cudaSuccess) return LOKA_ERR_CUDA;
+  double trh = 0.0;
+  if (cudaMemcpyAsync(&trh, tr, sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess) return LOKA_ERR_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return LOKA_ERR_CUDA;
+  const double t = trh * (double)a_scale / (double)n;
+  if (!std::isfinite(t)) return LOKA_ERR_NONFINITE;
+  double eps = (double)eps_rel * (t > 0.0 ? t : 1.0);
+  for (int att = 0; att <= escalations; ++att, eps *= 10.0) {
+    if (cudaMemsetAsync(status, 0, sizeof(int32_t), s) != cudaSuccess) return LOKA_ERR_CUDA;
+    if (launch_jitter_copy(a, lda, l, ldl, n, a_scale, (float)eps, nullptr, 0.0, 0.f, s) != cudaSuccess) return LOKA_ERR_CUDA;
+    if (launch_cholesky(l, ldl, n, status, s) != cudaSuccess) return LOKA_ERR_CUDA;
+    int32_t h = 0;
+    if (cudaMemcpyAsync(&h, status, sizeof(int32_t), cudaMemcpyDeviceToHost, s) != cudaSuccess) return LOKA_ERR_CUDA;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return LOKA_ERR_CUDA;
+    if (h == 0) {
+      if (eps_used) *eps_used = (float)eps;
+      return LOKA_OK;
+    }
+  }
+  return LOKA_ERR_NOT_PD;
+}
+
+static bool weight_tensor_ok(const loka_tensor* w, int64_t M, int64_t N) {
+  return w && w->data && (w->dtype == LOKA_F32 || w->dtype == LOKA_BF16) && w->rows == M && w->cols == N &&
+         w->ld >= N;
+}
+
+loka_status loka_probe_track_weight_init(loka_matnorm_state* st, const loka_tensor* w, loka_stream_t stream) {
+  if (!st || st->M <= 0 || st->N <= 0 || !st->mean || !st->U || !st->V) return LOKA_ERR_INVALID_ARG;
+  if (!weight_tensor_ok(w, st->M, st->N)) return LOKA_ERR_INVALID_ARG;
+  loka_status stt = check_device();
+  if (stt != LOKA_OK) return stt;
+  if (launch_matnorm_init(w->data, w->dtype == LOKA_BF16, w->ld, st->mean, st->U, st->M, st->V, st->N,
+                          reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess)
+    return LOKA_ERR_CUDA;
+  st->count = 0;
+  return LOKA_OK;
+}
+
+struct MatnormWs {
+  size_t wc, wct, lu, lv, u1, v1, tr, total;
+};
+static MatnormWs matnorm_ws(int64_t M, int64_t N) {
+  MatnormWs w;
+  size_t o = 0;
+  auto take = [&](size_t b) { size_t r = o; o += (b + 255) & ~size_t(255); return r; };
+  w.wc = take((size_t)M * N * 4);
+  w.wct = take((size_t)M * N * 4);
+  w.lu = take((size_t)M * M * 4);
+  w.lv = take((size_t)N * N * 4);
+  w.u1 = take((size_t)M * M * 4);
+  w.v1 = take((size_t)N * N * 4);
+  w.tr = take(64);
+  w.total = o;
+  return w;
+}
+
+size_t loka_probe_track_weight_workspace_size(const loka_matnorm_state* st) {
+  if (!st || st->M <= 0 || st->N <= 0) return 0;
+  return matnorm_ws(st->M, st->N).total;
+}
+
+loka_status loka_probe_track_weight(loka_matnorm_state* st, const loka_tensor* w, int32_t* status_dev, void* ws,
+                                    size_t ws_bytes, loka_stream_t stream) {
+  if (!st || st->M <= 0 || st->N <= 0 || !st->mean || !st->U || !st->V) return LOKA_ERR_INVALID_ARG;
+  if (!(st->momentum >= 0.f && st->momentum <= 1.f) || !(st->eps_rel >= 0.f)) return LOKA_ERR_INVALID_ARG;
+  if (!weight_tensor_ok(w, st->M, st->N)) return LOKA_ERR_INVALID_ARG;
+  if (st->M > (1 << 16) || st->N > (1 << 16)) return LOKA_ERR_SHAPE;
+  const MatnormWs L = matnorm_ws(st->M, st->N);
+  if (!ws || ws_bytes < L.total || !aligned16(ws)) return LOKA_ERR_WORKSPACE;
+  loka_status stt = check_device();
+  if (stt != LOKA_OK) return stt;
+  uint8_t* b = static_cast<uint8_t*>(ws);
+  MatnormParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.w = w->data;
+  p.w_bf16 = w->dtype == LOKA_BF16;
+  p.ldw = w->ld;
+  p.M = st->M;
+  p.N = st->N;
+  p.m = st->momentum;
+  p.eps_rel = st->eps_rel;
+  p.mean = st->mean;
+  p.u = st->U;
+  p.v = st->V;
+  p.wc = reinterpret_cast<float*>(b + L.wc);
+  p.wct = reinterpret_cast<float*>(b + L.wct);
+  p.lu = reinterpret_cast<float*>(b + L.lu);
+  p.lv = reinterpret_cast<float*>(b + L.lv);
+  p.u1 = reinterpret_cast<float*>(b + L.u1);
+  p.v1 = reinterpret_cast<float*>(b + L.v1);
+  p.tr = reinterpret_cast<double*>(b + L.tr);
+  p.status = status_dev;
+  if (launch_matnorm_update(p, reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess) return LOKA_ERR_CUDA;
+  st->count += 1;
+  return LOKA_OK;
+}
+
+size_t loka_probe_sample_workspace_size(int64_t rows, int64_t cols, int32_t is_weight) {
+  if (rows < 0 || cols < 0) return 0;
+  const size_t z = ((size_t)rows * cols * 4 + 255) & ~size_t(255);
+  return is_weight ? 2 * z : z;
+}
+
+static bool sample_out_ok(const loka_tensor* o, int64_t rows, int64_t cols) {
+  return o && o->data && (o->dtype == LOKA_F32 || o->dtype == LOKA_BF16) && o->rows == rows && o->cols == cols &&
+         o->ld >= cols;
+}
+
+loka_status loka_probe_sample_input(const float* mean, const float* l_sigma, int64_t K, int64_t B, uint64_t seed,
+                                    uint64_t offset, loka_tensor* out, void* ws, size_t ws_bytes, loka_stream_t stream) {
+  if (K <= 0 || B < 0 || !mean || !l_sigma || !sample_out_ok(out, B, K)) return LOKA_ERR_INVALID_ARG;
+  if (B == 0) return LOKA_OK;
+  if (!ws || ws_bytes < loka_probe_sample_workspace_size(B, K, 0) || !aligned16(ws)) return LOKA_ERR_WORKSPACE;
+  loka_status stt = check_device();
+  if (stt != LOKA_OK) return stt;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  float* z = static_cast<float*>(ws);
+  if (launch_philox_normal(seed, offset, B * K, z, s) != cudaSuccess) return LOKA_ERR_CUDA;
+  GemmF32Params g;
+  std::memset(&g, 0, sizeof(g));
+  g.M = B; g.N = K; g.K = K;
+  g.A = z; g.lda = K;
+  g.B = l_sigma; g.ldb = K;  // B(k, n) = L[n][k]
+  g.tri_b = 1;
+  g.bias = mean;
+  g.C = out->data; g.ldc = out->ld; g.c_bf16 = out->dtype == LOKA_BF16;
+  g.alpha = 1.f;
+  return launch_gemm_f32(g, false, true, s) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
+}
+
+loka_status loka_probe_sample_weight(const float* mean, const float* l_u, const float* l_v, int64_t M, int64_t N,
+                                     uint64_t seed, uint64_t offset, loka_tensor* out, void* ws, size_t ws_bytes,
+                                     loka_stream_t stream) {
+  if (M <= 0 || N <= 0 || !mean || !l_u || !l_v || !sample_out_ok(out, M, N)) return LOKA_ERR_INVALID_ARG;
+  if (!ws || ws_bytes < loka_probe_sample_workspace_size(M, N, 1) || !aligned16(ws)) return LOKA_ERR_WORKSPACE;
+  loka_status stt = check_device();
+  if (stt != LOKA_OK) return stt;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  float* z = static_cast<float*>(ws);
+  float* t1 = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + loka_probe_sample_workspace_size(M, N, 0));
+  if (launch_philox_normal(seed, offset, M * N, z, s) != cudaSuccess) return LOKA_ERR_CUDA;
+  GemmF32Params g;
+  std::memset(&g, 0, sizeof(g));
+  g.M = M; g.N = N; g.K = N;  // T1 = Z L_V^T
+  g.A = z; g.lda = N;
+  g.B = l_v; g.ldb = N;
+  g.tri_b = 1;
+  g.C = t1; g.ldc = N;
+  g.alpha = 1.f;
+  if (launch_gemm_f32(g, false, true, s) != cudaSuccess) return LOKA_ERR_CUDA;
+  std::memset(&g, 0, sizeof(g));
+  g.M = M; g.N = N; g.K = M;  // out = L_U T1 + mean
+  g.A = l_u; g.lda = M;
+  g.B = t1; g.ldb = N;
+  g.tri_a = 1;
+  g.Cin = mean; g.ldcin = N; g.beta = 1.f;
+  g.C = out->data; g.ldc = out->ld; g.c_bf16 = out->dtype == LOKA_BF16;
+  g.alpha = 1.f;
+  return launch_gemm_f32(g, false, false, s) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
 }
 
 loka_status loka_probe_error(int32_t L, const loka_probe_pair* pairs, double floor_rel, loka_probe_stats* stats_dev,

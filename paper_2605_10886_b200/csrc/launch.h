@@ -231,4 +231,38 @@ struct ProbeLayer {
 cudaError_t launch_probe(const ProbeLayer* layers_dev, int L, int64_t max_elems, double floor_rel,
                          void* stats_dev, double* partials, int nblk, cudaStream_t st);
 
+// ---- NEXT-3 (linalg.cu): FP32 linear algebra for the matrix-normal tracker and the sampling ----
+struct GemmF32Params {  // C = alpha op(A) op(B) + beta Cin + bias[n]  (see linalg.cu)
+  int64_t M, N, K;
+  const float* A; int64_t lda;
+  const float* B; int64_t ldb;
+  const float* Cin; int64_t ldcin;
+  void* C; int64_t ldc;
+  int32_t c_bf16;
+  const float* bias;
+  float alpha, beta;
+  int32_t tri_a, tri_b, lower_only;
+};
+cudaError_t launch_gemm_f32(const GemmF32Params& p, bool at, bool bt, cudaStream_t st);
+cudaError_t launch_cholesky(float* a, int64_t lda, int64_t n, int32_t* status, cudaStream_t st);
+cudaError_t launch_trsm_left(const float* l, int64_t ldl, int64_t n, float* b, int64_t ldb, int64_t ncols,
+                             cudaStream_t st);
+cudaError_t launch_trace2(const float* a, int64_t na, int64_t lda, const float* b, int64_t nb, int64_t ldb,
+                          double* tr, cudaStream_t st);
+cudaError_t launch_jitter_copy(const float* a, int64_t lda, float* l, int64_t ldl, int64_t n, float scale,
+                               float eps_host, const double* tr_dev, double tr_scale, float eps_rel, cudaStream_t st);
+cudaError_t launch_philox_normal(uint64_t seed, uint64_t offset, int64_t n, float* out, cudaStream_t st);
+struct MatnormParams {
+  const void* w; int32_t w_bf16; int64_t ldw;
+  int64_t M, N;
+  float m, eps_rel;
+  float *mean, *u, *v;              // state (updated in place)
+  float *wc, *wct, *lu, *lv, *u1, *v1;  // workspace
+  double* tr;                        // [4]
+  int32_t* status;                   // nullable: bit 0 = a Cholesky pivot was not positive
+};
+cudaError_t launch_matnorm_init(const void* w, bool bf16, int64_t ldw, float* mean, float* u, int64_t mm, float* v,
+                                int64_t nn, cudaStream_t st);
+cudaError_t launch_matnorm_update(const MatnormParams& p, cudaStream_t st);
+
 }  // namespace loka
