@@ -144,68 +144,130 @@ cudaError_t launch_gemm_f32(const GemmF32Params& p, bool at, bool bt, cudaStream
 constexpr int kNB = 64;
 
 // Unblocked right-looking Cholesky of the jb x jb diagonal block (lower part read, upper zeroed).
-// A pivot that is not positive and finite sets bit 0 of *status (the factor is then garbage).
+// Thread (ty, tx) of 4 x 64 holds column tx, rows i = ty + 4 q (q < 16), in registers.  Step j:
+// the owners of column j publish it (unscaled) to a double-buffered shared vector, one barrier,
+// then every thread updates its entries a[i][k] -= a[i][j] a[k][j] / d_j (= L[i][j] L[k][j]) for
+// i, k > j.  The column scaling by 1/sqrt(d_k) is deferred to the end, so one barrier per step.
+// A pivot d_j that is not positive and finite sets bit 0 of *status (the factor is then garbage).
 __global__ void __launch_bounds__(256) potf2_kernel(float* a, int64_t lda, int jb, int32_t* status) {
-  __shared__ float s[kNB][kNB + 1];
-  for (int idx = threadIdx.x; idx < jb * jb; idx += 256) {
-    const int i = idx / jb, j = idx - i * jb;
-    s[i][j] = j <= i ? a[(int64_t)i * lda + j] : 0.f;
+  __shared__ float col[2][kNB];
+  __shared__ float dvec[kNB];
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+  float r[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int i = ty + 4 * q;
+    r[q] = (i < jb && tx < jb && tx <= i) ? a[(int64_t)i * lda + tx] : 0.f;
   }
-  __syncthreads();
   for (int j = 0; j < jb; ++j) {
-    const float d = s[j][j];
-    const float piv = sqrtf(d);
+    float* cj = col[j & 1];
+    if (tx == j) {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) cj[ty + 4 * q] = r[q];
+    }
     __syncthreads();
+    const float d = cj[j];
     if (threadIdx.x == 0) {
-      s[j][j] = piv;
-      if (!(d > 0.f) || !(d < INFINITY)) {
-        if (status) atomicOr(status, 1);
+      dvec[j] = d;
+      if ((!(d > 0.f) || !(d < INFINITY)) && status) atomicOr(status, 1);
+    }
+    if (tx > j && tx < jb) {
+      const float lk = cj[tx] / d;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int i = ty + 4 * q;
+        if (i >= tx) r[q] = fmaf(-cj[i], lk, r[q]);
       }
     }
-    for (int i = j + 1 + threadIdx.x; i < jb; i += 256) s[i][j] = s[i][j] / piv;
-    __syncthreads();
-    const int w = jb - j - 1;
-    for (int idx = threadIdx.x; idx < w * w; idx += 256) {
-      const int i = j + 1 + idx / w, k = j + 1 + idx % w;
-      if (k <= i) s[i][k] = fmaf(-s[i][j], s[k][j], s[i][k]);
-    }
-    __syncthreads();
   }
-  for (int idx = threadIdx.x; idx < jb * jb; idx += 256) {
-    const int i = idx / jb, j = idx - i * jb;
-    a[(int64_t)i * lda + j] = j <= i ? s[i][j] : 0.f;
+  __syncthreads();
+  if (tx < jb) {
+    const float rs = 1.f / sqrtf(dvec[tx]);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int i = ty + 4 * q;
+      if (i < jb) a[(int64_t)i * lda + tx] = tx < i ? r[q] * rs : (tx == i ? sqrtf(dvec[i]) : 0.f);
+    }
   }
 }
 
 // Solve X L^T = B in place for a panel of jb <= 64 columns: X(r, c) = b[r sr + c sc], r < R.
-// One thread per r, the jb x jb lower factor in shared memory (broadcast reads):
-//   x_c = (b_c - sum_{i<c} x_i L[c][i]) / L[c][c].
-// Used both for the Cholesky panel (rows of A21: sr = lda, sc = 1) and for L X = B (the transposed
-// view of B's panel rows: sr = 1, sc = ldb — coalesced across threads).
+// A CTA stages 128 rows x jb columns through shared memory with coalesced loads/stores (along c
+// when sc == 1, along r otherwise), then one thread per row solves right-looking inside the thread
+// (x_j = v_j / L[j][j], then v_c -= x_j L[c][j] for all c > j: independent FMAs), the jb x jb
+// lower factor and its inverse diagonal in shared memory (broadcast reads).  Used for the
+// Cholesky panel (rows of A21: sr = lda, sc = 1) and for L X = B (the transposed view of B's panel
+// rows: sr = 1, sc = ldb).
 __global__ void __launch_bounds__(128) panel_trsm_kernel(float* b, int64_t sr, int64_t sc, int64_t R,
                                                          const float* l, int64_t ldl, int jb) {
-  __shared__ float L[kNB][kNB + 1];
+  extern __shared__ float trsm_smem[];  // L [64][65], rinv [64], tile [128][65]
+  float (*L)[kNB + 1] = reinterpret_cast<float (*)[kNB + 1]>(trsm_smem);
+  float* rinv = trsm_smem + kNB * (kNB + 1);
+  float (*tile)[kNB + 1] = reinterpret_cast<float (*)[kNB + 1]>(trsm_smem + kNB * (kNB + 1) + kNB);
   for (int idx = threadIdx.x; idx < jb * jb; idx += 128) {
     const int i = idx / jb, j = idx - i * jb;
     L[i][j] = j <= i ? l[(int64_t)i * ldl + j] : 0.f;
   }
+  const int64_t r0 = (int64_t)blockIdx.x * 128;
+  if (sc == 1) {  // 64 threads along a row
+    const int c = threadIdx.x & 63;
+    for (int rr = threadIdx.x >> 6; rr < 128; rr += 2)
+      if (c < jb && r0 + rr < R) tile[rr][c] = b[(r0 + rr) * sr + c];
+  } else {
+    for (int c = 0; c < jb; ++c)
+      if (r0 + threadIdx.x < R) tile[threadIdx.x][c] = b[(r0 + threadIdx.x) * sr + c * sc];
+  }
   __syncthreads();
-  const int64_t r = (int64_t)blockIdx.x * 128 + threadIdx.x;
-  if (r >= R) return;
-  float x[kNB];
-  float* row = b + r * sr;
+  if (threadIdx.x < jb) rinv[threadIdx.x] = 1.f / L[threadIdx.x][threadIdx.x];
+  __syncthreads();
+  if (r0 + threadIdx.x < R) {
+    // 16-column chunks (a fully unrolled 64-column solve is ~4K instructions: i-cache bound):
+    // chunk a first takes the updates of the already-solved columns j < 16a (runtime loop), then
+    // solves its own 16 columns with the unrolled right-looking step.
+    float* trow = tile[threadIdx.x];
+    for (int a0 = 0; a0 < jb; a0 += 16) {
+      float v[16];
 #pragma unroll
-  for (int c = 0; c < kNB; ++c) {
-    if (c < jb) {
-      float v = row[c * sc];
+      for (int c = 0; c < 16; ++c) v[c] = a0 + c < jb ? trow[a0 + c] : 0.f;
+      for (int j = 0; j < a0; ++j) {
+        const float x = trow[j];
 #pragma unroll
-      for (int i = 0; i < c; ++i) v = fmaf(-x[i], L[c][i], v);
-      x[c] = v / L[c][c];
-      row[c * sc] = x[c];
-    } else {
-      x[c] = 0.f;
+        for (int c = 0; c < 16; ++c) v[c] = fmaf(-x, L[a0 + c][j], v[c]);
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (a0 + j < jb) {
+          const float x = v[j] * rinv[a0 + j];
+          v[j] = x;
+#pragma unroll
+          for (int c = j + 1; c < 16; ++c) v[c] = fmaf(-x, L[a0 + c][a0 + j], v[c]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        if (a0 + c < jb) trow[a0 + c] = v[c];
     }
   }
+  __syncthreads();
+  if (sc == 1) {
+    const int c = threadIdx.x & 63;
+    for (int rr = threadIdx.x >> 6; rr < 128; rr += 2)
+      if (c < jb && r0 + rr < R) b[(r0 + rr) * sr + c] = tile[rr][c];
+  } else {
+    for (int c = 0; c < jb; ++c)
+      if (r0 + threadIdx.x < R) b[(r0 + threadIdx.x) * sr + c * sc] = tile[threadIdx.x][c];
+  }
+}
+
+constexpr int kTrsmSmem = (kNB * (kNB + 1) + kNB + 128 * (kNB + 1)) * 4;
+static cudaError_t trsm_attr() {
+  static bool done = false;
+  if (!done) {
+    cudaError_t e = cudaFuncSetAttribute(panel_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmem);
+    if (e != cudaSuccess) return e;
+    done = true;
+  }
+  return cudaSuccess;
 }
 
 __global__ void zero_upper_kernel(float* a, int64_t lda, int64_t n) {
@@ -231,7 +293,8 @@ cudaError_t launch_cholesky(float* a, int64_t lda, int64_t n, int32_t* status, c
     const int64_t rest = n - j0 - jb;
     if (rest > 0) {
       float* l21 = a + (j0 + jb) * lda + j0;
-      panel_trsm_kernel<<<(unsigned)((rest + 127) / 128), 128, 0, st>>>(l21, lda, 1, rest, d, lda, jb);
+      if (cudaError_t e = trsm_attr()) return e;
+      panel_trsm_kernel<<<(unsigned)((rest + 127) / 128), 128, kTrsmSmem, st>>>(l21, lda, 1, rest, d, lda, jb);
       note_launch();
       GemmF32Params g = {};
       g.M = rest; g.N = rest; g.K = jb;
@@ -254,7 +317,8 @@ cudaError_t launch_trsm_left(const float* l, int64_t ldl, int64_t n, float* b, i
                              cudaStream_t st) {
   for (int64_t j0 = 0; j0 < n; j0 += kNB) {
     const int jb = (int)(n - j0 < kNB ? n - j0 : kNB);
-    panel_trsm_kernel<<<(unsigned)((ncols + 127) / 128), 128, 0, st>>>(b + j0 * ldb, 1, ldb, ncols,
+    if (cudaError_t e = trsm_attr()) return e;
+    panel_trsm_kernel<<<(unsigned)((ncols + 127) / 128), 128, kTrsmSmem, st>>>(b + j0 * ldb, 1, ldb, ncols,
                                                                          l + j0 * ldl + j0, ldl, jb);
     note_launch();
     const int64_t rest = n - j0 - jb;
@@ -335,15 +399,17 @@ cudaError_t launch_jitter_copy(const float* a, int64_t lda, float* l, int64_t ld
   return cudaGetLastError();
 }
 
-// out = sym(m X + (1 - m) X1) + eps I, eps = eps_rel * tr_dev[0] / n
+// out = sym(m X + (1 - m) X1) + eps I, eps = eps_rel * tr_dev[0] / n; X1 is a
+// Gram product of which only the lower triangle is valid (it is symmetric by construction)
 __global__ void ema_sym_kernel(const float* x, const float* x1, float* out, int64_t n, float m, float eps_rel,
                                const double* tr_dev) {
   const float eps = (float)((double)eps_rel * tr_dev[0] / (double)n);
   const int64_t total = n * n;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / n, c = i - r * n;
-    const float a = fmaf(m, x[r * n + c], (1.f - m) * x1[r * n + c]);
-    const float b = fmaf(m, x[c * n + r], (1.f - m) * x1[c * n + r]);
+    const float g = x1[r >= c ? r * n + c : c * n + r];
+    const float a = fmaf(m, x[r * n + c], (1.f - m) * g);
+    const float b = fmaf(m, x[c * n + r], (1.f - m) * g);
     float v = 0.5f * (a + b);
     if (r == c) v += eps;
     out[i] = v;
@@ -448,6 +514,7 @@ cudaError_t launch_matnorm_update(const MatnormParams& p, cudaStream_t st) {
     g.B = p.wct; g.ldb = mm;
     g.C = p.u1; g.ldc = mm;
     g.alpha = (float)(1.0 / (double)nn);
+    g.lower_only = 1;  // symmetric: the strict upper tiles are not computed (ema_sym reads the lower)
     if ((e = launch_gemm_f32(g, true, false, st)) != cudaSuccess) return e;
     g.M = nn; g.N = nn; g.K = mm;
     g.A = p.wc; g.lda = nn;
