@@ -503,17 +503,48 @@ static bool plain_pair_ok(const loka_linear_args* a) {
 // 2048 x 123200 x 1024 layer): ks slices of kbps 128-K blocks; each slice's raw FP32
 // partial goes to the workspace and one reduction kernel applies the scales.  ks minimises
 // waves(ks) * kbps (in 128-K MMA-step units) + the partials' HBM round trip.
-static int split_k_shape(int64_t M, int64_t N, int64_t nkb, int* kbps_out);
-static int split_k_for(const loka_linear_args* a, int* kbps_out = nullptr) {
-  if (kbps_out) *kbps_out = 0;
-  if (!plain_pair_ok(a) || a->M % 32 || a->N % 4 || a->M <= 0 || a->N <= 0 || a->K <= 0) return 1;
-  return split_k_shape(a->M, a->N, cdiv(a->K, 128), kbps_out);
+static int split_k_shape(int64_t M, int64_t N, int64_t nkb, int* kbps_out, int tn = 256);
+// How a plain problem runs on the CTA-pair engine: tile width (256, or 512 = WIDE: two N = 256
+// MMAs per K step, 25% fewer operand bytes per FLOP through each SM's L2 port, one accumulator) and
+// the split-K factor.  WIDE is taken for long-K work units (see pair_plan); LOKA_PAIR_WIDE=0 / 1
+// turns it off / on everywhere.
+struct PairPlan {
+  bool wide;
+  int ks, kbps;
+};
+static int pair_wide_env() {
+  static const int v = [] {
+    const char* e = std::getenv("LOKA_PAIR_WIDE");
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
+  }();
+  return v;
 }
-// ks for an M x N output with nkb K-stages on the CTA-pair engine (1 = no split)
-static int split_k_shape(int64_t M, int64_t N, int64_t nkb, int* kbps_out) {
+static PairPlan pair_plan(const loka_linear_args* a) {
+  PairPlan pl{false, 1, 0};
+  if (!plain_pair_ok(a) || a->M % 32 || a->N % 4 || a->M <= 0 || a->N <= 0 || a->K <= 0) return pl;
+  const int64_t nkb = cdiv(a->K, 128);
+  pl.ks = split_k_shape(a->M, a->N, nkb, &pl.kbps, 256);
+  const int w = pair_wide_env();
+  // long K per work unit (>= 16 128-K stages): the single accumulator's non-overlapped epilogue
+  // is a small share and the operand-port saving wins (cfg4: 2.62 -> 2.80 PF; the stretch layer:
+  // 2.36 -> 2.72 PF); short-K work (the cfg3 ensemble, ~1-16 stages per tile) stays 256 wide
+  const bool long_k = nkb >= 16 && (pl.ks > 1 || cdiv(a->M, 256) * cdiv(a->N, 512) >= 74);
+  if (w == 1 || (w == -1 && long_k)) {
+    pl.wide = true;
+    pl.ks = split_k_shape(a->M, a->N, nkb, &pl.kbps, 512);
+  }
+  return pl;
+}
+static int split_k_for(const loka_linear_args* a, int* kbps_out = nullptr) {
+  const PairPlan pl = pair_plan(a);
+  if (kbps_out) *kbps_out = pl.kbps;
+  return pl.ks;
+}
+// ks for an M x N output with nkb K-stages on the CTA-pair engine with tn-wide tiles (1 = no split)
+static int split_k_shape(int64_t M, int64_t N, int64_t nkb, int* kbps_out, int tn) {
   constexpr int kPairs = 74;
   if (kbps_out) *kbps_out = 0;
-  const int64_t tiles = cdiv(M, 256) * cdiv(N, 256);
+  const int64_t tiles = cdiv(M, 256) * cdiv(N, tn);
   if (tiles >= kPairs || nkb < 16 || M % 32 || N % 4) return 1;
   double best = (double)nkb;  // one wave, no split
   int bks = 1, bkbps = (int)nkb;
@@ -826,7 +857,10 @@ loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* 
   }
   std::stable_sort(grouped.begin(), grouped.end(), [&](int x, int y) { return a[x].K > a[y].K; });
   int kbps = 0;
-  const int ksplit = (G == 1 && pair && grouped.size() == 1) ? split_k_for(&a[0], &kbps) : 1;
+  const bool one = G == 1 && pair && grouped.size() == 1;
+  const PairPlan plan = one ? pair_plan(&a[0]) : PairPlan{pair_wide_env() == 1, 1, 0};
+  const int ksplit = plan.ks;
+  kbps = plan.kbps;
   size_t mx_bytes = 0;
   for (int g = 0; g < G; ++g) mx_bytes += (mx_ws_bytes(&a[g]) + 255) & ~size_t(255);
   float* part = ksplit > 1 ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + mx_bytes) : nullptr;
@@ -835,6 +869,7 @@ loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* 
     std::memset(&gp, 0, sizeof(gp));
     const int n = (int)std::min<size_t>(kMaxGroups, grouped.size() - i0);
     gp.G = n;
+    gp.wide = pair && plan.wide;
     for (int k = 0; k < n; ++k) {
       const loka_linear_args& q = a[grouped[i0 + k]];
       if (!make_map_u8(&gp.ta[k], q.a.data, q.M, q.K, q.a.ld, 128)) return LOKA_ERR_CUDA;
@@ -845,8 +880,8 @@ loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* 
       d.M = (int32_t)q.M;
       d.N = (int32_t)q.N;
       d.K = (int32_t)q.K;
-      const int tile = pair ? 256 : 128;  // CTA-pair tiles are 256 x 256
-      d.tiles_n = (int32_t)cdiv(q.N, tile);
+      const int tile = pair ? 256 : 128;  // CTA-pair tiles are 256 x 256 (256 x 512 when wide)
+      d.tiles_n = (int32_t)cdiv(q.N, gp.wide ? 512 : tile);
       d.a_fmt = q.a.dtype == LOKA_E5M2 ? 1 : 0;
       d.b_fmt = q.b.dtype == LOKA_E5M2 ? 1 : 0;
       d.sa = q.a.scales;
@@ -861,7 +896,7 @@ loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* a, void* 
       if (ksplit > 1) {  // G == 1
         d.ksplit = ksplit;
         d.kb_per_split = kbps;
-        if (!make_map_out(&gp.tp[k], part, (int64_t)ksplit * q.M, q.N, q.N, LOKA_F32, 128, 32u)) return LOKA_ERR_CUDA;
+        if (!make_map_out(&gp.tp[0], part, (int64_t)ksplit * q.M, q.N, q.N, LOKA_F32, 128, 32u)) return LOKA_ERR_CUDA;
       }
       gp.tile_start[k + 1] = gp.tile_start[k] + (int32_t)(cdiv(q.M, tile) * d.tiles_n * d.ksplit);
     }

@@ -36,18 +36,41 @@ constexpr int k2OffBar = k2OffCol + 2 * 2 * 256 * 4;
 constexpr int k2Smem = k2OffBar + 256 + 1024;
 static_assert(k2Smem <= 227 * 1024, "gemm2 smem");
 
+// WIDE: 256 x 512 pair tiles — two N = 256 MMAs per K step share the A stage, so a pair moves
+// 96 KB of operands per 33.6 MFLOP instead of 64 KB per 16.8 MFLOP: 25% fewer bytes per FLOP
+// through each SM's L2 -> SM port (~40 B/clk, the bound of the 256 x 256 tile at ~80% of the MMA
+// rate).  All 512 TMEM columns hold one accumulator (no overlap of a tile's epilogue with the next
+// tile's MMAs), so WIDE is for long-K work units (split-K slices of the paper's largest layer).
+template <bool WIDE>
+struct G2 {
+  static constexpr int kTN = WIDE ? 512 : 256;  // tile columns
+  static constexpr int kStages = WIDE ? 3 : 4;
+  static constexpr int kStageA = 128 * 128;
+  static constexpr int kStageB = (WIDE ? 256 : 128) * 128;  // per CTA: 128 rows of each 256-col half
+  static constexpr int kOffB = kStages * kStageA;
+  static constexpr int kOffOut = kOffB + kStages * kStageB;
+  static constexpr int kOffCol = kOffOut + k2EpiWarps * 2 * 4096;  // [2 tiles][s_b | bias][kTN] FP32
+  static constexpr int kOffBar = kOffCol + 2 * 2 * kTN * 4;
+  static constexpr int kSmem = kOffBar + 256 + 1024;
+};
+static_assert(G2<true>::kSmem <= 227 * 1024 && G2<false>::kSmem == k2Smem, "gemm2 smem");
+
 // BF16IN: BF16 operands (kind::f16; a 128-byte stage row holds 64 K elements) — the probe
 // tracker's scatter GEMM (NEXT-2); otherwise FP8 (kind::f8f6f4, 128 K elements per row).
-template <bool BF16IN>
+// SPLIT: the launch is one split-K problem (raw FP32 partials to gp.tp); a template parameter so the
+// many-small-GEMM epilogue carries none of that code (it is epilogue-bound: ~1 K-block per tile).
+template <bool BF16IN, bool WIDE, bool SPLIT>
 __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_constant__ GroupedParams gp) {
+  using C2 = G2<WIDE>;
   constexpr int kKE = BF16IN ? 64 : 128;  // K elements per 128-byte stage row
+  constexpr int kTN = C2::kTN, kHN = kTN / 2;  // tile columns; columns per epilogue warp
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + k2OffB;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + k2OffBar);
-  uint64_t* empty_bar = full_bar + k2Stages;
-  uint64_t* acc_full = empty_bar + k2Stages;  // [2]
+  uint8_t* sB = smem + C2::kOffB;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C2::kOffBar);
+  uint64_t* empty_bar = full_bar + C2::kStages;
+  uint64_t* acc_full = empty_bar + C2::kStages;  // [2]
   uint64_t* acc_empty = acc_full + 2;          // [2] (leader's is the one used)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
@@ -57,7 +80,7 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
   const int T = gp.tile_start[gp.G];
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < k2Stages; ++s) {
+    for (int s = 0; s < C2::kStages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
@@ -86,15 +109,17 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
     g = lo;
     int local = t - gp.tile_start[g];
     const int tn = gp.g[g].tiles_n;
-    const int per = ((gp.g[g].M + 255) / 256) * tn;  // tiles of one K slice
-    ks = local / per;                                   // split-K slice (0 without split)
-    local -= ks * per;
+    if constexpr (SPLIT) {
+      const int per = ((gp.g[g].M + 255) / 256) * tn;  // tiles of one K slice
+      ks = local / per;                                   // split-K slice
+      local -= ks * per;
+    }
     mb = local / tn;
     nb = local - mb * tn;
   };
   auto krange = [&](int g, int ks, int& kb0, int& kb1) {
     const int nkb = (gp.g[g].K + kKE - 1) / kKE;
-    if (gp.g[g].ksplit > 1) {
+    if (SPLIT) {
       kb0 = ks * gp.g[g].kb_per_split;
       kb1 = min(nkb, kb0 + gp.g[g].kb_per_split);
     } else {
@@ -114,12 +139,15 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
         int kb0, kb1;
         krange(g, ks, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
-          const int s = it % k2Stages;
-          const uint32_t ph = (uint32_t)(it / k2Stages) & 1u;
+          const int s = it % C2::kStages;
+          const uint32_t ph = (uint32_t)(it / C2::kStages) & 1u;
           mbar_wait(&empty_bar[s], ph ^ 1u, 1);
-          if (rank == 0) mbar_arrive_expect_tx(&full_bar[s], 2u * (k2StageA + k2StageB));
-          tma_load_2d_cg2(sA + s * k2StageA, &gp.ta[g], full0 + 8u * s, kb * kKE, mb * 256 + rank * 128);
-          tma_load_2d_cg2(sB + s * k2StageB, &gp.tb[g], full0 + 8u * s, kb * kKE, nb * 256 + rank * 128);
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[s], 2u * (C2::kStageA + C2::kStageB));
+          tma_load_2d_cg2(sA + s * C2::kStageA, &gp.ta[g], full0 + 8u * s, kb * kKE, mb * 256 + rank * 128);
+#pragma unroll
+          for (int hh = 0; hh < kTN / 256; ++hh)  // this CTA's 128 rows of each 256-column half
+            tma_load_2d_cg2(sB + s * C2::kStageB + hh * 16384, &gp.tb[g], full0 + 8u * s, kb * kKE,
+                            nb * kTN + hh * 256 + rank * 128);
         }
       }
     }
@@ -133,26 +161,30 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
         locate(t, g, mb, nb);
         int kb0, kb1;
         krange(g, ks, kb0, kb1);
-        const int buf = j & 1;
-        mbar_wait(&acc_empty[buf], ((uint32_t)(j >> 1) & 1u) ^ 1u, 4);  // both CTAs drained it
+        const int buf = WIDE ? 0 : (j & 1);
+        const uint32_t use = WIDE ? (uint32_t)j : (uint32_t)(j >> 1);  // earlier uses of this buffer
+        mbar_wait(&acc_empty[buf], (use & 1u) ^ 1u, 4);  // both CTAs drained it
         tc_fence_after();
         const uint32_t idesc = BF16IN ? idesc_bf16(256, 256) : idesc_f8f6f4(gp.g[g].a_fmt, gp.g[g].b_fmt, 256, 256);
         const uint32_t dacc = tmem_base + (uint32_t)(buf * 256);
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
-          const int s = it % k2Stages;
-          const uint32_t ph = (uint32_t)(it / k2Stages) & 1u;
+          const int s = it % C2::kStages;
+          const uint32_t ph = (uint32_t)(it / C2::kStages) & 1u;
           mbar_wait(&full_bar[s], ph, 2);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + s * k2StageA);
-          const uint32_t b0 = smem_u32(sB + s * k2StageB);
+          const uint32_t a0 = smem_u32(sA + s * C2::kStageA);
+          const uint32_t b0 = smem_u32(sB + s * C2::kStageB);
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            if constexpr (BF16IN)
-              mma_bf16_cg2(dacc, smem_desc_kmajor_sw128(a0 + k * 32), smem_desc_kmajor_sw128(b0 + k * 32), idesc,
-                           (kb > kb0 || k) ? 1u : 0u);
-            else
-              mma_f8f6f4_cg2(dacc, smem_desc_kmajor_sw128(a0 + k * 32), smem_desc_kmajor_sw128(b0 + k * 32), idesc,
-                             (kb > kb0 || k) ? 1u : 0u);
+#pragma unroll
+            for (int hh = 0; hh < kTN / 256; ++hh) {  // WIDE: two N = 256 MMAs share the A stage
+              const uint64_t da = smem_desc_kmajor_sw128(a0 + k * 32);
+              const uint64_t db = smem_desc_kmajor_sw128(b0 + hh * 16384 + k * 32);
+              if constexpr (BF16IN)
+                mma_bf16_cg2(dacc + hh * 256, da, db, idesc, (kb > kb0 || k) ? 1u : 0u);
+              else
+                mma_f8f6f4_cg2(dacc + hh * 256, da, db, idesc, (kb > kb0 || k) ? 1u : 0u);
+            }
           mma_commit_cg2_mc(&empty_bar[s], 3);
         }
         mma_commit_cg2_mc(&acc_full[buf], 3);
@@ -163,8 +195,7 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
     // ===== epilogue (both CTAs): warp = TMEM lane quadrant q x column half h =====
     const int q = warp & 3;
     const int h = (warp - 2) >> 2;
-    const int r = q * 32 + lane;
-    uint8_t* stg = smem + k2OffOut + (warp - 2) * 8192;
+    uint8_t* stg = smem + C2::kOffOut + (warp - 2) * 8192;
     const uint32_t acc_empty0 = mapa_shared(smem_u32(acc_empty), 0);
     int nbox = 0;
     int j = 0;
@@ -172,52 +203,54 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
       int g, mb, nb;
       locate(t, g, mb, nb);
       const GroupDesc& d = gp.g[g];
-      const int buf = j & 1;
-      // this tile's 256 column parameters -> smem (while the MMAs run); buffer j & 1 was last read
+      const int buf = WIDE ? 0 : (j & 1);
+      const uint32_t use = WIDE ? (uint32_t)j : (uint32_t)(j >> 1);
+      // this tile's kTN column parameters -> smem (while the MMAs run); buffer j & 1 was last read
       // in tile j - 2, which every epilogue warp finished before the barrier of tile j - 1
-      float* colp = reinterpret_cast<float*>(smem + k2OffCol) + buf * 512;
-      {
-        const int e = threadIdx.x - 64;
-        const int n = nb * 256 + e;
+      float* colp = reinterpret_cast<float*>(smem + C2::kOffCol) + (j & 1) * 2 * kTN;
+      for (int e = threadIdx.x - 64; e < kTN; e += 32 * k2EpiWarps) {
+        const int n = nb * kTN + e;
         const bool ok = n < d.N;
         colp[e] = ok ? __ldg(d.sb + (d.sb_row ? n : 0)) : 0.f;
         float b = 0.f;
         if (ok && d.bias) b = d.bias_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(d.bias)[n])
                                           : reinterpret_cast<const float*>(d.bias)[n];
-        colp[256 + e] = b;
+        colp[kTN + e] = b;
       }
       named_bar_sync(2, 32 * k2EpiWarps);
-      if (lane == 0) mbar_wait(&acc_full[buf], (uint32_t)(j >> 1) & 1u, 3);
+      if (lane == 0) mbar_wait(&acc_full[buf], use & 1u, 3);
       __syncwarp();
       tc_fence_after();
       const int row0 = mb * 256 + rank * 128 + q * 32;  // first row of this warp's box
       const int grow = row0 + lane;
-      const bool split = d.ksplit > 1;  // raw FP32 partial of K slice ks -> partial buffer
+      constexpr bool split = SPLIT;  // raw FP32 partial of K slice ks -> partial buffer
       const float sa = grow < d.M ? (split ? 1.f : d.sa[d.sa_row ? grow : 0]) : 0.f;
       const int esz = (split || d.out_dtype == LOKA_F32) ? 4 : 2;
       const int cpb = 128 / esz;  // columns per 128-byte box row
-      const int col0 = nb * 256 + h * 128;
-      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * 256 + h * 128);
+      const int col0 = nb * kTN + h * kHN;
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * 256 + h * kHN);
       float amx = 0.f;  // NEXT-4 producer amax of this warp's stored values
 #pragma unroll 1
-      for (int cb = 0; cb < 128; cb += 32) {
+      for (int cb = 0; cb < kHN; cb += 32) {
         float y[32];
         tmem_ld32(tbase + (uint32_t)cb, y);
-        if (cb == 96) {  // accumulator fully in registers: hand the buffer back to the MMA
+        if (cb == kHN - 32) {  // accumulator fully in registers: hand the buffer back to the MMA
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(acc_empty0 + 8u * buf);
         }
-        const uint32_t cs = smem_u32(colp + h * 128 + cb);
+        const uint32_t cs = smem_u32(colp + h * kHN + cb);
         const float2 sa2 = make_float2(sa, sa);
+        if (!split) {
 #pragma unroll
-        for (int c = 0; c < 32 && !split; c += 4) {  // y = acc * (s_a s_b) + bias, column params from smem
-          const float4 s4 = lds_f4(cs + 4u * c), b4 = lds_f4(cs + 1024u + 4u * c);
-          const float2 a = fadd2(fmul2(make_float2(y[c], y[c + 1]), fmul2(sa2, make_float2(s4.x, s4.y))),
-                                 make_float2(b4.x, b4.y));
-          const float2 b = fadd2(fmul2(make_float2(y[c + 2], y[c + 3]), fmul2(sa2, make_float2(s4.z, s4.w))),
-                                 make_float2(b4.z, b4.w));
-          y[c] = a.x; y[c + 1] = a.y; y[c + 2] = b.x; y[c + 3] = b.y;
+          for (int c = 0; c < 32; c += 4) {  // y = acc * (s_a s_b) + bias, column params from smem
+            const float4 s4 = lds_f4(cs + 4u * c), b4 = lds_f4(cs + 4u * kTN + 4u * c);
+            const float2 a = fadd2(fmul2(make_float2(y[c], y[c + 1]), fmul2(sa2, make_float2(s4.x, s4.y))),
+                                   make_float2(b4.x, b4.y));
+            const float2 b = fadd2(fmul2(make_float2(y[c + 2], y[c + 3]), fmul2(sa2, make_float2(s4.z, s4.w))),
+                                   make_float2(b4.z, b4.w));
+            y[c] = a.x; y[c + 1] = a.y; y[c + 2] = b.x; y[c + 3] = b.y;
+          }
         }
         if (d.amax_out && !split && grow < d.M) {
 #pragma unroll
@@ -256,7 +289,7 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
           if (lane == 0) {
             const int c0 = col0 + cb + 32 - cpb;
             if (c0 < d.N && row0 < d.M) {
-              if (split) tma_store_2d(&gp.tp[g], box, c0, ks * d.M + row0);  // (M % 32 == 0 for split)
+              if (split) tma_store_2d(&gp.tp[0], box, c0, ks * d.M + row0);  // (M % 32 == 0 for split)
               else tma_store_2d(&gp.ty[g], box, c0, row0);
             }
             bulk_commit();
@@ -575,11 +608,12 @@ cudaError_t launch_splitk_reduce(const GroupDesc& d, const float* part, void* y,
   return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel, d, part, y, ldy);
 }
 
-template <bool BF16IN>
+template <bool BF16IN, bool WIDE, bool SPLIT>
 static cudaError_t launch_grouped2_t(const GroupedParams& gp, int num_sms, cudaStream_t st) {
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(grouped2_kernel<BF16IN>, cudaFuncAttributeMaxDynamicSharedMemorySize, k2Smem);
+    cudaError_t e = cudaFuncSetAttribute(grouped2_kernel<BF16IN, WIDE, SPLIT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, G2<WIDE>::kSmem);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
@@ -588,7 +622,7 @@ static cudaError_t launch_grouped2_t(const GroupedParams& gp, int num_sms, cudaS
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(2 * pairs), 1, 1);
   cfg.blockDim = dim3(k2Threads, 1, 1);
-  cfg.dynamicSmemBytes = k2Smem;
+  cfg.dynamicSmemBytes = G2<WIDE>::kSmem;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -599,15 +633,24 @@ static cudaError_t launch_grouped2_t(const GroupedParams& gp, int num_sms, cudaS
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, grouped2_kernel<BF16IN>, gp);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, grouped2_kernel<BF16IN, WIDE, SPLIT>, gp);
   note_launch();
   return e;
 }
+template <bool BF16IN>
+static cudaError_t launch_grouped2_any(const GroupedParams& gp, int num_sms, cudaStream_t st) {
+  const bool split = gp.G == 1 && gp.g[0].ksplit > 1;
+  if (gp.wide)
+    return split ? launch_grouped2_t<BF16IN, true, true>(gp, num_sms, st)
+                 : launch_grouped2_t<BF16IN, true, false>(gp, num_sms, st);
+  return split ? launch_grouped2_t<BF16IN, false, true>(gp, num_sms, st)
+               : launch_grouped2_t<BF16IN, false, false>(gp, num_sms, st);
+}
 cudaError_t launch_grouped2(const GroupedParams& gp, int num_sms, cudaStream_t st) {
-  return launch_grouped2_t<false>(gp, num_sms, st);
+  return launch_grouped2_any<false>(gp, num_sms, st);
 }
 cudaError_t launch_grouped2_bf16(const GroupedParams& gp, int num_sms, cudaStream_t st) {
-  return launch_grouped2_t<true>(gp, num_sms, st);
+  return launch_grouped2_any<true>(gp, num_sms, st);
 }
 
 }  // namespace loka

@@ -160,10 +160,11 @@ struct GroupDesc {
 };
 struct GroupedParams {
   CUtensorMap ta[kMaxGroups], tb[kMaxGroups], ty[kMaxGroups];  // A box {128,128}, B box {128,128}, Y out
-  CUtensorMap tp[kMaxGroups];                                    // split-K partials [ksplit*M, N] f32
+  CUtensorMap tp[1];  // split-K partials [ksplit*M, N] f32 (split-K is for lone problems: G == 1)
   GroupDesc g[kMaxGroups];
   int32_t G;
   int32_t tile_start[kMaxGroups + 1];  // prefix sum of 128x128 tiles
+  int32_t wide;                        // CTA-pair engine: 256 x 512 tiles (tiles_n = ceil(N/512))
 };
 cudaError_t launch_grouped(const GroupedParams& gp, int num_sms, cudaStream_t st);
 // CTA-pair variant (gemm2.cu): tiles 256 x 256 (tiles_n = ceil(N/256), tile_start counts them);

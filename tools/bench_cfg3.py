@@ -13,6 +13,7 @@ libloka (loka_probe_error, loka_dispatch_select).
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import math
 import os
@@ -104,9 +105,12 @@ def main():
             x1 = (lk.loka_tensor * 1)(qx[i])
             q1 = (lk.loka_tensor * 1)(qq[i])
 
+            nws1 = int(lk._lib.loka_grouped_workspace_size(1, a1))
+            ws1 = torch.empty(max(nws1, 16), dtype=torch.uint8, device=dev)
+
             def one_fp8():
                 assert lk._lib.loka_quantize_grouped(1, x1, q1, None, sh) == 0
-                assert lk._lib.loka_grouped_fp8_linear(1, a1, None, 0, sh) == 0
+                assert lk._lib.loka_grouped_fp8_linear(1, a1, ctypes.c_void_p(ws1.data_ptr()), ws1.numel(), sh) == 0
 
             def one_bf16():
                 torch.matmul(xs[i], ws[i][j].t(), out=yb[i][j])
