@@ -103,24 +103,35 @@ __global__ void __launch_bounds__(256) rownorm_kernel(const RowNormParams p) {
         }
       }
   };
-  for (int64_t row = blockIdx.x; row < p.M; row += gridDim.x) {
+  // the next row's loads are issued before this row's reductions (register double buffer): two
+  // rows in flight per CTA keep HBM busy across the block barriers
+  bool ok[V];
+  float4 nx[2 * V];
+  auto load_row = [&](int64_t row) {
     const float* xr = p.y32 + row * p.ld32;
-    float v[8 * V];
-    bool ok[V];
 #pragma unroll
     for (int u = 0; u < V; ++u) {
       const int c = (u * 256 + t) * 8;
-      ok[u] = c < p.N;
-      if (ok[u]) {
-        const float4 a = __ldg(reinterpret_cast<const float4*>(xr + c));
-        const float4 b = __ldg(reinterpret_cast<const float4*>(xr + c) + 1);
-        v[8 * u] = a.x; v[8 * u + 1] = a.y; v[8 * u + 2] = a.z; v[8 * u + 3] = a.w;
-        v[8 * u + 4] = b.x; v[8 * u + 5] = b.y; v[8 * u + 6] = b.z; v[8 * u + 7] = b.w;
+      if (row < p.M && c < p.N) {
+        nx[2 * u] = __ldg(reinterpret_cast<const float4*>(xr + c));
+        nx[2 * u + 1] = __ldg(reinterpret_cast<const float4*>(xr + c) + 1);
       } else {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v[8 * u + k] = 0.f;
+        nx[2 * u] = nx[2 * u + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
+  };
+#pragma unroll
+  for (int u = 0; u < V; ++u) ok[u] = (u * 256 + t) * 8 < p.N;
+  load_row(blockIdx.x);
+  for (int64_t row = blockIdx.x; row < p.M; row += gridDim.x) {
+    float v[8 * V];
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      const float4 a = nx[2 * u], b = nx[2 * u + 1];
+      v[8 * u] = a.x; v[8 * u + 1] = a.y; v[8 * u + 2] = a.z; v[8 * u + 3] = a.w;
+      v[8 * u + 4] = b.x; v[8 * u + 5] = b.y; v[8 * u + 6] = b.z; v[8 * u + 7] = b.w;
+    }
+    load_row(row + gridDim.x);
     float rstd = 1.f, c0 = 0.f;
     if (p.bwd) {
       // NEXT-1 norm backward: g = dh * act'(xhat*gamma + beta) * gamma,
