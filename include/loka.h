@@ -128,6 +128,10 @@ typedef struct loka_tensor {
  * qt : nullable.  K-major copy for backward: codes of the SAME quantization written transposed,
  *      [cols, rows]; qt->scales gets the same scales in the transposed frame's layout
  *      (qt->gran must be the transpose of q->gran: ROW<->COL, 1x128<->128x1, others equal).
+ *      One other combination: q->gran = qt->gran = BLK_1x128 quantizes x TWICE in one pass —
+ *      q = x at 1x128 granules, qt = x at 128x1 granules written transposed (in qt's frame those
+ *      granules are 1x128): the blockwise training recipe's forward and wgrad operands from one
+ *      read of x.
  * phase, amax_dev: see loka_phase; amax_dev is a device float (TENSOR only, else ignored).
  * Bit-exact with oracle/quantize.py (codes as bytes, scales as FP32 bit patterns).            */
 LOKA_API loka_status loka_quantize(const loka_tensor* x, loka_tensor* q, loka_tensor* qt, loka_phase phase,

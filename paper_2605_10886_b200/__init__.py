@@ -176,8 +176,10 @@ def loka_quantize(x: torch.Tensor, fmt: str = "e4m3", gran: str = "row", scale_f
                   phase: str = "full", amax: torch.Tensor | None = None, status: torch.Tensor | None = None,
                   out: torch.Tensor | None = None, scales: torch.Tensor | None = None, want_q: bool = True,
                   transpose: bool = False, out_t: torch.Tensor | None = None, scales_t: torch.Tensor | None = None,
-                  stream=None):
-    """a1-a3.  Returns (codes uint8 [rows, cols] or None, scales fp32) [+ (codes_t, scales_t)]."""
+                  gran_t: str | None = None, stream=None):
+    """a1-a3.  Returns (codes uint8 [rows, cols] or None, scales fp32) [+ (codes_t, scales_t)].
+    gran_t: the transposed copy's granularity in ITS frame (default: the same quantization,
+    transposed); gran="blk_1x128", gran_t="blk_1x128" = x's 128x1 quantization, transposed (one pass)."""
     rows, cols = x.shape
     dev = x.device
     if want_q and out is None:
@@ -190,7 +192,7 @@ def loka_quantize(x: torch.Tensor, fmt: str = "e4m3", gran: str = "row", scale_f
     qt = None
     qt_codes = qt_scales = None
     if transpose:
-        tg = _T_GRAN.get(gran, gran)
+        tg = _T_GRAN.get(gran, gran) if gran_t is None else gran_t
         # K-major copy for the backward GEMMs: leading dimension padded to 16 bytes (TMA)
         qt_codes = out_t if out_t is not None else \
             torch.empty(cols, (rows + 15) // 16 * 16, dtype=torch.uint8, device=dev)[:, :rows]

@@ -176,9 +176,12 @@ loka_status loka_quantize(const loka_tensor* x, loka_tensor* q, loka_tensor* qt,
   if (q->gran < LOKA_GRAN_TENSOR || q->gran > LOKA_GRAN_BLK_128x128) return LOKA_ERR_INVALID_ARG;
   if (phase != LOKA_PHASE_FULL && q->gran != LOKA_GRAN_TENSOR) return LOKA_ERR_INVALID_ARG;
   if (phase != LOKA_PHASE_FULL && !amax_dev) return LOKA_ERR_INVALID_ARG;
+  // dual: q = 1x128 granules, qt = x's own 128x1 quantization written transposed (its t-frame
+  // granule is again 1x128) — one read of x for the blockwise recipe's two operand layouts
+  const bool dual = qt && q->gran == LOKA_GRAN_BLK_1x128 && qt->gran == LOKA_GRAN_BLK_1x128;
   if (qt) {
-    if (qt->dtype != q->dtype || qt->rows != x->cols || qt->cols != x->rows || qt->gran != transpose_gran(q->gran) ||
-        qt->scale_fmt != q->scale_fmt)
+    if (qt->dtype != q->dtype || qt->rows != x->cols || qt->cols != x->rows ||
+        (qt->gran != transpose_gran(q->gran) && !dual) || qt->scale_fmt != q->scale_fmt)
       return LOKA_ERR_SHAPE;
     if (!qt->data || qt->ld < qt->cols) return LOKA_ERR_INVALID_ARG;
   }
@@ -211,8 +214,8 @@ loka_status loka_quantize(const loka_tensor* x, loka_tensor* q, loka_tensor* qt,
   p.scales_t = qt ? qt->scales : nullptr;
   p.status = status_dev;
   cudaError_t e =
-      tiled ? launch_quantize_tiled(p, x->dtype == LOKA_BF16, q->dtype, q->scale_fmt, q->gran, phase, amax, pre,
-                                    reinterpret_cast<cudaStream_t>(stream))
+      tiled ? launch_quantize_tiled(p, x->dtype == LOKA_BF16, q->dtype, q->scale_fmt, dual ? 64 : q->gran, phase, amax,
+                                    pre, reinterpret_cast<cudaStream_t>(stream))
             : launch_quantize(p, x->dtype == LOKA_BF16, q->dtype, q->scale_fmt, q->gran, phase, amax,
                               reinterpret_cast<cudaStream_t>(stream), sms);
   if (e == cudaErrorNotSupported) return LOKA_ERR_UNSUPPORTED;

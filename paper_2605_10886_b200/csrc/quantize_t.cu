@@ -137,6 +137,12 @@ __global__ void __launch_bounds__(256) col_amax_kernel(QuantParams p, uint32_t* 
 // XOR-swizzled by (row / 8) & 7; each thread then reads an 8-row x 4-column block as eight 32-bit
 // words (2-way bank conflicts at most), transposes it in registers with byte permutes (PRMT) and
 // writes 4 transposed rows x 8 bytes; 16 lanes cover 128 contiguous bytes of a transposed row.
+// GRAN = kGranDual: two quantizations of the same tile in one pass (the blockwise training recipe's
+// X and dY, DeepSeek-V3 style): q = 1x128 granules (row-major codes for the forward / dgrad A
+// operand) and qt = the 128x1 granules of x written transposed (K-major A / B of wgrad), i.e. the
+// input is read once for both instead of once per granularity.
+constexpr int kGranDual = 64;
+
 template <typename Tin, int GRAN> struct TileOcc {
   static constexpr int kBlocks =
       sizeof(Tin) == 2 && (GRAN == LOKA_GRAN_TENSOR || GRAN == LOKA_GRAN_ROW || GRAN == LOKA_GRAN_COL) ? 3 : 2;
@@ -180,10 +186,35 @@ __global__ void __launch_bounds__(256, TileOcc<Tin, GRAN>::kBlocks) quant_tile_k
   }
   // ---- granule amax -> cast multiplier per element: rrow[i] (row-like) or rcol[k] (column-like) ----
   constexpr bool kColwise = GRAN == LOKA_GRAN_BLK_128x1 || GRAN == LOKA_GRAN_COL;
+  constexpr bool kDual = GRAN == kGranDual;
   float rrow[8], rcol[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) rrow[i] = rcol[i] = 1.f;
-  if constexpr (GRAN == LOKA_GRAN_BLK_1x128) {
+  if constexpr (kDual) {  // 128x1 of x for the transposed copy (t-frame 1x128 scales [cols, nbr])
+    uint32_t colm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) colm[k] = max(colm[k], v[i].abits(k));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) colm[k] = max(colm[k], __shfl_xor_sync(0xFFFFFFFFu, colm[k], 16));
+    if (lane < 16) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) red[warp][cl + k] = colm[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      uint32_t m = 0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) m = max(m, red[w][cl + k]);
+      float s, r;
+      scales_from_amax<FMT, SF>(__uint_as_float(m), s, r);
+      rcol[k] = r;
+      if (warp == 0 && lane < 16 && k < nc && p.scales_t) p.scales_t[(c + k) * nbr + blockIdx.y] = s;
+    }
+  }
+  if constexpr (GRAN == LOKA_GRAN_BLK_1x128 || kDual) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       uint32_t m = 0;
@@ -197,7 +228,7 @@ __global__ void __launch_bounds__(256, TileOcc<Tin, GRAN>::kBlocks) quant_tile_k
       const int64_t row = r0 + warp * 16 + i * 2 + (lane >> 4);
       if ((lane & 15) == 0 && row < p.rows) {
         if (p.scales) p.scales[row * nbc + blockIdx.x] = s;
-        if (p.scales_t) p.scales_t[(int64_t)blockIdx.x * p.rows + row] = s;  // t-frame BLK_128x1 [nbc, rows]
+        if (!kDual && p.scales_t) p.scales_t[(int64_t)blockIdx.x * p.rows + row] = s;  // t-frame BLK_128x1 [nbc, rows]
       }
       rrow[i] = r;
     }
@@ -298,7 +329,16 @@ __global__ void __launch_bounds__(256, TileOcc<Tin, GRAN>::kBlocks) quant_tile_k
       else
         for (int k = 0; k < nc; ++k) dst[k] = (uint8_t)((k < 4 ? lo : hi) >> (8 * (k & 3)));
     }
-    if (p.qt) *reinterpret_cast<uint2*>(&tq[tq_off(lr, cl)]) = make_uint2(lo, hi);
+    if (p.qt) {
+      if constexpr (kDual) {  // the 128x1 quantization for the transposed copy
+#pragma unroll
+        for (int k = 0; k < 8; ++k) f[k] = __fmul_rn(v[i].f(k), rcol[k]);
+        *reinterpret_cast<uint2*>(&tq[tq_off(lr, cl)]) =
+            make_uint2(cvt_fp8x4<FMT>(f[0], f[1], f[2], f[3]), cvt_fp8x4<FMT>(f[4], f[5], f[6], f[7]));
+      } else {
+        *reinterpret_cast<uint2*>(&tq[tq_off(lr, cl)]) = make_uint2(lo, hi);
+      }
+    }
   }
   if (p.qt) {
     __syncthreads();
@@ -373,6 +413,7 @@ static cudaError_t launch_tiled_t(const QuantParams& p, int gran, int phase, flo
       return launch_pdl_t(quant_tile_kernel<Tin, FMT, SF, LOKA_GRAN_BLK_128x1>, tiles, dim3(256), st, p, ag);
     case LOKA_GRAN_BLK_128x128:
       return launch_pdl_t(quant_tile_kernel<Tin, FMT, SF, LOKA_GRAN_BLK_128x128>, tiles, dim3(256), st, p, ag);
+    case kGranDual: return launch_pdl_t(quant_tile_kernel<Tin, FMT, SF, kGranDual>, tiles, dim3(256), st, p, ag);
     default: return cudaErrorInvalidValue;
   }
 }

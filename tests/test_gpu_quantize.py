@@ -74,6 +74,25 @@ def test_transposed_copy(gran, shape, dtype):
     assert_scales_equal(st, np.ascontiguousarray(ts).reshape(lk.scale_shape(cols, rows, tg)))
 
 
+@pytest.mark.parametrize("shape", [(130, 272), (256, 384), (300, 100), (1, 16), (257, 1040)])
+@pytest.mark.parametrize("fmt,scale_fmt", [("e4m3", "f32"), ("e5m2", "ue8m0"), ("e4m3", "ue8m0")])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_dual_1x128_and_128x1_transposed(shape, fmt, scale_fmt, dtype):
+    """One pass, two quantizations (the blockwise recipe's X / dY): q = x at 1x128 granules,
+    qt = x at 128x1 granules written transposed; each bit-exact against its own oracle quantize."""
+    rows, cols = shape
+    x = _inputs(rows, cols, dtype, seed=rows + 3 * cols)
+    q, s, qt, st = lk.loka_quantize(to_dev_padded(x), fmt, "blk_1x128", scale_fmt, transpose=True, gran_t="blk_1x128")
+    torch.cuda.synchronize()
+    oq, os_ = oracle.quantize.quantize(x.double().numpy(), fmt, "blk_1x128", scale_fmt)
+    assert_scales_equal(s, os_, "1x128 scales")
+    assert_bytes_equal(q, oq, "1x128 codes")
+    tq, ts = oracle.quantize.quantize(x.double().numpy(), fmt, "blk_128x1", scale_fmt)
+    assert_bytes_equal(qt, tq.T.copy(), "128x1 codes, transposed")
+    ts = ts.reshape(lk.scale_shape(rows, cols, "blk_128x1")).T  # [nbr, cols] -> t-frame 1x128 [cols, nbr]
+    assert_scales_equal(st, np.ascontiguousarray(ts).reshape(lk.scale_shape(cols, rows, "blk_1x128")), "128x1 scales")
+
+
 def test_nonfinite_sets_status():
     x = synth.gaussian(8, 256, 1)
     x[5, 17] = float("nan")

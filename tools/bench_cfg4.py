@@ -87,9 +87,13 @@ def main():
             t_f, t_d, t_w = tmean(one(fa)), tmean(one(da)), tmean(one(wa))
 
             def quant(src, fmt, g_plain, g_t, q, s, qt, st):
-                # one pass writes both layouts when the two directions share the granules
+                # one pass writes both layouts when the two directions share the granules, or for the
+                # 1x128 / 128x1-transposed pair (the tile kernel's dual mode)
                 if g_plain == g_t:
                     lk.loka_quantize(src, fmt, g_plain, sf, out=q, scales=s, transpose=True, out_t=qt, scales_t=st)
+                elif g_plain == "blk_1x128" and g_t == "blk_128x1":
+                    lk.loka_quantize(src, fmt, g_plain, sf, out=q, scales=s, transpose=True, out_t=qt, scales_t=st,
+                                     gran_t="blk_1x128")
                 else:
                     lk.loka_quantize(src, fmt, g_plain, sf, out=q, scales=s)
                     lk.loka_quantize(src, fmt, g_t, sf, want_q=False, transpose=True, out_t=qt, scales_t=st)
