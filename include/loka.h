@@ -75,7 +75,12 @@ typedef enum loka_gran {
   LOKA_GRAN_COL = 2,
   LOKA_GRAN_BLK_1x128 = 3,
   LOKA_GRAN_BLK_128x1 = 4,
-  LOKA_GRAN_BLK_128x128 = 5
+  LOKA_GRAN_BLK_128x128 = 5,
+  /* MXFP8 block (NEXT-4): 1 row x 32 columns, scales [rows, ceil(cols/32)].  Quantize: row-major
+   * codes only (no transposed copy).  GEMM: with UE8M0 scales on A and/or B it runs on the
+   * block-scaled MMA (kind::mxf8f6f4.block_scale, one scale per 32-wide K block, its native
+   * granule); combinations: A in {1x128, 1x32} x B in {128x128, 1x128, 1x32}.                  */
+  LOKA_GRAN_BLK_1x32 = 6
 } loka_gran;
 
 /* F32: s = fl32(amax/max), r = fl32(max/amax) (D1).  UE8M0: s = 2^e, the smallest

@@ -23,7 +23,9 @@ import numpy as np
 
 from . import fp8
 
-GRANS = ("tensor", "row", "col", "blk_1x128", "blk_128x1", "blk_128x128")
+# blk_1x32: the MX block (OCP MXFP8 block size 32; NEXT-4), one scale per row per 32 columns
+GRANS = ("tensor", "row", "col", "blk_1x128", "blk_128x1", "blk_128x128", "blk_1x32")
+_BLK = {"blk_1x128": (1, 128), "blk_128x1": (128, 1), "blk_128x128": (128, 128), "blk_1x32": (1, 32)}
 
 
 class NonFiniteInput(ValueError):
@@ -42,6 +44,7 @@ def scale_shape(rows: int, cols: int, gran: str):
         "blk_1x128": (rows, _cdiv(cols, 128)),
         "blk_128x1": (_cdiv(rows, 128), cols),
         "blk_128x128": (_cdiv(rows, 128), _cdiv(cols, 128)),
+        "blk_1x32": (rows, _cdiv(cols, 32)),
     }[gran]
 
 
@@ -54,6 +57,7 @@ def granule_index(i: int, j: int, gran: str):
         "blk_1x128": (i, j // 128),
         "blk_128x1": (i // 128, j),
         "blk_128x128": (i // 128, j // 128),
+        "blk_1x32": (i, j // 32),
     }[gran]
 
 
@@ -68,7 +72,7 @@ def granule_slices(rows: int, cols: int, gran: str):
         for j in range(cols):
             yield (j,), slice(0, rows), slice(j, j + 1)
     else:
-        br, bc = {"blk_1x128": (1, 128), "blk_128x1": (128, 1), "blk_128x128": (128, 128)}[gran]
+        br, bc = _BLK[gran]
         for bi in range(_cdiv(rows, br)):
             for bj in range(_cdiv(cols, bc)):
                 yield (bi, bj), slice(bi * br, min(rows, (bi + 1) * br)), slice(bj * bc, min(cols, (bj + 1) * bc))
@@ -146,7 +150,7 @@ def expand(scale_arr, rows: int, cols: int, gran: str) -> np.ndarray:
         return np.repeat(a.reshape(rows, 1), cols, axis=1)
     if gran == "col":
         return np.repeat(a.reshape(1, cols), rows, axis=0)
-    br, bc = {"blk_1x128": (1, 128), "blk_128x1": (128, 1), "blk_128x128": (128, 128)}[gran]
+    br, bc = _BLK[gran]
     full = np.repeat(np.repeat(a, br, axis=0), bc, axis=1)
     return full[:rows, :cols]
 

@@ -27,7 +27,7 @@ _lib = C.CDLL(LIB_PATH)
 OK, ERR_INVALID_ARG, ERR_SHAPE, ERR_UNSUPPORTED, ERR_NONFINITE, ERR_WORKSPACE, ERR_CUDA = range(7)
 DEVSTATUS_NONFINITE = 0x1
 F32, BF16, E4M3, E5M2 = range(4)
-GRAN = {"tensor": 0, "row": 1, "col": 2, "blk_1x128": 3, "blk_128x1": 4, "blk_128x128": 5}
+GRAN = {"tensor": 0, "row": 1, "col": 2, "blk_1x128": 3, "blk_128x1": 4, "blk_128x128": 5, "blk_1x32": 6}
 SCALE = {"f32": 0, "ue8m0": 1}
 PHASE = {"full": 0, "amax": 1, "cast": 2}
 NORM = {"none": 0, "layer": 1, "rms": 2, "block_rms": 3}
@@ -166,7 +166,8 @@ def _tensor(data, dtype: int, rows: int, cols: int, scales=None, gran="tensor", 
 def scale_shape(rows: int, cols: int, gran: str):
     cd = lambda a, b: -(-a // b)
     return {"tensor": (1,), "row": (rows,), "col": (cols,), "blk_1x128": (rows, cd(cols, 128)),
-            "blk_128x1": (cd(rows, 128), cols), "blk_128x128": (cd(rows, 128), cd(cols, 128))}[gran]
+            "blk_128x1": (cd(rows, 128), cols), "blk_128x128": (cd(rows, 128), cd(cols, 128)),
+            "blk_1x32": (rows, cd(cols, 32))}[gran]
 
 
 _T_GRAN = {"row": "col", "col": "row", "blk_1x128": "blk_128x1", "blk_128x1": "blk_1x128"}

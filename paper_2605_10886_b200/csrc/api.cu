@@ -173,7 +173,8 @@ loka_status loka_quantize(const loka_tensor* x, loka_tensor* q, loka_tensor* qt,
   if (!x->data || !aligned16(x->data) || x->ld < x->cols || (x->ld * elem_size(x->dtype)) % 16) return LOKA_ERR_INVALID_ARG;
   if (!q->scales) return LOKA_ERR_INVALID_ARG;
   if (q->data && (!aligned16(q->data) || q->ld < q->cols || q->ld % 16)) return LOKA_ERR_INVALID_ARG;
-  if (q->gran < LOKA_GRAN_TENSOR || q->gran > LOKA_GRAN_BLK_128x128) return LOKA_ERR_INVALID_ARG;
+  if (q->gran < LOKA_GRAN_TENSOR || q->gran > LOKA_GRAN_BLK_1x32) return LOKA_ERR_INVALID_ARG;
+  if (qt && q->gran == LOKA_GRAN_BLK_1x32) return LOKA_ERR_UNSUPPORTED;  // MX blocks: row-major codes only
   if (phase != LOKA_PHASE_FULL && q->gran != LOKA_GRAN_TENSOR) return LOKA_ERR_INVALID_ARG;
   if (phase != LOKA_PHASE_FULL && !amax_dev) return LOKA_ERR_INVALID_ARG;
   // dual: q = 1x128 granules, qt = x's own 128x1 quantization written transposed (its t-frame
@@ -186,7 +187,8 @@ loka_status loka_quantize(const loka_tensor* x, loka_tensor* q, loka_tensor* qt,
     if (!qt->data || qt->ld < qt->cols) return LOKA_ERR_INVALID_ARG;
   }
   // the tiled cast(-transpose) path serves column-spanning granules and transposed copies
-  const bool tiled = (qt != nullptr || q->gran == LOKA_GRAN_COL || q->gran == LOKA_GRAN_BLK_128x1) &&
+  const bool tiled = (qt != nullptr || q->gran == LOKA_GRAN_COL || q->gran == LOKA_GRAN_BLK_128x1 ||
+                      q->gran == LOKA_GRAN_BLK_1x32) &&
                      phase != LOKA_PHASE_AMAX_ONLY;
   int sms = 148;
   loka_status st = check_device(&sms);
@@ -274,8 +276,9 @@ loka_status loka_quantize_grouped(int32_t G, const loka_tensor* x, loka_tensor* 
 // product: the full epilogue (bias, every norm, FP8 output) works as for rowwise.  The scales
 // are repacked into the MMA's 512-byte UE8M0 atoms in the workspace (sfpack.cu) first.
 static bool is_mx(const loka_linear_args* a) {
-  return a && a->a.gran == LOKA_GRAN_BLK_1x128 &&
-         (a->b.gran == LOKA_GRAN_BLK_128x128 || a->b.gran == LOKA_GRAN_BLK_1x128) &&
+  return a && (a->a.gran == LOKA_GRAN_BLK_1x128 || a->a.gran == LOKA_GRAN_BLK_1x32) &&
+         (a->b.gran == LOKA_GRAN_BLK_128x128 || a->b.gran == LOKA_GRAN_BLK_1x128 ||
+          a->b.gran == LOKA_GRAN_BLK_1x32) &&
          a->a.scale_fmt == LOKA_SCALE_UE8M0 && a->b.scale_fmt == LOKA_SCALE_UE8M0;
 }
 static size_t mx_pack_a_bytes(const loka_linear_args* a) {
@@ -306,9 +309,10 @@ static loka_status mx_pack(const loka_linear_args* a, LinearParams* p, void* ws,
   SfPackParams sp;
   std::memset(&sp, 0, sizeof(sp));
   sp.kblocks = (int32_t)kbs;
-  sp.seg[0] = {a->a.scales, kbs, a->M, 1, (int32_t)cdiv(a->M, 128), wa};
-  sp.seg[1] = {a->b.scales, kbs, a->N, a->b.gran == LOKA_GRAN_BLK_128x128 ? 128 : 1, (int32_t)(cdiv(a->N, 256) * 2),
-               wb};
+  const bool a32 = a->a.gran == LOKA_GRAN_BLK_1x32, b32 = a->b.gran == LOKA_GRAN_BLK_1x32;
+  sp.seg[0] = {a->a.scales, a32 ? cdiv(a->K, 32) : kbs, a->M, 1, (int32_t)cdiv(a->M, 128), wa, a32 ? 1 : 0};
+  sp.seg[1] = {a->b.scales, b32 ? cdiv(a->K, 32) : kbs, a->N, a->b.gran == LOKA_GRAN_BLK_128x128 ? 128 : 1,
+               (int32_t)(cdiv(a->N, 256) * 2), wb, b32 ? 1 : 0};
   if (launch_sf_pack(sp, s) != cudaSuccess) return LOKA_ERR_CUDA;
   p->sfa_pack = wa;
   p->sfb_pack = wb;

@@ -91,6 +91,7 @@ struct SfPackSeg {
   int32_t row_div;      // 1 (1x128 scales) or 128 (128x128 scales)
   int32_t row_blocks;   // 128-row atoms to write (>= ceil(rows/128))
   uint8_t* out;         // [row_blocks][kblocks][512]
+  int32_t k32;          // 1: MX 1x32 scales (one per 32-wide K block, [rows, ld = ceil(K/32)])
 };
 struct SfPackParams {
   SfPackSeg seg[2];

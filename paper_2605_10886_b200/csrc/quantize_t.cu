@@ -232,6 +232,22 @@ __global__ void __launch_bounds__(256, TileOcc<Tin, GRAN>::kBlocks) quant_tile_k
       }
       rrow[i] = r;
     }
+  } else if constexpr (GRAN == LOKA_GRAN_BLK_1x32) {  // MX block: 4 lanes x 8 columns
+    const int64_t nb32 = (p.cols + 31) / 32;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      uint32_t m = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) m = max(m, v[i].abits(k));
+#pragma unroll
+      for (int o = 2; o >= 1; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+      if (m >= 0x7F800000u && (lane & 3) == 0 && p.status) atomicOr(p.status, LOKA_DEVSTATUS_NONFINITE);
+      float s, r;
+      scales_from_amax<FMT, SF>(__uint_as_float(m), s, r);
+      const int64_t row = r0 + warp * 16 + i * 2 + (lane >> 4);
+      if ((lane & 3) == 0 && row < p.rows && nc > 0 && p.scales) p.scales[row * nb32 + (c >> 5)] = s;
+      rrow[i] = r;
+    }
   } else if constexpr (GRAN == LOKA_GRAN_BLK_128x1 || GRAN == LOKA_GRAN_BLK_128x128) {
     uint32_t colm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
@@ -414,6 +430,8 @@ static cudaError_t launch_tiled_t(const QuantParams& p, int gran, int phase, flo
     case LOKA_GRAN_BLK_128x128:
       return launch_pdl_t(quant_tile_kernel<Tin, FMT, SF, LOKA_GRAN_BLK_128x128>, tiles, dim3(256), st, p, ag);
     case kGranDual: return launch_pdl_t(quant_tile_kernel<Tin, FMT, SF, kGranDual>, tiles, dim3(256), st, p, ag);
+    case LOKA_GRAN_BLK_1x32:
+      return launch_pdl_t(quant_tile_kernel<Tin, FMT, SF, LOKA_GRAN_BLK_1x32>, tiles, dim3(256), st, p, ag);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -37,6 +37,17 @@ __global__ void __launch_bounds__(256) sf_pack_kernel(const SfPackParams p) {
   for (int j = 0; j < 4; ++j) {
     const int64_t r = rb * 128 + 32 * j + i;
     uint32_t e = 127u;
+    if (s.k32) {  // MX 1x32: byte kk = the scale of K block 4 kb + kk (127 past the end)
+      uint32_t b = 0;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int64_t col = (int64_t)kb * 4 + kk;
+        const uint32_t ek = (r < s.rows && col < s.ld) ? (__float_as_uint(s.scales[r * s.ld + col]) >> 23) & 0xFFu : 127u;
+        b |= ek << (8 * kk);
+      }
+      w[j] = b;
+      continue;
+    }
     if (r < s.rows) e = (__float_as_uint(s.scales[(r / s.row_div) * s.ld + kb]) >> 23) & 0xFFu;
     w[j] = e * 0x01010101u;
   }

@@ -187,3 +187,49 @@ def test_mx_pair_engine_vs_oracle(b_gran, a_fmt, od):
     rms = np.sqrt(np.mean(yo ** 2, axis=1, keepdims=True))
     extra = 2.0 ** -8 * np.abs(yo) if od == "bf16" else 0.0
     assert np.all(np.abs(yg - yo) <= TOL * np.maximum(np.abs(yo), rms) + extra)
+
+
+# ---- MXFP8 (NEXT-4): 1x32 blocks, the block-scaled MMA's native granule ----------------------
+def _exact_1x32(M, N, K, seed, b_gran):
+    """Integer codes times per-32-block powers of two (A 1x32, B per b_gran): every product and
+    partial sum exact in FP32, so any scale applied to the wrong row / column / 32-wide K block (a
+    wrong byte in the scale atoms or a wrong sf_id) changes the result."""
+    g = torch.Generator().manual_seed(seed)
+    xi = torch.randint(-8, 9, (M, K), generator=g).float()
+    wi = torch.randint(-8, 9, (N, K), generator=g).float()
+    ea = torch.randint(-2, 3, (M, K // 32), generator=g).float()
+    xv = xi * torch.repeat_interleave(2.0 ** ea, 32, dim=1)
+    if b_gran == "blk_1x32":
+        eb = torch.randint(-2, 3, (N, K // 32), generator=g).float()
+        wv = wi * torch.repeat_interleave(2.0 ** eb, 32, dim=1)
+    else:
+        eb = torch.randint(-1, 2, (N // 128, K // 128), generator=g).float()
+        wv = wi * torch.repeat_interleave(torch.repeat_interleave(2.0 ** eb, 128, dim=0), 128, dim=1)
+    xq, xs = lk.loka_quantize(xv.to(DEV), "e4m3", "blk_1x32", "ue8m0")
+    wq, ws = lk.loka_quantize(wv.to(DEV), "e4m3", b_gran, "ue8m0")
+    return xv, wv, xq, xs, wq, ws
+
+
+@pytest.mark.parametrize("M,N,K,b_gran", [(256, 256, 512, "blk_1x32"), (300, 384, 640, "blk_128x128"),
+                                          (2176, 2560, 384, "blk_1x32")])
+def test_mxfp8_1x32_exact(M, N, K, b_gran):
+    xv, wv, xq, xs, wq, ws = _exact_1x32(M, N, K, M + K, b_gran)
+    y, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, a_gran="blk_1x32", b_gran=b_gran, a_scale_fmt="ue8m0",
+                                   b_scale_fmt="ue8m0", out_dtype="f32")
+    torch.cuda.synchronize()
+    assert np.array_equal(f64(y), xv.double().numpy() @ wv.double().numpy().T)
+
+
+@pytest.mark.parametrize("M,N,K,norm", [(200, 384, 1000, "layer"), (512, 1024, 512, "none"),
+                                        (2048, 2816, 1000, "none")])
+def test_mxfp8_1x32_vs_oracle(M, N, K, norm):
+    x, w = synth.heavy(M, K, 31), synth.weight(N, K, 32)
+    xq, xs = lk.loka_quantize(to_dev_padded(x), "e4m3", "blk_1x32", "ue8m0")
+    wq, ws = lk.loka_quantize(to_dev_padded(w), "e4m3", "blk_1x32", "ue8m0")
+    y, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, a_gran="blk_1x32", b_gran="blk_1x32", a_scale_fmt="ue8m0",
+                                   b_scale_fmt="ue8m0", norm=norm, out_dtype="f32")
+    torch.cuda.synchronize()
+    rows = np.sort(np.random.default_rng(3).choice(M, min(M, 64), replace=False))
+    yo = oracle.linear.linear_norm(xq.cpu().numpy()[rows], xs.cpu().numpy()[rows], "e4m3", "blk_1x32",
+                                   wq.cpu().numpy(), ws.cpu().numpy(), "e4m3", "blk_1x32", norm=norm)
+    assert guarded_rel_err(f64(y)[rows], yo) <= TOL

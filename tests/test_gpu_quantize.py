@@ -24,7 +24,7 @@ def _inputs(rows, cols, dtype, seed):
 
 
 @pytest.mark.parametrize("shape", SHAPES)
-@pytest.mark.parametrize("gran", ["row", "col", "blk_1x128", "blk_128x1", "blk_128x128", "tensor"])
+@pytest.mark.parametrize("gran", ["row", "col", "blk_1x128", "blk_128x1", "blk_128x128", "tensor", "blk_1x32"])
 @pytest.mark.parametrize("fmt", ["e4m3", "e5m2"])
 @pytest.mark.parametrize("scale_fmt", ["f32", "ue8m0"])
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])

@@ -100,6 +100,25 @@ def test_quantize_matches_bruteforce(f, gran, scale_fmt):
     assert np.array_equal(codes, bc)
 
 
+def test_mx_1x32_blocks_closed_form():
+    """blk_1x32 (the MX block): one scale per row per 32 columns; a 1x128 granule whose four 32-column
+    sub-blocks have the same amax gives four copies of the 1x128 scale (D7), and a row whose
+    32-blocks hold amax 1, 2, 4, 8 gets the four different UE8M0 scales 2^(b-8) (smallest 2^e with
+    amax <= 448 * 2^e, e4m3)."""
+    x = np.zeros((2, 128))
+    for b in range(4):
+        x[0, 32 * b + 5] = 2.0 ** b
+        x[1, 32 * b + 7] = -3.0
+    c32, s32 = Q.quantize(x, "e4m3", "blk_1x32", "ue8m0")
+    assert s32.shape == (2, 4)
+    assert list(s32[0]) == [2.0 ** (b - 8) for b in range(4)]  # 448 * 2^(b-9) < 2^b <= 448 * 2^(b-8)
+    assert np.array_equal(s32[1], np.full(4, 2.0 ** -7, np.float32))  # 3 > 448 * 2^-8
+    c128, s128 = Q.quantize(x[1:], "e4m3", "blk_1x128", "ue8m0")
+    assert np.array_equal(np.repeat(s128, 4, axis=1), s32[1:]) and np.array_equal(c128, c32[1:])
+    assert Q.scale_shape(3, 65, "blk_1x32") == (3, 3)
+    assert Q.granule_index(2, 64, "blk_1x32") == (2, 2)
+
+
 def test_ue8m0_definition_edges():
     """s = smallest power of two (>= 2^-127) with a <= max*s; probed at max*2^j and neighbours."""
     for f, fm in FMAX.items():

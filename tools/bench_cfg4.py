@@ -116,6 +116,27 @@ def main():
                 "end_to_end_tflops": round(3 * fl / t_s / 1e9, 1),
             }
             del keep
+        # MXFP8 forward (NEXT-4): 1x32 UE8M0 blocks on A and B (the MMA's native granule); forward only
+        # (the transposed 32x1 copies the backward needs are not built)
+        xm, xms = lk.loka_quantize(x, "e4m3", "blk_1x32", "ue8m0")
+        wm, wms = lk.loka_quantize(w, "e4m3", "blk_1x32", "ue8m0")
+        keep = []
+        ma, ym, _ = lk.make_linear_args(xm, xms, wm, wms, a_gran="blk_1x32", b_gran="blk_1x32", a_scale_fmt="ue8m0",
+                                        b_scale_fmt="ue8m0", out_dtype="bf16", keep=keep)
+        wsm = torch.empty(max(1, lk.linear_workspace(ma)), dtype=torch.uint8, device=dev)
+        import ctypes
+        callm = lambda: lk._lib.loka_fp8_linear_norm(ctypes.byref(ma), ctypes.c_void_p(wsm.data_ptr()), wsm.numel(),
+                                                     stream.cuda_stream)
+        t_m = tmean(callm)
+
+        def mstep():
+            lk.loka_quantize(x, "e4m3", "blk_1x32", "ue8m0", out=xm, scales=xms)
+            lk.loka_quantize(w, "e4m3", "blk_1x32", "ue8m0", out=wm, scales=wms)
+            assert callm() == 0
+        t_ms = tmean(mstep)
+        res["mxfp8_fwd"] = {"gemm_ms": round(t_m, 4), "gemm_tflops": round(fl / t_m / 1e9, 1),
+                            "fwd_with_quantize_ms": round(t_ms, 4)}
+        del keep
         # BF16 path
         xb, wb, dyb = x, w, dy
         yb = torch.empty(M, N, dtype=torch.bfloat16, device=dev)
@@ -128,6 +149,7 @@ def main():
                        "step_tflops": round(3 * fl / (b_f + b_d + b_w) / 1e9, 1), "impl": "torch.matmul (cuBLAS)"}
         for name in RECIPES:
             res[name]["speedup_vs_bf16_end_to_end"] = round((b_f + b_d + b_w) / res[name]["step_ms_end_to_end"], 3)
+        res["mxfp8_fwd"]["speedup_vs_bf16_fwd"] = round(b_f / res["mxfp8_fwd"]["fwd_with_quantize_ms"], 3)
     print(json.dumps(res))
     if a.out:
         open(a.out, "w").write(json.dumps(res, indent=1))
