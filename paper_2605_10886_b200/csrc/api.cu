@@ -726,10 +726,20 @@ loka_status loka_fp8_linear_norm(const loka_linear_args* a, void* ws, size_t ws_
   return e == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
 }
 
+// All-gather transport of the stack's hand-offs (StackParams::gather); LOKA_STACK_GATHER overrides
+// the default for measurements (0 bulk DSMEM copies, 1 L2 + multicast TMA, 2 st.async).
+static int stack_gather_mode() {
+  static const int mode = [] {
+    const char* e = std::getenv("LOKA_STACK_GATHER");
+    const int v = e ? std::atoi(e) : kStackGatherL2;
+    return v >= 0 && v <= 2 ? v : (int)kStackGatherL2;
+  }();
+  return mode;
+}
 // Layer l's hand-off is all-gathered through L2 (global codes + multicast TMA loads) when the
 // cluster has peers and the CTA's slice is whole 128-wide K blocks (BN_l = N_l / C >= 128).
 static bool stack_l2_handoff(const loka_stack_args* a, int C, int l) {
-  return C > 1 && l + 1 < a->L && a->dims[l + 1] / C >= 128;
+  return stack_gather_mode() == kStackGatherL2 && C > 1 && l + 1 < a->L && a->dims[l + 1] / C >= 128;
 }
 static int stack_cluster(const loka_stack_args* a) {
   int64_t maxN = 0;
@@ -817,6 +827,7 @@ loka_status loka_fp8_mlp_stack(const loka_stack_args* a, loka_stream_t stream) {
     if (p.h_save[l] && !make_map_u8(&p.th[l], p.h_save[l], a->M, a->dims[l + 1], p.h_ld[l], 128))
       return LOKA_ERR_CUDA;
   }
+  p.gather = stack_gather_mode();
   loka_status st = check_device();
   if (st != LOKA_OK) return st;
   return launch_stack(p, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;

@@ -478,6 +478,14 @@ LOKA_DEVINL void bulk_copy_s2cluster(uint32_t dst_cluster, uint32_t src_cta, uin
                "r"(src_cta), "r"(bytes), "r"(mbar_cluster)
                : "memory");
 }
+// Remote (cluster peer) 16-B store that completes as 16 transaction bytes on the peer's mbarrier
+// (st.async: no barrier on the sender's side; the receiver waits on its own mbarrier).
+LOKA_DEVINL void st_async_u4(uint32_t dst_cluster, uint4 v, uint32_t mbar_cluster) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1,%2,%3,%4}, [%5];" ::"r"(
+                   dst_cluster),
+               "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(mbar_cluster)
+               : "memory");
+}
 LOKA_DEVINL void st_dsmem_f32(uint32_t addr, float v) {
   asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }

@@ -126,7 +126,9 @@ struct StackParams {
   int32_t h_ld[kMaxStackLayers];
   float* hs_save[kMaxStackLayers];    // nullable: its row scales [M]
   CUtensorMap th[kMaxStackLayers];    // map over h_save[l], box {128, 128}, SW128 (multicast loads)
+  int32_t gather;                     // all-gather transport: kStackGather* (stack.cu)
 };
+constexpr int kStackGatherDsmemBulk = 0, kStackGatherL2 = 1, kStackGatherStAsync = 2;
 cudaError_t launch_stack(const StackParams& p, cudaStream_t st);
 long long stack_debug_trace(int enable, unsigned long long* out, long long n);  // see loka_debug_trace
 

@@ -22,9 +22,10 @@
 
 namespace loka {
 
-constexpr int kQtStages = 2;
-constexpr int kQtRows = 8;                         // rows per stage = consumer warps
-constexpr int kQtThreads = 32 * (kQtRows + 1);     // + producer warp
+constexpr int kQtMaxStages = 12;  // ring depth: as many 8-row stages as fit (>= 2), so a CTA's whole
+                                  // share of a small grouped launch (cfg2: ~8 stages) is in flight at once
+// rows per stage = consumer warps (template R): 8 for long rows, 16 for rows <= 4 KB (each warp
+// works through its rows one after another, so short rows want more warps in flight per SM)
 constexpr int kQtMaxRowBytes = 16384;              // input row bytes per stage slot
 
 template <typename Tin> struct QtIn;
@@ -55,12 +56,13 @@ template <> struct QtIn<__nv_bfloat16> {
 
 // Work items are groups of 8 consecutive rows of one tensor of the QuantGroup (a single tensor
 // is a group of one); item gg belongs to tensor t with rgs[t] <= gg < rgs[t+1] (row-group prefix).
+template <int R>
 LOKA_DEVINL int qt_locate(const QuantGroup& grp, int64_t gg, int64_t& first_row) {
   int64_t acc = 0;
   for (int t = 0; t < grp.G; ++t) {
-    const int64_t n = (grp.p[t].rows + kQtRows - 1) / kQtRows;
+    const int64_t n = (grp.p[t].rows + R - 1) / R;
     if (gg < acc + n) {
-      first_row = (gg - acc) * kQtRows;
+      first_row = (gg - acc) * R;
       return t;
     }
     acc += n;
@@ -69,20 +71,21 @@ LOKA_DEVINL int qt_locate(const QuantGroup& grp, int64_t gg, int64_t& first_row)
   return -1;
 }
 
-template <typename Tin, int FMT, int SF, int GRAN>
-__global__ void __launch_bounds__(kQtThreads, 1)
-    quant_tma_kernel(const __grid_constant__ QuantGroup grp, int64_t ngroups, int max_cols, const float* amax_dev) {
+template <typename Tin, int FMT, int SF, int GRAN, int kQtRows>
+__global__ void __launch_bounds__(32 * (kQtRows + 1), 1)
+    quant_tma_kernel(const __grid_constant__ QuantGroup grp, int64_t ngroups, int max_cols, int nstages,
+                     const float* amax_dev) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   const int slot_in = (max_cols * (int)sizeof(Tin) + 127) & ~127, slot_out = (max_cols + 127) & ~127;
   uint8_t* sin = smem;                                          // [stage][row][slot_in]
-  uint8_t* sout = smem + kQtStages * kQtRows * slot_in;         // [warp][2][slot_out]
+  uint8_t* sout = smem + nstages * kQtRows * slot_in;           // [warp][2][slot_out]
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(sout + kQtRows * 2 * slot_out);
-  uint64_t* empty_bar = full_bar + kQtStages;
+  uint64_t* empty_bar = full_bar + kQtMaxStages;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kQtStages; ++s) {
+    for (int s = 0; s < nstages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], kQtRows);
     }
@@ -93,12 +96,12 @@ __global__ void __launch_bounds__(kQtThreads, 1)
 
   if (warp == kQtRows) {  // ===== producer =====
     if (lane == 0) {
-      int it = 0;
-      for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x, ++it) {
-        const int s = it % kQtStages;
-        mbar_wait(&empty_bar[s], ((uint32_t)(it / kQtStages) & 1u) ^ 1u, 1);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+        mbar_wait(&empty_bar[s], ph ^ 1u, 1);
         int64_t r0;
-        const QuantParams& p = grp.p[qt_locate(grp, g, r0)];
+        const QuantParams& p = grp.p[qt_locate<kQtRows>(grp, g, r0)];
         const int in_bytes = (int)(p.cols * (int64_t)sizeof(Tin));
         const int nr = (int)imin64(kQtRows, p.rows - r0);
         mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(nr * in_bytes));
@@ -108,6 +111,7 @@ __global__ void __launch_bounds__(kQtThreads, 1)
                         reinterpret_cast<const uint8_t*>(p.x) + row * p.ldx * (int64_t)sizeof(Tin),
                         (uint32_t)in_bytes, &full_bar[s]);
         }
+        if (++s == nstages) s = 0, ph ^= 1u;
       }
     }
     return;
@@ -123,14 +127,16 @@ __global__ void __launch_bounds__(kQtThreads, 1)
       if (grp.p[0].scales_t) grp.p[0].scales_t[0] = s_t;
     }
   }
-  int it = 0, nst = 0;
-  for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x, ++it) {
-    const int s = it % kQtStages;
+  int nst = 0, s = -1;
+  uint32_t ph = 1;
+  for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+    if (++s == nstages) s = 0;
+    if (s == 0) ph ^= 1u;
     int64_t r0;
-    const QuantParams& p = grp.p[qt_locate(grp, g, r0)];
+    const QuantParams& p = grp.p[qt_locate<kQtRows>(grp, g, r0)];
     const int in_bytes = (int)(p.cols * (int64_t)sizeof(Tin)), out_bytes = (int)p.cols;
     const int64_t row = r0 + warp;
-    if (lane == 0) mbar_wait(&full_bar[s], (uint32_t)(it / kQtStages) & 1u, 2);
+    if (lane == 0) mbar_wait(&full_bar[s], ph, 2);
     __syncwarp();
     if (row >= p.rows) {  // ragged last group: nothing to read, release the slot
       if (lane == 0) mbar_arrive(&empty_bar[s]);
@@ -178,9 +184,21 @@ __global__ void __launch_bounds__(kQtThreads, 1)
   if (lane == 0) bulk_wait0();
 }
 
-size_t quant_tma_smem(int64_t cols, int in_elem) {
+static int quant_tma_rows(int64_t cols, int in_elem) { return cols * in_elem <= 4096 ? 16 : 8; }
+static size_t quant_tma_smem_n(int64_t cols, int in_elem, int nstages) {
   const int64_t slot_in = (cols * in_elem + 127) & ~int64_t(127), slot_out = (cols + 127) & ~int64_t(127);
-  return (size_t)(kQtStages * kQtRows * slot_in + kQtRows * 2 * slot_out + 128 + 128);
+  const int R = quant_tma_rows(cols, in_elem);
+  return (size_t)(nstages * R * slot_in + R * 2 * slot_out + 2 * kQtMaxStages * 8 + 128);
+}
+// deepest ring (<= kQtMaxStages) that fits in 227 KB; 0 if not even two stages fit
+static int quant_tma_stages(int64_t cols, int in_elem) {
+  for (int n = kQtMaxStages; n >= 2; --n)
+    if (quant_tma_smem_n(cols, in_elem, n) <= 227 * 1024) return n;
+  return 0;
+}
+size_t quant_tma_smem(int64_t cols, int in_elem) {
+  const int n = quant_tma_stages(cols, in_elem);
+  return n ? quant_tma_smem_n(cols, in_elem, n) : (size_t)-1;
 }
 
 bool quant_tma_eligible(const QuantParams& p, bool in_bf16, int gran) {
@@ -193,11 +211,12 @@ bool quant_tma_eligible(const QuantParams& p, bool in_bf16, int gran) {
   return quant_tma_smem(p.cols, 2) <= 227 * 1024;
 }
 
-template <int FMT, int SF, int GRAN>
-static cudaError_t launch_qt(const QuantGroup& grp, int64_t max_cols, const float* amax_dev, int num_sms,
-                             cudaStream_t st) {
-  auto kern = quant_tma_kernel<__nv_bfloat16, FMT, SF, GRAN>;
+template <int FMT, int SF, int GRAN, int kQtRows>
+static cudaError_t launch_qt_r(const QuantGroup& grp, int64_t max_cols, const float* amax_dev, int num_sms,
+                               cudaStream_t st) {
+  auto kern = quant_tma_kernel<__nv_bfloat16, FMT, SF, GRAN, kQtRows>;
   const size_t smem = quant_tma_smem(max_cols, 2);
+  const int nstages = quant_tma_stages(max_cols, 2);
   static int attr_bytes = 0;  // per instantiation; the attribute only needs to grow
   if ((int)smem > attr_bytes) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -209,7 +228,7 @@ static cudaError_t launch_qt(const QuantGroup& grp, int64_t max_cols, const floa
   if (ngroups == 0) return cudaSuccess;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(ngroups < num_sms ? ngroups : num_sms));
-  cfg.blockDim = dim3(kQtThreads);
+  cfg.blockDim = dim3(32 * (kQtRows + 1));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -218,7 +237,13 @@ static cudaError_t launch_qt(const QuantGroup& grp, int64_t max_cols, const floa
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   note_launch();
-  return cudaLaunchKernelEx(&cfg, kern, grp, ngroups, (int)max_cols, amax_dev);
+  return cudaLaunchKernelEx(&cfg, kern, grp, ngroups, (int)max_cols, nstages, amax_dev);
+}
+template <int FMT, int SF, int GRAN>
+static cudaError_t launch_qt(const QuantGroup& grp, int64_t max_cols, const float* amax_dev, int num_sms,
+                             cudaStream_t st) {
+  if (quant_tma_rows(max_cols, 2) == 16) return launch_qt_r<FMT, SF, GRAN, 16>(grp, max_cols, amax_dev, num_sms, st);
+  return launch_qt_r<FMT, SF, GRAN, 8>(grp, max_cols, amax_dev, num_sms, st);
 }
 
 cudaError_t launch_quantize_tma_group(const QuantGroup& grp, int64_t max_cols, int fmt, int scale_fmt, int gran,

@@ -14,7 +14,7 @@
 //     normalisation, row amax from ymax/ymin) produces the next layer's e4m3 codes and row scale
 //     and writes the codes into the CTA's own A tile; the slice then reaches the peers through L2:
 //     TMA store of its K blocks to a global hand-off buffer, then one TMA load per K block
-//     multicast to every peer, completing on the peer's slice barrier (kSGatherL2; the SM-to-SM
+//     multicast to every peer, completing on the peer's slice barrier (kStackGatherL2; the SM-to-SM
 //     alternative — one bulk DSMEM copy per peer — measured ~4% slower).  Slices narrower than a
 //     128-wide K block go by per-thread DSMEM stores + a cluster barrier;
 //   * only the last layer's output goes to HBM (swizzled staging tile + TMA store); the global
@@ -89,11 +89,10 @@ LOKA_DEVINL SRow merge_rows(const SRow (&r)[K]) {
 // multiplied) was measured SLOWER: two N=128 passes re-read A from shared memory and the MMA
 // becomes shared-memory-bandwidth bound (A + B bytes per FLOP double).  Kept switchable.
 constexpr bool kSplitHalves = false;
-// All-gather of a layer's hand-off among the cluster: through L2 (codes stored to global memory,
-// multicast TMA loads back into the peers' A tiles) or SM-to-SM (bulk DSMEM copies).  Measured
-// equal on cfg2 (~4 us per 96 KB per CTA either way); L2 is the default because the global copy
-// doubles as the saved activation training needs.
-constexpr bool kSGatherL2 = true;
+// All-gather of a layer's hand-off among the cluster (StackParams::gather): through L2 (codes
+// stored to global memory, multicast TMA loads back into the peers' A tiles), SM-to-SM by bulk
+// DSMEM copies of the staged slice, or SM-to-SM straight from registers (st.async, each 16-B piece
+// completing on the peer's slice mbarrier: no staging, fence, CTA barrier or store/load round trip).
 
 // Layer schedule shared by the producer and the MMA issuer: unit u in [0, nh * nkb) is
 // (half h = u / nkb, K block kb); within a half the K blocks go slice by slice, own slice first.
@@ -304,6 +303,11 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
     const float2 rr = make_float2(r_out, r_out);
     const uint32_t a_local = smem_u32(c.smem + kSOffA);
     uint8_t* hsave = p.h_save[l];
+    const bool gl2 = p.gather == kStackGatherL2;
+    const bool st_async = p.gather == kStackGatherStAsync && c.C > 1;
+    // st.async pieces complete on the receiver's barrier of this CTA's slice (a_bar[0] when the
+    // slices are narrower than a K block and the next layer waits for the whole input at once)
+    const uint32_t bar_own = smem_u32(&c.a_bar[BN >= 128 ? c.rank : 0]);
 #pragma unroll
     for (int h = 0; h < NH; ++h) {
 #pragma unroll
@@ -320,13 +324,18 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
         const uint32_t off = (uint32_t)(k >> 7) * 16384u + (uint32_t)c.r * 128u +
                              ((((uint32_t)(k & 127) >> 4) ^ ((uint32_t)c.r & 7u)) << 4);
         sts_u4(a_local + off, make_uint4(w[0], w[1], w[2], w[3]));
-        if constexpr (BN < 128) {  // slice not contiguous in the swizzled tile: per-thread DSMEM stores
+        if (st_async) {
+          for (int t = 1; t < c.C; ++t) {
+            const uint32_t rk = (uint32_t)((c.rank + t) % c.C);
+            st_async_u4(mapa_shared(a_local + off, rk), make_uint4(w[0], w[1], w[2], w[3]), mapa_shared(bar_own, rk));
+          }
+        } else if constexpr (BN < 128) {  // slice not contiguous in the swizzled tile: per-thread DSMEM stores
           const float4 v = make_float4(__uint_as_float(w[0]), __uint_as_float(w[1]), __uint_as_float(w[2]),
                                        __uint_as_float(w[3]));
           for (int rk = 0; rk < c.C; ++rk)
             if (rk != c.rank) st_dsmem_f4(mapa_shared(a_local + off, (uint32_t)rk), v);
         }
-        if (hsave && c.row_ok && !(kSGatherL2 && BN >= 128 && c.C > 1))  // (L2 gather: TMA-stored below)
+        if (hsave && c.row_ok && !(gl2 && BN >= 128 && c.C > 1))  // (L2 gather: TMA-stored below)
           *reinterpret_cast<uint4*>(hsave + (size_t)c.grow * p.h_ld[l] + k) = make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
@@ -339,7 +348,22 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
         mbar_arrive(&c.a_bar[0]);
         LOKA_STRACE(c, 2 + 7 * l + 5);
       }
-    } else if (BN >= 128 && kSGatherL2) {
+    } else if (st_async) {
+      // own codes: generic smem writes -> async proxy (own MMA); the peers' pieces are in flight
+      fence_proxy_async_smem();
+      named_bar_sync(1, kSThreads);
+      if (threadIdx.x == 0) {
+        const uint32_t bytes = (uint32_t)BN * 128u;
+        if (BN >= 128) {
+          mbar_arrive(&c.a_bar[c.rank]);  // own slice
+          for (int s = 0; s < c.C; ++s)
+            if (s != c.rank) mbar_arrive_expect_tx(&c.a_bar[s], bytes);  // peers' slices (same BN)
+        } else {
+          mbar_arrive_expect_tx(&c.a_bar[0], (uint32_t)(c.C - 1) * bytes);  // whole input, one barrier
+        }
+        LOKA_STRACE(c, 2 + 7 * l + 5);
+      }
+    } else if (BN >= 128 && gl2) {
       // The slice [n0, n0 + BN) of h_{l+1} is BN/128 whole 16 KB K blocks of the A tile.  Its
       // codes also went to global memory (p.h_save[l], L2-resident); one TMA load per K block,
       // multicast to every peer, brings them back into the peers' A tiles and completes on each
@@ -546,6 +570,7 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
             mbar_wait(&a_bar[src], (aph >> src) & 1u, 5);
             aph ^= 1u << src;
             tc_fence_after();
+            fence_proxy_async_smem();  // peers' st.async pieces (generic proxy) -> this thread's MMAs
             if (l > 0) LOKA_STRACE(c, 2 + 7 * (l - 1) + 6);
           }
           const int st = mma_it % kSStages;
