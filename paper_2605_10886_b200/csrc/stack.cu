@@ -35,13 +35,13 @@ constexpr int kSThreads = 512;  // 16 warps: warp 0 lane 0 = TMA producer, warp 
                                 // then all 16 warps run each layer's epilogue
 constexpr int kSStages = 2;
 constexpr int kSKMax = 1024;
-constexpr int kSRec = 6;
 constexpr int kSOffA = 0;                                // [kb][128 rows][128 B] (<= 128 KB)
 constexpr int kSOffW = 128 * kSKMax;                     // weight ring [stage][<= 256 rows][128 B]
 constexpr int kSStageW = 256 * 128;
 constexpr int kSOffCs = kSOffW + kSStages * kSStageW;    // [8][128] float4 cluster records
 constexpr int kSOffCol = kSOffCs + 8 * 128 * 16;         // [256] W row scales of this slice
-constexpr int kSOffBar = kSOffCol + 256 * 4;
+constexpr int kSOffHx = kSOffCol + 256 * 4;             // [4][128] float4 column-quarter records
+constexpr int kSOffBar = kSOffHx + 4 * 128 * 16;
 constexpr int kSSmem = kSOffBar + 256 + 1024;
 static_assert(kSSmem <= 227 * 1024, "stack smem");
 
@@ -52,6 +52,13 @@ static_assert(kSSmem <= 227 * 1024, "stack smem");
 constexpr int kSTraceCtas = 512;
 static __device__ unsigned long long g_strace[kSTraceCtas * 64];
 static __device__ int g_strace_on;
+// fine trace of layer 1 (clock64 per CTA: slots 0-31 thread 0, 32-63 warp 15 lane 0)
+static __device__ unsigned long long g_sfine[kSTraceCtas * 64];
+#define LOKA_FST(c, l, i)                                                                          \
+  do {                                                                                             \
+    if ((c).trace && (l) == 1 && (c).cta < kSTraceCtas && (threadIdx.x == 0 || threadIdx.x == 480)) \
+      g_sfine[(c).cta * 64 + (threadIdx.x ? 32 : 0) + (i)] = clock64();                            \
+  } while (0)
 #define LOKA_STRACE(c, slot)                                                                    \
   do {                                                                                          \
     if ((c).trace && (c).cta < kSTraceCtas) g_strace[(c).cta * 64 + (slot)] = globaltimer_ns(); \
@@ -61,6 +68,43 @@ struct SRow {
   float n, mean, m2, ss, ymax, ymin;
   LOKA_DEVINL void init() { n = 0.f; mean = 0.f; m2 = 0.f; ss = 0.f; ymax = -INFINITY; ymin = INFINITY; }
 };
+// Record of a row segment as one float4: (mean | sum of squares, M2, ymax, ymin); n is implicit.
+LOKA_DEVINL float4 rec4(const SRow& r, int norm) {
+  return make_float4(norm == LOKA_NORM_LAYER ? r.mean : r.ss, r.m2, r.ymax, r.ymin);
+}
+// Merge of kv <= K records of equal counts n_each (Chan et al. with equal weights: no division;
+// inv_k = 1/kv).  Every CTA merges the same records in the same order: identical statistics.
+template <int K>
+LOKA_DEVINL SRow merge_eq(const float4 (&v)[K], int kv, float n_each, float inv_k, int norm) {
+  SRow o;
+  o.init();
+  o.n = (float)kv * n_each;
+  float s = 0.f, m2 = 0.f;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    if (k < kv) {
+      s += v[k].x;
+      m2 += v[k].y;
+      o.ymax = fmaxf(o.ymax, v[k].z);
+      o.ymin = fminf(o.ymin, v[k].w);
+    }
+  }
+  if (norm == LOKA_NORM_LAYER) {
+    o.mean = s * inv_k;
+    float d2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (k < kv) {
+        const float d = v[k].x - o.mean;
+        d2 = fmaf(d, d, d2);
+      }
+    }
+    o.m2 = fmaf(n_each, d2, m2);
+  } else {
+    o.ss = s;
+  }
+  return o;
+}
 template <int K>
 LOKA_DEVINL SRow merge_rows(const SRow (&r)[K]) {
   SRow o;
@@ -124,6 +168,7 @@ struct SCtx {
   int trace, cta;
   uint64_t* a_bar;     // [8] per-slice "layer input complete" barriers
   uint64_t* half_bar;  // [2] accumulator half ready
+  uint64_t* stat_bar;  // cluster row-statistics records arrived (one phase per layer)
   bool row_ok;
 };
 
@@ -187,19 +232,23 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
   const int n0 = c.rank * BN;
   const bool last = l + 1 == p.L;
   const bool fold = norm != LOKA_NORM_NONE;  // no bias in the stack: s_a goes into eps
-  float* cs = reinterpret_cast<float*>(c.smem + kSOffCs);
-  float* hx = reinterpret_cast<float*>(c.smem + kSOffA);  // A is drained once our MMAs completed
+  const uint32_t cs = smem_u32(c.smem + kSOffCs);
+  const uint32_t hx = smem_u32(c.smem + kSOffHx);
   const uint32_t col_s = smem_u32(c.smem + kSOffCol);
   const float ys = fold ? 1.f : sa;
+  // the cluster's records of this layer arrive as st.async transactions on stat_bar
+  if (c.C > 1 && threadIdx.x == 0) mbar_arrive_expect_tx(c.stat_bar, (uint32_t)c.C * 128u * 16u);
 
   // ---- accumulator halves -> registers (dequant, partial statistics) as each half completes ----
   float y[CPT];
   SRow hrec[NH];
 #pragma unroll
   for (int h = 0; h < NH; ++h) {
+    LOKA_FST(c, l, 0);
     if (c.lane == 0) mbar_wait(&c.half_bar[h], (hph >> h) & 1u, 3);
     __syncwarp();
     tc_fence_after();
+    LOKA_FST(c, l, 1);
     if (h == 0 && threadIdx.x == 0) LOKA_STRACE(c, 2 + 7 * l + 2);
     const int cbh = h * 128 + c.cq * SEG;
     const uint32_t taddr = c.tmem_base + ((uint32_t)(c.q * 32) << 16) + (uint32_t)cbh;
@@ -212,70 +261,79 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
     }
 #pragma unroll
     for (int i = 0; i < SEG / 16; ++i) tmem_wait16(yh + 16 * i);
+    LOKA_FST(c, l, 2);
 #pragma unroll
     for (int j = 0; j < SEG; j += 4) {
-      const float4 s4 = lds_f4(col_s + (uint32_t)(cbh + j) * 4u);
-      const float2 a = fmul2(make_float2(yh[j], yh[j + 1]), fmul2(make_float2(s4.x, s4.y), make_float2(ys, ys)));
-      const float2 b = fmul2(make_float2(yh[j + 2], yh[j + 3]), fmul2(make_float2(s4.z, s4.w), make_float2(ys, ys)));
+      float4 s4 = lds_f4(col_s + (uint32_t)(cbh + j) * 4u);
+      if (!fold) {
+        const float2 u = fmul2(make_float2(s4.x, s4.y), make_float2(ys, ys));
+        const float2 v = fmul2(make_float2(s4.z, s4.w), make_float2(ys, ys));
+        s4 = make_float4(u.x, u.y, v.x, v.y);
+      }
+      const float2 a = fmul2(make_float2(yh[j], yh[j + 1]), make_float2(s4.x, s4.y));
+      const float2 b = fmul2(make_float2(yh[j + 2], yh[j + 3]), make_float2(s4.z, s4.w));
       yh[j] = a.x; yh[j + 1] = a.y; yh[j + 2] = b.x; yh[j + 3] = b.y;
     }
+    LOKA_FST(c, l, 3);
     hrec[h] = seg_stats<SEG>(yh, norm);
+    LOKA_FST(c, l, 4);
   }
   hph ^= NH == 2 ? 3u : 1u;
   SRow rec = NH == 2 ? merge_rows(hrec) : hrec[0];
 
-  // ---- merge the four column quarters (component-major records in smem) ----
+  // ---- merge the four column quarters (float4 records in a dedicated smem area) ----
   {
-    float* my = hx + (size_t)c.cq * kSRec * 128 + c.r;
-    my[0] = rec.n; my[128] = rec.mean; my[256] = rec.m2; my[384] = rec.ss; my[512] = rec.ymax; my[640] = rec.ymin;
+    const float4 mine = rec4(rec, norm);
+    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(hx + (uint32_t)(c.cq * 128 + c.r) * 16u), "f"(mine.x),
+                 "f"(mine.y), "f"(mine.z), "f"(mine.w)
+                 : "memory");
     named_bar_sync(1, kSThreads);
-    SRow parts[4];
+    LOKA_FST(c, l, 5);
+    float4 parts[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float* o = hx + (size_t)k * kSRec * 128 + c.r;
-      parts[k].n = o[0]; parts[k].mean = o[128]; parts[k].m2 = o[256]; parts[k].ss = o[384];
-      parts[k].ymax = o[512]; parts[k].ymin = o[640];
-    }
-    rec = merge_rows(parts);
+    for (int k = 0; k < 4; ++k) parts[k] = lds_f4(hx + (uint32_t)(k * 128 + c.r) * 16u);
+    rec = merge_eq(parts, 4, (float)CPT, 0.25f, norm);
+    LOKA_FST(c, l, 6);
     if (threadIdx.x == 0) LOKA_STRACE(c, 2 + 7 * l + 3);
-    if (c.C == 1) named_bar_sync(1, kSThreads);  // hx (aliasing A) read by all before A is rewritten
   }
-  // ---- cluster exchange: push (mean|ss, m2, ymax, ymin) to every peer, barrier, merge ----
+  // ---- cluster exchange: every CTA's row records st.async'ed to every CTA (own included),
+  //      completing on each receiver's stat_bar; merged in rank order ----
   if (c.C > 1) {
     if (c.cq == 0) {
-      const float4 v = make_float4(norm == LOKA_NORM_LAYER ? rec.mean : rec.ss, rec.m2, rec.ymax, rec.ymin);
-      const uint32_t la = smem_u32(cs + ((size_t)c.rank * 128 + c.r) * 4);
-      for (int rk = 0; rk < c.C; ++rk) st_dsmem_f4(mapa_shared(la, (uint32_t)rk), v);
-    }
-    cluster_sync_all();  // barrier 1: also proves every cluster CTA finished this layer's MMAs
-    if (threadIdx.x == 0) LOKA_STRACE(c, 2 + 7 * l + 4);
-    SRow parts[8];
-#pragma unroll
-    for (int rk = 0; rk < 8; ++rk) {
-      parts[rk].init();
-      if (rk < c.C) {
-        const float4 v = lds_f4(smem_u32(cs + ((size_t)rk * 128 + c.r) * 4));
-        parts[rk].n = (float)BN;
-        parts[rk].mean = norm == LOKA_NORM_LAYER ? v.x : 0.f;
-        parts[rk].m2 = v.y;
-        parts[rk].ss = norm == LOKA_NORM_LAYER ? 0.f : v.x;
-        parts[rk].ymax = v.z;
-        parts[rk].ymin = v.w;
+      const float4 v = rec4(rec, norm);
+      const uint32_t la = cs + (uint32_t)(c.rank * 128 + c.r) * 16u, lb = smem_u32(c.stat_bar);
+      for (int t = 0; t < c.C; ++t) {
+        const uint32_t rk = (uint32_t)((c.rank + t) % c.C);
+        st_async_u4(mapa_shared(la, rk), make_uint4(__float_as_uint(v.x), __float_as_uint(v.y), __float_as_uint(v.z),
+                                                    __float_as_uint(v.w)),
+                    mapa_shared(lb, rk));
       }
     }
-    rec = merge_rows(parts);
+    LOKA_FST(c, l, 7);
+    // Receiving every peer's record also proves every cluster CTA finished this layer's MMAs
+    // (a record is sent after its CTA's accumulator was ready): the peers' A tiles are free.
+    mbar_wait(c.stat_bar, (uint32_t)l & 1u, 6);
+    LOKA_FST(c, l, 8);
+    if (threadIdx.x == 0) LOKA_STRACE(c, 2 + 7 * l + 4);
+    float4 parts[8];
+#pragma unroll
+    for (int rk = 0; rk < 8; ++rk)
+      parts[rk] = rk < c.C ? lds_f4(cs + (uint32_t)(rk * 128 + c.r) * 16u) : make_float4(0.f, 0.f, -INFINITY, INFINITY);
+    rec = merge_eq(parts, c.C, (float)BN, __fdividef(1.f, (float)c.C), norm);  // (exact for C = 2, 4, 8)
+    LOKA_FST(c, l, 9);
   }
   // ---- normalise (one FFMA) ----
   const float eps = p.eps[l];
   // rstd by the hardware reciprocal square root (~2 ulp): the statistics are FP32 estimates of
   // FP64 quantities anyway; only the FP8 scales derived from the normalised values are IEEE-exact
-  const float eps_eff = fold ? eps * __frcp_rn(sa * sa) : eps;
+  const float eps_eff = fold ? __fdividef(eps, sa * sa) : eps;
+  const float inv_n = __fdividef(1.f, rec.n);  // (exact for the power-of-two row widths)
   float rstd = 1.f, c0 = 0.f;
   if (norm == LOKA_NORM_LAYER) {
-    rstd = rsqrtf(fmaf(rec.m2, __frcp_rn(rec.n), eps_eff));
+    rstd = rsqrtf(fmaf(rec.m2, inv_n, eps_eff));
     c0 = -__fmul_rn(rec.mean, rstd);
   } else if (norm == LOKA_NORM_RMS) {
-    rstd = rsqrtf(fmaf(rec.ss, __frcp_rn(rec.n), eps_eff));
+    rstd = rsqrtf(fmaf(rec.ss, inv_n, eps_eff));
   }
   if (norm != LOKA_NORM_NONE) {
     const float2 r2 = make_float2(rstd, rstd), c2 = make_float2(c0, c0);
@@ -286,6 +344,7 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
       y[j + 1] = a.y;
     }
   }
+  LOKA_FST(c, l, 10);
   if (l == 1 && threadIdx.x == 0) LOKA_STRACE(c, 58);
   const bool fp8_next = !last || p.out_dtype == LOKA_E4M3 || p.out_dtype == LOKA_E5M2;
   const int ofmt = last ? p.out_dtype : LOKA_E4M3;
@@ -297,6 +356,7 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
     if (ofmt == LOKA_E5M2) scales_from_amax<LOKA_E5M2, LOKA_SCALE_F32>(amax, s_out, r_out);
     else scales_from_amax<LOKA_E4M3, LOKA_SCALE_F32>(amax, s_out, r_out);
   }
+  LOKA_FST(c, l, 11);
   if (l == 1 && threadIdx.x == 0) LOKA_STRACE(c, 59);
   if (!last) {
     // ---- next layer's A operand: codes into this CTA's swizzled A tile (+ saved hand-off) ----
@@ -340,10 +400,13 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
       }
     }
     if (p.hs_save[l] && c.row_ok && c.rank == 0 && c.cq == 0) p.hs_save[l][c.grow] = s_out;
+    LOKA_FST(c, l, 15);
+    LOKA_FST(c, l, 12);
     if (l == 1 && threadIdx.x == 0) LOKA_STRACE(c, 60);
     if (c.C == 1) {
       fence_proxy_async_smem();  // generic writes -> async proxy (own MMA)
       named_bar_sync(1, kSThreads);
+      LOKA_FST(c, l, 13);
       if (threadIdx.x == 0) {
         mbar_arrive(&c.a_bar[0]);
         LOKA_STRACE(c, 2 + 7 * l + 5);
@@ -369,24 +432,27 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
       // multicast to every peer, brings them back into the peers' A tiles and completes on each
       // peer's slice barrier a_bar[rank] — the all-gather runs on the L2 -> SM path instead of the
       // SM -> SM network (DSMEM: ~14-21 B/clk per SM, measured ~2x slower here).  Peers' A tiles
-      // are free: barrier 1 above proved every cluster CTA's layer-l MMAs (and hx reads) completed.
+      // are free: the stat_bar wait above proved every cluster CTA's layer-l MMAs completed.
       // The data are this CTA's own writes, so a CTA-wide barrier orders them before the load.
       fence_proxy_async_smem();  // generic smem writes -> async proxy (TMA store source, own MMA)
       named_bar_sync(1, kSThreads);
+      LOKA_FST(c, l, 13);
       if (l == 1 && threadIdx.x == 0) LOKA_STRACE(c, 61);
       if (threadIdx.x == 0) {
         const uint32_t bytes = (uint32_t)BN * 128u;
+        // own slice complete: the next layer's MMAs on it start now, under the store round trip
+        mbar_arrive(&c.a_bar[c.rank]);
+        for (int s = 0; s < c.C; ++s)
+          if (s != c.rank) mbar_arrive_expect_tx(&c.a_bar[s], bytes);  // peers' slices (same BN)
         // the slice's K blocks (already swizzled in A) -> global with TMA stores; wait until written
         for (int kb = n0 >> 7; kb < (n0 + BN) >> 7; ++kb) tma_store_2d(&p.th[l], c.smem + kSOffA + kb * 16384, kb * 128, c.m0);
         bulk_commit();
         bulk_wait0();
         fence_proxy_async_global();
+        LOKA_FST(c, l, 14);
         const uint16_t mask = (uint16_t)(((1u << c.C) - 1u) & ~(1u << c.rank));
         for (int kb = n0 >> 7; kb < (n0 + BN) >> 7; ++kb)
           tma_load_2d_mc(c.smem + kSOffA + kb * 16384, &p.th[l], &c.a_bar[c.rank], kb * 128, c.m0, mask);
-        mbar_arrive(&c.a_bar[c.rank]);  // own slice
-        for (int s = 0; s < c.C; ++s)
-          if (s != c.rank) mbar_arrive_expect_tx(&c.a_bar[s], bytes);  // peers' slices (same BN)
         LOKA_STRACE(c, 2 + 7 * l + 5);
       }
     } else if (BN >= 128) {
@@ -487,7 +553,8 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
   uint64_t* empty_bar = full_bar + kSStages;
   uint64_t* a_bar = empty_bar + kSStages;  // [8]
   uint64_t* half_bar = a_bar + 8;          // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(half_bar + 2);
+  uint64_t* stat_bar = half_bar + 2;       // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stat_bar + 1);
 
   SCtx c;
   c.smem = smem;
@@ -503,6 +570,7 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
   c.rank = p.C > 1 ? (int)cluster_ctarank() : 0;
   c.a_bar = a_bar;
   c.half_bar = half_bar;
+  c.stat_bar = stat_bar;
   c.trace = *reinterpret_cast<volatile int*>(&g_strace_on);
   c.cta = blockIdx.x + gridDim.x * blockIdx.y;
   if (threadIdx.x == 0) LOKA_STRACE(c, 0);
@@ -517,6 +585,7 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
     }
     for (int s = 0; s < 8; ++s) mbar_init(&a_bar[s], 1);
     for (int h = 0; h < 2; ++h) mbar_init(&half_bar[h], 1);
+    mbar_init(stat_bar, 1);
     fence_barrier_init();
   }
   if (c.warp == 1) tmem_alloc<256>(tmem_slot);
@@ -590,10 +659,12 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
       LOKA_STRACE(c, 2 + 7 * l + 1);
     }
     __syncwarp();
+    LOKA_FST(c, l, 16);
     // ===== epilogue (all warps) =====
     const float* ws = p.ws[l];
     for (int j = threadIdx.x; j < p.BN[l]; j += kSThreads) col[j] = ws[c.rank * p.BN[l] + j];
     named_bar_sync(1, kSThreads);
+    LOKA_FST(c, l, 17);
     float s_next;
     switch (p.BN[l]) {
       case 64: s_next = stack_epilogue<1, 16>(p, c, l, sa, hph); break;
@@ -618,11 +689,17 @@ long long stack_debug_trace(int enable, unsigned long long* out, long long n) {
   if (out && n > 0) {
     got = n < (long long)kSTraceCtas * 64 ? n : (long long)kSTraceCtas * 64;
     if (cudaMemcpyFromSymbol(out, g_strace, (size_t)got * 8) != cudaSuccess) return -1;
+    if (n > got) {  // the fine layer-1 trace follows
+      const long long g2 = n - got < (long long)kSTraceCtas * 64 ? n - got : (long long)kSTraceCtas * 64;
+      if (cudaMemcpyFromSymbol(out + got, g_sfine, (size_t)g2 * 8) != cudaSuccess) return -1;
+      got += g2;
+    }
   }
   if (enable >= 0) {
     if (enable) {
       static unsigned long long zero[kSTraceCtas * 64];
       if (cudaMemcpyToSymbol(g_strace, zero, sizeof(zero)) != cudaSuccess) return -1;
+      if (cudaMemcpyToSymbol(g_sfine, zero, sizeof(zero)) != cudaSuccess) return -1;
     }
     if (cudaMemcpyToSymbol(g_strace_on, &enable, sizeof(int)) != cudaSuccess) return -1;
   }
