@@ -50,3 +50,15 @@ def _gpu_watchdog(request):
     torch.cuda.synchronize()
     n, tag, blk, thr = lk.debug_hang_info(reset=True)
     assert n == 0, f"pipeline watchdog: {n} timed-out waits, tag={tag} block={blk} thread={thr & 0xffffffff} parity={thr >> 32}"
+
+
+@pytest.fixture(scope="session")
+def fp4_host_cast(tmp_path_factory):
+    """Build the test-only cuda_fp4.hpp host-cast helper (tests/helpers/fp4_host_cast.cpp)."""
+    out = tmp_path_factory.mktemp("helpers4") / "fp4_host_cast"
+    src = os.path.join(ROOT, "tests", "helpers", "fp4_host_cast.cpp")
+    cuda_inc = os.path.join(os.environ.get("CUDA_HOME", "/usr/local/cuda"), "include")
+    r = subprocess.run(["g++", "-O2", "-I", cuda_inc, src, "-o", str(out)], capture_output=True, text=True)
+    if r.returncode != 0:
+        pytest.skip("cannot build cuda_fp4 host helper: " + r.stderr[-300:])
+    return str(out)
