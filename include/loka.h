@@ -244,6 +244,53 @@ LOKA_API loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* 
                                     loka_stream_t stream);
 LOKA_API size_t loka_grouped_workspace_size(int32_t G, const loka_linear_args* args);
 
+/* ---- NEXT-4: NVFP4 ----------------------------------------------------------
+ * The paper names FP4 as future work; the recipe is DESIGN.md D35-D38 (oracle/nvfp4.py):
+ * E2M1 codes (values {0, .5, 1, 1.5, 2, 3, 4, 6}, saturating RNE), one E4M3 block-scale code per
+ * 16 consecutive elements of a row, one FP32 tensor scale s_t = fl32(A / 2688) from the tensor amax A:
+ *   sf = E4M3(fl32(fl32(a_block * r_t) / 6)), codes = E2M1(fl32(x * fl32(r_t / decode(sf)))),
+ *   r_t = fl32(2688 / A); x_hat = e2m1(code) * decode(sf) * s_t.
+ * Ownership and errors as everywhere: caller-owned device memory, async on `stream`.            */
+typedef struct loka_nvfp4_tensor {
+  void* data;               /* packed E2M1 codes [rows, cols/2] bytes; element 2j in the low nibble
+                               of byte j; 16-byte aligned                                         */
+  int64_t rows, cols;       /* logical elements; cols % 64 == 0                                  */
+  int64_t ld;               /* bytes between row starts: >= cols/2, multiple of 16               */
+  uint8_t* block_scales;    /* E4M3 codes [rows, cols/16], row-major, leading dimension cols/16  */
+  float* tensor_scale;      /* device FP32 [1]: s_t                                              */
+} loka_nvfp4_tensor;
+
+/* x: bf16 or f32 [rows, cols] (ld elements, 16-byte aligned rows).  amax_dev: nullable device float
+ * holding the tensor amax to use (data parallel: the all-reduced global amax, as the FP8 tensorwise
+ * split phase); NULL = computed here (workspace >= loka_quantize_nvfp4_workspace_size bytes).
+ * Non-finite input sets LOKA_DEVSTATUS_NONFINITE in *status_dev (when computing the amax).
+ * Bit-exact with oracle/nvfp4.py: codes, block-scale codes and s_t.                              */
+LOKA_API loka_status loka_quantize_nvfp4(const loka_tensor* x, loka_nvfp4_tensor* q, const float* amax_dev,
+                                         int32_t* status_dev, void* ws, size_t ws_bytes, loka_stream_t stream);
+LOKA_API size_t loka_quantize_nvfp4_workspace_size(const loka_tensor* x);
+
+/* y = epilogue(A_hat B_hat^T): A [M,K], B [N,K] NVFP4 (both K-major), on the block-scaled tensor
+ * cores (tcgen05.mma kind::mxf4nvf4.block_scale.scale_vec::4X; FP32 accumulation in TMEM), the
+ * tensor scales s_t(A) s_t(B) applied in the epilogue, then bias / LayerNorm / RMSNorm / BlockNorm
+ * and the output cast exactly as loka_fp8_linear_norm (y: F32 | BF16 | E4M3 + ROW scales).
+ * K % 64 == 0.  Workspace: the scale atoms (loka_nvfp4_linear_workspace_size).                  */
+typedef struct loka_nvfp4_linear_args {
+  int64_t M, N, K;
+  loka_nvfp4_tensor a, b;
+  const void* bias;         /* nullable [N] */
+  loka_dtype bias_dtype;
+  loka_norm norm;
+  int32_t norm_block;
+  float eps;
+  const float* gamma;       /* nullable [N] */
+  const float* beta;        /* nullable [N] */
+  loka_tensor y;
+  int32_t* status_dev;      /* nullable */
+} loka_nvfp4_linear_args;
+LOKA_API loka_status loka_nvfp4_linear_norm(const loka_nvfp4_linear_args* args, void* ws, size_t ws_bytes,
+                                            loka_stream_t stream);
+LOKA_API size_t loka_nvfp4_linear_workspace_size(const loka_nvfp4_linear_args* args);
+
 /* ---- a7: LoKA Probe error statistic ------------------------------------------------------- */
 typedef struct loka_probe_pair {
   const void* out;          /* device [M,N], dtype out_dtype (F32 | BF16): low-precision path */

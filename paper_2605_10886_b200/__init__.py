@@ -83,6 +83,18 @@ class loka_probe_stats(C.Structure):
                 ("count", C.c_int64), ("n_floored", C.c_int64)]
 
 
+class loka_nvfp4_tensor(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("rows", C.c_int64), ("cols", C.c_int64), ("ld", C.c_int64),
+                ("block_scales", C.c_void_p), ("tensor_scale", C.c_void_p)]
+
+
+class loka_nvfp4_linear_args(C.Structure):
+    _fields_ = [("M", C.c_int64), ("N", C.c_int64), ("K", C.c_int64), ("a", loka_nvfp4_tensor),
+                ("b", loka_nvfp4_tensor), ("bias", C.c_void_p), ("bias_dtype", C.c_int), ("norm", C.c_int),
+                ("norm_block", C.c_int32), ("eps", C.c_float), ("gamma", C.c_void_p), ("beta", C.c_void_p),
+                ("y", loka_tensor), ("status_dev", C.c_void_p)]
+
+
 class loka_candidate(C.Structure):
     _fields_ = [("id", C.c_char_p), ("dir", C.c_int), ("mere", C.c_double), ("time_us", C.c_double)]
 
@@ -103,6 +115,11 @@ _sig = {
     "loka_probe_workspace_size": ([C.c_int32, _P(loka_probe_pair)], C.c_size_t),
     "loka_dispatch_select": ([_P(loka_candidate), C.c_int32, C.c_double, C.c_double, C.c_double, _P(C.c_int32)],
                              C.c_int),
+    "loka_quantize_nvfp4": ([_P(loka_tensor), _P(loka_nvfp4_tensor), C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
+                             C.c_void_p], C.c_int),
+    "loka_quantize_nvfp4_workspace_size": ([_P(loka_tensor)], C.c_size_t),
+    "loka_nvfp4_linear_norm": ([_P(loka_nvfp4_linear_args), C.c_void_p, C.c_size_t, C.c_void_p], C.c_int),
+    "loka_nvfp4_linear_workspace_size": ([_P(loka_nvfp4_linear_args)], C.c_size_t),
     "loka_status_string": ([C.c_int], C.c_char_p),
     "loka_device_supported": ([C.c_int32], C.c_int32),
     "loka_version": ([], C.c_int32),
@@ -269,6 +286,67 @@ def loka_fp8_linear_norm(a, a_scales, b, b_scales, stream=None, ws=None, **kw):
     ws, nws = _workspace(linear_workspace(args), a.device, ws)
     _check(_lib.loka_fp8_linear_norm(C.byref(args), None if ws is None else C.c_void_p(ws.data_ptr()), nws,
                                      _stream(stream)), "loka_fp8_linear_norm")
+    return y, ys
+
+
+def _nvfp4_tensor(packed, sf, st, rows, cols):
+    return loka_nvfp4_tensor(packed.data_ptr(), rows, cols, packed.stride(0), sf.data_ptr(), st.data_ptr())
+
+
+def loka_quantize_nvfp4(x: torch.Tensor, amax: torch.Tensor | None = None, status: torch.Tensor | None = None,
+                        out=None, stream=None):
+    """NEXT-4 NVFP4 quantize.  Returns (packed uint8 [rows, cols/2], block-scale codes uint8
+    [rows, cols/16], tensor scale fp32 [1]).  amax: optional device float (the global amax)."""
+    rows, cols = x.shape
+    dev = x.device
+    if out is None:
+        out = (torch.empty(rows, (cols // 2 + 15) // 16 * 16, dtype=torch.uint8, device=dev)[:, :cols // 2],
+               torch.empty(rows, cols // 16, dtype=torch.uint8, device=dev),
+               torch.empty(1, dtype=torch.float32, device=dev))
+    packed, sf, st = out
+    qx = _tensor(x, _dtype_code(x), rows, cols)
+    q = _nvfp4_tensor(packed, sf, st, rows, cols)
+    nws = _lib.loka_quantize_nvfp4_workspace_size(C.byref(qx))
+    ws = torch.empty(nws, dtype=torch.uint8, device=dev)
+    _check(_lib.loka_quantize_nvfp4(C.byref(qx), C.byref(q), _ptr(amax), _ptr(status), _ptr(ws), nws,
+                                    _stream(stream)), "loka_quantize_nvfp4")
+    return packed, sf, st
+
+
+def make_nvfp4_linear_args(a, b, *, norm="none", norm_block=256, eps=0.0, gamma=None, beta=None, bias=None,
+                           out_dtype="f32", y=None, y_scales=None, status=None, keep=None):
+    """a, b: (packed, block_scales, tensor_scale) triples from loka_quantize_nvfp4 (A [M,K], B [N,K])."""
+    (ap, asf, ast), (bp, bsf, bst) = a, b
+    M, K = ap.shape[0], ap.shape[1] * 2
+    N = bp.shape[0]
+    od = {"f32": F32, "bf16": BF16, "e4m3": E4M3, "e5m2": E5M2}[out_dtype]
+    dev = ap.device
+    if y is None:
+        y = torch.empty(M, N, dtype=_TORCH_DT[od], device=dev)
+    if od in (E4M3, E5M2) and y_scales is None:
+        y_scales = torch.empty(M, dtype=torch.float32, device=dev)
+    args = loka_nvfp4_linear_args()
+    args.M, args.N, args.K = M, N, K
+    args.a = _nvfp4_tensor(ap, asf, ast, M, K)
+    args.b = _nvfp4_tensor(bp, bsf, bst, N, K)
+    args.bias = None if bias is None else bias.data_ptr()
+    args.bias_dtype = F32 if bias is None else _dtype_code(bias)
+    args.norm, args.norm_block, args.eps = NORM[norm], norm_block, eps
+    args.gamma = None if gamma is None else gamma.data_ptr()
+    args.beta = None if beta is None else beta.data_ptr()
+    args.y = _tensor(y, od, M, N, y_scales, "row")
+    args.status_dev = None if status is None else status.data_ptr()
+    if keep is not None:
+        keep.extend([ap, asf, ast, bp, bsf, bst, bias, gamma, beta, y, y_scales, status])
+    return args, y, y_scales
+
+
+def loka_nvfp4_linear_norm(a, b, stream=None, ws=None, **kw):
+    """NEXT-4 NVFP4 linear (+bias/norm) on the block-scaled tensor cores.  Returns (y, y_scales)."""
+    args, y, ys = make_nvfp4_linear_args(a, b, **kw)
+    ws, nws = _workspace(int(_lib.loka_nvfp4_linear_workspace_size(C.byref(args))), y.device, ws)
+    _check(_lib.loka_nvfp4_linear_norm(C.byref(args), None if ws is None else C.c_void_p(ws.data_ptr()), nws,
+                                       _stream(stream)), "loka_nvfp4_linear_norm")
     return y, ys
 
 

@@ -320,8 +320,9 @@ static loka_status mx_pack(const loka_linear_args* a, LinearParams* p, void* ws,
   return LOKA_OK;
 }
 
+// nvf4: the operands are NVFP4 presented as byte tensors [rows, K/2] (loka_nvfp4_linear_norm)
 static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CUtensorMap* tb, CUtensorMap* ty,
-                                  LinearParams* p, int* bn_out) {
+                                  LinearParams* p, int* bn_out, bool nvf4 = false) {
   if (!a) return LOKA_ERR_INVALID_ARG;
   const int64_t M = a->M, N = a->N, K = a->K;
   if (M <= 0 || N <= 0 || K <= 0 || M > (1ll << 31) - 1 || N > (1ll << 30) || K > (1ll << 31) - 1)
@@ -332,7 +333,7 @@ static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CU
   if (!A.data || !B.data || !Y.data || !A.scales || !B.scales) return LOKA_ERR_INVALID_ARG;
   if (!aligned16(A.data) || !aligned16(B.data) || !aligned16(Y.data)) return LOKA_ERR_INVALID_ARG;
   if (A.ld < K || B.ld < K || A.ld % 16 || B.ld % 16) return LOKA_ERR_INVALID_ARG;
-  const bool mx = is_mx(a);
+  const bool mx = is_mx(a) || nvf4;
   if (!mx && A.gran != LOKA_GRAN_TENSOR && A.gran != LOKA_GRAN_ROW) return LOKA_ERR_UNSUPPORTED;
   if (!mx && B.gran != LOKA_GRAN_TENSOR && B.gran != LOKA_GRAN_ROW) return LOKA_ERR_UNSUPPORTED;
   if (Y.dtype < LOKA_F32 || Y.dtype > LOKA_E5M2) return LOKA_ERR_INVALID_ARG;
@@ -414,7 +415,7 @@ static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CU
   p->status = a->status_dev;
   p->cluster_n = csize;
   p->act = a->act;
-  p->mx = mx ? 1 : 0;
+  p->mx = nvf4 ? 2 : mx ? 1 : 0;
   p->bwd = bwd ? 1 : 0;
   p->xhat = static_cast<const __nv_bfloat16*>(a->bwd_xhat);
   p->ld_xhat = a->bwd_xhat_ld;
@@ -724,6 +725,111 @@ loka_status loka_fp8_linear_norm(const loka_linear_args* a, void* ws, size_t ws_
   }
   cudaError_t e = launch_linear(ta, tb, ty, p, bn, reinterpret_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
+}
+
+// ---- NEXT-4: NVFP4 (nvfp4.cu + linear.cu MX = 2) ----------------------------------------------
+size_t loka_quantize_nvfp4_workspace_size(const loka_tensor* /*x*/) { return 256; }
+
+loka_status loka_quantize_nvfp4(const loka_tensor* x, loka_nvfp4_tensor* q, const float* amax_dev,
+                                int32_t* status_dev, void* ws, size_t ws_bytes, loka_stream_t stream) {
+  if (!x || !q) return LOKA_ERR_INVALID_ARG;
+  if (x->dtype != LOKA_BF16 && x->dtype != LOKA_F32) return LOKA_ERR_INVALID_ARG;
+  if (x->rows < 0 || x->cols < 0 || q->rows != x->rows || q->cols != x->cols) return LOKA_ERR_SHAPE;
+  if (x->cols % 16) return LOKA_ERR_SHAPE;
+  if (x->rows == 0 || x->cols == 0) return LOKA_OK;
+  const int esz = x->dtype == LOKA_BF16 ? 2 : 4;
+  if (!x->data || !aligned16(x->data) || x->ld < x->cols || (x->ld * esz) % 16) return LOKA_ERR_INVALID_ARG;
+  if (!q->data || !q->block_scales || !q->tensor_scale || q->ld < x->cols / 2 || (reinterpret_cast<uintptr_t>(q->data) & 7) ||
+      q->ld % 8)
+    return LOKA_ERR_INVALID_ARG;
+  int sms = 148;
+  loka_status st = check_device(&sms);
+  if (st != LOKA_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const float* amax = amax_dev;
+  if (!amax) {  // the tensor amax by quantize.cu's amax pass (AMAX_ONLY) into the workspace
+    if (!ws || ws_bytes < 256) return LOKA_ERR_WORKSPACE;
+    QuantParams qp;
+    std::memset(&qp, 0, sizeof(qp));
+    qp.x = x->data;
+    qp.rows = x->rows;
+    qp.cols = x->cols;
+    qp.ldx = x->ld;
+    qp.status = status_dev;
+    if (launch_quantize(qp, x->dtype == LOKA_BF16, LOKA_E4M3, LOKA_SCALE_F32, LOKA_GRAN_TENSOR, LOKA_PHASE_AMAX_ONLY,
+                        reinterpret_cast<float*>(ws), s, sms) != cudaSuccess)
+      return LOKA_ERR_CUDA;
+    amax = reinterpret_cast<const float*>(ws);
+  }
+  Nvfp4QParams p;
+  p.x = x->data;
+  p.rows = x->rows;
+  p.cols = x->cols;
+  p.ldx = x->ld;
+  p.q = static_cast<uint8_t*>(q->data);
+  p.ldq = q->ld;
+  p.sf = q->block_scales;
+  p.ld_sf = x->cols / 16;
+  p.amax = amax;
+  p.s_tensor = q->tensor_scale;
+  return launch_nvfp4_cast(p, x->dtype == LOKA_BF16, sms, s) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
+}
+
+// [ceil(rows/256)*2][4 ceil(K/256)][512]: four 64-wide K atoms per 256-element (128-byte) stage,
+// zero-padded past K
+static size_t nvf4_atoms_bytes(int64_t rows, int64_t K) {
+  return (size_t)(cdiv(rows, 256) * 2) * (size_t)(4 * cdiv(K, 256)) * 512;
+}
+size_t loka_nvfp4_linear_workspace_size(const loka_nvfp4_linear_args* a) {
+  if (!a || a->M <= 0 || a->N <= 0 || a->K <= 0) return 0;
+  return ((nvf4_atoms_bytes(a->M, a->K) + 255) & ~size_t(255)) + nvf4_atoms_bytes(a->N, a->K);
+}
+
+loka_status loka_nvfp4_linear_norm(const loka_nvfp4_linear_args* a, void* ws, size_t ws_bytes, loka_stream_t stream) {
+  if (!a) return LOKA_ERR_INVALID_ARG;
+  const int64_t M = a->M, N = a->N, K = a->K;
+  if (M <= 0 || N <= 0 || K <= 0 || K % 64) return LOKA_ERR_SHAPE;
+  const loka_nvfp4_tensor &A = a->a, &B = a->b;
+  if (A.rows != M || A.cols != K || B.rows != N || B.cols != K) return LOKA_ERR_SHAPE;
+  if (!A.block_scales || !B.block_scales || !A.tensor_scale || !B.tensor_scale) return LOKA_ERR_INVALID_ARG;
+  const size_t need = loka_nvfp4_linear_workspace_size(a);
+  if (!ws || ws_bytes < need || !aligned16(ws)) return LOKA_ERR_WORKSPACE;
+  // the FP8 path's argument checks and tile choice on byte views of the packed operands
+  loka_linear_args la;
+  std::memset(&la, 0, sizeof(la));
+  la.M = M;
+  la.N = N;
+  la.K = K / 2;
+  la.dir = LOKA_DIR_FWD;
+  la.a = {A.data, LOKA_E4M3, M, K / 2, A.ld, A.tensor_scale, LOKA_GRAN_TENSOR, LOKA_SCALE_F32};
+  la.b = {B.data, LOKA_E4M3, N, K / 2, B.ld, B.tensor_scale, LOKA_GRAN_TENSOR, LOKA_SCALE_F32};
+  la.bias = a->bias;
+  la.bias_dtype = a->bias_dtype;
+  la.norm = a->norm;
+  la.norm_block = a->norm_block;
+  la.eps = a->eps;
+  la.gamma = a->gamma;
+  la.beta = a->beta;
+  la.y = a->y;
+  la.status_dev = a->status_dev;
+  CUtensorMap ta, tb, ty;
+  LinearParams p;
+  int bn = 0;
+  loka_status st = prepare_linear(&la, &ta, &tb, &ty, &p, &bn, true);
+  if (st != LOKA_OK) return st;
+  st = check_device();
+  if (st != LOKA_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* wa = static_cast<uint8_t*>(ws);
+  uint8_t* wb = wa + ((nvf4_atoms_bytes(M, K) + 255) & ~size_t(255));
+  const int64_t k64 = 4 * cdiv(K, 256), nblk = K / 16;
+  if (launch_nvfp4_sf_pack(A.block_scales, nblk, M, nblk, cdiv(M, 256) * 2, k64, wa, s) != cudaSuccess ||
+      launch_nvfp4_sf_pack(B.block_scales, nblk, N, nblk, cdiv(N, 256) * 2, k64, wb, s) != cudaSuccess)
+    return LOKA_ERR_CUDA;
+  p.sfa_pack = wa;
+  p.sfb_pack = wb;
+  p.sf_kblocks = (int32_t)cdiv(K / 2, 128);
+  return launch_linear(ta, tb, ty, p, bn, s) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
 }
 
 // All-gather transport of the stack's hand-offs (StackParams::gather); LOKA_STACK_GATHER overrides

@@ -295,6 +295,26 @@ LOKA_DEVINL void mma_mxf8f6f4(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_
       "l"(da), "l"(db), "r"(id), "r"(tsfa | (k << 30)), "r"(tsfb | (k << 30)), "r"(accumulate)
       : "memory");
 }
+// NVFP4 (kind::mxf4nvf4, E2M1 x E2M1, UE4M3 scales, K = 64 per instruction)
+LOKA_DEVINL uint32_t idesc_nvf4(uint32_t M, uint32_t N) {
+  uint32_t d = 0;
+  d |= 1u << 7;   // A: E2M1
+  d |= 1u << 10;  // B: E2M1
+  d |= (N >> 3) << 17;
+  // bit 23 = 0: UE4M3 scales; bit 31 = 0: K = 64
+  d |= (M >> 4) << 24;
+  return d;
+}
+// scale_vec::4X: four 16-element scales per row per MMA = one full 32-bit TMEM column per row
+LOKA_DEVINL void mma_nvf4(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t tsfa, uint32_t tsfb,
+                          uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %6, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::mxf4nvf4.block_scale.scale_vec::4X [%0], %1, %2, %3, [%4], [%5], p;\n}" ::"r"(
+          tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(tsfa), "r"(tsfb), "r"(accumulate)
+      : "memory");
+}
 // smem -> TMEM copy of one 32 x 16 B scale-factor atom, broadcast to the four 32-lane groups
 // (lane i of every group gets row i: 4 TMEM columns).  Source: no-swizzle K-major descriptor,
 // 8-row core matrices 128 B apart (SBO).

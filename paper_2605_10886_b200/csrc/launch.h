@@ -23,6 +23,21 @@ struct QuantParams {
   int32_t* status;
 };
 
+// ---- NVFP4 (nvfp4.cu, NEXT-4) ----
+struct Nvfp4QParams {
+  const void* x;
+  int64_t rows, cols, ldx;  // cols % 16 == 0
+  uint8_t* q;               // packed E2M1 codes [rows, cols/2], ldq bytes
+  int64_t ldq;
+  uint8_t* sf;              // E4M3 block-scale codes [rows, cols/16], ld_sf
+  int64_t ld_sf;
+  const float* amax;        // device: the tensor amax
+  float* s_tensor;          // device: s_t out (nullable)
+};
+cudaError_t launch_nvfp4_cast(const Nvfp4QParams& p, bool in_bf16, int num_sms, cudaStream_t st);
+cudaError_t launch_nvfp4_sf_pack(const uint8_t* sf, int64_t ld, int64_t rows, int64_t nblk, int64_t row_blocks,
+                                 int64_t k64, uint8_t* out, cudaStream_t st);
+
 cudaError_t launch_quantize(const QuantParams& p, bool in_bf16, int fmt, int scale_fmt, int gran, int phase,
                             float* amax_dev, cudaStream_t st, int num_sms);
 
@@ -76,7 +91,9 @@ struct LinearParams {
   __nv_bfloat16* save_xhat; int64_t ld_save_xhat;
   float* save_rstd;
   float* amax_out;               // NEXT-4: atomicMax of |stored y| (bit pattern), nullable
-  // native block-scaled (MX) mode: UE8M0 blockwise scales applied by the tensor core; sa/sb unused
+  // native block-scaled mode: 1 = MX (UE8M0 blockwise scales applied by the tensor core; sa/sb
+  // unused), 2 = NVFP4 (E4M3 block scales by the tensor core; sa/sb = the FP32 tensor scales;
+  // K counts bytes of packed E2M1 codes; atoms [row blocks][sf_kblocks][4][512])
   int32_t mx;
   const uint8_t* sfa_pack;       // [ceil(M/128)][kblocks][512] (sfpack.cu layout)
   const uint8_t* sfb_pack;       // [ceil(N/256)*2][kblocks][512]

@@ -52,15 +52,20 @@ constexpr int kBigCluster = 16;  // non-portable (opt-in): rows up to 16 x 256 =
 
 constexpr uint32_t pow2_cols(uint32_t c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
 
-template <int BN, bool MX = false, int MAXC = kMaxCluster> struct LinCfg {
+// MX: 0 = plain FP8 (scales in the epilogue), 1 = MXFP8 / UE8M0 blockwise (kind::mxf8f6f4
+// .block_scale: one 512 B atom per 128-K stage and 128 rows), 2 = NVFP4 (kind::mxf4nvf4
+// .block_scale.scale_vec::4X: a stage row is 128 B = 256 packed E2M1 elements = 4 MMAs of K = 64,
+// each MMA reading one 512 B atom (128 rows x four 16-element E4M3 scales) per 128 rows).
+template <int BN, int MX = 0, int MAXC = kMaxCluster> struct LinCfg {
   static constexpr int kCPT = BN / 4;  // columns per epilogue thread
   static constexpr int kStageA = 128 * kBK;  // bytes
   static constexpr int kStageB = BN * kBK;
   static constexpr int kStageBytes = kStageA + kStageB;
   // MX mode: per stage one 512 B UE8M0 atom for A and BN/128 for B (bulk-copied with the stage),
   // copied to TMEM columns [BN + s*kSfCols, ...) by tcgen05.cp
-  static constexpr int kSf = MX ? 512 * (1 + BN / 128) : 0;
-  static constexpr int kSfCols = 4 * (1 + BN / 128);
+  static constexpr int kSfAtoms = MX == 2 ? 4 : 1;  // atoms per stage per 128 rows
+  static constexpr int kSf = MX ? 512 * kSfAtoms * (1 + BN / 128) : 0;
+  static constexpr int kSfCols = 4 * kSfAtoms * (1 + BN / 128);
   // everything but the operand ring: column params, pushed cluster records (+ amax), barriers
   static constexpr int kFixed = 4 * BN * 4 + MAXC * 128 * 16 + MAXC * 128 * 4 + 512 + 1024;
   static constexpr int kStagesFit = (227 * 1024 - kFixed) / (kStageBytes + kSf);
@@ -118,7 +123,7 @@ LOKA_DEVINL RowRec merge_recs(const RowRec (&r)[K]) {
   return o;
 }
 
-template <int BN, bool MX, int MAXC>
+template <int BN, int MX, int MAXC>
 __global__ void __launch_bounds__(kThreads, 1)
     linear_norm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                        const __grid_constant__ CUtensorMap tma_y, const LinearParams p) {
@@ -189,12 +194,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive_expect_tx(&full_bar[s], C::kStageBytes + C::kSf);
         tma_load_2d(sA + s * C::kStageA, &tma_a, &full_bar[s], kb * kBK, m0);
         tma_load_2d(sB + s * C::kStageB, &tma_b, &full_bar[s], kb * kBK, n0);
-        if constexpr (MX) {  // the stage's UE8M0 atoms: A rows m0.., B rows n0.. (BN/128 atoms)
+        if constexpr (MX) {  // the stage's scale atoms: A rows m0.., B rows n0.. (BN/128 row blocks)
+          constexpr int kA = 512 * C::kSfAtoms;  // bytes per 128 rows per stage
           uint8_t* sf = smem + C::kOffSf + s * C::kSf;
-          bulk_load_g2s(sf, p.sfa_pack + ((size_t)(m0 >> 7) * p.sf_kblocks + kb) * 512, 512, &full_bar[s]);
+          bulk_load_g2s(sf, p.sfa_pack + ((size_t)(m0 >> 7) * p.sf_kblocks + kb) * kA, kA, &full_bar[s]);
 #pragma unroll
           for (int j = 0; j < BN / 128; ++j)
-            bulk_load_g2s(sf + 512 * (j + 1), p.sfb_pack + ((size_t)((n0 >> 7) + j) * p.sf_kblocks + kb) * 512, 512,
+            bulk_load_g2s(sf + kA * (j + 1), p.sfb_pack + ((size_t)((n0 >> 7) + j) * p.sf_kblocks + kb) * kA, kA,
                           &full_bar[s]);
         }
         if (kb == 0) LOKA_TRACE(2);
@@ -204,7 +210,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ===== MMA issuer =====
     if (lane == 0) {
-      const uint32_t idesc = MX ? idesc_mxf8f6f4(p.a_fmt, p.b_fmt, 128, BN) : idesc_f8f6f4(p.a_fmt, p.b_fmt, 128, BN);
+      const uint32_t idesc = MX == 2   ? idesc_nvf4(128, BN)
+                             : MX == 1 ? idesc_mxf8f6f4(p.a_fmt, p.b_fmt, 128, BN)
+                                       : idesc_f8f6f4(p.a_fmt, p.b_fmt, 128, BN);
       for (int kb = 0; kb < num_kb; ++kb) {
         const int s = kb % C::kStages;
         const uint32_t ph = (uint32_t)(kb / C::kStages) & 1u;
@@ -213,7 +221,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t a0 = smem_u32(sA + s * C::kStageA);
         const uint32_t b0 = smem_u32(sB + s * C::kStageB);
-        if constexpr (MX) {
+        if constexpr (MX == 2) {
+          // scale atoms smem -> TMEM: A atom k at columns sft + 4k; B atom (row block j, k) at
+          // sft + 16 + 4 (k BN/128 + j), so MMA k reads B's BN rows from consecutive columns
+          const uint32_t sft = tmem_base + (uint32_t)(BN + s * C::kSfCols);
+          const uint32_t sfs = smem_u32(smem + C::kOffSf + s * C::kSf);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) utccp_32x128b_warpx4(sft + 4u * k, sfs + 512u * k);
+#pragma unroll
+          for (int j = 0; j < BN / 128; ++j)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              utccp_32x128b_warpx4(sft + 16u + 4u * (k * (BN / 128) + j), sfs + 2048u * (j + 1) + 512u * k);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            mma_nvf4(tmem_base, smem_desc_kmajor_sw128(a0 + k * 32), smem_desc_kmajor_sw128(b0 + k * 32), idesc,
+                     sft + 4u * k, sft + 16u + 4u * k * (BN / 128), (kb | k) != 0);
+        } else if constexpr (MX == 1) {
           // scales smem -> TMEM (executes in order with the MMAs issued by this thread)
           const uint32_t sft = tmem_base + (uint32_t)(BN + s * C::kSfCols);
           const uint32_t sfs = smem_u32(smem + C::kOffSf + s * C::kSf);
@@ -247,7 +271,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int cb = cq * CPT;                         // first local column of this thread
     const int nv = max(0, min(CPT, ncols - cb));     // valid columns of this thread
     const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)cb;
-    const float sa = row_ok ? (MX ? 1.f : p.sa[p.sa_row ? grow : 0]) : 0.f;  // MX: scales applied by the MMA
+    // MX: block scales applied by the MMA (NVFP4: the FP32 tensor scales remain, as sa / sb)
+    const float sa = row_ok ? (MX == 1 ? 1.f : p.sa[p.sa_row ? grow : 0]) : 0.f;
     const bool has_bias = p.bias != nullptr;
     const bool fold = !has_bias && norm != LOKA_NORM_NONE && !bwd;  // s_a folded into eps
     const float ys = fold ? 1.f : sa;
@@ -258,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = threadIdx.x; j < BN; j += kEpiThreads) {
       const int n = n0 + j;
       const bool ok = n < p.N;
-      col[j] = ok ? (MX ? 1.f : p.sb[p.sb_row ? n : 0]) : 0.f;
+      col[j] = ok ? (MX == 1 ? 1.f : p.sb[p.sb_row ? n : 0]) : 0.f;
       float b = 0.f;
       if (ok && p.bias) b = p.bias_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.bias)[n])
                                          : reinterpret_cast<const float*>(p.bias)[n];
@@ -743,7 +768,7 @@ long long debug_trace(int enable, unsigned long long* out, long long n) {
   return got;
 }
 
-template <int BN, bool MX, int MAXC = kMaxCluster>
+template <int BN, int MX, int MAXC = kMaxCluster>
 static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, const LinearParams& p,
                              cudaStream_t st) {
   using C = LinCfg<BN, MX, MAXC>;
@@ -782,19 +807,26 @@ cudaError_t launch_linear(const CUtensorMap& ta, const CUtensorMap& tb, const CU
                           int bn, cudaStream_t st) {
   if (p.cluster_n > kMaxCluster) {  // rows of 2304..4096 columns: 16-CTA cluster, BN = 256
     if (bn != 256 || p.mx || p.cluster_n > kBigCluster) return cudaErrorInvalidValue;
-    return launch_bn<256, false, kBigCluster>(ta, tb, ty, p, st);
+    return launch_bn<256, 0, kBigCluster>(ta, tb, ty, p, st);
+  }
+  if (p.mx == 2) {
+    switch (bn) {
+      case 128: return launch_bn<128, 2>(ta, tb, ty, p, st);
+      case 256: return launch_bn<256, 2>(ta, tb, ty, p, st);
+      default: return cudaErrorInvalidValue;
+    }
   }
   if (p.mx) {
     switch (bn) {
-      case 128: return launch_bn<128, true>(ta, tb, ty, p, st);
-      case 256: return launch_bn<256, true>(ta, tb, ty, p, st);
+      case 128: return launch_bn<128, 1>(ta, tb, ty, p, st);
+      case 256: return launch_bn<256, 1>(ta, tb, ty, p, st);
       default: return cudaErrorInvalidValue;
     }
   }
   switch (bn) {
-    case 64: return launch_bn<64, false>(ta, tb, ty, p, st);
-    case 128: return launch_bn<128, false>(ta, tb, ty, p, st);
-    case 256: return launch_bn<256, false>(ta, tb, ty, p, st);
+    case 64: return launch_bn<64, 0>(ta, tb, ty, p, st);
+    case 128: return launch_bn<128, 0>(ta, tb, ty, p, st);
+    case 256: return launch_bn<256, 0>(ta, tb, ty, p, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -28,7 +28,7 @@ def declared_symbols():
 
 def test_every_declared_symbol_is_exported(lk):
     syms = declared_symbols()
-    assert len(syms) == 29, syms
+    assert len(syms) == 33, syms
     out = subprocess.run(["nm", "-D", "--defined-only", lk.LIB_PATH], capture_output=True, text=True).stdout
     exported = set(re.findall(r" T (loka_\w+)", out))
     assert set(syms) <= exported, set(syms) - exported
@@ -48,6 +48,28 @@ def test_struct_layouts_match_header(lk, tmp_path):
            C.sizeof(lk.loka_probe_stats), C.sizeof(lk.loka_candidate), lk.loka_linear_args.y.offset,
            lk.loka_linear_args.status_dev.offset]
     assert got == exp
+
+
+def test_nvfp4_struct_layouts_match_header(lk, tmp_path):
+    src = tmp_path / "sz4.c"
+    src.write_text('#include "loka.h"\n#include <stdio.h>\n#include <stddef.h>\nint main(){printf("%zu %zu %zu %zu\\n",'
+                   'sizeof(loka_nvfp4_tensor), sizeof(loka_nvfp4_linear_args), offsetof(loka_nvfp4_linear_args, y),'
+                   'offsetof(loka_nvfp4_linear_args, status_dev));return 0;}\n')
+    exe = tmp_path / "sz4"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    exp = [C.sizeof(lk.loka_nvfp4_tensor), C.sizeof(lk.loka_nvfp4_linear_args), lk.loka_nvfp4_linear_args.y.offset,
+           lk.loka_nvfp4_linear_args.status_dev.offset]
+    assert got == exp
+
+
+def test_nvfp4_shape_validation_is_host_side(lk):
+    a = lk.loka_nvfp4_linear_args()
+    a.M, a.N, a.K = 128, 128, 96  # K % 64 != 0
+    assert lk._lib.loka_nvfp4_linear_norm(C.byref(a), None, 0, None) == 2  # LOKA_ERR_SHAPE
+    x = lk.loka_tensor(None, 1, 4, 24, 24, None, 0, 0)  # cols % 16 != 0
+    q = lk.loka_nvfp4_tensor(None, 4, 24, 16, None, None)
+    assert lk._lib.loka_quantize_nvfp4(C.byref(x), C.byref(q), None, None, None, 0, None) == 2
 
 
 def test_host_helpers(lk):
