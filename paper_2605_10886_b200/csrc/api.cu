@@ -74,12 +74,12 @@ static int elem_size(loka_dtype t) { return t == LOKA_F32 ? 4 : t == LOKA_BF16 ?
 
 // 2D map over a UE8M0 scale pack ([atoms][kblocks][512 B]) viewed as rows of 256 bytes; one box
 // {256, 2} is one atom, no swizzle (the tcgen05.cp source layout is the plain 512-byte atom).
-static bool make_map_pack(CUtensorMap* m, const void* ptr, int64_t rows256) {
+static bool make_map_pack(CUtensorMap* m, const void* ptr, int64_t rows256, uint32_t box_rows = 2) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {256, (cuuint64_t)rows256};
   cuuint64_t strides[1] = {256};
-  cuuint32_t box[2] = {256u, 2u};
+  cuuint32_t box[2] = {256u, box_rows};
   cuuint32_t es[2] = {1u, 1u};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -829,6 +829,37 @@ loka_status loka_nvfp4_linear_norm(const loka_nvfp4_linear_args* a, void* ws, si
   p.sfa_pack = wa;
   p.sfb_pack = wb;
   p.sf_kblocks = (int32_t)cdiv(K / 2, 128);
+  // plain epilogues with enough 256 x 256 tiles: the CTA-pair block-scaled engine (gemm2.cu)
+  if (use_pair_kernel() && a->norm == LOKA_NORM_NONE && (a->y.dtype == LOKA_BF16 || a->y.dtype == LOKA_F32) &&
+      cdiv(M, 256) * cdiv(N, 256) >= 74) {
+    int sms = 148;
+    st = check_device(&sms);
+    if (st != LOKA_OK) return st;
+    MxPairParams mp;
+    std::memset(&mp, 0, sizeof(mp));
+    const loka_tensor& Y = a->y;
+    if (!make_map_u8(&mp.ta, A.data, M, K / 2, A.ld, 128)) return LOKA_ERR_CUDA;
+    if (!make_map_u8(&mp.tb, B.data, N, K / 2, B.ld, 128)) return LOKA_ERR_CUDA;
+    if (!make_map_out(&mp.ty, Y.data, M, N, Y.ld, Y.dtype, 128, 32u)) return LOKA_ERR_CUDA;
+    const int64_t kbs = cdiv(K, 256);
+    if (!make_map_pack(&mp.tsa, wa, cdiv(M, 256) * 2 * kbs * 8, 8u)) return LOKA_ERR_CUDA;
+    if (!make_map_pack(&mp.tsb, wb, cdiv(N, 256) * 2 * kbs * 8, 8u)) return LOKA_ERR_CUDA;
+    GroupDesc& d = mp.d;
+    d.M = (int32_t)M;
+    d.N = (int32_t)N;
+    d.K = (int32_t)(K / 2);
+    d.tiles_n = (int32_t)cdiv(N, 256);
+    d.sa = A.tensor_scale;
+    d.sb = B.tensor_scale;
+    d.bias = a->bias;
+    d.bias_bf16 = a->bias_dtype == LOKA_BF16;
+    d.out_dtype = Y.dtype;
+    d.ksplit = 1;
+    mp.sf_kbs = (int32_t)kbs;
+    mp.tiles = (int32_t)(cdiv(M, 256) * d.tiles_n);
+    mp.nvfp4 = 1;
+    return launch_mx_pair(mp, sms, s) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
+  }
   return launch_linear(ta, tb, ty, p, bn, s) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
 }
 

@@ -373,6 +373,15 @@ LOKA_DEVINL void mma_mxf8f6f4_cg2(uint32_t tmem_d, uint64_t da, uint64_t db, uin
       "l"(da), "l"(db), "r"(id), "r"(tsfa | (k << 30)), "r"(tsfb | (k << 30)), "r"(accumulate)
       : "memory");
 }
+LOKA_DEVINL void mma_nvf4_cg2(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t tsfa, uint32_t tsfb,
+                              uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %6, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::mxf4nvf4.block_scale.scale_vec::4X [%0], %1, %2, %3, [%4], [%5], p;\n}" ::"r"(
+          tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(tsfa), "r"(tsfb), "r"(accumulate)
+      : "memory");
+}
 // smem -> TMEM scale-factor atom copy in both CTAs of the pair (each from its own smem)
 LOKA_DEVINL void utccp_32x128b_warpx4_cg2(uint32_t tmem_dst, uint32_t saddr) {
   uint64_t d = 0;

@@ -319,25 +319,42 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
 // tcgen05.cp.cta_group::2 right before the stage's MMAs (same pipeline, issue order).  TMEM: one
 // 256-column accumulator + a 4-stage ring of 12 scale columns, so the accumulator is single-
 // buffered: the epilogue warps pull their 128 columns into registers first and release it at once.
-constexpr int kMxStages = 4;
-constexpr int kMxSf = 512 * 3;                                   // SFA + 2 SFB atoms per stage
-constexpr int kMxOffB = kMxStages * k2StageA;
-constexpr int kMxOffSf = kMxOffB + kMxStages * k2StageB;
-constexpr int kMxOffOut = kMxOffSf + kMxStages * kMxSf;          // [8 warps][2][4096]
-constexpr int kMxOffCol = kMxOffOut + k2EpiWarps * 2 * 4096;     // bias [256]
-constexpr int kMxOffBar = kMxOffCol + 256 * 4;
-constexpr int kMxSmem = kMxOffBar + 256 + 1024;
-static_assert(kMxSmem <= 227 * 1024, "mx pair smem");
+// NV = true: NVFP4 (kind::mxf4nvf4.block_scale.scale_vec::4X; a stage row = 256 packed E2M1
+// elements = 4 MMAs of K = 64, each reading its own atoms: SFA 4 x 512 B and SFB 2 x 4 x 512 B per
+// stage; TMEM ring of 48 scale columns per stage; the FP32 tensor scales sa[0] * sb[0] applied in
+// the epilogue).
 
+template <bool NV> struct MxCfg {
+  // NVFP4: a stage's MMAs take half the time of FP8's, so the ring is deeper (5 stages) and the
+  // epilogue's staging boxes single-buffered to make room
+  static constexpr int kStages = NV ? 5 : 4;
+  static constexpr int kOutBufs = NV ? 1 : 2;
+  static constexpr int kSf = NV ? 512 * 12 : 512 * 3;              // SFA + SFB atoms per stage
+  static constexpr int kSfCols = NV ? 48 : 12;                     // TMEM scale columns per stage
+  static constexpr int kOffB = kStages * k2StageA;
+  static constexpr int kOffSf = kOffB + kStages * k2StageB;
+  static constexpr int kOffOut = kOffSf + kStages * kSf;            // [8 warps][kOutBufs][4096]
+  static constexpr int kOffCol = kOffOut + k2EpiWarps * kOutBufs * 4096;  // bias [256]
+  static constexpr int kOffBar = kOffCol + 256 * 4;
+  static constexpr int kSmem = kOffBar + 256 + 1024;
+  static_assert(kSmem <= 227 * 1024, "mx pair smem");
+  static_assert(256 + kStages * kSfCols <= 512, "mx pair tmem");
+};
+
+template <bool NV>
 __global__ void __launch_bounds__(k2Threads, 1) mx_pair_kernel(const __grid_constant__ MxPairParams mp) {
+  using Cf = MxCfg<NV>;
+  constexpr int kMxSf = Cf::kSf;
+  constexpr int kMxOffB = Cf::kOffB, kMxOffSf = Cf::kOffSf, kMxOffOut = Cf::kOffOut, kMxOffCol = Cf::kOffCol,
+                kMxOffBar = Cf::kOffBar;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + kMxOffB;
   uint8_t* sSf = smem + kMxOffSf;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kMxOffBar);
-  uint64_t* empty_bar = full_bar + kMxStages;
-  uint64_t* acc_full = empty_bar + kMxStages;
+  uint64_t* empty_bar = full_bar + Cf::kStages;
+  uint64_t* acc_full = empty_bar + Cf::kStages;
   uint64_t* acc_empty = acc_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
   const GroupDesc& d = mp.d;
@@ -353,7 +370,7 @@ __global__ void __launch_bounds__(k2Threads, 1) mx_pair_kernel(const __grid_cons
     tma_prefetch_desc(&mp.tb);
     tma_prefetch_desc(&mp.tsa);
     tma_prefetch_desc(&mp.tsb);
-    for (int s = 0; s < kMxStages; ++s) {
+    for (int s = 0; s < Cf::kStages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
@@ -377,17 +394,18 @@ __global__ void __launch_bounds__(k2Threads, 1) mx_pair_kernel(const __grid_cons
       for (int t = cid; t < T; t += ncl) {
         const int mb = t / d.tiles_n, nb = t - (t / d.tiles_n) * d.tiles_n;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % kMxStages;
-          const uint32_t ph = (uint32_t)(it / kMxStages) & 1u;
+          const int s = it % Cf::kStages;
+          const uint32_t ph = (uint32_t)(it / Cf::kStages) & 1u;
           mbar_wait(&empty_bar[s], ph ^ 1u, 1);
           if (rank == 0) mbar_arrive_expect_tx(&full_bar[s], 2u * (k2StageA + k2StageB + kMxSf));
           tma_load_2d_cg2(sA + s * k2StageA, &mp.ta, full0 + 8u * s, kb * 128, mb * 256 + rank * 128);
           tma_load_2d_cg2(sB + s * k2StageB, &mp.tb, full0 + 8u * s, kb * 128, nb * 256 + rank * 128);
           // scale atoms: (atom, kb) starts at 256-byte row (atom * kbs + kb) * 2 of the pack
           uint8_t* sf = sSf + s * kMxSf;
-          tma_load_2d_cg2(sf, &mp.tsa, full0 + 8u * s, 0, ((mb * 2 + rank) * mp.sf_kbs + kb) * 2);
-          tma_load_2d_cg2(sf + 512, &mp.tsb, full0 + 8u * s, 0, ((nb * 2) * mp.sf_kbs + kb) * 2);
-          tma_load_2d_cg2(sf + 1024, &mp.tsb, full0 + 8u * s, 0, ((nb * 2 + 1) * mp.sf_kbs + kb) * 2);
+          constexpr int kR = NV ? 8 : 2;  // 256-byte pack rows per 128 rows per stage (the map's box)
+          tma_load_2d_cg2(sf, &mp.tsa, full0 + 8u * s, 0, ((mb * 2 + rank) * mp.sf_kbs + kb) * kR);
+          tma_load_2d_cg2(sf + 256 * kR, &mp.tsb, full0 + 8u * s, 0, ((nb * 2) * mp.sf_kbs + kb) * kR);
+          tma_load_2d_cg2(sf + 512 * kR, &mp.tsb, full0 + 8u * s, 0, ((nb * 2 + 1) * mp.sf_kbs + kb) * kR);
         }
       }
     }
@@ -396,26 +414,42 @@ __global__ void __launch_bounds__(k2Threads, 1) mx_pair_kernel(const __grid_cons
     // ===== MMA issuer (leader only) =====
     if (lane == 0 && rank == 0) {
       int it = 0, j = 0;
-      const uint32_t idesc = idesc_mxf8f6f4(d.a_fmt, d.b_fmt, 256, 256);
+      const uint32_t idesc = NV ? idesc_nvf4(256, 256) : idesc_mxf8f6f4(d.a_fmt, d.b_fmt, 256, 256);
       for (int t = cid; t < T; t += ncl, ++j) {
         mbar_wait(acc_empty, ((uint32_t)j & 1u) ^ 1u, 4);  // both CTAs drained the accumulator
         tc_fence_after();
         for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % kMxStages;
-          const uint32_t ph = (uint32_t)(it / kMxStages) & 1u;
+          const int s = it % Cf::kStages;
+          const uint32_t ph = (uint32_t)(it / Cf::kStages) & 1u;
           mbar_wait(&full_bar[s], ph, 2);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + s * k2StageA);
           const uint32_t b0 = smem_u32(sB + s * k2StageB);
-          const uint32_t sft = tmem_base + 256u + 12u * (uint32_t)s;
+          const uint32_t sft = tmem_base + 256u + (uint32_t)(Cf::kSfCols * s);
           const uint32_t sfs = smem_u32(sSf + s * kMxSf);
-          utccp_32x128b_warpx4_cg2(sft, sfs);               // SFA (this CTA's 128 rows)
-          utccp_32x128b_warpx4_cg2(sft + 4u, sfs + 512u);   // SFB columns 0..127
-          utccp_32x128b_warpx4_cg2(sft + 8u, sfs + 1024u);  // SFB columns 128..255
+          if constexpr (NV) {
+            // SFA atom k -> columns +4k; SFB (column half j, atom k) -> +16 + 8k + 4j: MMA k reads
+            // its 256 B-scale rows from 8 consecutive columns
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            mma_mxf8f6f4_cg2(tmem_base, smem_desc_kmajor_sw128(a0 + k * 32), smem_desc_kmajor_sw128(b0 + k * 32),
-                             idesc, sft, sft + 4u, (uint32_t)k, (kb | k) != 0);
+            for (int k = 0; k < 4; ++k) utccp_32x128b_warpx4_cg2(sft + 4u * k, sfs + 512u * k);
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                utccp_32x128b_warpx4_cg2(sft + 16u + 8u * k + 4u * j, sfs + 2048u * (j + 1) + 512u * k);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_nvf4_cg2(tmem_base, smem_desc_kmajor_sw128(a0 + k * 32), smem_desc_kmajor_sw128(b0 + k * 32),
+                           idesc, sft + 4u * k, sft + 16u + 8u * k, (kb | k) != 0);
+          } else {
+            utccp_32x128b_warpx4_cg2(sft, sfs);               // SFA (this CTA's 128 rows)
+            utccp_32x128b_warpx4_cg2(sft + 4u, sfs + 512u);   // SFB columns 0..127
+            utccp_32x128b_warpx4_cg2(sft + 8u, sfs + 1024u);  // SFB columns 128..255
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_mxf8f6f4_cg2(tmem_base, smem_desc_kmajor_sw128(a0 + k * 32), smem_desc_kmajor_sw128(b0 + k * 32),
+                               idesc, sft, sft + 4u, (uint32_t)k, (kb | k) != 0);
+          }
           mma_commit_cg2_mc(&empty_bar[s], 3);
         }
         mma_commit_cg2_mc(acc_full, 3);
@@ -426,7 +460,7 @@ __global__ void __launch_bounds__(k2Threads, 1) mx_pair_kernel(const __grid_cons
     // ===== epilogue (both CTAs): warp = TMEM lane quadrant q x column half h =====
     const int q = warp & 3;
     const int h = (warp - 2) >> 2;
-    uint8_t* stg = smem + kMxOffOut + (warp - 2) * 8192;
+    uint8_t* stg = smem + kMxOffOut + (warp - 2) * (Cf::kOutBufs * 4096);
     float* colb = reinterpret_cast<float*>(smem + kMxOffCol);
     const uint32_t acc_empty0 = mapa_shared(smem_u32(acc_empty), 0);
     const int esz = d.out_dtype == LOKA_F32 ? 4 : 2;
@@ -459,6 +493,15 @@ __global__ void __launch_bounds__(k2Threads, 1) mx_pair_kernel(const __grid_cons
       const int row0 = mb * 256 + rank * 128 + q * 32;
       const int col0 = nb * 256 + h * 128;
       float amx = 0.f;
+      if constexpr (NV) {  // the FP32 tensor scales (the block scales were applied by the MMA)
+        const float st = __fmul_rn(d.sa[0], d.sb[0]);
+#pragma unroll
+        for (int c = 0; c < 128; c += 2) {
+          const float2 v = fmul2(make_float2(y[c], y[c + 1]), make_float2(st, st));
+          y[c] = v.x;
+          y[c + 1] = v.y;
+        }
+      }
 #pragma unroll
       for (int cb = 0; cb < 128; cb += 32) {
         float* yc = y + cb;
@@ -478,9 +521,12 @@ __global__ void __launch_bounds__(k2Threads, 1) mx_pair_kernel(const __grid_cons
             if (col0 + cb + c < d.N) amx = fmaxf(amx, fabsf(esz == 2 ? stored_bf16(yc[c]) : yc[c]));
         }
         const int in_box = cb % cpb;
-        uint8_t* box = stg + (nbox & 1) * 4096;
+        uint8_t* box = stg + (Cf::kOutBufs == 2 ? (nbox & 1) * 4096 : 0);
         if (in_box == 0) {
-          if (lane == 0) bulk_wait_read_le1();
+          if (lane == 0) {
+            if constexpr (Cf::kOutBufs == 2) bulk_wait_read_le1();
+            else bulk_wait_read0();
+          }
           __syncwarp();
         }
         const uint32_t rowa = smem_u32(box) + (uint32_t)lane * 128u;
@@ -528,10 +574,12 @@ __global__ void __launch_bounds__(k2Threads, 1) mx_pair_kernel(const __grid_cons
   }
 }
 
-cudaError_t launch_mx_pair(const MxPairParams& mp, int num_sms, cudaStream_t st) {
+template <bool NV>
+static cudaError_t launch_mx_pair_t(const MxPairParams& mp, int num_sms, cudaStream_t st) {
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(mx_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMxSmem);
+    cudaError_t e =
+        cudaFuncSetAttribute(mx_pair_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, MxCfg<NV>::kSmem);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
@@ -539,7 +587,7 @@ cudaError_t launch_mx_pair(const MxPairParams& mp, int num_sms, cudaStream_t st)
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(2 * pairs), 1, 1);
   cfg.blockDim = dim3(k2Threads, 1, 1);
-  cfg.dynamicSmemBytes = kMxSmem;
+  cfg.dynamicSmemBytes = MxCfg<NV>::kSmem;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -550,9 +598,12 @@ cudaError_t launch_mx_pair(const MxPairParams& mp, int num_sms, cudaStream_t st)
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, mx_pair_kernel, mp);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, mx_pair_kernel<NV>, mp);
   note_launch();
   return e;
+}
+cudaError_t launch_mx_pair(const MxPairParams& mp, int num_sms, cudaStream_t st) {
+  return mp.nvfp4 ? launch_mx_pair_t<true>(mp, num_sms, st) : launch_mx_pair_t<false>(mp, num_sms, st);
 }
 
 // ---- split-K reduction: y = (sum over slices) * s_a[m] * s_b[n] (+ bias[n]), fixed slice order ----

@@ -217,9 +217,10 @@ cudaError_t launch_track_merge(const TrackParams& p, cudaStream_t st);  // scatt
 // (+ bias), bf16 / f32 output.
 struct MxPairParams {
   CUtensorMap ta, tb, ty, tsa, tsb;
-  GroupDesc d;     // sa / sb unused (the MMA applies the scales)
-  int32_t sf_kbs;  // 128-K blocks (atoms per operand row block)
+  GroupDesc d;     // sa / sb unused (the MMA applies the scales); NVFP4: the tensor scales [1]
+  int32_t sf_kbs;  // 128-byte K stages (MX: one atom, NVFP4: four atoms per operand row block)
   int32_t tiles;
+  int32_t nvfp4;   // 1: E2M1 operands (K counts bytes), kind::mxf4nvf4 scale_vec::4X
 };
 cudaError_t launch_mx_pair(const MxPairParams& mp, int num_sms, cudaStream_t st);
 // Row-wise norm / act / cast over an FP32 GEMM output (rownorm.cu; the unfused form for wide rows)

@@ -101,3 +101,28 @@ def test_bf16_and_fp8_outputs():
     assert guarded_rel_err(f64(yb), yo) <= TOL + 2.0 ** -8
     y8d = oracle.quantize.dequantize(y8.cpu().numpy(), s8.cpu().numpy(), "e4m3", "row")
     assert guarded_rel_err(y8d, yo) <= 2.0 ** -4 + TOL
+
+
+@pytest.mark.parametrize("M,N,K", [(2560, 2048, 256), (2304, 2304, 320)])
+def test_pair_engine_block_scales_exact(M, N, K):
+    """>= 74 tiles of 256 x 256 and a plain epilogue: the CTA-pair block-scaled engine
+    (cta_group::2, SFB of both column halves in each CTA); exact-product construction as above."""
+    g = torch.Generator().manual_seed(M + K)
+    a = _rand_nvfp4(M, K, g)
+    b = _rand_nvfp4(N, K, g)
+    y, _ = lk.loka_nvfp4_linear_norm(a, b, out_dtype="f32")
+    torch.cuda.synchronize()
+    yo = oracle.nvfp4.linear_norm(*(t.cpu().numpy() for t in a), *(t.cpu().numpy() for t in b))
+    assert np.array_equal(f64(y), yo), float(np.abs(f64(y) - yo).max())
+
+
+@pytest.mark.parametrize("out_dtype", ["f32", "bf16"])
+def test_pair_engine_vs_oracle_ragged_bias(out_dtype):
+    M, N, K = 2500, 2000, 1088
+    a, b = _q(synth.heavy(M, K, 41)), _q(synth.weight(N, K, 42))
+    bias = torch.randn(N, device=DEV) * 0.1
+    y, _ = lk.loka_nvfp4_linear_norm(a, b, bias=bias, out_dtype=out_dtype)
+    torch.cuda.synchronize()
+    yo = oracle.nvfp4.linear_norm(*(t.cpu().numpy() for t in a), *(t.cpu().numpy() for t in b),
+                                  bias=bias.double().cpu().numpy())
+    assert guarded_rel_err(f64(y), yo) <= TOL + (2.0 ** -8 if out_dtype == "bf16" else 0.0)
