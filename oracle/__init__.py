@@ -19,4 +19,4 @@ prints no worked numeric example for any of these steps, so no function's
 parity is pinned to a number printed in the paper except the Table II
 geomean fixture.
 """
-from . import fp8, quantize, linear, probe, dispatch, track, sample, nvfp4  # noqa: F401
+from . import fp8, quantize, linear, probe, dispatch, track, sample, nvfp4, gradcomm  # noqa: F401
