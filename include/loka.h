@@ -291,6 +291,18 @@ LOKA_API loka_status loka_nvfp4_linear_norm(const loka_nvfp4_linear_args* args, 
                                             loka_stream_t stream);
 LOKA_API size_t loka_nvfp4_linear_workspace_size(const loka_nvfp4_linear_args* args);
 
+/* ---- NEXT-4: quantized data-parallel gradient reduction (D39) ------------------------
+ * out[i, j] = sum_{p=0}^{P-1} decode(codes[p][i*ld + j]) * scales[p][i]   (FP32 fmaf, rank order)
+ * codes / scales: host arrays of P (1..8) device pointers to each rank's rowwise-quantized shard
+ * (loka_quantize ROW codes + FP32 row scales, already offset to the shard's first row); they may
+ * point into peer GPUs' memory mapped into this device (symmetric memory over NVLink / NVSwitch):
+ * the kernel then pulls one byte per element from every rank.  fmt: E4M3 | E5M2.  cols % 16 == 0, ld % 16 == 0, 16-byte aligned rows; out FP32
+ * [rows, cols] (ld_out % 4 == 0).  The caller orders the peers' writes before the launch (stream
+ * sync + barrier) and the launch before the peers' next writes.                                 */
+LOKA_API loka_status loka_dequant_reduce(int32_t P, const uint8_t* const* codes, const float* const* scales,
+                                         loka_dtype fmt, int64_t rows, int64_t cols, int64_t ld, float* out,
+                                         int64_t ld_out, loka_stream_t stream);
+
 /* ---- a7: LoKA Probe error statistic ------------------------------------------------------- */
 typedef struct loka_probe_pair {
   const void* out;          /* device [M,N], dtype out_dtype (F32 | BF16): low-precision path */

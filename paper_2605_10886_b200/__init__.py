@@ -120,6 +120,8 @@ _sig = {
     "loka_quantize_nvfp4_workspace_size": ([_P(loka_tensor)], C.c_size_t),
     "loka_nvfp4_linear_norm": ([_P(loka_nvfp4_linear_args), C.c_void_p, C.c_size_t, C.c_void_p], C.c_int),
     "loka_nvfp4_linear_workspace_size": ([_P(loka_nvfp4_linear_args)], C.c_size_t),
+    "loka_dequant_reduce": ([C.c_int32, _P(C.c_void_p), _P(C.c_void_p), C.c_int, C.c_int64, C.c_int64, C.c_int64,
+                             C.c_void_p, C.c_int64, C.c_void_p], C.c_int),
     "loka_status_string": ([C.c_int], C.c_char_p),
     "loka_device_supported": ([C.c_int32], C.c_int32),
     "loka_version": ([], C.c_int32),
@@ -348,6 +350,23 @@ def loka_nvfp4_linear_norm(a, b, stream=None, ws=None, **kw):
     _check(_lib.loka_nvfp4_linear_norm(C.byref(args), None if ws is None else C.c_void_p(ws.data_ptr()), nws,
                                        _stream(stream)), "loka_nvfp4_linear_norm")
     return y, ys
+
+
+def loka_dequant_reduce(codes, scales, fmt="e5m2", out=None, stream=None):
+    """NEXT-4 (D39): out = sum_p decode(codes[p]) * scales[p][:, None] in FP32, rank order.  codes /
+    scales: lists of P device tensors, or of raw device addresses (ints, e.g. peer symmetric memory)
+    given with out= (rows, cols and ld are taken from out and ld_codes on the first tensor)."""
+    P = len(codes)
+    c0 = codes[0]
+    rows, cols = out.shape if out is not None else c0.shape
+    ld = c0.stride(0) if isinstance(c0, torch.Tensor) else (cols + 15) // 16 * 16
+    if out is None:
+        out = torch.empty(rows, cols, dtype=torch.float32, device=c0.device)
+    ca = (C.c_void_p * P)(*[c.data_ptr() if isinstance(c, torch.Tensor) else int(c) for c in codes])
+    sa = (C.c_void_p * P)(*[s.data_ptr() if isinstance(s, torch.Tensor) else int(s) for s in scales])
+    _check(_lib.loka_dequant_reduce(P, ca, sa, FMT[fmt], rows, cols, ld, C.c_void_p(out.data_ptr()), out.stride(0),
+                                    _stream(stream)), "loka_dequant_reduce")
+    return out
 
 
 def loka_grouped_fp8_linear(args_list, stream=None, ws=None):

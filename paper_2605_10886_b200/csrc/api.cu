@@ -863,6 +863,35 @@ loka_status loka_nvfp4_linear_norm(const loka_nvfp4_linear_args* a, void* ws, si
   return launch_linear(ta, tb, ty, p, bn, s) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
 }
 
+// ---- NEXT-4: quantized DP gradient reduction (gradcomm.cu) ---------------------------------------
+loka_status loka_dequant_reduce(int32_t P, const uint8_t* const* codes, const float* const* scales, loka_dtype fmt,
+                                int64_t rows, int64_t cols, int64_t ld, float* out, int64_t ld_out,
+                                loka_stream_t stream) {
+  if (P < 1 || P > kMaxRanks || !codes || !scales || (fmt != LOKA_E4M3 && fmt != LOKA_E5M2)) return LOKA_ERR_INVALID_ARG;
+  if (rows < 0 || cols < 0 || cols % 16 || ld < cols || ld % 16 || ld_out < cols || ld_out % 4) return LOKA_ERR_SHAPE;
+  if (rows == 0 || cols == 0) return LOKA_OK;
+  if (!out || !aligned16(out)) return LOKA_ERR_INVALID_ARG;
+  DeqReduceParams p;
+  std::memset(&p, 0, sizeof(p));
+  for (int r = 0; r < P; ++r) {
+    if (!codes[r] || !scales[r] || !aligned16(codes[r])) return LOKA_ERR_INVALID_ARG;
+    p.codes[r] = codes[r];
+    p.scales[r] = scales[r];
+  }
+  p.P = P;
+  p.fmt = fmt;
+  p.rows = rows;
+  p.cols = cols;
+  p.ld = ld;
+  p.out = out;
+  p.ld_out = ld_out;
+  int sms = 148;
+  loka_status st = check_device(&sms);
+  if (st != LOKA_OK) return st;
+  return launch_dequant_reduce(p, sms, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess ? LOKA_OK
+                                                                                                : LOKA_ERR_CUDA;
+}
+
 // All-gather transport of the stack's hand-offs (StackParams::gather); LOKA_STACK_GATHER overrides
 // the default for measurements (0 bulk DSMEM copies, 1 L2 + multicast TMA, 2 st.async).
 static int stack_gather_mode() {

@@ -38,6 +38,18 @@ cudaError_t launch_nvfp4_cast(const Nvfp4QParams& p, bool in_bf16, int num_sms, 
 cudaError_t launch_nvfp4_sf_pack(const uint8_t* sf, int64_t ld, int64_t rows, int64_t nblk, int64_t row_blocks,
                                  int64_t k64, uint8_t* out, cudaStream_t st);
 
+// ---- quantized DP gradient reduction (gradcomm.cu, NEXT-4) ----
+constexpr int kMaxRanks = 8;
+struct DeqReduceParams {
+  const uint8_t* codes[kMaxRanks];  // per rank: FP8 codes of the shard rows (may be peer memory)
+  const float* scales[kMaxRanks];   // per rank: row scales of the shard rows
+  int32_t P, fmt;
+  int64_t rows, cols, ld;           // cols % 16 == 0, ld % 16 == 0 (bytes = elements)
+  float* out;
+  int64_t ld_out;
+};
+cudaError_t launch_dequant_reduce(const DeqReduceParams& p, int num_sms, cudaStream_t st);
+
 cudaError_t launch_quantize(const QuantParams& p, bool in_bf16, int fmt, int scale_fmt, int gran, int phase,
                             float* amax_dev, cudaStream_t st, int num_sms);
 

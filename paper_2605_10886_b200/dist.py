@@ -76,3 +76,84 @@ def reduce_probe_stats(stats_list, group=None):
         cnt = int(t[2])
         out.append(dict(zip(keys, (float(t[0]) / cnt if cnt else 0.0, float(m[0]), float(t[1]), cnt, int(t[3])))))
     return out
+
+
+class QuantizedGradReducer:
+    """NEXT-4 (SURVEY.md §8(f) "quantized (FP8) DP gradient communication"; D39): the data-
+    parallel gradient reduce-scatter with FP8 payloads.  Every rank quantizes its gradient G [rows,
+    cols] rowwise (loka_quantize, e5m2 by default: D5) into a registered buffer; rank r owns rows
+    shard_rows(rows, P, r) and reduces the P ranks' codes of those rows with loka_dequant_reduce.
+
+    transport "p2p": the buffer is torch symmetric memory (every rank's buffer mapped into every
+      GPU over NVLink / NVSwitch); the reduction kernel reads the peers' codes directly — the kernel
+      is the collective's data path (1 byte + 4/cols bytes per element per peer instead of 4) — and
+      two device-side barriers (no host sync) order the peers' quantize before the reads and the
+      reads before the next quantize.
+    transport "nccl": all_to_all of the code / scale row shards, then the same kernel on the local
+      copies (the baseline).
+    The quantize / reduce steps are injectable only so the protocol can be exercised by CPU gloo
+    tests; the default is libloka on the current CUDA stream."""
+
+    def __init__(self, rows: int, cols: int, fmt: str = "e5m2", group=None, transport: str = "p2p", device=None,
+                 quant_fn=None, reduce_fn=None):
+        self.rows, self.cols, self.fmt, self.group = rows, cols, fmt, group
+        self.world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if self.world > 1 else 0
+        self.r0, self.r1 = shard_rows(rows, self.world, self.rank)
+        self.transport = transport if self.world > 1 else "local"
+        dev = device if device is not None else (torch.device("cuda", torch.cuda.current_device())
+                                                 if torch.cuda.is_available() else torch.device("cpu"))
+        self.ld = (cols + 15) // 16 * 16
+        self.off_s = (rows * self.ld + 255) // 256 * 256  # scales after the codes, 256-B aligned
+        nbytes = self.off_s + 4 * rows
+        self.hdl = None
+        if self.transport == "p2p":
+            import torch.distributed._symmetric_memory as symm_mem
+            self.buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=dev)
+            self.hdl = symm_mem.rendezvous(self.buf, (group or dist.group.WORLD).group_name)
+            self.peer_base = [self.hdl.get_buffer(p, (nbytes,), torch.uint8, 0).data_ptr() if p != self.rank
+                              else self.buf.data_ptr() for p in range(self.world)]
+        else:
+            self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+        self.codes = self.buf[:rows * self.ld].view(rows, self.ld)[:, :cols]
+        self.scales = self.buf[self.off_s:self.off_s + 4 * rows].view(torch.float32)
+        self.quant_fn = quant_fn or self._lk_quant
+        self.reduce_fn = reduce_fn or self._lk_reduce
+
+    def _lk_quant(self, g):
+        import paper_2605_10886_b200 as lk
+        lk.loka_quantize(g, self.fmt, "row", out=self.codes, scales=self.scales)
+
+    def _lk_reduce(self, codes, scales, out):
+        import paper_2605_10886_b200 as lk
+        return lk.loka_dequant_reduce(codes, scales, self.fmt, out=out)
+
+    def reduce_scatter(self, grad: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Returns this rank's reduced rows [r1 - r0, cols] (FP32), stream-ordered on the current stream."""
+        n = self.r1 - self.r0
+        if out is None:
+            out = torch.empty(n, self.cols, dtype=torch.float32, device=self.codes.device)
+        self.quant_fn(grad)
+        if self.transport == "local":
+            return self.reduce_fn([self.codes], [self.scales], out)
+        if self.transport == "p2p":
+            self.hdl.barrier(channel=0)  # every rank's codes are written (device-side)
+            cp = [b + self.r0 * self.ld for b in self.peer_base]
+            sp = [b + self.off_s + self.r0 * 4 for b in self.peer_base]
+            self.reduce_fn(cp, sp, out)
+            self.hdl.barrier(channel=1)  # every rank finished reading before anyone's next quantize
+            return out
+        # nccl: all_to_all of the row shards of the codes and scales
+        if self.cols % 16:
+            raise ValueError("cols % 16 != 0")
+        bounds = [shard_rows(self.rows, self.world, p) for p in range(self.world)]
+        in_split = [(b - a) * self.cols for a, b in bounds]
+        recv_c = torch.empty(self.world * n * self.cols, dtype=torch.uint8, device=self.codes.device)
+        send_c = self.codes.contiguous().view(-1)
+        dist.all_to_all_single(recv_c, send_c, [n * self.cols] * self.world, in_split, group=self.group)
+        recv_s = torch.empty(self.world * n, dtype=torch.float32, device=self.codes.device)
+        dist.all_to_all_single(recv_s, self.scales.contiguous(), [n] * self.world, [b - a for a, b in bounds],
+                               group=self.group)
+        rc = recv_c.view(self.world, n, self.cols)
+        rs = recv_s.view(self.world, n)
+        return self.reduce_fn([rc[p] for p in range(self.world)], [rs[p] for p in range(self.world)], out)

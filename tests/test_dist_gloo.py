@@ -79,3 +79,38 @@ def test_shard_rows_partition():
             assert spans[0][0] == 0 and spans[-1][1] == total
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
             assert max(b - a for a, b in spans) - min(b - a for a, b in spans) <= 1
+
+
+def _grad_worker(rank, world, port, rows, cols, out_dir):
+    """NEXT-4 quantized gradient reduce-scatter, NCCL-transport protocol over gloo (CPU), with the
+    device steps replaced by oracle functions."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    holder = {}
+
+    def quant(g):
+        q, s = oracle.quantize.quantize(g.double().numpy(), "e5m2", "row")
+        holder["r"].codes.copy_(torch.from_numpy(q))
+        holder["r"].scales.copy_(torch.from_numpy(s))
+
+    def reduce(codes, scales, out):
+        r = oracle.gradcomm.reduce_dequantized([c.numpy() for c in codes], [s.numpy() for s in scales], "e5m2")
+        out.copy_(torch.from_numpy(r))
+        return out
+
+    red = ldist.QuantizedGradReducer(rows, cols, "e5m2", transport="nccl", device=torch.device("cpu"),
+                                     quant_fn=quant, reduce_fn=reduce)
+    holder["r"] = red
+    out = red.reduce_scatter(synth.grad(rows, cols, 100 + rank))
+    np.save(os.path.join(out_dir, f"g{rank}.npy"), out.double().numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,rows", [(2, 64), (3, 50)])
+def test_quantized_grad_reduce_scatter_protocol(world, rows, tmp_path):
+    cols = 32
+    mp.spawn(_grad_worker, args=(world, _free_port(), rows, cols, str(tmp_path)), nprocs=world, join=True)
+    grads = [synth.grad(rows, cols, 100 + p).double().numpy() for p in range(world)]
+    ref, _, _ = oracle.gradcomm.quantized_allreduce(grads, "e5m2")
+    got = np.concatenate([np.load(tmp_path / f"g{r}.npy") for r in range(world)])
+    assert np.allclose(got, ref, rtol=2.0 ** -23, atol=0)  # each rank holds its rows of the sum (FP32 out)
