@@ -543,6 +543,9 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
   return 1.f;
 }
 
+// TRACE = false (the production instance) makes c.trace a compile-time 0: every trace stamp and
+// its predicate logic is compiled out of the epilogue (~10% of its instructions).
+template <bool TRACE>
 __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_constant__ StackParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -571,7 +574,7 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
   c.a_bar = a_bar;
   c.half_bar = half_bar;
   c.stat_bar = stat_bar;
-  c.trace = *reinterpret_cast<volatile int*>(&g_strace_on);
+  c.trace = TRACE ? *reinterpret_cast<volatile int*>(&g_strace_on) : 0;
   c.cta = blockIdx.x + gridDim.x * blockIdx.y;
   if (threadIdx.x == 0) LOKA_STRACE(c, 0);
 
@@ -684,6 +687,8 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
   }
 }
 
+static bool g_strace_host = false;  // launch the traced instance (set by loka_debug_trace)
+
 long long stack_debug_trace(int enable, unsigned long long* out, long long n) {
   long long got = 0;
   if (out && n > 0) {
@@ -702,16 +707,18 @@ long long stack_debug_trace(int enable, unsigned long long* out, long long n) {
       if (cudaMemcpyToSymbol(g_sfine, zero, sizeof(zero)) != cudaSuccess) return -1;
     }
     if (cudaMemcpyToSymbol(g_strace_on, &enable, sizeof(int)) != cudaSuccess) return -1;
+    g_strace_host = enable != 0;
   }
   return got;
 }
 
 cudaError_t launch_stack(const StackParams& p, cudaStream_t st) {
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(stack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSSmem);
+  auto kern = g_strace_host ? stack_kernel<true> : stack_kernel<false>;
+  static bool attr_done[2] = {false, false};
+  if (!attr_done[g_strace_host]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSSmem);
     if (e != cudaSuccess) return e;
-    attr_done = true;
+    attr_done[g_strace_host] = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)((p.M + 127) / 128), (unsigned)p.C, 1);
@@ -727,7 +734,7 @@ cudaError_t launch_stack(const StackParams& p, cudaStream_t st) {
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, stack_kernel, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
   note_launch();
   return e;
 }
