@@ -545,7 +545,9 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
 
 // TRACE = false (the production instance) makes c.trace a compile-time 0: every trace stamp and
 // its predicate logic is compiled out of the epilogue (~10% of its instructions).
-template <bool TRACE>
+// CT > 0: the cluster size as a compile-time constant (CT = p.C), so the rank-order loops unroll and
+// the modular rank arithmetic of the exchange and of the slice order folds (cfg2: C = 4).
+template <bool TRACE, int CT>
 __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_constant__ StackParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -569,8 +571,8 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
   c.m0 = blockIdx.x * 128;
   c.grow = c.m0 + c.r;
   c.row_ok = c.grow < p.M;
-  c.C = p.C;
-  c.rank = p.C > 1 ? (int)cluster_ctarank() : 0;
+  c.C = CT > 0 ? CT : p.C;
+  c.rank = c.C > 1 ? (int)cluster_ctarank() : 0;
   c.a_bar = a_bar;
   c.half_bar = half_bar;
   c.stat_bar = stat_bar;
@@ -597,7 +599,7 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
   __syncthreads();
   tc_fence_after();
   c.tmem_base = *tmem_slot;
-  if (p.C > 1) cluster_sync_all();  // every cluster CTA is running before any DSMEM traffic
+  if (c.C > 1) cluster_sync_all();  // every cluster CTA is running before any DSMEM traffic
   if (threadIdx.x == 0) LOKA_STRACE(c, 1);
 
   float sa = c.row_ok ? p.xs[c.grow] : 0.f;  // row scale of the current layer input
@@ -679,7 +681,7 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
     sa = c.row_ok ? s_next : 0.f;
     tc_fence_before();  // this layer's tcgen05.ld done before the next layer's MMAs overwrite TMEM
   }
-  if (p.C > 1) cluster_sync_all();
+  if (c.C > 1) cluster_sync_all();
   __syncthreads();
   if (c.warp == 1) {
     tc_fence_after();
@@ -713,12 +715,13 @@ long long stack_debug_trace(int enable, unsigned long long* out, long long n) {
 }
 
 cudaError_t launch_stack(const StackParams& p, cudaStream_t st) {
-  auto kern = g_strace_host ? stack_kernel<true> : stack_kernel<false>;
-  static bool attr_done[2] = {false, false};
-  if (!attr_done[g_strace_host]) {
+  const int inst = g_strace_host ? 0 : p.C == 4 ? 2 : 1;
+  auto kern = inst == 0 ? stack_kernel<true, 0> : inst == 2 ? stack_kernel<false, 4> : stack_kernel<false, 0>;
+  static bool attr_done[3] = {false, false, false};
+  if (!attr_done[inst]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSSmem);
     if (e != cudaSuccess) return e;
-    attr_done[g_strace_host] = true;
+    attr_done[inst] = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)((p.M + 127) / 128), (unsigned)p.C, 1);

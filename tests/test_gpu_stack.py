@@ -112,6 +112,21 @@ def test_stack_single_cta_cluster_and_short():
             _check_out(y, None, yo, "f32")
 
 
+@pytest.mark.parametrize("dims,M", [([512, 512, 256, 512], 260),     # max N 512 -> C = 2 (generic-C instance)
+                                    ([256, 1024, 2048], 200)])        # max N 2048 -> C = 8
+def test_stack_cluster_sizes_2_and_8(dims, M):
+    """The C = 4 launch runs a compile-time-C kernel instance; other cluster sizes run the generic
+    one: both checked layer by layer against the oracle."""
+    xq, xs, ws, save, y, _ = _run(M, dims, "layer", "f32")
+    ins = [(xq, xs)] + save
+    for l in range(len(dims) - 1):
+        yo = _layer_oracle(ins[l][0], ins[l][1], ws[l][0], ws[l][1], "layer")
+        if l + 1 < len(dims) - 1:
+            _check_handoff(save[l][0], save[l][1], yo)
+        else:
+            _check_out(y, None, yo, "f32")
+
+
 def test_stack_matches_layer_chain_closely():
     """The fused stack and the chain of per-layer launches compute the same function; they differ
     only in FP32 summation order, so the final outputs agree to accumulation noise except where an
