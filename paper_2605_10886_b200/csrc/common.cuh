@@ -35,8 +35,19 @@ template <int FMT> LOKA_DEVINL uint32_t cvt_fp8x2(float lo, float hi) {
     asm("{ cvt.rn.satfinite.e5m2x2.f32 %0, %1, %2; }" : "=h"(r) : "f"(hi), "f"(lo));
   return (uint32_t)r;
 }
+// Four codes in one register (a in the low byte): the two pair conversions are packed with one
+// mov.b32 {lo, hi}, which ptxas folds into the second F2FP's MERGE_C operand (no shift / OR).
 template <int FMT> LOKA_DEVINL uint32_t cvt_fp8x4(float a, float b, float c, float d) {
-  return cvt_fp8x2<FMT>(a, b) | (cvt_fp8x2<FMT>(c, d) << 16);
+  uint32_t r;
+  if constexpr (FMT == LOKA_E4M3)
+    asm("{ .reg .b16 lo, hi;\n cvt.rn.satfinite.e4m3x2.f32 lo, %2, %1;\n cvt.rn.satfinite.e4m3x2.f32 hi, %4, %3;\n"
+        " mov.b32 %0, {lo, hi}; }"
+        : "=r"(r) : "f"(a), "f"(b), "f"(c), "f"(d));
+  else
+    asm("{ .reg .b16 lo, hi;\n cvt.rn.satfinite.e5m2x2.f32 lo, %2, %1;\n cvt.rn.satfinite.e5m2x2.f32 hi, %4, %3;\n"
+        " mov.b32 %0, {lo, hi}; }"
+        : "=r"(r) : "f"(a), "f"(b), "f"(c), "f"(d));
+  return r;
 }
 
 // Exact IEEE scale computation for one granule (D1/D2/D7).  amax >= 0, finite.

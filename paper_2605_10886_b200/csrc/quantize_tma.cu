@@ -93,6 +93,10 @@ __global__ void __launch_bounds__(32 * (kQtRows + 1), 1)
   }
   __syncthreads();
   pdl_wait();
+  // Every CTA of this grid is resident (grid <= SMs): let the dependent launch (the layer stack /
+  // GEMM that consumes these codes) start its prologue on SMs as they free up.  Safe at any point:
+  // the dependent's griddepcontrol.wait still waits for this grid's completion and memory flush.
+  pdl_launch_dependents();
 
   if (warp == kQtRows) {  // ===== producer =====
     if (lane == 0) {
