@@ -166,6 +166,8 @@ struct SCtx {
   uint32_t tmem_base;
   int warp, lane, q, cq, r, grow, m0, rank, C;
   int trace, cta;
+  int norm_c;     // >= 0: every layer's norm, a compile-time constant in the specialised instance
+  bool gather_l2; // true: the L2 all-gather, a compile-time constant in the specialised instance
   uint64_t* a_bar;     // [8] per-slice "layer input complete" barriers
   uint64_t* half_bar;  // [2] accumulator half ready
   uint64_t* stat_bar;  // cluster row-statistics records arrived (one phase per layer)
@@ -227,7 +229,7 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
   static_assert(NH == 1 || SEG == 32, "halves are 128 columns");
   constexpr int BN = NH == 2 ? 256 : 4 * SEG;
   constexpr int CPT = NH * SEG;
-  const int norm = p.norm[l];
+  const int norm = c.norm_c >= 0 ? c.norm_c : p.norm[l];
   const int N = p.N[l];
   const int n0 = c.rank * BN;
   const bool last = l + 1 == p.L;
@@ -363,8 +365,8 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
     const float2 rr = make_float2(r_out, r_out);
     const uint32_t a_local = smem_u32(c.smem + kSOffA);
     uint8_t* hsave = p.h_save[l];
-    const bool gl2 = p.gather == kStackGatherL2;
-    const bool st_async = p.gather == kStackGatherStAsync && c.C > 1;
+    const bool gl2 = c.gather_l2 || p.gather == kStackGatherL2;
+    const bool st_async = !c.gather_l2 && p.gather == kStackGatherStAsync && c.C > 1;
     // st.async pieces complete on the receiver's barrier of this CTA's slice (a_bar[0] when the
     // slices are narrower than a K block and the next layer waits for the whole input at once)
     const uint32_t bar_own = smem_u32(&c.a_bar[BN >= 128 ? c.rank : 0]);
@@ -547,7 +549,8 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
 // its predicate logic is compiled out of the epilogue (~10% of its instructions).
 // CT > 0: the cluster size as a compile-time constant (CT = p.C), so the rank-order loops unroll and
 // the modular rank arithmetic of the exchange and of the slice order folds (cfg2: C = 4).
-template <bool TRACE, int CT>
+// LN: every layer is LayerNorm and the all-gather goes through L2 (cfg2), both compile-time.
+template <bool TRACE, int CT, bool LN>
 __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_constant__ StackParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -572,6 +575,8 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
   c.grow = c.m0 + c.r;
   c.row_ok = c.grow < p.M;
   c.C = CT > 0 ? CT : p.C;
+  c.norm_c = LN ? (int)LOKA_NORM_LAYER : -1;
+  c.gather_l2 = LN;
   c.rank = c.C > 1 ? (int)cluster_ctarank() : 0;
   c.a_bar = a_bar;
   c.half_bar = half_bar;
@@ -715,8 +720,12 @@ long long stack_debug_trace(int enable, unsigned long long* out, long long n) {
 }
 
 cudaError_t launch_stack(const StackParams& p, cudaStream_t st) {
-  const int inst = g_strace_host ? 0 : p.C == 4 ? 2 : 1;
-  auto kern = inst == 0 ? stack_kernel<true, 0> : inst == 2 ? stack_kernel<false, 4> : stack_kernel<false, 0>;
+  bool all_ln = p.gather == kStackGatherL2;
+  for (int l = 0; l < p.L; ++l) all_ln = all_ln && p.norm[l] == LOKA_NORM_LAYER;
+  const int inst = g_strace_host ? 0 : p.C == 4 && all_ln ? 2 : 1;
+  auto kern = inst == 0   ? stack_kernel<true, 0, false>
+              : inst == 2 ? stack_kernel<false, 4, true>
+                          : stack_kernel<false, 0, false>;
   static bool attr_done[3] = {false, false, false};
   if (!attr_done[inst]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSSmem);
