@@ -167,7 +167,7 @@ struct SCtx {
   int warp, lane, q, cq, r, grow, m0, rank, C;
   int trace, cta;
   int norm_c;     // >= 0: every layer's norm, a compile-time constant in the specialised instance
-  bool gather_l2; // true: the L2 all-gather, a compile-time constant in the specialised instance
+  int gather_c;   // >= 0: the all-gather transport, a compile-time constant in the specialised instance
   uint64_t* a_bar;     // [8] per-slice "layer input complete" barriers
   uint64_t* half_bar;  // [2] accumulator half ready
   uint64_t* stat_bar;  // cluster row-statistics records arrived (one phase per layer)
@@ -365,8 +365,9 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
     const float2 rr = make_float2(r_out, r_out);
     const uint32_t a_local = smem_u32(c.smem + kSOffA);
     uint8_t* hsave = p.h_save[l];
-    const bool gl2 = c.gather_l2 || p.gather == kStackGatherL2;
-    const bool st_async = !c.gather_l2 && p.gather == kStackGatherStAsync && c.C > 1;
+    const int gather = c.gather_c >= 0 ? c.gather_c : p.gather;
+    const bool gl2 = gather == kStackGatherL2;
+    const bool st_async = gather == kStackGatherStAsync && c.C > 1;
     // st.async pieces complete on the receiver's barrier of this CTA's slice (a_bar[0] when the
     // slices are narrower than a K block and the next layer waits for the whole input at once)
     const uint32_t bar_own = smem_u32(&c.a_bar[BN >= 128 ? c.rank : 0]);
@@ -549,8 +550,8 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
 // its predicate logic is compiled out of the epilogue (~10% of its instructions).
 // CT > 0: the cluster size as a compile-time constant (CT = p.C), so the rank-order loops unroll and
 // the modular rank arithmetic of the exchange and of the slice order folds (cfg2: C = 4).
-// LN: every layer is LayerNorm and the all-gather goes through L2 (cfg2), both compile-time.
-template <bool TRACE, int CT, bool LN>
+// GT >= 0: every layer is LayerNorm and the all-gather transport is GT (cfg2: L2), both compile-time.
+template <bool TRACE, int CT, int GT>
 __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_constant__ StackParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -575,8 +576,8 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
   c.grow = c.m0 + c.r;
   c.row_ok = c.grow < p.M;
   c.C = CT > 0 ? CT : p.C;
-  c.norm_c = LN ? (int)LOKA_NORM_LAYER : -1;
-  c.gather_l2 = LN;
+  c.norm_c = GT >= 0 ? (int)LOKA_NORM_LAYER : -1;
+  c.gather_c = GT;
   c.rank = c.C > 1 ? (int)cluster_ctarank() : 0;
   c.a_bar = a_bar;
   c.half_bar = half_bar;
@@ -720,13 +721,16 @@ long long stack_debug_trace(int enable, unsigned long long* out, long long n) {
 }
 
 cudaError_t launch_stack(const StackParams& p, cudaStream_t st) {
-  bool all_ln = p.gather == kStackGatherL2;
+  bool all_ln = true;
   for (int l = 0; l < p.L; ++l) all_ln = all_ln && p.norm[l] == LOKA_NORM_LAYER;
-  const int inst = g_strace_host ? 0 : p.C == 4 && all_ln ? 2 : 1;
-  auto kern = inst == 0   ? stack_kernel<true, 0, false>
-              : inst == 2 ? stack_kernel<false, 4, true>
-                          : stack_kernel<false, 0, false>;
-  static bool attr_done[3] = {false, false, false};
+  // (a DSMEM-gather instance was measured 2 us slower per step than the L2 one: not instantiated)
+  const bool spec = p.C == 4 && all_ln && p.gather == kStackGatherL2;
+  const int inst = (g_strace_host ? 2 : 0) + (spec ? 1 : 0);
+  auto kern = inst == 0   ? stack_kernel<false, 0, -1>
+              : inst == 1 ? stack_kernel<false, 4, kStackGatherL2>
+              : inst == 2 ? stack_kernel<true, 0, -1>
+                          : stack_kernel<true, 4, kStackGatherL2>;
+  static bool attr_done[4] = {false, false, false, false};
   if (!attr_done[inst]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSSmem);
     if (e != cudaSuccess) return e;
