@@ -893,19 +893,20 @@ loka_status loka_dequant_reduce(int32_t P, const uint8_t* const* codes, const fl
 }
 
 // All-gather transport of the stack's hand-offs (StackParams::gather); LOKA_STACK_GATHER overrides
-// the default for measurements (0 bulk DSMEM copies, 1 L2 + multicast TMA, 2 st.async).
+// the default for measurements (0 bulk DSMEM copies, 1 L2 + multicast TMA, 2 st.async, 3 = default:
+// L2 for slices of whole K blocks, st.async for narrower ones — 2 us per cfg2 step faster than 1).
 static int stack_gather_mode() {
   static const int mode = [] {
     const char* e = std::getenv("LOKA_STACK_GATHER");
-    const int v = e ? std::atoi(e) : kStackGatherL2;
-    return v >= 0 && v <= 2 ? v : (int)kStackGatherL2;
+    const int v = e ? std::atoi(e) : kStackGatherL2StAsync;
+    return v >= 0 && v <= 3 ? v : (int)kStackGatherL2StAsync;
   }();
   return mode;
 }
 // Layer l's hand-off is all-gathered through L2 (global codes + multicast TMA loads) when the
 // cluster has peers and the CTA's slice is whole 128-wide K blocks (BN_l = N_l / C >= 128).
 static bool stack_l2_handoff(const loka_stack_args* a, int C, int l) {
-  return stack_gather_mode() == kStackGatherL2 && C > 1 && l + 1 < a->L && a->dims[l + 1] / C >= 128;
+  return (stack_gather_mode() == kStackGatherL2 || stack_gather_mode() == kStackGatherL2StAsync) && C > 1 && l + 1 < a->L && a->dims[l + 1] / C >= 128;
 }
 static int stack_cluster(const loka_stack_args* a) {
   int64_t maxN = 0;

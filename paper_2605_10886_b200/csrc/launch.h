@@ -158,6 +158,9 @@ struct StackParams {
   int32_t gather;                     // all-gather transport: kStackGather* (stack.cu)
 };
 constexpr int kStackGatherDsmemBulk = 0, kStackGatherL2 = 1, kStackGatherStAsync = 2;
+// L2 for slices of whole K blocks (BN >= 128), st.async pieces on the receiver's barrier for
+// narrower slices (instead of per-thread DSMEM stores + a cluster barrier)
+constexpr int kStackGatherL2StAsync = 3;
 cudaError_t launch_stack(const StackParams& p, cudaStream_t st);
 long long stack_debug_trace(int enable, unsigned long long* out, long long n);  // see loka_debug_trace
 

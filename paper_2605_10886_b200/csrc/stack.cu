@@ -366,8 +366,9 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
     const uint32_t a_local = smem_u32(c.smem + kSOffA);
     uint8_t* hsave = p.h_save[l];
     const int gather = c.gather_c >= 0 ? c.gather_c : p.gather;
-    const bool gl2 = gather == kStackGatherL2;
-    const bool st_async = gather == kStackGatherStAsync && c.C > 1;
+    const bool gl2 = gather == kStackGatherL2 || gather == kStackGatherL2StAsync;
+    const bool st_async =
+        (gather == kStackGatherStAsync || (gather == kStackGatherL2StAsync && BN < 128)) && c.C > 1;
     // st.async pieces complete on the receiver's barrier of this CTA's slice (a_bar[0] when the
     // slices are narrower than a K block and the next layer waits for the whole input at once)
     const uint32_t bar_own = smem_u32(&c.a_bar[BN >= 128 ? c.rank : 0]);
@@ -724,13 +725,16 @@ cudaError_t launch_stack(const StackParams& p, cudaStream_t st) {
   bool all_ln = true;
   for (int l = 0; l < p.L; ++l) all_ln = all_ln && p.norm[l] == LOKA_NORM_LAYER;
   // (a DSMEM-gather instance was measured 2 us slower per step than the L2 one: not instantiated)
-  const bool spec = p.C == 4 && all_ln && p.gather == kStackGatherL2;
-  const int inst = (g_strace_host ? 2 : 0) + (spec ? 1 : 0);
+  const bool spec = p.C == 4 && all_ln && (p.gather == kStackGatherL2 || p.gather == kStackGatherL2StAsync);
+  const bool hyb = p.gather == kStackGatherL2StAsync;
+  const int inst = (g_strace_host ? 3 : 0) + (spec ? (hyb ? 2 : 1) : 0);
   auto kern = inst == 0   ? stack_kernel<false, 0, -1>
               : inst == 1 ? stack_kernel<false, 4, kStackGatherL2>
-              : inst == 2 ? stack_kernel<true, 0, -1>
-                          : stack_kernel<true, 4, kStackGatherL2>;
-  static bool attr_done[4] = {false, false, false, false};
+              : inst == 2 ? stack_kernel<false, 4, kStackGatherL2StAsync>
+              : inst == 3 ? stack_kernel<true, 0, -1>
+              : inst == 4 ? stack_kernel<true, 4, kStackGatherL2>
+                          : stack_kernel<true, 4, kStackGatherL2StAsync>;
+  static bool attr_done[6] = {false, false, false, false, false, false};
   if (!attr_done[inst]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSSmem);
     if (e != cudaSuccess) return e;
