@@ -899,14 +899,17 @@ static int stack_gather_mode() {
   static const int mode = [] {
     const char* e = std::getenv("LOKA_STACK_GATHER");
     const int v = e ? std::atoi(e) : kStackGatherL2StAsync;
-    return v >= 0 && v <= 3 ? v : (int)kStackGatherL2StAsync;
+    return v >= 0 && v <= 4 ? v : (int)kStackGatherL2StAsync;
   }();
   return mode;
 }
 // Layer l's hand-off is all-gathered through L2 (global codes + multicast TMA loads) when the
 // cluster has peers and the CTA's slice is whole 128-wide K blocks (BN_l = N_l / C >= 128).
 static bool stack_l2_handoff(const loka_stack_args* a, int C, int l) {
-  return (stack_gather_mode() == kStackGatherL2 || stack_gather_mode() == kStackGatherL2StAsync) && C > 1 && l + 1 < a->L && a->dims[l + 1] / C >= 128;
+  const int g = stack_gather_mode();
+  const int l2min = g == kStackGatherL2StAsync256 ? 256 : 128;
+  return (g == kStackGatherL2 || g == kStackGatherL2StAsync || g == kStackGatherL2StAsync256) && C > 1 &&
+         l + 1 < a->L && a->dims[l + 1] / C >= l2min;
 }
 static int stack_cluster(const loka_stack_args* a) {
   int64_t maxN = 0;

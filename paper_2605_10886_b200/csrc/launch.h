@@ -161,6 +161,7 @@ constexpr int kStackGatherDsmemBulk = 0, kStackGatherL2 = 1, kStackGatherStAsync
 // L2 for slices of whole K blocks (BN >= 128), st.async pieces on the receiver's barrier for
 // narrower slices (instead of per-thread DSMEM stores + a cluster barrier)
 constexpr int kStackGatherL2StAsync = 3;
+constexpr int kStackGatherL2StAsync256 = 4;  // the same split at BN = 256 (measurement variant)
 cudaError_t launch_stack(const StackParams& p, cudaStream_t st);
 long long stack_debug_trace(int enable, unsigned long long* out, long long n);  // see loka_debug_trace
 

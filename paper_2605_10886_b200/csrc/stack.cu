@@ -366,9 +366,11 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
     const uint32_t a_local = smem_u32(c.smem + kSOffA);
     uint8_t* hsave = p.h_save[l];
     const int gather = c.gather_c >= 0 ? c.gather_c : p.gather;
-    const bool gl2 = gather == kStackGatherL2 || gather == kStackGatherL2StAsync;
-    const bool st_async =
-        (gather == kStackGatherStAsync || (gather == kStackGatherL2StAsync && BN < 128)) && c.C > 1;
+    const bool hybrid = gather == kStackGatherL2StAsync || gather == kStackGatherL2StAsync256;
+    const int l2min = gather == kStackGatherL2StAsync256 ? 256 : 128;
+    const bool gl2 = gather == kStackGatherL2 || hybrid;
+    const bool st_async = (gather == kStackGatherStAsync || (hybrid && BN < l2min)) && c.C > 1;
+    const bool l2_path = gl2 && BN >= l2min && c.C > 1;
     // st.async pieces complete on the receiver's barrier of this CTA's slice (a_bar[0] when the
     // slices are narrower than a K block and the next layer waits for the whole input at once)
     const uint32_t bar_own = smem_u32(&c.a_bar[BN >= 128 ? c.rank : 0]);
@@ -399,7 +401,7 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
           for (int rk = 0; rk < c.C; ++rk)
             if (rk != c.rank) st_dsmem_f4(mapa_shared(a_local + off, (uint32_t)rk), v);
         }
-        if (hsave && c.row_ok && !(gl2 && BN >= 128 && c.C > 1))  // (L2 gather: TMA-stored below)
+        if (hsave && c.row_ok && !l2_path)  // (L2 gather: TMA-stored below)
           *reinterpret_cast<uint4*>(hsave + (size_t)c.grow * p.h_ld[l] + k) = make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
@@ -430,7 +432,7 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
         }
         LOKA_STRACE(c, 2 + 7 * l + 5);
       }
-    } else if (BN >= 128 && gl2) {
+    } else if (l2_path) {
       // The slice [n0, n0 + BN) of h_{l+1} is BN/128 whole 16 KB K blocks of the A tile.  Its
       // codes also went to global memory (p.h_save[l], L2-resident); one TMA load per K block,
       // multicast to every peer, brings them back into the peers' A tiles and completes on each
@@ -727,7 +729,7 @@ cudaError_t launch_stack(const StackParams& p, cudaStream_t st) {
   // (a DSMEM-gather instance was measured 2 us slower per step than the L2 one: not instantiated)
   const bool spec = p.C == 4 && all_ln && (p.gather == kStackGatherL2 || p.gather == kStackGatherL2StAsync);
   const bool hyb = p.gather == kStackGatherL2StAsync;
-  const int inst = (g_strace_host ? 3 : 0) + (spec ? (hyb ? 2 : 1) : 0);
+  const int inst = (g_strace_host ? 3 : 0) + (spec ? (hyb ? 2 : 1) : 0);  // (mode 4: generic instance)
   auto kern = inst == 0   ? stack_kernel<false, 0, -1>
               : inst == 1 ? stack_kernel<false, 4, kStackGatherL2>
               : inst == 2 ? stack_kernel<false, 4, kStackGatherL2StAsync>
