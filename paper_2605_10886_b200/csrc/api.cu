@@ -1443,6 +1443,18 @@ loka_status loka_probe_error(int32_t L, const loka_probe_pair* pairs, double flo
     const int rv = aligned16(q.ref) && (q.ld_ref * elem_size(q.ref_dtype)) % 16 == 0;
     layers[l] = ProbeLayer{q.out, q.ref, q.out_dtype == LOKA_BF16, q.ref_dtype == LOKA_BF16, q.M, q.N, q.ld_out, q.ld_ref,
                            ov, rv};
+    // The statistic is a sum over elements, blind to row boundaries: dense pairs (ld = N) are
+    // viewed as rows of kW = 2048 elements, so narrow layers (cfg3: N = 128 ... 2048) run the
+    // kernels' wide-span paths with every lane busy.
+    constexpr int64_t kW = 2048;
+    const int64_t cnt = q.M * q.N;
+    if (q.ld_out == q.N && q.ld_ref == q.N && cnt >= kW && cnt % kW == 0 && q.N != kW) {
+      ProbeLayer& y = layers[l];
+      y.M = cnt / kW;
+      y.N = y.ld_out = y.ld_ref = kW;
+      y.out_vec = aligned16(q.out);
+      y.ref_vec = aligned16(q.ref);
+    }
   }
   loka_status st = check_device();
   if (st != LOKA_OK) return st;

@@ -85,8 +85,27 @@ __global__ void __launch_bounds__(256) probe_p1(const __grid_constant__ ProbeBat
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nw = (int64_t)nblk * 8;
   double acc = 0.0;
+  const bool fast = L.ref_vec && L.ref_bf16;
   for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < L.M; row += nw) {
-    for (int64_t c0 = lane * 8; c0 < L.N; c0 += 512) {  // two independent 16-B loads per lane in flight
+    int64_t cstart = lane * 8;
+    if (fast) {  // whole 256*U-column spans: U independent 16-B loads per lane in flight
+      constexpr int U = 8;
+      for (; (cstart - lane * 8) + 256 * U <= L.N; cstart += 256 * U) {  // warp-uniform span test
+        const __nv_bfloat16* rp = reinterpret_cast<const __nv_bfloat16*>(L.ref) + row * L.ld_ref + cstart;
+        uint4 rv4[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) rv4[u] = __ldg(reinterpret_cast<const uint4*>(rp + 256 * u));
+        float s = 0.f;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t w[4] = {rv4[u].x, rv4[u].y, rv4[u].z, rv4[u].w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) s += fabsf(bf16lo_to_f32(w[i])) + fabsf(bf16hi_to_f32(w[i]));
+        }
+        acc += (double)s;
+      }
+    }
+    for (int64_t c0 = cstart; c0 < L.N; c0 += 512) {  // two independent 16-B loads per lane in flight
       float v[8], u[8];
       load8(L.ref, L.ref_bf16, row * L.ld_ref + c0, v, (int)max((int64_t)0, imin64(8, L.N - c0)), L.ref_vec);
       load8(L.ref, L.ref_bf16, row * L.ld_ref + c0 + 256, u, (int)max((int64_t)0, imin64(8, L.N - c0 - 256)),
@@ -218,21 +237,36 @@ __global__ void __launch_bounds__(256) probe_p2(const __grid_constant__ ProbeBat
   }
 }
 
-__global__ void probe_p3(const __grid_constant__ ProbeBatch b, const double* part1, const double* part2,
-                         const float* partmax, const long long* partfl, int nblk, ProbeStatsDev* out) {
-  if (threadIdx.x != 0) return;
+// One 256-thread block per layer: strided per-thread sums in a fixed order, then the fixed shuffle
+// tree of block_sum (deterministic; s1 is bit-identical to the sum P2 derived f from).  (A single
+// thread walking nblk ~ 1200 partials serially took 130 us for one 32768 x 4096 layer.)
+__global__ void __launch_bounds__(256) probe_p3(const __grid_constant__ ProbeBatch b, const double* part1,
+                                                const double* part2, const float* partmax,
+                                                const long long* partfl, int nblk, ProbeStatsDev* out) {
+  __shared__ double red[8];
+  __shared__ long long redl[8];
+  __shared__ float redf[8];
   const int l = blockIdx.x;
   const ProbeLayer& L = b.layer[l];
   double s1 = 0.0, s2 = 0.0;
   float m = 0.f;
   long long nf = 0;
-  for (int i = 0; i < nblk; ++i) {
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
     const int64_t k = (int64_t)l * nblk + i;
     s1 += part1[k];
     s2 += part2[k];
     m = fmaxf(m, partmax[k]);
     nf += partfl[k];
   }
+  s1 = block_sum(s1, red);
+  s2 = block_sum(s2, red);
+  nf = block_sum(nf, redl);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+  if ((threadIdx.x & 31) == 0) redf[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int i = 1; i < 8; ++i) m = fmaxf(m, redf[i]);
   const long long count = (long long)(L.M * L.N);
   ProbeStatsDev st;
   st.mere = count > 0 ? s2 / (double)count : 0.0;
@@ -258,7 +292,7 @@ cudaError_t launch_probe(const ProbeLayer* layers, int L, int64_t /*max_elems*/,
     float* partmax = reinterpret_cast<float*>(ws + 3 * n);
     probe_p1<<<dim3((unsigned)nblk, (unsigned)nl), 256, 0, st>>>(b, part1, nblk);
     probe_p2<<<dim3((unsigned)nblk, (unsigned)nl), 256, 0, st>>>(b, part1, part2, partmax, partfl, nblk, floor_rel);
-    probe_p3<<<dim3((unsigned)nl), 32, 0, st>>>(b, part1, part2, partmax, partfl, nblk,
+    probe_p3<<<dim3((unsigned)nl), 256, 0, st>>>(b, part1, part2, partmax, partfl, nblk,
                                                 reinterpret_cast<ProbeStatsDev*>(stats_dev) + l0);
     note_launch(3);
     cudaError_t e = cudaGetLastError();
