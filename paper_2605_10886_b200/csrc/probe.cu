@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(256) probe_p2(const __grid_constant__ ProbeBat
     const bool fast = L.out_vec && L.ref_vec && L.out_bf16 && L.ref_bf16 && f32 > 0.f;
     int64_t cstart = lane * 8;
     if (fast) {
-      constexpr int U = 4;  // 16-B loads of each operand per lane in flight
+      constexpr int U = 8;  // 16-B loads of each operand per lane in flight
       for (; (cstart - lane * 8) + 256 * U <= L.N; cstart += 256 * U) {  // warp-uniform span test
         const __nv_bfloat16* op = reinterpret_cast<const __nv_bfloat16*>(L.out) + row * L.ld_out + cstart;
         const __nv_bfloat16* rp = reinterpret_cast<const __nv_bfloat16*>(L.ref) + row * L.ld_ref + cstart;
