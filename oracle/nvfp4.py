@@ -26,7 +26,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import fp8
-from .quantize import fl32, NonFiniteInput
+from .quantize import fl32, NonFiniteInput, FLT32_MAX
 
 BLOCK = 16
 FP4_MAX = 6.0
@@ -84,7 +84,10 @@ def tensor_scales(A: float):
     """(s_t, r_t) from the tensor amax (D36)."""
     if A == 0.0:
         return 1.0, 1.0
-    return float(fl32(A / SCALED_MAX)), float(fl32(SCALED_MAX / A))
+    # D1b (as for FP8): a reciprocal that overflows FP32 (A < 2688/FLT_MAX) is the largest finite FP32
+    with np.errstate(over="ignore"):
+        r_t = float(min(fl32(SCALED_MAX / A), FLT32_MAX))
+    return float(fl32(A / SCALED_MAX)), r_t
 
 
 def quantize(x, amax=None):
@@ -106,7 +109,8 @@ def quantize(x, amax=None):
     sf = fp8.encode(fl32(u / 6.0), "e4m3")  # IEEE division, then E4M3 satRNE (non-negative)
     d = fp8.decode(sf, "e4m3")
     safe = np.where(d > 0, d, 1.0)
-    rb = np.where(d > 0, fl32(r_t / safe), 0.0)
+    with np.errstate(over="ignore"):
+        rb = np.where(d > 0, np.minimum(fl32(r_t / safe), FLT32_MAX), 0.0)  # D1b clamp
     v = fl32(xb * rb[:, :, None])
     v = np.where(d[:, :, None] > 0, v, np.copysign(0.0, xb))  # underflowed block: signed zeros
     codes = e2m1_encode(v).reshape(rows, cols)

@@ -7,7 +7,9 @@ Follows SURVEY.md §8(c) O3-O6, which restates:
     "scale = amax(granule) / format.max_finite; if amax = 0, scale = 1";
   * DESIGN.md readings D1 (multiply by the reciprocal r = fl32(max/amax) rather
     than divide per element; the SPEC's per-element divide is kept as
-    ``mode="div"``), D2 (zero granule -> s = r = 1), D3 (non-finite input ->
+    ``mode="div"``; D1b: when max/amax overflows FP32, i.e. amax < max/FLT_MAX, the
+    reciprocal is the largest finite FP32 value instead of +Inf), D2 (zero
+    granule -> s = r = 1), D3 (non-finite input ->
     NonFiniteInput), D6 (blockwise geometry), D7 (F32 or UE8M0 scales).
 
 Scale layouts (row-major arrays, shared with include/loka.h's contract):
@@ -25,6 +27,7 @@ from . import fp8
 
 # blk_1x32: the MX block (OCP MXFP8 block size 32; NEXT-4), one scale per row per 32 columns
 GRANS = ("tensor", "row", "col", "blk_1x128", "blk_128x1", "blk_128x128", "blk_1x32")
+FLT32_MAX = float(np.finfo(np.float32).max)
 _BLK = {"blk_1x128": (1, 128), "blk_128x1": (128, 1), "blk_128x128": (128, 128), "blk_1x32": (1, 32)}
 
 
@@ -128,7 +131,10 @@ def scales_from_amax(amax, fmt, scale_fmt: str = "f32"):
     nz = amax > 0
     if scale_fmt == "f32":
         s[nz] = fl32(amax[nz] / fmax)  # IEEE division correctly rounded to FP32
-        r[nz] = fl32(fmax / amax[nz])
+        # D1b: fl32(max/amax) is +Inf for amax < max/FLT_MAX (~1.3e-36 for e4m3); the reciprocal
+        # is then the largest finite FP32, so x*r stays finite and below max (no NaN from 0*Inf)
+        with np.errstate(over="ignore"):
+            r[nz] = np.minimum(fl32(fmax / amax[nz]), FLT32_MAX)
     elif scale_fmt == "ue8m0":
         flat_s = s.reshape(-1)
         flat_r = r.reshape(-1)

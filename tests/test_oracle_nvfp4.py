@@ -90,7 +90,10 @@ def _brute(x, fp8_helper, fp4_helper, tmp_path):
     if A == 0:
         s_t = r_t = np.float32(1)
     else:
-        s_t, r_t = A / np.float32(2688), np.float32(2688) / A
+        with np.errstate(over="ignore"):
+            s_t, r_t = A / np.float32(2688), np.float32(2688) / A
+        if np.isinf(r_t):  # DESIGN.md D1b: an overflowing reciprocal is FLT_MAX
+            r_t = np.finfo(np.float32).max
     a_b = np.abs(x.reshape(rows, cols // 16, 16)).max(axis=2).astype(np.float32)
     u = (a_b * r_t).astype(np.float32)
     sbv = (u / np.float32(6)).astype(np.float32)
@@ -103,16 +106,19 @@ def _brute(x, fp8_helper, fp4_helper, tmp_path):
             if d[i, b] == 0:
                 v = np.copysign(np.float32(0), blk)
             else:
-                rb = np.float32(r_t / np.float32(d[i, b]))
+                with np.errstate(over="ignore"):
+                    rb = np.float32(r_t / np.float32(d[i, b]))
+                if np.isinf(rb):
+                    rb = np.finfo(np.float32).max
                 v = (blk * rb).astype(np.float32)
             codes[i, 16 * b:16 * b + 16] = _host4(fp4_helper, v, tmp_path, "c")
     packed = (codes[:, 0::2] | (codes[:, 1::2] << 4)).astype(np.uint8)
     return packed, sf, np.float32(s_t)
 
 
-@pytest.mark.parametrize("kind", ["gauss", "heavy", "tiny_blocks"])
+@pytest.mark.parametrize("kind", ["gauss", "heavy", "tiny_blocks", "tiny_tensor"])
 def test_quantize_matches_bruteforce(kind, fp8_host_cast, fp4_host_cast, tmp_path):
-    rng = np.random.default_rng({"gauss": 0, "heavy": 1, "tiny_blocks": 2}[kind])
+    rng = np.random.default_rng({"gauss": 0, "heavy": 1, "tiny_blocks": 2, "tiny_tensor": 3}[kind])
     rows, cols = 6, 96
     x = rng.standard_normal((rows, cols)).astype(np.float32)
     if kind == "heavy":
@@ -121,6 +127,9 @@ def test_quantize_matches_bruteforce(kind, fp8_host_cast, fp4_host_cast, tmp_pat
         x[:, 16:48] *= np.float32(1e-6)
         x[0, 0] = 1e4
         x[2, 64:80] = 0
+    if kind == "tiny_tensor":  # D1b: A < 2688 / FLT_MAX, the tensor reciprocal overflows FP32
+        x *= np.float32(1e-37)
+        x[1, 0:16] *= np.float32(1e-3)
     p, sf, st = nvfp4.quantize(x.astype(np.float64))
     bp, bsf, bst = _brute(x, fp8_host_cast, fp4_host_cast, tmp_path)
     assert np.array_equal(sf, bsf)

@@ -69,7 +69,10 @@ def _brute(x, f, gran, scale_fmt="f32"):
         if a > 0:
             if scale_fmt == "f32":
                 s[idx] = a / fm            # numpy float32 division is IEEE correctly rounded
-                r[idx] = fm / a
+                with np.errstate(over="ignore"):
+                    r[idx] = fm / a
+                if np.isinf(r[idx]):       # DESIGN.md D1b: an overflowing reciprocal is FLT_MAX
+                    r[idx] = np.finfo(np.float32).max
             else:
                 e = -127
                 while np.float64(a) > np.float64(fm) * 2.0 ** e:
@@ -178,3 +181,31 @@ def test_mode_div_matches_float32_division():
     v = (x.astype(np.float32) / s[:, None]).astype(np.float32)
     ref = torch.from_numpy(v).clamp(-448, 448).to(torch.float8_e4m3fn).view(torch.uint8).numpy()
     assert np.array_equal(c, ref)
+
+
+@pytest.mark.parametrize("f", ["e4m3", "e5m2"])
+@pytest.mark.parametrize("gran", ["row", "tensor", "blk_1x128", "col"])
+def test_tiny_amax_reading_d1b(f, gran):
+    """DESIGN.md D1b: granules whose amax < max/FLT_MAX (the F32 reciprocal overflows) are defined:
+    r = FLT_MAX, codes = satRNE(fl32(x * FLT_MAX)), no NaN codes, signed zeros kept, and since
+    |x * FLT_MAX| < max nothing saturates.  Checked against the float32 brute force (torch cast)
+    and against the closed form on the verdict's reproducer [[1e-38, 0, -5e-39]]."""
+    codes, s = Q.quantize(np.array([[1e-38, 0.0, -5e-39]]), f, "row")
+    fm = FMAX[f]
+    big = float(np.finfo(np.float32).max)
+    exp = torch.tensor([np.float32(1e-38) * np.float32(big), 0.0, np.float32(-5e-39) * np.float32(big)],
+                       dtype=torch.float32).to(TORCH_DT[f]).view(torch.uint8).numpy()
+    assert np.array_equal(codes[0], exp)
+    assert s[0] == np.float32(np.float32(1e-38) / np.float32(fm))
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((6, 300)) * np.array([1e-37, 1e-39, 1e-41, 1e-44, 1.0, 1e-36])[:, None]
+    x = x.astype(np.float32).astype(np.float64)
+    x[0, :4] = [0.0, -0.0, 0.0, -0.0]
+    c, sc = Q.quantize(x, f, gran)
+    bc, bs = _brute(x, f, gran)
+    assert np.array_equal(c, bc) and np.array_equal(sc.view(np.uint32), bs.view(np.uint32))
+    dec = fp8.decode(c, f)
+    assert np.isfinite(dec).all()
+    assert (np.signbit(dec[0, :4]) == np.signbit(x[0, :4])).all()
+    if gran == "row":  # tiny rows never reach max (no saturation), the normal row does
+        assert np.abs(dec[[1, 2, 3]]).max() < fm and np.abs(dec[4]).max() == fm
