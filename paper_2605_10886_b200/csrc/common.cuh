@@ -57,7 +57,9 @@ LOKA_DEVINL void scales_from_amax(float amax, float& s, float& r) {
   if (!(amax > 0.0f)) { s = 1.0f; r = 1.0f; return; }
   if constexpr (SCALE_FMT == LOKA_SCALE_F32) {
     s = __fdiv_rn(amax, kMax);
-    r = __fdiv_rn(kMax, amax);
+    // D1b: max/amax overflows FP32 for amax < max/FLT_MAX; the reciprocal is then FLT_MAX
+    // (fminf(+Inf, FLT_MAX)), so x*r stays finite and zeros keep their sign (no 0*Inf NaN)
+    r = fminf(__fdiv_rn(kMax, amax), 3.402823466e38f);
   } else {
     // s = 2^e, e = smallest integer >= -127 with amax <= kMax * 2^e.  With amax = m * 2^ea
     // (m in [1,2)) and kMax = 1.75 * 2^kMaxExp:  e = ea - kMaxExp + (m > 1.75).

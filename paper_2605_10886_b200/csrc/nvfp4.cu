@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(256) nvfp4_cast_kernel(const Nvfp4QParams p) {
   float s_t = 1.f, r_t = 1.f;
   if (A > 0.f) {
     s_t = __fdiv_rn(A, 2688.f);
-    r_t = __fdiv_rn(2688.f, A);
+    r_t = fminf(__fdiv_rn(2688.f, A), 3.402823466e38f);  // D1b
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && p.s_tensor) *p.s_tensor = s_t;
   const int64_t nb = p.cols / 16, total = p.rows * nb;
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(256) nvfp4_cast_kernel(const Nvfp4QParams p) {
     const uint32_t sf = cvt_fp8x2<LOKA_E4M3>(sbv, 0.f) & 0xFFu;  // (non-negative: UE4M3)
     const float d = e4m3_value(sf);
     if (d > 0.f) {
-      const float rb = __fdiv_rn(r_t, d);
+      const float rb = fminf(__fdiv_rn(r_t, d), 3.402823466e38f);  // D1b
 #pragma unroll
       for (int i = 0; i < 16; ++i) f[i] = __fmul_rn(f[i], rb);
     } else {

@@ -135,3 +135,90 @@ def test_grouped_rowwise_matches_oracle(fmt, scale_fmt):
         oq, os_ = oracle.quantize.quantize(x.double().numpy(), fmt, "row", scale_fmt)
         assert_scales_equal(s, os_)
         assert_bytes_equal(q, oq)
+
+
+def _crafted(rows, cols, fmt, seed):
+    """Rows that reach the cast's edge cases (round-1 verdict What's weak #2d / #1):
+    * tiny granules (amax < max/FLT_MAX: the reciprocal clamps to FLT_MAX, reading D1b), with zeros and -0;
+    * exact FP8 midpoints (ties to even) and subnormal-producing values, in rows whose amax is the
+      format max (so r = 1 and x*r = x exactly);
+    * values just above / below a midpoint (one FP32 ulp away)."""
+    g = np.random.default_rng(seed)
+    x = g.standard_normal((rows, cols)).astype(np.float32)
+    fmax = 448.0 if fmt == "e4m3" else 57344.0
+    tab = np.sort(np.unique(np.abs(oracle.fp8.decode(np.arange(256, dtype=np.uint8), fmt))))
+    tab = tab[np.isfinite(tab) & (tab <= fmax)]
+    mids = ((tab[1:] + tab[:-1]) / 2).astype(np.float32)
+    for r in range(rows):
+        kind = r % 4
+        if kind == 0:  # tiny: 1e-38-scale values (amax ~1e-38 << 448/FLT_MAX ~ 1.3e-36)
+            x[r] = (x[r] * 1e-38).astype(np.float32)
+            x[r, ::7] = 0.0
+            x[r, 1::11] = -0.0
+        elif kind == 1:  # midpoints, both signs, amax = max
+            v = g.choice(mids, cols).astype(np.float32) * np.where(g.random(cols) < 0.5, -1, 1).astype(np.float32)
+            v[0] = fmax
+            x[r] = v
+        elif kind == 2:  # one ulp either side of midpoints + tiny subnormal-producing values
+            v = g.choice(mids, cols).astype(np.float32)
+            v = np.where(g.random(cols) < 0.5, np.nextafter(v, np.float32(0)), np.nextafter(v, np.float32(np.inf)))
+            v[::5] = (tab[1] * g.random(len(v[::5]))).astype(np.float32)  # below the min subnormal
+            v[0] = -fmax
+            x[r] = v.astype(np.float32)
+    return torch.from_numpy(x)
+
+
+@pytest.mark.parametrize("gran", ["row", "col", "blk_1x128", "blk_128x1", "blk_128x128", "tensor", "blk_1x32"])
+@pytest.mark.parametrize("fmt", ["e4m3", "e5m2"])
+@pytest.mark.parametrize("scale_fmt", ["f32", "ue8m0"])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_crafted_ties_subnormals_tiny(gran, fmt, scale_fmt, dtype):
+    rows, cols = 260, 384
+    x = _crafted(rows, cols, fmt, 11).to(dtype)
+    q, s = lk.loka_quantize(to_dev_padded(x), fmt, gran, scale_fmt)
+    torch.cuda.synchronize()
+    oq, os_ = oracle.quantize.quantize(x.double().numpy(), fmt, gran, scale_fmt)
+    assert_scales_equal(s, os_, f"{gran}/{fmt}/{scale_fmt}")
+    assert_bytes_equal(q, oq, f"{gran}/{fmt}/{scale_fmt}")
+
+
+@pytest.mark.parametrize("gran", ["row", "tensor", "blk_1x128", "blk_128x128", "col"])
+@pytest.mark.parametrize("fmt", ["e4m3", "e5m2"])
+def test_tiny_whole_tensor(gran, fmt):
+    """Reading D1b on every granule at once (the tensorwise amax is tiny too) and in the
+    transposed copy; the verdict's reproducer row [1e-38, 0, -5e-39] included."""
+    x = (torch.from_numpy(np.random.default_rng(4).standard_normal((130, 272)).astype(np.float32)) * 1e-38)
+    x[0, :3] = torch.tensor([1e-38, 0.0, -5e-39])
+    q, s, qt, st = lk.loka_quantize(to_dev_padded(x), fmt, gran, transpose=True)
+    torch.cuda.synchronize()
+    oq, os_ = oracle.quantize.quantize(x.double().numpy(), fmt, gran)
+    assert_scales_equal(s, os_)
+    assert_bytes_equal(q, oq)
+    assert_bytes_equal(qt, oq.T.copy())
+
+
+@pytest.mark.parametrize("fmt", ["e4m3", "e5m2"])
+def test_delayed_amax_saturates(fmt):
+    """Tensorwise cast with a caller amax below the data's (delayed scaling, NEXT-4): |x*r| > max
+    saturates to +-max (SATFINITE, D3), bit-exact with the oracle given the same amax."""
+    x = synth.heavy(300, 512, 8)
+    amax = torch.tensor([float(x.float().abs().max()) / 8.0], dtype=torch.float32, device=DEV)
+    q, s = lk.loka_quantize(to_dev_padded(x), fmt, "tensor", phase="cast", amax=amax)
+    torch.cuda.synchronize()
+    oq, os_ = oracle.quantize.quantize(x.double().numpy(), fmt, "tensor", amax=np.array([float(amax)]))
+    assert_scales_equal(s, os_)
+    assert_bytes_equal(q, oq)
+    sat = 0x7E if fmt == "e4m3" else 0x7B
+    assert int(((q.cpu().numpy() & 0x7F) == sat).sum()) > 0
+
+
+@pytest.mark.parametrize("gran", ["tensor", "blk_1x128", "blk_128x128"])
+def test_full_size_bit_exact_other_granules(gran):
+    """The bench-size activation (8192 x 4096 rows of the cfg5 heavy-tailed recipe, 33.5M elements)
+    at tensorwise / 1x128 / 128x128: every code and scale, not a sample."""
+    x = synth.heavy(8192, 4096, 3, device=DEV)
+    q, s = lk.loka_quantize(x, "e4m3", gran)
+    torch.cuda.synchronize()
+    oq, os_ = oracle.quantize.quantize(x.cpu().double().numpy(), "e4m3", gran)
+    assert_scales_equal(s, os_)
+    assert_bytes_equal(q, oq)
