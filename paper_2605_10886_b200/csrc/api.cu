@@ -294,7 +294,10 @@ static size_t mx_ws_bytes(const loka_linear_args* a) {
 static bool pair_eligible(const loka_linear_args* a);
 static size_t split_ws_bytes(const loka_linear_args* a);
 static bool wide_norm_unfused(const loka_linear_args* a);
+static bool pair_norm_taken(const loka_linear_args* a, size_t* ws);
 size_t loka_linear_workspace_size(const loka_linear_args* a) {
+  size_t pn = 0;
+  if (pair_norm_taken(a, &pn)) return pn;
   if (wide_norm_unfused(a)) return (size_t)a->M * (size_t)a->N * 4;
   return mx_ws_bytes(a) + (pair_eligible(a) ? split_ws_bytes(a) : 0);
 }
@@ -321,8 +324,8 @@ static loka_status mx_pack(const loka_linear_args* a, LinearParams* p, void* ws,
 }
 
 // nvf4: the operands are NVFP4 presented as byte tensors [rows, K/2] (loka_nvfp4_linear_norm)
-static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CUtensorMap* tb, CUtensorMap* ty,
-                                  LinearParams* p, int* bn_out, bool nvf4 = false) {
+// Argument checks shared by every linear route (shapes, pointers, alignment, enum ranges).
+static loka_status validate_linear(const loka_linear_args* a, bool nvf4 = false) {
   if (!a) return LOKA_ERR_INVALID_ARG;
   const int64_t M = a->M, N = a->N, K = a->K;
   if (M <= 0 || N <= 0 || K <= 0 || M > (1ll << 31) - 1 || N > (1ll << 30) || K > (1ll << 31) - 1)
@@ -355,6 +358,19 @@ static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CU
     return LOKA_ERR_INVALID_ARG;
   if ((a->save_xhat || a->save_rstd) && a->norm == LOKA_NORM_NONE) return LOKA_ERR_INVALID_ARG;
   if (a->amax_out && (fp8_out || (reinterpret_cast<uintptr_t>(a->amax_out) & 3))) return LOKA_ERR_INVALID_ARG;
+  if (a->norm == LOKA_NORM_BLOCK_RMS && (a->norm_block <= 0 || N % a->norm_block)) return LOKA_ERR_SHAPE;
+  return LOKA_OK;
+}
+
+static loka_status prepare_linear(const loka_linear_args* a, CUtensorMap* ta, CUtensorMap* tb, CUtensorMap* ty,
+                                  LinearParams* p, int* bn_out, bool nvf4 = false) {
+  loka_status vs = validate_linear(a, nvf4);
+  if (vs != LOKA_OK) return vs;
+  const int64_t M = a->M, N = a->N, K = a->K;
+  const loka_tensor &A = a->a, &B = a->b, &Y = a->y;
+  const bool mx = is_mx(a) || nvf4;
+  const bool fp8_out = is_fp8(Y.dtype);
+  const bool bwd = a->bwd_xhat != nullptr;
 
   // Tile width BN in {64,128,256}: the widest tile that still gives >= ~120 CTAs (most of the
   // 148 SMs) for this M, else the narrowest allowed.  Row-coupled epilogues (full-row norm or an
@@ -700,8 +716,119 @@ static loka_status run_wide_norm(const loka_linear_args* a, void* ws, size_t ws_
   return launch_rownorm(rp, sms, s) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
 }
 
+// ---- a4 + a5 at scale: the norm fused into the CTA-pair engine (pairnorm.cu) ------------------
+// Rows wider than one pair tile exchange row records through the caller's workspace
+// (pair_xchg_bytes: flags zeroed by a memset in the same stream before the launch, then records).
+static int pair_norm_env() {  // LOKA_PAIRNORM: 0 = off; 256 / 512 = force the tile width (read per call)
+  const char* e = std::getenv("LOKA_PAIRNORM");
+  return e ? std::atoi(e) : -1;
+}
+struct PnPlan {
+  bool ok = false, xchg = false;
+  int tn = 512, tiles_n = 1, row_blocks = 1, groups = 1, pairs = 0, order = 0;
+};
+static PnPlan pair_norm_plan(const loka_linear_args* a, int sms) {
+  PnPlan pl;
+  const int env = pair_norm_env();
+  if (!a || env == 0 || !use_pair_kernel() || is_mx(a) || a->bwd_xhat || a->save_xhat || a->save_rstd) return pl;
+  if (a->a.gran != LOKA_GRAN_TENSOR && a->a.gran != LOKA_GRAN_ROW) return pl;
+  if (a->b.gran != LOKA_GRAN_TENSOR && a->b.gran != LOKA_GRAN_ROW) return pl;
+  const bool blk = a->norm == LOKA_NORM_BLOCK_RMS;
+  if (a->norm != LOKA_NORM_LAYER && a->norm != LOKA_NORM_RMS && !(blk && a->norm_block == 256)) return pl;
+  if (a->M <= 0 || a->N <= 0 || a->K <= 0 || a->N > 16384) return pl;
+  const bool fp8_out = is_fp8(a->y.dtype);
+  if (fp8_out && (a->gamma || a->beta || a->act != LOKA_ACT_NONE)) return pl;  // row amax not monotone
+  pl.tn = (env == 256 || env == 512) ? env : (a->N <= 256 ? 256 : 512);
+  pl.tiles_n = (int)cdiv(a->N, pl.tn);
+  pl.row_blocks = (int)cdiv(a->M, 256);
+  pl.xchg = pl.tiles_n > 1 && (!blk || fp8_out);
+  const int avail = std::min(sms / 2, kPnMaxPairs);
+  const int64_t tiles = (int64_t)pl.row_blocks * pl.tiles_n;
+  // enough tiles for the pairs, or a row wider than the single-CTA engine's clusters (N > 2048)
+  const bool big = tiles >= avail || (!blk && a->N > 2048) || env == 256 || env == 512;
+  if (!big) return pl;
+  // a single accumulator (TN = 512) cannot wait for a peer's next wave without idling its tensor
+  // core, so its pairs walk row blocks in static groups of tiles_n; double-buffered tiles (TN = 256)
+  // go round-robin over all pairs (a row block's tiles then span at most two waves)
+  pl.order = (pl.xchg && pl.tn == 512) ? 1 : 0;
+  if (pl.xchg && (pl.tiles_n > avail || pl.tiles_n > 32)) return pl;
+  if (pl.order) {
+    pl.groups = std::min(avail / pl.tiles_n, pl.row_blocks);
+    pl.pairs = pl.groups * pl.tiles_n;
+  } else {
+    pl.pairs = (int)std::min<int64_t>(avail, tiles);
+  }
+  pl.ok = pl.pairs > 0;
+  return pl;
+}
+static size_t pair_norm_ws(const PnPlan& pl) { return pl.xchg ? pair_xchg_bytes(pl.row_blocks, pl.tiles_n) : 0; }
+static loka_status run_pair_norm(const loka_linear_args* a, const PnPlan& pl, void* ws, size_t ws_bytes,
+                                 cudaStream_t s) {
+  const size_t need = pair_norm_ws(pl);
+  if (need && (!ws || ws_bytes < need || !aligned16(ws))) return LOKA_ERR_WORKSPACE;
+  PairNormParams p;
+  std::memset(&p, 0, sizeof(p));
+  const loka_tensor &A = a->a, &B = a->b, &Y = a->y;
+  if (!make_map_u8(&p.ta, A.data, a->M, a->K, A.ld, 128)) return LOKA_ERR_CUDA;
+  if (!make_map_u8(&p.tb, B.data, a->N, a->K, B.ld, 128)) return LOKA_ERR_CUDA;
+  if (!make_map_out(&p.ty, Y.data, a->M, a->N, Y.ld, Y.dtype, 128, 32u)) return LOKA_ERR_CUDA;
+  p.M = (int32_t)a->M;
+  p.N = (int32_t)a->N;
+  p.K = (int32_t)a->K;
+  p.a_fmt = A.dtype == LOKA_E5M2 ? 1 : 0;
+  p.b_fmt = B.dtype == LOKA_E5M2 ? 1 : 0;
+  p.sa = A.scales;
+  p.sa_row = A.gran == LOKA_GRAN_ROW;
+  p.sb = B.scales;
+  p.sb_row = B.gran == LOKA_GRAN_ROW;
+  p.bias = a->bias;
+  p.bias_bf16 = a->bias_dtype == LOKA_BF16;
+  p.gamma = a->gamma;
+  p.beta = a->beta;
+  p.eps = a->eps > 0.f ? a->eps : (a->norm == LOKA_NORM_LAYER ? 1e-5f : 1e-6f);
+  p.norm = a->norm;
+  p.act = a->act;
+  p.out_dtype = Y.dtype;
+  p.y_scales = is_fp8(Y.dtype) ? Y.scales : nullptr;
+  p.precast = a->debug_precast;
+  p.ld_pre = a->N;
+  p.amax_out = a->amax_out;
+  p.status = a->status_dev;
+  p.tiles_n = pl.tiles_n;
+  p.row_blocks = pl.row_blocks;
+  p.xchg = pl.xchg ? 1 : 0;
+  p.order = pl.order;
+  p.ngroups = pl.groups;
+  if (pl.xchg) {
+    const size_t flag_bytes = ((size_t)pl.row_blocks * pl.tiles_n * 2 * 4 + 255) & ~size_t(255);
+    p.xws = static_cast<uint8_t*>(ws);
+    p.xrec_off = (int64_t)flag_bytes;
+    if (cudaMemsetAsync(ws, 0, flag_bytes, s) != cudaSuccess) return LOKA_ERR_CUDA;
+  }
+  return launch_pair_norm(p, pl.tn, pl.pairs, s) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
+}
+static PnPlan pair_norm_plan_dev(const loka_linear_args* a) {
+  int sms = 148;
+  if (check_device(&sms) != LOKA_OK) return PnPlan{};
+  return pair_norm_plan(a, sms);
+}
+static bool pair_norm_taken(const loka_linear_args* a, size_t* ws) {
+  if (is_blockwise(a)) return false;
+  const PnPlan pl = pair_norm_plan_dev(a);
+  if (pl.ok && ws) *ws = pair_norm_ws(pl);
+  return pl.ok;
+}
+
 loka_status loka_fp8_linear_norm(const loka_linear_args* a, void* ws, size_t ws_bytes, loka_stream_t stream) {
   if (is_blockwise(a)) return run_bw(a, reinterpret_cast<cudaStream_t>(stream));
+  {
+    const PnPlan pl = pair_norm_plan_dev(a);
+    if (pl.ok) {
+      loka_status vs = validate_linear(a);
+      if (vs != LOKA_OK) return vs;
+      return run_pair_norm(a, pl, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+    }
+  }
   if (wide_norm_unfused(a)) return run_wide_norm(a, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
   if (mx_pair_ok(a)) {
     if (!ws || ws_bytes < mx_ws_bytes(a) || !aligned16(ws)) return LOKA_ERR_WORKSPACE;

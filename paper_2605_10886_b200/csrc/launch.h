@@ -303,4 +303,35 @@ cudaError_t launch_matnorm_init(const void* w, bool bf16, int64_t ldw, float* me
                                 int64_t nn, cudaStream_t st);
 cudaError_t launch_matnorm_update(const MatnormParams& p, cudaStream_t st);
 
+// ---- a4 + a5 at scale: CTA-pair GEMM with the norm fused in the epilogue (pairnorm.cu) ----
+constexpr int kPnMaxPairs = 128;  // CTA pairs per launch (148 SMs -> 74)
+// workspace of the Case 2 row-record exchange: u32 flags [row_blocks][tiles_n][2] (zeroed before each
+// launch), then float4 records [row_blocks][tiles_n][2][128] at the 256-byte aligned offset
+size_t pair_xchg_bytes(int64_t row_blocks, int tiles_n);
+struct PairNormParams {
+  CUtensorMap ta, tb, ty;  // A [M,K] / B [N,K] codes box {128, 128}; Y box {128 bytes, 32 rows} SW128
+  int32_t M, N, K;
+  int32_t a_fmt, b_fmt;
+  const float* sa; int32_t sa_row;
+  const float* sb; int32_t sb_row;
+  const void* bias; int32_t bias_bf16;
+  const float* gamma; const float* beta;  // nullable (FP8 output: both null)
+  float eps;
+  int32_t norm;       // LAYER, RMS, BLOCK_RMS (block 256, N % 256 == 0)
+  int32_t act;        // loka_act (bf16 / f32 output)
+  int32_t out_dtype;  // f32, bf16, e4m3, e5m2 (+ ROW scales y_scales)
+  float* y_scales;
+  float* precast; int64_t ld_pre;
+  float* amax_out;
+  int32_t* status;
+  int32_t tiles_n;     // ceil(N / TN)
+  int32_t row_blocks;  // ceil(M / 256)
+  int32_t xchg;        // 1: the tiles_n pairs of a row block exchange row records (Case 2)
+  int32_t order;       // 0: round-robin over the tile list; 1: static groups of tiles_n pairs
+  int32_t ngroups;     // order 1: the launch is ngroups x tiles_n pairs
+  uint8_t* xws;        // xchg: flags at 0, records at xrec_off (pair_xchg_bytes)
+  int64_t xrec_off;
+};
+// tn = 512 (one accumulator, two N = 256 MMAs per K step) or 256 (double-buffered accumulators)
+cudaError_t launch_pair_norm(const PairNormParams& p, int tn, int pairs, cudaStream_t st);
 }  // namespace loka

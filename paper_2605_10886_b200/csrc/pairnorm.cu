@@ -1,0 +1,626 @@
+// pairnorm.cu — a4 + a5 at scale: the CTA-pair FP8 GEMM (gemm2.cu's engine) with the row norm
+// fused into its epilogue, so the FP32 tile never goes to HBM ("fuse normalization
+// directly into the GEMM epilogue to minimize HBM I/O"; Case 1 / Case 2).
+//
+// Tile: a 2-CTA cluster (tcgen05.mma.cta_group::2, M = 256) computes 256 rows x TN columns; each
+// CTA holds its 128 rows x TN columns of FP32 accumulator in TMEM.
+//   * TN = 512 ("WIDE"): two N = 256 MMAs per K step share the A stage (the L2 -> SM port saving of
+//     gemm2's WIDE tiles); one accumulator, so a tile's epilogue does not overlap the next tile's MMAs.
+//   * TN = 256: two accumulator buffers; tile j+1's MMAs run while the epilogue drains tile j.
+// Epilogue (8 warps per CTA; warp = TMEM lane quadrant q x column half h; thread = one row x TN/2
+// columns in 32-column chunks):
+//   pass S  tcgen05.ld -> y = acc * s_a[m] * s_b[n] (+ bias[n]) -> per-chunk (mean, M2) (LayerNorm;
+//           Chan's parallel merge of PAPER.md:293-299 applied to column partitions) or sum of
+//           squares (RMS / BlockNorm), y max / min (FP8 row amax); the two halves merged through smem;
+//   xchg    rows wider than one tile (Case 2): the G = ceil(N / TN) pairs that own the column tiles
+//           of one 256-row block run in lock step (a static group of G pairs walks row blocks
+//           gi, gi + #groups, ...); each CTA publishes its 128 row records to global memory (L2) with
+//           a release flag, waits for its G - 1 peers' flags (acquire) and merges the G records in
+//           tile order — bit-identical statistics in every CTA of the row, no cluster needed;
+//   pass N  tcgen05.ld again -> the same y -> (y - mu) * rstd [* gamma + beta] [h-swish] -> bf16 /
+//           f32 / FP8 (row scale from the merged y max / min: the map is monotone) -> swizzled smem
+//           box -> TMA store.
+// Row records are exchanged through global memory rather than DSMEM because a 4096-wide row needs
+// 8 WIDE pairs (16 CTAs), which as one cluster would leave ~14% of the SMs idle (one 16-CTA
+// cluster per GPC); the flags make the exchange an L2 round trip (~1-2 us), overlapped with
+// nothing only for TN = 512.  Co-residency: the grid is one CTA per SM and at most 2 x 74 CTAs.
+#include "common.cuh"
+#include "launch.h"
+
+namespace loka {
+
+constexpr int kPnEpiWarps = 8;
+constexpr int kPnThreads = 64 + 32 * kPnEpiWarps;
+
+template <int TN>
+struct PnCfg {
+  static constexpr int kStages = TN == 512 ? 3 : 4;
+  static constexpr int kAcc = TN == 512 ? 1 : 2;      // accumulator buffers in the 512 TMEM columns
+  static constexpr int kColBufs = TN == 512 ? 1 : 2;  // column-parameter buffers (sb, bias, gamma, beta)
+  static constexpr int kStageA = 128 * 128;
+  static constexpr int kStageB = (TN / 2) * 128;      // per CTA: 128 rows of each 256-column half
+  static constexpr int kOffB = kStages * kStageA;
+  static constexpr int kOffOut = kOffB + kStages * kStageB;      // [8 warps][2][32 rows x 128 B]
+  static constexpr int kOffCol = kOffOut + kPnEpiWarps * 2 * 4096;
+  static constexpr int kOffRec = kOffCol + kColBufs * 4 * TN * 4;  // [2 halves][128 rows] float4
+  static constexpr int kOffBar = kOffRec + 2 * 128 * 16;
+  static constexpr int kSmem = kOffBar + 256 + 1024;
+  static_assert(kSmem <= 227 * 1024, "pairnorm smem");
+};
+
+// Case 2 exchange buffers (caller's workspace): one float4 record per (row block, column tile, CTA
+// rank, row) and one u32 flag per (row block, column tile, CTA rank), zeroed by the host (a memset
+// node in the same stream) before every launch: a record slot is written once per launch, so a flag
+// is a plain 0 -> 1 publish with release / acquire semantics and no state survives a launch.
+size_t pair_xchg_bytes(int64_t row_blocks, int tiles_n) {
+  const size_t slots = (size_t)row_blocks * (size_t)tiles_n * 2;
+  return ((slots * 4 + 255) & ~size_t(255)) + slots * 128 * 16;
+}
+
+LOKA_DEVINL uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+LOKA_DEVINL void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+LOKA_DEVINL float4 ldcg_f4(const float4* p) { return __ldcg(p); }
+
+// spin on a peer's flag with the watchdog of mbar_wait (common.cuh): a wait longer than 4 s
+// records where it stalled and gives up instead of hanging the GPU
+LOKA_DEVINL void flag_wait(const uint32_t* f, int where) {
+  if (ld_acquire_u32(f) != 0u) return;
+  uint64_t t0 = 0;
+  uint32_t spins = 0;
+  while (ld_acquire_u32(f) == 0u) {
+    __nanosleep(20);
+    if ((++spins & 255u) != 0) continue;
+    const uint64_t t = globaltimer_ns();
+    if (t0 == 0) t0 = t;
+    if (*reinterpret_cast<volatile int*>(&g_loka_abort)) return;
+    if (t - t0 > kHangNs) {
+      if (atomicAdd(&g_loka_hang[0], 1ull) == 0) {
+        g_loka_hang[1] = (unsigned long long)(100 + where);
+        g_loka_hang[2] = (unsigned long long)blockIdx.x;
+        g_loka_hang[3] = (unsigned long long)threadIdx.x;
+      }
+      atomicExch(&g_loka_abort, 1);
+      return;
+    }
+  }
+}
+
+LOKA_DEVINL float hswish(float x) {  // x * ReLU6(x + 3) / 6
+  const float t = fminf(fmaxf(x + 3.f, 0.f), 6.f);
+  return __fdiv_rn(__fmul_rn(x, t), 6.f);
+}
+
+template <int TN, int NORM>
+__global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_constant__ PairNormParams p) {
+  using Cf = PnCfg<TN>;
+  constexpr int kHN = TN / 2;     // columns per epilogue thread
+  constexpr int kNch = kHN / 32;  // 32-column chunks per thread
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + Cf::kOffB;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cf::kOffBar);
+  uint64_t* empty_bar = full_bar + Cf::kStages;
+  uint64_t* acc_full = empty_bar + Cf::kStages;  // [2]
+  uint64_t* acc_empty = acc_full + 2;           // [2] (the leader's is used)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  float4* hrec = reinterpret_cast<float4*>(smem + Cf::kOffRec);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = (int)cluster_ctarank();
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int G = p.tiles_n;
+  // schedule: round-robin over the tile list (row-block major; p.order = 0), or static groups of G
+  // pairs that walk row blocks gi, gi + #groups, ... in lock step (p.order = 1: a single-accumulator
+  // tile cannot wait for a peer's next wave without idling its tensor core)
+  const bool xchg = p.xchg != 0;
+  const bool grouped = p.order != 0;
+  const int gi = grouped ? cid / G : 0, gj = grouped ? cid - (cid / G) * G : 0;
+  const int T = p.row_blocks * G;
+  auto tile_of = [&](int k, int& mb, int& nb) -> bool {  // k-th tile of this pair
+    if (grouped) {
+      mb = gi + k * p.ngroups;
+      nb = gj;
+      return mb < p.row_blocks;
+    }
+    const int t = cid + k * ncl;
+    mb = t / G;
+    nb = t - mb * G;
+    return t < T;
+  };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&p.ta);
+    tma_prefetch_desc(&p.tb);
+    tma_prefetch_desc(&p.ty);
+    for (int s = 0; s < Cf::kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 2 * kPnEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_cg2<512>(tmem_slot);
+  pdl_wait();
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int nkb = (p.K + 127) / 128;
+
+  if (warp == 0) {
+    // ===== TMA producer (both CTAs): this CTA's 128 A rows and half of each 256-row B half =====
+    if (lane == 0) {
+      const uint32_t full0 = mapa_shared(smem_u32(full_bar), 0);
+      int it = 0, mb, nb;
+      for (int k = 0; tile_of(k, mb, nb); ++k) {
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % Cf::kStages;
+          const uint32_t ph = (uint32_t)(it / Cf::kStages) & 1u;
+          mbar_wait(&empty_bar[s], ph ^ 1u, 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[s], 2u * (Cf::kStageA + Cf::kStageB));
+          tma_load_2d_cg2(sA + s * Cf::kStageA, &p.ta, full0 + 8u * s, kb * 128, mb * 256 + rank * 128);
+#pragma unroll
+          for (int hh = 0; hh < TN / 256; ++hh)
+            tma_load_2d_cg2(sB + s * Cf::kStageB + hh * 16384, &p.tb, full0 + 8u * s, kb * 128,
+                            nb * TN + hh * 256 + rank * 128);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ===== MMA issuer (leader only) =====
+    if (lane == 0 && rank == 0) {
+      const uint32_t idesc = idesc_f8f6f4(p.a_fmt, p.b_fmt, 256, 256);
+      int it = 0, mb, nb;
+      for (int j = 0; tile_of(j, mb, nb); ++j) {
+        const int buf = Cf::kAcc == 1 ? 0 : (j & 1);
+        const uint32_t use = Cf::kAcc == 1 ? (uint32_t)j : (uint32_t)(j >> 1);
+        mbar_wait(&acc_empty[buf], (use & 1u) ^ 1u, 4);
+        tc_fence_after();
+        const uint32_t dacc = tmem_base + (uint32_t)(buf * 256);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % Cf::kStages;
+          const uint32_t ph = (uint32_t)(it / Cf::kStages) & 1u;
+          mbar_wait(&full_bar[s], ph, 2);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + s * Cf::kStageA);
+          const uint32_t b0 = smem_u32(sB + s * Cf::kStageB);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int hh = 0; hh < TN / 256; ++hh)
+              mma_f8f6f4_cg2(dacc + hh * 256, smem_desc_kmajor_sw128(a0 + k * 32),
+                             smem_desc_kmajor_sw128(b0 + hh * 16384 + k * 32), idesc, (kb | k) ? 1u : 0u);
+          mma_commit_cg2_mc(&empty_bar[s], 3);
+        }
+        mma_commit_cg2_mc(&acc_full[buf], 3);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===== epilogue (both CTAs) =====
+    const int q = warp & 3;          // TMEM lane quadrant (hardware: warp w reads lanes 32 (w % 4) ..)
+    const int h = (warp - 2) >> 2;   // column half
+    const int r = q * 32 + lane;     // row within this CTA's 128
+    const int et = threadIdx.x - 64;  // 0..255
+    uint8_t* stg = smem + Cf::kOffOut + (warp - 2) * 8192;
+    const uint32_t acc_empty0 = mapa_shared(smem_u32(acc_empty), 0);
+    const int esz = p.out_dtype == LOKA_F32 ? 4 : p.out_dtype == LOKA_BF16 ? 2 : 1;
+    const bool fp8_out = esz == 1;
+    const int cpb = 128 / esz;  // columns per 128-byte box row
+    const bool has_gb = p.gamma != nullptr || p.beta != nullptr;
+    const bool act = p.act == LOKA_ACT_HARDSWISH;
+    // fold: with a tensor-wide s_b and no bias, y = acc * c (c = s_a s_b per row), so the statistics
+    // are taken on acc and scaled (mean * c, M2 * c^2), and pass N is one FMA per element
+    const bool fold = !p.sb_row && p.bias == nullptr;
+    const bool need_x = xchg && (NORM != LOKA_NORM_BLOCK_RMS || fp8_out);
+    uint32_t* xflag = reinterpret_cast<uint32_t*>(p.xws);
+    const float4* xrec_r = reinterpret_cast<const float4*>(p.xws + p.xrec_off);
+    float4* xrec = reinterpret_cast<float4*>(p.xws + p.xrec_off);
+    int nbox = 0;
+    int mb, nb;
+    for (int j = 0; tile_of(j, mb, nb); ++j) {
+      const int buf = Cf::kAcc == 1 ? 0 : (j & 1);
+      const uint32_t use = Cf::kAcc == 1 ? (uint32_t)j : (uint32_t)(j >> 1);
+      // ---- column parameters of this tile -> smem (sb, bias, gamma, beta) ----
+      float* colp = reinterpret_cast<float*>(smem + Cf::kOffCol) + (Cf::kColBufs == 1 ? 0 : (j & 1)) * 4 * TN;
+      if (Cf::kColBufs == 1) named_bar_sync(2, 32 * kPnEpiWarps);  // the previous tile's reads are done
+      if (!fold || has_gb) {
+        for (int e = et; e < TN; e += 32 * kPnEpiWarps) {
+          const int n = nb * TN + e;
+          const bool ok = n < p.N;
+          colp[e] = ok ? __ldg(p.sb + (p.sb_row ? n : 0)) : 0.f;
+          float b = 0.f;
+          if (ok && p.bias) b = p.bias_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.bias)[n])
+                                            : reinterpret_cast<const float*>(p.bias)[n];
+          colp[TN + e] = b;
+          colp[2 * TN + e] = (ok && p.gamma) ? __ldg(p.gamma + n) : 1.f;
+          colp[3 * TN + e] = (ok && p.beta) ? __ldg(p.beta + n) : 0.f;
+        }
+      }
+      named_bar_sync(2, 32 * kPnEpiWarps);
+      if (lane == 0) mbar_wait(&acc_full[buf], use & 1u, 3);
+      __syncwarp();
+      tc_fence_after();
+
+      const int grow = mb * 256 + rank * 128 + r;
+      const bool row_ok = grow < p.M;
+      const float sa = row_ok ? __ldg(p.sa + (p.sa_row ? grow : 0)) : 0.f;
+      const float cfold = fold ? __fmul_rn(sa, __ldg(p.sb)) : 1.f;  // y = acc * cfold when folding
+      const float2 sa2 = make_float2(sa, sa);
+      const int col0 = nb * TN + h * kHN;  // first column of this thread
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * 256 + h * kHN);
+      const uint32_t cs = smem_u32(colp + h * kHN);
+      // y = acc * (s_a s_b[n]) + bias[n] for one 32-column chunk (identical instructions in both passes)
+      auto dequant = [&](float (&y)[32], int cb) {
+#pragma unroll
+        for (int c = 0; c < 32; c += 4) {
+          const float4 s4 = lds_f4(cs + 4u * (cb + c)), b4 = lds_f4(cs + 4u * TN + 4u * (cb + c));
+          const float2 a = fadd2(fmul2(make_float2(y[c], y[c + 1]), fmul2(sa2, make_float2(s4.x, s4.y))),
+                                 make_float2(b4.x, b4.y));
+          const float2 b = fadd2(fmul2(make_float2(y[c + 2], y[c + 3]), fmul2(sa2, make_float2(s4.z, s4.w))),
+                                 make_float2(b4.z, b4.w));
+          y[c] = a.x; y[c + 1] = a.y; y[c + 2] = b.x; y[c + 3] = b.y;
+        }
+      };
+
+      // ---- pass S: this thread's statistics over its kHN columns (of acc when folding, else y) ----
+      // Columns >= N hold exact zeros (zero-filled B rows, s_b = bias = 0): sums need no mask,
+      // the LayerNorm chunk M2 is corrected for them and max / min skip them.
+      float cm[kNch], c2[kNch];
+      float ss = 0.f, ymax = -INFINITY, ymin = INFINITY;
+      int nh = 0;  // valid columns of this thread
+#pragma unroll 1
+      for (int c = 0; c < kNch; ++c) {
+        const int cb = 32 * c;
+        const int nv = max(0, min(32, p.N - (col0 + cb)));
+        float y[32];
+        tmem_ld32(tbase + (uint32_t)cb, y);
+        if (!fold) dequant(y, cb);
+        nh += nv;
+        if (nv > 0 && fp8_out) {
+          if (nv == 32) {
+#pragma unroll
+            for (int k = 0; k < 32; k += 2) ymax = fmax3(ymax, y[k], y[k + 1]), ymin = fmin3(ymin, y[k], y[k + 1]);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 32; ++k)
+              if (k < nv) ymax = fmaxf(ymax, y[k]), ymin = fminf(ymin, y[k]);
+          }
+        }
+        if constexpr (NORM == LOKA_NORM_LAYER) {
+          float2 s0 = make_float2(0.f, 0.f), s1 = s0, s2 = s0, s3 = s0;
+#pragma unroll
+          for (int k = 0; k < 32; k += 8) {
+            s0 = fadd2(s0, make_float2(y[k], y[k + 1]));
+            s1 = fadd2(s1, make_float2(y[k + 2], y[k + 3]));
+            s2 = fadd2(s2, make_float2(y[k + 4], y[k + 5]));
+            s3 = fadd2(s3, make_float2(y[k + 6], y[k + 7]));
+          }
+          s0 = fadd2(fadd2(s0, s1), fadd2(s2, s3));
+          const float mc = nv > 0 ? (s0.x + s0.y) / (float)nv : 0.f;
+          const float2 nm = make_float2(-mc, -mc);
+          float2 q0 = make_float2(0.f, 0.f), q1 = q0;
+#pragma unroll
+          for (int k = 0; k < 32; k += 4) {
+            const float2 d0 = fadd2(make_float2(y[k], y[k + 1]), nm);
+            const float2 d1 = fadd2(make_float2(y[k + 2], y[k + 3]), nm);
+            q0 = ffma2(d0, d0, q0);
+            q1 = ffma2(d1, d1, q1);
+          }
+          q0 = fadd2(q0, q1);
+          float m2 = q0.x + q0.y;
+          if (nv < 32) m2 = nv > 0 ? fmaxf(0.f, m2 - (float)(32 - nv) * mc * mc) : 0.f;
+          cm[c] = mc;
+          c2[c] = m2;
+        } else {
+          float2 q0 = make_float2(0.f, 0.f), q1 = q0;
+#pragma unroll
+          for (int k = 0; k < 32; k += 4) {
+            const float2 a = make_float2(y[k], y[k + 1]), b = make_float2(y[k + 2], y[k + 3]);
+            q0 = ffma2(a, a, q0);
+            q1 = ffma2(b, b, q1);
+          }
+          q0 = fadd2(q0, q1);
+          ss += q0.x + q0.y;
+          cm[c] = c2[c] = 0.f;
+        }
+      }
+      // n-way merge of the chunks (fixed order): mean = sum n_c mean_c / n, M2 = sum M2_c + n_c d_c^2
+      float mean = 0.f, m2 = 0.f;
+      if constexpr (NORM == LOKA_NORM_LAYER) {
+        float sm = 0.f;
+#pragma unroll
+        for (int c = 0; c < kNch; ++c) {
+          const int nv = max(0, min(32, p.N - (col0 + 32 * c)));
+          sm = fmaf((float)nv, cm[c], sm);
+        }
+        mean = nh > 0 ? __fdiv_rn(sm, (float)nh) : 0.f;
+#pragma unroll
+        for (int c = 0; c < kNch; ++c) {
+          const int nv = max(0, min(32, p.N - (col0 + 32 * c)));
+          const float d = cm[c] - mean;
+          m2 += c2[c] + (float)nv * d * d;
+        }
+      }
+      if (fold) {  // back to y = c acc (the statistics of y)
+        mean = __fmul_rn(mean, cfold);
+        m2 = __fmul_rn(m2, __fmul_rn(cfold, cfold));
+        ss = __fmul_rn(ss, __fmul_rn(cfold, cfold));
+      }
+
+      // ---- the two halves of the row (fixed order h = 0, 1), then Case 2 exchange ----
+      hrec[h * 128 + r] = make_float4(NORM == LOKA_NORM_LAYER ? mean : ss, m2, ymax, ymin);
+      named_bar_sync(1, 32 * kPnEpiWarps);
+      // rstd, c0: z = y rstd + c0; with folding z = acc (c rstd) + c0 and ymax / ymin are of acc
+      float rstd = 1.f, c0 = 0.f, amax = 0.f;
+      {
+        const float4 v0 = hrec[r], v1 = hrec[128 + r];
+        const int n0 = max(0, min(kHN, p.N - nb * TN)), n1 = max(0, min(kHN, p.N - nb * TN - kHN));
+        const float sc = fold ? cfold : 1.f;  // acc -> y for the max / min of a BlockNorm block
+        float4 cr;  // this CTA's record of the row: (mean | ss, M2, ymax, ymin)
+        if constexpr (NORM == LOKA_NORM_LAYER) {
+          const float n = (float)(n0 + n1);
+          const float mu = n > 0.f ? __fdiv_rn(fmaf((float)n0, v0.x, (float)n1 * v1.x), n) : 0.f;
+          const float d0 = v0.x - mu, d1 = v1.x - mu;
+          cr = make_float4(mu, v0.y + (float)n0 * d0 * d0 + (v1.y + (float)n1 * d1 * d1), fmaxf(v0.z, v1.z),
+                           fminf(v0.w, v1.w));
+        } else if constexpr (NORM == LOKA_NORM_RMS) {
+          cr = make_float4(v0.x + v1.x, 0.f, fmaxf(v0.z, v1.z), fminf(v0.w, v1.w));
+        } else {  // BlockNorm-256: TN = 512 -> each half is one block; TN = 256 -> the two halves are
+          const float ssb = TN == 512 ? (h ? v1.x : v0.x) : v0.x + v1.x;
+          rstd = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(ssb, 256.f), p.eps)));
+          if (fp8_out) {  // the row amax candidate of this CTA's blocks (max |y| * rstd of each block)
+            if (TN == 512) {
+              const float r0 = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(v0.x, 256.f), p.eps)));
+              const float r1 = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(v1.x, 256.f), p.eps)));
+              amax = fmaxf(n0 > 0 ? fmaxf(fabsf(fmaf(v0.z, __fmul_rn(sc, r0), 0.f)), fabsf(fmaf(v0.w, __fmul_rn(sc, r0), 0.f))) : 0.f,
+                           n1 > 0 ? fmaxf(fabsf(fmaf(v1.z, __fmul_rn(sc, r1), 0.f)), fabsf(fmaf(v1.w, __fmul_rn(sc, r1), 0.f))) : 0.f);
+            } else {
+              const float rs = __fmul_rn(sc, rstd);
+              amax = (n0 + n1) > 0 ? fmaxf(fabsf(fmaf(fmaxf(v0.z, v1.z), rs, 0.f)), fabsf(fmaf(fminf(v0.w, v1.w), rs, 0.f)))
+                                   : 0.f;
+            }
+          }
+          cr = make_float4(0.f, 0.f, amax, 0.f);
+        }
+        if (need_x) {
+          const size_t slot = ((size_t)mb * G + nb) * 2 + rank;
+          if (h == 0) xrec[slot * 128 + r] = cr;
+          named_bar_sync(1, 32 * kPnEpiWarps);  // all 128 records written (and hrec reads done)
+          if (warp == 2) {
+            if (lane == 0) {
+              __threadfence();
+              st_release_u32(&xflag[slot], 1u);
+            }
+            if (lane < G) flag_wait(&xflag[((size_t)mb * G + lane) * 2 + rank], 0);
+            __threadfence();
+            __syncwarp();
+          }
+          named_bar_sync(1, 32 * kPnEpiWarps);
+          // merge the G tile records of the row in tile order (identical in every CTA of the row)
+          const float4* rr = xrec_r + ((size_t)mb * G * 2 + rank) * 128 + r;  // tile k at rr[k * 256]
+          float4 o = make_float4(0.f, 0.f, -INFINITY, INFINITY);
+          float n = 0.f, sm = 0.f;
+          for (int k = 0; k < G; ++k) {
+            const float4 v = ldcg_f4(rr + (size_t)k * 256);
+            const float nk = (float)max(0, min(TN, p.N - k * TN));
+            n += nk;
+            sm = fmaf(nk, v.x, sm);
+            o.y += v.y;
+            o.z = fmaxf(o.z, v.z);
+            o.w = fminf(o.w, v.w);
+          }
+          if constexpr (NORM == LOKA_NORM_LAYER) {
+            const float mu = n > 0.f ? __fdiv_rn(sm, n) : 0.f;
+            float mm = 0.f;
+            for (int k = 0; k < G; ++k) {
+              const float4 v = ldcg_f4(rr + (size_t)k * 256);
+              const float nk = (float)max(0, min(TN, p.N - k * TN));
+              const float dk = v.x - mu;
+              mm += v.y + nk * dk * dk;
+            }
+            cr = make_float4(mu, mm, o.z, o.w);
+          } else if constexpr (NORM == LOKA_NORM_RMS) {
+            float s2 = 0.f;
+            for (int k = 0; k < G; ++k) s2 += ldcg_f4(rr + (size_t)k * 256).x;
+            cr = make_float4(s2, 0.f, o.z, o.w);
+          } else {
+            cr = make_float4(0.f, 0.f, o.z, 0.f);
+          }
+        } else {
+          named_bar_sync(1, 32 * kPnEpiWarps);  // hrec reads done before the next tile's writes
+        }
+        const float nrow = (float)p.N;
+        if constexpr (NORM == LOKA_NORM_LAYER) {
+          rstd = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(cr.y, nrow), p.eps)));
+          c0 = -__fmul_rn(cr.x, rstd);
+        } else if constexpr (NORM == LOKA_NORM_RMS) {
+          rstd = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(cr.x, nrow), p.eps)));
+        }
+        if constexpr (NORM != LOKA_NORM_BLOCK_RMS) {
+          if (fp8_out) {  // the stored values are fma(y_or_acc, rs, c0): monotone, exact at ymax / ymin
+            const float rs = __fmul_rn(sc, rstd);
+            amax = fmaxf(fabsf(fmaf(cr.z, rs, c0)), fabsf(fmaf(cr.w, rs, c0)));
+          }
+        } else {
+          if (fp8_out) amax = cr.z;
+        }
+      }
+      float r_out = 1.f;
+      if (fp8_out) {
+        if (__float_as_uint(amax) >= 0x7F800000u && p.status) atomicOr(p.status, LOKA_DEVSTATUS_NONFINITE);
+        float s_out;
+        if (p.out_dtype == LOKA_E4M3) scales_from_amax<LOKA_E4M3, LOKA_SCALE_F32>(amax, s_out, r_out);
+        else scales_from_amax<LOKA_E5M2, LOKA_SCALE_F32>(amax, s_out, r_out);
+        if (row_ok && nb == 0 && h == 0 && p.y_scales) p.y_scales[grow] = s_out;
+      }
+
+      // ---- pass N: normalise, activation, cast, store ----
+      const float rs = fold ? __fmul_rn(cfold, rstd) : rstd;
+      const float2 r2 = make_float2(rs, rs), c02 = make_float2(c0, c0);
+      float amx = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < kNch; ++c) {
+        const int cb = 32 * c;
+        float y[32];
+        tmem_ld32(tbase + (uint32_t)cb, y);
+        if (c == kNch - 1) {  // the whole accumulator read: hand it back to the MMA
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(acc_empty0 + 8u * buf);
+        }
+        if (!fold) dequant(y, cb);
+#pragma unroll
+        for (int k = 0; k < 32; k += 4) {
+          float2 a = ffma2(make_float2(y[k], y[k + 1]), r2, c02);
+          float2 b = ffma2(make_float2(y[k + 2], y[k + 3]), r2, c02);
+          if (has_gb) {
+            const uint32_t o = cs + 2u * TN * 4u + 4u * (cb + k);
+            const float4 g4 = lds_f4(o), e4 = lds_f4(o + TN * 4u);
+            a = ffma2(a, make_float2(g4.x, g4.y), make_float2(e4.x, e4.y));
+            b = ffma2(b, make_float2(g4.z, g4.w), make_float2(e4.z, e4.w));
+          }
+          y[k] = a.x; y[k + 1] = a.y; y[k + 2] = b.x; y[k + 3] = b.y;
+        }
+        if (act) {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) y[k] = hswish(y[k]);
+        }
+        const int nv = max(0, min(32, p.N - (col0 + cb)));
+        if (p.amax_out && row_ok) {
+#pragma unroll
+          for (int k = 0; k < 32; ++k)
+            if (k < nv) amx = fmaxf(amx, fabsf(esz == 2 ? stored_bf16(y[k]) : y[k]));
+        }
+        if (p.precast && row_ok) {
+          float* dst = p.precast + (int64_t)grow * p.ld_pre + col0 + cb;
+#pragma unroll
+          for (int k = 0; k < 32; ++k)
+            if (k < nv) dst[k] = y[k];
+        }
+        const int in_box = cb % cpb;
+        uint8_t* box = stg + (nbox & 1) * 4096;
+        if (in_box == 0) {  // this buffer's previous store (two boxes ago) must have been read
+          if (lane == 0) bulk_wait_read_le1();
+          __syncwarp();
+        }
+        const uint32_t rowa = smem_u32(box) + (uint32_t)lane * 128u;
+        if (esz == 4) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            sts_u4(rowa + ((((uint32_t)k) ^ ((uint32_t)lane & 7u)) << 4),
+                   make_uint4(__float_as_uint(y[4 * k]), __float_as_uint(y[4 * k + 1]), __float_as_uint(y[4 * k + 2]),
+                              __float_as_uint(y[4 * k + 3])));
+        } else if (esz == 2) {
+          const uint32_t p0 = (uint32_t)(in_box * 2) >> 4;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            uint32_t w[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              __nv_bfloat162 hh = __floats2bfloat162_rn(y[8 * k + 2 * i], y[8 * k + 2 * i + 1]);
+              w[i] = *reinterpret_cast<uint32_t*>(&hh);
+            }
+            sts_u4(rowa + (((p0 + (uint32_t)k) ^ ((uint32_t)lane & 7u)) << 4), make_uint4(w[0], w[1], w[2], w[3]));
+          }
+        } else {
+          const uint32_t p0 = (uint32_t)in_box >> 4;
+          const float2 rr = make_float2(r_out, r_out);
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            uint32_t w[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int e = 16 * k + 4 * i;
+              const float2 a = fmul2(make_float2(y[e], y[e + 1]), rr);
+              const float2 b = fmul2(make_float2(y[e + 2], y[e + 3]), rr);
+              w[i] = p.out_dtype == LOKA_E4M3 ? cvt_fp8x4<LOKA_E4M3>(a.x, a.y, b.x, b.y)
+                                              : cvt_fp8x4<LOKA_E5M2>(a.x, a.y, b.x, b.y);
+            }
+            sts_u4(rowa + (((p0 + (uint32_t)k) ^ ((uint32_t)lane & 7u)) << 4), make_uint4(w[0], w[1], w[2], w[3]));
+          }
+        }
+        if (in_box + 32 == cpb) {  // box complete: store it
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const int cbox = col0 + cb + 32 - cpb;
+            const int row0 = mb * 256 + rank * 128 + q * 32;
+            if (cbox < p.N && row0 < p.M) tma_store_2d(&p.ty, box, cbox, row0);
+            bulk_commit();
+          }
+          ++nbox;
+        }
+      }
+      if (p.amax_out) warp_amax_to(p.amax_out, amx);
+    }
+    if (lane == 0) bulk_wait0();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_cg2<512>(tmem_base);
+  }
+}
+
+template <int TN, int NORM>
+static cudaError_t launch_pn(const PairNormParams& p, int pairs, cudaStream_t st) {
+  static int attr_done[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (!attr_done[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(pair_norm_kernel<TN, NORM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         PnCfg<TN>::kSmem);
+    if (e != cudaSuccess) return e;
+    attr_done[dev] = 1;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * pairs), 1, 1);
+  cfg.blockDim = dim3(kPnThreads, 1, 1);
+  cfg.dynamicSmemBytes = PnCfg<TN>::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, pair_norm_kernel<TN, NORM>, p);
+  note_launch();
+  return e;
+}
+
+template <int TN>
+static cudaError_t launch_pn_norm(const PairNormParams& p, int pairs, cudaStream_t st) {
+  switch (p.norm) {
+    case LOKA_NORM_LAYER: return launch_pn<TN, LOKA_NORM_LAYER>(p, pairs, st);
+    case LOKA_NORM_RMS: return launch_pn<TN, LOKA_NORM_RMS>(p, pairs, st);
+    case LOKA_NORM_BLOCK_RMS: return launch_pn<TN, LOKA_NORM_BLOCK_RMS>(p, pairs, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_pair_norm(const PairNormParams& p, int tn, int pairs, cudaStream_t st) {
+  return tn == 512 ? launch_pn_norm<512>(p, pairs, st) : launch_pn_norm<256>(p, pairs, st);
+}
+
+}  // namespace loka

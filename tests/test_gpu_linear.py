@@ -246,12 +246,15 @@ def test_wide_rows_unfused_pair_plus_rownorm(norm, od, act, affine):
                                      wq.cpu().numpy(), ws.cpu().numpy(), "e4m3", "row", **kw0)
     rms = np.sqrt(np.mean(base ** 2, axis=1, keepdims=True))
     guard = np.maximum(np.abs(base), rms)
-    assert np.max(np.abs(f64(pre)[rows] - yo) / guard) <= 1.5 * TOL
+    # the guard is taken on the pre-activation values; h-swish's slope (<= 1.5 on [-3, 3]) may scale
+    # an error by up to 1.5 against it, so only the activated cases get the 1.5x
+    tol = TOL if act == "none" else 1.5 * TOL
+    assert np.max(np.abs(f64(pre)[rows] - yo) / guard) <= tol
     if od == "e4m3":
         oq, os_ = oracle.quantize.quantize(f64(pre), "e4m3", "row")
         assert_scales_equal(ys, os_)
         assert_bytes_equal(y, oq)
     elif od == "bf16":
-        assert np.all(np.abs(f64(y)[rows] - yo) <= 1.5 * TOL * guard + 2.0 ** -8 * np.abs(yo))
+        assert np.all(np.abs(f64(y)[rows] - yo) <= tol * guard + 2.0 ** -8 * np.abs(yo))
     else:
-        assert np.max(np.abs(f64(y)[rows] - yo) / guard) <= 1.5 * TOL
+        assert np.max(np.abs(f64(y)[rows] - yo) / guard) <= tol

@@ -1,0 +1,172 @@
+"""-m gpu: the norm fused into the CTA-pair engine (pairnorm.cu; SURVEY.md §8(a) a4+a5 at the cfg4 /
+cfg5 sizes, "fuse normalization directly into the GEMM epilogue", Case 2 P:467) against
+oracle/linear.py on the dequantized operands the GPU consumed.  Both tile widths (LOKA_PAIRNORM=512:
+one accumulator, two N=256 MMAs per K step; =256: double-buffered accumulators), the cross-pair row
+record exchange (rows wider than one tile), ragged M / N / K, every output dtype.  Tolerances as
+test_gpu_linear.py (D17/D18): FP32 2e-3 guarded; BF16 + one bf16 half-ulp; FP8 codes and
+row scales bit-exact vs the oracle's quantize of the GPU's own pre-cast values."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from gpu_util import DEV, assert_bytes_equal, assert_scales_equal, f64, guarded_rel_err, to_dev_padded
+
+pytestmark = pytest.mark.gpu
+lk = pytest.importorskip("paper_2605_10886_b200") if torch.cuda.is_available() else None
+TOL = 2e-3
+
+
+@pytest.fixture(params=["512", "256"])
+def tn(request):
+    old = os.environ.get("LOKA_PAIRNORM")
+    os.environ["LOKA_PAIRNORM"] = request.param
+    yield int(request.param)
+    if old is None:
+        del os.environ["LOKA_PAIRNORM"]
+    else:
+        os.environ["LOKA_PAIRNORM"] = old
+
+
+def _operands(M, N, K, seed, a_gran="row", b_gran="row", xdist="heavy"):
+    x = synth.heavy(M, K, seed) if xdist == "heavy" else synth.gaussian(M, K, seed)
+    w = synth.weight(N, K, seed + 1)
+    xq, xs = lk.loka_quantize(to_dev_padded(x), "e4m3", a_gran)
+    wq, ws = lk.loka_quantize(to_dev_padded(w), "e4m3", b_gran)
+    return xq, xs, wq, ws
+
+
+def _oracle(xq, xs, wq, ws, a_gran="row", b_gran="row", rows=None, **kw):
+    a, s = xq.cpu().numpy(), xs.cpu().numpy()
+    if rows is not None:
+        a = a[rows]
+        s = s[rows] if a_gran == "row" else s
+    return oracle.linear.linear_norm(a, s, "e4m3", a_gran, wq.cpu().numpy(), ws.cpu().numpy(), "e4m3", b_gran, **kw)
+
+
+def _check(y, yo, od, base=None):
+    if od == "f32":
+        assert guarded_rel_err(f64(y), yo) <= TOL
+    else:
+        b = yo if base is None else base
+        guard = np.maximum(np.abs(b), np.sqrt(np.mean(b ** 2, axis=1, keepdims=True)))
+        assert np.all(np.abs(f64(y) - yo) <= TOL * guard + 2.0 ** -8 * np.abs(yo))
+
+
+@pytest.mark.parametrize("M,N,K", [(600, 4096, 1000), (300, 512, 256), (700, 2176, 384), (257, 256, 1152),
+                                   (1030, 1280, 520)])
+@pytest.mark.parametrize("norm", ["layer", "rms"])
+def test_full_row_norm_f32(tn, M, N, K, norm):
+    xq, xs, wq, ws = _operands(M, N, K, M + N)
+    y, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm=norm, out_dtype="f32")
+    torch.cuda.synchronize()
+    _check(y, _oracle(xq, xs, wq, ws, norm=norm), "f32")
+
+
+@pytest.mark.parametrize("M,N,K", [(600, 4096, 512), (300, 256, 256), (513, 768, 640)])
+def test_blocknorm_hardswish(tn, M, N, K):
+    """NEXT-1's fused form (PAPER.md:471-473 BlockNorm-256, P:502 Hard Swish) on the pair engine."""
+    xq, xs, wq, ws = _operands(M, N, K, 5)
+    for act in ("none", "hardswish"):
+        y, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm="block_rms", norm_block=256, act=act, out_dtype="f32")
+        torch.cuda.synchronize()
+        yo = _oracle(xq, xs, wq, ws, norm="block_rms", act=act)
+        base = _oracle(xq, xs, wq, ws, norm="block_rms")
+        guard = np.maximum(np.abs(base), np.sqrt(np.mean(base ** 2, axis=1, keepdims=True)))
+        assert np.max(np.abs(f64(y) - yo) / guard) <= TOL, act
+
+
+@pytest.mark.parametrize("a_gran,b_gran", [("tensor", "tensor"), ("row", "tensor"), ("tensor", "row")])
+def test_bias_gamma_beta_bf16_and_scale_grans(tn, a_gran, b_gran):
+    M, N, K = 520, 2304, 768
+    xq, xs, wq, ws = _operands(M, N, K, 9, a_gran, b_gran)
+    g = torch.Generator().manual_seed(2)
+    bias = torch.randn(N, generator=g).to(torch.bfloat16)
+    gamma = (1 + 0.2 * torch.randn(N, generator=g)).float()
+    beta = (0.1 * torch.randn(N, generator=g)).float()
+    for act in ("none", "hardswish"):
+        y, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, a_gran=a_gran, b_gran=b_gran, norm="layer", act=act,
+                                       bias=bias.to(DEV), gamma=gamma.to(DEV), beta=beta.to(DEV), out_dtype="bf16")
+        torch.cuda.synchronize()
+        kw = dict(norm="layer", bias=bias.double().numpy(), gamma=gamma.double().numpy(), beta=beta.double().numpy())
+        yo = _oracle(xq, xs, wq, ws, a_gran, b_gran, act=act, **kw)
+        _check(y, yo, "bf16", base=_oracle(xq, xs, wq, ws, a_gran, b_gran, **kw))
+
+
+@pytest.mark.parametrize("norm,N", [("layer", 4096), ("rms", 1024), ("block_rms", 4096), ("block_rms", 256),
+                                    ("layer", 384)])
+@pytest.mark.parametrize("od", ["e4m3", "e5m2"])
+def test_fp8_output_bit_exact(tn, norm, N, od):
+    """FP8 output with row scales (the next layer's rowwise input): the row amax spans every pair of
+    the row (exchanged with the statistics); codes + scales bit-exact vs the oracle's quantize of the
+    GPU's own pre-cast values, which are within 2e-3 of the oracle."""
+    M, K = 520, 512
+    xq, xs, wq, ws = _operands(M, N, K, 13)
+    pre = torch.full((M, N), float("nan"), dtype=torch.float32, device=DEV)
+    y, ys = lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm=norm, out_dtype=od, precast=pre)
+    torch.cuda.synchronize()
+    oq, os_ = oracle.quantize.quantize(f64(pre), od, "row")
+    assert_scales_equal(ys, os_)
+    assert_bytes_equal(y, oq)
+    assert guarded_rel_err(f64(pre), _oracle(xq, xs, wq, ws, norm=norm)) <= TOL
+
+
+def test_amax_out_producer_side(tn):
+    """NEXT-4 producer amax over the stored bf16 values equals max |y| of the output."""
+    M, N, K = 600, 4096, 256
+    xq, xs, wq, ws = _operands(M, N, K, 21)
+    amax = torch.zeros(1, dtype=torch.float32, device=DEV)
+    y, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm="layer", out_dtype="bf16", amax_out=amax)
+    torch.cuda.synchronize()
+    assert float(amax) == float(y.float().abs().max())
+
+
+def test_repeated_launches_and_graph_replay(tn):
+    """The exchange state (epoch-tagged flags) across many launches and CUDA-graph replays, where the
+    kernel parameters are frozen: every replay must equal the eager result bit for bit."""
+    M, N, K = 1100, 4096, 256
+    xq, xs, wq, ws = _operands(M, N, K, 31)
+    y0, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm="layer", out_dtype="f32")
+    for _ in range(5):
+        y1, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm="layer", out_dtype="f32")
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1)
+    yg = torch.empty_like(y0)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm="layer", out_dtype="f32", y=yg, stream=s)  # warm
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm="layer", out_dtype="f32", y=yg, stream=s)
+    for _ in range(7):
+        yg.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(yg, y0)
+    _check(y0, _oracle(xq, xs, wq, ws, norm="layer"), "f32")
+
+
+@pytest.mark.parametrize("M", [32768, 262144])
+def test_cfg5_shape_sampled(M):
+    """The bench's launch configuration (BJ configs[4] at P=1 and P=8's per-GPU M): heavy-tailed X,
+    tensorwise e4m3, K = N = 4096, LayerNorm, default route; 48 sampled rows vs the oracle (bf16 out)
+    and the FP32 route on the same rows at 2e-3."""
+    K = N = 4096
+    x = synth.heavy(M, K, 3, device=DEV)
+    w = synth.weight(N, K, 1, device=DEV)
+    xq, xs = lk.loka_quantize(x, "e4m3", "tensor")
+    wq, ws = lk.loka_quantize(w, "e4m3", "tensor")
+    del x
+    rows = np.sort(np.random.default_rng(M).choice(M, 48, replace=False))
+    yb, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, a_gran="tensor", b_gran="tensor", norm="layer", out_dtype="bf16")
+    torch.cuda.synchronize()
+    yo = _oracle(xq, xs, wq, ws, "tensor", "tensor", rows=rows, norm="layer")
+    _check(yb[torch.from_numpy(rows).to(DEV)], yo, "bf16")
+    del yb
+    yf, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, a_gran="tensor", b_gran="tensor", norm="layer", out_dtype="f32")
+    torch.cuda.synchronize()
+    _check(yf[torch.from_numpy(rows).to(DEV)], yo, "f32")
