@@ -444,6 +444,12 @@ LOKA_API int64_t loka_debug_hang_info(uint64_t* info3, int32_t reset);
  * enable = 0 turns it off, enable = -1 leaves it unchanged.  Copies up to n stamps into out
  * (host, may be NULL).  Returns the number copied, -1 on a CUDA error.  Synchronous.          */
 LOKA_API int64_t loka_debug_trace(int32_t enable, uint64_t* out, int64_t n);
+/* Pair-norm phase trace (debug/profiling): dev_buf (device, >= 148 * 64 * 8 u64, caller-owned) makes
+ * later pair-norm launches record globaltimer stamps per CTA and tile (< 64) at
+ * dev_buf[(blockIdx.x * 64 + tile) * 8 + slot]: 0 accumulator ready, 1 statistics pass done,
+ * 2 row records merged, 3 stores issued (epilogue thread 0); 4 / 5 / 6 MMA thread (leader CTAs):
+ * waiting for the accumulator buffer, buffer acquired, last MMA committed.  NULL turns it off.    */
+LOKA_API void loka_debug_pairnorm_trace(unsigned long long* dev_buf);
 
 #ifdef __cplusplus
 }

@@ -128,6 +128,7 @@ _sig = {
     "loka_launch_count": ([], C.c_int64),
     "loka_debug_hang_info": ([_P(C.c_uint64), C.c_int32], C.c_int64),
     "loka_debug_trace": ([C.c_int32, _P(C.c_uint64), C.c_int64], C.c_int64),
+    "loka_debug_pairnorm_trace": ([C.c_void_p], None),
     "loka_stack_workspace_size": ([_P(loka_stack_args)], C.c_size_t),
     "loka_probe_track_workspace_size": ([_P(loka_welford_state), C.c_int64], C.c_size_t),
     "loka_probe_track_input": ([_P(loka_welford_state), _P(loka_tensor), C.c_void_p, C.c_size_t, C.c_void_p], C.c_int),

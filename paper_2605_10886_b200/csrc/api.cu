@@ -536,12 +536,9 @@ struct PairPlan {
   bool wide;
   int ks, kbps;
 };
-static int pair_wide_env() {
-  static const int v = [] {
-    const char* e = std::getenv("LOKA_PAIR_WIDE");
-    return e ? (e[0] == '1' ? 1 : 0) : -1;
-  }();
-  return v;
+static int pair_wide_env() {  // read per call (A/B measurements switch it inside one process)
+  const char* e = std::getenv("LOKA_PAIR_WIDE");
+  return e ? (e[0] == '1' ? 1 : 0) : -1;
 }
 static PairPlan pair_plan(const loka_linear_args* a) {
   PairPlan pl{false, 1, 0};
@@ -719,6 +716,10 @@ static loka_status run_wide_norm(const loka_linear_args* a, void* ws, size_t ws_
 // ---- a4 + a5 at scale: the norm fused into the CTA-pair engine (pairnorm.cu) ------------------
 // Rows wider than one pair tile exchange row records through the caller's workspace
 // (pair_xchg_bytes: flags zeroed by a memset in the same stream before the launch, then records).
+static uint64_t* g_pn_trace = nullptr;  // measurement aid: see loka_debug_pairnorm_trace
+void loka_debug_pairnorm_trace(unsigned long long* dev_buf) {
+  g_pn_trace = reinterpret_cast<uint64_t*>(dev_buf);
+}
 static int pair_norm_env() {  // LOKA_PAIRNORM: 0 = off; 256 / 512 = force the tile width (read per call)
   const char* e = std::getenv("LOKA_PAIRNORM");
   return e ? std::atoi(e) : -1;
@@ -738,7 +739,10 @@ static PnPlan pair_norm_plan(const loka_linear_args* a, int sms) {
   if (a->M <= 0 || a->N <= 0 || a->K <= 0 || a->N > 16384) return pl;
   const bool fp8_out = is_fp8(a->y.dtype);
   if (fp8_out && (a->gamma || a->beta || a->act != LOKA_ACT_NONE)) return pl;  // row amax not monotone
-  pl.tn = (env == 256 || env == 512) ? env : (a->N <= 256 ? 256 : 512);
+  // 256-wide tiles with double-buffered accumulators by default: the epilogue (two TMEM passes and
+  // the row-record exchange) runs under the next tile's MMAs; WIDE 512-column tiles (LOKA_PAIRNORM=512)
+  // move 25% fewer operand bytes per FLOP but expose the whole epilogue (measured slower)
+  pl.tn = (env == 256 || env == 512) ? env : 256;
   pl.tiles_n = (int)cdiv(a->N, pl.tn);
   pl.row_blocks = (int)cdiv(a->M, 256);
   pl.xchg = pl.tiles_n > 1 && (!blk || fp8_out);
@@ -751,6 +755,10 @@ static PnPlan pair_norm_plan(const loka_linear_args* a, int sms) {
   // core, so its pairs walk row blocks in static groups of tiles_n; double-buffered tiles (TN = 256)
   // go round-robin over all pairs (a row block's tiles then span at most two waves)
   pl.order = (pl.xchg && pl.tn == 512) ? 1 : 0;
+  if (const char* e = std::getenv("LOKA_PN_ORDER")) {  // measurement knob: 0 / 1
+    const int o = std::atoi(e);
+    if (pl.xchg && (o == 0 || o == 1)) pl.order = o;
+  }
   if (pl.xchg && (pl.tiles_n > avail || pl.tiles_n > 32)) return pl;
   if (pl.order) {
     pl.groups = std::min(avail / pl.tiles_n, pl.row_blocks);
@@ -799,11 +807,12 @@ static loka_status run_pair_norm(const loka_linear_args* a, const PnPlan& pl, vo
   p.xchg = pl.xchg ? 1 : 0;
   p.order = pl.order;
   p.ngroups = pl.groups;
+  if (const char* e = std::getenv("LOKA_PN_DEBUG")) p.dbg = std::atoi(e);
+  p.trace = g_pn_trace;
   if (pl.xchg) {
-    const size_t flag_bytes = ((size_t)pl.row_blocks * pl.tiles_n * 2 * 4 + 255) & ~size_t(255);
+    // the records start as 0xFF bytes (the sentinel NaN the readers wait on), every launch
     p.xws = static_cast<uint8_t*>(ws);
-    p.xrec_off = (int64_t)flag_bytes;
-    if (cudaMemsetAsync(ws, 0, flag_bytes, s) != cudaSuccess) return LOKA_ERR_CUDA;
+    if (cudaMemsetAsync(ws, 0xFF, need, s) != cudaSuccess) return LOKA_ERR_CUDA;
   }
   return launch_pair_norm(p, pl.tn, pl.pairs, s) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
 }

@@ -230,15 +230,8 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
       const int col0 = nb * kTN + h * kHN;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * 256 + h * kHN);
       float amx = 0.f;  // NEXT-4 producer amax of this warp's stored values
-#pragma unroll 1
-      for (int cb = 0; cb < kHN; cb += 32) {
-        float y[32];
-        tmem_ld32(tbase + (uint32_t)cb, y);
-        if (cb == kHN - 32) {  // accumulator fully in registers: hand the buffer back to the MMA
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(acc_empty0 + 8u * buf);
-        }
+      // 32-column chunks streamed out of TMEM with the next chunk's load in flight (two buffers)
+      auto chunk = [&](float (&y)[32], int cb) {
         const uint32_t cs = smem_u32(colp + h * kHN + cb);
         const float2 sa2 = make_float2(sa, sa);
         if (!split) {
@@ -295,6 +288,26 @@ __global__ void __launch_bounds__(k2Threads, 1) grouped2_kernel(const __grid_con
             bulk_commit();
           }
           ++nbox;
+        }
+      };
+      {
+        float ya[32], yb[32];
+        tmem_ld32_nowait(tbase, ya);
+        tmem_wait32(ya);
+#pragma unroll 1
+        for (int cb = 0; cb < kHN; cb += 64) {
+          tmem_ld32_nowait(tbase + (uint32_t)(cb + 32), yb);
+          chunk(ya, cb);
+          tmem_wait32(yb);
+          if (cb + 64 < kHN) {
+            tmem_ld32_nowait(tbase + (uint32_t)(cb + 64), ya);
+          } else {  // accumulator fully in registers: hand the buffer back to the MMA
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(acc_empty0 + 8u * buf);
+          }
+          chunk(yb, cb + 32);
+          if (cb + 64 < kHN) tmem_wait32(ya);
         }
       }
       if (d.amax_out && !split) warp_amax_to(d.amax_out, amx);

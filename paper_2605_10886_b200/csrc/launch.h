@@ -305,8 +305,8 @@ cudaError_t launch_matnorm_update(const MatnormParams& p, cudaStream_t st);
 
 // ---- a4 + a5 at scale: CTA-pair GEMM with the norm fused in the epilogue (pairnorm.cu) ----
 constexpr int kPnMaxPairs = 128;  // CTA pairs per launch (148 SMs -> 74)
-// workspace of the Case 2 row-record exchange: u32 flags [row_blocks][tiles_n][2] (zeroed before each
-// launch), then float4 records [row_blocks][tiles_n][2][128] at the 256-byte aligned offset
+// workspace of the Case 2 row-record exchange: float4 records [row_blocks][tiles_n][2][128], filled
+// with 0xFF bytes (a sentinel NaN) by the host before each launch
 size_t pair_xchg_bytes(int64_t row_blocks, int tiles_n);
 struct PairNormParams {
   CUtensorMap ta, tb, ty;  // A [M,K] / B [N,K] codes box {128, 128}; Y box {128 bytes, 32 rows} SW128
@@ -327,10 +327,12 @@ struct PairNormParams {
   int32_t tiles_n;     // ceil(N / TN)
   int32_t row_blocks;  // ceil(M / 256)
   int32_t xchg;        // 1: the tiles_n pairs of a row block exchange row records (Case 2)
-  int32_t order;       // 0: round-robin over the tile list; 1: static groups of tiles_n pairs
+  int32_t order;       // 0: round-robin over the tile list; 1: static groups of tiles_n pairs (TN 512)
   int32_t ngroups;     // order 1: the launch is ngroups x tiles_n pairs
-  uint8_t* xws;        // xchg: flags at 0, records at xrec_off (pair_xchg_bytes)
-  int64_t xrec_off;
+  uint8_t* xws;        // xchg: the records (pair_xchg_bytes)
+  int32_t dbg;         // measurement knobs (LOKA_PN_DEBUG; results are wrong when set): 1 = no
+                       // waits for peers' records, 2 = no statistics pass
+  uint64_t* trace;     // nullable: globaltimer stamps [CTA][tile < 64][8] (loka_debug_pairnorm_trace)
 };
 // tn = 512 (one accumulator, two N = 256 MMAs per K step) or 256 (double-buffered accumulators)
 cudaError_t launch_pair_norm(const PairNormParams& p, int tn, int pairs, cudaStream_t st);

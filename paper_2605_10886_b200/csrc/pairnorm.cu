@@ -4,26 +4,28 @@
 //
 // Tile: a 2-CTA cluster (tcgen05.mma.cta_group::2, M = 256) computes 256 rows x TN columns; each
 // CTA holds its 128 rows x TN columns of FP32 accumulator in TMEM.
-//   * TN = 512 ("WIDE"): two N = 256 MMAs per K step share the A stage (the L2 -> SM port saving of
-//     gemm2's WIDE tiles); one accumulator, so a tile's epilogue does not overlap the next tile's MMAs.
 //   * TN = 256: two accumulator buffers; tile j+1's MMAs run while the epilogue drains tile j.
+//   * TN = 512 ("WIDE"): two N = 256 MMAs per K step share the A stage (gemm2's L2 -> SM port
+//     saving); one accumulator, so a tile's epilogue does not overlap the next tile's MMAs.
 // Epilogue (8 warps per CTA; warp = TMEM lane quadrant q x column half h; thread = one row x TN/2
-// columns in 32-column chunks):
-//   pass S  tcgen05.ld -> y = acc * s_a[m] * s_b[n] (+ bias[n]) -> per-chunk (mean, M2) (LayerNorm;
-//           Chan's parallel merge of PAPER.md:293-299 applied to column partitions) or sum of
-//           squares (RMS / BlockNorm), y max / min (FP8 row amax); the two halves merged through smem;
-//   xchg    rows wider than one tile (Case 2): the G = ceil(N / TN) pairs that own the column tiles
-//           of one 256-row block run in lock step (a static group of G pairs walks row blocks
-//           gi, gi + #groups, ...); each CTA publishes its 128 row records to global memory (L2) with
-//           a release flag, waits for its G - 1 peers' flags (acquire) and merges the G records in
-//           tile order — bit-identical statistics in every CTA of the row, no cluster needed;
-//   pass N  tcgen05.ld again -> the same y -> (y - mu) * rstd [* gamma + beta] [h-swish] -> bf16 /
-//           f32 / FP8 (row scale from the merged y max / min: the map is monotone) -> swizzled smem
-//           box -> TMA store.
-// Row records are exchanged through global memory rather than DSMEM because a 4096-wide row needs
-// 8 WIDE pairs (16 CTAs), which as one cluster would leave ~14% of the SMs idle (one 16-CTA
-// cluster per GPC); the flags make the exchange an L2 round trip (~1-2 us), overlapped with
-// nothing only for TN = 512.  Co-residency: the grid is one CTA per SM and at most 2 x 74 CTAs.
+// columns, streamed out of TMEM in 32-column chunks with the next chunk's load in flight):
+//   pass S  y = acc * s_a[m] * s_b[n] (+ bias[n]) -> per-chunk (mean, M2) merged in order with
+//           Chan's update (LayerNorm; the parallel merge of PAPER.md:293-299 applied to column
+//           partitions) or the sum of squares (RMS / BlockNorm), y max / min (FP8 row amax); the two
+//           column halves merged through smem.  With a tensor-wide s_b and no bias the statistics are
+//           taken on acc and scaled (mean * c, M2 * c^2; c = s_a s_b), and pass N is one FMA;
+//   xchg    rows wider than one tile (Case 2): the G = ceil(N / TN) tiles of a row are
+//           computed by G different pairs.  Each CTA stores its 128 row records (float4) to the
+//           workspace, which the host fills with a sentinel NaN pattern before the launch; the
+//           readers load the G records of their row directly and re-load any element still holding
+//           the sentinel (a 32-bit store is single-copy atomic, and no statistic of finite data is
+//           that NaN), so the exchange is one L2 round trip after the last peer's store — no flags,
+//           no fences; the G records are merged in tile order (bit-identical in every CTA of a row);
+//   pass N  the same y -> (y - mu) * rstd [* gamma + beta] [h-swish] -> bf16 / f32 / FP8 (row scale
+//           from the merged y max / min: the map is monotone) -> swizzled smem box -> TMA store.
+// Exchange through global memory (L2), not DSMEM: a 4096-wide row spans 16 (TN = 256) or 8 WIDE
+// pairs, and clusters of 16+ CTAs would leave ~14% of the SMs idle.  Co-residency: one CTA per SM,
+// at most 2 x 74 CTAs, every CTA resident (a reader only waits for tiles other resident pairs own).
 #include "common.cuh"
 #include "launch.h"
 
@@ -31,6 +33,7 @@ namespace loka {
 
 constexpr int kPnEpiWarps = 8;
 constexpr int kPnThreads = 64 + 32 * kPnEpiWarps;
+constexpr uint32_t kPnSentinel = 0xFFFFFFFFu;  // a NaN no statistic of finite data can take
 
 template <int TN>
 struct PnCfg {
@@ -48,47 +51,47 @@ struct PnCfg {
   static_assert(kSmem <= 227 * 1024, "pairnorm smem");
 };
 
-// Case 2 exchange buffers (caller's workspace): one float4 record per (row block, column tile, CTA
-// rank, row) and one u32 flag per (row block, column tile, CTA rank), zeroed by the host (a memset
-// node in the same stream) before every launch: a record slot is written once per launch, so a flag
-// is a plain 0 -> 1 publish with release / acquire semantics and no state survives a launch.
-size_t pair_xchg_bytes(int64_t row_blocks, int tiles_n) {
-  const size_t slots = (size_t)row_blocks * (size_t)tiles_n * 2;
-  return ((slots * 4 + 255) & ~size_t(255)) + slots * 128 * 16;
-}
+// Case 2 records (caller's workspace): float4 [row blocks][tiles_n][2 CTA ranks][128 rows], set to
+// the sentinel by the host (a memset node in the same stream) before every launch.
+size_t pair_xchg_bytes(int64_t row_blocks, int tiles_n) { return (size_t)row_blocks * tiles_n * 2 * 128 * 16; }
 
-LOKA_DEVINL uint32_t ld_acquire_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+LOKA_DEVINL float4 ld_relaxed_f4(const float4* p) {
+  float4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p)
+               : "memory");
   return v;
 }
-LOKA_DEVINL void st_release_u32(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+LOKA_DEVINL bool rec_pending(const float4& v) {
+  return __float_as_uint(v.x) == kPnSentinel || __float_as_uint(v.y) == kPnSentinel ||
+         __float_as_uint(v.z) == kPnSentinel || __float_as_uint(v.w) == kPnSentinel;
 }
-LOKA_DEVINL float4 ldcg_f4(const float4* p) { return __ldcg(p); }
-
-// spin on a peer's flag with the watchdog of mbar_wait (common.cuh): a wait longer than 4 s
-// records where it stalled and gives up instead of hanging the GPU
-LOKA_DEVINL void flag_wait(const uint32_t* f, int where) {
-  if (ld_acquire_u32(f) != 0u) return;
-  uint64_t t0 = 0;
+// re-load a peer's record until no element holds the sentinel; the watchdog of mbar_wait
+// (common.cuh): a wait longer than 4 s records where it stalled and gives up instead of hanging
+LOKA_DEVINL float4 rec_wait(const float4* p) {
+  float4 v = ld_relaxed_f4(p);
   uint32_t spins = 0;
-  while (ld_acquire_u32(f) == 0u) {
-    __nanosleep(20);
-    if ((++spins & 255u) != 0) continue;
-    const uint64_t t = globaltimer_ns();
-    if (t0 == 0) t0 = t;
-    if (*reinterpret_cast<volatile int*>(&g_loka_abort)) return;
-    if (t - t0 > kHangNs) {
-      if (atomicAdd(&g_loka_hang[0], 1ull) == 0) {
-        g_loka_hang[1] = (unsigned long long)(100 + where);
-        g_loka_hang[2] = (unsigned long long)blockIdx.x;
-        g_loka_hang[3] = (unsigned long long)threadIdx.x;
+  uint64_t t0 = 0;
+  while (rec_pending(v)) {
+    if ((++spins & 15u) == 0) {
+      __nanosleep(64);
+      const uint64_t t = globaltimer_ns();
+      if (t0 == 0) t0 = t;
+      if (*reinterpret_cast<volatile int*>(&g_loka_abort)) break;
+      if (t - t0 > kHangNs) {
+        if (atomicAdd(&g_loka_hang[0], 1ull) == 0) {
+          g_loka_hang[1] = 100ull;
+          g_loka_hang[2] = (unsigned long long)blockIdx.x;
+          g_loka_hang[3] = (unsigned long long)threadIdx.x;
+        }
+        atomicExch(&g_loka_abort, 1);
+        break;
       }
-      atomicExch(&g_loka_abort, 1);
-      return;
     }
+    v = ld_relaxed_f4(p);
   }
+  return v;
 }
 
 LOKA_DEVINL float hswish(float x) {  // x * ReLU6(x + 3) / 6
@@ -116,15 +119,15 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
   const int rank = (int)cluster_ctarank();
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int G = p.tiles_n;
-  // schedule: round-robin over the tile list (row-block major; p.order = 0), or static groups of G
-  // pairs that walk row blocks gi, gi + #groups, ... in lock step (p.order = 1: a single-accumulator
-  // tile cannot wait for a peer's next wave without idling its tensor core)
+  // schedule: order 0 = round-robin over the tile list (row-block major: the G tiles of a row are
+  // computed by G consecutive pairs, mostly in the same wave); order 1 = static groups of G pairs
+  // that walk row blocks gi, gi + #groups, ... in lock step (for the single-accumulator WIDE tile,
+  // which cannot wait for a peer's next wave without idling its tensor core)
   const bool xchg = p.xchg != 0;
-  const bool grouped = p.order != 0;
-  const int gi = grouped ? cid / G : 0, gj = grouped ? cid - (cid / G) * G : 0;
+  const int gi = p.order == 1 ? cid / G : 0, gj = p.order == 1 ? cid - (cid / G) * G : 0;
   const int T = p.row_blocks * G;
   auto tile_of = [&](int k, int& mb, int& nb) -> bool {  // k-th tile of this pair
-    if (grouped) {
+    if (p.order == 1) {
       mb = gi + k * p.ngroups;
       nb = gj;
       return mb < p.row_blocks;
@@ -186,7 +189,10 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
       for (int j = 0; tile_of(j, mb, nb); ++j) {
         const int buf = Cf::kAcc == 1 ? 0 : (j & 1);
         const uint32_t use = Cf::kAcc == 1 ? (uint32_t)j : (uint32_t)(j >> 1);
+        uint64_t* tr = (p.trace && j < 64) ? p.trace + ((size_t)blockIdx.x * 64 + j) * 8 : nullptr;
+        if (tr) tr[4] = globaltimer_ns();
         mbar_wait(&acc_empty[buf], (use & 1u) ^ 1u, 4);
+        if (tr) tr[5] = globaltimer_ns();
         tc_fence_after();
         const uint32_t dacc = tmem_base + (uint32_t)(buf * 256);
         for (int kb = 0; kb < nkb; ++kb, ++it) {
@@ -205,6 +211,7 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
           mma_commit_cg2_mc(&empty_bar[s], 3);
         }
         mma_commit_cg2_mc(&acc_full[buf], 3);
+        if (tr) tr[6] = globaltimer_ns();
       }
     }
     __syncwarp();
@@ -225,9 +232,7 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
     // are taken on acc and scaled (mean * c, M2 * c^2), and pass N is one FMA per element
     const bool fold = !p.sb_row && p.bias == nullptr;
     const bool need_x = xchg && (NORM != LOKA_NORM_BLOCK_RMS || fp8_out);
-    uint32_t* xflag = reinterpret_cast<uint32_t*>(p.xws);
-    const float4* xrec_r = reinterpret_cast<const float4*>(p.xws + p.xrec_off);
-    float4* xrec = reinterpret_cast<float4*>(p.xws + p.xrec_off);
+    float4* xrec = reinterpret_cast<float4*>(p.xws);
     int nbox = 0;
     int mb, nb;
     for (int j = 0; tile_of(j, mb, nb); ++j) {
@@ -253,6 +258,8 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
       if (lane == 0) mbar_wait(&acc_full[buf], use & 1u, 3);
       __syncwarp();
       tc_fence_after();
+      uint64_t* tr = (p.trace && j < 64 && et == 0) ? p.trace + ((size_t)blockIdx.x * 64 + j) * 8 : nullptr;
+      if (tr) tr[0] = globaltimer_ns();
 
       const int grow = mb * 256 + rank * 128 + r;
       const bool row_ok = grow < p.M;
@@ -274,21 +281,38 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
           y[c] = a.x; y[c + 1] = a.y; y[c + 2] = b.x; y[c + 3] = b.y;
         }
       };
+      // both passes stream the thread's kHN columns out of TMEM in 32-column chunks, the next chunk's
+      // tcgen05.ld in flight while the current one is processed (two register buffers)
+      auto stream_tmem = [&](auto&& fn, bool release) {
+        float ya[32], yb[32];
+        tmem_ld32_nowait(tbase, ya);
+        tmem_wait32(ya);
+#pragma unroll 1
+        for (int c = 0; c < kNch; c += 2) {
+          tmem_ld32_nowait(tbase + (uint32_t)(32 * (c + 1)), yb);
+          fn(ya, c);
+          tmem_wait32(yb);
+          if (c + 2 < kNch) {
+            tmem_ld32_nowait(tbase + (uint32_t)(32 * (c + 2)), ya);
+          } else if (release) {  // the whole accumulator is in registers: hand it back to the MMA
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(acc_empty0 + 8u * buf);
+          }
+          fn(yb, c + 1);
+          if (c + 2 < kNch) tmem_wait32(ya);
+        }
+      };
 
       // ---- pass S: this thread's statistics over its kHN columns (of acc when folding, else y) ----
       // Columns >= N hold exact zeros (zero-filled B rows, s_b = bias = 0): sums need no mask,
       // the LayerNorm chunk M2 is corrected for them and max / min skip them.
-      float cm[kNch], c2[kNch];
       float ss = 0.f, ymax = -INFINITY, ymin = INFINITY;
-      int nh = 0;  // valid columns of this thread
-#pragma unroll 1
-      for (int c = 0; c < kNch; ++c) {
+      float mean = 0.f, m2 = 0.f, nacc = 0.f;
+      auto stats_chunk = [&](float (&y)[32], int c) {
         const int cb = 32 * c;
         const int nv = max(0, min(32, p.N - (col0 + cb)));
-        float y[32];
-        tmem_ld32(tbase + (uint32_t)cb, y);
         if (!fold) dequant(y, cb);
-        nh += nv;
         if (nv > 0 && fp8_out) {
           if (nv == 32) {
 #pragma unroll
@@ -320,10 +344,16 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
             q1 = ffma2(d1, d1, q1);
           }
           q0 = fadd2(q0, q1);
-          float m2 = q0.x + q0.y;
-          if (nv < 32) m2 = nv > 0 ? fmaxf(0.f, m2 - (float)(32 - nv) * mc * mc) : 0.f;
-          cm[c] = mc;
-          c2[c] = m2;
+          float mc2 = q0.x + q0.y;
+          if (nv < 32) mc2 = nv > 0 ? fmaxf(0.f, mc2 - (float)(32 - nv) * mc * mc) : 0.f;
+          if (nv > 0) {  // Chan's pairwise update: (nacc, mean, m2) += (nv, mc, mc2)
+            const float nn = nacc + (float)nv;
+            const float d = mc - mean;
+            const float f = __fdiv_rn((float)nv, nn);
+            mean = fmaf(d, f, mean);
+            m2 += mc2 + d * d * nacc * f;
+            nacc = nn;
+          }
         } else {
           float2 q0 = make_float2(0.f, 0.f), q1 = q0;
 #pragma unroll
@@ -334,41 +364,25 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
           }
           q0 = fadd2(q0, q1);
           ss += q0.x + q0.y;
-          cm[c] = c2[c] = 0.f;
         }
-      }
-      // n-way merge of the chunks (fixed order): mean = sum n_c mean_c / n, M2 = sum M2_c + n_c d_c^2
-      float mean = 0.f, m2 = 0.f;
-      if constexpr (NORM == LOKA_NORM_LAYER) {
-        float sm = 0.f;
-#pragma unroll
-        for (int c = 0; c < kNch; ++c) {
-          const int nv = max(0, min(32, p.N - (col0 + 32 * c)));
-          sm = fmaf((float)nv, cm[c], sm);
-        }
-        mean = nh > 0 ? __fdiv_rn(sm, (float)nh) : 0.f;
-#pragma unroll
-        for (int c = 0; c < kNch; ++c) {
-          const int nv = max(0, min(32, p.N - (col0 + 32 * c)));
-          const float d = cm[c] - mean;
-          m2 += c2[c] + (float)nv * d * d;
-        }
-      }
+      };
+      if (!(p.dbg & 2)) stream_tmem(stats_chunk, false);
+      if (tr) tr[1] = globaltimer_ns();
       if (fold) {  // back to y = c acc (the statistics of y)
         mean = __fmul_rn(mean, cfold);
         m2 = __fmul_rn(m2, __fmul_rn(cfold, cfold));
         ss = __fmul_rn(ss, __fmul_rn(cfold, cfold));
       }
 
-      // ---- the two halves of the row (fixed order h = 0, 1), then Case 2 exchange ----
+      // ---- the two halves of the row (fixed order h = 0, 1), then the Case 2 exchange ----
       hrec[h * 128 + r] = make_float4(NORM == LOKA_NORM_LAYER ? mean : ss, m2, ymax, ymin);
       named_bar_sync(1, 32 * kPnEpiWarps);
-      // rstd, c0: z = y rstd + c0; with folding z = acc (c rstd) + c0 and ymax / ymin are of acc
+      // z = y rstd + c0; with folding z = acc (c rstd) + c0 and ymax / ymin are of acc
       float rstd = 1.f, c0 = 0.f, amax = 0.f;
+      const float sc = fold ? cfold : 1.f;
       {
         const float4 v0 = hrec[r], v1 = hrec[128 + r];
         const int n0 = max(0, min(kHN, p.N - nb * TN)), n1 = max(0, min(kHN, p.N - nb * TN - kHN));
-        const float sc = fold ? cfold : 1.f;  // acc -> y for the max / min of a BlockNorm block
         float4 cr;  // this CTA's record of the row: (mean | ss, M2, ymax, ymin)
         if constexpr (NORM == LOKA_NORM_LAYER) {
           const float n = (float)(n0 + n1);
@@ -381,12 +395,12 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
         } else {  // BlockNorm-256: TN = 512 -> each half is one block; TN = 256 -> the two halves are
           const float ssb = TN == 512 ? (h ? v1.x : v0.x) : v0.x + v1.x;
           rstd = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(ssb, 256.f), p.eps)));
-          if (fp8_out) {  // the row amax candidate of this CTA's blocks (max |y| * rstd of each block)
+          if (fp8_out) {  // the row amax candidate of this CTA's blocks (max |stored value| per block)
             if (TN == 512) {
-              const float r0 = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(v0.x, 256.f), p.eps)));
-              const float r1 = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(v1.x, 256.f), p.eps)));
-              amax = fmaxf(n0 > 0 ? fmaxf(fabsf(fmaf(v0.z, __fmul_rn(sc, r0), 0.f)), fabsf(fmaf(v0.w, __fmul_rn(sc, r0), 0.f))) : 0.f,
-                           n1 > 0 ? fmaxf(fabsf(fmaf(v1.z, __fmul_rn(sc, r1), 0.f)), fabsf(fmaf(v1.w, __fmul_rn(sc, r1), 0.f))) : 0.f);
+              const float r0 = __fmul_rn(sc, __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(v0.x, 256.f), p.eps))));
+              const float r1 = __fmul_rn(sc, __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(v1.x, 256.f), p.eps))));
+              amax = fmaxf(n0 > 0 ? fmaxf(fabsf(fmaf(v0.z, r0, 0.f)), fabsf(fmaf(v0.w, r0, 0.f))) : 0.f,
+                           n1 > 0 ? fmaxf(fabsf(fmaf(v1.z, r1, 0.f)), fabsf(fmaf(v1.w, r1, 0.f))) : 0.f);
             } else {
               const float rs = __fmul_rn(sc, rstd);
               amax = (n0 + n1) > 0 ? fmaxf(fabsf(fmaf(fmaxf(v0.z, v1.z), rs, 0.f)), fabsf(fmaf(fminf(v0.w, v1.w), rs, 0.f)))
@@ -396,52 +410,66 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
           cr = make_float4(0.f, 0.f, amax, 0.f);
         }
         if (need_x) {
-          const size_t slot = ((size_t)mb * G + nb) * 2 + rank;
-          if (h == 0) xrec[slot * 128 + r] = cr;
-          named_bar_sync(1, 32 * kPnEpiWarps);  // all 128 records written (and hrec reads done)
-          if (warp == 2) {
-            if (lane == 0) {
-              __threadfence();
-              st_release_u32(&xflag[slot], 1u);
-            }
-            if (lane < G) flag_wait(&xflag[((size_t)mb * G + lane) * 2 + rank], 0);
-            __threadfence();
-            __syncwarp();
+          // publish this CTA's record of row r: one float4 store, waited for element-wise by readers
+          const size_t rb = (size_t)mb * G * 2 + rank;  // record of tile k, row i: xrec[(rb + 2 k) * 128 + i]
+          if (h == 0) xrec[(rb + 2 * nb) * 128 + r] = cr;
+          if (tr) tr[7] = globaltimer_ns();
+          // each column half of the row's threads loads half of the G records (all loads in flight),
+          // merges them in tile order; the two partial records meet in smem (order h = 0, 1)
+          const int kb0 = h ? (G + 1) / 2 : 0, kb1 = h ? G : (G + 1) / 2;
+          float n = 0.f, sm = 0.f, mx = -INFINITY, mn = INFINITY;
+          float4 v[8];
+          auto load8 = [&](int k0) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (k0 + u < kb1)
+                v[u] = (p.dbg & 1) ? make_float4(0.f, 0.f, 0.f, 0.f) : ld_relaxed_f4(xrec + (rb + 2 * (k0 + u)) * 128 + r);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (k0 + u < kb1 && rec_pending(v[u])) v[u] = rec_wait(xrec + (rb + 2 * (k0 + u)) * 128 + r);
+          };
+          for (int k0 = kb0; k0 < kb1; k0 += 8) {  // sum n_k mean_k (LayerNorm) | sum ss_k; max / min
+            load8(k0);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (k0 + u < kb1) {
+                const float nk = (float)max(0, min(TN, p.N - (k0 + u) * TN));
+                n += nk;
+                sm = NORM == LOKA_NORM_LAYER ? fmaf(nk, v[u].x, sm) : sm + v[u].x;
+                mx = fmaxf(mx, v[u].z);
+                mn = fminf(mn, v[u].w);
+              }
           }
-          named_bar_sync(1, 32 * kPnEpiWarps);
-          // merge the G tile records of the row in tile order (identical in every CTA of the row)
-          const float4* rr = xrec_r + ((size_t)mb * G * 2 + rank) * 128 + r;  // tile k at rr[k * 256]
-          float4 o = make_float4(0.f, 0.f, -INFINITY, INFINITY);
-          float n = 0.f, sm = 0.f;
-          for (int k = 0; k < G; ++k) {
-            const float4 v = ldcg_f4(rr + (size_t)k * 256);
-            const float nk = (float)max(0, min(TN, p.N - k * TN));
-            n += nk;
-            sm = fmaf(nk, v.x, sm);
-            o.y += v.y;
-            o.z = fmaxf(o.z, v.z);
-            o.w = fminf(o.w, v.w);
-          }
+          float pm = sm, pm2 = 0.f;  // LayerNorm: this half's (mean, M2) of its tiles
           if constexpr (NORM == LOKA_NORM_LAYER) {
-            const float mu = n > 0.f ? __fdiv_rn(sm, n) : 0.f;
-            float mm = 0.f;
-            for (int k = 0; k < G; ++k) {
-              const float4 v = ldcg_f4(rr + (size_t)k * 256);
-              const float nk = (float)max(0, min(TN, p.N - k * TN));
-              const float dk = v.x - mu;
-              mm += v.y + nk * dk * dk;
+            pm = n > 0.f ? __fdiv_rn(sm, n) : 0.f;
+            for (int k0 = kb0; k0 < kb1; k0 += 8) {
+              if (kb1 - kb0 > 8) load8(k0);  // (more than 8 tiles per half, G > 16: load again)
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if (k0 + u < kb1) {
+                  const float nk = (float)max(0, min(TN, p.N - (k0 + u) * TN));
+                  const float dk = v[u].x - pm;
+                  pm2 += v[u].y + nk * dk * dk;
+                }
             }
-            cr = make_float4(mu, mm, o.z, o.w);
-          } else if constexpr (NORM == LOKA_NORM_RMS) {
-            float s2 = 0.f;
-            for (int k = 0; k < G; ++k) s2 += ldcg_f4(rr + (size_t)k * 256).x;
-            cr = make_float4(s2, 0.f, o.z, o.w);
-          } else {
-            cr = make_float4(0.f, 0.f, o.z, 0.f);
           }
-        } else {
-          named_bar_sync(1, 32 * kPnEpiWarps);  // hrec reads done before the next tile's writes
+          named_bar_sync(1, 32 * kPnEpiWarps);  // the halves' hrec reads above are done
+          hrec[h * 128 + r] = make_float4(pm, pm2, mx, mn);
+          named_bar_sync(1, 32 * kPnEpiWarps);
+          const float4 a0 = hrec[r], a1 = hrec[128 + r];
+          if constexpr (NORM == LOKA_NORM_LAYER) {
+            const float na = (float)min((G + 1) / 2 * TN, p.N), nbb = (float)p.N - na;
+            const float mu = __fdiv_rn(fmaf(na, a0.x, nbb * a1.x), (float)p.N);
+            const float d0 = a0.x - mu, d1 = a1.x - mu;
+            cr = make_float4(mu, a0.y + na * d0 * d0 + (a1.y + nbb * d1 * d1), fmaxf(a0.z, a1.z), fminf(a0.w, a1.w));
+          } else if constexpr (NORM == LOKA_NORM_RMS) {
+            cr = make_float4(a0.x + a1.x, 0.f, fmaxf(a0.z, a1.z), fminf(a0.w, a1.w));
+          } else {
+            cr = make_float4(0.f, 0.f, fmaxf(a0.z, a1.z), 0.f);
+          }
         }
+        named_bar_sync(1, 32 * kPnEpiWarps);  // hrec reads done before the next tile's writes
         const float nrow = (float)p.N;
         if constexpr (NORM == LOKA_NORM_LAYER) {
           rstd = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(cr.y, nrow), p.eps)));
@@ -458,6 +486,7 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
           if (fp8_out) amax = cr.z;
         }
       }
+      if (tr) tr[2] = globaltimer_ns();
       float r_out = 1.f;
       if (fp8_out) {
         if (__float_as_uint(amax) >= 0x7F800000u && p.status) atomicOr(p.status, LOKA_DEVSTATUS_NONFINITE);
@@ -468,19 +497,11 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
       }
 
       // ---- pass N: normalise, activation, cast, store ----
-      const float rs = fold ? __fmul_rn(cfold, rstd) : rstd;
+      const float rs = __fmul_rn(sc, rstd);
       const float2 r2 = make_float2(rs, rs), c02 = make_float2(c0, c0);
       float amx = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < kNch; ++c) {
+      auto out_chunk = [&](float (&y)[32], int c) {
         const int cb = 32 * c;
-        float y[32];
-        tmem_ld32(tbase + (uint32_t)cb, y);
-        if (c == kNch - 1) {  // the whole accumulator read: hand it back to the MMA
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(acc_empty0 + 8u * buf);
-        }
         if (!fold) dequant(y, cb);
 #pragma unroll
         for (int k = 0; k < 32; k += 4) {
@@ -563,7 +584,9 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
           }
           ++nbox;
         }
-      }
+      };
+      stream_tmem(out_chunk, true);
+      if (tr) tr[3] = globaltimer_ns();
       if (p.amax_out) warp_amax_to(p.amax_out, amx);
     }
     if (lane == 0) bulk_wait0();

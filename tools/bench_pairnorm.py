@@ -64,11 +64,35 @@ def run_case(name, M, N, K, norm, od, act="none", gran="tensor", reps=10, modes=
         del wsb
     os.environ.pop("LOKA_PAIRNORM", None)
 
+    os.environ["LOKA_PAIR_WIDE"] = "0"
+
+    def plain256():
+        lk.loka_fp8_linear_norm(xq, xs, wq, ws, a_gran=gran, b_gran=gran, norm="none", out_dtype=od, y=y)
+    with ClockSampler(torch.cuda.current_device()) as cs:
+        ms = timed(plain256, reps)
+    out["plain_gemm_256_tiles"] = {"ms": round(ms, 4), "tflops": round(fl / ms / 1e9, 1), "clocks": cs.summary()}
+    os.environ.pop("LOKA_PAIR_WIDE", None)
+
     def plain():
         lk.loka_fp8_linear_norm(xq, xs, wq, ws, a_gran=gran, b_gran=gran, norm="none", out_dtype=od, y=y)
     with ClockSampler(torch.cuda.current_device()) as cs:
         ms = timed(plain, reps)
     out["plain_gemm_same_shape"] = {"ms": round(ms, 4), "tflops": round(fl / ms / 1e9, 1), "clocks": cs.summary()}
+    # achievability reference: cuBLASLt FP8 (torch._scaled_mm, tensorwise scales, bf16 out) on the same
+    # operands (library GEMM, no norm)
+    try:
+        a8 = xq.view(torch.float8_e4m3fn)
+        b8 = wq.view(torch.float8_e4m3fn)
+        sa = xs.reshape(()) if xs.numel() == 1 else xs.reshape(-1, 1)
+        sb = ws.reshape(()) if ws.numel() == 1 else ws.reshape(1, -1)
+        def smm():
+            torch._scaled_mm(a8, b8.t(), scale_a=sa, scale_b=sb, out_dtype=torch.bfloat16)
+        with ClockSampler(torch.cuda.current_device()) as cs:
+            ms = timed(smm, reps)
+        out["cublaslt_scaled_mm_same_shape"] = {"ms": round(ms, 4), "tflops": round(fl / ms / 1e9, 1),
+                                                "clocks": cs.summary()}
+    except Exception as e:  # noqa: BLE001
+        out["cublaslt_scaled_mm_same_shape"] = {"error": str(e)[:200]}
     res.update(out)
     return res
 
