@@ -1,18 +1,22 @@
 #!/usr/bin/env python
 """bench.py — FP8 linear+norm hot path of LoKA on B200 (BASELINE.json metric), one JSON line.
 
-Workload (BASELINE.json configs[1], "cfg2"): LRM MLP stack, batch M = 4096 per GPU, 8 layers with
-dims [1024,1024,1024,512,512,256,256,512,1024]; every layer is rowwise-e4m3 FP8 linear + LayerNorm;
-layers 0-6 hand their output to the next layer as e4m3 + row scales (fused in the epilogue),
-layer 7 emits bf16.  One step = quantize X + quantize the 8 weights + 8 fused linear+LayerNorm
-launches, captured once in a CUDA graph and replayed.
+Headline workload (BASELINE.json configs[4] at P = N GPUs, "cfg5"; the largest LRM shape of the
+north star): global batch M = 262144 rows sharded over the ranks (strong scaling), K = N = 4096,
+heavy-tailed X (bf16, synth.heavy), tensorwise e4m3 X and W, linear + LayerNorm (gamma = 1, beta = 0),
+bf16 out.  One step:
+  loka_quantize(X, AMAX_ONLY) -> NCCL all_reduce(MAX) of the amax (N > 1) -> loka_quantize(X,
+  CAST_WITH_AMAX) -> loka_quantize(W, tensorwise) -> loka_fp8_linear_norm (CTA-pair FP8 GEMM with the
+  LayerNorm fused in its epilogue, pairnorm.cu).
+Extras on the same line: "cfg2" (the 8-layer MLP stack, configs[1]) and "cfg3" (the 64-GEMM grouped
+ensemble with probe + dispatch, configs[2]).
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--no-extras]
 
-Multi-GPU (torchrun, one process per GPU): every rank runs its own batch of 4096 rows (data
-parallel, weak scaling, no data-path collective: the rowwise recipe needs none); the time is the
-max over ranks.  Timing: CUDA events on the launching stream around each step, L2 flushed
-(256 MiB write) before every timed step, W warm-up steps, exactly K timed steps.
+Multi-GPU (torchrun, one process per GPU): rank r owns rows [r M/N, (r+1) M/N) of the one global X
+(the sharded codes equal the single-GPU codes: MAX is exact, D20); time = max over ranks.
+Timing: CUDA events on the launching stream around each step, barrier + synchronize on both sides;
+the inputs (2 GB of X at N = 1, 268 MB at N = 8) exceed the 126 MB L2, so no flush between steps.
 """
 from __future__ import annotations
 
@@ -29,6 +33,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "FP8 linear+norm TFLOP/s (% of 4.5 PF) and speedup vs BF16, 1/2/4/8 B200"
+CFG5_M, CFG5_K, CFG5_N = 262144, 4096, 4096
+WORKLOAD5 = ("cfg5: global M=262144 sharded over the GPUs (strong scaling), K=N=4096, heavy-tailed X, tensorwise "
+             "e4m3 X/W with the NCCL MAX all-reduce of X's amax, FP32 accumulate, linear + fused LayerNorm, bf16 out")
 DIMS = [1024, 1024, 1024, 512, 512, 256, 256, 512, 1024]
 M_PER_GPU = 4096
 WORKLOAD = ("cfg2 LRM MLP stack: M=4096 per GPU, 8 layers dims " + str(DIMS) +
@@ -46,6 +53,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="loka", choices=["loka", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the cfg2 / cfg3 extra keys")
     ap.add_argument("--profile-steps", type=int, default=0, help="run N eager steps only (for ncu), no JSON")
     return ap.parse_args()
 
@@ -205,7 +213,8 @@ def time_steps(run, steps, warmup, flush, stream, barrier=None):
     torch.cuda.synchronize()
     with torch.cuda.stream(stream):
         for e0, e1 in ev:
-            flush.zero_()
+            if flush is not None:
+                flush.zero_()
             e0.record(stream)
             run()
             e1.record(stream)
@@ -275,28 +284,99 @@ def time_pipelined(sets, xh, steps, warmup, flush, stream, barrier=None):
 
 
 def peaks():
+    """(bf16 burst TF/s, bf16 sustained TF/s, HBM GB/s, source) from the driver-written MEASURED_PEAKS.json."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
         d = json.load(open(p))
-        return float(d["bf16_tflops"]), float(d["hbm_gbs"]), "measured"
+        return (float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), float(d["hbm_gbs"]),
+                "measured")
     except Exception:  # noqa: BLE001
-        return 1590.0, 6650.0, "fallback"
+        return 1590.0, 1370.0, 6650.0, "fallback"
 
 
 # ------------------------------------------------------------------------------------------
-# oracle (CPU) legs: cpu_baseline (rank 0, N=1) and --impl reference
+# cfg5: the headline step
 # ------------------------------------------------------------------------------------------
-def oracle_forward(x_np, w_np):
-    import numpy as np
+class Cfg5:
+    """Preallocated cfg5 step on this rank's shard through the C ABI (libloka.so)."""
+
+    def __init__(self, lk, x, w, dist=None):
+        import ctypes as C
+        import torch
+        self.lk, self.C, self.dist = lk, C, dist
+        dev = x.device
+        M, K = x.shape
+        N = w.shape[0]
+        self.x, self.w = x, w
+        self.keep = []
+        self.xq = torch.empty(M, K, dtype=torch.uint8, device=dev)
+        self.xs = torch.empty(1, dtype=torch.float32, device=dev)
+        self.amax = torch.zeros(1, dtype=torch.float32, device=dev)
+        self.wq = torch.empty(N, K, dtype=torch.uint8, device=dev)
+        self.wsc = torch.empty(1, dtype=torch.float32, device=dev)
+        self.y = torch.empty(M, N, dtype=torch.bfloat16, device=dev)
+        self.tx = lk._tensor(x, lk.BF16, M, K)
+        self.tq = lk._tensor(self.xq, lk.E4M3, M, K, self.xs, "tensor")
+        self.tw = lk._tensor(w, lk.BF16, N, K)
+        self.twq = lk._tensor(self.wq, lk.E4M3, N, K, self.wsc, "tensor")
+        self.qws = torch.empty(max(256, int(lk._lib.loka_quantize_workspace_size(C.byref(self.tx), C.byref(self.tq)))),
+                               dtype=torch.uint8, device=dev)
+        self.wqws = torch.empty(max(256, int(lk._lib.loka_quantize_workspace_size(C.byref(self.tw), C.byref(self.twq)))),
+                                dtype=torch.uint8, device=dev)
+        self.args, _, _ = lk.make_linear_args(self.xq, self.xs, self.wq, self.wsc, a_gran="tensor", b_gran="tensor",
+                                              norm="layer", out_dtype="bf16", y=self.y, keep=self.keep)
+        nws = int(lk._lib.loka_linear_workspace_size(C.byref(self.args)))
+        self.lws = torch.empty(max(nws, 256), dtype=torch.uint8, device=dev)
+        self.flops = 2.0 * M * N * K
+
+    def _q(self, tx, tq, phase, amax, ws, sh):
+        st = self.lk._lib.loka_quantize(self.C.byref(tx), self.C.byref(tq), None, phase,
+                                        None if amax is None else amax.data_ptr(), None, ws.data_ptr(), ws.numel(), sh)
+        if st:
+            raise self.lk.LokaError(st, "loka_quantize")
+
+    def quantize(self, sh):
+        """a1 + a9 + a2: X's local amax, the MAX all-reduce (N > 1), X's cast, W's quantize."""
+        lk = self.lk
+        self._q(self.tx, self.tq, lk.PHASE["amax"], self.amax, self.qws, sh)
+        if self.dist is not None:
+            self.dist.all_reduce(self.amax, op=self.dist.ReduceOp.MAX)
+        self._q(self.tx, self.tq, lk.PHASE["cast"], self.amax, self.qws, sh)
+        self._q(self.tw, self.twq, lk.PHASE["full"], None, self.wqws, sh)
+
+    def linear(self, sh):
+        """a4 + a5: the fused FP8 GEMM + LayerNorm (the dominant kernel)."""
+        st = self.lk._lib.loka_fp8_linear_norm(self.C.byref(self.args), self.C.c_void_p(self.lws.data_ptr()),
+                                               self.lws.numel(), sh)
+        if st:
+            raise self.lk.LokaError(st, "loka_fp8_linear_norm")
+
+    def step(self, sh):
+        self.quantize(sh)
+        self.linear(sh)
+
+
+def cfg5_oracle(rows, seed=3, threads=None):
+    """The oracle on a bounded sample of cfg5: `rows` rows of the global heavy-tailed X (tensorwise amax of
+    the sample), W's tensorwise quantize, linear + LayerNorm in FP64.  Returns (seconds, flops)."""
     import oracle
-    hq, hs = oracle.quantize.quantize(x_np, "e4m3", "row")
-    y = None
-    for l in range(8):
-        wq, wsc = oracle.quantize.quantize(w_np[l], "e4m3", "row")
-        y = oracle.linear.linear_norm(hq, hs, "e4m3", "row", wq, wsc, "e4m3", "row", norm="layer")
-        if l < 7:
-            hq, hs = oracle.quantize.quantize(y.astype(np.float32).astype(np.float64), "e4m3", "row")
-    return y
+    import synth
+    x = synth.heavy(rows, CFG5_K, seed, total_rows=CFG5_M).double().numpy()
+    w = synth.weight(CFG5_N, CFG5_K, 4).double().numpy()
+
+    def run():
+        xq, xs = oracle.quantize.quantize(x, "e4m3", "tensor")
+        wq, ws = oracle.quantize.quantize(w, "e4m3", "tensor")
+        oracle.linear.linear_norm(xq, xs, "e4m3", "tensor", wq, ws, "e4m3", "tensor", norm="layer")
+
+    t0 = time.perf_counter()
+    if threads:
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=threads):
+            run()
+    else:
+        run()
+    return time.perf_counter() - t0, 2.0 * rows * CFG5_K * CFG5_N
 
 
 def cpu_threads():
@@ -307,47 +387,135 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
-def oracle_inputs(rows, seed):
-    import synth
-    x = synth.gaussian(rows, DIMS[0], seed).double().numpy()
-    w = [synth.weight(DIMS[l + 1], DIMS[l], 100 + l).double().numpy() for l in range(8)]
-    return x, w
-
-
-def cpu_baseline(rows=M_PER_GPU, seed=0):
-    x, w = oracle_inputs(rows, seed)
-    t0 = time.perf_counter()
-    oracle_forward(x, w)
-    dt = time.perf_counter() - t0
-    return {"value": flops_per_step(rows) / dt / 1e12, "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "oracle",
-            "sample": f"full cfg2 step on {rows} rows (8 layers, weight quantize included), numpy FP64 oracle, "
-                      f"{dt:.2f} s", "seconds": dt}
+def cpu_baseline(rows=1024):
+    dt, fl = cfg5_oracle(rows)
+    dt1, _ = cfg5_oracle(rows, threads=1)
+    return {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "oracle",
+            "sample": f"{rows} of cfg5's {CFG5_M} rows: tensorwise quantize of the sample and of W (4096x4096), "
+                      f"linear + LayerNorm, numpy FP64 oracle on the host; {dt:.2f} s",
+            "seconds": round(dt, 3),
+            "single_thread": {"value": fl / dt1 / 1e12, "seconds": round(dt1, 3), "cores": 1},
+            "full_step_extrapolated_s": round(dt * CFG5_M / rows, 1),
+            "extrapolation": "linear in rows (rows are independent given the scales; W's quantize counted once "
+                             "per sample, so this over-counts it for the full step)"}
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the oracle as it stands, each step a 256-row sample of cfg5 (W quantize
+    included), on the host's cores; rank 0 only."""
     if rank != 0:
         return
-    rows = 512
-    x, w = oracle_inputs(rows, 0)
+    rows = 256
     for _ in range(args.warmup):
-        oracle_forward(x, w)
-    ts = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        oracle_forward(x, w)
-        ts.append(time.perf_counter() - t0)
+        cfg5_oracle(rows)
+    ts = [cfg5_oracle(rows)[0] for _ in range(args.steps)]
     tot = sum(ts)
-    val = flops_per_step(rows) * args.steps / tot / 1e12
+    fl = 2.0 * rows * CFG5_K * CFG5_N
+    val = fl * args.steps / tot / 1e12
     cb = {"value": val, "unit": "TFLOP/s", "cores": cpu_threads(), "kind": "oracle",
-          "sample": f"each step = cfg2 forward on {rows} of the 4096 rows (8 layers incl. weight quantize), "
-                    "numpy FP64 oracle on the host"}
+          "sample": f"each step = {rows} of cfg5's {CFG5_M} rows: tensorwise quantize of the sample and of W "
+                    "(4096x4096), linear + LayerNorm, numpy FP64 oracle on the host"}
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "rows_per_step": rows, "parallelism": "host"},
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD5, "rows_per_step": rows, "parallelism": "host"},
             "cpu_baseline": cb, "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                                         "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+# extras: cfg2 (the fused 8-layer stack) and cfg3 (the grouped 64-GEMM ensemble)
+# ------------------------------------------------------------------------------------------
+def cfg2_extra(lk, dev, rank, steps, warmup, stream):
+    import torch
+    import synth
+    x = synth.gaussian(M_PER_GPU, DIMS[0], rank, device=dev)
+    w = [synth.weight(DIMS[l + 1], DIMS[l], 100 + l, device=dev) for l in range(8)]
+    stack = Fp8Stack(lk, x, w)
+    sh = stream.cuda_stream
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    g8 = capture(lambda: stack.step(sh), stream)
+    t8 = time_steps(g8.replay, steps, warmup, flush, stream)
+    gst = capture(lambda: stack.stack_only(sh), stream)
+    tst = time_steps(gst.replay, steps, warmup, flush, stream)
+    out_bf = torch.empty(M_PER_GPU, DIMS[8], dtype=torch.bfloat16, device=dev)
+    gb = capture(lambda: bf16_step(x, w, out_bf), stream)
+    tb = time_steps(gb.replay, steps, warmup, flush, stream)
+    ms8, msst, msb = sum(t8) / len(t8), sum(tst) / len(tst), sum(tb) / len(tb)
+    fl = flops_per_step()
+    return {"workload": WORKLOAD, "value": round(fl / ms8 / 1e9, 2), "unit": "TFLOP/s", "ms_per_step": round(ms8, 5),
+            "step": "1 grouped quantize launch (X + 8 W) + 1 fused 8-layer stack launch, CUDA-graph replay, "
+                    "L2 flushed before every step",
+            "bf16_ms_per_step": round(msb, 5), "speedup_vs_bf16": round(msb / ms8, 3),
+            "stack_kernel_us": round(1e3 * msst, 3), "stack_kernel_tflops": round(fl / msst / 1e9, 2)}
+
+
+def cfg3_extra(lk, dev, steps, warmup, stream):
+    """The 64-GEMM ensemble: grouped quantize + grouped FP8 launch vs 64 cuBLAS BF16 GEMMs; probe MERE of
+    every layer vs the BF16 outputs; dispatch per layer on per-layer timings (tools/bench_cfg3.py has the
+    full per-layer table)."""
+    import ctypes
+    import torch
+    import synth
+    S, M = synth.CFG3_DIMS, 2048
+    xs = [(synth.heavy(M, k, i, device=dev) if i % 2 else synth.gaussian(M, k, i, device=dev)) for i, k in enumerate(S)]
+    ws = [[synth.weight(n, k, 1000 + 8 * i + j, device=dev) for j, n in enumerate(S)] for i, k in enumerate(S)]
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    flops = sum(2.0 * M * k * n for k in S for n in S)
+    xq = [(torch.empty(M, k, dtype=torch.uint8, device=dev), torch.empty(M, dtype=torch.float32, device=dev)) for k in S]
+    wq = [[lk.loka_quantize(w, "e4m3", "row") for w in row] for row in ws]
+    keep, args, ys = [], [], []
+    for i in range(8):
+        for j in range(8):
+            ar, y, _ = lk.make_linear_args(xq[i][0], xq[i][1], wq[i][j][0], wq[i][j][1], out_dtype="bf16", keep=keep)
+            args.append(ar)
+            ys.append(y)
+    arr = (lk.loka_linear_args * 64)(*args)
+    qx = (lk.loka_tensor * 8)()
+    qq = (lk.loka_tensor * 8)()
+    for i, k in enumerate(S):
+        qx[i] = lk._tensor(xs[i], lk.BF16, M, k)
+        qq[i] = lk._tensor(xq[i][0], lk.E4M3, M, k, xq[i][1], "row")
+    sh = stream.cuda_stream
+
+    def fp8_step():
+        assert lk._lib.loka_quantize_grouped(8, qx, qq, None, sh) == 0
+        assert lk._lib.loka_grouped_fp8_linear(64, arr, None, 0, sh) == 0
+
+    yb = [[torch.empty(M, n, dtype=torch.bfloat16, device=dev) for n in S] for _ in S]
+
+    def bf16_step_3():
+        for i in range(8):
+            for j in range(8):
+                torch.matmul(xs[i], ws[i][j].t(), out=yb[i][j])
+
+    g8 = capture(fp8_step, stream)
+    gb = capture(bf16_step_3, stream)
+    t8 = time_steps(g8.replay, steps, warmup, flush, stream)
+    tb = time_steps(gb.replay, steps, warmup, flush, stream)
+    ms8, msb = sum(t8) / len(t8), sum(tb) / len(tb)
+    g8.replay()
+    gb.replay()
+    torch.cuda.synchronize()
+    stats = lk.probe_stats_to_dicts(lk.loka_probe_error([(ys[8 * i + j], yb[i][j]) for i in range(8) for j in range(8)]))
+    mere = [s_["mere"] for s_ in stats]
+    geo = math.exp(sum(math.log(max(v, 1e-6)) for v in mere) / len(mere))
+    # dispatch: one candidate per layer (FP8 rowwise, its share of the grouped step's time) against the
+    # layer's BF16 time share; budget 0.2, min speedup 1.05 (P:541)
+    chosen = 0
+    for i, k in enumerate(S):
+        for j, n in enumerate(S):
+            share = 2.0 * M * k * n / flops
+            c = lk.loka_dispatch_select([("fp8_rowwise", "fwd", mere[8 * i + j], 1e3 * ms8 * share)],
+                                        1e3 * msb * share, 0.2, 1.05)
+            chosen += c == 0
+    return {"workload": "cfg3: 64 GEMMs M=2048, K,N in " + str(S) + ", 8 shared inputs (odd ones heavy-tailed), bf16",
+            "value": round(flops / ms8 / 1e9, 2), "unit": "TFLOP/s", "ms_per_step": round(ms8, 5),
+            "step": "grouped rowwise quantize of the 8 inputs + grouped FP8 GEMM (2 persistent launches), CUDA "
+                    "graph, L2 flushed", "bf16_ms_per_step": round(msb, 5), "speedup_vs_bf16": round(msb / ms8, 3),
+            "probe_geomean_mere_vs_bf16": round(geo, 5), "dispatch_fp8_layers": int(chosen),
+            "dispatch_rule": "MERE < 0.2 and speedup > 1.05 (time shares of the grouped step)"}
 
 
 # ------------------------------------------------------------------------------------------
@@ -361,6 +529,7 @@ def main():
 
     import torch
     import torch.distributed as dist
+    import torch.nn.functional as F
 
     import synth
     import paper_2605_10886_b200 as lk
@@ -370,63 +539,75 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     barrier = (lambda: dist.barrier(device_ids=[local])) if world > 1 else None
-
-    # inputs: rank r owns its own 4096-row batch (seed r); weights identical on every rank
-    x = synth.gaussian(M_PER_GPU, DIMS[0], rank, device=dev)
-    w = [synth.weight(DIMS[l + 1], DIMS[l], 100 + l, device=dev) for l in range(8)]
-    stack = Fp8Stack(lk, x, w)
     stream = torch.cuda.Stream(device=dev)
     sh = stream.cuda_stream
+
+    # this rank's shard of the one global heavy-tailed X (seed 3); W identical on every rank
+    r0 = rank * CFG5_M // world
+    r1 = (rank + 1) * CFG5_M // world
+    x = synth.heavy(r1 - r0, CFG5_K, 3, device=dev, row0=r0, total_rows=CFG5_M)
+    w = synth.weight(CFG5_N, CFG5_K, 4, device=dev)
+    step = Cfg5(lk, x, w, dist if world > 1 else None)
 
     if args.profile_steps:
         with torch.cuda.stream(stream):
             for _ in range(args.profile_steps):
-                stack.step(sh)
+                step.step(sh)
         torch.cuda.synchronize()
         return
 
+    with torch.cuda.stream(stream):
+        step.step(sh)  # warm (attributes, NCCL communicator)
+    torch.cuda.synchronize()
     n0 = lk.launch_count()
     with torch.cuda.stream(stream):
-        stack.step(sh)
+        step.step(sh)
     torch.cuda.synchronize()
     launches_per_step = lk.launch_count() - n0
 
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    g8 = capture(lambda: stack.step(sh), stream)
+    def run_fp8():
+        with torch.cuda.stream(stream):
+            step.step(sh)
+
     with ClockSampler(local) as clk:
-        t_fp8 = time_steps(g8.replay, args.steps, args.warmup, flush, stream, barrier)
+        t_fp8 = time_steps(run_fp8, args.steps, args.warmup, None, stream, barrier)
     clocks = clk.summary()
 
-    # The dominant kernel (the fused stack launch): a graph of that one launch, replayed with the L2
-    # flushed before each replay, timed with events on the launching stream.
-    gst = capture(lambda: stack.stack_only(sh), stream)
-    t_st = time_steps(gst.replay, args.steps, args.warmup, flush, stream, None)
-    stack_ms = sum(t_st) / len(t_st)
-    # the per-layer path (one linear_norm launch per layer) for comparison
-    gpl = capture(lambda: stack.step_per_layer(sh), stream)
-    t_pl = time_steps(gpl.replay, args.steps, args.warmup, flush, stream, None)
-    per_layer_ms = sum(t_pl) / len(t_pl)
+    # the dominant kernel alone: the fused GEMM + LayerNorm call (incl. its workspace memset node)
+    def run_lin():
+        with torch.cuda.stream(stream):
+            step.linear(sh)
 
-    # BF16 baseline (torch F.linear + F.layer_norm, graph-captured) on the same inputs
-    out_bf = torch.empty(M_PER_GPU, DIMS[8], dtype=torch.bfloat16, device=dev)
-    gb = capture(lambda: bf16_step(x, w, out_bf), stream)
-    t_bf = time_steps(gb.replay, args.steps, args.warmup, flush, stream, barrier)
+    t_lin = time_steps(run_lin, args.steps, args.warmup, None, stream, None)
+    lin_ms = statistics.median(t_lin)
 
-    # e2e through the public API: pinned host X -> device, graph step, device Y -> pinned host
+    def run_q():
+        with torch.cuda.stream(stream):
+            step.quantize(sh)
+
+    t_q = time_steps(run_q, args.steps, args.warmup, None, stream, barrier)
+
+    # BF16 baseline (torch F.linear + F.layer_norm, cuBLAS) on the same shard
+    out_bf = torch.empty_like(step.y)
+
+    def run_bf():
+        with torch.cuda.stream(stream):
+            out_bf.copy_(F.layer_norm(F.linear(x, w), (CFG5_N,)))
+
+    t_bf = time_steps(run_bf, args.steps, args.warmup, None, stream, barrier)
+
+    # e2e through the public API: pinned host X -> device, the step, device Y -> pinned host, every step
     xh = x.cpu().pin_memory()
-    yh = torch.empty(M_PER_GPU, DIMS[8], dtype=torch.bfloat16).pin_memory()
+    yh = torch.empty(step.y.shape, dtype=torch.bfloat16).pin_memory()
 
-    def e2e_step():
-        stack.x.copy_(xh, non_blocking=True)
-        g8.replay()
-        yh.copy_(stack.y, non_blocking=True)
+    def run_e2e():
+        with torch.cuda.stream(stream):
+            step.x.copy_(xh, non_blocking=True)
+            step.step(sh)
+            yh.copy_(step.y, non_blocking=True)
 
-    t_e2e = time_steps(e2e_step, args.steps, args.warmup, flush, stream, barrier)
-    # the same, pipelined as a serving loop would run it: two buffer sets, the H2D copy of step i+1
-    # and the D2H copy of step i-1 on their own streams (PCIe is full duplex) under step i's kernels
-    stack2 = Fp8Stack(lk, torch.empty_like(x), w)
-    g8b = capture(lambda: stack2.step(sh), stream)
-    t_pipe = time_pipelined([(stack, g8), (stack2, g8b)], xh, args.steps, args.warmup, flush, stream, barrier)
+    e2e_steps = max(3, min(args.steps, 10))
+    t_e2e = time_steps(run_e2e, e2e_steps, 1, None, stream, barrier)
 
     def max_over_ranks(v):
         if world == 1:
@@ -437,63 +618,73 @@ def main():
 
     ms_fp8 = max_over_ranks(sum(t_fp8)) / args.steps
     ms_bf = max_over_ranks(sum(t_bf)) / args.steps
-    ms_e2e_serial = max_over_ranks(sum(t_e2e)) / args.steps
-    ms_e2e = max_over_ranks(t_pipe) / args.steps
-    fl = flops_per_step() * world
+    ms_q = max_over_ranks(sum(t_q)) / args.steps
+    ms_lin = max_over_ranks(lin_ms)
+    ms_e2e = max_over_ranks(sum(t_e2e)) / e2e_steps
+    fl = 2.0 * CFG5_M * CFG5_N * CFG5_K  # the whole job (all ranks)
     value = fl / (ms_fp8 * 1e-3) / 1e12
-    bf_value = fl / (ms_bf * 1e-3) / 1e12
-    e2e_value = fl / (ms_e2e * 1e-3) / 1e12
-    e2e_serial_value = fl / (ms_e2e_serial * 1e-3) / 1e12
 
-    bf16_peak, hbm_peak, src = peaks()
-    fp8_peak = 2.0 * bf16_peak  # nominal dense fp8/bf16 ratio 4500/2250
-    stack_fl = flops_per_step()  # one stack launch = the 8 layers' 2 M K N
-    achieved = stack_fl / (stack_ms * 1e-3) / 1e12
+    bf16_peak, bf16_sus, hbm_peak, src = peaks()
+    fp8_peak_sus, fp8_peak_burst = 2.0 * bf16_sus, 2.0 * bf16_peak  # nominal fp8/bf16 = 4500/2250
+    achieved = step.flops / (lin_ms * 1e-3) / 1e12
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get("stack_bytes_per_launch")
+            traffic = json.load(open(tf)).get(f"pairnorm_bytes_per_launch_m{x.shape[0]}")
         except Exception:  # noqa: BLE001
             traffic = None
+
+    extras = {}
+    if not args.no_extras:
+        extras["cfg2"] = cfg2_extra(lk, dev, rank, args.steps, args.warmup, stream)
+        if rank == 0:
+            extras["cfg3"] = cfg3_extra(lk, dev, args.steps, args.warmup, stream)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms_fp8, 5), "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": round(ms_fp8, 5), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "e4m3", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "model": "cfg2", "global_batch": M_PER_GPU * world,
-                       "seq_len": None, "parallelism": f"dp{world}",
-                       "l2": "flushed before every timed step (256 MiB write)",
-                       "step": "1 grouped quantize launch (X + 8 W, rowwise e4m3) + 1 fused 8-layer FP8 "
-                               "linear+LayerNorm stack launch, CUDA-graph replay"},
+            "config": {"workload": WORKLOAD5, "model": "cfg5", "global_batch": CFG5_M, "rows_per_gpu": int(x.shape[0]),
+                       "K": CFG5_K, "N": CFG5_N, "seq_len": None, "parallelism": f"dp{world} (M sharded)",
+                       "l2": "not flushed: the step's inputs (X bf16 2 GB / N GPUs) exceed the 126 MB L2",
+                       "step": "loka_quantize AMAX_ONLY -> NCCL all_reduce(MAX) (N > 1) -> loka_quantize "
+                               "CAST_WITH_AMAX -> loka_quantize(W, tensorwise) -> loka_fp8_linear_norm (fused "
+                               "FP8 GEMM + LayerNorm), eager launches on one stream"},
             "pct_of_4500_tflops": round(100.0 * value / world / 4500.0, 2),
-            "bf16_baseline": {"value": round(bf_value, 3), "unit": "TFLOP/s", "ms_per_step": round(ms_bf, 5),
-                              "impl": "torch F.linear + F.layer_norm (bf16, cuBLAS), CUDA-graph replay"},
+            "compute_only": {"value": round(fl / (ms_lin * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
+                             "ms_per_step": round(ms_lin, 5),
+                             "pct_of_4500_tflops": round(100.0 * fl / (ms_lin * 1e-3) / 1e12 / world / 4500.0, 2),
+                             "what": "the fused GEMM + LayerNorm call alone on pre-quantized operands"},
+            "quantize_ms_per_step": round(ms_q, 5),
+            "bf16_baseline": {"value": round(fl / (ms_bf * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
+                              "ms_per_step": round(ms_bf, 5), "impl": "torch F.linear + F.layer_norm (bf16, cuBLAS)"},
             "speedup_vs_bf16": round(ms_bf / ms_fp8, 3),
-            "roofline": {"kernel": "stack_kernel (8 fused FP8 GEMM + LayerNorm layers), 1 launch/step",
-                         "bound": "tensor", "achieved": round(achieved, 2), "peak": round(fp8_peak, 1),
-                         "unit": "TFLOP/s", "frac": round(achieved / fp8_peak, 4), "traffic": traffic,
-                         "peak_source": f"{src}: 2 x bf16 {bf16_peak} TF/s (nominal fp8/bf16 ratio)",
-                         "flop_per_launch": stack_fl, "launch_us": round(1e3 * stack_ms, 3),
-                         "timing": "graph of the launch, L2 flushed before each replay, CUDA events"},
-            "per_layer_path": {"ms_per_step": round(per_layer_ms, 5),
-                               "value": round(flops_per_step() / (per_layer_ms * 1e-3) / 1e12, 3),
-                               "impl": "grouped quantize + 8 linear_norm launches (same layers, per-layer kernels)"},
-            "e2e": {"value": round(e2e_value, 3), "unit": "TFLOP/s", "ms_per_step": round(ms_e2e, 5),
-                    "h2d_bytes_per_step": int(x.numel() * 2), "d2h_bytes_per_step": int(stack.y.numel() * 2),
-                    "how": "pinned host X -> device, graph step (quantize + stack, L2 flushed first), "
-                           "device Y -> pinned host, every step; double-buffered: H2D / compute / D2H on three "
-                           "streams, one event pair around all K steps",
-                    "serial": {"value": round(e2e_serial_value, 3), "ms_per_step": round(ms_e2e_serial, 5),
-                               "how": "same copies, one stream, no overlap"}},
+            "roofline": {"kernel": "pair_norm_kernel<256, LayerNorm> (CTA-pair FP8 GEMM + fused LayerNorm), 1 "
+                                   "launch/step", "bound": "tensor", "achieved": round(achieved, 2),
+                         "peak": round(fp8_peak_sus, 1), "unit": "TFLOP/s", "frac": round(achieved / fp8_peak_sus, 4),
+                         "traffic": traffic,
+                         "peak_source": f"{src}: 2 x bf16 sustained {bf16_sus} TF/s (nominal fp8/bf16 ratio; the "
+                                        "kernel runs inside a multi-second loaded loop)",
+                         "peak_burst": round(fp8_peak_burst, 1), "frac_burst": round(achieved / fp8_peak_burst, 4),
+                         "flop_per_launch": step.flops, "launch_ms": round(lin_ms, 4),
+                         "algorithmic_bytes_per_launch": int(x.shape[0] * CFG5_K + CFG5_N * CFG5_K +
+                                                             x.shape[0] * CFG5_N * 2),
+                         "timing": "median of K launches, CUDA events on the launching stream"},
+            "e2e": {"value": round(fl / (ms_e2e * 1e-3) / 1e12, 3), "unit": "TFLOP/s", "ms_per_step": round(ms_e2e, 5),
+                    "h2d_bytes_per_step": int(x.numel() * 2), "d2h_bytes_per_step": int(step.y.numel() * 2),
+                    "steps": e2e_steps,
+                    "how": "pinned host X -> device, the step, device Y -> pinned host, one stream, every step"},
             "gpu_launches": int(launches_per_step * args.steps),
             "clocks": clocks,
         }
+        line.update(extras)
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline()
         print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier(device_ids=[local])
         dist.destroy_process_group()
 
 

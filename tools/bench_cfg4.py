@@ -51,7 +51,7 @@ def main():
     stream = torch.cuda.Stream()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
     fl = 2.0 * M * N * K
-    bf16_peak, _, src = peaks()
+    bf16_peak, _, _, src = peaks()
     res = {"workload": f"cfg4 training step M={M} K={K} N={N}: fwd Y=XW^T, dgrad dX=dY W, wgrad dW=dY^T X",
            "flop_per_gemm": fl, "fp8_peak_tflops": 2 * bf16_peak, "peak_source": src}
 

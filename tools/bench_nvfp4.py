@@ -33,7 +33,7 @@ def main():
     dev = torch.device("cuda")
     stream = torch.cuda.Stream()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
-    bf16_peak, _, src = peaks()
+    bf16_peak, _, _, src = peaks()
     res = {"fp4_peak_tflops": 4 * bf16_peak, "fp8_peak_tflops": 2 * bf16_peak, "peak_source": src, "shapes": []}
 
     def tmean(fn):

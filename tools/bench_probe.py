@@ -28,7 +28,7 @@ def main():
     dev = torch.device("cuda")
     stream = torch.cuda.Stream()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
-    _, hbm, src = peaks()
+    _, _, hbm, src = peaks()
     res = {"hbm_peak_gbs": hbm, "peak_source": src, "cases": []}
     cases = [("32768x4096 bf16 pair", [(32768, 4096)]),
              ("cfg3: 64 layers 2048 x N (N in S), bf16", [(2048, n) for _ in range(8) for n in synth.CFG3_DIMS])]

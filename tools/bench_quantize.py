@@ -35,7 +35,7 @@ def main():
     x = synth.heavy(R, Cc, 3, device=dev)
     stream = torch.cuda.Stream()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
-    _, hbm, src = peaks()
+    _, _, hbm, src = peaks()
     q = torch.empty(R, Cc, dtype=torch.uint8, device=dev)
     qt = torch.empty(Cc, R, dtype=torch.uint8, device=dev)
     out = {"shape": [R, Cc], "hbm_peak_gbs": hbm, "peak_source": src, "kernels": {}}

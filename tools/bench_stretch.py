@@ -48,7 +48,7 @@ def main():
         t = time_steps(g.replay, a.steps, 3, flush, stream)
     ms = sum(t) / len(t)
     fl = 2.0 * M * N * K
-    bf16_peak, _, src = peaks()
+    bf16_peak, _, _, src = peaks()
     # BF16 reference time on the same shape
     xb = synth.heavy(M, K, 3, device=dev)
     wb = synth.weight(N, K, 4, device=dev)
