@@ -356,6 +356,66 @@ __global__ void __launch_bounds__(256) amax_tensor_kernel(QuantParams p, uint32_
   }
 }
 
+// Dense (ld == cols) tensors: the tensor is one flat array of 16-byte vectors; every lane keeps 8
+// streaming (evict-first) 16-B loads in flight before reducing them, persistent grid of 4 CTAs per SM.
+template <typename Tin>
+__global__ void __launch_bounds__(256) amax_flat_kernel(QuantParams p, uint32_t* amax_bits) {
+  pdl_wait();
+  __shared__ uint32_t red[8];
+  constexpr int E = 16 / sizeof(Tin);  // elements per 16-B vector
+  constexpr int U = 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t n = p.rows * p.cols;
+  const int64_t nv = n / E;
+  const uint4* xv = reinterpret_cast<const uint4*>(p.x);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  uint32_t am = 0;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * stride < nv; i += U * stride) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = __ldcs(xv + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      Vec8<Tin> t;
+      if constexpr (sizeof(Tin) == 2) {
+        t.w = v[u];
+      } else {
+        t.a = make_float4(__uint_as_float(v[u].x), __uint_as_float(v[u].y), __uint_as_float(v[u].z),
+                          __uint_as_float(v[u].w));
+        t.b = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      am = max(am, t.amax_bits());
+    }
+  }
+  for (; i < nv; i += stride) {
+    Vec8<Tin> t;
+    const uint4 v = __ldcs(xv + i);
+    if constexpr (sizeof(Tin) == 2) {
+      t.w = v;
+    } else {
+      t.a = make_float4(__uint_as_float(v.x), __uint_as_float(v.y), __uint_as_float(v.z), __uint_as_float(v.w));
+      t.b = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    am = max(am, t.amax_bits());
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // the n % E tail elements
+    const Tin* xt = reinterpret_cast<const Tin*>(p.x) + nv * E;
+    Vec8<Tin> t;
+    t.load_partial(xt, (int)(n - nv * E));
+    am = max(am, t.amax_bits());
+  }
+  am = warp_max_u32(am);
+  if (lane == 0) red[warp] = am;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) am = max(am, red[w]);
+    am = max(am, red[0]);
+    if (am) atomicMax(amax_bits, am);
+    flag_nonfinite(am, p.status);
+  }
+}
+
 template <typename Tin, int FMT, int SF>
 __global__ void __launch_bounds__(256) cast_tensor_kernel(QuantParams p, const float* amax_dev) {
   pdl_wait();
@@ -461,7 +521,12 @@ static cudaError_t launch_quant_t(const QuantParams& p, int gran, int phase, flo
       if (phase == LOKA_PHASE_FULL || phase == LOKA_PHASE_AMAX_ONLY) {
         e = cudaMemsetAsync(amax_dev, 0, sizeof(float), st);
         if (e != cudaSuccess) return e;
-        e = launch_pdl(amax_tensor_kernel<Tin>, dim3((unsigned)nb), blk, st, p, reinterpret_cast<uint32_t*>(amax_dev));
+        const bool flat = p.ldx == p.cols && (reinterpret_cast<uintptr_t>(p.x) & 15) == 0;
+        if (flat)
+          e = launch_pdl(amax_flat_kernel<Tin>, dim3((unsigned)(num_sms * 4)), blk, st, p,
+                         reinterpret_cast<uint32_t*>(amax_dev));
+        else
+          e = launch_pdl(amax_tensor_kernel<Tin>, dim3((unsigned)nb), blk, st, p, reinterpret_cast<uint32_t*>(amax_dev));
         if (e != cudaSuccess) return e;
       }
       if (phase == LOKA_PHASE_FULL || phase == LOKA_PHASE_CAST_WITH_AMAX) {

@@ -54,6 +54,28 @@ template <> struct QtIn<__nv_bfloat16> {
   static constexpr int kElemsPer16B = 8;
 };
 
+// cast a row held in smem into the staging row: 4 chunks of 16 B per lane loaded before any is
+// converted (the smem latency of one chunk hides behind the others' conversion)
+template <typename Tin, int FMT>
+LOKA_DEVINL void qt_cast_row(uint32_t src, uint32_t dsts, int nchunks, int lane, float r) {
+  int c = lane;
+  for (; c + 96 < nchunks; c += 128) {
+    uint4 w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) w[u] = QtIn<Tin>::ld(src + 16u * (c + 32 * u));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint2 code = QtIn<Tin>::template cast<FMT>(w[u], r);
+      asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(dsts + 8u * (c + 32 * u)), "r"(code.x), "r"(code.y)
+                   : "memory");
+    }
+  }
+  for (; c < nchunks; c += 32) {
+    const uint2 code = QtIn<Tin>::template cast<FMT>(QtIn<Tin>::ld(src + 16u * c), r);
+    asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(dsts + 8u * c), "r"(code.x), "r"(code.y) : "memory");
+  }
+}
+
 // Work items are groups of 8 consecutive rows of one tensor of the QuantGroup (a single tensor
 // is a group of one); item gg belongs to tensor t with rgs[t] <= gg < rgs[t+1] (row-group prefix).
 template <int R>
@@ -163,15 +185,39 @@ __global__ void __launch_bounds__(32 * (kQtRows + 1), 1)
         if (p.scales) p.scales[row] = sc;
         if (p.scales_t) p.scales_t[row] = sc;
       }
-      for (int c = lane; c < nchunks; c += 32) {
-        const uint2 code = QtIn<Tin>::template cast<FMT>(QtIn<Tin>::ld(src + 16u * c), r);
-        asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(dsts + 8u * c), "r"(code.x), "r"(code.y) : "memory");
+      qt_cast_row<Tin, FMT>(src, dsts, nchunks, lane, r);
+    } else if constexpr (GRAN == LOKA_GRAN_BLK_1x128) {
+      // 1x128 granules: chunk c (8 elements) lies in block c / 16, so in each 32-chunk step the two
+      // half-warps hold one block each: half-warp max reduction, then scale and cast in registers
+      const int nblk = (int)((p.cols + 127) / 128);
+      for (int c0 = 0; c0 < nchunks; c0 += 128) {
+        uint4 w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + 32 * u + lane;
+          w[u] = c < nchunks ? QtIn<Tin>::ld(src + 16u * c) : make_uint4(0u, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + 32 * u + lane;
+          if (c0 + 32 * u >= nchunks) break;  // (uniform over the warp)
+          uint32_t am = QtIn<Tin>::amax(w[u]);
+#pragma unroll
+          for (int o = 8; o >= 1; o >>= 1) am = max(am, __shfl_xor_sync(0xFFFFFFFFu, am, o));
+          if (am >= 0x7F800000u && (lane & 15) == 0 && p.status) atomicOr(p.status, LOKA_DEVSTATUS_NONFINITE);
+          float sc, r;
+          scales_from_amax<FMT, SF>(__uint_as_float(am), sc, r);
+          const int blk = (c0 + 32 * u) / 16 + (lane >> 4);
+          if ((lane & 15) == 0 && blk < nblk && p.scales) p.scales[row * nblk + blk] = sc;
+          if (c < nchunks) {
+            const uint2 code = QtIn<Tin>::template cast<FMT>(w[u], r);
+            asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(dsts + 8u * c), "r"(code.x), "r"(code.y)
+                         : "memory");
+          }
+        }
       }
     } else {  // TENSOR cast with the pre-computed amax
-      for (int c = lane; c < nchunks; c += 32) {
-        const uint2 code = QtIn<Tin>::template cast<FMT>(QtIn<Tin>::ld(src + 16u * c), r_tensor);
-        asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(dsts + 8u * c), "r"(code.x), "r"(code.y) : "memory");
-      }
+      qt_cast_row<Tin, FMT>(src, dsts, nchunks, lane, r_tensor);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[s]);  // input row consumed
@@ -207,7 +253,8 @@ size_t quant_tma_smem(int64_t cols, int in_elem) {
 
 bool quant_tma_eligible(const QuantParams& p, bool in_bf16, int gran) {
   if (!in_bf16 || !p.q || p.qt || p.rows <= 0) return false;
-  // (BLK_1x128 measured slower here than the register-resident kernel: ROW and TENSOR only)
+  // (BLK_1x128 runs here too, but measured slower than quantize.cu's register-resident kernel at
+  // 262144 x 4096: 1.18 vs 0.81 ms (profiles/r02g_quantize_262k.json) — ROW and TENSOR only)
   if (gran != LOKA_GRAN_ROW && gran != LOKA_GRAN_TENSOR) return false;
   if (p.cols % 16 || p.cols * 2 > kQtMaxRowBytes) return false;
   if ((p.ldx * 2) % 16 || p.ldq % 16) return false;
@@ -256,7 +303,8 @@ cudaError_t launch_quantize_tma_group(const QuantGroup& grp, int64_t max_cols, i
   if (fmt == F && scale_fmt == S && gran == G) return launch_qt<F, S, G>(grp, max_cols, amax_dev, num_sms, st);
 #define LOKA_QT_G(F, S)                     \
   LOKA_QT(F, S, LOKA_GRAN_ROW)              \
-  LOKA_QT(F, S, LOKA_GRAN_TENSOR)
+  LOKA_QT(F, S, LOKA_GRAN_TENSOR)           \
+  LOKA_QT(F, S, LOKA_GRAN_BLK_1x128)
   LOKA_QT_G(LOKA_E4M3, LOKA_SCALE_F32)
   LOKA_QT_G(LOKA_E4M3, LOKA_SCALE_UE8M0)
   LOKA_QT_G(LOKA_E5M2, LOKA_SCALE_F32)

@@ -43,6 +43,9 @@ def main():
              ("tensor", "tensor", False), ("col", "col", False), ("blk_128x1", "blk_128x1", False),
              ("row+transpose", "row", True), ("tensor+transpose", "tensor", True),
              ("blk_128x1+transpose", "blk_128x1", True)]
+    from bench import ClockSampler
+    clk = ClockSampler(torch.cuda.current_device())
+    clk.__enter__()
     with torch.cuda.stream(stream):
         for name, gran, tr in cases:
             s = torch.empty(lk.scale_shape(R, Cc, gran), dtype=torch.float32, device=dev)
@@ -60,6 +63,20 @@ def main():
             gbs = nbytes / (ms * 1e-3) / 1e9
             out["kernels"][name] = {"ms": round(ms, 4), "algorithmic_bytes": nbytes, "gbs": round(gbs, 1),
                                     "frac_of_hbm": round(gbs / hbm, 3)}
+        # the tensorwise recipe's two phases separately (split-phase for the DP all-reduce)
+        amax = torch.zeros(1, dtype=torch.float32, device=dev)
+        s1 = torch.empty(1, dtype=torch.float32, device=dev)
+        for name, ph, nbytes in (("tensor_amax_pass", "amax", R * Cc * 2), ("tensor_cast_pass", "cast", R * Cc * 3)):
+            fn = (lambda ph=ph: lk.loka_quantize(x, "e4m3", "tensor", phase=ph, amax=amax, out=q, scales=s1,
+                                                 want_q=ph != "amax"))
+            g = capture(fn, stream)
+            t = time_steps(g.replay, a.steps, 3, flush, stream)
+            ms = sum(t) / len(t)
+            gbs = nbytes / (ms * 1e-3) / 1e9
+            out["kernels"][name] = {"ms": round(ms, 4), "algorithmic_bytes": nbytes, "gbs": round(gbs, 1),
+                                    "frac_of_hbm": round(gbs / hbm, 3)}
+    clk.__exit__()
+    out["clocks"] = clk.summary()
     print(json.dumps(out))
     if a.out:
         open(a.out, "w").write(json.dumps(out, indent=1))
