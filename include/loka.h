@@ -326,6 +326,18 @@ typedef struct loka_probe_stats {
 LOKA_API loka_status loka_probe_error(int32_t L, const loka_probe_pair* pairs, double floor_rel,
                              loka_probe_stats* stats_dev, void* ws, size_t ws_bytes, loka_stream_t stream);
 LOKA_API size_t loka_probe_workspace_size(int32_t L, const loka_probe_pair* pairs);
+/* Data-parallel probe (SURVEY.md §8(e) "probe sums and max values can be all-reduced"): each rank
+ * holds row shards of the layers' pairs.  global_sum_count_dev (DEVICE, [L][2] doubles) holds each
+ * layer's (sum |ref|, element count) summed over all ranks (the caller's all-reduce of the local
+ * loka_probe_error results' sum_abs_ref and count), so every shard uses the floor
+ * f = floor_rel * sum / count of the whole layer; the per-rank results then combine exactly with
+ * loka_probe_merge into the statistic of the concatenated tensor.  Same workspace as above.      */
+LOKA_API loka_status loka_probe_error_global(int32_t L, const loka_probe_pair* pairs, double floor_rel,
+                                            const double* global_sum_count_dev, loka_probe_stats* stats_dev,
+                                            void* ws, size_t ws_bytes, loka_stream_t stream);
+/* Host: combine R ranks' stats of L layers, parts[r * L + l] -> out[l] (counts, floored counts and
+ * sum |ref| add; max_rel max; mere = sum mere_r count_r / sum count_r).                         */
+LOKA_API loka_status loka_probe_merge(int32_t R, int32_t L, const loka_probe_stats* parts, loka_probe_stats* out);
 
 /* ---- NEXT-2: LoKA Probe online input tracker (batched Welford) ------------
  * Running summaries of one layer's input distribution, feature dimension only (the batch rows are

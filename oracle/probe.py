@@ -20,7 +20,10 @@ import math
 import numpy as np
 
 
-def mere_stats(out, ref, floor_rel: float = 1e-6) -> dict:
+def mere_stats(out, ref, floor_rel: float = 1e-6, floor: float | None = None) -> dict:
+    """``floor`` (optional) is the absolute floor f of a row shard of a larger tensor: D10 applied
+    to the whole tensor (f = floor_rel * mean |ref| over every shard), as the data-parallel probe
+    uses it; by default f is this array's own floor_rel * mean |ref|."""
     out = np.asarray(out, np.float64)
     ref = np.asarray(ref, np.float64)
     if out.shape != ref.shape:
@@ -30,7 +33,7 @@ def mere_stats(out, ref, floor_rel: float = 1e-6) -> dict:
         return dict(mere=0.0, max_rel=0.0, sum_abs_ref=0.0, count=0, n_floored=0)
     aref = np.abs(ref).reshape(-1)
     sum_abs_ref = math.fsum(aref)
-    f = floor_rel * (sum_abs_ref / n)
+    f = floor_rel * (sum_abs_ref / n) if floor is None else float(floor)
     denom = np.maximum(aref, f)
     n_floored = int(np.count_nonzero(aref < f))
     rel = np.abs(out.reshape(-1) - ref.reshape(-1))

@@ -113,6 +113,9 @@ _sig = {
     "loka_probe_error": ([C.c_int32, _P(loka_probe_pair), C.c_double, C.c_void_p, C.c_void_p, C.c_size_t,
                           C.c_void_p], C.c_int),
     "loka_probe_workspace_size": ([C.c_int32, _P(loka_probe_pair)], C.c_size_t),
+    "loka_probe_error_global": ([C.c_int32, _P(loka_probe_pair), C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.c_size_t, C.c_void_p], C.c_int),
+    "loka_probe_merge": ([C.c_int32, C.c_int32, _P(loka_probe_stats), _P(loka_probe_stats)], C.c_int),
     "loka_dispatch_select": ([_P(loka_candidate), C.c_int32, C.c_double, C.c_double, C.c_double, _P(C.c_int32)],
                              C.c_int),
     "loka_quantize_nvfp4": ([_P(loka_tensor), _P(loka_nvfp4_tensor), C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
@@ -380,10 +383,11 @@ def loka_grouped_fp8_linear(args_list, stream=None, ws=None):
                                         _stream(stream)), "loka_grouped_fp8_linear")
 
 
-def loka_probe_error(pairs, floor_rel: float = 1e-6, stream=None, stats=None, ws=None):
+def loka_probe_error(pairs, floor_rel: float = 1e-6, stream=None, stats=None, ws=None, global_sum_count=None):
     """a7.  pairs: [(out, ref)] device tensors (f32/bf16, 2-D).  Returns a float64 tensor [L, 5]
     viewing the device loka_probe_stats array (mere, max_rel, sum_abs_ref, count*, n_floored*)
-    where the last two are int64 bit patterns; use probe_stats_to_dicts()."""
+    where the last two are int64 bit patterns; use probe_stats_to_dicts().  global_sum_count: device
+    float64 [L, 2] (sum |ref|, count) of the whole sharded layers -> loka_probe_error_global."""
     L = len(pairs)
     arr = (loka_probe_pair * L)()
     for i, (o, r) in enumerate(pairs):
@@ -395,9 +399,30 @@ def loka_probe_error(pairs, floor_rel: float = 1e-6, stream=None, stats=None, ws
     nws = _lib.loka_probe_workspace_size(L, arr)
     if ws is None or ws.numel() < nws:
         ws = torch.empty(nws, dtype=torch.uint8, device=dev)
-    _check(_lib.loka_probe_error(L, arr, floor_rel, C.c_void_p(stats.data_ptr()), C.c_void_p(ws.data_ptr()), nws,
-                                 _stream(stream)), "loka_probe_error")
+    if global_sum_count is not None:
+        g = global_sum_count.to(device=dev, dtype=torch.float64).contiguous()
+        _check(_lib.loka_probe_error_global(L, arr, floor_rel, C.c_void_p(g.data_ptr()), C.c_void_p(stats.data_ptr()),
+                                            C.c_void_p(ws.data_ptr()), nws, _stream(stream)), "loka_probe_error_global")
+    else:
+        _check(_lib.loka_probe_error(L, arr, floor_rel, C.c_void_p(stats.data_ptr()), C.c_void_p(ws.data_ptr()), nws,
+                                     _stream(stream)), "loka_probe_error")
     return stats
+
+
+def probe_merge(per_rank):
+    """Combine per-rank probe statistics (lists of dicts, one list per rank, same layers) with the
+    library's host loka_probe_merge."""
+    R = len(per_rank)
+    L = len(per_rank[0]) if R else 0
+    parts = (loka_probe_stats * max(1, R * L))()
+    for r, lst in enumerate(per_rank):
+        for l, st in enumerate(lst):
+            parts[r * L + l] = loka_probe_stats(st["mere"], st["max_rel"], st["sum_abs_ref"], int(st["count"]),
+                                                int(st["n_floored"]))
+    out = (loka_probe_stats * max(1, L))()
+    _check(_lib.loka_probe_merge(R, L, parts, out), "loka_probe_merge")
+    return [dict(mere=out[l].mere, max_rel=out[l].max_rel, sum_abs_ref=out[l].sum_abs_ref, count=int(out[l].count),
+                 n_floored=int(out[l].n_floored)) for l in range(L)]
 
 
 def probe_stats_to_dicts(stats: torch.Tensor):

@@ -184,7 +184,8 @@ loka_status loka_quantize(const loka_tensor* x, loka_tensor* q, loka_tensor* qt,
     if (qt->dtype != q->dtype || qt->rows != x->cols || qt->cols != x->rows ||
         (qt->gran != transpose_gran(q->gran) && !dual) || qt->scale_fmt != q->scale_fmt)
       return LOKA_ERR_SHAPE;
-    if (!qt->data || qt->ld < qt->cols) return LOKA_ERR_INVALID_ARG;
+    // the tiled path writes the transposed codes with 8-byte stores: same rules as q
+    if (!qt->data || qt->ld < qt->cols || !aligned16(qt->data) || qt->ld % 16) return LOKA_ERR_INVALID_ARG;
   }
   // the tiled cast(-transpose) path serves column-spanning granules and transposed copies
   const bool tiled = (qt != nullptr || q->gran == LOKA_GRAN_COL || q->gran == LOKA_GRAN_BLK_128x1 ||
@@ -1562,8 +1563,44 @@ loka_status loka_probe_sample_weight(const float* mean, const float* l_u, const 
   return launch_gemm_f32(g, false, false, s) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
 }
 
+static loka_status probe_error_impl(int32_t L, const loka_probe_pair* pairs, double floor_rel, const double* gsum,
+                                    loka_probe_stats* stats_dev, void* ws, size_t ws_bytes, loka_stream_t stream);
 loka_status loka_probe_error(int32_t L, const loka_probe_pair* pairs, double floor_rel, loka_probe_stats* stats_dev,
                              void* ws, size_t ws_bytes, loka_stream_t stream) {
+  return probe_error_impl(L, pairs, floor_rel, nullptr, stats_dev, ws, ws_bytes, stream);
+}
+loka_status loka_probe_error_global(int32_t L, const loka_probe_pair* pairs, double floor_rel,
+                                    const double* global_sum_count_dev, loka_probe_stats* stats_dev, void* ws,
+                                    size_t ws_bytes, loka_stream_t stream) {
+  if (!global_sum_count_dev) return LOKA_ERR_INVALID_ARG;
+  return probe_error_impl(L, pairs, floor_rel, global_sum_count_dev, stats_dev, ws, ws_bytes, stream);
+}
+// Combine R shards' statistics of L layers (host arrays parts[r * L + l]) into out[l]: counts,
+// floored counts and sum |ref| add, max_rel is the max, MERE = sum_r mere_r count_r / sum_r count_r
+// (the per-element mean over the union of the shards; exact when the shards used the same floor).
+loka_status loka_probe_merge(int32_t R, int32_t L, const loka_probe_stats* parts, loka_probe_stats* out) {
+  if (R < 0 || L < 0 || ((R > 0 && L > 0) && (!parts || !out))) return LOKA_ERR_INVALID_ARG;
+  for (int32_t l = 0; l < L; ++l) {
+    double s = 0.0, mx = 0.0, sabs = 0.0;
+    int64_t cnt = 0, nfl = 0;
+    for (int32_t r = 0; r < R; ++r) {
+      const loka_probe_stats& q = parts[(size_t)r * L + l];
+      s += q.mere * (double)q.count;
+      mx = q.max_rel > mx ? q.max_rel : mx;
+      sabs += q.sum_abs_ref;
+      cnt += q.count;
+      nfl += q.n_floored;
+    }
+    out[l].mere = cnt > 0 ? s / (double)cnt : 0.0;
+    out[l].max_rel = mx;
+    out[l].sum_abs_ref = sabs;
+    out[l].count = cnt;
+    out[l].n_floored = nfl;
+  }
+  return LOKA_OK;
+}
+static loka_status probe_error_impl(int32_t L, const loka_probe_pair* pairs, double floor_rel, const double* gsum,
+                                    loka_probe_stats* stats_dev, void* ws, size_t ws_bytes, loka_stream_t stream) {
   if (L < 0 || (L > 0 && (!pairs || !stats_dev))) return LOKA_ERR_INVALID_ARG;
   if (L == 0) return LOKA_OK;
   if (!ws || ws_bytes < loka_probe_workspace_size(L, pairs) || !aligned16(ws)) return LOKA_ERR_WORKSPACE;
@@ -1595,7 +1632,7 @@ loka_status loka_probe_error(int32_t L, const loka_probe_pair* pairs, double flo
   loka_status st = check_device();
   if (st != LOKA_OK) return st;
   cudaError_t e = launch_probe(layers.data(), L, 0, floor_rel, stats_dev, reinterpret_cast<double*>(ws),
-                               probe_nblk(L), reinterpret_cast<cudaStream_t>(stream));
+                               probe_nblk(L), reinterpret_cast<cudaStream_t>(stream), gsum);
   return e == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;
 }
 
@@ -1604,6 +1641,9 @@ loka_status loka_probe_error(int32_t L, const loka_probe_pair* pairs, double flo
 loka_status loka_dispatch_select(const loka_candidate* c, int32_t n, double baseline_time_us, double mere_budget,
                                  double min_speedup, int32_t* chosen) {
   if (!chosen || n < 0 || (n > 0 && !c)) return LOKA_ERR_INVALID_ARG;
+  // one decision per (layer, direction): candidates of different directions are an error
+  for (int32_t i = 1; i < n; ++i)
+    if (c[i].dir != c[0].dir) return LOKA_ERR_INVALID_ARG;
   int32_t best = -1;
   for (int32_t i = 0; i < n; ++i) {
     const double t = c[i].time_us;

@@ -250,11 +250,9 @@ __global__ void __launch_bounds__(kWThreads, 1)
 
 cudaError_t launch_linear_bw(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, const BwParams& p,
                              cudaStream_t st) {
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(linear_bw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWSmem);
+  {
+    cudaError_t e = ensure_func_attrs(reinterpret_cast<const void*>(linear_bw_kernel), kWSmem);
     if (e != cudaSuccess) return e;
-    attr_done = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)((p.M + 127) / 128), (unsigned)((p.N + kWBN - 1) / kWBN), 1);

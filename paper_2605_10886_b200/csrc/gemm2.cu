@@ -589,12 +589,9 @@ __global__ void __launch_bounds__(k2Threads, 1) mx_pair_kernel(const __grid_cons
 
 template <bool NV>
 static cudaError_t launch_mx_pair_t(const MxPairParams& mp, int num_sms, cudaStream_t st) {
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e =
-        cudaFuncSetAttribute(mx_pair_kernel<NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, MxCfg<NV>::kSmem);
+  {
+    cudaError_t e = ensure_func_attrs(reinterpret_cast<const void*>(mx_pair_kernel<NV>), MxCfg<NV>::kSmem);
     if (e != cudaSuccess) return e;
-    attr_done = true;
   }
   const int pairs = mp.tiles < num_sms / 2 ? mp.tiles : num_sms / 2;
   cudaLaunchConfig_t cfg = {};
@@ -674,12 +671,9 @@ cudaError_t launch_splitk_reduce(const GroupDesc& d, const float* part, void* y,
 
 template <bool BF16IN, bool WIDE, bool SPLIT>
 static cudaError_t launch_grouped2_t(const GroupedParams& gp, int num_sms, cudaStream_t st) {
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(grouped2_kernel<BF16IN, WIDE, SPLIT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, G2<WIDE>::kSmem);
+  {
+    cudaError_t e = ensure_func_attrs(reinterpret_cast<const void*>(grouped2_kernel<BF16IN, WIDE, SPLIT>), G2<WIDE>::kSmem);
     if (e != cudaSuccess) return e;
-    attr_done = true;
   }
   const int T = gp.tile_start[gp.G];
   const int pairs = T < num_sms / 2 ? T : num_sms / 2;

@@ -212,11 +212,9 @@ __global__ void __launch_bounds__(kGThreads, 1) grouped_linear_kernel(const __gr
 }
 
 cudaError_t launch_grouped(const GroupedParams& gp, int num_sms, cudaStream_t st) {
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(grouped_linear_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGSmem);
+  {
+    cudaError_t e = ensure_func_attrs(reinterpret_cast<const void*>(grouped_linear_kernel), kGSmem);
     if (e != cudaSuccess) return e;
-    attr_done = true;
   }
   const int T = gp.tile_start[gp.G];
   cudaLaunchConfig_t cfg = {};

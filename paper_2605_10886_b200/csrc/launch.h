@@ -8,6 +8,9 @@
 namespace loka {
 
 void note_launch(int n = 1);
+// set a kernel's max dynamic smem (and optionally non-portable cluster size) once per (function,
+// device), thread-safe (attrs.cu)
+cudaError_t ensure_func_attrs(const void* func, int smem_bytes, bool nonportable_cluster = false);
 long long debug_hang_info(unsigned long long* info, int reset);
 long long debug_trace(int enable, unsigned long long* out, long long n);  // process-wide launch counter (loka_launch_count)
 
@@ -266,8 +269,9 @@ struct ProbeLayer {
   int64_t M, N, ld_out, ld_ref;
   int32_t out_vec, ref_vec;  // rows 16B-aligned: vector loads allowed
 };
+// gsum (nullable, device [L][2]): the global (sum |ref|, count) of each layer for the floor
 cudaError_t launch_probe(const ProbeLayer* layers_dev, int L, int64_t max_elems, double floor_rel,
-                         void* stats_dev, double* partials, int nblk, cudaStream_t st);
+                         void* stats_dev, double* partials, int nblk, cudaStream_t st, const double* gsum = nullptr);
 
 // ---- NEXT-3 (linalg.cu): FP32 linear algebra for the matrix-normal tracker and the sampling ----
 struct GemmF32Params {  // C = alpha op(A) op(B) + beta Cin + bias[n]  (see linalg.cu)

@@ -261,13 +261,7 @@ __global__ void __launch_bounds__(128) panel_trsm_kernel(float* b, int64_t sr, i
 
 constexpr int kTrsmSmem = (kNB * (kNB + 1) + kNB + 128 * (kNB + 1)) * 4;
 static cudaError_t trsm_attr() {
-  static bool done = false;
-  if (!done) {
-    cudaError_t e = cudaFuncSetAttribute(panel_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmem);
-    if (e != cudaSuccess) return e;
-    done = true;
-  }
-  return cudaSuccess;
+  return ensure_func_attrs(reinterpret_cast<const void*>(panel_trsm_kernel), kTrsmSmem);
 }
 
 __global__ void zero_upper_kernel(float* a, int64_t lda, int64_t n) {

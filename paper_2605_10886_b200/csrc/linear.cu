@@ -772,17 +772,10 @@ template <int BN, int MX, int MAXC = kMaxCluster>
 static cudaError_t launch_bn(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& ty, const LinearParams& p,
                              cudaStream_t st) {
   using C = LinCfg<BN, MX, MAXC>;
-  static bool attr_done = false;  // idempotent; racing threads set the same value
-  if (!attr_done) {
-    if (MAXC > 8) {
-      cudaError_t e = cudaFuncSetAttribute(linear_norm_kernel<BN, MX, MAXC>,
-                                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      if (e != cudaSuccess) return e;
-    }
-    cudaError_t e = cudaFuncSetAttribute(linear_norm_kernel<BN, MX, MAXC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::kSmemBytes);
+  {
+    cudaError_t e = ensure_func_attrs(reinterpret_cast<const void*>(linear_norm_kernel<BN, MX, MAXC>), C::kSmemBytes,
+                                      MAXC > 8);
     if (e != cudaSuccess) return e;
-    attr_done = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)((p.M + 127) / 128), (unsigned)((p.N + BN - 1) / BN), 1);

@@ -603,15 +603,9 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
 
 template <int TN, int NORM>
 static cudaError_t launch_pn(const PairNormParams& p, int pairs, cudaStream_t st) {
-  static int attr_done[64] = {0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-  if (!attr_done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(pair_norm_kernel<TN, NORM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         PnCfg<TN>::kSmem);
+  {
+    cudaError_t e = ensure_func_attrs(reinterpret_cast<const void*>(pair_norm_kernel<TN, NORM>), PnCfg<TN>::kSmem);
     if (e != cudaSuccess) return e;
-    attr_done[dev] = 1;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(2 * pairs), 1, 1);

@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(256) probe_p1(const __grid_constant__ ProbeBat
 
 __global__ void __launch_bounds__(256) probe_p2(const __grid_constant__ ProbeBatch b, const double* part1,
                                                 double* part2, float* partmax, long long* partfl, int nblk,
-                                                double floor_rel) {
+                                                double floor_rel, const double* gsum) {
   __shared__ double red[8];
   __shared__ long long redl[8];
   __shared__ float redf[8];
@@ -132,7 +132,10 @@ __global__ void __launch_bounds__(256) probe_p2(const __grid_constant__ ProbeBat
   for (int i = threadIdx.x; i < nblk; i += blockDim.x) sabs += part1[(int64_t)blockIdx.y * nblk + i];
   sabs = block_sum(sabs, red);
   const int64_t count = L.M * L.N;
-  const double f = count > 0 ? floor_rel * (sabs / (double)count) : 0.0;
+  double f = count > 0 ? floor_rel * (sabs / (double)count) : 0.0;
+  // data-parallel form: the floor from the global sum |ref| and count (all-reduced over the ranks
+  // that hold shards of this layer's pair), so every shard is measured against the same f
+  if (gsum) f = gsum[2 * blockIdx.y + 1] > 0.0 ? floor_rel * (gsum[2 * blockIdx.y] / gsum[2 * blockIdx.y + 1]) : 0.0;
   const float f32 = (float)f;  // used only as the denominator
   // floored <=> |r| < f (FP64).  For an FP32 |r| that is |r| < t with t = f rounded UP to FP32
   // (no FP32 value lies in [f, t)), so the decision stays exact with an FP32 compare.
@@ -208,10 +211,12 @@ __global__ void __launch_bounds__(256) probe_p2(const __grid_constant__ ProbeBat
           nfl32 += floored ? 1u : 0u;
           const float den = floored ? f32 : ar;
           const float d = fabsf(__fsub_rn(o[i], r[i]));
-          // den >= f is a normal FP32 number: the fast division (<= 2 ulp) is far inside the
-          // statistic's 1e-5 tolerance (SV §8(c) parity matrix)
+          // the fast division (<= 2 ulp, far inside the statistic's 1e-5 tolerance) is exact enough
+          // only for a denominator in [2^-126, 2^126]; a floor f = 1e-6 mean|ref| can be subnormal or
+          // the refs huge, so outside that range the IEEE division is taken
           float rel;
-          if (den > 0.f) rel = __fdividef(d, den);
+          if (den >= 1.17549435e-38f && den <= 8.5070592e37f) rel = __fdividef(d, den);
+          else if (den > 0.f) rel = __fdiv_rn(d, den);
           else rel = d > 0.f ? INFINITY : 0.f;
           part += rel;
           mx = fmaxf(mx, rel);
@@ -278,7 +283,7 @@ __global__ void __launch_bounds__(256) probe_p3(const __grid_constant__ ProbeBat
 }
 
 cudaError_t launch_probe(const ProbeLayer* layers, int L, int64_t /*max_elems*/, double floor_rel, void* stats_dev,
-                         double* ws, int nblk, cudaStream_t st) {
+                         double* ws, int nblk, cudaStream_t st, const double* gsum) {
   // ws layout per batch of <= 64 layers: part1 [64*nblk] f64 | part2 [64*nblk] f64 | partfl [64*nblk] i64
   //                                      | partmax [64*nblk] f32
   for (int l0 = 0; l0 < L; l0 += kMaxProbeLayers) {
@@ -291,7 +296,8 @@ cudaError_t launch_probe(const ProbeLayer* layers, int L, int64_t /*max_elems*/,
     long long* partfl = reinterpret_cast<long long*>(ws + 2 * n);
     float* partmax = reinterpret_cast<float*>(ws + 3 * n);
     probe_p1<<<dim3((unsigned)nblk, (unsigned)nl), 256, 0, st>>>(b, part1, nblk);
-    probe_p2<<<dim3((unsigned)nblk, (unsigned)nl), 256, 0, st>>>(b, part1, part2, partmax, partfl, nblk, floor_rel);
+    probe_p2<<<dim3((unsigned)nblk, (unsigned)nl), 256, 0, st>>>(b, part1, part2, partmax, partfl, nblk, floor_rel,
+                                                                 gsum ? gsum + 2 * l0 : nullptr);
     probe_p3<<<dim3((unsigned)nl), 256, 0, st>>>(b, part1, part2, partmax, partfl, nblk,
                                                 reinterpret_cast<ProbeStatsDev*>(stats_dev) + l0);
     note_launch(3);

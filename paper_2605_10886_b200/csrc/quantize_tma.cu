@@ -268,11 +268,9 @@ static cudaError_t launch_qt_r(const QuantGroup& grp, int64_t max_cols, const fl
   auto kern = quant_tma_kernel<__nv_bfloat16, FMT, SF, GRAN, kQtRows>;
   const size_t smem = quant_tma_smem(max_cols, 2);
   const int nstages = quant_tma_stages(max_cols, 2);
-  static int attr_bytes = 0;  // per instantiation; the attribute only needs to grow
-  if ((int)smem > attr_bytes) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  {
+    cudaError_t e = ensure_func_attrs(reinterpret_cast<const void*>(kern), 227 * 1024);
     if (e != cudaSuccess) return e;
-    attr_bytes = 227 * 1024;
   }
   int64_t ngroups = 0;
   for (int t = 0; t < grp.G; ++t) ngroups += (grp.p[t].rows + kQtRows - 1) / kQtRows;

@@ -736,11 +736,9 @@ cudaError_t launch_stack(const StackParams& p, cudaStream_t st) {
               : inst == 3 ? stack_kernel<true, 0, -1>
               : inst == 4 ? stack_kernel<true, 4, kStackGatherL2>
                           : stack_kernel<true, 4, kStackGatherL2StAsync>;
-  static bool attr_done[6] = {false, false, false, false, false, false};
-  if (!attr_done[inst]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSSmem);
+  {
+    cudaError_t e = ensure_func_attrs(reinterpret_cast<const void*>(kern), kSSmem);
     if (e != cudaSuccess) return e;
-    attr_done[inst] = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)((p.M + 127) / 128), (unsigned)p.C, 1);

@@ -57,25 +57,37 @@ def quantize_tensorwise_sharded(x_local: torch.Tensor, fmt: str = "e4m3", scale_
     return q, s, amax
 
 
-def reduce_probe_stats(stats_list, group=None):
-    """Combine per-rank probe statistics of one layer: counts and sums add,
-    maxima max; MERE = sum of per-element relative errors / total count."""
-    keys = ("mere", "max_rel", "sum_abs_ref", "count", "n_floored")
+def probe_error_sharded(pairs, floor_rel: float = 1e-6, group=None, stream=None, probe_fn=None, merge_fn=None):
+    """LoKA Probe (a7) over row-sharded layers ("probe sums and max values can be
+    all-reduced"), equal to the single-device statistic of the concatenated tensors:
+
+      pass 1  every rank: loka_probe_error on its shards -> per layer (sum |ref|, count);
+      reduce  all_reduce(SUM) of the [L, 2] (sum |ref|, count) array: the layer's global floor
+              f = floor_rel * sum / count (DESIGN.md D10 applied to the whole tensor, not the shard);
+      pass 2  every rank: loka_probe_error_global with that floor;
+      merge   all_gather of the per-rank stats, combined by libloka's loka_probe_merge (host C).
+
+    Returns a list of dicts (probe_stats_to_dicts).  probe_fn(pairs, floor_rel, gsum_or_None) -> list
+    of dicts and merge_fn(list of per-rank lists) -> list of dicts are injectable so the protocol runs
+    under CPU gloo tests; the defaults are libloka on the current CUDA stream."""
+    lk = _lk()
+    if probe_fn is None:
+        def probe_fn(prs, fr, gsum):
+            return lk.probe_stats_to_dicts(lk.loka_probe_error(prs, fr, stream=stream, global_sum_count=gsum))
+    if merge_fn is None:
+        merge_fn = lk.probe_merge
+    local = probe_fn(pairs, floor_rel, None)
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
-        return stats_list
-    out = []
-    for st in stats_list:
-        t = torch.tensor([st["mere"] * st["count"], st["sum_abs_ref"], float(st["count"]), float(st["n_floored"])],
-                         dtype=torch.float64)
-        m = torch.tensor([st["max_rel"]], dtype=torch.float64)
-        dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else t.device
-        t, m = t.to(dev), m.to(dev)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-        dist.all_reduce(m, op=dist.ReduceOp.MAX, group=group)
-        t, m = t.cpu(), m.cpu()
-        cnt = int(t[2])
-        out.append(dict(zip(keys, (float(t[0]) / cnt if cnt else 0.0, float(m[0]), float(t[1]), cnt, int(t[3])))))
-    return out
+        return local
+    nccl = dist.get_backend(group) == "nccl"
+    dev = torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
+    gsum = torch.tensor([[st["sum_abs_ref"], float(st["count"])] for st in local], dtype=torch.float64, device=dev)
+    dist.all_reduce(gsum, op=dist.ReduceOp.SUM, group=group)
+    mine = probe_fn(pairs, floor_rel, gsum)
+    world = dist.get_world_size(group)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, mine, group=group)
+    return merge_fn(gathered)
 
 
 class QuantizedGradReducer:

@@ -28,7 +28,7 @@ def declared_symbols():
 
 def test_every_declared_symbol_is_exported(lk):
     syms = declared_symbols()
-    assert len(syms) == 35, syms
+    assert len(syms) == 37, syms
     out = subprocess.run(["nm", "-D", "--defined-only", lk.LIB_PATH], capture_output=True, text=True).stdout
     exported = set(re.findall(r" T (loka_\w+)", out))
     assert set(syms) <= exported, set(syms) - exported
@@ -114,3 +114,36 @@ def test_shape_validation_is_host_side(lk):
     assert lk._lib.loka_fp8_linear_norm(C.byref(a), None, 0, None) == lk.ERR_SHAPE
     a.b.rows = 299
     assert lk._lib.loka_fp8_linear_norm(C.byref(a), None, 0, None) == lk.ERR_SHAPE
+
+
+def test_transposed_copy_alignment_is_validated(lk):
+    """a transposed copy whose rows are not 16-byte aligned (ld = rows = 100) or
+    whose base is misaligned is refused with LOKA_ERR_INVALID_ARG before any device work."""
+    fake = 1 << 20
+    x = lk.loka_tensor(fake, lk.BF16, 100, 64, 64, None, 1, 0)
+    q = lk.loka_tensor(fake, lk.E4M3, 100, 64, 64, fake, 1, 0)          # ROW granules
+    qt = lk.loka_tensor(fake, lk.E4M3, 64, 100, 100, fake, 2, 0)        # COL in the t-frame, ld % 16 != 0
+    assert lk._lib.loka_quantize(C.byref(x), C.byref(q), C.byref(qt), 0, None, None, None, 0, None) == lk.ERR_INVALID_ARG
+    qt = lk.loka_tensor(fake + 8, lk.E4M3, 64, 100, 112, fake, 2, 0)    # base not 16-byte aligned
+    assert lk._lib.loka_quantize(C.byref(x), C.byref(q), C.byref(qt), 0, None, None, None, 0, None) == lk.ERR_INVALID_ARG
+
+
+def test_dispatch_rejects_mixed_directions(lk):
+    """one decision per (layer, direction) — candidates of different
+    directions in one call are an argument error, not a silent cross-direction winner."""
+    cands = (lk.loka_candidate * 2)(lk.loka_candidate(b"a", 0, 0.1, 50.0), lk.loka_candidate(b"b", 1, 0.1, 40.0))
+    chosen = C.c_int32(-7)
+    assert lk._lib.loka_dispatch_select(cands, 2, 100.0, 0.2, 1.05, C.byref(chosen)) == lk.ERR_INVALID_ARG
+
+
+def test_probe_merge_host(lk):
+    """loka_probe_merge combines shards' stats: counts / floored counts / sum |ref| add, max_rel max,
+    MERE count-weighted (host function, no GPU)."""
+    a = [dict(mere=0.5, max_rel=2.0, sum_abs_ref=10.0, count=30, n_floored=1),
+         dict(mere=0.1, max_rel=1.0, sum_abs_ref=5.0, count=10, n_floored=0)]
+    b = [dict(mere=0.3, max_rel=3.0, sum_abs_ref=20.0, count=10, n_floored=2),
+         dict(mere=0.2, max_rel=0.5, sum_abs_ref=1.0, count=30, n_floored=4)]
+    m = lk.probe_merge([a, b])
+    assert m[0]["count"] == 40 and m[0]["n_floored"] == 3 and m[0]["max_rel"] == 3.0
+    assert abs(m[0]["mere"] - (0.5 * 30 + 0.3 * 10) / 40) < 1e-15 and m[0]["sum_abs_ref"] == 30.0
+    assert abs(m[1]["mere"] - (0.1 * 10 + 0.2 * 30) / 40) < 1e-15 and m[1]["n_floored"] == 4

@@ -44,11 +44,16 @@ def _worker(rank, world, port, total, cols, out_dir):
     # probe statistics of the shard (oracle), then the cross-rank reduction
     ref = x.double().numpy()
     out = oracle.quantize.dequantize(q.numpy(), s.numpy(), "e4m3", "tensor")
-    st = ldist.reduce_probe_stats([oracle.probe.mere_stats(out, ref)])[0]
+    # (the injected probe is the oracle; the merge is libloka's host loka_probe_merge)
+    def probe_fn(prs, fr, gsum):
+        return [oracle.probe.mere_stats(o, r, fr, None if gsum is None else fr * float(gsum[i, 0]) / float(gsum[i, 1]))
+                for i, (o, r) in enumerate(prs)]
+    st = ldist.probe_error_sharded([(out, ref)], probe_fn=probe_fn)[0]
     np.save(os.path.join(out_dir, f"q{rank}.npy"), q.numpy())
     np.save(os.path.join(out_dir, f"s{rank}.npy"), s.numpy())
     if rank == 0:
-        np.save(os.path.join(out_dir, "probe.npy"), np.array([st["mere"], st["max_rel"], st["count"]]))
+        np.save(os.path.join(out_dir, "probe.npy"), np.array([st["mere"], st["max_rel"], st["count"], st["n_floored"],
+                                                              st["sum_abs_ref"]]))
     dist.destroy_process_group()
 
 
@@ -70,6 +75,10 @@ def test_sharded_tensorwise_equals_single_device(world, total, tmp_path):
     st = oracle.probe.mere_stats(oracle.quantize.dequantize(qg, sg, "e4m3", "tensor"), x.double().numpy())
     pr = np.load(tmp_path / "probe.npy")
     assert int(pr[2]) == st["count"] and abs(pr[1] - st["max_rel"]) <= 1e-12 * st["max_rel"]
+    # exact two-pass protocol (global floor, then the merge): MERE, floored count and sum |ref| of
+    # the concatenated tensor (per-shard floors made the combination approximate)
+    assert abs(pr[0] - st["mere"]) <= 1e-12 * st["mere"]
+    assert int(pr[3]) == st["n_floored"] and abs(pr[4] - st["sum_abs_ref"]) <= 1e-12 * st["sum_abs_ref"]
 
 
 def test_shard_rows_partition():

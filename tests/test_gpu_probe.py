@@ -51,3 +51,24 @@ def test_probe_64_layers_one_call():
     stats = lk.probe_stats_to_dicts(lk.loka_probe_error(pairs))
     for (o, r), st in list(zip(pairs, stats))[::9]:
         _check(st, oracle.probe.mere_stats(f64(o), f64(r)))
+
+
+def test_sharded_probe_equals_whole_tensor():
+    """The data-parallel probe protocol (dist.probe_error_sharded's two passes) on one GPU with three
+    row shards of a layer: pass 1 per shard -> summed (sum |ref|, count) -> loka_probe_error_global per
+    shard -> loka_probe_merge: within 1e-5 of the oracle on the whole tensor, floored count exact."""
+    g = torch.Generator().manual_seed(4)
+    ref = torch.randn(900, 768, generator=g)
+    ref[::7] *= 1e-9  # rows that fall under the floor
+    out = ref * (1 + 0.02 * torch.randn(900, 768, generator=g))
+    o, r = out.to(torch.bfloat16).to(DEV), ref.to(torch.bfloat16).to(DEV)
+    shards = [(0, 300), (300, 611), (611, 900)]
+    first = [lk.probe_stats_to_dicts(lk.loka_probe_error([(o[a:b], r[a:b])]))[0] for a, b in shards]
+    gsum = torch.tensor([[sum(s["sum_abs_ref"] for s in first), float(sum(s["count"] for s in first))]],
+                        dtype=torch.float64, device=DEV)
+    per = [lk.probe_stats_to_dicts(lk.loka_probe_error([(o[a:b], r[a:b])], global_sum_count=gsum)) for a, b in shards]
+    m = lk.probe_merge(per)[0]
+    po = oracle.probe.mere_stats(o.cpu().double().numpy(), r.cpu().double().numpy())
+    assert m["count"] == po["count"] and m["n_floored"] == po["n_floored"] > 0
+    for k in ("mere", "max_rel", "sum_abs_ref"):
+        assert abs(m[k] - po[k]) <= 1e-5 * max(abs(po[k]), 1e-30), (k, m[k], po[k])

@@ -84,3 +84,20 @@ def test_build_plan_per_direction():
     res = {("l0", "fwd"): [("rw", 0.1, 50.0)], ("l0", "wgrad"): [("rw", 0.3, 50.0), ("tw", 0.15, 90.0)]}
     plan = dispatch.build_plan(res, {("l0", "fwd"): 100.0, ("l0", "wgrad"): 100.0})
     assert plan == {("l0", "fwd"): "rw", ("l0", "wgrad"): "tw"}
+
+
+def test_mere_shard_floor_reading():
+    """The data-parallel reading of D10: with the whole tensor's floor passed to each row shard, the
+    count-weighted mean of the shards' MEREs equals the whole tensor's MERE (brute force)."""
+    rng = np.random.default_rng(3)
+    ref = rng.standard_normal((40, 7)) * np.where(rng.random((40, 1)) < 0.3, 1e-9, 1.0)
+    out = ref * (1 + 0.01 * rng.standard_normal(ref.shape))
+    whole = probe.mere_stats(out, ref)
+    f = 1e-6 * np.abs(ref).mean()
+    parts = [probe.mere_stats(out[a:b], ref[a:b], floor=f) for a, b in ((0, 13), (13, 29), (29, 40))]
+    n = sum(p["count"] for p in parts)
+    assert abs(sum(p["mere"] * p["count"] for p in parts) / n - whole["mere"]) <= 1e-12 * whole["mere"]
+    assert sum(p["n_floored"] for p in parts) == whole["n_floored"] > 0
+    # the same per-element brute force
+    den = np.maximum(np.abs(ref), f)
+    assert abs(np.mean(np.abs(out - ref) / den) - whole["mere"]) <= 1e-12 * whole["mere"]
