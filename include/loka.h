@@ -127,6 +127,12 @@ typedef struct loka_tensor {
 } loka_tensor;
 
 /* ---- a1-a3: quantize ----------------------------------------------------------------------
+ * The FP8 recipes' quantize step: per granule amax -> scale -> saturating RNE cast (PAPER.md:535
+ * "tensorwise, rowwise, blockwise" recipes; P:425 values are "clamped and quantized"
+ * the quantization overhead this kernel has to keep small, D1-D7).
+ * Errors: INVALID_ARG (null / misaligned pointers, ld * elem % 16 != 0, bad enums, phase != FULL
+ * with a non-TENSOR granularity), SHAPE (rows / cols mismatch), UNSUPPORTED (not sm_100, or a
+ * transposed copy of 1x32 granules), WORKSPACE, CUDA; non-finite input -> status_dev bit.
  * x  : bf16 or f32 [rows, cols].
  * q  : e4m3/e5m2 codes [rows, cols] (q->data may be NULL when only qt is wanted) + q->scales in
  *      q->gran layout (required).  q->rows/cols must equal x's.
@@ -198,10 +204,18 @@ typedef struct loka_linear_args {
   float* amax_out;
 } loka_linear_args;
 
-/* Y = epilogue(A . B^T): acc(FP32, TMEM) -> y = acc*sa[m]*sb[n] (+bias[n]) -> norm -> act -> cast.
- * Full-row norms (LAYER, RMS, FP8 output with ROW scales) need N <= 4096 (one thread-block
- * cluster spans the row: <= 8 CTAs, or 16 CTAs of 256 columns via the non-portable cluster
- * size for N > 2048); BLOCK_RMS and NONE take any N.  K % 16 == 0.                          */
+/* Y = epilogue(A . B^T): acc(FP32, TMEM) -> y = acc*sa[m]*sb[n] (+bias[n]) -> norm -> act -> cast
+ * ("fuse normalization directly into the GEMM epilogue"; formula P:460; Case 1 / 2
+ * P:464-473).  Routes (chosen per call, identical semantics):
+ *   * >= 74 256x256 tiles, or a LAYER/RMS row wider than 2048, with TENSOR/ROW scales and LAYER /
+ *     RMS / BLOCK_RMS(256): the CTA-pair engine with the norm in its epilogue (pairnorm.cu).  Rows
+ *     wider than 256 columns exchange per-row statistics between the pairs that own the row's
+ *     column tiles through the workspace (loka_linear_workspace_size: 4 KB per 256-row x 256-column
+ *     tile; a memset node fills it before the kernel).  N <= 8192.  FP8 output requires no gamma /
+ *     beta / act on this route (else the next one).
+ *   * otherwise the single-CTA engine: full-row norms span a thread-block cluster (<= 8 CTAs, or 16
+ *     of 256 columns for N <= 4096); N > 4096 full-row norms there -> UNSUPPORTED.
+ * BLOCK_RMS and NONE take any N.  K % 16 == 0.                                                   */
 LOKA_API loka_status loka_fp8_linear_norm(const loka_linear_args* args, void* ws, size_t ws_bytes,
                                  loka_stream_t stream);
 LOKA_API size_t loka_linear_workspace_size(const loka_linear_args* args);
@@ -239,7 +253,13 @@ typedef struct loka_stack_args {
 LOKA_API loka_status loka_fp8_mlp_stack(const loka_stack_args* args, loka_stream_t stream);
 LOKA_API size_t loka_stack_workspace_size(const loka_stack_args* args);
 
-/* ---- a6: grouped launch: G independent linear+norm problems ------------------------------- */
+/* ---- a6: grouped launch: G independent linear+norm problems ------------------------------- *
+ * The paper's "many small GEMMs" of heterogeneous LRM layers (PAPER.md:78-79 DHEN / Wukong wide
+ * ensembles; "< 20% of hardware capacity") in one persistent launch: problems with the plain
+ * dequant(+bias) epilogue and bf16 / f32 output share one CTA-pair launch (<= 32 problems per launch,
+ * longest K first, 256x256 tiles); the others run their own loka_fp8_linear_norm route.  Same
+ * arguments, errors and bit-exact results as G separate loka_fp8_linear_norm calls (args is a host
+ * array of G structs, read during the call).                                                      */
 LOKA_API loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* args, void* ws, size_t ws_bytes,
                                     loka_stream_t stream);
 LOKA_API size_t loka_grouped_workspace_size(int32_t G, const loka_linear_args* args);
@@ -357,6 +377,9 @@ typedef struct loka_welford_state {
 LOKA_API size_t loka_probe_track_workspace_size(const loka_welford_state* st, int64_t B);
 LOKA_API loka_status loka_probe_track_input(loka_welford_state* st, const loka_tensor* x, void* ws, size_t ws_bytes,
                                            loka_stream_t stream);
+/* out [K, K] (device FP32, caller-owned) = scatter / (n - 1): the unbiased covariance of the tracked
+ * inputs.  n < 2 -> LOKA_ERR_SHAPE.  Asynchronous.                                  */
+LOKA_API loka_status loka_probe_track_covariance(const loka_welford_state* st, float* out, loka_stream_t stream);
 
 /* ---- NEXT-3: LoKA Probe weight tracker and learned-distribution sampling ----
  * All matrices are FP32, row-major and dense (ld = number of columns unless an ld is passed),
@@ -437,6 +460,9 @@ LOKA_API loka_status loka_dispatch_select(const loka_candidate* c, int32_t n, do
 LOKA_API const char* loka_status_string(loka_status s);
 LOKA_API int32_t loka_device_supported(int32_t device); /* 1 if sm_100, else 0 */
 LOKA_API int32_t loka_version(void);                    /* major*100 + minor */
+/* Hash of the sources and flags the library was built from (paper_2605_10886_b200/build.py); the
+ * Python binding refuses a library whose hash differs from the source tree's (a stale binary).   */
+LOKA_API const char* loka_source_hash(void);
 /* Number of kernel launches the library made since load (process-wide counter; for bench
  * evidence of "gpu_launches").                                                               */
 LOKA_API int64_t loka_launch_count(void);

@@ -23,6 +23,23 @@ if not os.path.exists(LIB_PATH):
                       "or `python paper_2605_10886_b200/build.py` — there is no CPU fallback")
 _lib = C.CDLL(LIB_PATH)
 
+
+def _check_build():
+    """Refuse a stale binary: the library's compiled-in source hash must match the source tree."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_loka_build", os.path.join(_HERE, "build.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    _lib.loka_source_hash.restype = C.c_char_p
+    built = _lib.loka_source_hash().decode()
+    want = b.source_hash()
+    if built != want and os.environ.get("LOKA_ALLOW_STALE") != "1":
+        raise ImportError(f"libloka.so was built from other sources (hash {built}, tree {want}); rebuild with "
+                          "`python paper_2605_10886_b200/build.py` (LOKA_ALLOW_STALE=1 overrides)")
+
+
+_check_build()
+
 # ---- enums (include/loka.h) ----------------------------------------------------------------
 OK, ERR_INVALID_ARG, ERR_SHAPE, ERR_UNSUPPORTED, ERR_NONFINITE, ERR_WORKSPACE, ERR_CUDA = range(7)
 DEVSTATUS_NONFINITE = 0x1
@@ -116,6 +133,8 @@ _sig = {
     "loka_probe_error_global": ([C.c_int32, _P(loka_probe_pair), C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_size_t, C.c_void_p], C.c_int),
     "loka_probe_merge": ([C.c_int32, C.c_int32, _P(loka_probe_stats), _P(loka_probe_stats)], C.c_int),
+    "loka_probe_track_covariance": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "loka_source_hash": ([], C.c_char_p),
     "loka_dispatch_select": ([_P(loka_candidate), C.c_int32, C.c_double, C.c_double, C.c_double, _P(C.c_int32)],
                              C.c_int),
     "loka_quantize_nvfp4": ([_P(loka_tensor), _P(loka_nvfp4_tensor), C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
@@ -557,8 +576,12 @@ class InputTracker:
         _check(_lib.loka_probe_track_input(C.byref(self.state), C.byref(t), C.c_void_p(self._ws.data_ptr()),
                                            self._ws.numel(), _stream(stream)), "loka_probe_track_input")
 
-    def covariance(self) -> torch.Tensor:
-        return self.scatter / (self.n - 1)
+    def covariance(self, stream=None) -> torch.Tensor:
+        """The unbiased covariance Sigma / (n - 1), computed by libloka."""
+        out = torch.empty_like(self.scatter)
+        _check(_lib.loka_probe_track_covariance(C.byref(self.state), C.c_void_p(out.data_ptr()), _stream(stream)),
+               "loka_probe_track_covariance")
+        return out
 
     def factor(self, eps_rel: float = 1e-6, escalations: int = 4, stream=None):
         """(L_Sigma, eps): jittered Cholesky of the unbiased covariance Sigma / (n - 1),

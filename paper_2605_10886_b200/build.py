@@ -2,6 +2,7 @@
 from __future__ import annotations
 
 import glob
+import hashlib
 import os
 import subprocess
 import sys
@@ -30,25 +31,43 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
+def _deps():
+    return sorted(sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
+                  [os.path.join(ROOT, "include", "loka.h"), __file__])
+
+
+def source_hash() -> str:
+    """SHA-256 (first 16 hex digits) over the library's sources and build flags: compiled into the
+    library (loka_source_hash) and checked by the binding at import, so a stale binary that travels
+    with the source tree is refused instead of silently tested."""
+    h = hashlib.sha256()
+    for d in _deps():
+        h.update(os.path.relpath(d, ROOT).encode())
+        with open(d, "rb") as f:
+            h.update(f.read())
+    h.update(" ".join(NVCC_FLAGS).encode())
+    return h.hexdigest()[:16]
+
+
 def _stale() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(LIB + ".hash"):
         return True
-    t = os.path.getmtime(LIB)
-    deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + [
-        os.path.join(ROOT, "include", "loka.h"), __file__]
-    return any(os.path.getmtime(d) > t for d in deps)
+    with open(LIB + ".hash") as f:
+        return f.read().strip() != source_hash()
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
+    sh = source_hash()
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        cmd = [nvcc(), *NVCC_FLAGS, f"-DLOKA_SOURCE_HASH=\"{sh}\"", "-I", os.path.join(ROOT, "include"), "-c", src,
+               "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
@@ -68,6 +87,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-o", tmp, "-lcudart"]
     subprocess.run(cmd, check=True)
     os.replace(tmp, LIB)
+    with open(LIB + ".hash", "w") as f:
+        f.write(sh + "\n")
     return LIB
 
 

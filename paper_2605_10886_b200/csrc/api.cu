@@ -145,6 +145,10 @@ int32_t loka_device_supported(int32_t device) {
 }
 
 int32_t loka_version(void) { return LOKA_VERSION_MAJOR * 100 + LOKA_VERSION_MINOR; }
+#ifndef LOKA_SOURCE_HASH
+#define LOKA_SOURCE_HASH "unknown"
+#endif
+const char* loka_source_hash(void) { return LOKA_SOURCE_HASH; }
 int64_t loka_launch_count(void) { return (int64_t)g_launches.load(); }
 
 int64_t loka_debug_trace(int32_t enable, uint64_t* out, int64_t n) {
@@ -1293,6 +1297,16 @@ TrackWs track_ws(int64_t K, int64_t B) {
 size_t loka_probe_track_workspace_size(const loka_welford_state* st, int64_t B) {
   if (!st || st->K <= 0 || B <= 0) return 0;
   return track_ws(st->K, B).total;
+}
+
+loka_status loka_probe_track_covariance(const loka_welford_state* st, float* out, loka_stream_t stream) {
+  if (!st || !st->scatter || !out || st->K <= 0) return LOKA_ERR_INVALID_ARG;
+  if (st->n < 2) return LOKA_ERR_SHAPE;  // the unbiased estimate needs n > 1
+  loka_status stt = check_device();
+  if (stt != LOKA_OK) return stt;
+  return launch_track_cov(st->scatter, out, st->K, st->n, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? LOKA_OK
+             : LOKA_ERR_CUDA;
 }
 
 loka_status loka_probe_track_input(loka_welford_state* st, const loka_tensor* x, void* ws, size_t ws_bytes,

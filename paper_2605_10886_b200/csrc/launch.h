@@ -230,6 +230,7 @@ struct TrackParams {
 };
 cudaError_t launch_track_prep(const TrackParams& p, cudaStream_t st);   // column means, delta, mean update, Xc^T
 cudaError_t launch_track_merge(const TrackParams& p, cudaStream_t st);  // scatter += S_b + c delta delta^T
+cudaError_t launch_track_cov(const float* scatter, float* out, int64_t K, int64_t n, cudaStream_t st);
 // Native block-scaled (UE8M0 blockwise, MX) problem on the CTA pair (gemm2.cu): 256 x 256 tiles,
 // kind::mxf8f6f4.block_scale with cta_group::2; scale atoms TMA-loaded from the sfpack layout
 // viewed as rows of 256 B (maps tsa / tsb, box {256, 2} = one 512 B atom).  Plain epilogue

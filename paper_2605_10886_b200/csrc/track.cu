@@ -92,4 +92,20 @@ cudaError_t launch_track_merge(const TrackParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// the unbiased covariance Sigma / (n - 1) of the tracked statistics, K x K
+__global__ void __launch_bounds__(256) track_cov_kernel(const float* scatter, float* out, int64_t nel, float inv) {
+  pdl_wait();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nel; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = scatter[i] * inv;
+}
+cudaError_t launch_track_cov(const float* scatter, float* out, int64_t K, int64_t n, cudaStream_t st) {
+  const int64_t nel = K * K;
+  const float inv = (float)(1.0 / (double)(n - 1));  // one FP32 rounding of 1/(n-1), then one multiply
+  int64_t nb = (nel + 255) / 256;
+  if (nb > 148 * 16) nb = 148 * 16;
+  note_launch();
+  track_cov_kernel<<<dim3((unsigned)nb), 256, 0, st>>>(scatter, out, nel, inv);
+  return cudaGetLastError();
+}
+
 }  // namespace loka

@@ -28,7 +28,7 @@ def declared_symbols():
 
 def test_every_declared_symbol_is_exported(lk):
     syms = declared_symbols()
-    assert len(syms) == 37, syms
+    assert len(syms) == 39, syms
     out = subprocess.run(["nm", "-D", "--defined-only", lk.LIB_PATH], capture_output=True, text=True).stdout
     exported = set(re.findall(r" T (loka_\w+)", out))
     assert set(syms) <= exported, set(syms) - exported
@@ -147,3 +147,13 @@ def test_probe_merge_host(lk):
     assert m[0]["count"] == 40 and m[0]["n_floored"] == 3 and m[0]["max_rel"] == 3.0
     assert abs(m[0]["mere"] - (0.5 * 30 + 0.3 * 10) / 40) < 1e-15 and m[0]["sum_abs_ref"] == 30.0
     assert abs(m[1]["mere"] - (0.1 * 10 + 0.2 * 30) / 40) < 1e-15 and m[1]["n_floored"] == 4
+
+
+def test_library_matches_source_tree(lk):
+    """The library carries the hash of the sources it was built from (build.py); the binding refuses
+    a mismatch at import, so a stale libloka.so cannot pass the tests (round-1 verdict weak #11)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_b", os.path.join(ROOT, "paper_2605_10886_b200", "build.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    assert lk._lib.loka_source_hash().decode() == b.source_hash()
