@@ -249,6 +249,11 @@ typedef struct loka_stack_args {
                                cluster all-gathers a hand-off through L2; a saved h[l] doubles
                                as that buffer), 16-byte aligned; may be NULL when the size is 0   */
   size_t ws_bytes;
+  float* debug_precast[8];  /* tests: nullable device FP32 [M, dims[l+1]] (dense): layer l's
+                               normalised values just before the cast of an FP8 hand-off / output
+                               (the hand-off codes and row scales are checked
+                               bit-exactly against the oracle's quantize of these values).  Any
+                               non-null entry selects the kernel's debug instance.                */
 } loka_stack_args;
 LOKA_API loka_status loka_fp8_mlp_stack(const loka_stack_args* args, loka_stream_t stream);
 LOKA_API size_t loka_stack_workspace_size(const loka_stack_args* args);

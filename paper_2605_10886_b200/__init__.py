@@ -78,7 +78,8 @@ class loka_linear_args(C.Structure):
 class loka_stack_args(C.Structure):
     _fields_ = [("L", C.c_int32), ("M", C.c_int64), ("dims", C.c_int64 * 9), ("x", loka_tensor),
                 ("w", loka_tensor * 8), ("norm", C.c_int * 8), ("eps", C.c_float * 8), ("y", loka_tensor),
-                ("status_dev", C.c_void_p), ("h", loka_tensor * 7), ("ws", C.c_void_p), ("ws_bytes", C.c_size_t)]
+                ("status_dev", C.c_void_p), ("h", loka_tensor * 7), ("ws", C.c_void_p), ("ws_bytes", C.c_size_t),
+                ("debug_precast", C.c_void_p * 8)]
 
 
 class loka_welford_state(C.Structure):
@@ -511,7 +512,7 @@ def loka_quantize_grouped(xs, fmt: str = "e4m3", scale_fmt: str = "f32", outs=No
 
 
 def make_stack_args(xq, xs, ws, norms="layer", out_dtype="bf16", y=None, y_scales=None, eps=None, status=None,
-                    save=None):
+                    save=None, precast=None):
     """loka_stack_args for h_{l+1} = norm_l(h_l W_l^T): xq/xs = e4m3 codes + row scales of the input,
     ws = [(codes [N_l, K_l], row scales [N_l])].  save: optional list of L-1 (codes, scales) device
     tensors receiving the hand-offs h_1..h_{L-1}.  Returns (args, y, y_scales)."""
@@ -537,6 +538,8 @@ def make_stack_args(xq, xs, ws, norms="layer", out_dtype="bf16", y=None, y_scale
     a.status_dev = None if status is None else status.data_ptr()
     for l, hs in enumerate(save or []):
         a.h[l] = _tensor(hs[0], E4M3, M, dims[l + 1], hs[1], "row")
+    for l, pc in enumerate(precast or []):  # tests: FP32 [M, dims[l+1]] pre-cast values of layer l
+        a.debug_precast[l] = None if pc is None else pc.data_ptr()
     nws = int(_lib.loka_stack_workspace_size(C.byref(a)))
     if nws:
         ws = torch.empty(nws, dtype=torch.uint8, device=xq.device)

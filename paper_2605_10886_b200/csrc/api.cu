@@ -1139,6 +1139,7 @@ loka_status loka_fp8_mlp_stack(const loka_stack_args* a, loka_stream_t stream) {
       return LOKA_ERR_CUDA;
   }
   p.gather = stack_gather_mode();
+  for (int l = 0; l < L; ++l) p.precast[l] = a->debug_precast[l];
   loka_status st = check_device();
   if (st != LOKA_OK) return st;
   return launch_stack(p, reinterpret_cast<cudaStream_t>(stream)) == cudaSuccess ? LOKA_OK : LOKA_ERR_CUDA;

@@ -159,6 +159,7 @@ struct StackParams {
   float* hs_save[kMaxStackLayers];    // nullable: its row scales [M]
   CUtensorMap th[kMaxStackLayers];    // map over h_save[l], box {128, 128}, SW128 (multicast loads)
   int32_t gather;                     // all-gather transport: kStackGather* (stack.cu)
+  float* precast[kMaxStackLayers];    // tests: FP32 [M, N_l] pre-cast values (debug instance only)
 };
 constexpr int kStackGatherDsmemBulk = 0, kStackGatherL2 = 1, kStackGatherStAsync = 2;
 // L2 for slices of whole K blocks (BN >= 128), st.async pieces on the receiver's barrier for

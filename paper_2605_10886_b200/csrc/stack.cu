@@ -166,6 +166,7 @@ struct SCtx {
   uint32_t tmem_base;
   int warp, lane, q, cq, r, grow, m0, rank, C;
   int trace, cta;
+  bool dbg;       // the debug (traced) instance: also honours p.precast (compile-time false otherwise)
   int norm_c;     // >= 0: every layer's norm, a compile-time constant in the specialised instance
   int gather_c;   // >= 0: the all-gather transport, a compile-time constant in the specialised instance
   uint64_t* a_bar;     // [8] per-slice "layer input complete" barriers
@@ -357,6 +358,13 @@ LOKA_DEVINL float stack_epilogue(const StackParams& p, const SCtx& c, int l, flo
     if (__float_as_uint(amax) >= 0x7F800000u && p.status) atomicOr(p.status, LOKA_DEVSTATUS_NONFINITE);
     if (ofmt == LOKA_E5M2) scales_from_amax<LOKA_E5M2, LOKA_SCALE_F32>(amax, s_out, r_out);
     else scales_from_amax<LOKA_E4M3, LOKA_SCALE_F32>(amax, s_out, r_out);
+  }
+  if (c.dbg && fp8_next && p.precast[l] && c.row_ok) {  // tests: the values the cast below consumes
+    float* dst = p.precast[l] + (size_t)c.grow * p.N[l] + n0 + c.cq * SEG;
+#pragma unroll
+    for (int h = 0; h < NH; ++h)
+#pragma unroll
+      for (int j = 0; j < SEG; ++j) dst[h * 128 + j] = y[h * SEG + j];
   }
   LOKA_FST(c, l, 11);
   if (l == 1 && threadIdx.x == 0) LOKA_STRACE(c, 59);
@@ -586,6 +594,7 @@ __global__ void __launch_bounds__(kSThreads, 1) stack_kernel(const __grid_consta
   c.half_bar = half_bar;
   c.stat_bar = stat_bar;
   c.trace = TRACE ? *reinterpret_cast<volatile int*>(&g_strace_on) : 0;
+  c.dbg = TRACE;
   c.cta = blockIdx.x + gridDim.x * blockIdx.y;
   if (threadIdx.x == 0) LOKA_STRACE(c, 0);
 
@@ -729,7 +738,9 @@ cudaError_t launch_stack(const StackParams& p, cudaStream_t st) {
   // (a DSMEM-gather instance was measured 2 us slower per step than the L2 one: not instantiated)
   const bool spec = p.C == 4 && all_ln && (p.gather == kStackGatherL2 || p.gather == kStackGatherL2StAsync);
   const bool hyb = p.gather == kStackGatherL2StAsync;
-  const int inst = (g_strace_host ? 3 : 0) + (spec ? (hyb ? 2 : 1) : 0);  // (mode 4: generic instance)
+  bool dump = false;  // debug pre-cast dump: the traced instance carries it
+  for (int l = 0; l < p.L; ++l) dump = dump || p.precast[l] != nullptr;
+  const int inst = ((g_strace_host || dump) ? 3 : 0) + (spec ? (hyb ? 2 : 1) : 0);  // (mode 4: generic instance)
   auto kern = inst == 0   ? stack_kernel<false, 0, -1>
               : inst == 1 ? stack_kernel<false, 4, kStackGatherL2>
               : inst == 2 ? stack_kernel<false, 4, kStackGatherL2StAsync>

@@ -140,3 +140,33 @@ def test_stack_matches_layer_chain_closely():
     torch.cuda.synchronize()
     d = (y - hq).abs()
     assert float((d <= 2e-2 * hq.abs().clamp_min(1.0)).float().mean()) > 0.99
+
+
+@pytest.mark.parametrize("M,dims,norm", [(4096, synth.CFG2_DIMS, "layer"), (520, [512, 1024, 512, 256], "rms"),
+                                         (300, [256, 256, 256], "layer")])
+def test_handoffs_bit_exact_vs_precast(M, dims, norm):
+    """Round-1 verdict What's missing #4: the stack's FP8 hand-offs (codes and row scales) equal the
+    oracle's rowwise quantize of the kernel's own pre-cast FP32 values bit for bit (SURVEY.md §8(c) O10,
+    the parity matrix's "FP8 output of the fused epilogue ... bit-exact"), for every layer, every row;
+    and those values are within 2e-3 of the oracle on the layer's own input."""
+    import ctypes as C
+    xq, xs, ws = _inputs(M, dims)
+    L = len(dims) - 1
+    save = [(torch.empty(M, n, dtype=torch.uint8, device=DEV), torch.empty(M, dtype=torch.float32, device=DEV))
+            for n in dims[1:-1]]
+    pre = [torch.full((M, n), float("nan"), dtype=torch.float32, device=DEV) for n in dims[1:]]
+    a, y, ys = lk.make_stack_args(xq, xs, ws, norms=norm, out_dtype="e4m3", save=save, precast=pre)
+    assert lk._lib.loka_fp8_mlp_stack(C.byref(a), None) == 0
+    torch.cuda.synchronize()
+    outs = save + [(y, ys)]
+    ins = [(xq, xs)] + save
+    for l in range(L):
+        p = f64(pre[l])
+        assert np.isfinite(p).all(), l
+        oq, os_ = oracle.quantize.quantize(p, "e4m3", "row")
+        assert np.array_equal(outs[l][1].cpu().numpy().view(np.uint32), os_.view(np.uint32)), l
+        assert np.array_equal(outs[l][0].cpu().numpy(), oq), l
+        rows = np.arange(M) if M <= 600 else np.sort(np.random.default_rng(l).choice(M, 64, replace=False))
+        yo = _layer_oracle(ins[l][0], ins[l][1], ws[l][0], ws[l][1], norm, rows)
+        rms = np.sqrt(np.mean(yo ** 2, axis=1, keepdims=True))
+        assert np.max(np.abs(p[rows] - yo) / np.maximum(np.abs(yo), rms)) <= TOL, l
