@@ -565,27 +565,33 @@ def main():
     torch.cuda.synchronize()
     launches_per_step = lk.launch_count() - n0
 
-    def run_fp8():
-        with torch.cuda.stream(stream):
+    # the timed steps: events at the start, between the quantize calls and the fused GEMM + LayerNorm
+    # call, and at the end of every step, so the dominant kernel's time comes from the same steps
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
             step.step(sh)
-
+    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        t_fp8 = time_steps(run_fp8, args.steps, args.warmup, None, stream, barrier)
+        with torch.cuda.stream(stream):
+            for e0, e1, e2 in ev:
+                e0.record(stream)
+                step.quantize(sh)
+                e1.record(stream)
+                step.linear(sh)
+                e2.record(stream)
+        torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    torch.cuda.synchronize()
     clocks = clk.summary()
-
-    # the dominant kernel alone: the fused GEMM + LayerNorm call (incl. its workspace memset node)
-    def run_lin():
-        with torch.cuda.stream(stream):
-            step.linear(sh)
-
-    t_lin = time_steps(run_lin, args.steps, args.warmup, None, stream, None)
+    t_fp8 = [e0.elapsed_time(e2) for e0, _, e2 in ev]
+    t_q = [e0.elapsed_time(e1) for e0, e1, _ in ev]
+    t_lin = [e1.elapsed_time(e2) for _, e1, e2 in ev]
     lin_ms = statistics.median(t_lin)
-
-    def run_q():
-        with torch.cuda.stream(stream):
-            step.quantize(sh)
-
-    t_q = time_steps(run_q, args.steps, args.warmup, None, stream, barrier)
 
     # BF16 baseline (torch F.linear + F.layer_norm, cuBLAS) on the same shard
     out_bf = torch.empty_like(step.y)
@@ -595,6 +601,23 @@ def main():
             out_bf.copy_(F.layer_norm(F.linear(x, w), (CFG5_N,)))
 
     t_bf = time_steps(run_bf, args.steps, args.warmup, None, stream, barrier)
+
+    # the library's own BF16 path with the same fused epilogue (kind::f16 on the CTA-pair engine):
+    # separates the FP8 gain from the fusion gain (SURVEY.md §8(d) secondary denominator)
+    import ctypes
+    bargs, _, _ = lk.make_linear_args(x, step.xs, w, step.wsc, a_gran="tensor", b_gran="tensor", norm="layer",
+                                      out_dtype="bf16", y=out_bf, keep=step.keep)
+    bargs.a.dtype = lk.BF16
+    bargs.b.dtype = lk.BF16
+    bws = torch.empty(max(256, int(lk._lib.loka_bf16_linear_workspace_size(ctypes.byref(bargs)))), dtype=torch.uint8,
+                      device=dev)
+
+    def run_bf_lib():
+        with torch.cuda.stream(stream):
+            st_ = lk._lib.loka_bf16_linear_norm(ctypes.byref(bargs), ctypes.c_void_p(bws.data_ptr()), bws.numel(), sh)
+            assert st_ == 0, st_
+
+    t_bfl = time_steps(run_bf_lib, args.steps, args.warmup, None, stream, barrier)
 
     # e2e through the public API: pinned host X -> device, the step, device Y -> pinned host, every step
     xh = x.cpu().pin_memory()
@@ -618,6 +641,7 @@ def main():
 
     ms_fp8 = max_over_ranks(sum(t_fp8)) / args.steps
     ms_bf = max_over_ranks(sum(t_bf)) / args.steps
+    ms_bfl = max_over_ranks(sum(t_bfl)) / args.steps
     ms_q = max_over_ranks(sum(t_q)) / args.steps
     ms_lin = max_over_ranks(lin_ms)
     ms_e2e = max_over_ranks(sum(t_e2e)) / e2e_steps
@@ -656,11 +680,18 @@ def main():
             "compute_only": {"value": round(fl / (ms_lin * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
                              "ms_per_step": round(ms_lin, 5),
                              "pct_of_4500_tflops": round(100.0 * fl / (ms_lin * 1e-3) / 1e12 / world / 4500.0, 2),
-                             "what": "the fused GEMM + LayerNorm call alone on pre-quantized operands"},
+                             "what": "the fused GEMM + LayerNorm call of each timed step (events between the "
+                                     "quantize calls and it; median over the K steps)"},
             "quantize_ms_per_step": round(ms_q, 5),
             "bf16_baseline": {"value": round(fl / (ms_bf * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
                               "ms_per_step": round(ms_bf, 5), "impl": "torch F.linear + F.layer_norm (bf16, cuBLAS)"},
             "speedup_vs_bf16": round(ms_bf / ms_fp8, 3),
+            "bf16_library_fused": {"value": round(fl / (ms_bfl * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
+                                   "ms_per_step": round(ms_bfl, 5),
+                                   "impl": "this library's BF16 path: kind::f16 CTA-pair GEMM + the same fused "
+                                           "LayerNorm epilogue (loka_bf16_linear_norm), no quantize",
+                                   "fp8_step_speedup": round(ms_bfl / ms_fp8, 3),
+                                   "fp8_compute_only_speedup": round(ms_bfl / ms_lin, 3)},
             "roofline": {"kernel": "pair_norm_kernel<256, LayerNorm> (CTA-pair FP8 GEMM + fused LayerNorm), 1 "
                                    "launch/step", "bound": "tensor", "achieved": round(achieved, 2),
                          "peak": round(fp8_peak_sus, 1), "unit": "TFLOP/s", "frac": round(achieved / fp8_peak_sus, 4),
@@ -671,7 +702,7 @@ def main():
                          "flop_per_launch": step.flops, "launch_ms": round(lin_ms, 4),
                          "algorithmic_bytes_per_launch": int(x.shape[0] * CFG5_K + CFG5_N * CFG5_K +
                                                              x.shape[0] * CFG5_N * 2),
-                         "timing": "median of K launches, CUDA events on the launching stream"},
+                         "timing": "median over the K timed steps of the launch's events (launching stream)"},
             "e2e": {"value": round(fl / (ms_e2e * 1e-3) / 1e12, 3), "unit": "TFLOP/s", "ms_per_step": round(ms_e2e, 5),
                     "h2d_bytes_per_step": int(x.numel() * 2), "d2h_bytes_per_step": int(step.y.numel() * 2),
                     "steps": e2e_steps,

@@ -220,6 +220,17 @@ LOKA_API loka_status loka_fp8_linear_norm(const loka_linear_args* args, void* ws
                                  loka_stream_t stream);
 LOKA_API size_t loka_linear_workspace_size(const loka_linear_args* args);
 
+/* The library's own BF16 path with the same fused epilogue (the secondary BF16
+ * denominator, which separates the gain of FP8 from the gain of fusion): A [M,K] and B [N,K] are
+ * BF16 (a/b dtype LOKA_BF16, K-major, ld * 2 % 16 == 0; scales ignored, unit), C = A . B^T by
+ * tcgen05.mma.cta_group::2.kind::f16 (FP32 accumulation in TMEM) on the CTA-pair engine, then the
+ * pair-norm epilogue (LAYER / RMS / BLOCK_RMS(256), bias, gamma / beta, h-swish, FP8 row-scale
+ * output without gamma / beta / act).  Workspace: loka_bf16_linear_workspace_size.  Errors as
+ * loka_fp8_linear_norm; other norms or the NEXT-1 backward fields -> UNSUPPORTED.              */
+LOKA_API loka_status loka_bf16_linear_norm(const loka_linear_args* args, void* ws, size_t ws_bytes,
+                                           loka_stream_t stream);
+LOKA_API size_t loka_bf16_linear_workspace_size(const loka_linear_args* args);
+
 /* ---- a4+a5 for a whole LRM MLP stack in ONE launch (BASELINE.json configs[1]) --------------
  * Layer l: h_{l+1} = norm_l(h_l . W_l^T) with h_0 = x (e4m3 + ROW scales) and W_l e4m3 + ROW
  * scales (No Bias, unparameterized norm: PAPER.md:443, 483).  Every intermediate h_l (l = 1..L-1)

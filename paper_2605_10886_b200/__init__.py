@@ -136,6 +136,8 @@ _sig = {
     "loka_probe_merge": ([C.c_int32, C.c_int32, _P(loka_probe_stats), _P(loka_probe_stats)], C.c_int),
     "loka_probe_track_covariance": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "loka_source_hash": ([], C.c_char_p),
+    "loka_bf16_linear_norm": ([C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p], C.c_int),
+    "loka_bf16_linear_workspace_size": ([C.c_void_p], C.c_size_t),
     "loka_dispatch_select": ([_P(loka_candidate), C.c_int32, C.c_double, C.c_double, C.c_double, _P(C.c_int32)],
                              C.c_int),
     "loka_quantize_nvfp4": ([_P(loka_tensor), _P(loka_nvfp4_tensor), C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
@@ -312,6 +314,20 @@ def loka_fp8_linear_norm(a, a_scales, b, b_scales, stream=None, ws=None, **kw):
     ws, nws = _workspace(linear_workspace(args), a.device, ws)
     _check(_lib.loka_fp8_linear_norm(C.byref(args), None if ws is None else C.c_void_p(ws.data_ptr()), nws,
                                      _stream(stream)), "loka_fp8_linear_norm")
+    return y, ys
+
+
+def loka_bf16_linear_norm(a, b, stream=None, ws=None, **kw):
+    """The library's BF16 (kind::f16) path with the fused epilogue: a [M,K], b [N,K] bf16 device
+    tensors.  kw as make_linear_args (norm, act, gamma, beta, bias, out_dtype, y, ...).  Returns (y, ys)."""
+    one = torch.ones(1, dtype=torch.float32, device=a.device)  # (scales are ignored by this path)
+    args, y, ys = make_linear_args(a, one, b, one, a_gran="tensor", b_gran="tensor", **kw)
+    args.a.dtype = BF16
+    args.b.dtype = BF16
+    nws = int(_lib.loka_bf16_linear_workspace_size(C.byref(args)))
+    ws, nws = _workspace(nws, a.device, ws)
+    _check(_lib.loka_bf16_linear_norm(C.byref(args), None if ws is None else C.c_void_p(ws.data_ptr()), nws,
+                                      _stream(stream)), "loka_bf16_linear_norm")
     return y, ys
 
 

@@ -782,18 +782,22 @@ static loka_status run_pair_norm(const loka_linear_args* a, const PnPlan& pl, vo
   PairNormParams p;
   std::memset(&p, 0, sizeof(p));
   const loka_tensor &A = a->a, &B = a->b, &Y = a->y;
-  if (!make_map_u8(&p.ta, A.data, a->M, a->K, A.ld, 128)) return LOKA_ERR_CUDA;
-  if (!make_map_u8(&p.tb, B.data, a->N, a->K, B.ld, 128)) return LOKA_ERR_CUDA;
+  const bool bf16 = A.dtype == LOKA_BF16;  // the BF16 (kind::f16) path: byte views of the operands
+  const int eb = bf16 ? 2 : 1;
+  if (!make_map_u8(&p.ta, A.data, a->M, a->K * eb, A.ld * eb, 128)) return LOKA_ERR_CUDA;
+  if (!make_map_u8(&p.tb, B.data, a->N, a->K * eb, B.ld * eb, 128)) return LOKA_ERR_CUDA;
   if (!make_map_out(&p.ty, Y.data, a->M, a->N, Y.ld, Y.dtype, 128, 32u)) return LOKA_ERR_CUDA;
+  p.bf16_in = bf16 ? 1 : 0;
   p.M = (int32_t)a->M;
   p.N = (int32_t)a->N;
   p.K = (int32_t)a->K;
   p.a_fmt = A.dtype == LOKA_E5M2 ? 1 : 0;
   p.b_fmt = B.dtype == LOKA_E5M2 ? 1 : 0;
-  p.sa = A.scales;
-  p.sa_row = A.gran == LOKA_GRAN_ROW;
-  p.sb = B.scales;
-  p.sb_row = B.gran == LOKA_GRAN_ROW;
+  p.sa = bf16 ? pair_norm_unit_scale() : A.scales;
+  p.sa_row = !bf16 && A.gran == LOKA_GRAN_ROW;
+  p.sb = bf16 ? pair_norm_unit_scale() : B.scales;
+  p.sb_row = !bf16 && B.gran == LOKA_GRAN_ROW;
+  if (!p.sa || !p.sb) return LOKA_ERR_CUDA;
   p.bias = a->bias;
   p.bias_bf16 = a->bias_dtype == LOKA_BF16;
   p.gamma = a->gamma;
@@ -831,6 +835,57 @@ static bool pair_norm_taken(const loka_linear_args* a, size_t* ws) {
   const PnPlan pl = pair_norm_plan_dev(a);
   if (pl.ok && ws) *ws = pair_norm_ws(pl);
   return pl.ok;
+}
+
+// The library's own BF16 path (kind::f16) with the same fused epilogue, on the CTA-pair engine: the
+// secondary BF16 denominator of SURVEY.md §8(d) (separates the FP8 gain from the fusion gain).
+static loka_status bf16_plan(const loka_linear_args* a, PnPlan* pl) {
+  if (!a) return LOKA_ERR_INVALID_ARG;
+  const int64_t M = a->M, N = a->N, K = a->K;
+  if (M <= 0 || N <= 0 || K <= 0 || M > (1ll << 31) - 1 || N > 16384 || K > (1ll << 30)) return LOKA_ERR_SHAPE;
+  const loka_tensor &A = a->a, &B = a->b, &Y = a->y;
+  if (A.dtype != LOKA_BF16 || B.dtype != LOKA_BF16) return LOKA_ERR_INVALID_ARG;
+  if (A.rows != M || A.cols != K || B.rows != N || B.cols != K || Y.rows != M || Y.cols != N) return LOKA_ERR_SHAPE;
+  if (!A.data || !B.data || !Y.data || !aligned16(A.data) || !aligned16(B.data) || !aligned16(Y.data))
+    return LOKA_ERR_INVALID_ARG;
+  if (A.ld < K || B.ld < K || (A.ld * 2) % 16 || (B.ld * 2) % 16) return LOKA_ERR_INVALID_ARG;
+  if (Y.dtype < LOKA_F32 || Y.dtype > LOKA_E5M2 || Y.ld < N || (Y.ld * elem_size(Y.dtype)) % 16)
+    return LOKA_ERR_INVALID_ARG;
+  const bool fp8_out = is_fp8(Y.dtype);
+  if (fp8_out && (!Y.scales || Y.gran != LOKA_GRAN_ROW || a->gamma || a->beta || a->act != LOKA_ACT_NONE))
+    return LOKA_ERR_UNSUPPORTED;
+  const bool blk = a->norm == LOKA_NORM_BLOCK_RMS;
+  if (a->norm != LOKA_NORM_LAYER && a->norm != LOKA_NORM_RMS && !blk) return LOKA_ERR_UNSUPPORTED;
+  if (blk && (a->norm_block != 256 || N % 256)) return LOKA_ERR_SHAPE;
+  if (a->beta && a->norm != LOKA_NORM_LAYER) return LOKA_ERR_INVALID_ARG;
+  if (a->gamma && blk) return LOKA_ERR_INVALID_ARG;
+  if (a->act != LOKA_ACT_NONE && a->act != LOKA_ACT_HARDSWISH) return LOKA_ERR_INVALID_ARG;
+  if (a->bias && a->bias_dtype != LOKA_F32 && a->bias_dtype != LOKA_BF16) return LOKA_ERR_INVALID_ARG;
+  if (a->bwd_xhat || a->save_xhat || a->save_rstd) return LOKA_ERR_UNSUPPORTED;
+  if (a->amax_out && (fp8_out || (reinterpret_cast<uintptr_t>(a->amax_out) & 3))) return LOKA_ERR_INVALID_ARG;
+  int sms = 148;
+  loka_status st = check_device(&sms);
+  if (st != LOKA_OK) return st;
+  pl->tn = 256;
+  pl->tiles_n = (int)cdiv(N, 256);
+  pl->row_blocks = (int)cdiv(M, 256);
+  pl->xchg = pl->tiles_n > 1 && (!blk || fp8_out);
+  pl->order = 0;
+  const int avail = std::min(sms / 2, kPnMaxPairs);
+  if (pl->xchg && pl->tiles_n > 32) return LOKA_ERR_UNSUPPORTED;
+  pl->pairs = (int)std::min<int64_t>(avail, (int64_t)pl->row_blocks * pl->tiles_n);
+  pl->ok = true;
+  return LOKA_OK;
+}
+size_t loka_bf16_linear_workspace_size(const loka_linear_args* a) {
+  PnPlan pl;
+  return bf16_plan(a, &pl) == LOKA_OK ? pair_norm_ws(pl) : 0;
+}
+loka_status loka_bf16_linear_norm(const loka_linear_args* a, void* ws, size_t ws_bytes, loka_stream_t stream) {
+  PnPlan pl;
+  loka_status st = bf16_plan(a, &pl);
+  if (st != LOKA_OK) return st;
+  return run_pair_norm(a, pl, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
 }
 
 loka_status loka_fp8_linear_norm(const loka_linear_args* a, void* ws, size_t ws_bytes, loka_stream_t stream) {

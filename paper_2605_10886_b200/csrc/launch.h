@@ -339,7 +339,9 @@ struct PairNormParams {
   int32_t dbg;         // measurement knobs (LOKA_PN_DEBUG; results are wrong when set): 1 = no
                        // waits for peers' records, 2 = no statistics pass
   uint64_t* trace;     // nullable: globaltimer stamps [CTA][tile < 64][8] (loka_debug_pairnorm_trace)
+  int32_t bf16_in;     // 1: BF16 operands (kind::f16), K in elements, maps are byte views (2K wide)
 };
+const float* pair_norm_unit_scale();  // device address of 1.0f (the BF16 path's s_a = s_b)
 // tn = 512 (one accumulator, two N = 256 MMAs per K step) or 256 (double-buffered accumulators)
 cudaError_t launch_pair_norm(const PairNormParams& p, int tn, int pairs, cudaStream_t st);
 }  // namespace loka

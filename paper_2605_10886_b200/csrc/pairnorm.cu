@@ -99,7 +99,10 @@ LOKA_DEVINL float hswish(float x) {  // x * ReLU6(x + 3) / 6
   return __fdiv_rn(__fmul_rn(x, t), 6.f);
 }
 
-template <int TN, int NORM>
+// BF16IN: BF16 operands (kind::f16; a 128-byte stage row holds 64 K elements; the maps are byte views
+// of the bf16 data): the library's own BF16 path with the same fused epilogue (SURVEY.md §8(d)'s
+// secondary denominator, separating the FP8 gain from the fusion gain)
+template <int TN, int NORM, bool BF16IN>
 __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_constant__ PairNormParams p) {
   using Cf = PnCfg<TN>;
   constexpr int kHN = TN / 2;     // columns per epilogue thread
@@ -159,7 +162,7 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int nkb = (p.K + 127) / 128;
+  const int nkb = (p.K * (BF16IN ? 2 : 1) + 127) / 128;  // 128-byte K stages
 
   if (warp == 0) {
     // ===== TMA producer (both CTAs): this CTA's 128 A rows and half of each 256-row B half =====
@@ -184,7 +187,7 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
   } else if (warp == 1) {
     // ===== MMA issuer (leader only) =====
     if (lane == 0 && rank == 0) {
-      const uint32_t idesc = idesc_f8f6f4(p.a_fmt, p.b_fmt, 256, 256);
+      const uint32_t idesc = BF16IN ? idesc_bf16(256, 256) : idesc_f8f6f4(p.a_fmt, p.b_fmt, 256, 256);
       int it = 0, mb, nb;
       for (int j = 0; tile_of(j, mb, nb); ++j) {
         const int buf = Cf::kAcc == 1 ? 0 : (j & 1);
@@ -205,9 +208,12 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
 #pragma unroll
           for (int k = 0; k < 4; ++k)
 #pragma unroll
-            for (int hh = 0; hh < TN / 256; ++hh)
-              mma_f8f6f4_cg2(dacc + hh * 256, smem_desc_kmajor_sw128(a0 + k * 32),
-                             smem_desc_kmajor_sw128(b0 + hh * 16384 + k * 32), idesc, (kb | k) ? 1u : 0u);
+            for (int hh = 0; hh < TN / 256; ++hh) {
+              const uint64_t da = smem_desc_kmajor_sw128(a0 + k * 32);
+              const uint64_t db = smem_desc_kmajor_sw128(b0 + hh * 16384 + k * 32);
+              if constexpr (BF16IN) mma_bf16_cg2(dacc + hh * 256, da, db, idesc, (kb | k) ? 1u : 0u);
+              else mma_f8f6f4_cg2(dacc + hh * 256, da, db, idesc, (kb | k) ? 1u : 0u);
+            }
           mma_commit_cg2_mc(&empty_bar[s], 3);
         }
         mma_commit_cg2_mc(&acc_full[buf], 3);
@@ -601,10 +607,11 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
   }
 }
 
-template <int TN, int NORM>
+template <int TN, int NORM, bool BF16IN>
 static cudaError_t launch_pn(const PairNormParams& p, int pairs, cudaStream_t st) {
   {
-    cudaError_t e = ensure_func_attrs(reinterpret_cast<const void*>(pair_norm_kernel<TN, NORM>), PnCfg<TN>::kSmem);
+    cudaError_t e =
+        ensure_func_attrs(reinterpret_cast<const void*>(pair_norm_kernel<TN, NORM, BF16IN>), PnCfg<TN>::kSmem);
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg = {};
@@ -621,7 +628,7 @@ static cudaError_t launch_pn(const PairNormParams& p, int pairs, cudaStream_t st
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, pair_norm_kernel<TN, NORM>, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, pair_norm_kernel<TN, NORM, BF16IN>, p);
   note_launch();
   return e;
 }
@@ -629,15 +636,29 @@ static cudaError_t launch_pn(const PairNormParams& p, int pairs, cudaStream_t st
 template <int TN>
 static cudaError_t launch_pn_norm(const PairNormParams& p, int pairs, cudaStream_t st) {
   switch (p.norm) {
-    case LOKA_NORM_LAYER: return launch_pn<TN, LOKA_NORM_LAYER>(p, pairs, st);
-    case LOKA_NORM_RMS: return launch_pn<TN, LOKA_NORM_RMS>(p, pairs, st);
-    case LOKA_NORM_BLOCK_RMS: return launch_pn<TN, LOKA_NORM_BLOCK_RMS>(p, pairs, st);
+    case LOKA_NORM_LAYER: return launch_pn<TN, LOKA_NORM_LAYER, false>(p, pairs, st);
+    case LOKA_NORM_RMS: return launch_pn<TN, LOKA_NORM_RMS, false>(p, pairs, st);
+    case LOKA_NORM_BLOCK_RMS: return launch_pn<TN, LOKA_NORM_BLOCK_RMS, false>(p, pairs, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t launch_pair_norm(const PairNormParams& p, int tn, int pairs, cudaStream_t st) {
+  if (p.bf16_in) {  // (256-wide tiles only)
+    switch (p.norm) {
+      case LOKA_NORM_LAYER: return launch_pn<256, LOKA_NORM_LAYER, true>(p, pairs, st);
+      case LOKA_NORM_RMS: return launch_pn<256, LOKA_NORM_RMS, true>(p, pairs, st);
+      case LOKA_NORM_BLOCK_RMS: return launch_pn<256, LOKA_NORM_BLOCK_RMS, true>(p, pairs, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   return tn == 512 ? launch_pn_norm<512>(p, pairs, st) : launch_pn_norm<256>(p, pairs, st);
+}
+
+__device__ const float g_pn_one = 1.0f;  // the unit scale of the BF16 path
+const float* pair_norm_unit_scale() {
+  void* a = nullptr;
+  return cudaGetSymbolAddress(&a, g_pn_one) == cudaSuccess ? static_cast<const float*>(a) : nullptr;
 }
 
 }  // namespace loka

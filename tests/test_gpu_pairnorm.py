@@ -170,3 +170,15 @@ def test_cfg5_shape_sampled(M):
     yf, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, a_gran="tensor", b_gran="tensor", norm="layer", out_dtype="f32")
     torch.cuda.synchronize()
     _check(yf[torch.from_numpy(rows).to(DEV)], yo, "f32")
+
+
+@pytest.mark.parametrize("M,N,K,norm", [(600, 4096, 1000, "layer"), (300, 512, 256, "rms"), (520, 768, 384, "block_rms")])
+def test_bf16_path_same_epilogue(M, N, K, norm):
+    """The library's own BF16 (kind::f16) path with the same fused epilogue (SURVEY.md §8(d)'s secondary
+    denominator): y = norm(X W^T) on the bf16 values, against the oracle's FP64 linear + norm at 2e-3."""
+    x = synth.heavy(M, K, 2)
+    w = synth.weight(N, K, 3)
+    y, _ = lk.loka_bf16_linear_norm(to_dev_padded(x), to_dev_padded(w), norm=norm, norm_block=256, out_dtype="f32")
+    torch.cuda.synchronize()
+    yo = oracle.linear.apply_norm(oracle.linear.fwd(x.double().numpy(), w.double().numpy()), norm, block=256)
+    assert guarded_rel_err(f64(y), yo) <= TOL
