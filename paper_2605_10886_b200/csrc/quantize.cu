@@ -252,30 +252,41 @@ __global__ void __launch_bounds__(256) quant_1x128_kernel(QuantParams p) {
   const Tin* xr = reinterpret_cast<const Tin*>(p.x) + row * p.ldx;
   const int64_t cols = p.cols;
   const int64_t nblk = (cols + 127) / 128;
-  for (int64_t c0 = 0; c0 < cols; c0 += 256) {
-    const int64_t c = c0 + lane * 8;
-    Vec8<Tin> t;
-    if (c + 8 <= cols) t.load(xr + c);
-    else if (c < cols) t.load_partial(xr + c, (int)(cols - c));
-    else t.zero();
-    uint32_t am = t.amax_bits();
+  constexpr int U = 4;  // 256-column steps whose loads are in flight together (x and q may alias: all
+                        // loads of a group precede its stores, and the groups cover disjoint columns)
+  for (int64_t g0 = 0; g0 < cols; g0 += 256 * U) {
+    Vec8<Tin> t[U];
 #pragma unroll
-    for (int o = 8; o >= 1; o >>= 1) am = max(am, __shfl_xor_sync(0xFFFFFFFFu, am, o));
-    flag_nonfinite(am, p.status);
-    float s, r;
-    scales_from_amax<FMT, SF>(__uint_as_float(am), s, r);
-    const int64_t blk = c0 / 128 + (lane >> 4);
-    if ((lane & 15) == 0 && blk < nblk) {
-      if (p.scales) p.scales[row * nblk + blk] = s;
-      if (p.scales_t) p.scales_t[blk * p.rows + row] = s;  // transposed frame: BLK_128x1 [nblk, rows]
+    for (int u = 0; u < U; ++u) {
+      const int64_t c = g0 + 256 * u + lane * 8;
+      if (c + 8 <= cols) t[u].load(xr + c);
+      else if (c < cols) t[u].load_partial(xr + c, (int)(cols - c));
+      else t[u].zero();
     }
-    if (c < cols) {
-      uint2 code = cast8<FMT>(t, r);
-      const int n = (int)imin64(8, cols - c);
-      if (p.q) store8(p.q + row * p.ldq + c, code, n);
-      if (p.qt) {
-        const uint8_t* b = reinterpret_cast<const uint8_t*>(&code);
-        for (int i = 0; i < n; ++i) p.qt[(c + i) * p.ldqt + row] = b[i];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t c0 = g0 + 256 * u;
+      if (c0 >= cols) break;  // (uniform over the warp)
+      const int64_t c = c0 + lane * 8;
+      uint32_t am = t[u].amax_bits();
+#pragma unroll
+      for (int o = 8; o >= 1; o >>= 1) am = max(am, __shfl_xor_sync(0xFFFFFFFFu, am, o));
+      flag_nonfinite(am, p.status);
+      float s, r;
+      scales_from_amax<FMT, SF>(__uint_as_float(am), s, r);
+      const int64_t blk = c0 / 128 + (lane >> 4);
+      if ((lane & 15) == 0 && blk < nblk) {
+        if (p.scales) p.scales[row * nblk + blk] = s;
+        if (p.scales_t) p.scales_t[blk * p.rows + row] = s;  // transposed frame: BLK_128x1 [nblk, rows]
+      }
+      if (c < cols) {
+        uint2 code = cast8<FMT>(t[u], r);
+        const int n = (int)imin64(8, cols - c);
+        if (p.q) store8(p.q + row * p.ldq + c, code, n);
+        if (p.qt) {
+          const uint8_t* b = reinterpret_cast<const uint8_t*>(&code);
+          for (int i = 0; i < n; ++i) p.qt[(c + i) * p.ldqt + row] = b[i];
+        }
       }
     }
   }
@@ -284,46 +295,61 @@ __global__ void __launch_bounds__(256) quant_1x128_kernel(QuantParams p) {
 // ----- BLK_128x128: one CTA (8 warps) per 128x128 block, block held in registers --------
 template <typename Tin, int FMT, int SF>
 __global__ void __launch_bounds__(256) quant_128x128_kernel(QuantParams p) {
+  // two horizontally adjacent 128x128 blocks per CTA: all 16 loads per thread in flight before the
+  // first reduction (one block's 8 left the SMs' memory pipes half empty: 3.6 TB/s)
   pdl_wait();
-  __shared__ uint32_t red[8];
+  __shared__ uint32_t red[2][8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t bc = blockIdx.x, br = blockIdx.y;
+  const int64_t br = blockIdx.y;
   const int64_t nbc = (p.cols + 127) / 128, nbr = (p.rows + 127) / 128;
-  const int64_t col = bc * 128 + (lane & 15) * 8;
-  Vec8<Tin> v[8];
-  uint32_t am = 0;
+  Vec8<Tin> v[2][8];
+  uint32_t am[2] = {0u, 0u};
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int64_t row = br * 128 + warp * 16 + i * 2 + (lane >> 4);
-    const Tin* xr = reinterpret_cast<const Tin*>(p.x) + row * p.ldx;
-    if (row < p.rows && col + 8 <= p.cols) v[i].load(xr + col);
-    else if (row < p.rows && col < p.cols) v[i].load_partial(xr + col, (int)(p.cols - col));
-    else v[i].zero();
-    am = max(am, v[i].amax_bits());
+  for (int b = 0; b < 2; ++b) {
+    const int64_t col = (2 * (int64_t)blockIdx.x + b) * 128 + (lane & 15) * 8;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int64_t row = br * 128 + warp * 16 + i * 2 + (lane >> 4);
+      const Tin* xr = reinterpret_cast<const Tin*>(p.x) + row * p.ldx;
+      if (row < p.rows && col + 8 <= p.cols) v[b][i].load(xr + col);
+      else if (row < p.rows && col < p.cols) v[b][i].load_partial(xr + col, (int)(p.cols - col));
+      else v[b][i].zero();
+    }
   }
-  am = warp_max_u32(am);
-  if (lane == 0) red[warp] = am;
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) am[b] = max(am[b], v[b][i].amax_bits());
+    am[b] = warp_max_u32(am[b]);
+    if (lane == 0) red[b][warp] = am[b];
+  }
   __syncthreads();
-  am = red[0];
 #pragma unroll
-  for (int w = 1; w < 8; ++w) am = max(am, red[w]);
-  if (threadIdx.x == 0) flag_nonfinite(am, p.status);
-  float s, r;
-  scales_from_amax<FMT, SF>(__uint_as_float(am), s, r);
-  if (threadIdx.x == 0) {
-    if (p.scales) p.scales[br * nbc + bc] = s;
-    if (p.scales_t) p.scales_t[bc * nbr + br] = s;
-  }
+  for (int b = 0; b < 2; ++b) {
+    const int64_t bc = 2 * (int64_t)blockIdx.x + b;
+    if (bc >= nbc) break;
+    uint32_t a = red[b][0];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int64_t row = br * 128 + warp * 16 + i * 2 + (lane >> 4);
-    if (row >= p.rows || col >= p.cols) continue;
-    uint2 code = cast8<FMT>(v[i], r);
-    const int n = (int)imin64(8, p.cols - col);
-    if (p.q) store8(p.q + row * p.ldq + col, code, n);
-    if (p.qt) {
-      const uint8_t* b = reinterpret_cast<const uint8_t*>(&code);
-      for (int k = 0; k < n; ++k) p.qt[(col + k) * p.ldqt + row] = b[k];
+    for (int w = 1; w < 8; ++w) a = max(a, red[b][w]);
+    if (threadIdx.x == 0) flag_nonfinite(a, p.status);
+    float s, r;
+    scales_from_amax<FMT, SF>(__uint_as_float(a), s, r);
+    if (threadIdx.x == 0) {
+      if (p.scales) p.scales[br * nbc + bc] = s;
+      if (p.scales_t) p.scales_t[bc * nbr + br] = s;
+    }
+    const int64_t col = bc * 128 + (lane & 15) * 8;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int64_t row = br * 128 + warp * 16 + i * 2 + (lane >> 4);
+      if (row >= p.rows || col >= p.cols) continue;
+      uint2 code = cast8<FMT>(v[b][i], r);
+      const int n = (int)imin64(8, p.cols - col);
+      if (p.q) store8(p.q + row * p.ldq + col, code, n);
+      if (p.qt) {
+        const uint8_t* bb = reinterpret_cast<const uint8_t*>(&code);
+        for (int k = 0; k < n; ++k) p.qt[(col + k) * p.ldqt + row] = bb[k];
+      }
     }
   }
 }
@@ -511,7 +537,7 @@ static cudaError_t launch_quant_t(const QuantParams& p, int gran, int phase, flo
       break;
     case LOKA_GRAN_BLK_128x128:
       e = launch_pdl(quant_128x128_kernel<Tin, FMT, SF>,
-                     dim3((unsigned)((p.cols + 127) / 128), (unsigned)((p.rows + 127) / 128)), blk, st, p);
+                     dim3((unsigned)((p.cols + 255) / 256), (unsigned)((p.rows + 127) / 128)), blk, st, p);
       break;
     case LOKA_GRAN_TENSOR: {
       int64_t nb = (p.rows + 7) / 8;
