@@ -736,7 +736,11 @@ struct PnPlan {
 static PnPlan pair_norm_plan(const loka_linear_args* a, int sms) {
   PnPlan pl;
   const int env = pair_norm_env();
-  if (!a || env == 0 || !use_pair_kernel() || is_mx(a) || a->bwd_xhat || a->save_xhat || a->save_rstd) return pl;
+  if (!a || env == 0 || !use_pair_kernel() || is_mx(a) || a->save_xhat || a->save_rstd) return pl;
+  const bool bwd = a->bwd_xhat != nullptr;  // NEXT-1 norm backward: bf16 / f32 dz, no bias, 256-wide tiles
+  if (bwd && (!a->bwd_rstd || a->bias || is_fp8(a->y.dtype) || (a->bwd_xhat_ld * 2) % 16 || a->bwd_xhat_ld < a->N ||
+              !aligned16(a->bwd_xhat)))
+    return pl;
   if (a->a.gran != LOKA_GRAN_TENSOR && a->a.gran != LOKA_GRAN_ROW) return pl;
   if (a->b.gran != LOKA_GRAN_TENSOR && a->b.gran != LOKA_GRAN_ROW) return pl;
   const bool blk = a->norm == LOKA_NORM_BLOCK_RMS;
@@ -747,7 +751,7 @@ static PnPlan pair_norm_plan(const loka_linear_args* a, int sms) {
   // 256-wide tiles with double-buffered accumulators by default: the epilogue (two TMEM passes and
   // the row-record exchange) runs under the next tile's MMAs; WIDE 512-column tiles (LOKA_PAIRNORM=512)
   // move 25% fewer operand bytes per FLOP but expose the whole epilogue (measured slower)
-  pl.tn = (env == 256 || env == 512) ? env : 256;
+  pl.tn = bwd ? 256 : (env == 256 || env == 512) ? env : 256;
   pl.tiles_n = (int)cdiv(a->N, pl.tn);
   pl.row_blocks = (int)cdiv(a->M, 256);
   pl.xchg = pl.tiles_n > 1 && (!blk || fp8_out);
@@ -817,6 +821,14 @@ static loka_status run_pair_norm(const loka_linear_args* a, const PnPlan& pl, vo
   p.order = pl.order;
   p.ngroups = pl.groups;
   if (const char* e = std::getenv("LOKA_PN_DEBUG")) p.dbg = std::atoi(e);
+  if (a->bwd_xhat) {
+    p.bwd = 1;
+    p.xhat = static_cast<const __nv_bfloat16*>(a->bwd_xhat);
+    p.ld_xhat = a->bwd_xhat_ld;
+    p.rstd_in = a->bwd_rstd;
+    if (!make_map_out(&p.tx, const_cast<void*>(a->bwd_xhat), a->M, a->N, a->bwd_xhat_ld, LOKA_BF16, 128, 32u))
+      return LOKA_ERR_CUDA;
+  }
   p.trace = g_pn_trace;
   if (pl.xchg) {
     // the records start as 0xFF bytes (the sentinel NaN the readers wait on), every launch

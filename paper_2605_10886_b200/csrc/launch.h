@@ -340,6 +340,12 @@ struct PairNormParams {
                        // waits for peers' records, 2 = no statistics pass
   uint64_t* trace;     // nullable: globaltimer stamps [CTA][tile < 64][8] (loka_debug_pairnorm_trace)
   int32_t bf16_in;     // 1: BF16 operands (kind::f16), K in elements, maps are byte views (2K wide)
+  // NEXT-1 backward: the accumulator is dL/dh; xhat (bf16 [M, N], ld_xhat) and rstd_in ([M], BLOCK_RMS
+  // [M, N/256]) are the forward's saves; bf16 / f32 dz out
+  int32_t bwd;
+  const __nv_bfloat16* xhat; int64_t ld_xhat;
+  const float* rstd_in;
+  CUtensorMap tx;      // bwd with bf16 dz: xhat [M, N] box {64 elements, 32 rows} SW128
 };
 const float* pair_norm_unit_scale();  // device address of 1.0f (the BF16 path's s_a = s_b)
 // tn = 512 (one accumulator, two N = 256 MMAs per K step) or 256 (double-buffered accumulators)

@@ -102,7 +102,8 @@ LOKA_DEVINL float hswish(float x) {  // x * ReLU6(x + 3) / 6
 // BF16IN: BF16 operands (kind::f16; a 128-byte stage row holds 64 K elements; the maps are byte views
 // of the bf16 data): the library's own BF16 path with the same fused epilogue (SURVEY.md §8(d)'s
 // secondary denominator, separating the FP8 gain from the fusion gain)
-template <int TN, int NORM, bool BF16IN>
+// BWD: the NEXT-1 norm backward epilogue (a separate instance, so the forward carries none of it)
+template <int TN, int NORM, bool BF16IN, bool BWD>
 __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_constant__ PairNormParams p) {
   using Cf = PnCfg<TN>;
   constexpr int kHN = TN / 2;     // columns per epilogue thread
@@ -115,7 +116,8 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
   uint64_t* empty_bar = full_bar + Cf::kStages;
   uint64_t* acc_full = empty_bar + Cf::kStages;  // [2]
   uint64_t* acc_empty = acc_full + 2;           // [2] (the leader's is used)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* xbar = acc_empty + 2;  // [8] backward: the warps' staged xhat sub-tiles landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbar + kPnEpiWarps);
   float4* hrec = reinterpret_cast<float4*>(smem + Cf::kOffRec);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -153,6 +155,7 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], 2 * kPnEpiWarps);
     }
+    for (int w = 0; w < kPnEpiWarps; ++w) mbar_init(&xbar[w], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc_cg2<512>(tmem_slot);
@@ -236,7 +239,10 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
     const bool act = p.act == LOKA_ACT_HARDSWISH;
     // fold: with a tensor-wide s_b and no bias, y = acc * c (c = s_a s_b per row), so the statistics
     // are taken on acc and scaled (mean * c, M2 * c^2), and pass N is one FMA per element
-    const bool fold = !p.sb_row && p.bias == nullptr;
+    constexpr bool bwd = BWD;  // NEXT-1 norm backward (dL/dz from dL/dh, the forward's saved xhat / rstd)
+    const bool xs_stage = BWD && p.out_dtype == LOKA_BF16;  // xhat staged in smem (bf16 dz boxes match it)
+    uint32_t xph = 0;
+    const bool fold = !p.sb_row && p.bias == nullptr && !bwd;
     const bool need_x = xchg && (NORM != LOKA_NORM_BLOCK_RMS || fp8_out);
     float4* xrec = reinterpret_cast<float4*>(p.xws);
     int nbox = 0;
@@ -261,6 +267,18 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
         }
       }
       named_bar_sync(2, 32 * kPnEpiWarps);
+      // backward with bf16 dz: this warp's xhat sub-tile (32 rows x 128 columns, 8 KB) is TMA-loaded into
+      // its output staging area (two 32 x 64 SW128 boxes, exactly the layout of the dz boxes it will
+      // store), so both passes read it from smem and pass N overwrites each chunk's xhat with its dz
+      if constexpr (BWD) {
+        if (xs_stage && lane == 0) {
+          bulk_wait_read0();  // the previous tile's dz boxes have been read out of the staging area
+          mbar_arrive_expect_tx(&xbar[warp - 2], 8192u);
+          const int xr0 = mb * 256 + rank * 128 + q * 32, xc0 = nb * TN + h * kHN;
+          tma_load_2d(stg, &p.tx, &xbar[warp - 2], xc0, xr0);
+          tma_load_2d(stg + 4096, &p.tx, &xbar[warp - 2], xc0 + 64, xr0);
+        }
+      }
       if (lane == 0) mbar_wait(&acc_full[buf], use & 1u, 3);
       __syncwarp();
       tc_fence_after();
@@ -285,6 +303,51 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
           const float2 b = fadd2(fmul2(make_float2(y[c + 2], y[c + 3]), fmul2(sa2, make_float2(s4.z, s4.w))),
                                  make_float2(b4.z, b4.w));
           y[c] = a.x; y[c + 1] = a.y; y[c + 2] = b.x; y[c + 3] = b.y;
+        }
+      };
+      // backward: g = dh * act'(xhat gamma + beta) * gamma for one chunk (y: dequantized dh in, g out), and
+      // the chunk's saved xhat values (bf16, global) into xv
+      auto load_g = [&](float (&y)[32], int cb, float (&xv)[32]) {
+        if (xs_stage) {  // from the staged SW128 box (cb / 64), 16-B pieces (cb % 64) / 8 .. + 3 of row `lane`
+          const uint32_t base = smem_u32(stg) + (uint32_t)(cb / 64) * 4096u + (uint32_t)lane * 128u;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t pc = ((uint32_t)((cb % 64) / 8 + u)) ^ ((uint32_t)lane & 7u);
+            uint4 w;
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                         : "r"(base + (pc << 4)));
+            xv[8 * u + 0] = bf16lo_to_f32(w.x); xv[8 * u + 1] = bf16hi_to_f32(w.x);
+            xv[8 * u + 2] = bf16lo_to_f32(w.y); xv[8 * u + 3] = bf16hi_to_f32(w.y);
+            xv[8 * u + 4] = bf16lo_to_f32(w.z); xv[8 * u + 5] = bf16hi_to_f32(w.z);
+            xv[8 * u + 6] = bf16lo_to_f32(w.w); xv[8 * u + 7] = bf16hi_to_f32(w.w);
+          }
+        } else if (row_ok) {
+          const uint4* src = reinterpret_cast<const uint4*>(p.xhat + (int64_t)grow * p.ld_xhat + col0 + cb);
+          uint4 w[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) w[u] = (col0 + cb + 8 * u < p.N) ? __ldg(src + u) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            xv[8 * u + 0] = bf16lo_to_f32(w[u].x); xv[8 * u + 1] = bf16hi_to_f32(w[u].x);
+            xv[8 * u + 2] = bf16lo_to_f32(w[u].y); xv[8 * u + 3] = bf16hi_to_f32(w[u].y);
+            xv[8 * u + 4] = bf16lo_to_f32(w[u].z); xv[8 * u + 5] = bf16hi_to_f32(w[u].z);
+            xv[8 * u + 6] = bf16lo_to_f32(w[u].w); xv[8 * u + 7] = bf16hi_to_f32(w[u].w);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) xv[k] = 0.f;
+        }
+        if (has_gb || act) {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const float ga = colp[2 * TN + h * kHN + cb + k], be = colp[3 * TN + h * kHN + cb + k];
+            float g = y[k];
+            if (act) {  // h-swish' at u = xhat gamma + beta (PyTorch at the kinks: 0 below -3, 1 above 3)
+              const float u = fmaf(xv[k], ga, be);
+              g = g * (u < -3.f ? 0.f : (u > 3.f ? 1.f : __fdiv_rn(fmaf(2.f, u, 3.f), 6.f)));
+            }
+            y[k] = g * ga;
+          }
         }
       };
       // both passes stream the thread's kHN columns out of TMEM in 32-column chunks, the next chunk's
@@ -315,10 +378,30 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
       // the LayerNorm chunk M2 is corrected for them and max / min skip them.
       float ss = 0.f, ymax = -INFINITY, ymin = INFINITY;
       float mean = 0.f, m2 = 0.f, nacc = 0.f;
+      float sg = 0.f, sgx = 0.f;  // backward: sum g, sum g xhat
       auto stats_chunk = [&](float (&y)[32], int c) {
         const int cb = 32 * c;
         const int nv = max(0, min(32, p.N - (col0 + cb)));
         if (!fold) dequant(y, cb);
+        if constexpr (BWD) {  // (columns >= N: dh = 0 and xhat = 0)
+          float xv[32];
+          load_g(y, cb, xv);
+          float2 a0 = make_float2(0.f, 0.f), a1 = a0;
+#pragma unroll
+          for (int k = 0; k < 32; k += 4) {
+            a0 = ffma2(make_float2(y[k], y[k + 1]), make_float2(xv[k], xv[k + 1]), a0);
+            a1 = ffma2(make_float2(y[k + 2], y[k + 3]), make_float2(xv[k + 2], xv[k + 3]), a1);
+          }
+          a0 = fadd2(a0, a1);
+          sgx += a0.x + a0.y;
+          if constexpr (NORM == LOKA_NORM_LAYER) {
+            float t = 0.f;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) t += y[k];
+            sg += t;
+          }
+          return;
+        }
         if (nv > 0 && fp8_out) {
           if (nv == 32) {
 #pragma unroll
@@ -372,6 +455,13 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
           ss += q0.x + q0.y;
         }
       };
+      if constexpr (BWD) {
+        if (xs_stage) {
+          if (lane == 0) mbar_wait(&xbar[warp - 2], xph, 8);
+          xph ^= 1u;
+          __syncwarp();
+        }
+      }
       if (!(p.dbg & 2)) stream_tmem(stats_chunk, false);
       if (tr) tr[1] = globaltimer_ns();
       if (fold) {  // back to y = c acc (the statistics of y)
@@ -381,7 +471,8 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
       }
 
       // ---- the two halves of the row (fixed order h = 0, 1), then the Case 2 exchange ----
-      hrec[h * 128 + r] = make_float4(NORM == LOKA_NORM_LAYER ? mean : ss, m2, ymax, ymin);
+      hrec[h * 128 + r] = bwd ? make_float4(sg, sgx, 0.f, 0.f)
+                              : make_float4(NORM == LOKA_NORM_LAYER ? mean : ss, m2, ymax, ymin);
       named_bar_sync(1, 32 * kPnEpiWarps);
       // z = y rstd + c0; with folding z = acc (c rstd) + c0 and ymax / ymin are of acc
       float rstd = 1.f, c0 = 0.f, amax = 0.f;
@@ -389,8 +480,11 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
       {
         const float4 v0 = hrec[r], v1 = hrec[128 + r];
         const int n0 = max(0, min(kHN, p.N - nb * TN)), n1 = max(0, min(kHN, p.N - nb * TN - kHN));
-        float4 cr;  // this CTA's record of the row: (mean | ss, M2, ymax, ymin)
-        if constexpr (NORM == LOKA_NORM_LAYER) {
+        float4 cr;  // this CTA's record of the row: (mean | ss, M2, ymax, ymin); backward (sum g, sum g xhat)
+        if (bwd) {
+          cr = (NORM == LOKA_NORM_BLOCK_RMS && TN == 512) ? (h ? v1 : v0)
+                                                            : make_float4(v0.x + v1.x, v0.y + v1.y, 0.f, 0.f);
+        } else if constexpr (NORM == LOKA_NORM_LAYER) {
           const float n = (float)(n0 + n1);
           const float mu = n > 0.f ? __fdiv_rn(fmaf((float)n0, v0.x, (float)n1 * v1.x), n) : 0.f;
           const float d0 = v0.x - mu, d1 = v1.x - mu;
@@ -434,6 +528,7 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
             for (int u = 0; u < 8; ++u)
               if (k0 + u < kb1 && rec_pending(v[u])) v[u] = rec_wait(xrec + (rb + 2 * (k0 + u)) * 128 + r);
           };
+          float sy = 0.f;  // backward: sum of the records' sum g xhat
           for (int k0 = kb0; k0 < kb1; k0 += 8) {  // sum n_k mean_k (LayerNorm) | sum ss_k; max / min
             load8(k0);
 #pragma unroll
@@ -441,13 +536,14 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
               if (k0 + u < kb1) {
                 const float nk = (float)max(0, min(TN, p.N - (k0 + u) * TN));
                 n += nk;
-                sm = NORM == LOKA_NORM_LAYER ? fmaf(nk, v[u].x, sm) : sm + v[u].x;
+                sm = (NORM == LOKA_NORM_LAYER && !bwd) ? fmaf(nk, v[u].x, sm) : sm + v[u].x;
+                sy += v[u].y;
                 mx = fmaxf(mx, v[u].z);
                 mn = fminf(mn, v[u].w);
               }
           }
-          float pm = sm, pm2 = 0.f;  // LayerNorm: this half's (mean, M2) of its tiles
-          if constexpr (NORM == LOKA_NORM_LAYER) {
+          float pm = sm, pm2 = bwd ? sy : 0.f;  // LayerNorm: this half's (mean, M2) of its tiles
+          if (NORM == LOKA_NORM_LAYER && !bwd) {
             pm = n > 0.f ? __fdiv_rn(sm, n) : 0.f;
             for (int k0 = kb0; k0 < kb1; k0 += 8) {
               if (kb1 - kb0 > 8) load8(k0);  // (more than 8 tiles per half, G > 16: load again)
@@ -464,7 +560,9 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
           hrec[h * 128 + r] = make_float4(pm, pm2, mx, mn);
           named_bar_sync(1, 32 * kPnEpiWarps);
           const float4 a0 = hrec[r], a1 = hrec[128 + r];
-          if constexpr (NORM == LOKA_NORM_LAYER) {
+          if (bwd) {
+            cr = make_float4(a0.x + a1.x, a0.y + a1.y, 0.f, 0.f);
+          } else if constexpr (NORM == LOKA_NORM_LAYER) {
             const float na = (float)min((G + 1) / 2 * TN, p.N), nbb = (float)p.N - na;
             const float mu = __fdiv_rn(fmaf(na, a0.x, nbb * a1.x), (float)p.N);
             const float d0 = a0.x - mu, d1 = a1.x - mu;
@@ -477,13 +575,21 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
         }
         named_bar_sync(1, 32 * kPnEpiWarps);  // hrec reads done before the next tile's writes
         const float nrow = (float)p.N;
-        if constexpr (NORM == LOKA_NORM_LAYER) {
+        if (bwd) {  // mean(g) (LayerNorm), mean(g xhat) over the row (BlockNorm: its 256-column block)
+          const float nb = NORM == LOKA_NORM_BLOCK_RMS ? 256.f : nrow;
+          c0 = NORM == LOKA_NORM_LAYER ? __fdiv_rn(cr.x, nb) : 0.f;
+          amax = __fdiv_rn(cr.y, nb);  // (mean(g xhat), kept in amax's register)
+          rstd = row_ok ? (NORM == LOKA_NORM_BLOCK_RMS ? __ldg(p.rstd_in + (int64_t)grow * (p.N / 256) + (col0 / 256))
+                                                       : __ldg(p.rstd_in + grow))
+                        : 0.f;
+        } else if constexpr (NORM == LOKA_NORM_LAYER) {
           rstd = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(cr.y, nrow), p.eps)));
           c0 = -__fmul_rn(cr.x, rstd);
         } else if constexpr (NORM == LOKA_NORM_RMS) {
           rstd = __fdiv_rn(1.f, __fsqrt_rn(__fadd_rn(__fdiv_rn(cr.x, nrow), p.eps)));
         }
-        if constexpr (NORM != LOKA_NORM_BLOCK_RMS) {
+        if (bwd) {
+        } else if constexpr (NORM != LOKA_NORM_BLOCK_RMS) {
           if (fp8_out) {  // the stored values are fma(y_or_acc, rs, c0): monotone, exact at ymax / ymin
             const float rs = __fmul_rn(sc, rstd);
             amax = fmaxf(fabsf(fmaf(cr.z, rs, c0)), fabsf(fmaf(cr.w, rs, c0)));
@@ -506,9 +612,16 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
       const float rs = __fmul_rn(sc, rstd);
       const float2 r2 = make_float2(rs, rs), c02 = make_float2(c0, c0);
       float amx = 0.f;
+      const float mgx = bwd ? amax : 0.f;
       auto out_chunk = [&](float (&y)[32], int c) {
         const int cb = 32 * c;
         if (!fold) dequant(y, cb);
+        if constexpr (BWD) {  // dz = rstd (g - mean(g) - xhat mean(g xhat))
+          float xv[32];
+          load_g(y, cb, xv);
+#pragma unroll
+          for (int k = 0; k < 32; ++k) y[k] = rstd * (y[k] - c0 - xv[k] * mgx);
+        } else {
 #pragma unroll
         for (int k = 0; k < 32; k += 4) {
           float2 a = ffma2(make_float2(y[k], y[k + 1]), r2, c02);
@@ -525,6 +638,7 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
 #pragma unroll
           for (int k = 0; k < 32; ++k) y[k] = hswish(y[k]);
         }
+        }
         const int nv = max(0, min(32, p.N - (col0 + cb)));
         if (p.amax_out && row_ok) {
 #pragma unroll
@@ -538,8 +652,10 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
             if (k < nv) dst[k] = y[k];
         }
         const int in_box = cb % cpb;
-        uint8_t* box = stg + (nbox & 1) * 4096;
-        if (in_box == 0) {  // this buffer's previous store (two boxes ago) must have been read
+        // (backward with staged xhat: 2 bf16 boxes per tile, so box (nbox & 1) == cb / 64 and each chunk's
+        // dz overwrites exactly its own, already consumed, xhat pieces of this lane's row)
+        uint8_t* box = stg + (xs_stage ? (cb / 64) : (nbox & 1)) * 4096;
+        if (in_box == 0 && !xs_stage) {  // this buffer's previous store (two boxes ago) must have been read
           if (lane == 0) bulk_wait_read_le1();
           __syncwarp();
         }
@@ -607,11 +723,11 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
   }
 }
 
-template <int TN, int NORM, bool BF16IN>
+template <int TN, int NORM, bool BF16IN, bool BWD = false>
 static cudaError_t launch_pn(const PairNormParams& p, int pairs, cudaStream_t st) {
   {
     cudaError_t e =
-        ensure_func_attrs(reinterpret_cast<const void*>(pair_norm_kernel<TN, NORM, BF16IN>), PnCfg<TN>::kSmem);
+        ensure_func_attrs(reinterpret_cast<const void*>(pair_norm_kernel<TN, NORM, BF16IN, BWD>), PnCfg<TN>::kSmem);
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg = {};
@@ -628,7 +744,7 @@ static cudaError_t launch_pn(const PairNormParams& p, int pairs, cudaStream_t st
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, pair_norm_kernel<TN, NORM, BF16IN>, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, pair_norm_kernel<TN, NORM, BF16IN, BWD>, p);
   note_launch();
   return e;
 }
@@ -644,6 +760,14 @@ static cudaError_t launch_pn_norm(const PairNormParams& p, int pairs, cudaStream
 }
 
 cudaError_t launch_pair_norm(const PairNormParams& p, int tn, int pairs, cudaStream_t st) {
+  if (p.bwd) {  // (256-wide tiles, FP8 operands)
+    switch (p.norm) {
+      case LOKA_NORM_LAYER: return launch_pn<256, LOKA_NORM_LAYER, false, true>(p, pairs, st);
+      case LOKA_NORM_RMS: return launch_pn<256, LOKA_NORM_RMS, false, true>(p, pairs, st);
+      case LOKA_NORM_BLOCK_RMS: return launch_pn<256, LOKA_NORM_BLOCK_RMS, false, true>(p, pairs, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   if (p.bf16_in) {  // (256-wide tiles only)
     switch (p.norm) {
       case LOKA_NORM_LAYER: return launch_pn<256, LOKA_NORM_LAYER, true>(p, pairs, st);

@@ -182,3 +182,34 @@ def test_bf16_path_same_epilogue(M, N, K, norm):
     torch.cuda.synchronize()
     yo = oracle.linear.apply_norm(oracle.linear.fwd(x.double().numpy(), w.double().numpy()), norm, block=256)
     assert guarded_rel_err(f64(y), yo) <= TOL
+
+
+@pytest.mark.parametrize("norm,N,act,affine", [("layer", 4096, "none", False), ("layer", 2304, "hardswish", True),
+                                               ("rms", 1024, "none", True), ("block_rms", 4096, "hardswish", False),
+                                               ("block_rms", 768, "none", False)])
+@pytest.mark.parametrize("od", ["f32", "bf16"])
+def test_norm_backward_on_pair_engine(tn, norm, N, act, affine, od):
+    """NEXT-1's norm backward fused into the pair engine's epilogue:
+    dh = A . B^T (the next layer's dgrad), g = dh act'(xhat gamma + beta) gamma, dz = rstd (g - mean g
+    - xhat mean(g xhat)) (RMS / BlockNorm without mean g), the row sums exchanged like the forward's
+    statistics; against oracle.linear.norm_backward on the same saved xhat / rstd at 2e-3."""
+    M, K2 = 600, 384
+    aq, as_ = lk.loka_quantize(to_dev_padded(synth.grad(M, K2, 3) * 1024), "e5m2", "row")
+    bq, bs = lk.loka_quantize(to_dev_padded(synth.weight(N, K2, 4)), "e4m3", "row")
+    rng = np.random.default_rng(N)
+    xh = torch.tensor(rng.normal(size=(M, N)), dtype=torch.bfloat16)
+    nb = N // 256
+    rstd = torch.tensor(rng.uniform(0.5, 2.0, size=(M, nb) if norm == "block_rms" else (M,)), dtype=torch.float32)
+    gamma = torch.tensor(1 + 0.2 * rng.normal(size=N), dtype=torch.float32) if affine else None
+    beta = torch.tensor(0.3 * rng.normal(size=N), dtype=torch.float32) if (affine and norm == "layer") else None
+    y, _ = lk.loka_fp8_linear_norm(aq, as_, bq, bs, a_fmt="e5m2", norm=norm, act=act, out_dtype=od,
+                                   bwd_xhat=xh.to(DEV), bwd_rstd=rstd.to(DEV), direction="dgrad",
+                                   gamma=None if gamma is None else gamma.to(DEV),
+                                   beta=None if beta is None else beta.to(DEV))
+    torch.cuda.synchronize()
+    dh = oracle.linear.linear_norm(aq.cpu().numpy(), as_.cpu().numpy(), "e5m2", "row", bq.cpu().numpy(),
+                                   bs.cpu().numpy(), "e4m3", "row")
+    dz = oracle.linear.norm_backward(dh, xh.double().numpy(), rstd.double().numpy(), norm,
+                                     gamma=None if gamma is None else gamma.double().numpy(),
+                                     beta=None if beta is None else beta.double().numpy(), act=act)
+    _check(y, dz, od)

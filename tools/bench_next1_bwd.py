@@ -51,7 +51,11 @@ def main():
                                              bwd_xhat=xh, bwd_rstd=rstd, direction="dgrad", keep=keep)
 
             wsb = torch.empty(max(1, lk.linear_workspace(args)), dtype=torch.uint8, device=dev)
-            row["path"] = "pair GEMM (FP32) + row-wise backward pass" if lk.linear_workspace(args) else "fused epilogue"
+            tiles = -(-M // 256) * -(-N // 256)
+            row[f"path_{od}"] = ("CTA-pair engine, norm backward fused in its epilogue (pairnorm.cu)"
+                                 if od == "bf16" and tiles >= 74 else
+                                 "CTA-pair GEMM (FP32) + row-wise backward pass (FP8 dz needs the row amax)"
+                                 if tiles >= 74 else "single-CTA fused epilogue (linear.cu)")
 
             def fp8_step():
                 lk.loka_quantize(dy, "e5m2", "row", out=dq, scales=ds, stream=stream)
