@@ -27,7 +27,7 @@ import torch.nn.functional as F  # noqa: E402
 
 import synth  # noqa: E402
 import paper_2605_10886_b200 as lk  # noqa: E402
-from bench import capture, time_steps  # noqa: E402
+from bench import ClockSampler, capture, time_steps  # noqa: E402
 
 
 def main():
@@ -69,6 +69,8 @@ def main():
     def fp8_gemm_only():
         assert lk._lib.loka_grouped_fp8_linear(64, arr, None, 0, sh) == 0
 
+    clk = ClockSampler(torch.cuda.current_device())
+    clk.__enter__()
     g8 = capture(fp8_step, stream)
     t8 = time_steps(g8.replay, a.steps, a.warmup, flush, stream)
     gg = capture(fp8_gemm_only, stream)
@@ -85,6 +87,7 @@ def main():
     gb = capture(bf16_step, stream)
     tb = time_steps(gb.replay, a.steps, a.warmup, flush, stream)
     ms8, msg, msb = sum(t8) / len(t8), sum(tg) / len(tg), sum(tb) / len(tb)
+    clk.__exit__()
 
     # ---- LoKA Probe: MERE of every FP8 layer against the BF16 path (one libloka call) ----
     g8.replay()
@@ -119,8 +122,19 @@ def main():
             f = sum(time_steps(capture(one_fp8, stream).replay, reps, 3, flush, stream)) / reps
             b = sum(time_steps(capture(one_bf16, stream).replay, reps, 3, flush, stream)) / reps
             ch = lk.loka_dispatch_select([("fp8_rowwise", "fwd", mere[8 * i + j], 1e3 * f)], 1e3 * b, 0.2, 1.05)
-            plan.append({"K": k, "N": n, "mere": round(mere[8 * i + j], 5), "fp8_us": round(1e3 * f, 2),
-                         "bf16_us": round(1e3 * b, 2), "choice": "fp8_rowwise" if ch == 0 else "baseline"})
+            # the same decision on the layer's share of the grouped steps (how the layer runs inside the
+            # ensemble: one grouped FP8 launch vs 64 BF16 GEMMs), FLOP-proportional
+            share = 2.0 * M * k * n / flops
+            chg = lk.loka_dispatch_select([("fp8_rowwise", "fwd", mere[8 * i + j], 1e3 * ms8 * share)],
+                                          1e3 * msb * share, 0.2, 1.05)
+            plan.append({"K": k, "N": n, "mere": round(mere[8 * i + j], 5), "max_rel": round(stats[8 * i + j]["max_rel"], 3),
+                         "n_floored": stats[8 * i + j]["n_floored"],
+                         "fp8_us_alone": round(1e3 * f, 2), "bf16_us_alone": round(1e3 * b, 2),
+                         "speedup_alone": round(b / f, 3), "choice_alone": "fp8_rowwise" if ch == 0 else "baseline",
+                         "speedup_grouped_share": round(msb / ms8, 3),
+                         "choice_grouped": "fp8_rowwise" if chg == 0 else "baseline",
+                         "binding": ("mere" if mere[8 * i + j] >= 0.2 else "") +
+                                    ("+speedup_alone" if b / f <= 1.05 else "")})
     out = {
         "workload": "cfg3: 64 GEMMs M=2048, K,N in " + str(S) + ", 8 shared inputs (odd ones heavy-tailed), bf16 out",
         "flop_per_step": flops,
@@ -133,8 +147,18 @@ def main():
         "probe": {"geomean_mere_all": round(geo(mere), 5), "geomean_mere_gaussian_inputs": round(geo(normal), 5),
                   "geomean_mere_heavy_inputs": round(geo(heavy), 5), "ref": "BF16 path (DESIGN.md D9)"},
         "dispatch": {"budget": 0.2, "min_speedup": 1.05,
-                     "fp8_layers": sum(p["choice"] != "baseline" for p in plan), "plan": plan},
+                     "fp8_layers_alone": sum(p["choice_alone"] != "baseline" for p in plan),
+                     "fp8_layers_grouped": sum(p["choice_grouped"] != "baseline" for p in plan),
+                     "layers_mere_below_budget": sum(p["mere"] < 0.2 for p in plan),
+                     "why": "MERE (P:192) is a mean of per-element relative errors; these synthetic layers' outputs "
+                            "are zero-centred, so elements near 0 dominate it (the floor f = 1e-6 mean|ref| "
+                            "barely clips them) and FP8's ~3-4% per-element error turns into MERE 0.2-0.6 > the "
+                            "paper's 0.2 budget (P:541) for most layers; alone, each small GEMM is launch/latency-"
+                            "bound and FP8's extra quantize launch makes it slower than BF16 (speedup_alone < 1), "
+                            "while inside the grouped launch FP8 is faster for every layer",
+                     "plan": plan},
         "l2": "flushed before every timed step", "timing": "CUDA-graph replays, CUDA events",
+        "clocks": clk.summary(),
     }
     s = json.dumps(out)
     print(s)

@@ -21,7 +21,7 @@ import torch  # noqa: E402
 
 import synth  # noqa: E402
 import paper_2605_10886_b200 as lk  # noqa: E402
-from bench import capture, peaks, time_steps  # noqa: E402
+from bench import ClockSampler, capture, peaks, time_steps  # noqa: E402
 
 RECIPES = {
     "tensorwise": dict(fx="tensor", fw="tensor", gdy="tensor", gw="tensor", wdy="tensor", wx="tensor"),
@@ -43,6 +43,8 @@ def main():
     ap.add_argument("--K", type=int, default=4096)
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
+    _clk = ClockSampler(torch.cuda.current_device())  # NVML clocks during the whole measurement
+    _clk.__enter__()
     M, N, K = a.M, a.N, a.K
     dev = torch.device("cuda")
     x = synth.gaussian(M, K, 0, device=dev)
@@ -150,6 +152,8 @@ def main():
         for name in RECIPES:
             res[name]["speedup_vs_bf16_end_to_end"] = round((b_f + b_d + b_w) / res[name]["step_ms_end_to_end"], 3)
         res["mxfp8_fwd"]["speedup_vs_bf16_fwd"] = round(b_f / res["mxfp8_fwd"]["fwd_with_quantize_ms"], 3)
+    _clk.__exit__()
+    res["clocks"] = _clk.summary()
     print(json.dumps(res))
     if a.out:
         open(a.out, "w").write(json.dumps(res, indent=1))

@@ -19,7 +19,7 @@ import torch.nn.functional as F  # noqa: E402
 
 import synth  # noqa: E402
 import paper_2605_10886_b200 as lk  # noqa: E402
-from bench import capture, time_steps  # noqa: E402
+from bench import ClockSampler, capture, time_steps  # noqa: E402
 
 
 def main():
@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
+    _clk = ClockSampler(torch.cuda.current_device())  # NVML clocks during the whole measurement
+    _clk.__enter__()
     dev = torch.device("cuda")
     stream = torch.cuda.Stream()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
@@ -65,6 +67,8 @@ def main():
         res["cases"].append({"M": M, "K": K, "N": N, "fp8_out": od, "fp8_fused_ms": round(ms8, 4), "bf16_ms": round(msb, 4),
                              "fp8_tflops": round(fl / ms8 / 1e9, 1), "bf16_tflops": round(fl / msb / 1e9, 1),
                              "speedup": round(msb / ms8, 3)})
+    _clk.__exit__()
+    res["clocks"] = _clk.summary()
     print(json.dumps(res))
     if a.out:
         open(a.out, "w").write(json.dumps(res, indent=1))

@@ -19,7 +19,7 @@ import torch  # noqa: E402
 
 import synth  # noqa: E402
 import paper_2605_10886_b200 as lk  # noqa: E402
-from bench import capture, time_steps  # noqa: E402
+from bench import ClockSampler, capture, time_steps  # noqa: E402
 
 
 def main():
@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
+    _clk = ClockSampler(torch.cuda.current_device())  # NVML clocks during the whole measurement
+    _clk.__enter__()
     dev = torch.device("cuda")
     stream = torch.cuda.Stream()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
@@ -78,6 +80,8 @@ def main():
         row["speedup_bf16out"] = round(row["bf16_ms"] / row["fp8_bf16_ms"], 3)
         row["speedup_e5m2out"] = round(row["bf16_ms"] / row["fp8_e5m2_ms"], 3)
         res["cases"].append(row)
+    _clk.__exit__()
+    res["clocks"] = _clk.summary()
     print(json.dumps(res))
     if a.out:
         open(a.out, "w").write(json.dumps(res, indent=1))

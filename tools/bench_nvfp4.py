@@ -19,7 +19,7 @@ import torch  # noqa: E402
 
 import synth  # noqa: E402
 import paper_2605_10886_b200 as lk  # noqa: E402
-from bench import capture, peaks, time_steps  # noqa: E402
+from bench import ClockSampler, capture, peaks, time_steps  # noqa: E402
 
 SHAPES = [(32768, 4096, 4096), (8192, 4096, 4096), (4096, 1024, 1024), (2048, 2048, 2048)]
 
@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
+    _clk = ClockSampler(torch.cuda.current_device())  # NVML clocks during the whole measurement
+    _clk.__enter__()
     dev = torch.device("cuda")
     stream = torch.cuda.Stream()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
@@ -84,6 +86,8 @@ def main():
         r["fp8_fwd_speedup_vs_bf16"] = round(r["bf16_cublas"]["ms"] / r["fp8_tensorwise_fwd"]["ms"], 3)
         res["shapes"].append(r)
         print(json.dumps(r), flush=True)
+    _clk.__exit__()
+    res["clocks"] = _clk.summary()
     if a.out:
         json.dump(res, open(a.out, "w"), indent=1)
 

@@ -17,7 +17,7 @@ import torch  # noqa: E402
 
 import synth  # noqa: E402
 import paper_2605_10886_b200 as lk  # noqa: E402
-from bench import capture, peaks, time_steps  # noqa: E402
+from bench import ClockSampler, capture, peaks, time_steps  # noqa: E402
 
 
 def main():
@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
+    _clk = ClockSampler(torch.cuda.current_device())  # NVML clocks during the whole measurement
+    _clk.__enter__()
     dev = torch.device("cuda")
     stream = torch.cuda.Stream()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
@@ -49,6 +51,8 @@ def main():
         algo = sum(M * N * 4 for M, N in shapes)
         res["cases"].append({"case": name, "ms": round(ms, 4), "algorithmic_bytes": algo,
                              "gbs": round(algo / ms / 1e6, 1), "frac_of_hbm": round(algo / ms / 1e6 / hbm, 3)})
+    _clk.__exit__()
+    res["clocks"] = _clk.summary()
     print(json.dumps(res))
     if a.out:
         open(a.out, "w").write(json.dumps(res, indent=1))

@@ -18,7 +18,7 @@ import torch  # noqa: E402
 
 import synth  # noqa: E402
 import paper_2605_10886_b200 as lk  # noqa: E402
-from bench import capture, peaks, time_steps  # noqa: E402
+from bench import ClockSampler, capture, peaks, time_steps  # noqa: E402
 
 
 def main():
@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
+    _clk = ClockSampler(torch.cuda.current_device())  # NVML clocks during the whole measurement
+    _clk.__enter__()
     M, K, N = a.M, a.K, a.N
     dev = torch.device("cuda")
     x = synth.heavy(M, K, 3, device=dev)
@@ -61,6 +63,8 @@ def main():
            "tflops": round(fl / ms / 1e9, 1), "frac_of_measured_fp8_peak": round(fl / ms / 1e9 / (2 * bf16_peak), 4),
            "frac_of_4500": round(fl / ms / 1e9 / 4500, 4), "bf16_ms": round(msb, 4),
            "bf16_tflops": round(fl / msb / 1e9, 1), "speedup_vs_bf16": round(msb / ms, 3), "peak_source": src}
+    _clk.__exit__()
+    res["clocks"] = _clk.summary()
     print(json.dumps(res))
     if a.out:
         open(a.out, "w").write(json.dumps(res, indent=1))

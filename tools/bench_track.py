@@ -17,7 +17,7 @@ import torch  # noqa: E402
 
 import synth  # noqa: E402
 import paper_2605_10886_b200 as lk  # noqa: E402
-from bench import capture, time_steps  # noqa: E402
+from bench import ClockSampler, capture, time_steps  # noqa: E402
 
 
 def main():
@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
+    _clk = ClockSampler(torch.cuda.current_device())  # NVML clocks during the whole measurement
+    _clk.__enter__()
     dev = torch.device("cuda")
     stream = torch.cuda.Stream()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
@@ -57,6 +59,8 @@ def main():
         fl = 2.0 * K * K * B
         res["cases"].append({"B": B, "K": K, "ms": round(ms, 4), "gemm_equiv_tflops": round(fl / ms / 1e9, 1),
                              "torch_ms": round(mst, 4), "speedup_vs_torch": round(mst / ms, 3)})
+    _clk.__exit__()
+    res["clocks"] = _clk.summary()
     print(json.dumps(res))
     if a.out:
         open(a.out, "w").write(json.dumps(res, indent=1))
