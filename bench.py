@@ -312,6 +312,7 @@ class Cfg5:
         self.xq = torch.empty(M, K, dtype=torch.uint8, device=dev)
         self.xs = torch.empty(1, dtype=torch.float32, device=dev)
         self.amax = torch.zeros(1, dtype=torch.float32, device=dev)
+        self.amax2 = torch.zeros(2, dtype=torch.float32, device=dev)  # delayed scaling: [previous, this step]
         self.wq = torch.empty(N, K, dtype=torch.uint8, device=dev)
         self.wsc = torch.empty(1, dtype=torch.float32, device=dev)
         self.y = torch.empty(M, N, dtype=torch.bfloat16, device=dev)
@@ -354,6 +355,18 @@ class Cfg5:
     def step(self, sh):
         self.quantize(sh)
         self.linear(sh)
+
+    def step_delayed(self, sh):
+        """NEXT-4 delayed scaling: X cast with the previous step's (all-reduced) amax while the same pass
+        records this step's amax for the next (LOKA_PHASE_CAST_DELAYED: no separate amax read of X); the
+        all-reduce of the new amax is issued after the GEMM, off the critical path."""
+        lk = self.lk
+        self._q(self.tx, self.tq, lk.PHASE["delayed"], self.amax2, self.qws, sh)
+        self._q(self.tw, self.twq, lk.PHASE["full"], None, self.wqws, sh)
+        self.linear(sh)
+        self.amax2[0:1].copy_(self.amax2[1:2])
+        if self.dist is not None:
+            self.dist.all_reduce(self.amax2[0:1], op=self.dist.ReduceOp.MAX)
 
 
 def cfg5_oracle(rows, seed=3, threads=None):
@@ -593,6 +606,17 @@ def main():
     t_lin = [e1.elapsed_time(e2) for _, e1, e2 in ev]
     lin_ms = statistics.median(t_lin)
 
+    # NEXT-4 delayed scaling (extra key): the scale from the previous step's amax, recorded by the cast
+    with torch.cuda.stream(stream):
+        step.quantize(sh)
+        step.amax2[0:1].copy_(step.amax)  # (the first step's "previous" amax)
+
+    def run_delayed():
+        with torch.cuda.stream(stream):
+            step.step_delayed(sh)
+
+    t_dl = time_steps(run_delayed, args.steps, args.warmup, None, stream, barrier)
+
     # BF16 baseline (torch F.linear + F.layer_norm, cuBLAS) on the same shard
     out_bf = torch.empty_like(step.y)
 
@@ -641,6 +665,7 @@ def main():
 
     ms_fp8 = max_over_ranks(sum(t_fp8)) / args.steps
     ms_bf = max_over_ranks(sum(t_bf)) / args.steps
+    ms_dl = max_over_ranks(sum(t_dl)) / args.steps
     ms_bfl = max_over_ranks(sum(t_bfl)) / args.steps
     ms_q = max_over_ranks(sum(t_q)) / args.steps
     ms_lin = max_over_ranks(lin_ms)
@@ -686,6 +711,11 @@ def main():
             "bf16_baseline": {"value": round(fl / (ms_bf * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
                               "ms_per_step": round(ms_bf, 5), "impl": "torch F.linear + F.layer_norm (bf16, cuBLAS)"},
             "speedup_vs_bf16": round(ms_bf / ms_fp8, 3),
+            "delayed_scaling": {"value": round(fl / (ms_dl * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
+                                "ms_per_step": round(ms_dl, 5), "speedup_vs_bf16": round(ms_bf / ms_dl, 3),
+                                "step": "loka_quantize(X, CAST_DELAYED: the previous step's amax, this step's "
+                                        "amax recorded in the same read) -> W quantize -> fused GEMM + LayerNorm -> "
+                                        "all_reduce(MAX) of the new amax (N > 1) after the GEMM (NEXT-4)"},
             "bf16_library_fused": {"value": round(fl / (ms_bfl * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
                                    "ms_per_step": round(ms_bfl, 5),
                                    "impl": "this library's BF16 path: kind::f16 CTA-pair GEMM + the same fused "

@@ -91,7 +91,11 @@ typedef enum loka_scale_fmt { LOKA_SCALE_F32 = 0, LOKA_SCALE_UE8M0 = 1 } loka_sc
 typedef enum loka_phase {
   LOKA_PHASE_FULL = 0,          /* amax + cast in one call                                   */
   LOKA_PHASE_AMAX_ONLY = 1,     /* TENSOR only: write the local amax to *amax_dev            */
-  LOKA_PHASE_CAST_WITH_AMAX = 2 /* TENSOR only: cast with the (all-reduced) amax in *amax_dev */
+  LOKA_PHASE_CAST_WITH_AMAX = 2, /* TENSOR only: cast with the (all-reduced) amax in *amax_dev */
+  /* TENSOR only, delayed scaling: cast with amax_dev[0] (a previous step's
+   * all-reduced amax; values beyond it saturate, D3) and write max |x| of THIS tensor to amax_dev[1]
+   * in the same read of x (the next step's scale source: its all-reduce runs off the critical path). */
+  LOKA_PHASE_CAST_DELAYED = 3
 } loka_phase;
 
 typedef enum loka_norm {

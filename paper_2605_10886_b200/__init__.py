@@ -46,7 +46,7 @@ DEVSTATUS_NONFINITE = 0x1
 F32, BF16, E4M3, E5M2 = range(4)
 GRAN = {"tensor": 0, "row": 1, "col": 2, "blk_1x128": 3, "blk_128x1": 4, "blk_128x128": 5, "blk_1x32": 6}
 SCALE = {"f32": 0, "ue8m0": 1}
-PHASE = {"full": 0, "amax": 1, "cast": 2}
+PHASE = {"full": 0, "amax": 1, "cast": 2, "delayed": 3}
 NORM = {"none": 0, "layer": 1, "rms": 2, "block_rms": 3}
 ACT = {"none": 0, "hardswish": 1}
 DIR = {"fwd": 0, "dgrad": 1, "wgrad": 2}

@@ -179,7 +179,9 @@ loka_status loka_quantize(const loka_tensor* x, loka_tensor* q, loka_tensor* qt,
   if (q->data && (!aligned16(q->data) || q->ld < q->cols || q->ld % 16)) return LOKA_ERR_INVALID_ARG;
   if (q->gran < LOKA_GRAN_TENSOR || q->gran > LOKA_GRAN_BLK_1x32) return LOKA_ERR_INVALID_ARG;
   if (qt && q->gran == LOKA_GRAN_BLK_1x32) return LOKA_ERR_UNSUPPORTED;  // MX blocks: row-major codes only
+  if (phase < LOKA_PHASE_FULL || phase > LOKA_PHASE_CAST_DELAYED) return LOKA_ERR_INVALID_ARG;
   if (phase != LOKA_PHASE_FULL && q->gran != LOKA_GRAN_TENSOR) return LOKA_ERR_INVALID_ARG;
+  if (phase == LOKA_PHASE_CAST_DELAYED && qt) return LOKA_ERR_UNSUPPORTED;
   if (phase != LOKA_PHASE_FULL && !amax_dev) return LOKA_ERR_INVALID_ARG;
   // dual: q = 1x128 granules, qt = x's own 128x1 quantization written transposed (its t-frame
   // granule is again 1x128) — one read of x for the blockwise recipe's two operand layouts

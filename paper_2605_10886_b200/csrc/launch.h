@@ -59,11 +59,13 @@ cudaError_t launch_quantize(const QuantParams& p, bool in_bf16, int fmt, int sca
 // Streaming quantize through smem with bulk copies (quantize_tma.cu): ROW / TENSOR
 // cast (amax_dev = the tensor amax), bf16 input, no transposed copy; see quant_tma_eligible.
 bool quant_tma_eligible(const QuantParams& p, bool in_bf16, int gran);
+// amax_next (nullable, TENSOR only): also atomicMax the tensor's own max |x| bits into it (delayed scaling)
 cudaError_t launch_quantize_tma(const QuantParams& p, int fmt, int scale_fmt, int gran, const float* amax_dev,
-                                int num_sms, cudaStream_t st);
+                                int num_sms, cudaStream_t st, uint32_t* amax_next = nullptr);
 struct QuantGroup;
 cudaError_t launch_quantize_tma_group(const QuantGroup& grp, int64_t max_cols, int fmt, int scale_fmt, int gran,
-                                      const float* amax_dev, int num_sms, cudaStream_t st);
+                                      const float* amax_dev, int num_sms, cudaStream_t st,
+                                      uint32_t* amax_next = nullptr);
 
 // Tiled quantize (quantize_t.cu): any granularity incl. COL / BLK_128x1, optional transposed
 // copy; ws holds the ROW / COL amax pre-pass array (4 * max(rows, cols) bytes).

@@ -559,6 +559,18 @@ static cudaError_t launch_quant_t(const QuantParams& p, int gran, int phase, flo
         if (tma) e = launch_quantize_tma(p, FMT, SF, gran, amax_dev, num_sms, st);
         else e = launch_pdl(cast_tensor_kernel<Tin, FMT, SF>, dim3((unsigned)nb), blk, st, p, (const float*)amax_dev);
       }
+      if (phase == LOKA_PHASE_CAST_DELAYED) {  // cast with amax_dev[0], this tensor's amax -> amax_dev[1]
+        uint32_t* next = reinterpret_cast<uint32_t*>(amax_dev + 1);
+        e = cudaMemsetAsync(next, 0, sizeof(float), st);
+        if (e != cudaSuccess) return e;
+        if (tma) {  // one pass: the bulk-copy cast reduces max |x| of the rows it casts
+          e = launch_quantize_tma(p, FMT, SF, gran, amax_dev, num_sms, st, next);
+        } else {    // (same result in two passes)
+          e = launch_pdl(amax_tensor_kernel<Tin>, dim3((unsigned)nb), blk, st, p, next);
+          if (e != cudaSuccess) return e;
+          e = launch_pdl(cast_tensor_kernel<Tin, FMT, SF>, dim3((unsigned)nb), blk, st, p, (const float*)amax_dev);
+        }
+      }
       break;
     }
     default:

@@ -56,8 +56,9 @@ template <> struct QtIn<__nv_bfloat16> {
 
 // cast a row held in smem into the staging row: 4 chunks of 16 B per lane loaded before any is
 // converted (the smem latency of one chunk hides behind the others' conversion)
-template <typename Tin, int FMT>
-LOKA_DEVINL void qt_cast_row(uint32_t src, uint32_t dsts, int nchunks, int lane, float r) {
+template <typename Tin, int FMT, bool AMAX = false>
+LOKA_DEVINL uint32_t qt_cast_row(uint32_t src, uint32_t dsts, int nchunks, int lane, float r) {
+  uint32_t am = 0;  // AMAX: this lane's max |x| bits over the row (the delayed-scaling phase)
   int c = lane;
   for (; c + 96 < nchunks; c += 128) {
     uint4 w[4];
@@ -65,15 +66,19 @@ LOKA_DEVINL void qt_cast_row(uint32_t src, uint32_t dsts, int nchunks, int lane,
     for (int u = 0; u < 4; ++u) w[u] = QtIn<Tin>::ld(src + 16u * (c + 32 * u));
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
+      if (AMAX) am = max(am, QtIn<Tin>::amax(w[u]));
       const uint2 code = QtIn<Tin>::template cast<FMT>(w[u], r);
       asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(dsts + 8u * (c + 32 * u)), "r"(code.x), "r"(code.y)
                    : "memory");
     }
   }
   for (; c < nchunks; c += 32) {
-    const uint2 code = QtIn<Tin>::template cast<FMT>(QtIn<Tin>::ld(src + 16u * c), r);
+    const uint4 w = QtIn<Tin>::ld(src + 16u * c);
+    if (AMAX) am = max(am, QtIn<Tin>::amax(w));
+    const uint2 code = QtIn<Tin>::template cast<FMT>(w, r);
     asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(dsts + 8u * c), "r"(code.x), "r"(code.y) : "memory");
   }
+  return am;
 }
 
 // Work items are groups of 8 consecutive rows of one tensor of the QuantGroup (a single tensor
@@ -96,7 +101,7 @@ LOKA_DEVINL int qt_locate(const QuantGroup& grp, int64_t gg, int64_t& first_row)
 template <typename Tin, int FMT, int SF, int GRAN, int kQtRows>
 __global__ void __launch_bounds__(32 * (kQtRows + 1), 1)
     quant_tma_kernel(const __grid_constant__ QuantGroup grp, int64_t ngroups, int max_cols, int nstages,
-                     const float* amax_dev) {
+                     const float* amax_dev, uint32_t* amax_next) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   const int slot_in = (max_cols * (int)sizeof(Tin) + 127) & ~127, slot_out = (max_cols + 127) & ~127;
@@ -155,6 +160,7 @@ __global__ void __launch_bounds__(32 * (kQtRows + 1), 1)
   }
   int nst = 0, s = -1;
   uint32_t ph = 1;
+  uint32_t am_next = 0;
   for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
     if (++s == nstages) s = 0;
     if (s == 0) ph ^= 1u;
@@ -216,6 +222,8 @@ __global__ void __launch_bounds__(32 * (kQtRows + 1), 1)
           }
         }
       }
+    } else if (amax_next) {  // TENSOR, delayed scaling: cast with the given amax, record this tensor's
+      am_next = max(am_next, qt_cast_row<Tin, FMT, true>(src, dsts, nchunks, lane, r_tensor));
     } else {  // TENSOR cast with the pre-computed amax
       qt_cast_row<Tin, FMT>(src, dsts, nchunks, lane, r_tensor);
     }
@@ -232,6 +240,13 @@ __global__ void __launch_bounds__(32 * (kQtRows + 1), 1)
     ++nst;
   }
   if (lane == 0) bulk_wait0();
+  if (GRAN == LOKA_GRAN_TENSOR && amax_next) {  // one atomicMax of the bit pattern per warp
+    am_next = warp_max_u32(am_next);
+    if (lane == 0 && am_next) {
+      atomicMax(amax_next, am_next);
+      if (am_next >= 0x7F800000u && grp.p[0].status) atomicOr(grp.p[0].status, LOKA_DEVSTATUS_NONFINITE);
+    }
+  }
 }
 
 static int quant_tma_rows(int64_t cols, int in_elem) { return cols * in_elem <= 4096 ? 16 : 8; }
@@ -264,7 +279,7 @@ bool quant_tma_eligible(const QuantParams& p, bool in_bf16, int gran) {
 
 template <int FMT, int SF, int GRAN, int kQtRows>
 static cudaError_t launch_qt_r(const QuantGroup& grp, int64_t max_cols, const float* amax_dev, int num_sms,
-                               cudaStream_t st) {
+                               cudaStream_t st, uint32_t* amax_next) {
   auto kern = quant_tma_kernel<__nv_bfloat16, FMT, SF, GRAN, kQtRows>;
   const size_t smem = quant_tma_smem(max_cols, 2);
   const int nstages = quant_tma_stages(max_cols, 2);
@@ -286,19 +301,21 @@ static cudaError_t launch_qt_r(const QuantGroup& grp, int64_t max_cols, const fl
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   note_launch();
-  return cudaLaunchKernelEx(&cfg, kern, grp, ngroups, (int)max_cols, nstages, amax_dev);
+  return cudaLaunchKernelEx(&cfg, kern, grp, ngroups, (int)max_cols, nstages, amax_dev, amax_next);
 }
 template <int FMT, int SF, int GRAN>
 static cudaError_t launch_qt(const QuantGroup& grp, int64_t max_cols, const float* amax_dev, int num_sms,
-                             cudaStream_t st) {
-  if (quant_tma_rows(max_cols, 2) == 16) return launch_qt_r<FMT, SF, GRAN, 16>(grp, max_cols, amax_dev, num_sms, st);
-  return launch_qt_r<FMT, SF, GRAN, 8>(grp, max_cols, amax_dev, num_sms, st);
+                             cudaStream_t st, uint32_t* amax_next) {
+  if (quant_tma_rows(max_cols, 2) == 16)
+    return launch_qt_r<FMT, SF, GRAN, 16>(grp, max_cols, amax_dev, num_sms, st, amax_next);
+  return launch_qt_r<FMT, SF, GRAN, 8>(grp, max_cols, amax_dev, num_sms, st, amax_next);
 }
 
 cudaError_t launch_quantize_tma_group(const QuantGroup& grp, int64_t max_cols, int fmt, int scale_fmt, int gran,
-                                      const float* amax_dev, int num_sms, cudaStream_t st) {
+                                      const float* amax_dev, int num_sms, cudaStream_t st, uint32_t* amax_next) {
 #define LOKA_QT(F, S, G) \
-  if (fmt == F && scale_fmt == S && gran == G) return launch_qt<F, S, G>(grp, max_cols, amax_dev, num_sms, st);
+  if (fmt == F && scale_fmt == S && gran == G) \
+    return launch_qt<F, S, G>(grp, max_cols, amax_dev, num_sms, st, amax_next);
 #define LOKA_QT_G(F, S)                     \
   LOKA_QT(F, S, LOKA_GRAN_ROW)              \
   LOKA_QT(F, S, LOKA_GRAN_TENSOR)           \
@@ -313,13 +330,13 @@ cudaError_t launch_quantize_tma_group(const QuantGroup& grp, int64_t max_cols, i
 }
 
 cudaError_t launch_quantize_tma(const QuantParams& p, int fmt, int scale_fmt, int gran, const float* amax_dev,
-                                int num_sms, cudaStream_t st) {
+                                int num_sms, cudaStream_t st, uint32_t* amax_next) {
   static thread_local QuantGroup grp;  // ~7 KB: not on the stack
   grp.G = 1;
   grp.row_start[0] = 0;
   grp.row_start[1] = p.rows;
   grp.p[0] = p;
-  return launch_quantize_tma_group(grp, p.cols, fmt, scale_fmt, gran, amax_dev, num_sms, st);
+  return launch_quantize_tma_group(grp, p.cols, fmt, scale_fmt, gran, amax_dev, num_sms, st, amax_next);
 }
 
 }  // namespace loka

@@ -222,3 +222,21 @@ def test_full_size_bit_exact_other_granules(gran):
     oq, os_ = oracle.quantize.quantize(x.cpu().double().numpy(), "e4m3", gran)
     assert_scales_equal(s, os_)
     assert_bytes_equal(q, oq)
+
+
+@pytest.mark.parametrize("dtype,rows", [(torch.bfloat16, 300), (torch.float32, 300), (torch.bfloat16, 20)])
+@pytest.mark.parametrize("fmt", ["e4m3", "e5m2"])
+def test_delayed_scaling_phase(dtype, rows, fmt):
+    """NEXT-4 delayed scaling (LOKA_PHASE_CAST_DELAYED): codes and scale from the given previous amax
+    (amax[0], values beyond it saturate), and this tensor's own max |x| written to amax[1] in the same
+    pass (bf16 dense: the bulk-copy cast; otherwise two passes) — bit-exact with the oracle."""
+    x = synth.heavy(rows, 512, 12).to(dtype)
+    prev = float(x.float().abs().max()) * 0.5
+    amax = torch.tensor([prev, -1.0], dtype=torch.float32, device=DEV)
+    q, s = lk.loka_quantize(to_dev_padded(x), fmt, "tensor", phase="delayed", amax=amax)
+    torch.cuda.synchronize()
+    oq, os_ = oracle.quantize.quantize(x.double().numpy(), fmt, "tensor", amax=np.array([prev]))
+    assert_scales_equal(s, os_)
+    assert_bytes_equal(q, oq)
+    a = amax.cpu().numpy()
+    assert a[0] == np.float32(prev) and a[1] == np.float32(np.abs(x.double().numpy()).max())

@@ -66,7 +66,10 @@ def main():
         # the tensorwise recipe's two phases separately (split-phase for the DP all-reduce)
         amax = torch.zeros(1, dtype=torch.float32, device=dev)
         s1 = torch.empty(1, dtype=torch.float32, device=dev)
-        for name, ph, nbytes in (("tensor_amax_pass", "amax", R * Cc * 2), ("tensor_cast_pass", "cast", R * Cc * 3)):
+        amax = torch.zeros(2, dtype=torch.float32, device=dev)
+        lk.loka_quantize(x, "e4m3", "tensor", phase="amax", amax=amax, want_q=False, scales=s1)
+        for name, ph, nbytes in (("tensor_amax_pass", "amax", R * Cc * 2), ("tensor_cast_pass", "cast", R * Cc * 3),
+                                 ("tensor_cast_delayed_with_amax", "delayed", R * Cc * 3)):
             fn = (lambda ph=ph: lk.loka_quantize(x, "e4m3", "tensor", phase=ph, amax=amax, out=q, scales=s1,
                                                  want_q=ph != "amax"))
             g = capture(fn, stream)
