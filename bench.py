@@ -615,7 +615,6 @@ def main():
         with torch.cuda.stream(stream):
             step.step_delayed(sh)
 
-    t_dl = time_steps(run_delayed, args.steps, args.warmup, None, stream, barrier)
 
     # BF16 baseline (torch F.linear + F.layer_norm, cuBLAS) on the same shard
     out_bf = torch.empty_like(step.y)
@@ -624,7 +623,6 @@ def main():
         with torch.cuda.stream(stream):
             out_bf.copy_(F.layer_norm(F.linear(x, w), (CFG5_N,)))
 
-    t_bf = time_steps(run_bf, args.steps, args.warmup, None, stream, barrier)
 
     # the library's own BF16 path with the same fused epilogue (kind::f16 on the CTA-pair engine):
     # separates the FP8 gain from the fusion gain (SURVEY.md §8(d) secondary denominator)
@@ -641,7 +639,33 @@ def main():
             st_ = lk._lib.loka_bf16_linear_norm(ctypes.byref(bargs), ctypes.c_void_p(bws.data_ptr()), bws.numel(), sh)
             assert st_ == 0, st_
 
-    t_bfl = time_steps(run_bf_lib, args.steps, args.warmup, None, stream, barrier)
+
+    # the comparison paths, interleaved step by step with the FP8 step (same thermal / power state for
+    # every path: B200 clocks drift under sustained tensor load, so back-to-back blocks would bias it)
+    def run_fp8():
+        with torch.cuda.stream(stream):
+            step.step(sh)
+
+    paths = {"fp8": run_fp8, "bf16": run_bf, "delayed": run_delayed, "bf16_lib": run_bf_lib}
+    for _ in range(args.warmup):
+        for fn in paths.values():
+            fn()
+    iev = {k: [] for k in paths}
+    torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    for _ in range(args.steps):
+        for k, fn in paths.items():
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            iev[k].append((e0, e1))
+    torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    it = {k: [a.elapsed_time(b) for a, b in v] for k, v in iev.items()}
+    t_bf, t_dl, t_bfl, t_fp8i = it["bf16"], it["delayed"], it["bf16_lib"], it["fp8"]
 
     # e2e through the public API: pinned host X -> device, the step, device Y -> pinned host, every step
     xh = x.cpu().pin_memory()
@@ -664,6 +688,7 @@ def main():
         return float(t.item())
 
     ms_fp8 = max_over_ranks(sum(t_fp8)) / args.steps
+    ms_fp8i = max_over_ranks(sum(t_fp8i)) / args.steps
     ms_bf = max_over_ranks(sum(t_bf)) / args.steps
     ms_dl = max_over_ranks(sum(t_dl)) / args.steps
     ms_bfl = max_over_ranks(sum(t_bfl)) / args.steps
@@ -710,9 +735,14 @@ def main():
             "quantize_ms_per_step": round(ms_q, 5),
             "bf16_baseline": {"value": round(fl / (ms_bf * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
                               "ms_per_step": round(ms_bf, 5), "impl": "torch F.linear + F.layer_norm (bf16, cuBLAS)"},
-            "speedup_vs_bf16": round(ms_bf / ms_fp8, 3),
+            "speedup_vs_bf16": round(ms_bf / ms_fp8i, 3),
+            "comparison_protocol": "bf16_baseline, bf16_library_fused, delayed_scaling and fp8_step_interleaved: "
+                                   "the K steps of each path interleaved step by step (same clock / power state); "
+                                   "speedups divide those",
+            "fp8_step_interleaved_ms": round(ms_fp8i, 5),
             "delayed_scaling": {"value": round(fl / (ms_dl * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
                                 "ms_per_step": round(ms_dl, 5), "speedup_vs_bf16": round(ms_bf / ms_dl, 3),
+                                "vs_current_scaling_step": round(ms_fp8i / ms_dl, 3),
                                 "step": "loka_quantize(X, CAST_DELAYED: the previous step's amax, this step's "
                                         "amax recorded in the same read) -> W quantize -> fused GEMM + LayerNorm -> "
                                         "all_reduce(MAX) of the new amax (N > 1) after the GEMM (NEXT-4)"},
@@ -720,7 +750,7 @@ def main():
                                    "ms_per_step": round(ms_bfl, 5),
                                    "impl": "this library's BF16 path: kind::f16 CTA-pair GEMM + the same fused "
                                            "LayerNorm epilogue (loka_bf16_linear_norm), no quantize",
-                                   "fp8_step_speedup": round(ms_bfl / ms_fp8, 3),
+                                   "fp8_step_speedup": round(ms_bfl / ms_fp8i, 3),
                                    "fp8_compute_only_speedup": round(ms_bfl / ms_lin, 3)},
             "roofline": {"kernel": "pair_norm_kernel<256, LayerNorm> (CTA-pair FP8 GEMM + fused LayerNorm), 1 "
                                    "launch/step", "bound": "tensor", "achieved": round(achieved, 2),
