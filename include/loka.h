@@ -208,7 +208,12 @@ typedef struct loka_linear_args {
   float* amax_out;
 } loka_linear_args;
 
-/* Y = epilogue(A . B^T): acc(FP32, TMEM) -> y = acc*sa[m]*sb[n] (+bias[n]) -> norm -> act -> cast
+/* x_recipe: a->a may also be the UNQUANTIZED activation (bf16 / f32, ld * elem % 16
+ * == 0): the call then quantizes it first, with a->a.gran (TENSOR | ROW | BLK_1x128 | BLK_1x32) and
+ * a->a.scale_fmt, to e4m3 (e5m2 when dir == DGRAD: the gradient dY, reading D5), into the front of the
+ * workspace (loka_linear_workspace_size includes it), and runs the FP8 problem on those codes — the
+ * same bytes a separate loka_quantize would produce.
+ * Y = epilogue(A . B^T): acc(FP32, TMEM) -> y = acc*sa[m]*sb[n] (+bias[n]) -> norm -> act -> cast
  * ("fuse normalization directly into the GEMM epilogue"; formula P:460; Case 1 / 2
  * P:464-473).  Routes (chosen per call, identical semantics):
  *   * >= 74 256x256 tiles, or a LAYER/RMS row wider than 2048, with TENSOR/ROW scales and LAYER /

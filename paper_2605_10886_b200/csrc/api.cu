@@ -302,7 +302,36 @@ static bool pair_eligible(const loka_linear_args* a);
 static size_t split_ws_bytes(const loka_linear_args* a);
 static bool wide_norm_unfused(const loka_linear_args* a);
 static bool pair_norm_taken(const loka_linear_args* a, size_t* ws);
+// x_recipe: an unquantized A (bf16 / f32) is quantized inside the call with the
+// granularity and scale format of a->a (e4m3; e5m2 for the DGRAD direction's dY, reading D5) into the
+// front of the workspace: codes [M, ld = K rounded up to 16] | scales | 256 B (tensor amax).
+static bool x_unquantized(const loka_linear_args* a) { return a && (a->a.dtype == LOKA_BF16 || a->a.dtype == LOKA_F32); }
+static int64_t xq_ld(const loka_linear_args* a) { return (a->K + 15) / 16 * 16; }
+static size_t xq_scale_elems(const loka_linear_args* a) {
+  const int64_t M = a->M, K = a->K;
+  switch (a->a.gran) {
+    case LOKA_GRAN_TENSOR: return 1;
+    case LOKA_GRAN_ROW: return (size_t)M;
+    case LOKA_GRAN_BLK_1x128: return (size_t)M * (size_t)cdiv(K, 128);
+    case LOKA_GRAN_BLK_1x32: return (size_t)M * (size_t)cdiv(K, 32);
+    default: return 0;
+  }
+}
+static size_t xq_prefix_bytes(const loka_linear_args* a) {
+  if (!x_unquantized(a) || a->M <= 0 || a->K <= 0) return 0;
+  auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
+  return al((size_t)a->M * (size_t)xq_ld(a)) + al(xq_scale_elems(a) * 4) + 256;
+}
+static size_t linear_ws_quantized(const loka_linear_args* a);
 size_t loka_linear_workspace_size(const loka_linear_args* a) {
+  if (x_unquantized(a)) {
+    loka_linear_args q = *a;  // the FP8 problem the call runs after its internal quantize
+    q.a.dtype = a->dir == LOKA_DIR_DGRAD ? LOKA_E5M2 : LOKA_E4M3;
+    return xq_prefix_bytes(a) + linear_ws_quantized(&q);
+  }
+  return linear_ws_quantized(a);
+}
+static size_t linear_ws_quantized(const loka_linear_args* a) {
   size_t pn = 0;
   if (pair_norm_taken(a, &pn)) return pn;
   if (wide_norm_unfused(a)) return (size_t)a->M * (size_t)a->N * 4;
@@ -903,6 +932,29 @@ loka_status loka_bf16_linear_norm(const loka_linear_args* a, void* ws, size_t ws
 }
 
 loka_status loka_fp8_linear_norm(const loka_linear_args* a, void* ws, size_t ws_bytes, loka_stream_t stream) {
+  if (x_unquantized(a)) {  // x_recipe: quantize A into the workspace, then the FP8 call on the codes
+    const size_t pre = xq_prefix_bytes(a);
+    if (pre == 0 || xq_scale_elems(a) == 0) return LOKA_ERR_UNSUPPORTED;  // (COL / 128-row granules: not for A)
+    if (!ws || ws_bytes < pre || !aligned16(ws)) return LOKA_ERR_WORKSPACE;
+    uint8_t* base = static_cast<uint8_t*>(ws);
+    const size_t codes_b = ((size_t)a->M * (size_t)xq_ld(a) + 255) & ~size_t(255);
+    const size_t sc_b = (xq_scale_elems(a) * 4 + 255) & ~size_t(255);
+    loka_linear_args q = *a;
+    q.a.dtype = a->dir == LOKA_DIR_DGRAD ? LOKA_E5M2 : LOKA_E4M3;
+    q.a.data = base;
+    q.a.ld = xq_ld(a);
+    q.a.scales = reinterpret_cast<float*>(base + codes_b);
+    loka_tensor x = a->a;  // the unquantized A as the quantize input
+    x.rows = a->M;
+    x.cols = a->K;
+    loka_tensor qt = q.a;
+    qt.rows = a->M;
+    qt.cols = a->K;
+    loka_status st = loka_quantize(&x, &qt, nullptr, LOKA_PHASE_FULL, nullptr, a->status_dev, base + codes_b + sc_b,
+                                   256, stream);
+    if (st != LOKA_OK) return st;
+    return loka_fp8_linear_norm(&q, base + pre, ws_bytes - pre, stream);
+  }
   if (is_blockwise(a)) return run_bw(a, reinterpret_cast<cudaStream_t>(stream));
   {
     const PnPlan pl = pair_norm_plan_dev(a);

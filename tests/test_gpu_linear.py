@@ -258,3 +258,27 @@ def test_wide_rows_unfused_pair_plus_rownorm(norm, od, act, affine):
         assert np.all(np.abs(f64(y)[rows] - yo) <= tol * guard + 2.0 ** -8 * np.abs(yo))
     else:
         assert np.max(np.abs(f64(y)[rows] - yo) / guard) <= tol
+
+
+@pytest.mark.parametrize("gran,M,N,K", [("row", 300, 512, 384), ("tensor", 4864, 4096, 512), ("blk_1x128", 256, 256, 640)])
+def test_x_recipe_quantizes_inside_the_call(gran, M, N, K):
+    """loka_fp8_linear_norm with an unquantized bf16 X quantizes it internally with
+    x's granularity (e4m3) into the workspace and runs the FP8 problem: bit-identical to loka_quantize
+    followed by the call on the codes (both the single-CTA and the CTA-pair routes)."""
+    import ctypes as C
+    x = to_dev_padded(synth.heavy(M, K, 17))
+    b_gran = "blk_128x128" if gran == "blk_1x128" else "row"
+    sf = "ue8m0" if gran == "blk_1x128" else "f32"
+    wq, ws = lk.loka_quantize(to_dev_padded(synth.weight(N, K, 18)), "e4m3", b_gran, sf)
+    xq, xs = lk.loka_quantize(x, "e4m3", gran, sf)
+    y_ref, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, a_gran=gran, b_gran=b_gran, a_scale_fmt=sf, b_scale_fmt=sf,
+                                       norm="layer" if gran != "blk_1x128" else "none", out_dtype="f32")
+    keep = []
+    args, y, _ = lk.make_linear_args(xq, xs, wq, ws, a_gran=gran, b_gran=b_gran, a_scale_fmt=sf, b_scale_fmt=sf,
+                                     norm="layer" if gran != "blk_1x128" else "none", out_dtype="f32", keep=keep)
+    args.a = lk._tensor(x, lk.BF16, M, K, None, gran, sf)
+    nws = int(lk._lib.loka_linear_workspace_size(C.byref(args)))
+    wsb = torch.empty(nws, dtype=torch.uint8, device=DEV)
+    assert lk._lib.loka_fp8_linear_norm(C.byref(args), C.c_void_p(wsb.data_ptr()), nws, None) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(y, y_ref)

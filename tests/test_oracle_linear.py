@@ -178,3 +178,30 @@ def test_norm_backward_finite_differences():
         e[i, j] = h
         fd = (loss(z + e) - loss(z - e)) / (2 * h)
         assert abs(fd - dz[i, j]) < 1e-6
+
+
+def test_bias_pinned_by_augmented_gemm():
+    """O8 bias ("(Wx + b)", before the norm), pinned independently of add_bias: the bias is
+    the extra output column of an augmented product [X, 1] [W, b]^T computed by the GEMM path itself
+    (matmul_nt), then every norm on top; a sign or broadcast-axis mistake in the bias step fails here
+    (round-1 verdict What's weak #13)."""
+    rng = np.random.default_rng(12)
+    M, N, K = 5, 512, 7
+    x = rng.standard_normal((M, K))
+    w = rng.standard_normal((N, K))
+    b = rng.standard_normal(N) * 3.0
+    xa = np.concatenate([x, np.ones((M, 1))], axis=1)
+    wa = np.concatenate([w, b[:, None]], axis=1)
+    ya = L.matmul_nt(xa, wa)
+    assert np.allclose(L.add_bias(L.fwd(x, w), b), ya, rtol=0, atol=1e-12)
+    for norm in ("layer", "rms", "block_rms"):
+        got = L.apply_norm(L.add_bias(L.fwd(x, w), b), norm, block=256)
+        assert np.allclose(got, L.apply_norm(ya, norm, block=256), rtol=0, atol=1e-12), norm
+    # the oracle's linear_norm with bias on quantized operands == the augmented product on their values
+    from oracle import quantize as Q
+    xq, xs = Q.quantize(x, "e4m3", "row")
+    wq, ws = Q.quantize(w, "e4m3", "row")
+    y = L.linear_norm(xq, xs, "e4m3", "row", wq, ws, "e4m3", "row", bias=b, norm="layer")
+    xh, wh = Q.dequantize(xq, xs, "e4m3", "row"), Q.dequantize(wq, ws, "e4m3", "row")
+    ref = L.layer_norm(L.matmul_nt(np.concatenate([xh, np.ones((M, 1))], 1), np.concatenate([wh, b[:, None]], 1)))
+    assert np.allclose(y, ref, rtol=0, atol=1e-12)
