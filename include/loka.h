@@ -206,6 +206,10 @@ typedef struct loka_linear_args {
      layer's tensorwise quantize can skip its amax pass (LOKA_PHASE_CAST_WITH_AMAX), and a data-
      parallel job all-reduces this word instead (a9).  Non-finite outputs raise it to Inf/NaN.    */
   float* amax_out;
+  /* x_recipe with a TENSOR-granular unquantized A (see loka_fp8_linear_norm): nullable device float,
+     the amax to cast A with (a data-parallel caller's all-reduced global amax, a9); NULL = the call
+     computes A's own amax first.                                                                 */
+  const float* x_amax;
 } loka_linear_args;
 
 /* x_recipe: a->a may also be the UNQUANTIZED activation (bf16 / f32, ld * elem % 16

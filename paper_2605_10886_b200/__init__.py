@@ -72,7 +72,7 @@ class loka_linear_args(C.Structure):
                 ("beta", C.c_void_p), ("y", loka_tensor), ("debug_precast", C.c_void_p), ("status_dev", C.c_void_p),
                 ("act", C.c_int), ("bwd_xhat", C.c_void_p), ("bwd_xhat_ld", C.c_int64), ("bwd_rstd", C.c_void_p),
                 ("save_xhat", C.c_void_p), ("save_xhat_ld", C.c_int64), ("save_rstd", C.c_void_p),
-                ("amax_out", C.c_void_p)]
+                ("amax_out", C.c_void_p), ("x_amax", C.c_void_p)]
 
 
 class loka_stack_args(C.Structure):

@@ -320,7 +320,8 @@ static size_t xq_scale_elems(const loka_linear_args* a) {
 static size_t xq_prefix_bytes(const loka_linear_args* a) {
   if (!x_unquantized(a) || a->M <= 0 || a->K <= 0) return 0;
   auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
-  return al((size_t)a->M * (size_t)xq_ld(a)) + al(xq_scale_elems(a) * 4) + 256;
+  // codes | scales | amax (256 B) | fused-cast row-block counters
+  return al((size_t)a->M * (size_t)xq_ld(a)) + al(xq_scale_elems(a) * 4) + 256 + al((size_t)cdiv(a->M, 256) * 4);
 }
 static size_t linear_ws_quantized(const loka_linear_args* a);
 size_t loka_linear_workspace_size(const loka_linear_args* a) {
@@ -810,8 +811,17 @@ static PnPlan pair_norm_plan(const loka_linear_args* a, int sms) {
   return pl;
 }
 static size_t pair_norm_ws(const PnPlan& pl) { return pl.xchg ? pair_xchg_bytes(pl.row_blocks, pl.tiles_n) : 0; }
+struct CastX {  // the fused tensorwise cast of X (x_recipe on the pair-norm route)
+  const __nv_bfloat16* xb;
+  int64_t ld_xb;
+  uint8_t* xq;
+  int64_t ld_xq;
+  const float* amax;
+  uint32_t* counters;
+  float* xs_out;
+};
 static loka_status run_pair_norm(const loka_linear_args* a, const PnPlan& pl, void* ws, size_t ws_bytes,
-                                 cudaStream_t s) {
+                                 cudaStream_t s, const CastX* cx = nullptr) {
   const size_t need = pair_norm_ws(pl);
   if (need && (!ws || ws_bytes < need || !aligned16(ws))) return LOKA_ERR_WORKSPACE;
   PairNormParams p;
@@ -852,6 +862,16 @@ static loka_status run_pair_norm(const loka_linear_args* a, const PnPlan& pl, vo
   p.order = pl.order;
   p.ngroups = pl.groups;
   if (const char* e = std::getenv("LOKA_PN_DEBUG")) p.dbg = std::atoi(e);
+  if (cx) {
+    p.castx = 1;
+    p.xb = cx->xb;
+    p.ld_xb = cx->ld_xb;
+    p.xq = cx->xq;
+    p.ld_xq = cx->ld_xq;
+    p.xamax = cx->amax;
+    p.xcnt = cx->counters;
+    p.xs_out = cx->xs_out;
+  }
   if (a->bwd_xhat) {
     p.bwd = 1;
     p.xhat = static_cast<const __nv_bfloat16*>(a->bwd_xhat);
@@ -950,8 +970,32 @@ loka_status loka_fp8_linear_norm(const loka_linear_args* a, void* ws, size_t ws_
     loka_tensor qt = q.a;
     qt.rows = a->M;
     qt.cols = a->K;
-    loka_status st = loka_quantize(&x, &qt, nullptr, LOKA_PHASE_FULL, nullptr, a->status_dev, base + codes_b + sc_b,
-                                   256, stream);
+    float* amax_slot = reinterpret_cast<float*>(base + codes_b + sc_b);
+    uint32_t* counters = reinterpret_cast<uint32_t*>(base + codes_b + sc_b + 256);
+    // tensorwise bf16 A on the pair-norm route: the cast runs inside the GEMM kernel (CASTX), overlapped
+    // with the MMAs of earlier row blocks; only the amax pass precedes it (skipped with a given x_amax)
+    const PnPlan pl = pair_norm_plan_dev(&q);
+    if (pl.ok && pl.tn == 256 && a->a.gran == LOKA_GRAN_TENSOR && a->a.dtype == LOKA_BF16 && a->K % 8 == 0 &&
+        !a->bwd_xhat && std::getenv("LOKA_NO_FUSED_CAST") == nullptr) {
+      const float* amax = a->x_amax;
+      if (!amax) {
+        loka_status st = loka_quantize(&x, &qt, nullptr, LOKA_PHASE_AMAX_ONLY, amax_slot, a->status_dev, nullptr, 0,
+                                       stream);
+        if (st != LOKA_OK) return st;
+        amax = amax_slot;
+      }
+      cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+      if (cudaMemsetAsync(counters, 0, (size_t)cdiv(a->M, 256) * 4, s) != cudaSuccess) return LOKA_ERR_CUDA;
+      CastX cx{static_cast<const __nv_bfloat16*>(a->a.data), a->a.ld, base, xq_ld(a), amax, counters, q.a.scales};
+      loka_status vs = validate_linear(&q);
+      if (vs != LOKA_OK) return vs;
+      return run_pair_norm(&q, pl, base + pre, ws_bytes - pre, s, &cx);
+    }
+    loka_status st = a->x_amax && a->a.gran == LOKA_GRAN_TENSOR
+                         ? loka_quantize(&x, &qt, nullptr, LOKA_PHASE_CAST_WITH_AMAX, const_cast<float*>(a->x_amax),
+                                         a->status_dev, nullptr, 0, stream)
+                         : loka_quantize(&x, &qt, nullptr, LOKA_PHASE_FULL, nullptr, a->status_dev, amax_slot, 256,
+                                         stream);
     if (st != LOKA_OK) return st;
     return loka_fp8_linear_norm(&q, base + pre, ws_bytes - pre, stream);
   }

@@ -348,6 +348,14 @@ struct PairNormParams {
   const __nv_bfloat16* xhat; int64_t ld_xhat;
   const float* rstd_in;
   CUtensorMap tx;      // bwd with bf16 dz: xhat [M, N] box {64 elements, 32 rows} SW128
+  // castx (x_recipe, tensorwise): the kernel casts X itself (bf16 xb -> codes xq, the buffer ta maps)
+  // with the amax at xamax; xcnt [row_blocks] counters (zeroed before the launch); xs_out: X's scale
+  int32_t castx;
+  const __nv_bfloat16* xb; int64_t ld_xb;
+  uint8_t* xq; int64_t ld_xq;
+  const float* xamax;
+  uint32_t* xcnt;
+  float* xs_out;
 };
 const float* pair_norm_unit_scale();  // device address of 1.0f (the BF16 path's s_a = s_b)
 // tn = 512 (one accumulator, two N = 256 MMAs per K step) or 256 (double-buffered accumulators)

@@ -33,6 +33,7 @@ namespace loka {
 
 constexpr int kPnEpiWarps = 8;
 constexpr int kPnThreads = 64 + 32 * kPnEpiWarps;
+constexpr int kPnCastWarps = 2;  // CASTX: warps that quantize X for the tiles ahead of the MMAs
 constexpr uint32_t kPnSentinel = 0xFFFFFFFFu;  // a NaN no statistic of finite data can take
 
 template <int TN>
@@ -94,6 +95,33 @@ LOKA_DEVINL float4 rec_wait(const float4* p) {
   return v;
 }
 
+// CASTX producer side: wait until a row block's cast parts are all published (acquire), with the watchdog
+LOKA_DEVINL void xcnt_wait(const uint32_t* c, uint32_t need) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+  if (v >= need) return;
+  uint32_t spins = 0;
+  uint64_t t0 = 0;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+    if (v >= need) return;
+    __nanosleep(64);
+    if ((++spins & 63u) != 0) continue;
+    const uint64_t t = globaltimer_ns();
+    if (t0 == 0) t0 = t;
+    if (*reinterpret_cast<volatile int*>(&g_loka_abort)) return;
+    if (t - t0 > kHangNs) {
+      if (atomicAdd(&g_loka_hang[0], 1ull) == 0) {
+        g_loka_hang[1] = 101ull;
+        g_loka_hang[2] = (unsigned long long)blockIdx.x;
+        g_loka_hang[3] = (unsigned long long)threadIdx.x;
+      }
+      atomicExch(&g_loka_abort, 1);
+      return;
+    }
+  }
+}
+
 LOKA_DEVINL float hswish(float x) {  // x * ReLU6(x + 3) / 6
   const float t = fminf(fmaxf(x + 3.f, 0.f), 6.f);
   return __fdiv_rn(__fmul_rn(x, t), 6.f);
@@ -102,9 +130,13 @@ LOKA_DEVINL float hswish(float x) {  // x * ReLU6(x + 3) / 6
 // BF16IN: BF16 operands (kind::f16; a 128-byte stage row holds 64 K elements; the maps are byte views
 // of the bf16 data): the library's own BF16 path with the same fused epilogue (SURVEY.md §8(d)'s
 // secondary denominator, separating the FP8 gain from the fusion gain)
-// BWD: the NEXT-1 norm backward epilogue (a separate instance, so the forward carries none of it)
-template <int TN, int NORM, bool BF16IN, bool BWD>
-__global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_constant__ PairNormParams p) {
+// BWD: the NEXT-1 norm backward epilogue (a separate instance, so the forward carries none of it).
+// CASTX: the tensorwise cast of X fused into the GEMM (x_recipe, "quantization overhead"):
+// two extra warps per CTA cast this pair's share of each upcoming row block from bf16 to FP8 codes with
+// the given (all-reduced) amax, publishing per-row-block counters that the TMA producers wait on.
+template <int TN, int NORM, bool BF16IN, bool BWD, bool CASTX = false>
+__global__ void __launch_bounds__(kPnThreads + (CASTX ? 32 * kPnCastWarps : 0), 1)
+    pair_norm_kernel(const __grid_constant__ PairNormParams p) {
   using Cf = PnCfg<TN>;
   constexpr int kHN = TN / 2;     // columns per epilogue thread
   constexpr int kNch = kHN / 32;  // 32-column chunks per thread
@@ -173,6 +205,10 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
       const uint32_t full0 = mapa_shared(smem_u32(full_bar), 0);
       int it = 0, mb, nb;
       for (int k = 0; tile_of(k, mb, nb); ++k) {
+        if constexpr (CASTX) {  // this row block's codes: all 4 G cast parts published
+          xcnt_wait(&p.xcnt[mb], 4u * (uint32_t)G);
+          fence_proxy_async_global();  // (generic-proxy stores of other SMs -> this SM's TMA reads)
+        }
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % Cf::kStages;
           const uint32_t ph = (uint32_t)(it / Cf::kStages) & 1u;
@@ -224,6 +260,54 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
       }
     }
     __syncwarp();
+  } else if (CASTX && warp >= 2 + kPnEpiWarps) {
+    // ===== X cast warps (both CTAs): row block mb's 256 rows are split over its G tiles' pairs, and a
+    // pair's share over its 2 CTAs x 2 cast warps; each warp casts its rows (fl32(x r), satRNE, the
+    // arithmetic of loka_quantize's tensorwise cast: bit-identical codes), then publishes one part ====
+    const int cw = warp - (2 + kPnEpiWarps);
+    float s_x, r_x;
+    if (p.a_fmt) scales_from_amax<LOKA_E5M2, LOKA_SCALE_F32>(*p.xamax, s_x, r_x);
+    else scales_from_amax<LOKA_E4M3, LOKA_SCALE_F32>(*p.xamax, s_x, r_x);
+    if (blockIdx.x == 0 && cw == 0 && lane == 0 && p.xs_out) p.xs_out[0] = s_x;
+    int mb, nb;
+    for (int k = 0; tile_of(k, mb, nb); ++k) {
+      const int j0 = (256 * nb) / G, j1 = (256 * (nb + 1)) / G, part = rank * kPnCastWarps + cw;
+      const int r0 = j0 + ((j1 - j0) * part) / 4, r1 = j0 + ((j1 - j0) * (part + 1)) / 4;
+      for (int rr = r0; rr < r1; ++rr) {
+        const int64_t row = (int64_t)mb * 256 + rr;
+        if (row >= p.M) break;
+        const __nv_bfloat16* xr = p.xb + row * p.ld_xb;
+        uint8_t* qr = p.xq + row * p.ld_xq;
+        for (int c0 = lane * 8; c0 < p.K; c0 += 256 * 4) {
+          uint4 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int c = c0 + 256 * u;
+            v[u] = c < p.K ? __ldcs(reinterpret_cast<const uint4*>(xr + c)) : make_uint4(0u, 0u, 0u, 0u);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int c = c0 + 256 * u;
+            if (c >= p.K) break;
+            float f[8] = {bf16lo_to_f32(v[u].x), bf16hi_to_f32(v[u].x), bf16lo_to_f32(v[u].y), bf16hi_to_f32(v[u].y),
+                          bf16lo_to_f32(v[u].z), bf16hi_to_f32(v[u].z), bf16lo_to_f32(v[u].w), bf16hi_to_f32(v[u].w)};
+#pragma unroll
+            for (int i = 0; i < 8; ++i) f[i] = __fmul_rn(f[i], r_x);
+            const uint2 code = p.a_fmt ? make_uint2(cvt_fp8x4<LOKA_E5M2>(f[0], f[1], f[2], f[3]),
+                                                    cvt_fp8x4<LOKA_E5M2>(f[4], f[5], f[6], f[7]))
+                                       : make_uint2(cvt_fp8x4<LOKA_E4M3>(f[0], f[1], f[2], f[3]),
+                                                    cvt_fp8x4<LOKA_E4M3>(f[4], f[5], f[6], f[7]));
+            *reinterpret_cast<uint2*>(qr + c) = code;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {  // release this part: the codes above, then the counter
+        __threadfence();
+        fence_proxy_async_global();
+        atomicAdd(&p.xcnt[mb], 1u);
+      }
+    }
   } else {
     // ===== epilogue (both CTAs) =====
     const int q = warp & 3;          // TMEM lane quadrant (hardware: warp w reads lanes 32 (w % 4) ..)
@@ -240,6 +324,12 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
     // fold: with a tensor-wide s_b and no bias, y = acc * c (c = s_a s_b per row), so the statistics
     // are taken on acc and scaled (mean * c, M2 * c^2), and pass N is one FMA per element
     constexpr bool bwd = BWD;  // NEXT-1 norm backward (dL/dz from dL/dh, the forward's saved xhat / rstd)
+    float sa_castx = 1.f;
+    if constexpr (CASTX) {
+      float r_unused;
+      if (p.a_fmt) scales_from_amax<LOKA_E5M2, LOKA_SCALE_F32>(*p.xamax, sa_castx, r_unused);
+      else scales_from_amax<LOKA_E4M3, LOKA_SCALE_F32>(*p.xamax, sa_castx, r_unused);
+    }
     const bool xs_stage = BWD && p.out_dtype == LOKA_BF16;  // xhat staged in smem (bf16 dz boxes match it)
     uint32_t xph = 0;
     const bool fold = !p.sb_row && p.bias == nullptr && !bwd;
@@ -287,7 +377,8 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
 
       const int grow = mb * 256 + rank * 128 + r;
       const bool row_ok = grow < p.M;
-      const float sa = row_ok ? __ldg(p.sa + (p.sa_row ? grow : 0)) : 0.f;
+      // (CASTX: X's scale from the amax itself — p.sa is written by another CTA's cast warps)
+      const float sa = !row_ok ? 0.f : CASTX ? sa_castx : __ldg(p.sa + (p.sa_row ? grow : 0));
       const float cfold = fold ? __fmul_rn(sa, __ldg(p.sb)) : 1.f;  // y = acc * cfold when folding
       const float2 sa2 = make_float2(sa, sa);
       const int col0 = nb * TN + h * kHN;  // first column of this thread
@@ -723,16 +814,16 @@ __global__ void __launch_bounds__(kPnThreads, 1) pair_norm_kernel(const __grid_c
   }
 }
 
-template <int TN, int NORM, bool BF16IN, bool BWD = false>
+template <int TN, int NORM, bool BF16IN, bool BWD = false, bool CASTX = false>
 static cudaError_t launch_pn(const PairNormParams& p, int pairs, cudaStream_t st) {
   {
     cudaError_t e =
-        ensure_func_attrs(reinterpret_cast<const void*>(pair_norm_kernel<TN, NORM, BF16IN, BWD>), PnCfg<TN>::kSmem);
+        ensure_func_attrs(reinterpret_cast<const void*>(pair_norm_kernel<TN, NORM, BF16IN, BWD, CASTX>), PnCfg<TN>::kSmem);
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(2 * pairs), 1, 1);
-  cfg.blockDim = dim3(kPnThreads, 1, 1);
+  cfg.blockDim = dim3(kPnThreads + (CASTX ? 32 * kPnCastWarps : 0), 1, 1);
   cfg.dynamicSmemBytes = PnCfg<TN>::kSmem;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
@@ -744,7 +835,7 @@ static cudaError_t launch_pn(const PairNormParams& p, int pairs, cudaStream_t st
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, pair_norm_kernel<TN, NORM, BF16IN, BWD>, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, pair_norm_kernel<TN, NORM, BF16IN, BWD, CASTX>, p);
   note_launch();
   return e;
 }
@@ -760,6 +851,14 @@ static cudaError_t launch_pn_norm(const PairNormParams& p, int pairs, cudaStream
 }
 
 cudaError_t launch_pair_norm(const PairNormParams& p, int tn, int pairs, cudaStream_t st) {
+  if (p.castx) {  // (256-wide tiles, FP8, forward)
+    switch (p.norm) {
+      case LOKA_NORM_LAYER: return launch_pn<256, LOKA_NORM_LAYER, false, false, true>(p, pairs, st);
+      case LOKA_NORM_RMS: return launch_pn<256, LOKA_NORM_RMS, false, false, true>(p, pairs, st);
+      case LOKA_NORM_BLOCK_RMS: return launch_pn<256, LOKA_NORM_BLOCK_RMS, false, false, true>(p, pairs, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   if (p.bwd) {  // (256-wide tiles, FP8 operands)
     switch (p.norm) {
       case LOKA_NORM_LAYER: return launch_pn<256, LOKA_NORM_LAYER, false, true>(p, pairs, st);

@@ -213,3 +213,33 @@ def test_norm_backward_on_pair_engine(tn, norm, N, act, affine, od):
                                      gamma=None if gamma is None else gamma.double().numpy(),
                                      beta=None if beta is None else beta.double().numpy(), act=act)
     _check(y, dz, od)
+
+
+@pytest.mark.parametrize("M,N,K,norm", [(600, 4096, 1000, "layer"), (1300, 768, 512, "rms"), (520, 512, 256, "block_rms")])
+@pytest.mark.parametrize("given_amax", [False, True])
+def test_fused_tensorwise_cast_x_recipe(M, N, K, norm, given_amax, monkeypatch):
+    """x_recipe with a tensorwise bf16 A on the pair route: the cast runs inside the GEMM kernel (two
+    cast warps per CTA publish per-row-block counters the TMA producers wait on).  Output bit-identical
+    to loka_quantize(tensor) + the call on the codes; the codes in the workspace equal the oracle's;
+    with x_amax given (the data-parallel all-reduced amax) the cast uses it."""
+    import ctypes as C
+    monkeypatch.setenv("LOKA_PAIRNORM", "256")  # the pair route also for the small shapes
+    x = to_dev_padded(synth.heavy(M, K, 19))
+    wq, ws = lk.loka_quantize(to_dev_padded(synth.weight(N, K, 20)), "e4m3", "row")
+    amax = torch.tensor([float(x.float().abs().max()) * (1.5 if given_amax else 1.0)], device=DEV)
+    xq, xs = lk.loka_quantize(x, "e4m3", "tensor", phase="cast", amax=amax)
+    y_ref, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, a_gran="tensor", norm=norm, out_dtype="f32")
+    keep = []
+    args, y, _ = lk.make_linear_args(xq, xs, wq, ws, a_gran="tensor", norm=norm, out_dtype="f32", keep=keep)
+    args.a = lk._tensor(x, lk.BF16, M, K, None, "tensor")
+    if given_amax:
+        args.x_amax = amax.data_ptr()
+    nws = int(lk._lib.loka_linear_workspace_size(C.byref(args)))
+    wsb = torch.empty(nws, dtype=torch.uint8, device=DEV)
+    assert lk._lib.loka_fp8_linear_norm(C.byref(args), C.c_void_p(wsb.data_ptr()), nws, None) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(y, y_ref)
+    ld = (K + 15) // 16 * 16
+    codes = wsb[:M * ld].view(M, ld)[:, :K]
+    oq, _ = oracle.quantize.quantize(x.cpu().double().numpy(), "e4m3", "tensor", amax=np.array([float(amax)]))
+    assert np.array_equal(codes.cpu().numpy(), oq)
