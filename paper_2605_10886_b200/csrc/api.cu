@@ -324,6 +324,13 @@ static size_t xq_prefix_bytes(const loka_linear_args* a) {
   return al((size_t)a->M * (size_t)xq_ld(a)) + al(xq_scale_elems(a) * 4) + 256 + al((size_t)cdiv(a->M, 256) * 4);
 }
 static size_t linear_ws_quantized(const loka_linear_args* a);
+// LOKA_FUSED_CAST=1: x_recipe's tensorwise cast inside the GEMM kernel (CASTX).  Off by default: measured
+// interleaved at cfg5 it is not faster than the separate cast under the B200's power cap (the cast's HBM
+// and ALU work costs the same energy either way; profiles/r02o_castx_ab.json), and it slows the MMAs.
+static bool fused_cast_env() {
+  const char* e = std::getenv("LOKA_FUSED_CAST");
+  return e && e[0] == '1';
+}
 size_t loka_linear_workspace_size(const loka_linear_args* a) {
   if (x_unquantized(a)) {
     loka_linear_args q = *a;  // the FP8 problem the call runs after its internal quantize
@@ -871,6 +878,8 @@ static loka_status run_pair_norm(const loka_linear_args* a, const PnPlan& pl, vo
     p.xamax = cx->amax;
     p.xcnt = cx->counters;
     p.xs_out = cx->xs_out;
+    p.cast_ahead = 3;
+    if (const char* e = std::getenv("LOKA_CAST_AHEAD")) p.cast_ahead = std::atoi(e);
   }
   if (a->bwd_xhat) {
     p.bwd = 1;
@@ -976,7 +985,7 @@ loka_status loka_fp8_linear_norm(const loka_linear_args* a, void* ws, size_t ws_
     // with the MMAs of earlier row blocks; only the amax pass precedes it (skipped with a given x_amax)
     const PnPlan pl = pair_norm_plan_dev(&q);
     if (pl.ok && pl.tn == 256 && a->a.gran == LOKA_GRAN_TENSOR && a->a.dtype == LOKA_BF16 && a->K % 8 == 0 &&
-        !a->bwd_xhat && std::getenv("LOKA_NO_FUSED_CAST") == nullptr) {
+        !a->bwd_xhat && fused_cast_env()) {
       const float* amax = a->x_amax;
       if (!amax) {
         loka_status st = loka_quantize(&x, &qt, nullptr, LOKA_PHASE_AMAX_ONLY, amax_slot, a->status_dev, nullptr, 0,

@@ -356,6 +356,7 @@ struct PairNormParams {
   const float* xamax;
   uint32_t* xcnt;
   float* xs_out;
+  int32_t cast_ahead;  // castx pacing (tiles ahead of the epilogue; LOKA_CAST_AHEAD, default 3)
 };
 const float* pair_norm_unit_scale();  // device address of 1.0f (the BF16 path's s_a = s_b)
 // tn = 512 (one accumulator, two N = 256 MMAs per K step) or 256 (double-buffered accumulators)

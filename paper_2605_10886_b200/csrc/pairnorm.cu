@@ -34,6 +34,8 @@ namespace loka {
 constexpr int kPnEpiWarps = 8;
 constexpr int kPnThreads = 64 + 32 * kPnEpiWarps;
 constexpr int kPnCastWarps = 2;  // CASTX: warps that quantize X for the tiles ahead of the MMAs
+constexpr int kPnCastAhead = 3;  // CASTX default: the cast warps stay <= this many tiles ahead of the epilogue
+                                 // (spreads their HBM / L2 traffic over the GEMM instead of bursting it)
 constexpr uint32_t kPnSentinel = 0xFFFFFFFFu;  // a NaN no statistic of finite data can take
 
 template <int TN>
@@ -151,6 +153,7 @@ __global__ void __launch_bounds__(kPnThreads + (CASTX ? 32 * kPnCastWarps : 0), 
   uint64_t* xbar = acc_empty + 2;  // [8] backward: the warps' staged xhat sub-tiles landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbar + kPnEpiWarps);
   float4* hrec = reinterpret_cast<float4*>(smem + Cf::kOffRec);
+  volatile int* ep_tile = reinterpret_cast<volatile int*>(tmem_slot + 1);  // CASTX pacing: the epilogue's tile
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = (int)cluster_ctarank();
@@ -191,6 +194,7 @@ __global__ void __launch_bounds__(kPnThreads + (CASTX ? 32 * kPnCastWarps : 0), 
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc_cg2<512>(tmem_slot);
+  if (threadIdx.x == 0) *ep_tile = 0;
   pdl_wait();
   tc_fence_before();
   __syncthreads();
@@ -271,6 +275,9 @@ __global__ void __launch_bounds__(kPnThreads + (CASTX ? 32 * kPnCastWarps : 0), 
     if (blockIdx.x == 0 && cw == 0 && lane == 0 && p.xs_out) p.xs_out[0] = s_x;
     int mb, nb;
     for (int k = 0; tile_of(k, mb, nb); ++k) {
+      if (k > p.cast_ahead) {  // pacing: wait for the epilogue to reach tile k - cast_ahead
+        while (*ep_tile < k - p.cast_ahead) __nanosleep(256);
+      }
       const int j0 = (256 * nb) / G, j1 = (256 * (nb + 1)) / G, part = rank * kPnCastWarps + cw;
       const int r0 = j0 + ((j1 - j0) * part) / 4, r1 = j0 + ((j1 - j0) * (part + 1)) / 4;
       for (int rr = r0; rr < r1; ++rr) {
@@ -372,6 +379,7 @@ __global__ void __launch_bounds__(kPnThreads + (CASTX ? 32 * kPnCastWarps : 0), 
       if (lane == 0) mbar_wait(&acc_full[buf], use & 1u, 3);
       __syncwarp();
       tc_fence_after();
+      if (CASTX && et == 0) *ep_tile = j;  // (the cast warps pace themselves on this)
       uint64_t* tr = (p.trace && j < 64 && et == 0) ? p.trace + ((size_t)blockIdx.x * 64 + j) * 8 : nullptr;
       if (tr) tr[0] = globaltimer_ns();
 

@@ -224,6 +224,7 @@ def test_fused_tensorwise_cast_x_recipe(M, N, K, norm, given_amax, monkeypatch):
     with x_amax given (the data-parallel all-reduced amax) the cast uses it."""
     import ctypes as C
     monkeypatch.setenv("LOKA_PAIRNORM", "256")  # the pair route also for the small shapes
+    monkeypatch.setenv("LOKA_FUSED_CAST", "1")  # (the opt-in route)
     x = to_dev_padded(synth.heavy(M, K, 19))
     wq, ws = lk.loka_quantize(to_dev_padded(synth.weight(N, K, 20)), "e4m3", "row")
     amax = torch.tensor([float(x.float().abs().max()) * (1.5 if given_amax else 1.0)], device=DEV)
