@@ -72,6 +72,20 @@ static bool make_map_u8(CUtensorMap* m, const void* ptr, int64_t rows, int64_t c
 
 static int elem_size(loka_dtype t) { return t == LOKA_F32 ? 4 : t == LOKA_BF16 ? 2 : 1; }
 
+// 2D map over a row-major bf16 matrix [rows, cols] (ld elements), box {128, 128}, no swizzle
+// (the streaming quantize's input tile: rows of 256 B read by half-warps without conflicts).
+static bool make_map_bf16_tile(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {128u, 128u};
+  cuuint32_t es[2] = {1u, 1u};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // 2D map over a UE8M0 scale pack ([atoms][kblocks][512 B]) viewed as rows of 256 bytes; one box
 // {256, 2} is one atom, no swizzle (the tcgen05.cp source layout is the plain 512-byte atom).
 static bool make_map_pack(CUtensorMap* m, const void* ptr, int64_t rows256, uint32_t box_rows = 2) {
@@ -193,9 +207,14 @@ loka_status loka_quantize(const loka_tensor* x, loka_tensor* q, loka_tensor* qt,
     // the tiled path writes the transposed codes with 8-byte stores: same rules as q
     if (!qt->data || qt->ld < qt->cols || !aligned16(qt->data) || qt->ld % 16) return LOKA_ERR_INVALID_ARG;
   }
-  // the tiled cast(-transpose) path serves column-spanning granules and transposed copies
+  // the tiled cast(-transpose) path serves column-spanning granules and transposed copies; with
+  // bf16 input its tile pass — and the 1x128 / 128x128 casts — run on the streaming TMA kernel
+  const int tgran = dual ? 64 : q->gran;
+  const bool stream_tile = x->dtype == LOKA_BF16 && phase != LOKA_PHASE_AMAX_ONLY &&
+                           phase != LOKA_PHASE_CAST_DELAYED && quant_tile_tma_eligible(tgran) &&
+                           (qt != nullptr || (q->gran != LOKA_GRAN_ROW && q->gran != LOKA_GRAN_TENSOR));
   const bool tiled = (qt != nullptr || q->gran == LOKA_GRAN_COL || q->gran == LOKA_GRAN_BLK_128x1 ||
-                      q->gran == LOKA_GRAN_BLK_1x32) &&
+                      q->gran == LOKA_GRAN_BLK_1x32 || stream_tile) &&
                      phase != LOKA_PHASE_AMAX_ONLY;
   int sms = 148;
   loka_status st = check_device(&sms);
@@ -222,9 +241,20 @@ loka_status loka_quantize(const loka_tensor* x, loka_tensor* q, loka_tensor* qt,
   p.ldqt = qt ? qt->ld : 0;
   p.scales_t = qt ? qt->scales : nullptr;
   p.status = status_dev;
+  static thread_local QuantTileParams tp;  // (3 tensor maps: not on the stack)
+  if (stream_tile) {
+    tp.p = p;
+    tp.amax_g = nullptr;
+    tp.nbc = (int)cdiv(x->cols, 128);
+    tp.nbr = (int)cdiv(x->rows, 128);
+    tp.ntiles = (int64_t)tp.nbc * tp.nbr;
+    if (!make_map_bf16_tile(&tp.tx, x->data, x->rows, x->cols, x->ld)) return LOKA_ERR_CUDA;
+    if (p.q && !make_map_u8(&tp.tq, p.q, x->rows, x->cols, q->ld, 128)) return LOKA_ERR_CUDA;
+    if (p.qt && !make_map_u8(&tp.tqt, p.qt, x->cols, x->rows, qt->ld, 128)) return LOKA_ERR_CUDA;
+  }
   cudaError_t e =
-      tiled ? launch_quantize_tiled(p, x->dtype == LOKA_BF16, q->dtype, q->scale_fmt, dual ? 64 : q->gran, phase, amax,
-                                    pre, reinterpret_cast<cudaStream_t>(stream))
+      tiled ? launch_quantize_tiled(p, x->dtype == LOKA_BF16, q->dtype, q->scale_fmt, tgran, phase, amax,
+                                    pre, reinterpret_cast<cudaStream_t>(stream), stream_tile ? &tp : nullptr, sms)
             : launch_quantize(p, x->dtype == LOKA_BF16, q->dtype, q->scale_fmt, q->gran, phase, amax,
                               reinterpret_cast<cudaStream_t>(stream), sms);
   if (e == cudaErrorNotSupported) return LOKA_ERR_UNSUPPORTED;

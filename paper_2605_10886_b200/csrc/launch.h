@@ -67,10 +67,26 @@ cudaError_t launch_quantize_tma_group(const QuantGroup& grp, int64_t max_cols, i
                                       const float* amax_dev, int num_sms, cudaStream_t st,
                                       uint32_t* amax_next = nullptr);
 
+// Streaming tile quantize (quantize_tile.cu, bf16 input): maps built by api.cu — tx over x
+// [rows, cols] bf16 box {128, 128} no swizzle; tq over q [rows, cols] u8 and tqt over qt
+// [cols, rows] u8, box {128, 128} SW128 (unused maps when q / qt are null).
+struct QuantTileParams {
+  CUtensorMap tx, tq, tqt;
+  QuantParams p;
+  const uint32_t* amax_g;  // TENSOR: [1] amax bits; ROW / COL: the pre-pass array; else null
+  int64_t ntiles;          // nbr * nbc
+  int nbc, nbr;            // 128-wide column / row tiles
+};
+bool quant_tile_tma_eligible(int gran);
+cudaError_t launch_quant_tile_tma(const QuantTileParams& tp, int fmt, int scale_fmt, int gran, int num_sms,
+                                  cudaStream_t st);
+
 // Tiled quantize (quantize_t.cu): any granularity incl. COL / BLK_128x1, optional transposed
-// copy; ws holds the ROW / COL amax pre-pass array (4 * max(rows, cols) bytes).
+// copy; ws holds the ROW / COL amax pre-pass array (4 * max(rows, cols) bytes).  tile (nullable,
+// bf16 input only): the streaming kernel's maps — the tile pass then runs in quantize_tile.cu.
 cudaError_t launch_quantize_tiled(const QuantParams& p, bool in_bf16, int fmt, int scale_fmt, int gran, int phase,
-                                  float* amax_dev, void* ws, cudaStream_t st);
+                                  float* amax_dev, void* ws, cudaStream_t st, QuantTileParams* tile = nullptr,
+                                  int num_sms = 148);
 
 constexpr int kMaxQuantGroup = 64;
 struct QuantGroup {

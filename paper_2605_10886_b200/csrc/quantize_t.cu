@@ -81,7 +81,17 @@ __global__ void __launch_bounds__(256) row_amax_kernel(QuantParams p, uint32_t* 
   if (row >= p.rows) return;
   const Tin* xr = reinterpret_cast<const Tin*>(p.x) + row * p.ldx;
   uint32_t am = 0;
-  for (int64_t c = lane * 8; c < p.cols; c += 256) {
+  int64_t c = lane * 8;
+  for (; c + 768 + 8 <= p.cols; c += 1024) {  // 4 independent 16-byte loads in flight per lane
+    float f[4][8];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) In8<Tin>::load(xr + c + 256 * u, 8, f[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) am = max(am, absbits(f[u][i]));
+  }
+  for (; c < p.cols; c += 256) {
     float f[8];
     In8<Tin>::load(xr + c, (int)imin64(8, p.cols - c), f);
 #pragma unroll
@@ -401,7 +411,7 @@ static cudaError_t launch_pdl_t(void (*kern)(KArgs...), dim3 grid, dim3 block, c
 
 template <typename Tin, int FMT, int SF>
 static cudaError_t launch_tiled_t(const QuantParams& p, int gran, int phase, float* amax_dev, void* ws,
-                                  cudaStream_t st) {
+                                  cudaStream_t st, QuantTileParams* tile, int num_sms) {
   const dim3 tiles((unsigned)((p.cols + 127) / 128), (unsigned)((p.rows + 127) / 128));
   uint32_t* amax = nullptr;
   cudaError_t e = cudaSuccess;
@@ -419,6 +429,10 @@ static cudaError_t launch_tiled_t(const QuantParams& p, int gran, int phase, flo
   }
   if (e != cudaSuccess) return e;
   const uint32_t* ag = amax;
+  if (tile && sizeof(Tin) == 2) {  // the streaming kernel (bf16 input; api.cu built the maps)
+    tile->amax_g = ag;
+    return launch_quant_tile_tma(*tile, FMT, SF, gran, num_sms, st);
+  }
   switch (gran) {
     case LOKA_GRAN_TENSOR: return launch_pdl_t(quant_tile_kernel<Tin, FMT, SF, LOKA_GRAN_TENSOR>, tiles, dim3(256), st, p, ag);
     case LOKA_GRAN_ROW: return launch_pdl_t(quant_tile_kernel<Tin, FMT, SF, LOKA_GRAN_ROW>, tiles, dim3(256), st, p, ag);
@@ -437,9 +451,9 @@ static cudaError_t launch_tiled_t(const QuantParams& p, int gran, int phase, flo
 }
 
 cudaError_t launch_quantize_tiled(const QuantParams& p, bool in_bf16, int fmt, int scale_fmt, int gran, int phase,
-                                  float* amax_dev, void* ws, cudaStream_t st) {
+                                  float* amax_dev, void* ws, cudaStream_t st, QuantTileParams* tile, int num_sms) {
 #define LOKA_T(T, F, S) \
-  if (fmt == F && scale_fmt == S) return launch_tiled_t<T, F, S>(p, gran, phase, amax_dev, ws, st);
+  if (fmt == F && scale_fmt == S) return launch_tiled_t<T, F, S>(p, gran, phase, amax_dev, ws, st, tile, num_sms);
   if (in_bf16) {
     LOKA_T(__nv_bfloat16, LOKA_E4M3, LOKA_SCALE_F32)
     LOKA_T(__nv_bfloat16, LOKA_E4M3, LOKA_SCALE_UE8M0)

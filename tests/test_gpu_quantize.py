@@ -240,3 +240,60 @@ def test_delayed_scaling_phase(dtype, rows, fmt):
     assert_bytes_equal(q, oq)
     a = amax.cpu().numpy()
     assert a[0] == np.float32(prev) and a[1] == np.float32(np.abs(x.double().numpy()).max())
+
+
+@pytest.mark.parametrize("gran,gran_t", [("blk_1x128", None), ("blk_128x1", None), ("blk_128x128", None),
+                                         ("blk_1x128", "blk_1x128"), ("row", None), ("col", None)])
+@pytest.mark.parametrize("transpose", [False, True])
+def test_streaming_tile_many_tiles_sampled(gran, gran_t, transpose):
+    """The streaming tile kernel (quantize_tile.cu) with ~28 tiles per CTA, so both consumer groups
+    and every stage of the ring wrap many times (a parity race there showed only at this scale):
+    16384 x 2048 heavy-tailed bf16, sampled 128 x 128 tiles (block granules depend on their tile
+    only), rows (ROW) or columns (COL) checked bit-exact, codes and transposed codes and scales."""
+    if gran_t is not None and not transpose:
+        pytest.skip("dual needs the transposed copy")
+    R, C = 16384, 2048
+    x = synth.heavy(R, C, 7, device=DEV)
+    res = lk.loka_quantize(x, "e4m3", gran, transpose=transpose, gran_t=gran_t)
+    q, s = res[0], res[1]
+    qt, st = (res[2], res[3]) if transpose else (None, None)
+    torch.cuda.synchronize()
+    g = torch.Generator().manual_seed(1)
+    Q = lambda a, gr: oracle.quantize.quantize(a.cpu().double().numpy(), "e4m3", gr)
+    if gran in ("row", "col"):
+        n = R if gran == "row" else C
+        idx = torch.randperm(n, generator=g)[:48].sort().values.to(DEV)
+        xs = x[idx] if gran == "row" else x[:, idx]
+        oq, os_ = Q(xs, gran)
+        assert_bytes_equal(q[idx] if gran == "row" else q[:, idx], oq)
+        assert_scales_equal(s[idx], os_)
+        if transpose:
+            assert_bytes_equal(qt[:, idx] if gran == "row" else qt[idx], oq.T.copy())
+            assert_scales_equal(st[idx], os_)
+        return
+    for t in torch.randperm((R // 128) * (C // 128), generator=g)[:24].tolist():
+        tr, tc = divmod(t, C // 128)
+        r0, c0 = tr * 128, tc * 128
+        tile = x[r0:r0 + 128, c0:c0 + 128]
+        oq, os_ = Q(tile, gran)
+        assert_bytes_equal(q[r0:r0 + 128, c0:c0 + 128], oq, f"tile {tr},{tc}")
+        if gran == "blk_1x128":
+            assert_scales_equal(s[r0:r0 + 128, tc], os_.reshape(-1))
+        elif gran == "blk_128x1":
+            assert_scales_equal(s[tr, c0:c0 + 128], os_.reshape(-1))
+        else:
+            assert_scales_equal(s[tr, tc].reshape(1), os_.reshape(-1))
+        if not transpose:
+            continue
+        if gran_t is not None:  # dual: qt = the tile's 128x1 quantization, transposed
+            tq_, ts_ = Q(tile, "blk_128x1")
+            assert_bytes_equal(qt[c0:c0 + 128, r0:r0 + 128], tq_.T.copy(), f"dual tile {tr},{tc}")
+            assert_scales_equal(st[c0:c0 + 128, tr], ts_.reshape(-1))
+            continue
+        assert_bytes_equal(qt[c0:c0 + 128, r0:r0 + 128], oq.T.copy(), f"t tile {tr},{tc}")
+        if gran == "blk_1x128":      # t-frame 128x1 [nbc, rows]
+            assert_scales_equal(st[tc, r0:r0 + 128], os_.reshape(-1))
+        elif gran == "blk_128x1":    # t-frame 1x128 [cols, nbr]
+            assert_scales_equal(st[c0:c0 + 128, tr], os_.reshape(-1))
+        else:
+            assert_scales_equal(st[tc, tr].reshape(1), os_.reshape(-1))

@@ -61,8 +61,12 @@ def main():
             ms = sum(t) / len(t)
             nbytes = R * Cc * (2 + (2 if tr else 1))
             gbs = nbytes / (ms * 1e-3) / 1e9
+            # the granularities whose amax spans the whole tensor / row / column beyond one tile
+            # read x twice (amax pre-pass, then the cast): the bytes HBM actually moves
+            moved = nbytes + (R * Cc * 2 if gran in ("tensor", "col") or (gran == "row" and tr) else 0)
             out["kernels"][name] = {"ms": round(ms, 4), "algorithmic_bytes": nbytes, "gbs": round(gbs, 1),
-                                    "frac_of_hbm": round(gbs / hbm, 3)}
+                                    "frac_of_hbm": round(gbs / hbm, 3), "moved_bytes": moved,
+                                    "gbs_moved": round(moved / (ms * 1e-3) / 1e9, 1)}
         # the tensorwise recipe's two phases separately (split-phase for the DP all-reduce)
         amax = torch.zeros(1, dtype=torch.float32, device=dev)
         s1 = torch.empty(1, dtype=torch.float32, device=dev)
