@@ -488,12 +488,40 @@ def cfg2_extra(lk, dev, rank, steps, warmup, stream):
     out_bf = torch.empty(M_PER_GPU, DIMS[8], dtype=torch.bfloat16, device=dev)
     gb = capture(lambda: bf16_step(x, w, out_bf), stream)
     tb = time_steps(gb.replay, steps, warmup, flush, stream)
+    # the library's own BF16 path (kind::f16 CTA-pair engine + the same fused LayerNorm), layer by layer
+    # (a BF16 layer input of 128 rows x 1024 K is 256 KB: it cannot stay resident in one CTA's shared
+    # memory, so there is no BF16 form of the one-launch stack)
+    import ctypes
+    hb = [x.to(torch.bfloat16)] + [torch.empty(M_PER_GPU, DIMS[l + 1], dtype=torch.bfloat16, device=dev)
+                                   for l in range(8)]
+    wb = [t.to(torch.bfloat16) for t in w]
+    one = torch.ones(1, dtype=torch.float32, device=dev)
+    keep, bl_args = [], []
+    for l in range(8):
+        ar, _, _ = lk.make_linear_args(hb[l], one, wb[l], one, a_gran="tensor", b_gran="tensor", norm="layer",
+                                       eps=1e-5, out_dtype="bf16", y=hb[l + 1], keep=keep)
+        ar.a.dtype = lk.BF16
+        ar.b.dtype = lk.BF16
+        bl_args.append(ar)
+    bl_ws = torch.empty(max(256, max(int(lk._lib.loka_bf16_linear_workspace_size(ctypes.byref(a_))) for a_ in bl_args)),
+                        dtype=torch.uint8, device=dev)
+
+    def bf16_lib_step():
+        for a_ in bl_args:
+            assert lk._lib.loka_bf16_linear_norm(ctypes.byref(a_), ctypes.c_void_p(bl_ws.data_ptr()), bl_ws.numel(),
+                                                 sh) == 0
+
+    gbl = capture(bf16_lib_step, stream)
+    tbl = time_steps(gbl.replay, steps, warmup, flush, stream)
     ms8, msst, msb = sum(t8) / len(t8), sum(tst) / len(tst), sum(tb) / len(tb)
+    msbl = sum(tbl) / len(tbl)
     fl = flops_per_step()
     return {"workload": WORKLOAD, "value": round(fl / ms8 / 1e9, 2), "unit": "TFLOP/s", "ms_per_step": round(ms8, 5),
             "step": "1 grouped quantize launch (X + 8 W) + 1 fused 8-layer stack launch, CUDA-graph replay, "
                     "L2 flushed before every step",
             "bf16_ms_per_step": round(msb, 5), "speedup_vs_bf16": round(msb / ms8, 3),
+            "bf16_library_fused_ms_per_step": round(msbl, 5), "speedup_vs_bf16_library_fused": round(msbl / ms8, 3),
+            "bf16_library_fused_impl": "8 x loka_bf16_linear_norm (kind::f16 CTA-pair GEMM + fused LayerNorm), graph",
             "stack_kernel_us": round(1e3 * msst, 3), "stack_kernel_tflops": round(fl / msst / 1e9, 2)}
 
 
@@ -536,11 +564,30 @@ def cfg3_extra(lk, dev, steps, warmup, stream):
             for j in range(8):
                 torch.matmul(xs[i], ws[i][j].t(), out=yb[i][j])
 
+    # the library's own BF16 grouped path (kind::f16 on the same CTA-pair engine, 2 launches of 32)
+    ybl = [[torch.empty(M, n, dtype=torch.bfloat16, device=dev) for n in S] for _ in S]
+    one = torch.ones(1, dtype=torch.float32, device=dev)
+    bl_args = []
+    for i in range(8):
+        for j in range(8):
+            ar, _, _ = lk.make_linear_args(xs[i], one, ws[i][j], one, a_gran="tensor", b_gran="tensor",
+                                           out_dtype="bf16", y=ybl[i][j], keep=keep)
+            ar.a.dtype = lk.BF16
+            ar.b.dtype = lk.BF16
+            bl_args.append(ar)
+    bl_arr = (lk.loka_linear_args * 64)(*bl_args)
+
+    def bf16_lib_step_3():
+        assert lk._lib.loka_grouped_bf16_linear(64, bl_arr, sh) == 0
+
     g8 = capture(fp8_step, stream)
     gb = capture(bf16_step_3, stream)
+    gbl = capture(bf16_lib_step_3, stream)
     t8 = time_steps(g8.replay, steps, warmup, flush, stream)
     tb = time_steps(gb.replay, steps, warmup, flush, stream)
+    tbl = time_steps(gbl.replay, steps, warmup, flush, stream)
     ms8, msb = sum(t8) / len(t8), sum(tb) / len(tb)
+    msbl = sum(tbl) / len(tbl)
     g8.replay()
     gb.replay()
     torch.cuda.synchronize()
@@ -560,6 +607,9 @@ def cfg3_extra(lk, dev, steps, warmup, stream):
             "value": round(flops / ms8 / 1e9, 2), "unit": "TFLOP/s", "ms_per_step": round(ms8, 5),
             "step": "grouped rowwise quantize of the 8 inputs + grouped FP8 GEMM (2 persistent launches), CUDA "
                     "graph, L2 flushed", "bf16_ms_per_step": round(msb, 5), "speedup_vs_bf16": round(msb / ms8, 3),
+            "bf16_library_grouped_ms_per_step": round(msbl, 5),
+            "speedup_vs_bf16_library_grouped": round(msbl / ms8, 3),
+            "bf16_library_grouped_impl": "loka_grouped_bf16_linear: the same CTA-pair engine with kind::f16 operands",
             "probe_geomean_mere_vs_bf16": round(geo, 5), "dispatch_fp8_layers": int(chosen),
             "dispatch_rule": "MERE < 0.2 and speedup > 1.05 (time shares of the grouped step)"}
 

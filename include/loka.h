@@ -293,6 +293,15 @@ LOKA_API loka_status loka_grouped_fp8_linear(int32_t G, const loka_linear_args* 
                                     loka_stream_t stream);
 LOKA_API size_t loka_grouped_workspace_size(int32_t G, const loka_linear_args* args);
 
+/* The library's own BF16 form of a6 (the secondary BF16 denominator of the
+ * ensemble, "many small GEMMs"): G problems with BF16 A [M,K] and B [N,K] (a/b dtype
+ * LOKA_BF16, K-major, ld * 2 % 16 == 0, scales ignored), Y = A . B^T (+ bias[n]) in bf16 or f32,
+ * in ONE persistent launch of the CTA-pair engine with tcgen05.mma.cta_group::2.kind::f16 (FP32
+ * accumulation in TMEM), longest K first, 256x256 tiles.  norm / act must be NONE, no FP8 output, no
+ * backward fields (else UNSUPPORTED); G <= 64 per call.  No workspace.  args: a host array of G
+ * structs, read during the call.                                                                  */
+LOKA_API loka_status loka_grouped_bf16_linear(int32_t G, const loka_linear_args* args, loka_stream_t stream);
+
 /* ---- NEXT-4: NVFP4 ----------------------------------------------------------
  * The paper names FP4 as future work; the recipe is DESIGN.md D35-D38 (oracle/nvfp4.py):
  * E2M1 codes (values {0, .5, 1, 1.5, 2, 3, 4, 6}, saturating RNE), one E4M3 block-scale code per

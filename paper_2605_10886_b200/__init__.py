@@ -137,6 +137,7 @@ _sig = {
     "loka_probe_track_covariance": ([C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "loka_source_hash": ([], C.c_char_p),
     "loka_bf16_linear_norm": ([C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p], C.c_int),
+    "loka_grouped_bf16_linear": ([C.c_int32, _P(loka_linear_args), C.c_void_p], C.c_int),
     "loka_bf16_linear_workspace_size": ([C.c_void_p], C.c_size_t),
     "loka_dispatch_select": ([_P(loka_candidate), C.c_int32, C.c_double, C.c_double, C.c_double, _P(C.c_int32)],
                              C.c_int),
@@ -417,6 +418,25 @@ def loka_grouped_fp8_linear(args_list, stream=None, ws=None):
     ws, nws = _workspace(int(_lib.loka_grouped_workspace_size(G, arr)), dev, ws)
     _check(_lib.loka_grouped_fp8_linear(G, arr, None if ws is None else C.c_void_p(ws.data_ptr()), nws,
                                         _stream(stream)), "loka_grouped_fp8_linear")
+
+
+def loka_grouped_bf16_linear(problems, stream=None, out_dtype="bf16", keep=None):
+    """The library's BF16 grouped denominator: problems = [(a [M,K] bf16, b [N,K] bf16[, y])] device
+    tensors; one kind::f16 CTA-pair launch per 32 problems.  Returns the outputs."""
+    one = torch.ones(1, dtype=torch.float32, device=problems[0][0].device)
+    keep = [] if keep is None else keep
+    args, ys = [], []
+    for pr in problems:
+        a, b = pr[0], pr[1]
+        ar, y, _ = make_linear_args(a, one, b, one, a_gran="tensor", b_gran="tensor", out_dtype=out_dtype,
+                                    y=pr[2] if len(pr) > 2 else None, keep=keep)
+        ar.a.dtype = BF16
+        ar.b.dtype = BF16
+        args.append(ar)
+        ys.append(y)
+    arr = (loka_linear_args * len(args))(*args)
+    _check(_lib.loka_grouped_bf16_linear(len(args), arr, _stream(stream)), "loka_grouped_bf16_linear")
+    return ys
 
 
 def loka_probe_error(pairs, floor_rel: float = 1e-6, stream=None, stats=None, ws=None, global_sum_count=None):

@@ -1352,6 +1352,75 @@ loka_status loka_fp8_mlp_stack(const loka_stack_args* a, loka_stream_t stream) {
 
 // MX problems need their scale packs (each 256-byte aligned, back to back); everything else none.
 // (a lone plain problem may also split K: its FP32 partials follow the MX packs)
+// The library's BF16 grouped denominator (loka.h): the CTA-pair engine's kind::f16 instance.
+loka_status loka_grouped_bf16_linear(int32_t G, const loka_linear_args* a, loka_stream_t stream) {
+  if (G < 0 || (G > 0 && !a)) return LOKA_ERR_INVALID_ARG;
+  for (int g = 0; g < G; ++g) {  // full validation before any launch
+    const loka_linear_args& q = a[g];
+    const int64_t M = q.M, N = q.N, K = q.K;
+    if (M <= 0 || N <= 0 || K <= 0 || M > (1ll << 31) - 1 || N > (1ll << 31) - 1 || K > (1ll << 30))
+      return LOKA_ERR_SHAPE;
+    if (q.a.dtype != LOKA_BF16 || q.b.dtype != LOKA_BF16) return LOKA_ERR_INVALID_ARG;
+    if (q.a.rows != M || q.a.cols != K || q.b.rows != N || q.b.cols != K || q.y.rows != M || q.y.cols != N)
+      return LOKA_ERR_SHAPE;
+    if (!q.a.data || !q.b.data || !q.y.data || !aligned16(q.a.data) || !aligned16(q.b.data) || !aligned16(q.y.data))
+      return LOKA_ERR_INVALID_ARG;
+    if (q.a.ld < K || q.b.ld < K || (q.a.ld * 2) % 16 || (q.b.ld * 2) % 16) return LOKA_ERR_INVALID_ARG;
+    if ((q.y.dtype != LOKA_BF16 && q.y.dtype != LOKA_F32) || q.y.ld < N || (q.y.ld * elem_size(q.y.dtype)) % 16)
+      return LOKA_ERR_INVALID_ARG;
+    if (q.bias && q.bias_dtype != LOKA_F32 && q.bias_dtype != LOKA_BF16) return LOKA_ERR_INVALID_ARG;
+    if (q.norm != LOKA_NORM_NONE || q.act != LOKA_ACT_NONE || q.bwd_xhat || q.save_xhat || q.save_rstd ||
+        q.amax_out || q.debug_precast)
+      return LOKA_ERR_UNSUPPORTED;
+  }
+  if (G == 0) return LOKA_OK;
+  int sms = 148;
+  loka_status st = check_device(&sms);
+  if (st != LOKA_OK) return st;
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return LOKA_ERR_CUDA;
+  auto map_k64 = [&](CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld) {
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+    cuuint32_t box[2] = {64u, 128u};  // one 128-byte (64-element) K row per stage row, SW128
+    cuuint32_t es[2] = {1u, 1u};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  std::vector<int> order(G);
+  for (int g = 0; g < G; ++g) order[g] = g;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return a[x].K > a[y].K; });
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const float* one = pair_norm_unit_scale();
+  for (int i0 = 0; i0 < G; i0 += kMaxGroups) {
+    GroupedParams gp;
+    std::memset(&gp, 0, sizeof(gp));
+    const int n = std::min(kMaxGroups, G - i0);
+    gp.G = n;
+    for (int k = 0; k < n; ++k) {
+      const loka_linear_args& q = a[order[i0 + k]];
+      if (!map_k64(&gp.ta[k], q.a.data, q.M, q.K, q.a.ld) || !map_k64(&gp.tb[k], q.b.data, q.N, q.K, q.b.ld))
+        return LOKA_ERR_CUDA;
+      if (!make_map_out(&gp.ty[k], q.y.data, q.M, q.N, q.y.ld, q.y.dtype, 128, 32u)) return LOKA_ERR_CUDA;
+      GroupDesc& d = gp.g[k];
+      d.M = (int32_t)q.M;
+      d.N = (int32_t)q.N;
+      d.K = (int32_t)q.K;
+      d.tiles_n = (int32_t)cdiv(q.N, 256);
+      d.sa = one;
+      d.sb = one;
+      d.bias = q.bias;
+      d.bias_bf16 = q.bias_dtype == LOKA_BF16;
+      d.out_dtype = q.y.dtype;
+      d.ksplit = 1;
+      gp.tile_start[k + 1] = gp.tile_start[k] + (int32_t)(cdiv(q.M, 256) * d.tiles_n);
+    }
+    if (launch_grouped2_bf16(gp, sms, s) != cudaSuccess) return LOKA_ERR_CUDA;
+  }
+  return LOKA_OK;
+}
+
 size_t loka_grouped_workspace_size(int32_t G, const loka_linear_args* a) {
   size_t n = 0;
   for (int g = 0; g < G && a; ++g) n += (mx_ws_bytes(&a[g]) + 255) & ~size_t(255);

@@ -28,7 +28,7 @@ def declared_symbols():
 
 def test_every_declared_symbol_is_exported(lk):
     syms = declared_symbols()
-    assert len(syms) == 41, syms
+    assert len(syms) == 42, syms
     out = subprocess.run(["nm", "-D", "--defined-only", lk.LIB_PATH], capture_output=True, text=True).stdout
     exported = set(re.findall(r" T (loka_\w+)", out))
     assert set(syms) <= exported, set(syms) - exported

@@ -147,3 +147,49 @@ def test_split_k_lone_gemm(M, N, K, od, bias):
     else:
         rms = np.sqrt(np.mean(yo ** 2, axis=1, keepdims=True))
         assert np.max(np.abs(f64(y[rows]) - yo) / np.maximum(np.abs(yo), rms)) <= TOL
+
+
+def test_grouped_bf16_denominator():
+    """The library's own BF16 grouped path (loka_grouped_bf16_linear: the kind::f16 instance of the
+    CTA-pair engine, SURVEY.md §8(d)'s secondary denominator for the ensemble): 40 problems (two
+    launches of <= 32), ragged M / N / K, bias, bf16 and f32 out — y = X W^T (+ b) on the bf16 values
+    against the oracle's FP64 product at 2e-3 (bf16 out) / 1e-5 (f32 out)."""
+    rng = np.random.default_rng(5)
+    probs, keep, ref = [], [], []
+    for t in range(40):
+        M, N, K = int(rng.integers(1, 700)), int(rng.integers(1, 75)) * 8, int(rng.integers(1, 80)) * 16
+        x, w = synth.heavy(M, K, 200 + t), synth.weight(N, K, 300 + t)
+        od = "f32" if t % 3 == 0 else "bf16"
+        bias = torch.randn(N, generator=torch.Generator().manual_seed(t)) if t % 4 == 1 else None
+        xd, wd = to_dev_padded(x), to_dev_padded(w)
+        one = torch.ones(1, dtype=torch.float32, device=DEV)
+        a, y, _ = lk.make_linear_args(xd, one, wd, one, a_gran="tensor", b_gran="tensor", out_dtype=od,
+                                      bias=None if bias is None else bias.to(DEV), keep=keep)
+        a.a.dtype = lk.BF16
+        a.b.dtype = lk.BF16
+        probs.append(a)
+        yo = oracle.linear.fwd(x.double().numpy(), w.double().numpy())
+        if bias is not None:
+            yo = oracle.linear.add_bias(yo, bias.double().numpy())
+        ref.append((y, yo, od))
+    arr = (lk.loka_linear_args * len(probs))(*probs)
+    assert lk._lib.loka_grouped_bf16_linear(len(probs), arr, None) == 0
+    torch.cuda.synchronize()
+    for y, yo, od in ref:
+        if od == "bf16":
+            _check_bf16(y, yo)
+        else:
+            yg = f64(y)
+            rms = np.sqrt(np.mean(yo ** 2, axis=1, keepdims=True))
+            assert (np.abs(yg - yo) <= 1e-5 * np.maximum(np.abs(yo), rms)).all(), float(np.abs(yg - yo).max())
+
+
+def test_grouped_bf16_rejects_epilogues():
+    x = to_dev_padded(synth.heavy(64, 64, 1))
+    one = torch.ones(1, dtype=torch.float32, device=DEV)
+    keep = []
+    a, _, _ = lk.make_linear_args(x, one, x, one, a_gran="tensor", b_gran="tensor", norm="layer", out_dtype="f32",
+                                  keep=keep)
+    a.a.dtype = lk.BF16
+    a.b.dtype = lk.BF16
+    assert lk._lib.loka_grouped_bf16_linear(1, (lk.loka_linear_args * 1)(a), None) == lk.ERR_UNSUPPORTED

@@ -1,16 +1,4 @@
 # scratch driver for one gpurun call (overwritten per experiment)
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_quantize.py -m gpu -q -x > gpurun_out/r43_t.log 2>&1; echo "EXIT $?" >> gpurun_out/r43_t.log
-timeout 300 python tools/bench_quantize.py --rows 32768 --cols 4096 --out gpurun_out/r43_q32k.json > /dev/null 2> gpurun_out/r43_q.err
-timeout 300 python tools/bench_quantize.py --rows 262144 --cols 4096 --out gpurun_out/r43_q262k.json > /dev/null 2>> gpurun_out/r43_q.err
-LOKA_QUANT_TILE=0 timeout 300 python tools/bench_quantize.py --rows 32768 --cols 4096 --out gpurun_out/r43_q32k_old.json > /dev/null 2>> gpurun_out/r43_q.err
-tail -3 gpurun_out/r43_t.log; tail -3 gpurun_out/r43_q.err
-python - <<'PY'
-import json
-for f in ("r43_q32k", "r43_q32k_old", "r43_q262k"):
-    try:
-        d = json.load(open(f"gpurun_out/{f}.json"))
-        print(f, {k: v["gbs"] for k, v in d["kernels"].items()}, d["clocks"].get("sm_mhz"))
-    except Exception as e:
-        print(f, "ERR", e)
-PY
+timeout 900 python -m pytest tests/test_gpu_grouped.py -m gpu -q -x > gpurun_out/r46_t.log 2>&1; echo "EXIT $?" >> gpurun_out/r46_t.log
+tail -3 gpurun_out/r46_t.log
