@@ -56,9 +56,20 @@ template <> struct QtIn<__nv_bfloat16> {
 
 // cast a row held in smem into the staging row: 4 chunks of 16 B per lane loaded before any is
 // converted (the smem latency of one chunk hides behind the others' conversion)
+// AMAX (bf16): a running max of the 16-bit |x| patterns, two per word (max.u16x2), folded once at the end
+LOKA_DEVINL uint32_t vmax16x2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("max.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+LOKA_DEVINL void amax_acc(uint32_t& pm, uint4 w) {
+  pm = vmax16x2(vmax16x2(pm, w.x & 0x7FFF7FFFu), vmax16x2(w.y & 0x7FFF7FFFu, vmax16x2(w.z & 0x7FFF7FFFu,
+                                                                                   w.w & 0x7FFF7FFFu)));
+}
 template <typename Tin, int FMT, bool AMAX = false>
 LOKA_DEVINL uint32_t qt_cast_row(uint32_t src, uint32_t dsts, int nchunks, int lane, float r) {
-  uint32_t am = 0;  // AMAX: this lane's max |x| bits over the row (the delayed-scaling phase)
+  static_assert(!AMAX || sizeof(Tin) == 2, "packed amax: bf16 rows");
+  uint32_t pm = 0;  // AMAX: this lane's max |x| over the row, 16-bit patterns packed in pairs
   int c = lane;
   for (; c + 96 < nchunks; c += 128) {
     uint4 w[4];
@@ -66,7 +77,7 @@ LOKA_DEVINL uint32_t qt_cast_row(uint32_t src, uint32_t dsts, int nchunks, int l
     for (int u = 0; u < 4; ++u) w[u] = QtIn<Tin>::ld(src + 16u * (c + 32 * u));
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      if (AMAX) am = max(am, QtIn<Tin>::amax(w[u]));
+      if (AMAX) amax_acc(pm, w[u]);
       const uint2 code = QtIn<Tin>::template cast<FMT>(w[u], r);
       asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(dsts + 8u * (c + 32 * u)), "r"(code.x), "r"(code.y)
                    : "memory");
@@ -74,11 +85,11 @@ LOKA_DEVINL uint32_t qt_cast_row(uint32_t src, uint32_t dsts, int nchunks, int l
   }
   for (; c < nchunks; c += 32) {
     const uint4 w = QtIn<Tin>::ld(src + 16u * c);
-    if (AMAX) am = max(am, QtIn<Tin>::amax(w));
+    if (AMAX) amax_acc(pm, w);
     const uint2 code = QtIn<Tin>::template cast<FMT>(w, r);
     asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(dsts + 8u * c), "r"(code.x), "r"(code.y) : "memory");
   }
-  return am;
+  return max(pm & 0xFFFFu, pm >> 16) << 16;  // as FP32 bits
 }
 
 // Work items are groups of 8 consecutive rows of one tensor of the QuantGroup (a single tensor
