@@ -446,6 +446,40 @@ def cpu_baseline(rows=1024):
                              "per sample, so this over-counts it for the full step)"}
 
 
+def extras_oracle_times():
+    """The oracle timed on cfg2 (all 4096 rows, the 8 chained layers with the e4m3 row-scale hand-offs)
+    and on a 256-row sample of cfg3's 64 GEMMs (rows are independent under rowwise scales), on the
+    host's threads — SURVEY.md §8(d) "oracle timing beside it"; a reported baseline, not a target."""
+    import oracle
+    import synth
+    out = {}
+    x = synth.gaussian(M_PER_GPU, DIMS[0], 0).double().numpy()
+    w = [synth.weight(DIMS[l + 1], DIMS[l], 100 + l).double().numpy() for l in range(8)]
+    t0 = time.perf_counter()
+    hq, hs = oracle.quantize.quantize(x, "e4m3", "row")
+    for l in range(8):
+        wq, ws = oracle.quantize.quantize(w[l], "e4m3", "row")
+        y = oracle.linear.linear_norm(hq, hs, "e4m3", "row", wq, ws, "e4m3", "row", norm="layer", eps=1e-5)
+        if l < 7:
+            hq, hs = oracle.quantize.quantize(y, "e4m3", "row")
+    dt = time.perf_counter() - t0
+    out["cfg2"] = {"value": flops_per_step() / dt / 1e12, "unit": "TFLOP/s", "seconds": round(dt, 3),
+                   "cores": cpu_threads(), "kind": "oracle", "sample": "the full cfg2 step (4096 rows, 8 layers)"}
+    S, rows = synth.CFG3_DIMS, 256
+    xs = [(synth.heavy(rows, k, i) if i % 2 else synth.gaussian(rows, k, i)).double().numpy() for i, k in enumerate(S)]
+    t0 = time.perf_counter()
+    for i, k in enumerate(S):
+        xq, xsc = oracle.quantize.quantize(xs[i], "e4m3", "row")
+        for j, n in enumerate(S):
+            wq, wsc = oracle.quantize.quantize(synth.weight(n, k, 1000 + 8 * i + j).double().numpy(), "e4m3", "row")
+            oracle.linear.linear_norm(xq, xsc, "e4m3", "row", wq, wsc, "e4m3", "row")
+    dt = time.perf_counter() - t0
+    fl = sum(2.0 * rows * k * n for k in S for n in S)
+    out["cfg3"] = {"value": fl / dt / 1e12, "unit": "TFLOP/s", "seconds": round(dt, 3), "cores": cpu_threads(),
+                   "kind": "oracle", "sample": f"{rows} of cfg3's 2048 rows, all 64 GEMMs incl. the 64 weight quantizes"}
+    return out
+
+
 def run_reference(args, rank, world):
     """--impl reference: the oracle as it stands, each step a 256-row sample of cfg5 (W quantize
     included), on the host's cores; rank 0 only."""
@@ -876,6 +910,13 @@ def main():
         line.update(extras)
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline()
+            if extras:
+                try:
+                    for k_, v_ in extras_oracle_times().items():
+                        if k_ in line:
+                            line[k_]["cpu_oracle"] = v_
+                except Exception as e:  # noqa: BLE001  (a reported baseline: never fails the bench line)
+                    line["cpu_oracle_error"] = str(e)[:200]
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier(device_ids=[local])
