@@ -919,6 +919,10 @@ static loka_status run_pair_norm(const loka_linear_args* a, const PnPlan& pl, vo
     if (!make_map_out(&p.tx, const_cast<void*>(a->bwd_xhat), a->M, a->N, a->bwd_xhat_ld, LOKA_BF16, 128, 32u))
       return LOKA_ERR_CUDA;
   }
+  if (const char* e = std::getenv("LOKA_PN_MC"); e && e[0] == '1' && pl.tn == 256 && !cx) {  // (opt-in, A/B)
+    p.mc = 1;
+    if (!make_map_u8(&p.ta64, A.data, a->M, a->K * eb, A.ld * eb, 64)) return LOKA_ERR_CUDA;
+  }
   p.trace = g_pn_trace;
   if (pl.xchg) {
     // the records start as 0xFF bytes (the sentinel NaN the readers wait on), every launch

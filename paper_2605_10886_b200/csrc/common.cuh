@@ -421,6 +421,16 @@ LOKA_DEVINL void tma_load_2d_cg2(void* dst, const CUtensorMap* m, uint32_t bar_c
       "l"((uint64_t)m), "r"(bar_cluster), "r"(c0), "r"(c1)
       : "memory");
 }
+// the same, multicast to the CTAs of cta_mask (cluster ranks): each destination's transaction bytes
+// complete on the barrier at bar_cluster's offset in that destination's pair leader
+LOKA_DEVINL void tma_load_2d_cg2_mc(void* dst, const CUtensorMap* m, uint32_t bar_cluster, int32_t c0, int32_t c1,
+                                   uint16_t cta_mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)m), "r"(bar_cluster), "r"(c0), "r"(c1), "h"(cta_mask)
+      : "memory");
+}
 LOKA_DEVINL void mbar_arrive_expect_tx_cluster(uint32_t bar_cluster, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(bar_cluster),
                "r"(bytes)

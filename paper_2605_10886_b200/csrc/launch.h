@@ -373,6 +373,11 @@ struct PairNormParams {
   uint32_t* xcnt;
   float* xs_out;
   int32_t cast_ahead;  // castx pacing (tiles ahead of the epilogue; LOKA_CAST_AHEAD, default 3)
+  // mc: 4-CTA clusters of two pairs that own adjacent column tiles of the same row block; each CTA
+  // loads half of its A rows (box {128, 64}: ta64) multicast to itself and its counterpart in the
+  // other pair (TN = 256, order 0, tiles_n and the pair count even)
+  int32_t mc;
+  CUtensorMap ta64;
 };
 const float* pair_norm_unit_scale();  // device address of 1.0f (the BF16 path's s_a = s_b)
 // tn = 512 (one accumulator, two N = 256 MMAs per K step) or 256 (double-buffered accumulators)

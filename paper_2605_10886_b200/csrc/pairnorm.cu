@@ -26,6 +26,8 @@
 // Exchange through global memory (L2), not DSMEM: a 4096-wide row spans 16 (TN = 256) or 8 WIDE
 // pairs, and clusters of 16+ CTAs would leave ~14% of the SMs idle.  Co-residency: one CTA per SM,
 // at most 2 x 74 CTAs, every CTA resident (a reader only waits for tiles other resident pairs own).
+#include <algorithm>
+
 #include "common.cuh"
 #include "launch.h"
 
@@ -156,7 +158,11 @@ __global__ void __launch_bounds__(kPnThreads + (CASTX ? 32 * kPnCastWarps : 0), 
   volatile int* ep_tile = reinterpret_cast<volatile int*>(tmem_slot + 1);  // CASTX pacing: the epilogue's tile
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rank = (int)cluster_ctarank();
+  // cluster rank: bit 0 = the CTA within its pair (the cta_group::2 peer), bit 1 = the pair within a
+  // 4-CTA cluster (mc); `rank` below is the CTA's rank within its pair
+  const int crank = (int)cluster_ctarank();
+  const int rank = crank & 1, lead = crank & ~1, cq = crank >> 1;
+  const bool mc = p.mc != 0;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int G = p.tiles_n;
   // schedule: order 0 = round-robin over the tile list (row-block major: the G tiles of a row are
@@ -184,7 +190,7 @@ __global__ void __launch_bounds__(kPnThreads + (CASTX ? 32 * kPnCastWarps : 0), 
     tma_prefetch_desc(&p.ty);
     for (int s = 0; s < Cf::kStages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], mc ? 2 : 1);  // mc: both pairs' MMAs read this CTA's A stage
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
@@ -206,7 +212,7 @@ __global__ void __launch_bounds__(kPnThreads + (CASTX ? 32 * kPnCastWarps : 0), 
   if (warp == 0) {
     // ===== TMA producer (both CTAs): this CTA's 128 A rows and half of each 256-row B half =====
     if (lane == 0) {
-      const uint32_t full0 = mapa_shared(smem_u32(full_bar), 0);
+      const uint32_t full0 = mapa_shared(smem_u32(full_bar), (uint32_t)lead);
       int it = 0, mb, nb;
       for (int k = 0; tile_of(k, mb, nb); ++k) {
         if constexpr (CASTX) {  // this row block's codes: all 4 G cast parts published
@@ -218,7 +224,11 @@ __global__ void __launch_bounds__(kPnThreads + (CASTX ? 32 * kPnCastWarps : 0), 
           const uint32_t ph = (uint32_t)(it / Cf::kStages) & 1u;
           mbar_wait(&empty_bar[s], ph ^ 1u, 1);
           if (rank == 0) mbar_arrive_expect_tx(&full_bar[s], 2u * (Cf::kStageA + Cf::kStageB));
-          tma_load_2d_cg2(sA + s * Cf::kStageA, &p.ta, full0 + 8u * s, kb * 128, mb * 256 + rank * 128);
+          if (mc)  // half of the 128 A rows, to this CTA and its counterpart in the other pair
+            tma_load_2d_cg2_mc(sA + s * Cf::kStageA + cq * 8192, &p.ta64, full0 + 8u * s, kb * 128,
+                               mb * 256 + rank * 128 + cq * 64, (uint16_t)((1u << rank) | (1u << (2 + rank))));
+          else
+            tma_load_2d_cg2(sA + s * Cf::kStageA, &p.ta, full0 + 8u * s, kb * 128, mb * 256 + rank * 128);
 #pragma unroll
           for (int hh = 0; hh < TN / 256; ++hh)
             tma_load_2d_cg2(sB + s * Cf::kStageB + hh * 16384, &p.tb, full0 + 8u * s, kb * 128,
@@ -257,9 +267,9 @@ __global__ void __launch_bounds__(kPnThreads + (CASTX ? 32 * kPnCastWarps : 0), 
               if constexpr (BF16IN) mma_bf16_cg2(dacc + hh * 256, da, db, idesc, (kb | k) ? 1u : 0u);
               else mma_f8f6f4_cg2(dacc + hh * 256, da, db, idesc, (kb | k) ? 1u : 0u);
             }
-          mma_commit_cg2_mc(&empty_bar[s], 3);
+          mma_commit_cg2_mc(&empty_bar[s], mc ? (uint16_t)0xF : (uint16_t)(3u << lead));
         }
-        mma_commit_cg2_mc(&acc_full[buf], 3);
+        mma_commit_cg2_mc(&acc_full[buf], (uint16_t)(3u << lead));
         if (tr) tr[6] = globaltimer_ns();
       }
     }
@@ -322,7 +332,7 @@ __global__ void __launch_bounds__(kPnThreads + (CASTX ? 32 * kPnCastWarps : 0), 
     const int r = q * 32 + lane;     // row within this CTA's 128
     const int et = threadIdx.x - 64;  // 0..255
     uint8_t* stg = smem + Cf::kOffOut + (warp - 2) * 8192;
-    const uint32_t acc_empty0 = mapa_shared(smem_u32(acc_empty), 0);
+    const uint32_t acc_empty0 = mapa_shared(smem_u32(acc_empty), (uint32_t)lead);
     const int esz = p.out_dtype == LOKA_F32 ? 4 : p.out_dtype == LOKA_BF16 ? 2 : 1;
     const bool fp8_out = esz == 1;
     const int cpb = 128 / esz;  // columns per 128-byte box row
@@ -823,11 +833,38 @@ __global__ void __launch_bounds__(kPnThreads + (CASTX ? 32 * kPnCastWarps : 0), 
 }
 
 template <int TN, int NORM, bool BF16IN, bool BWD = false, bool CASTX = false>
-static cudaError_t launch_pn(const PairNormParams& p, int pairs, cudaStream_t st) {
+static cudaError_t launch_pn(const PairNormParams& p_in, int pairs, cudaStream_t st) {
+  auto kern = pair_norm_kernel<TN, NORM, BF16IN, BWD, CASTX>;
   {
-    cudaError_t e =
-        ensure_func_attrs(reinterpret_cast<const void*>(pair_norm_kernel<TN, NORM, BF16IN, BWD, CASTX>), PnCfg<TN>::kSmem);
+    cudaError_t e = ensure_func_attrs(reinterpret_cast<const void*>(kern), PnCfg<TN>::kSmem);
     if (e != cudaSuccess) return e;
+  }
+  PairNormParams p = p_in;
+  if (p.mc) {  // 4-CTA clusters: only as many as are co-resident (the record exchange needs every pair resident)
+    if (TN != 256 || p.order != 0 || CASTX || (p.tiles_n & 1)) {
+      p.mc = 0;
+    } else {
+      static int max_clusters = -1;  // per instance (one device type per process)
+      if (max_clusters < 0) {
+        cudaLaunchConfig_t q = {};
+        q.gridDim = dim3(4 * 64, 1, 1);
+        q.blockDim = dim3(kPnThreads + (CASTX ? 32 * kPnCastWarps : 0), 1, 1);
+        q.dynamicSmemBytes = PnCfg<TN>::kSmem;
+        cudaLaunchAttribute qa[1];
+        qa[0].id = cudaLaunchAttributeClusterDimension;
+        qa[0].val.clusterDim.x = 4;
+        qa[0].val.clusterDim.y = 1;
+        qa[0].val.clusterDim.z = 1;
+        q.attrs = qa;
+        q.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, kern, &q) != cudaSuccess) n = 0;
+        max_clusters = n;
+      }
+      const int np = std::min(pairs, 2 * max_clusters) & ~1;
+      if (np < 2) p.mc = 0;
+      else pairs = np;
+    }
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(2 * pairs), 1, 1);
@@ -836,14 +873,14 @@ static cudaError_t launch_pn(const PairNormParams& p, int pairs, cudaStream_t st
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = p.mc ? 4 : 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, pair_norm_kernel<TN, NORM, BF16IN, BWD, CASTX>, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
   note_launch();
   return e;
 }

@@ -33,7 +33,7 @@ wq, ws = lk.loka_quantize(w, "e4m3", "tensor")
 del x
 y = torch.empty(a.M, a.N, dtype=torch.bfloat16 if a.out == "bf16" else torch.float32, device="cuda")
 wsb = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
-KEYS = {"PN": "LOKA_PAIRNORM", "DBG": "LOKA_PN_DEBUG", "WIDE": "LOKA_PAIR_WIDE", "ORDER": "LOKA_PN_ORDER"}
+KEYS = {"PN": "LOKA_PAIRNORM", "DBG": "LOKA_PN_DEBUG", "WIDE": "LOKA_PAIR_WIDE", "ORDER": "LOKA_PN_ORDER", "MC": "LOKA_PN_MC"}
 
 
 def setenv(v):
