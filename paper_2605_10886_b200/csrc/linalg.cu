@@ -149,6 +149,9 @@ constexpr int kNB = 64;
 // then every thread updates its entries a[i][k] -= a[i][j] a[k][j] / d_j (= L[i][j] L[k][j]) for
 // i, k > j.  The column scaling by 1/sqrt(d_k) is deferred to the end, so one barrier per step.
 // A pivot d_j that is not positive and finite sets bit 0 of *status (the factor is then garbage).
+// (One warp instead — the block in registers with every step unrolled, or in shared memory with
+// runtime loops — measured 117 / 98 us per panel against this kernel's 22: instruction fetch of
+// ~12K straight-line instructions, resp. a 2K-long dependent load-FMA-store chain per lane.)
 __global__ void __launch_bounds__(256) potf2_kernel(float* a, int64_t lda, int jb, int32_t* status) {
   __shared__ float col[2][kNB];
   __shared__ float dvec[kNB];
@@ -191,6 +194,47 @@ __global__ void __launch_bounds__(256) potf2_kernel(float* a, int64_t lda, int j
   }
 }
 
+// Trailing update of one Cholesky panel, C -= L21 L21^T (K = jb <= 64), on the lower 64 x 64 tiles:
+// the whole K extent of both operand tiles is loaded once (no K loop, one barrier), 4 x 4 outputs
+// per thread.  The 128 x 128 / K-steps-of-8 SIMT GEMM spent ~27 us per panel here (36 CTAs, eight
+// dependent load rounds); these tiles give ~4x the CTAs and one load round.  Tiles on the diagonal
+// also update their upper part, which zero_upper clears at the end (nothing reads it before).
+__global__ void __launch_bounds__(256) syrk_k64_kernel(float* c, int64_t ldc, const float* l21, int64_t ldl,
+                                                       int64_t n, int jb) {
+  const int64_t m0 = (int64_t)blockIdx.y * 64, n0 = (int64_t)blockIdx.x * 64;
+  if (n0 > m0) return;
+  __shared__ __align__(16) float As[kNB][64 + 4];
+  __shared__ __align__(16) float Bs[kNB][64 + 4];
+  const int t = threadIdx.x;
+  for (int idx = t; idx < 64 * kNB; idx += 256) {  // row r, column k of L21 (coalesced along k)
+    const int r = idx / kNB, k = idx - r * kNB;
+    const bool kin = k < jb;
+    As[k][r] = (kin && m0 + r < n) ? l21[(m0 + r) * ldl + k] : 0.f;
+    Bs[k][r] = (kin && n0 + r < n) ? l21[(n0 + r) * ldl + k] : 0.f;
+  }
+  __syncthreads();
+  const int tx = t & 15, ty = t >> 4;
+  float acc[4][4] = {};
+  for (int k = 0; k < jb; ++k) {
+    const float4 a = *reinterpret_cast<const float4*>(&As[k][ty * 4]);
+    const float4 b = *reinterpret_cast<const float4*>(&Bs[k][tx * 4]);
+    const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = m0 + ty * 4 + i;
+    if (r >= n) continue;
+    float* cr = c + r * ldc + n0 + tx * 4;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (n0 + tx * 4 + j < n) cr[j] -= acc[i][j];
+  }
+}
+
 // Solve X L^T = B in place for a panel of jb <= 64 columns: X(r, c) = b[r sr + c sc], r < R.
 // A CTA stages 128 rows x jb columns through shared memory with coalesced loads/stores (along c
 // when sc == 1, along r otherwise), then one thread per row solves right-looking inside the thread
@@ -199,28 +243,34 @@ __global__ void __launch_bounds__(256) potf2_kernel(float* a, int64_t lda, int j
 // Cholesky panel (rows of A21: sr = lda, sc = 1) and for L X = B (the transposed view of B's panel
 // rows: sr = 1, sc = ldb).
 __global__ void __launch_bounds__(128) panel_trsm_kernel(float* b, int64_t sr, int64_t sc, int64_t R,
-                                                         const float* l, int64_t ldl, int jb) {
-  extern __shared__ float trsm_smem[];  // L [64][65], rinv [64], tile [128][65]
-  float (*L)[kNB + 1] = reinterpret_cast<float (*)[kNB + 1]>(trsm_smem);
-  float* rinv = trsm_smem + kNB * (kNB + 1);
-  float (*tile)[kNB + 1] = reinterpret_cast<float (*)[kNB + 1]>(trsm_smem + kNB * (kNB + 1) + kNB);
-  for (int idx = threadIdx.x; idx < jb * jb; idx += 128) {
-    const int i = idx / jb, j = idx - i * jb;
-    L[i][j] = j <= i ? l[(int64_t)i * ldl + j] : 0.f;
+                                                         const float* l, int64_t ldl, int jb, int nr) {
+  // smem: Lt [64][68] (L transposed: the 16 factors a chunk update needs are one float4 run),
+  // rinv [64], tile [nr][65]; 128 threads stage L and the tile, then threads < nr solve a row each
+  // (nr = 32 for the Cholesky panel, so the ~1000-row panels spread over ~30 SMs; 128 for the wide
+  // L X = B solves)
+  extern __shared__ float trsm_smem[];
+  float (*Lt)[kNB + 4] = reinterpret_cast<float (*)[kNB + 4]>(trsm_smem);
+  float* rinv = trsm_smem + kNB * (kNB + 4);
+  float (*tile)[kNB + 1] = reinterpret_cast<float (*)[kNB + 1]>(trsm_smem + kNB * (kNB + 4) + kNB);
+  const int nt = blockDim.x;
+  for (int idx = threadIdx.x; idx < kNB * kNB; idx += nt) {
+    const int i = idx / kNB, j = idx - i * kNB;
+    Lt[j][i] = (i < jb && j <= i) ? l[(int64_t)i * ldl + j] : 0.f;
   }
-  const int64_t r0 = (int64_t)blockIdx.x * 128;
-  if (sc == 1) {  // 64 threads along a row
-    const int c = threadIdx.x & 63;
-    for (int rr = threadIdx.x >> 6; rr < 128; rr += 2)
+  const int64_t r0 = (int64_t)blockIdx.x * nr;
+  if (sc == 1) {  // along a row: coalesced
+    for (int idx = threadIdx.x; idx < nr * kNB; idx += nt) {
+      const int rr = idx / kNB, c = idx - rr * kNB;
       if (c < jb && r0 + rr < R) tile[rr][c] = b[(r0 + rr) * sr + c];
+    }
   } else {
     for (int c = 0; c < jb; ++c)
-      if (r0 + threadIdx.x < R) tile[threadIdx.x][c] = b[(r0 + threadIdx.x) * sr + c * sc];
+      if (threadIdx.x < nr && r0 + threadIdx.x < R) tile[threadIdx.x][c] = b[(r0 + threadIdx.x) * sr + c * sc];
   }
   __syncthreads();
-  if (threadIdx.x < jb) rinv[threadIdx.x] = 1.f / L[threadIdx.x][threadIdx.x];
+  for (int i = threadIdx.x; i < jb; i += nt) rinv[i] = 1.f / Lt[i][i];
   __syncthreads();
-  if (r0 + threadIdx.x < R) {
+  if (threadIdx.x < nr && r0 + threadIdx.x < R) {
     // 16-column chunks (a fully unrolled 64-column solve is ~4K instructions: i-cache bound):
     // chunk a first takes the updates of the already-solved columns j < 16a (runtime loop), then
     // solves its own 16 columns with the unrolled right-looking step.
@@ -231,16 +281,24 @@ __global__ void __launch_bounds__(128) panel_trsm_kernel(float* b, int64_t sr, i
       for (int c = 0; c < 16; ++c) v[c] = a0 + c < jb ? trow[a0 + c] : 0.f;
       for (int j = 0; j < a0; ++j) {
         const float x = trow[j];
+        const float4* lj = reinterpret_cast<const float4*>(&Lt[j][a0]);  // L[a0 .. a0+15][j]
 #pragma unroll
-        for (int c = 0; c < 16; ++c) v[c] = fmaf(-x, L[a0 + c][j], v[c]);
+        for (int q = 0; q < 4; ++q) {
+          const float4 f = lj[q];
+          v[4 * q] = fmaf(-x, f.x, v[4 * q]);
+          v[4 * q + 1] = fmaf(-x, f.y, v[4 * q + 1]);
+          v[4 * q + 2] = fmaf(-x, f.z, v[4 * q + 2]);
+          v[4 * q + 3] = fmaf(-x, f.w, v[4 * q + 3]);
+        }
       }
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         if (a0 + j < jb) {
           const float x = v[j] * rinv[a0 + j];
           v[j] = x;
+          const float* lcol = &Lt[a0 + j][a0];  // L[a0 + c][a0 + j]
 #pragma unroll
-          for (int c = j + 1; c < 16; ++c) v[c] = fmaf(-x, L[a0 + c][a0 + j], v[c]);
+          for (int c = j + 1; c < 16; ++c) v[c] = fmaf(-x, lcol[c], v[c]);
         }
       }
 #pragma unroll
@@ -250,16 +308,17 @@ __global__ void __launch_bounds__(128) panel_trsm_kernel(float* b, int64_t sr, i
   }
   __syncthreads();
   if (sc == 1) {
-    const int c = threadIdx.x & 63;
-    for (int rr = threadIdx.x >> 6; rr < 128; rr += 2)
+    for (int idx = threadIdx.x; idx < nr * kNB; idx += nt) {
+      const int rr = idx / kNB, c = idx - rr * kNB;
       if (c < jb && r0 + rr < R) b[(r0 + rr) * sr + c] = tile[rr][c];
+    }
   } else {
     for (int c = 0; c < jb; ++c)
-      if (r0 + threadIdx.x < R) b[(r0 + threadIdx.x) * sr + c * sc] = tile[threadIdx.x][c];
+      if (threadIdx.x < nr && r0 + threadIdx.x < R) b[(r0 + threadIdx.x) * sr + c * sc] = tile[threadIdx.x][c];
   }
 }
 
-constexpr int kTrsmSmem = (kNB * (kNB + 1) + kNB + 128 * (kNB + 1)) * 4;
+constexpr int kTrsmSmem = (kNB * (kNB + 4) + kNB + 128 * (kNB + 1)) * 4;
 static cudaError_t trsm_attr() {
   return ensure_func_attrs(reinterpret_cast<const void*>(panel_trsm_kernel), kTrsmSmem);
 }
@@ -288,18 +347,11 @@ cudaError_t launch_cholesky(float* a, int64_t lda, int64_t n, int32_t* status, c
     if (rest > 0) {
       float* l21 = a + (j0 + jb) * lda + j0;
       if (cudaError_t e = trsm_attr()) return e;
-      panel_trsm_kernel<<<(unsigned)((rest + 127) / 128), 128, kTrsmSmem, st>>>(l21, lda, 1, rest, d, lda, jb);
+      panel_trsm_kernel<<<(unsigned)((rest + 31) / 32), 128, kTrsmSmem, st>>>(l21, lda, 1, rest, d, lda, jb, 32);
       note_launch();
-      GemmF32Params g = {};
-      g.M = rest; g.N = rest; g.K = jb;
-      g.A = l21; g.lda = lda;
-      g.B = l21; g.ldb = lda;  // B(k, n) = L21[n][k]
-      g.C = a + (j0 + jb) * lda + (j0 + jb); g.ldc = lda;
-      g.Cin = static_cast<const float*>(g.C); g.ldcin = lda;
-      g.alpha = -1.f; g.beta = 1.f;
-      g.lower_only = 1;
-      cudaError_t e = launch_gemm_f32(g, false, true, st);
-      if (e != cudaSuccess) return e;
+      const unsigned nt = (unsigned)((rest + 63) / 64);
+      syrk_k64_kernel<<<dim3(nt, nt), 256, 0, st>>>(a + (j0 + jb) * lda + (j0 + jb), lda, l21, lda, rest, jb);
+      note_launch();
     }
   }
   zero_upper_kernel<<<grid_for(n * n, 256), 256, 0, st>>>(a, lda, n);
@@ -313,7 +365,7 @@ cudaError_t launch_trsm_left(const float* l, int64_t ldl, int64_t n, float* b, i
     const int jb = (int)(n - j0 < kNB ? n - j0 : kNB);
     if (cudaError_t e = trsm_attr()) return e;
     panel_trsm_kernel<<<(unsigned)((ncols + 127) / 128), 128, kTrsmSmem, st>>>(b + j0 * ldb, 1, ldb, ncols,
-                                                                         l + j0 * ldl + j0, ldl, jb);
+                                                                         l + j0 * ldl + j0, ldl, jb, 128);
     note_launch();
     const int64_t rest = n - j0 - jb;
     if (rest > 0) {
