@@ -244,3 +244,26 @@ def test_fused_tensorwise_cast_x_recipe(M, N, K, norm, given_amax, monkeypatch):
     codes = wsb[:M * ld].view(M, ld)[:, :K]
     oq, _ = oracle.quantize.quantize(x.cpu().double().numpy(), "e4m3", "tensor", amax=np.array([float(amax)]))
     assert np.array_equal(codes.cpu().numpy(), oq)
+
+
+@pytest.mark.parametrize("M,N,K,norm,od", [(4100, 4096, 1000, "layer", "f32"), (2600, 2048, 512, "rms", "f32"),
+                                          (3000, 1024, 384, "layer", "e4m3")])
+def test_operand_multicast_variant(M, N, K, norm, od, monkeypatch):
+    """The opt-in 4-CTA-cluster variant of the pair engine (LOKA_PN_MC=1: two pairs on adjacent column
+    tiles of a row block, each CTA's A half multicast to its counterpart): same
+    results as the oracle, at shapes with many tiles per pair and an even tile count per row."""
+    monkeypatch.setenv("LOKA_PAIRNORM", "256")
+    monkeypatch.setenv("LOKA_PN_MC", "1")
+    xq, xs, wq, ws = _operands(M, N, K, 29)
+    if od == "f32":
+        y, _ = lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm=norm, out_dtype="f32")
+        torch.cuda.synchronize()
+        _check(y, _oracle(xq, xs, wq, ws, norm=norm), "f32")
+    else:
+        pre = torch.full((M, N), float("nan"), dtype=torch.float32, device=DEV)
+        y, ys = lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm=norm, out_dtype=od, precast=pre)
+        torch.cuda.synchronize()
+        oq, os_ = oracle.quantize.quantize(f64(pre), od, "row")
+        assert_scales_equal(ys, os_)
+        assert_bytes_equal(y, oq)
+        assert guarded_rel_err(f64(pre), _oracle(xq, xs, wq, ws, norm=norm)) <= TOL
