@@ -179,7 +179,11 @@ typedef struct loka_linear_args {
   const float* gamma;       /* nullable [N] (LAYER, RMS)                                      */
   const float* beta;        /* nullable [N] (LAYER)                                           */
   loka_tensor y;            /* [M,N]: F32 | BF16 | E4M3/E5M2 with y.scales ROW (next layer's
-                               rowwise input, amax over the full normalised row)             */
+                               rowwise input, amax over the full normalised row) or, with a
+                               LAYER / RMS / BLOCK_RMS norm and no gamma / beta / act,
+                               BLK_1x128 [M, ceil(N/128)] (the blockwise recipe's next input;
+                               the CTA-pair route, PAPER.md:535 + P:464; other routes ->
+                               LOKA_ERR_UNSUPPORTED)                                           */
   float* debug_precast;     /* nullable [M,N] FP32 (ld = N): post-norm values before the
                                output cast, for tests                                        */
   int32_t* status_dev;      /* nullable                                                       */

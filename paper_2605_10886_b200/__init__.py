@@ -259,8 +259,9 @@ def loka_quantize(x: torch.Tensor, fmt: str = "e4m3", gran: str = "row", scale_f
 def make_linear_args(a, a_scales, b, b_scales, *, a_fmt="e4m3", b_fmt="e4m3", a_gran="row", b_gran="row",
                      a_scale_fmt="f32", b_scale_fmt="f32", norm="none", act="none", bwd_xhat=None, bwd_rstd=None,
                      save_xhat=None, save_rstd=None, amax_out=None, norm_block=256, eps=0.0, gamma=None, beta=None, bias=None, out_dtype="f32",
-                     y=None, y_scales=None, precast=None, status=None, direction="fwd", keep=None):
-    """Build a loka_linear_args for C = A . B^T (A [M,K], B [N,K] FP8 codes, K-major)."""
+                     y=None, y_scales=None, precast=None, status=None, direction="fwd", keep=None, y_gran="row"):
+    """Build a loka_linear_args for C = A . B^T (A [M,K], B [N,K] FP8 codes, K-major).
+    y_gran: the FP8 output's scale granularity, "row" [M] or "blk_1x128" [M, ceil(N/128)]."""
     M, K = a.shape
     N = b.shape[0]
     od = {"f32": F32, "bf16": BF16, "e4m3": E4M3, "e5m2": E5M2}[out_dtype]
@@ -268,7 +269,7 @@ def make_linear_args(a, a_scales, b, b_scales, *, a_fmt="e4m3", b_fmt="e4m3", a_
     if y is None:
         y = torch.empty(M, N, dtype=_TORCH_DT[od], device=dev)
     if od in (E4M3, E5M2) and y_scales is None:
-        y_scales = torch.empty(M, dtype=torch.float32, device=dev)
+        y_scales = torch.empty(scale_shape(M, N, y_gran), dtype=torch.float32, device=dev)
     args = loka_linear_args()
     args.M, args.N, args.K, args.dir = M, N, K, DIR[direction]
     args.a = _tensor(a, FMT[a_fmt], M, K, a_scales, a_gran, a_scale_fmt)
@@ -278,7 +279,7 @@ def make_linear_args(a, a_scales, b, b_scales, *, a_fmt="e4m3", b_fmt="e4m3", a_
     args.norm, args.norm_block, args.eps = NORM[norm], norm_block, eps
     args.gamma = None if gamma is None else gamma.data_ptr()
     args.beta = None if beta is None else beta.data_ptr()
-    args.y = _tensor(y, od, M, N, y_scales, "row")
+    args.y = _tensor(y, od, M, N, y_scales, y_gran)
     args.debug_precast = None if precast is None else precast.data_ptr()
     args.status_dev = None if status is None else status.data_ptr()
     args.act = ACT[act]

@@ -399,7 +399,8 @@ static loka_status mx_pack(const loka_linear_args* a, LinearParams* p, void* ws,
 
 // nvf4: the operands are NVFP4 presented as byte tensors [rows, K/2] (loka_nvfp4_linear_norm)
 // Argument checks shared by every linear route (shapes, pointers, alignment, enum ranges).
-static loka_status validate_linear(const loka_linear_args* a, bool nvf4 = false) {
+// blk_out_ok: the caller's route writes FP8 output with 1x128 scales (the pair-norm engine only).
+static loka_status validate_linear(const loka_linear_args* a, bool nvf4 = false, bool blk_out_ok = false) {
   if (!a) return LOKA_ERR_INVALID_ARG;
   const int64_t M = a->M, N = a->N, K = a->K;
   if (M <= 0 || N <= 0 || K <= 0 || M > (1ll << 31) - 1 || N > (1ll << 30) || K > (1ll << 31) - 1)
@@ -416,7 +417,8 @@ static loka_status validate_linear(const loka_linear_args* a, bool nvf4 = false)
   if (Y.dtype < LOKA_F32 || Y.dtype > LOKA_E5M2) return LOKA_ERR_INVALID_ARG;
   if (Y.ld < N || (Y.ld * elem_size(Y.dtype)) % 16) return LOKA_ERR_INVALID_ARG;
   const bool fp8_out = is_fp8(Y.dtype);
-  if (fp8_out && (!Y.scales || Y.gran != LOKA_GRAN_ROW)) return LOKA_ERR_INVALID_ARG;
+  if (fp8_out && (!Y.scales || (Y.gran != LOKA_GRAN_ROW && Y.gran != LOKA_GRAN_BLK_1x128))) return LOKA_ERR_INVALID_ARG;
+  if (fp8_out && Y.gran == LOKA_GRAN_BLK_1x128 && !blk_out_ok) return LOKA_ERR_UNSUPPORTED;
   if (a->bias && a->bias_dtype != LOKA_F32 && a->bias_dtype != LOKA_BF16) return LOKA_ERR_INVALID_ARG;
   if (a->norm < LOKA_NORM_NONE || a->norm > LOKA_NORM_BLOCK_RMS) return LOKA_ERR_INVALID_ARG;
   if (a->beta && a->norm != LOKA_NORM_LAYER) return LOKA_ERR_INVALID_ARG;
@@ -820,14 +822,16 @@ static PnPlan pair_norm_plan(const loka_linear_args* a, int sms) {
   // 256-wide tiles with double-buffered accumulators by default: the epilogue (two TMEM passes and
   // the row-record exchange) runs under the next tile's MMAs; WIDE 512-column tiles (LOKA_PAIRNORM=512)
   // move 25% fewer operand bytes per FLOP but expose the whole epilogue (measured slower)
-  pl.tn = bwd ? 256 : (env == 256 || env == 512) ? env : 256;
+  // FP8 output with 1x128 scales: one 128-column half-tile per epilogue thread is one scale granule
+  const bool y_blk = fp8_out && a->y.gran == LOKA_GRAN_BLK_1x128;
+  pl.tn = (bwd || y_blk) ? 256 : (env == 256 || env == 512) ? env : 256;
   pl.tiles_n = (int)cdiv(a->N, pl.tn);
   pl.row_blocks = (int)cdiv(a->M, 256);
   pl.xchg = pl.tiles_n > 1 && (!blk || fp8_out);
   const int avail = std::min(sms / 2, kPnMaxPairs);
   const int64_t tiles = (int64_t)pl.row_blocks * pl.tiles_n;
   // enough tiles for the pairs, or a row wider than the single-CTA engine's clusters (N > 2048)
-  const bool big = tiles >= avail || (!blk && a->N > 2048) || env == 256 || env == 512;
+  const bool big = tiles >= avail || (!blk && a->N > 2048) || env == 256 || env == 512 || y_blk;
   if (!big) return pl;
   // a single accumulator (TN = 512) cannot wait for a peer's next wave without idling its tensor
   // core, so its pairs walk row blocks in static groups of tiles_n; double-buffered tiles (TN = 256)
@@ -889,6 +893,7 @@ static loka_status run_pair_norm(const loka_linear_args* a, const PnPlan& pl, vo
   p.act = a->act;
   p.out_dtype = Y.dtype;
   p.y_scales = is_fp8(Y.dtype) ? Y.scales : nullptr;
+  p.y_blk = is_fp8(Y.dtype) && Y.gran == LOKA_GRAN_BLK_1x128 ? 1 : 0;
   p.precast = a->debug_precast;
   p.ld_pre = a->N;
   p.amax_out = a->amax_out;
@@ -1030,7 +1035,7 @@ loka_status loka_fp8_linear_norm(const loka_linear_args* a, void* ws, size_t ws_
       cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
       if (cudaMemsetAsync(counters, 0, (size_t)cdiv(a->M, 256) * 4, s) != cudaSuccess) return LOKA_ERR_CUDA;
       CastX cx{static_cast<const __nv_bfloat16*>(a->a.data), a->a.ld, base, xq_ld(a), amax, counters, q.a.scales};
-      loka_status vs = validate_linear(&q);
+      loka_status vs = validate_linear(&q, false, true);
       if (vs != LOKA_OK) return vs;
       return run_pair_norm(&q, pl, base + pre, ws_bytes - pre, s, &cx);
     }
@@ -1046,7 +1051,7 @@ loka_status loka_fp8_linear_norm(const loka_linear_args* a, void* ws, size_t ws_
   {
     const PnPlan pl = pair_norm_plan_dev(a);
     if (pl.ok) {
-      loka_status vs = validate_linear(a);
+      loka_status vs = validate_linear(a, false, true);
       if (vs != LOKA_OK) return vs;
       return run_pair_norm(a, pl, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
     }

@@ -345,6 +345,7 @@ struct PairNormParams {
   int32_t act;        // loka_act (bf16 / f32 output)
   int32_t out_dtype;  // f32, bf16, e4m3, e5m2 (+ ROW scales y_scales)
   float* y_scales;
+  int32_t y_blk;      // FP8 output scales: 0 = ROW [M]; 1 = BLK_1x128 [M, ceil(N/128)] (TN = 256)
   float* precast; int64_t ld_pre;
   float* amax_out;
   int32_t* status;

@@ -710,11 +710,20 @@ __global__ void __launch_bounds__(kPnThreads + (CASTX ? 32 * kPnCastWarps : 0), 
       if (tr) tr[2] = globaltimer_ns();
       float r_out = 1.f;
       if (fp8_out) {
+        // 1x128 scales (TN = 256): this thread's 128 columns are one granule; its amax comes from the
+        // thread's own y max / min of pass S through the same monotone map as the row amax
+        if (TN == 256 && !bwd && p.y_blk)
+          amax = col0 < p.N ? fmaxf(fabsf(fmaf(ymax, __fmul_rn(sc, rstd), c0)), fabsf(fmaf(ymin, __fmul_rn(sc, rstd), c0)))
+                            : 0.f;
         if (__float_as_uint(amax) >= 0x7F800000u && p.status) atomicOr(p.status, LOKA_DEVSTATUS_NONFINITE);
         float s_out;
         if (p.out_dtype == LOKA_E4M3) scales_from_amax<LOKA_E4M3, LOKA_SCALE_F32>(amax, s_out, r_out);
         else scales_from_amax<LOKA_E5M2, LOKA_SCALE_F32>(amax, s_out, r_out);
-        if (row_ok && nb == 0 && h == 0 && p.y_scales) p.y_scales[grow] = s_out;
+        if (p.y_blk) {
+          if (row_ok && col0 < p.N && p.y_scales) p.y_scales[(int64_t)grow * ((p.N + 127) / 128) + col0 / 128] = s_out;
+        } else if (row_ok && nb == 0 && h == 0 && p.y_scales) {
+          p.y_scales[grow] = s_out;
+        }
       }
 
       // ---- pass N: normalise, activation, cast, store ----

@@ -267,3 +267,33 @@ def test_operand_multicast_variant(M, N, K, norm, od, monkeypatch):
         assert_scales_equal(ys, os_)
         assert_bytes_equal(y, oq)
         assert guarded_rel_err(f64(pre), _oracle(xq, xs, wq, ws, norm=norm)) <= TOL
+
+
+@pytest.mark.parametrize("norm,N", [("layer", 4096), ("rms", 384), ("block_rms", 768), ("layer", 256)])
+@pytest.mark.parametrize("od", ["e4m3", "e5m2"])
+@pytest.mark.parametrize("M", [520, 64])
+def test_fp8_output_1x128_scales(norm, N, od, M):
+    """FP8 output with 1x128 scales ("e4m3 + scales (ROW or BLK_1x128)") — the
+    pair engine's epilogue thread owns one 128-column granule of its row; its amax comes through the
+    same monotone map from the thread's y max / min.  Codes + scales bit-exact vs the oracle's 1x128
+    quantize of the GPU's own pre-cast values, which are within 2e-3 of the oracle."""
+    K = 512
+    xq, xs, wq, ws = _operands(M, N, K, 31)
+    pre = torch.full((M, N), float("nan"), dtype=torch.float32, device=DEV)
+    y, ys = lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm=norm, norm_block=256, out_dtype=od, precast=pre,
+                                    y_gran="blk_1x128")
+    torch.cuda.synchronize()
+    assert tuple(ys.shape) == (M, (N + 127) // 128)
+    oq, os_ = oracle.quantize.quantize(f64(pre), od, "blk_1x128")
+    assert_scales_equal(ys, os_)
+    assert_bytes_equal(y, oq)
+    assert guarded_rel_err(f64(pre), _oracle(xq, xs, wq, ws, norm=norm)) <= TOL
+
+
+def test_fp8_output_1x128_only_on_the_fused_norm_route():
+    """1x128 output scales exist on the pair engine's norm epilogue; a plain (norm NONE) problem asks
+    for them -> LOKA_ERR_UNSUPPORTED, not ROW scales under a 1x128 label."""
+    xq, xs, wq, ws = _operands(256, 256, 256, 3)
+    with pytest.raises(lk.LokaError) as ei:
+        lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm="none", out_dtype="e4m3", y_gran="blk_1x128")
+    assert ei.value.status == lk.ERR_UNSUPPORTED

@@ -1,4 +1,4 @@
 # scratch driver for one gpurun call (overwritten per experiment)
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_pairnorm.py -m gpu -q -x -k multicast > gpurun_out/r59_t.log 2>&1; echo "EXIT $?" >> gpurun_out/r59_t.log
-tail -3 gpurun_out/r59_t.log
+timeout 900 python -m pytest tests/test_gpu_pairnorm.py tests/test_gpu_linear.py tests/test_gpu_grouped.py -m gpu -q -x > gpurun_out/r60_t.log 2>&1; echo "EXIT $?" >> gpurun_out/r60_t.log
+tail -3 gpurun_out/r60_t.log
