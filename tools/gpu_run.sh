@@ -1,4 +1,8 @@
 # scratch driver for one gpurun call (overwritten per experiment)
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_pairnorm.py tests/test_gpu_linear.py tests/test_gpu_grouped.py -m gpu -q -x > gpurun_out/r60_t.log 2>&1; echo "EXIT $?" >> gpurun_out/r60_t.log
-tail -3 gpurun_out/r60_t.log
+P=29611
+for sz in "4096 4096" "8192 8192" "16384 8192" "32768 8192"; do
+  P=$((P+1))
+  timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port $P tools/dist_grad_check.py p2p $sz --bench >> gpurun_out/r62_gradcomm.jsonl 2>> gpurun_out/r62_gradcomm.err
+done
+cat gpurun_out/r62_gradcomm.jsonl | cut -c 1-600
