@@ -57,6 +57,37 @@ def quantize_tensorwise_sharded(x_local: torch.Tensor, fmt: str = "e4m3", scale_
     return q, s, amax
 
 
+def dispatch_plan_sharded(tables, mere_budget: float = 0.2, min_speedup: float = 1.05, group=None,
+                          select_fn=None):
+    """LoKA Dispatch under data parallelism (SURVEY.md §8(e) "the dispatch plan is computed on rank 0 and
+    broadcast so every rank runs the same recipe"; the selection rule is PAPER.md:541/547, one decision
+    per (layer, direction)).  Per-rank timings differ (clocks, neighbours), and ranks that chose
+    different recipes would compute different numerics for the same layer; so rank 0 decides from its
+    own table with loka_dispatch_select (host C) and the plan is broadcast.
+
+    tables: {(layer, direction): (baseline_time_us, [(candidate_id, mere, time_us), ...])} — the MERE
+    values are the rank-merged ones (probe_error_sharded), identical on every rank.
+    Returns {(layer, direction): candidate_id or None (the BF16 baseline)}."""
+    if select_fn is None:
+        def select_fn(cands, direction, base):
+            return _lk().loka_dispatch_select([(c[0], direction, c[1], c[2]) for c in cands], base, mere_budget,
+                                              min_speedup)
+    multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
+    plan = None
+    if not multi or dist.get_rank(group) == 0:
+        plan = {}
+        for key in sorted(tables):
+            base, cands = tables[key]
+            i = select_fn(list(cands), key[1], base)
+            plan[key] = cands[i][0] if i >= 0 else None
+    if multi:
+        obj = [plan]
+        src = dist.get_global_rank(group, 0) if group is not None else 0
+        dist.broadcast_object_list(obj, src=src, group=group)
+        plan = obj[0]
+    return plan
+
+
 def probe_error_sharded(pairs, floor_rel: float = 1e-6, group=None, stream=None, probe_fn=None, merge_fn=None):
     """LoKA Probe (a7) over row-sharded layers ("probe sums and max values can be
     all-reduced"), equal to the single-device statistic of the concatenated tensors:

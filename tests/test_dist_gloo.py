@@ -123,3 +123,40 @@ def test_quantized_grad_reduce_scatter_protocol(world, rows, tmp_path):
     ref, _, _ = oracle.gradcomm.quantized_allreduce(grads, "e5m2")
     got = np.concatenate([np.load(tmp_path / f"g{r}.npy") for r in range(world)])
     assert np.allclose(got, ref, rtol=2.0 ** -23, atol=0)  # each rank holds its rows of the sum (FP32 out)
+
+
+def _dispatch_worker(rank, world, port, out_dir):
+    """Every rank measures its own (rank-dependent) timings; the plan must be rank 0's."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    tables = {}
+    for layer in range(6):
+        for d in ("fwd", "dgrad", "wgrad"):
+            base = 100.0
+            # rank 0 sees FP8 rowwise fastest; the other ranks see the blockwise candidate fastest
+            cands = [("fp8_tw", 0.25, 60.0), ("fp8_rw", 0.05 + 0.01 * layer, 70.0 if rank == 0 else 90.0),
+                     ("fp8_bw", 0.04, 85.0 if rank == 0 else 50.0), ("nvfp4", 0.15, 96.0)]
+            tables[(layer, d)] = (base, cands)
+    plan = ldist.dispatch_plan_sharded(tables)
+    import pickle
+    with open(os.path.join(out_dir, f"plan{rank}.pkl"), "wb") as f:
+        pickle.dump((plan, tables), f)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_dispatch_plan_broadcast_from_rank0(world, tmp_path):
+    """the dispatch plan is rank 0's decision on every rank (a per-rank decision would
+    pick different recipes here), and it equals the oracle's select on rank 0's table."""
+    import pickle
+    mp.spawn(_dispatch_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    res = [pickle.load(open(tmp_path / f"plan{r}.pkl", "rb")) for r in range(world)]
+    plan0, tables0 = res[0]
+    for plan, _ in res[1:]:
+        assert plan == plan0
+    for key, (base, cands) in tables0.items():
+        i = oracle.dispatch.select([(c[0], c[1], c[2]) for c in cands], base, 0.2, 1.05)
+        assert plan0[key] == (cands[i][0] if i >= 0 else None)
+    assert set(plan0.values()) == {"fp8_rw"}
+    local1 = ldist.dispatch_plan_sharded(res[1][1])  # what rank 1 alone would have chosen
+    assert set(local1.values()) == {"fp8_bw"}
