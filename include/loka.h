@@ -90,8 +90,13 @@ typedef enum loka_scale_fmt { LOKA_SCALE_F32 = 0, LOKA_SCALE_UE8M0 = 1 } loka_sc
 
 typedef enum loka_phase {
   LOKA_PHASE_FULL = 0,          /* amax + cast in one call                                   */
-  LOKA_PHASE_AMAX_ONLY = 1,     /* TENSOR only: write the local amax to *amax_dev            */
-  LOKA_PHASE_CAST_WITH_AMAX = 2, /* TENSOR only: cast with the (all-reduced) amax in *amax_dev */
+  LOKA_PHASE_AMAX_ONLY = 1,     /* TENSOR: write the local amax to *amax_dev; COL: the local
+                                   per-column amax to amax_dev[cols] (float, >= 0)            */
+  LOKA_PHASE_CAST_WITH_AMAX = 2, /* TENSOR / COL: cast with the (all-reduced MAX) amax in
+                                   amax_dev[0] / amax_dev[cols].  COL split-phase: the rowwise
+                                   recipe's wgrad operands (per-column scales over M) stay
+                                   bit-identical to one device when M is sharded (SURVEY.md
+                                   §8(e): all-reduce MAX of the K- and N-length vectors)        */
   /* TENSOR only, delayed scaling: cast with amax_dev[0] (a previous step's
    * all-reduced amax; values beyond it saturate, D3) and write max |x| of THIS tensor to amax_dev[1]
    * in the same read of x (the next step's scale source: its all-reduce runs off the critical path). */
@@ -135,7 +140,7 @@ typedef struct loka_tensor {
  * "tensorwise, rowwise, blockwise" recipes; P:425 values are "clamped and quantized"
  * the quantization overhead this kernel has to keep small, D1-D7).
  * Errors: INVALID_ARG (null / misaligned pointers, ld * elem % 16 != 0, bad enums, phase != FULL
- * with a non-TENSOR granularity), SHAPE (rows / cols mismatch), UNSUPPORTED (not sm_100, or a
+ * with a granularity other than TENSOR / COL), SHAPE (rows / cols mismatch), UNSUPPORTED (not sm_100, or a
  * transposed copy of 1x32 granules), WORKSPACE, CUDA; non-finite input -> status_dev bit.
  * x  : bf16 or f32 [rows, cols].
  * q  : e4m3/e5m2 codes [rows, cols] (q->data may be NULL when only qt is wanted) + q->scales in
@@ -147,7 +152,8 @@ typedef struct loka_tensor {
  *      q = x at 1x128 granules, qt = x at 128x1 granules written transposed (in qt's frame those
  *      granules are 1x128): the blockwise training recipe's forward and wgrad operands from one
  *      read of x.
- * phase, amax_dev: see loka_phase; amax_dev is a device float (TENSOR only, else ignored).
+ * phase, amax_dev: see loka_phase; amax_dev is a device float (TENSOR) or float[cols] (COL, split
+ *      phases), else ignored.
  * Bit-exact with oracle/quantize.py (codes as bytes, scales as FP32 bit patterns).            */
 LOKA_API loka_status loka_quantize(const loka_tensor* x, loka_tensor* q, loka_tensor* qt, loka_phase phase,
                           float* amax_dev, int32_t* status_dev, void* ws, size_t ws_bytes,

@@ -194,8 +194,8 @@ loka_status loka_quantize(const loka_tensor* x, loka_tensor* q, loka_tensor* qt,
   if (q->gran < LOKA_GRAN_TENSOR || q->gran > LOKA_GRAN_BLK_1x32) return LOKA_ERR_INVALID_ARG;
   if (qt && q->gran == LOKA_GRAN_BLK_1x32) return LOKA_ERR_UNSUPPORTED;  // MX blocks: row-major codes only
   if (phase < LOKA_PHASE_FULL || phase > LOKA_PHASE_CAST_DELAYED) return LOKA_ERR_INVALID_ARG;
-  if (phase != LOKA_PHASE_FULL && q->gran != LOKA_GRAN_TENSOR) return LOKA_ERR_INVALID_ARG;
-  if (phase == LOKA_PHASE_CAST_DELAYED && qt) return LOKA_ERR_UNSUPPORTED;
+  if (phase != LOKA_PHASE_FULL && q->gran != LOKA_GRAN_TENSOR && q->gran != LOKA_GRAN_COL) return LOKA_ERR_INVALID_ARG;
+  if (phase == LOKA_PHASE_CAST_DELAYED && (qt || q->gran != LOKA_GRAN_TENSOR)) return LOKA_ERR_UNSUPPORTED;
   if (phase != LOKA_PHASE_FULL && !amax_dev) return LOKA_ERR_INVALID_ARG;
   // dual: q = 1x128 granules, qt = x's own 128x1 quantization written transposed (its t-frame
   // granule is again 1x128) — one read of x for the blockwise recipe's two operand layouts
@@ -213,9 +213,10 @@ loka_status loka_quantize(const loka_tensor* x, loka_tensor* q, loka_tensor* qt,
   const bool stream_tile = x->dtype == LOKA_BF16 && phase != LOKA_PHASE_AMAX_ONLY &&
                            phase != LOKA_PHASE_CAST_DELAYED && quant_tile_tma_eligible(tgran) &&
                            (qt != nullptr || (q->gran != LOKA_GRAN_ROW && q->gran != LOKA_GRAN_TENSOR));
-  const bool tiled = (qt != nullptr || q->gran == LOKA_GRAN_COL || q->gran == LOKA_GRAN_BLK_128x1 ||
-                      q->gran == LOKA_GRAN_BLK_1x32 || stream_tile) &&
-                     phase != LOKA_PHASE_AMAX_ONLY;
+  const bool tiled = ((qt != nullptr || q->gran == LOKA_GRAN_COL || q->gran == LOKA_GRAN_BLK_128x1 ||
+                       q->gran == LOKA_GRAN_BLK_1x32 || stream_tile) &&
+                      phase != LOKA_PHASE_AMAX_ONLY) ||
+                     q->gran == LOKA_GRAN_COL;  // (COL AMAX_ONLY: the column pre-pass alone)
   int sms = 148;
   loka_status st = check_device(&sms);
   if (st != LOKA_OK) return st;
@@ -225,7 +226,10 @@ loka_status loka_quantize(const loka_tensor* x, loka_tensor* q, loka_tensor* qt,
     amax = reinterpret_cast<float*>(ws);
   }
   void* pre = nullptr;  // ROW / COL amax pre-pass array of the tiled path
-  if (tiled && (q->gran == LOKA_GRAN_ROW || q->gran == LOKA_GRAN_COL)) {
+  if (q->gran == LOKA_GRAN_COL && phase != LOKA_PHASE_FULL) {
+    if (!amax_dev || (reinterpret_cast<uintptr_t>(amax_dev) & 3)) return LOKA_ERR_INVALID_ARG;
+    pre = amax_dev;  // split phases: the caller's (all-reducible) column amax vector
+  } else if (tiled && (q->gran == LOKA_GRAN_ROW || q->gran == LOKA_GRAN_COL)) {
     if (!ws || ws_bytes < loka_quantize_workspace_size(x, q) || !aligned16(ws)) return LOKA_ERR_WORKSPACE;
     pre = reinterpret_cast<uint8_t*>(ws) + 256;
   }

@@ -423,9 +423,14 @@ static cudaError_t launch_tiled_t(const QuantParams& p, int gran, int phase, flo
     amax = reinterpret_cast<uint32_t*>(ws);
     e = launch_pdl_t(row_amax_kernel<Tin>, dim3((unsigned)((p.rows + 7) / 8)), dim3(256), st, p, amax);
   } else if (gran == LOKA_GRAN_COL) {
+    // ws: the pre-pass array (FULL) or the caller's column amax vector (split phases: AMAX_ONLY writes
+    // it, CAST_WITH_AMAX reads the all-reduced one); |x| bit patterns order like the floats they are
     amax = reinterpret_cast<uint32_t*>(ws);
-    e = cudaMemsetAsync(amax, 0, (size_t)p.cols * 4, st);
-    if (e == cudaSuccess) e = launch_pdl_t(col_amax_kernel<Tin>, tiles, dim3(256), st, p, amax);
+    if (phase != LOKA_PHASE_CAST_WITH_AMAX) {
+      e = cudaMemsetAsync(amax, 0, (size_t)p.cols * 4, st);
+      if (e == cudaSuccess) e = launch_pdl_t(col_amax_kernel<Tin>, tiles, dim3(256), st, p, amax);
+      if (e != cudaSuccess || phase == LOKA_PHASE_AMAX_ONLY) return e;
+    }
   }
   if (e != cudaSuccess) return e;
   const uint32_t* ag = amax;

@@ -57,6 +57,33 @@ def quantize_tensorwise_sharded(x_local: torch.Tensor, fmt: str = "e4m3", scale_
     return q, s, amax
 
 
+def _default_col_amax(x, fmt):
+    lk = _lk()
+    amax = torch.empty(x.shape[1], dtype=torch.float32, device=x.device)
+    lk.loka_quantize(x, fmt, "col", phase="amax", amax=amax, want_q=False)
+    return amax
+
+
+def _default_col_cast(x, fmt, amax, scale_fmt, transpose=False):
+    lk = _lk()
+    return lk.loka_quantize(x, fmt, "col", scale_fmt, phase="cast", amax=amax, transpose=transpose)
+
+
+def quantize_colwise_sharded(x_local: torch.Tensor, fmt: str = "e4m3", scale_fmt: str = "f32", group=None,
+                             transpose: bool = False, amax_fn=None, cast_fn=None):
+    """COL-granule quantization (one scale per column over ALL rows) of a row-sharded tensor — the
+    rowwise recipe's wgrad operands dY^T / X^T: the per-column amax vector
+    (loka_quantize COL AMAX_ONLY, cols floats) is all-reduced with MAX, then each rank casts its rows
+    with the global column scales (CAST_WITH_AMAX), so the codes and scales are bit-identical to the
+    single-device quantization of the concatenated tensor.  Returns the cast's outputs (+ the
+    transposed copy when transpose) and the global amax vector."""
+    amax = (amax_fn or _default_col_amax)(x_local, fmt)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(amax, op=dist.ReduceOp.MAX, group=group)
+    res = (cast_fn or _default_col_cast)(x_local, fmt, amax, scale_fmt, transpose)
+    return (*res, amax)
+
+
 def dispatch_plan_sharded(tables, mere_budget: float = 0.2, min_speedup: float = 1.05, group=None,
                           select_fn=None):
     """LoKA Dispatch under data parallelism (SURVEY.md §8(e) "the dispatch plan is computed on rank 0 and

@@ -160,3 +160,35 @@ def test_dispatch_plan_broadcast_from_rank0(world, tmp_path):
     assert set(plan0.values()) == {"fp8_rw"}
     local1 = ldist.dispatch_plan_sharded(res[1][1])  # what rank 1 alone would have chosen
     assert set(local1.values()) == {"fp8_bw"}
+
+
+def _col_worker(rank, world, port, total, cols, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    r0, r1 = ldist.shard_rows(total, world, rank)
+    x = synth.heavy(total, cols, 7)[r0:r1]
+
+    def amax_fn(xl, fmt):
+        return torch.from_numpy(oracle.quantize.granule_amax(xl.double().numpy(), "col").astype(np.float32).reshape(-1))
+
+    def cast_fn(xl, fmt, amax, scale_fmt, transpose):
+        q, s = oracle.quantize.quantize(xl.double().numpy(), fmt, "col", scale_fmt, amax=amax.double().numpy())
+        return torch.from_numpy(q), torch.from_numpy(s)
+
+    q, s, amax = ldist.quantize_colwise_sharded(x, "e5m2", amax_fn=amax_fn, cast_fn=cast_fn)
+    np.save(os.path.join(out_dir, f"c{rank}.npy"), q.numpy())
+    np.save(os.path.join(out_dir, f"s{rank}.npy"), s.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,total", [(2, 300), (3, 257)])
+def test_sharded_colwise_equals_single_device(world, total, tmp_path):
+    """COL granules under M sharding: the all-reduced column amax vector makes every
+    rank's codes the rows of the single-device COL quantization, and every rank's scales equal it."""
+    cols = 96
+    mp.spawn(_col_worker, args=(world, _free_port(), total, cols, str(tmp_path)), nprocs=world, join=True)
+    oq, os_ = oracle.quantize.quantize(synth.heavy(total, cols, 7).double().numpy(), "e5m2", "col")
+    got = np.concatenate([np.load(tmp_path / f"c{r}.npy") for r in range(world)])
+    assert np.array_equal(got, oq)
+    for r in range(world):
+        assert np.array_equal(np.load(tmp_path / f"s{r}.npy").view(np.uint32), np.asarray(os_, np.float32).view(np.uint32))

@@ -297,3 +297,31 @@ def test_streaming_tile_many_tiles_sampled(gran, gran_t, transpose):
             assert_scales_equal(st[c0:c0 + 128, tr], os_.reshape(-1))
         else:
             assert_scales_equal(st[tc, tr].reshape(1), os_.reshape(-1))
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("transpose", [False, True])
+def test_colwise_split_phase_shards(dtype, transpose):
+    """COL split phases (loka.h: AMAX_ONLY writes the column amax vector, CAST_WITH_AMAX casts with a
+    given one): three row shards, their vectors combined with MAX (what the NCCL all-reduce does),
+    cast shard by shard — bit-identical to the one-device COL quantize (codes, scales, transposed copy)."""
+    R, C = 600, 384
+    x = synth.heavy(R, C, 17).to(dtype)
+    xd = to_dev_padded(x)
+    bounds = [(0, 250), (250, 256), (256, 600)]
+    vecs = []
+    for a, b in bounds:
+        v = torch.empty(C, dtype=torch.float32, device=DEV)
+        lk.loka_quantize(xd[a:b], "e4m3", "col", phase="amax", amax=v, want_q=False)
+        vecs.append(v)
+    torch.cuda.synchronize()
+    g = torch.stack(vecs).amax(0)
+    assert torch.equal(g.cpu(), x.float().abs().amax(0))
+    oq, os_ = oracle.quantize.quantize(x.double().numpy(), "e4m3", "col")
+    for a, b in bounds:
+        res = lk.loka_quantize(xd[a:b], "e4m3", "col", phase="cast", amax=g, transpose=transpose)
+        torch.cuda.synchronize()
+        assert_bytes_equal(res[0], oq[a:b])
+        assert_scales_equal(res[1], os_)
+        if transpose:
+            assert_bytes_equal(res[2], oq[a:b].T.copy())
