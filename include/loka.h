@@ -295,7 +295,7 @@ LOKA_API size_t loka_stack_workspace_size(const loka_stack_args* args);
 /* ---- a6: grouped launch: G independent linear+norm problems ------------------------------- *
  * The paper's "many small GEMMs" of heterogeneous LRM layers (PAPER.md:78-79 DHEN / Wukong wide
  * ensembles; "< 20% of hardware capacity") in one persistent launch: problems with the plain
- * dequant(+bias) epilogue and bf16 / f32 output share one CTA-pair launch (<= 32 problems per launch,
+ * dequant(+bias) epilogue and bf16 / f32 output share one CTA-pair launch (<= 64 problems per launch,
  * longest K first, 256x256 tiles); the others run their own loka_fp8_linear_norm route.  Same
  * arguments, errors and bit-exact results as G separate loka_fp8_linear_norm calls (args is a host
  * array of G structs, read during the call).                                                      */
@@ -306,9 +306,9 @@ LOKA_API size_t loka_grouped_workspace_size(int32_t G, const loka_linear_args* a
 /* The library's own BF16 form of a6 (the secondary BF16 denominator of the
  * ensemble, "many small GEMMs"): G problems with BF16 A [M,K] and B [N,K] (a/b dtype
  * LOKA_BF16, K-major, ld * 2 % 16 == 0, scales ignored), Y = A . B^T (+ bias[n]) in bf16 or f32,
- * in ONE persistent launch of the CTA-pair engine with tcgen05.mma.cta_group::2.kind::f16 (FP32
+ * in persistent launches of the CTA-pair engine (one per 64 problems) with tcgen05.mma.cta_group::2.kind::f16 (FP32
  * accumulation in TMEM), longest K first, 256x256 tiles.  norm / act must be NONE, no FP8 output, no
- * backward fields (else UNSUPPORTED); G <= 64 per call.  No workspace.  args: a host array of G
+ * backward fields (else UNSUPPORTED).  No workspace.  args: a host array of G
  * structs, read during the call.                                                                  */
 LOKA_API loka_status loka_grouped_bf16_linear(int32_t G, const loka_linear_args* args, loka_stream_t stream);
 

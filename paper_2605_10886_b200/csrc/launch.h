@@ -203,7 +203,7 @@ cudaError_t launch_linear_bw(const CUtensorMap& tma_a, const CUtensorMap& tma_b,
                              const BwParams& p, cudaStream_t st);
 
 // ---- grouped persistent launch (grouped.cu) ----
-constexpr int kMaxGroups = 32;  // per launch (kernel-parameter space: 3 tensor maps per group)
+constexpr int kMaxGroups = 64;  // per launch (kernel-parameter space: 3 tensor maps per group, ~30.8 KB of the 32 KB)
 struct GroupDesc {
   int32_t M, N, K, tiles_n;
   int32_t a_fmt, b_fmt;

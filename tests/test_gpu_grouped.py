@@ -1,5 +1,5 @@
 """-m gpu: loka_grouped_fp8_linear (a6) against oracle/linear.py: the cfg3 DHEN-style ensemble
-(64 heterogeneous GEMMs over 8 shared inputs, one persistent launch per <= 32 problems) and a
+(64 heterogeneous GEMMs over 8 shared inputs, one persistent launch per <= 64 problems) and a
 mixed list that also routes norm / FP8-output problems through their own fused launches."""
 import numpy as np
 import pytest
@@ -151,12 +151,12 @@ def test_split_k_lone_gemm(M, N, K, od, bias):
 
 def test_grouped_bf16_denominator():
     """The library's own BF16 grouped path (loka_grouped_bf16_linear: the kind::f16 instance of the
-    CTA-pair engine, SURVEY.md §8(d)'s secondary denominator for the ensemble): 40 problems (two
-    launches of <= 32), ragged M / N / K, bias, bf16 and f32 out — y = X W^T (+ b) on the bf16 values
+    CTA-pair engine, SURVEY.md §8(d)'s secondary denominator for the ensemble): 70 problems (two
+    launches of <= 64), ragged M / N / K, bias, bf16 and f32 out — y = X W^T (+ b) on the bf16 values
     against the oracle's FP64 product at 2e-3 (bf16 out) / 1e-5 (f32 out)."""
     rng = np.random.default_rng(5)
     probs, keep, ref = [], [], []
-    for t in range(40):
+    for t in range(70):
         M, N, K = int(rng.integers(1, 700)), int(rng.integers(1, 75)) * 8, int(rng.integers(1, 80)) * 16
         x, w = synth.heavy(M, K, 200 + t), synth.weight(N, K, 300 + t)
         od = "f32" if t % 3 == 0 else "bf16"
