@@ -13,16 +13,22 @@
 // registers, reduces, casts and stores, then exits — with 2-3 CTAs per SM the loads of the next
 // tile only start when a CTA retires, and it reached 3.1-4.4 TB/s.  Here a persistent CTA per SM:
 //   * one producer lane streams 128 x 128 bf16 tiles (32 KB, rows of 256 B, no swizzle: a
-//     half-warp's 16-byte reads of one row are conflict-free) into a 4-stage ring with 2D TMA loads;
-//   * 8 consumer warps take each tile from shared memory (16 rows per warp, 8 elements per lane
-//     per row), release the stage at once, reduce the granule amax (half-warp shuffles for
-//     row-like granules, a shared-memory column reduction for column-like ones), compute ONE
-//     reciprocal per lane (the granule's lanes share it by shuffle or through shared memory instead
-//     of each dividing), cast, and write the codes into a 128B-swizzled staging tile;
-//   * the transposed copy goes through a second code tile (XOR-swizzled by row/8 so the 4 x 4
-//     byte transposes read it with at most 2-way conflicts) into its own staging tile;
-//   * one thread stores the staging tiles with 2D TMA stores (bulk group; the staging pair is
-//     double-buffered and reused after wait_group.read).
+//     half-warp's 16-byte reads of one row are conflict-free) into a 4-stage ring (3 with a
+//     transposed copy) with 2D TMA loads;
+//   * two consumer groups of 4 warps take alternate tiles and synchronise only among themselves
+//     (named barriers 1 / 2), so one group's barrier waits and reciprocal latencies overlap the
+//     other's loads and casts; full barriers are per (group, stage) — with 3 stages both groups use
+//     every stage, and a shared barrier's parity would let a group take the other group's pending
+//     fill for its own completed phase;
+//   * a warp owns 32 rows of its group's tile, 8 elements per lane per row, in two half-passes of 16
+//     rows: reduce the granule amax (16-bit maxima of two rows / columns per word; half-warp
+//     shuffles for row-like granules, a shared-memory column reduction for column-like ones),
+//     compute ONE reciprocal per lane (the granule's lanes share it by shuffle or through shared
+//     memory instead of each dividing), cast, and write the codes into a 128B-swizzled staging tile;
+//   * the transposed copy goes through a code tile (XOR-swizzled by row/8 so the 4 x 4 byte
+//     transposes read it with at most 2-way conflicts) into its own staging tile;
+//   * one thread per group stores its staging tiles with 2D TMA stores (bulk group, reused after
+//     wait_group.read).
 // Ragged edges cost nothing: TMA zero-fills out-of-range input (|0| never raises an amax) and
 // clips out-of-range output; only the scale writes are bounds-checked.
 #include "common.cuh"
