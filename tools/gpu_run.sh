@@ -1,11 +1,7 @@
 # scratch driver for one gpurun call (overwritten per experiment)
 mkdir -p gpurun_out
-timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r67_gpu_tests.txt 2>&1; echo "EXIT $?" >> gpurun_out/r67_gpu_tests.txt
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/r67_smoke.txt 2>&1
-timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/r67_bench10.json 2> gpurun_out/r67_bench10.err
-timeout 900 python bench.py > gpurun_out/r67_bench.json 2> gpurun_out/r67_bench.err
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r67_launches.csv python bench.py --steps 2 --warmup 3 --no-extras --no-cpu-baseline > gpurun_out/r67_ncu_launch.log 2>&1
-grep -v "^\[W" gpurun_out/r67_gpu_tests.txt | tail -2; tail -1 gpurun_out/r67_smoke.txt
-for f in r67_bench10 r67_bench; do python -c "
-import json; d=json.loads(open('gpurun_out/$f.json').read().strip().splitlines()[-1])
-print('$f', d['value'], d['ms_per_step'], d['compute_only']['value'], d['roofline']['frac'], d['roofline']['peak'], d['clocks'], d['speedup_vs_bf16'], d['cfg2']['value'], d['cfg3']['value'])"; done
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29633 bench.py --gpus 2 --steps 10 --warmup 3 > gpurun_out/r69_bench_n2.json 2> gpurun_out/r69_bench_n2.err
+tail -2 gpurun_out/r69_bench_n2.err
+python -c "
+import json; d=json.loads(open('gpurun_out/r69_bench_n2.json').read().strip().splitlines()[-1])
+print(d['value'], d['n_gpus'], d['e2e']['value'], d['e2e']['serial']['value'], d['clocks'])"
