@@ -155,6 +155,8 @@ constexpr int kNB = 64;
 __global__ void __launch_bounds__(256) potf2_kernel(float* a, int64_t lda, int jb, int32_t* status) {
   __shared__ float col[2][kNB];
   __shared__ float dvec[kNB];
+  pdl_wait();
+  pdl_launch_dependents();
   const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
   float r[16];
 #pragma unroll
@@ -201,6 +203,8 @@ __global__ void __launch_bounds__(256) potf2_kernel(float* a, int64_t lda, int j
 // also update their upper part, which zero_upper clears at the end (nothing reads it before).
 __global__ void __launch_bounds__(256) syrk_k64_kernel(float* c, int64_t ldc, const float* l21, int64_t ldl,
                                                        int64_t n, int jb) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int64_t m0 = (int64_t)blockIdx.y * 64, n0 = (int64_t)blockIdx.x * 64;
   if (n0 > m0) return;
   __shared__ __align__(16) float As[kNB][64 + 4];
@@ -249,6 +253,8 @@ __global__ void __launch_bounds__(128) panel_trsm_kernel(float* b, int64_t sr, i
   // (nr = 32 for the Cholesky panel, so the ~1000-row panels spread over ~30 SMs; 128 for the wide
   // L X = B solves)
   extern __shared__ float trsm_smem[];
+  pdl_wait();
+  pdl_launch_dependents();
   float (*Lt)[kNB + 4] = reinterpret_cast<float (*)[kNB + 4]>(trsm_smem);
   float* rinv = trsm_smem + kNB * (kNB + 4);
   float (*tile)[kNB + 1] = reinterpret_cast<float (*)[kNB + 1]>(trsm_smem + kNB * (kNB + 4) + kNB);
@@ -324,11 +330,32 @@ static cudaError_t trsm_attr() {
 }
 
 __global__ void zero_upper_kernel(float* a, int64_t lda, int64_t n) {
+  pdl_wait();
   const int64_t total = n * n;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / n, c = i - r * n;
     if (c > r) a[r * lda + c] = 0.f;
   }
+}
+
+// the Cholesky's ~3 dependent launches per 64-column panel go out with programmatic dependent launch:
+// each kernel's launch and CTA scheduling overlap the previous one (its griddepcontrol.wait still
+// waits for the previous grid's completion and memory flush before reading its output)
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_la(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                             Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  note_launch();
+  return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
 static unsigned grid_for(int64_t n, int threads) {
@@ -338,25 +365,24 @@ static unsigned grid_for(int64_t n, int threads) {
 }
 
 cudaError_t launch_cholesky(float* a, int64_t lda, int64_t n, int32_t* status, cudaStream_t st) {
+  if (cudaError_t e = trsm_attr()) return e;
   for (int64_t j0 = 0; j0 < n; j0 += kNB) {
     const int jb = (int)(n - j0 < kNB ? n - j0 : kNB);
     float* d = a + j0 * lda + j0;
-    potf2_kernel<<<1, 256, 0, st>>>(d, lda, jb, status);
-    note_launch();
+    if (cudaError_t e = launch_la(potf2_kernel, dim3(1), dim3(256), 0, st, d, lda, jb, status)) return e;
     const int64_t rest = n - j0 - jb;
     if (rest > 0) {
       float* l21 = a + (j0 + jb) * lda + j0;
-      if (cudaError_t e = trsm_attr()) return e;
-      panel_trsm_kernel<<<(unsigned)((rest + 31) / 32), 128, kTrsmSmem, st>>>(l21, lda, 1, rest, d, lda, jb, 32);
-      note_launch();
+      if (cudaError_t e = launch_la(panel_trsm_kernel, dim3((unsigned)((rest + 31) / 32)), dim3(128), (size_t)kTrsmSmem, st,
+                                    l21, (int64_t)lda, (int64_t)1, rest, static_cast<const float*>(d), (int64_t)lda, jb, 32))
+        return e;
       const unsigned nt = (unsigned)((rest + 63) / 64);
-      syrk_k64_kernel<<<dim3(nt, nt), 256, 0, st>>>(a + (j0 + jb) * lda + (j0 + jb), lda, l21, lda, rest, jb);
-      note_launch();
+      if (cudaError_t e = launch_la(syrk_k64_kernel, dim3(nt, nt), dim3(256), 0, st, a + (j0 + jb) * lda + (j0 + jb),
+                                    (int64_t)lda, static_cast<const float*>(l21), (int64_t)lda, rest, jb))
+        return e;
     }
   }
-  zero_upper_kernel<<<grid_for(n * n, 256), 256, 0, st>>>(a, lda, n);
-  note_launch();
-  return cudaGetLastError();
+  return launch_la(zero_upper_kernel, dim3(grid_for(n * n, 256)), dim3(256), 0, st, a, (int64_t)lda, n);
 }
 
 cudaError_t launch_trsm_left(const float* l, int64_t ldl, int64_t n, float* b, int64_t ldb, int64_t ncols,
