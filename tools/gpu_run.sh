@@ -1,9 +1,11 @@
 # scratch driver for one gpurun call (overwritten per experiment)
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_sample.py tests/test_gpu_track.py -m gpu -q -x > gpurun_out/r71_t.log 2>&1; echo "EXIT $?" >> gpurun_out/r71_t.log
-grep -v "^\[W" gpurun_out/r71_t.log | tail -2
-timeout 900 python tools/bench_sample.py --out gpurun_out/r71_sample.json > gpurun_out/r71.log 2>&1
+timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r72_gpu_tests.txt 2>&1; echo "EXIT $?" >> gpurun_out/r72_gpu_tests.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/r72_smoke.txt 2>&1
+timeout 900 python bench.py > gpurun_out/r72_bench.json 2> gpurun_out/r72_bench.err
+timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/r72_ref.json 2> gpurun_out/r72_ref.err
+grep -v "^\[W" gpurun_out/r72_gpu_tests.txt | tail -2; tail -1 gpurun_out/r72_smoke.txt
 python -c "
-import json; d=json.load(open('gpurun_out/r71_sample.json'))
-for r in d['rows']:
-    if 'cholesky' in r['op'] or 'weight' in r['op']: print(r['op'][:20], r.get('n', r.get('M')), r['ms'], r['torch_ms'], r['speedup_vs_torch'])"
+import json; d=json.loads(open('gpurun_out/r72_bench.json').read().strip().splitlines()[-1])
+print(d['value'], d['ms_per_step'], d['compute_only']['value'], d['roofline']['frac'], d['roofline']['peak'], d['clocks'], d['speedup_vs_bf16'], d['cfg2']['value'], d['cfg3']['value'], d['e2e']['value'])
+r=json.loads(open('gpurun_out/r72_ref.json').read().strip().splitlines()[-1]); print('ref', r['value'], r['unit'], r.get('cpu_baseline',{}).get('cores'))"
