@@ -1,11 +1,9 @@
 # scratch driver for one gpurun call (overwritten per experiment)
 mkdir -p gpurun_out
-timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r72_gpu_tests.txt 2>&1; echo "EXIT $?" >> gpurun_out/r72_gpu_tests.txt
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/r72_smoke.txt 2>&1
-timeout 900 python bench.py > gpurun_out/r72_bench.json 2> gpurun_out/r72_bench.err
-timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/r72_ref.json 2> gpurun_out/r72_ref.err
-grep -v "^\[W" gpurun_out/r72_gpu_tests.txt | tail -2; tail -1 gpurun_out/r72_smoke.txt
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29733 bench.py --gpus 4 > gpurun_out/r73_bench_n4.json 2> gpurun_out/r73_bench_n4.err
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29734 bench.py --impl reference --gpus 4 --steps 2 --warmup 3 > gpurun_out/r73_ref_n4.json 2> gpurun_out/r73_ref_n4.err
+tail -2 gpurun_out/r73_bench_n4.err
 python -c "
-import json; d=json.loads(open('gpurun_out/r72_bench.json').read().strip().splitlines()[-1])
-print(d['value'], d['ms_per_step'], d['compute_only']['value'], d['roofline']['frac'], d['roofline']['peak'], d['clocks'], d['speedup_vs_bf16'], d['cfg2']['value'], d['cfg3']['value'], d['e2e']['value'])
-r=json.loads(open('gpurun_out/r72_ref.json').read().strip().splitlines()[-1]); print('ref', r['value'], r['unit'], r.get('cpu_baseline',{}).get('cores'))"
+import json; d=json.loads(open('gpurun_out/r73_bench_n4.json').read().strip().splitlines()[-1])
+print(d['value'], d['n_gpus'], d['ms_per_step'], d['compute_only']['value'], d['e2e']['value'], d['clocks'], d.get('cpu_baseline'))
+r=open('gpurun_out/r73_ref_n4.json').read().strip().splitlines(); print(len(r), r[-1][:200])"
