@@ -134,9 +134,16 @@ LOKA_DEVINL void ql_tile(int64_t t, int nbc, int nbr, int& tr, int& tc) {
   }
 }
 
-template <int FMT, int SF, int GRAN, bool QT>
+// NG consumer groups: 2 (4 warps each, alternate tiles) or 1 (all 8 warps on every tile).  Two groups
+// hide each other's barrier and reciprocal latencies — better when a CTA has few tiles (32768 x 4096:
+// ~55); one group keeps more loads in flight per tile in the long steady state (262144 x 4096: ~440
+// tiles per CTA, 8-10% faster there).  The launch picks by tiles per CTA.
+template <int FMT, int SF, int GRAN, bool QT, int NG>
 __global__ void __launch_bounds__(kQlThreads, 1) quant_tile_tma_kernel(const __grid_constant__ QuantTileParams P) {
   using L = QlLayout<QT>;
+  constexpr int WG = 8 / NG;    // warps per group
+  constexpr int TG = 32 * WG;   // threads per group
+  constexpr int RW = 128 / WG;  // tile rows per warp (16 or 32): RW / 16 half-passes of 8 rows per lane
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const QuantParams& p = P.p;
@@ -150,7 +157,7 @@ __global__ void __launch_bounds__(kQlThreads, 1) quant_tile_tma_kernel(const __g
     for (int s = 0; s < L::kStages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&full_bar[L::kStages + s], 1);
-      mbar_init(&empty_bar[s], 4);  // the consuming group's 4 warps
+      mbar_init(&empty_bar[s], WG);  // the consuming group's warps
     }
     fence_barrier_init();
   }
@@ -165,7 +172,7 @@ __global__ void __launch_bounds__(kQlThreads, 1) quant_tile_tma_kernel(const __g
       uint32_t ph = 0;
       for (int64_t t = blockIdx.x; t < P.ntiles; t += gridDim.x, ++k) {
         mbar_wait(&empty_bar[s], ph ^ 1u, 1);
-        uint64_t* fb = &full_bar[(k & 1) * L::kStages + s];  // tile k goes to group k & 1
+        uint64_t* fb = &full_bar[(k % NG) * L::kStages + s];  // tile k goes to group k % NG
         mbar_arrive_expect_tx(fb, (uint32_t)kQlIn);
         int tr, tc;
         ql_tile<QT>(t, P.nbc, P.nbr, tr, tc);
@@ -184,14 +191,12 @@ __global__ void __launch_bounds__(kQlThreads, 1) quant_tile_tma_kernel(const __g
   constexpr bool kRowBlk = GRAN == LOKA_GRAN_BLK_1x128 || kDual;       // half-warp granules
   constexpr bool kColRed = GRAN == LOKA_GRAN_BLK_128x1 || GRAN == LOKA_GRAN_BLK_128x128 || kDual;
   constexpr bool kColwise = GRAN == LOKA_GRAN_BLK_128x1 || GRAN == LOKA_GRAN_COL;  // q's r per column
-  const int g = warp >> 2, gw = warp & 3, gt = threadIdx.x & 127;
+  const int g = warp / WG, gw = warp % WG, gt = threadIdx.x % TG;
   const uint32_t bar_id = 1u + (uint32_t)g;
   const int hl = lane & 15, hw = lane >> 4, cl = hl * 8;
-  const uint32_t red = smem_u32(smem + L::kOffRed) + (uint32_t)g * 2048u;
+  const uint32_t red = smem_u32(smem + L::kOffRed) + (uint32_t)g * 2048u;  // [WG][128] per group
   const uint32_t rb = smem_u32(smem + L::kOffR) + (uint32_t)g * 512u;
   const uint32_t red2 = smem_u32(smem + L::kOffRed2) + (uint32_t)g * 16u;
-  const uint32_t sq = smem_u32(smem + L::kOffQ) + (uint32_t)g * 16384u;
-  const uint32_t sqt = smem_u32(smem + L::kOffQT) + (uint32_t)g * 16384u;
   const uint32_t tq = smem_u32(smem + L::kOffTQ) + (uint32_t)g * 16384u;
   const bool want_q = p.q != nullptr;
   float r_tensor = 1.f;
@@ -203,24 +208,28 @@ __global__ void __launch_bounds__(kQlThreads, 1) quant_tile_tma_kernel(const __g
       if (p.scales_t) p.scales_t[0] = s_t;
     }
   }
-  for (int64_t k = g;; k += 2) {
+  for (int64_t k = g;; k += NG) {
     const int64_t t = blockIdx.x + k * (int64_t)gridDim.x;
     if (t >= P.ntiles) break;
     const int s = (int)(k % L::kStages);
-    constexpr int kPeriod = L::kStages % 2 ? 2 * L::kStages : L::kStages;  // lcm(stages, 2)
+    constexpr int kPeriod = (NG == 2 && L::kStages % 2) ? 2 * L::kStages : L::kStages;  // lcm(stages, NG)
     const uint32_t ph = (uint32_t)((k / kPeriod) & 1);  // this group's earlier fills of its barrier
     int tr, tc;
     ql_tile<QT>(t, P.nbc, P.nbr, tr, tc);
     const int64_t c0 = (int64_t)tc * 128, r0 = (int64_t)tr * 128;
     if (lane == 0) mbar_wait(&full_bar[g * L::kStages + s], ph, 2);
     __syncwarp();
-    const uint32_t src = smem_u32(smem + s * kQlIn) + (uint32_t)(gw * 32 + hw) * 256u + (uint32_t)hl * 16u;
+    const uint32_t src = smem_u32(smem + s * kQlIn) + (uint32_t)(gw * RW + hw) * 256u + (uint32_t)hl * 16u;
+    // staging tiles: one per group (NG = 2), or double-buffered for the single group (NG = 1)
+    const int sbuf = NG == 2 ? g : (int)(k & 1);
+    const uint32_t sq = smem_u32(smem + L::kOffQ) + (uint32_t)sbuf * 16384u;
+    const uint32_t sqt = smem_u32(smem + L::kOffQT) + (uint32_t)sbuf * 16384u;
     // ---- column-like granules: per-column partial max of this warp's 32 rows ----
     if constexpr (kColRed) {
       // columns (2j, 2j+1) share a word: 16-bit |x| maxima, two per max.u16x2
       uint32_t pk[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
+      for (int i = 0; i < RW / 2; ++i) {
         const uint4 w = lds_u4(src + (uint32_t)i * 512u);
         pk[0] = vmax_u16x2(pk[0], w.x & 0x7FFF7FFFu);
         pk[1] = vmax_u16x2(pk[1], w.y & 0x7FFF7FFFu);
@@ -239,12 +248,13 @@ __global__ void __launch_bounds__(kQlThreads, 1) quant_tile_tma_kernel(const __g
         sts_u4(a, make_uint4(cm[0], cm[1], cm[2], cm[3]));
         sts_u4(a + 16u, make_uint4(cm[4], cm[5], cm[6], cm[7]));
       }
-      named_bar_sync(bar_id, 128);  // (A) partials complete
+      named_bar_sync(bar_id, TG);  // (A) partials complete
     }
     if constexpr (GRAN == LOKA_GRAN_BLK_128x1 || kDual) {  // thread gt finalises column c0 + gt
+     if (gt < 128) {
       uint32_t m = 0;
 #pragma unroll
-      for (int w = 0; w < 4; ++w) m = max(m, lds_u32(red + (uint32_t)(w * 128 + gt) * 4u));
+      for (int w = 0; w < WG; ++w) m = max(m, lds_u32(red + (uint32_t)(w * 128 + gt) * 4u));
       float sc, r;
       scales_from_amax<FMT, SF>(__uint_as_float(m), sc, r);
       asm volatile("st.shared.f32 [%0], %1;" ::"r"(rb + (uint32_t)gt * 4u), "f"(r) : "memory");
@@ -254,13 +264,17 @@ __global__ void __launch_bounds__(kQlThreads, 1) quant_tile_tma_kernel(const __g
         if (!kDual && p.scales) p.scales[(int64_t)tr * p.cols + cc] = sc;  // [nbr, cols]
         if (p.scales_t) p.scales_t[cc * P.nbr + tr] = sc;                   // t-frame 1x128 [cols, nbr]
       }
+     }
     } else if constexpr (GRAN == LOKA_GRAN_BLK_128x128) {
-      uint32_t m = 0;
+      if (gt < 128) {  // warps gw = 0..3 each reduce 32 columns
+        uint32_t m = 0;
 #pragma unroll
-      for (int w = 0; w < 4; ++w) m = max(m, lds_u32(red + (uint32_t)(w * 128 + gt) * 4u));
-      m = warp_max_u32(m);
-      if (lane == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(red2 + (uint32_t)gw * 4u), "r"(m) : "memory");
+        for (int w = 0; w < WG; ++w) m = max(m, lds_u32(red + (uint32_t)(w * 128 + gt) * 4u));
+        m = warp_max_u32(m);
+        if (lane == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(red2 + (uint32_t)gw * 4u), "r"(m) : "memory");
+      }
     } else if constexpr (GRAN == LOKA_GRAN_ROW || GRAN == LOKA_GRAN_COL) {  // from the pre-pass array
+     if (gt < 128) {
       const bool row_g = GRAN == LOKA_GRAN_ROW;
       const int64_t idx = (row_g ? r0 : c0) + gt;
       const bool ok = idx < (row_g ? p.rows : p.cols);
@@ -271,11 +285,15 @@ __global__ void __launch_bounds__(kQlThreads, 1) quant_tile_tma_kernel(const __g
         if (p.scales) p.scales[idx] = sc;
         if (p.scales_t) p.scales_t[idx] = sc;
       }
+     }
     }
     // (B) the group's staging tiles free (its store thread waits for the previous stores' reads
     // here) and this tile's per-row / per-column r ready
-    if (gt == 0) bulk_wait_read0();
-    named_bar_sync(bar_id, 128);
+    if (gt == 0) {
+      if constexpr (NG == 2) bulk_wait_read0();
+      else bulk_wait_read_le1();  // (double-buffered staging)
+    }
+    named_bar_sync(bar_id, TG);
     float rcol[8];
     if constexpr (kColwise || kDual) {
       const float4 a = lds_f4(rb + (uint32_t)cl * 4u), b = lds_f4(rb + (uint32_t)cl * 4u + 16u);
@@ -296,11 +314,11 @@ __global__ void __launch_bounds__(kQlThreads, 1) quant_tile_tma_kernel(const __g
     // ---- two half-passes of 8 rows: load, (1x128) reduce, cast into the staging tiles (a lane's
     // 16 rows at once measured slower: 168 registers, and no gain from the earlier stage release) ----
 #pragma unroll 1
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < RW / 16; ++h) {
       uint4 vh[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) vh[i] = lds_u4(src + (uint32_t)(8 * h + i) * 512u);
-      if (h == 1) {
+      if (h == RW / 16 - 1) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[s]);  // the group's last read of the stage
       }
@@ -326,7 +344,7 @@ __global__ void __launch_bounds__(kQlThreads, 1) quant_tile_tma_kernel(const __g
         const uint32_t mine = b2 ? (b1 ? x3 : x2) : (b1 ? x1 : x0);
         float sc, r;
         scales_from_amax<FMT, SF>(__uint_as_float(mine), sc, r);
-        const int64_t row = r0 + gw * 32 + 2 * (8 * h + (lane & 7)) + hw;
+        const int64_t row = r0 + gw * RW + 2 * (8 * h + (lane & 7)) + hw;
         if ((lane & 8) == 0 && row < p.rows) {
           if (mine >= 0x7F800000u && p.status) atomicOr(p.status, LOKA_DEVSTATUS_NONFINITE);
           if (p.scales) p.scales[row * P.nbc + tc] = sc;
@@ -339,13 +357,13 @@ __global__ void __launch_bounds__(kQlThreads, 1) quant_tile_tma_kernel(const __g
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           float r;
-          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(r) : "r"(rb + (uint32_t)(gw * 32 + 2 * (8 * h + i) + hw) * 4u));
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(r) : "r"(rb + (uint32_t)(gw * RW + 2 * (8 * h + i) + hw) * 4u));
           rrow[i] = r;
         }
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const int lr = gw * 32 + 2 * (8 * h + i) + hw;
+        const int lr = gw * RW + 2 * (8 * h + i) + hw;
         const uint2 code = kColwise ? cast8_col<FMT>(vh[i], rcol) : cast8_row<FMT>(vh[i], rrow[i]);
         if (want_q) sts_u2(sq + sw128_off(lr, cl), code.x, code.y);
         if constexpr (QT) {
@@ -355,10 +373,10 @@ __global__ void __launch_bounds__(kQlThreads, 1) quant_tile_tma_kernel(const __g
       }
     }
     if constexpr (QT) {
-      named_bar_sync(bar_id, 128);  // (C) the code tile is complete
+      named_bar_sync(bar_id, TG);  // (C) the code tile is complete
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int item = gt + 128 * u;
+      for (int u = 0; u < 512 / TG; ++u) {
+        const int item = gt + TG * u;
         const int rg = item & 15, cg = item >> 4;  // rows 8rg .. 8rg+7, columns 4cg .. 4cg+3
         uint32_t w[8];
 #pragma unroll
@@ -371,10 +389,10 @@ __global__ void __launch_bounds__(kQlThreads, 1) quant_tile_tma_kernel(const __g
       }
     }
     fence_proxy_async_smem();     // staging writes -> the TMA stores
-    named_bar_sync(bar_id, 128);  // (D) staging complete (and, with QT, the code tile's reads done)
+    named_bar_sync(bar_id, TG);  // (D) staging complete (and, with QT, the code tile's reads done)
     if (gt == 0) {
-      if (want_q) tma_store_2d(&P.tq, smem + L::kOffQ + g * 16384, (int32_t)c0, (int32_t)r0);
-      if constexpr (QT) tma_store_2d(&P.tqt, smem + L::kOffQT + g * 16384, (int32_t)r0, (int32_t)c0);
+      if (want_q) tma_store_2d(&P.tq, smem + L::kOffQ + sbuf * 16384, (int32_t)c0, (int32_t)r0);
+      if constexpr (QT) tma_store_2d(&P.tqt, smem + L::kOffQT + sbuf * 16384, (int32_t)r0, (int32_t)c0);
       bulk_commit();
     }
   }
@@ -395,7 +413,15 @@ bool quant_tile_tma_eligible(int gran) {
 
 template <int FMT, int SF, int GRAN, bool QT>
 static cudaError_t launch_ql(const QuantTileParams& tp, int num_sms, cudaStream_t st) {
-  auto kern = quant_tile_tma_kernel<FMT, SF, GRAN, QT>;
+  // two consumer groups when each CTA gets few tiles; one in the long steady state for the granules
+  // measured faster that way at 262144 x 4096 (~440 tiles per CTA): 1x128 5.91 vs 5.53, 128x128 6.29
+  // vs 5.90, 128x1 + transpose 5.71 vs 4.97 TB/s — while 128x1 (5.52 vs 5.82) and ROW + transpose
+  // (3.59 vs 4.46) stay faster with two (profiles/r02ai_quantize_262k_groups.json)
+  constexpr bool kOneWhenLong = GRAN == LOKA_GRAN_BLK_1x128 || GRAN == LOKA_GRAN_BLK_128x128 ||
+                                (GRAN == LOKA_GRAN_BLK_128x1 && QT);
+  bool two = !kOneWhenLong || tp.ntiles <= (int64_t)num_sms * 128;
+  if (const char* e = std::getenv("LOKA_QUANT_GROUPS")) two = e[0] != '1';  // (tests / A-B: 1 or 2)
+  auto kern = two ? quant_tile_tma_kernel<FMT, SF, GRAN, QT, 2> : quant_tile_tma_kernel<FMT, SF, GRAN, QT, 1>;
   constexpr int smem = QlLayout<QT>::kSmem;
   cudaError_t e = ensure_func_attrs(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;

@@ -245,13 +245,15 @@ def test_delayed_scaling_phase(dtype, rows, fmt):
 @pytest.mark.parametrize("gran,gran_t", [("blk_1x128", None), ("blk_128x1", None), ("blk_128x128", None),
                                          ("blk_1x128", "blk_1x128"), ("row", None), ("col", None)])
 @pytest.mark.parametrize("transpose", [False, True])
-def test_streaming_tile_many_tiles_sampled(gran, gran_t, transpose):
+@pytest.mark.parametrize("groups", ["2", "1"])
+def test_streaming_tile_many_tiles_sampled(gran, gran_t, transpose, groups, monkeypatch):
     """The streaming tile kernel (quantize_tile.cu) with ~28 tiles per CTA, so both consumer groups
     and every stage of the ring wrap many times (a parity race there showed only at this scale):
     16384 x 2048 heavy-tailed bf16, sampled 128 x 128 tiles (block granules depend on their tile
     only), rows (ROW) or columns (COL) checked bit-exact, codes and transposed codes and scales."""
     if gran_t is not None and not transpose:
         pytest.skip("dual needs the transposed copy")
+    monkeypatch.setenv("LOKA_QUANT_GROUPS", groups)  # both consumer-group layouts of the kernel
     R, C = 16384, 2048
     x = synth.heavy(R, C, 7, device=DEV)
     res = lk.loka_quantize(x, "e4m3", gran, transpose=transpose, gran_t=gran_t)
