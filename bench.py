@@ -851,7 +851,11 @@ def main():
     fp8_peak_sus, fp8_peak_burst = 2.0 * bf16_sus, 2.0 * bf16_peak  # nominal fp8/bf16 = 4500/2250
     # the denominator: the burst peak when the SM clock held its maximum through the timed steps (the
     # measured sustained figure was taken at ~1.3 GHz under a 4 s cuBLAS loop), else the sustained one
-    at_max = clocks.get("sm_mhz") is not None and clocks["sm_mhz"] >= 0.97 * float(clocks.get("sm_max_mhz") or 1e9)
+    # (and no throttle reason at all: with sw_power_cap in the samples the median clock can still read
+    # max while the kernel ran capped part of the time — profiles/r02aj_bench.json: 1965 MHz median,
+    # sw_power_cap, the fused kernel at 2538 TF/s)
+    at_max = (clocks.get("sm_mhz") is not None and clocks["sm_mhz"] >= 0.97 * float(clocks.get("sm_max_mhz") or 1e9)
+              and not clocks.get("reasons"))
     fp8_peak = fp8_peak_burst if at_max else fp8_peak_sus
     achieved = step.flops / (lin_ms * 1e-3) / 1e12
     traffic = None
