@@ -1,10 +1,10 @@
 # scratch driver for one gpurun call (overwritten per experiment)
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_probe.py -m gpu -q -x > gpurun_out/r85_t.log 2>&1; echo "EXIT $?" >> gpurun_out/r85_t.log
-grep -v "^\[W" gpurun_out/r85_t.log | tail -3
-timeout 600 python tools/bench_probe.py --out gpurun_out/r85_probe.json > /dev/null 2> gpurun_out/r85_p.err
-LOKA_PROBE_TWO_PASS=1 timeout 600 python tools/bench_probe.py --out gpurun_out/r85_probe_2p.json > /dev/null 2>> gpurun_out/r85_p.err
+timeout 300 python tools/example_readme.py > gpurun_out/r86_example.txt 2>&1; echo "EXIT $?" >> gpurun_out/r86_example.txt
+timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r86_gpu_tests.txt 2>&1; echo "EXIT $?" >> gpurun_out/r86_gpu_tests.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/r86_smoke.txt 2>&1
+timeout 900 python bench.py > gpurun_out/r86_bench.json 2> gpurun_out/r86_bench.err
+tail -2 gpurun_out/r86_example.txt; grep -v "^\[W" gpurun_out/r86_gpu_tests.txt | tail -2; tail -1 gpurun_out/r86_smoke.txt
 python -c "
-import json
-for f in ('r85_probe','r85_probe_2p'):
-    d=json.load(open('gpurun_out/'+f+'.json')); print(f, [(c['case'][:20], c['ms'], c['gbs']) for c in d['cases']], d['clocks'].get('sm_mhz'))"
+import json; d=json.loads(open('gpurun_out/r86_bench.json').read().strip().splitlines()[-1])
+print(d['value'], d['ms_per_step'], d['compute_only']['value'], d['roofline']['frac'], d['roofline']['peak'], d['clocks'], d['speedup_vs_bf16'], d['cfg2']['value'], d['cfg3']['value'], d['e2e']['value'])"
