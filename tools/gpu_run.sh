@@ -1,10 +1,5 @@
 # scratch driver for one gpurun call (overwritten per experiment)
 mkdir -p gpurun_out
-timeout 300 python tools/example_readme.py > gpurun_out/r86_example.txt 2>&1; echo "EXIT $?" >> gpurun_out/r86_example.txt
-timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r86_gpu_tests.txt 2>&1; echo "EXIT $?" >> gpurun_out/r86_gpu_tests.txt
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/r86_smoke.txt 2>&1
-timeout 900 python bench.py > gpurun_out/r86_bench.json 2> gpurun_out/r86_bench.err
-tail -2 gpurun_out/r86_example.txt; grep -v "^\[W" gpurun_out/r86_gpu_tests.txt | tail -2; tail -1 gpurun_out/r86_smoke.txt
-python -c "
-import json; d=json.loads(open('gpurun_out/r86_bench.json').read().strip().splitlines()[-1])
-print(d['value'], d['ms_per_step'], d['compute_only']['value'], d['roofline']['frac'], d['roofline']['peak'], d['clocks'], d['speedup_vs_bf16'], d['cfg2']['value'], d['cfg3']['value'], d['e2e']['value'])"
+timeout 300 python tools/run_stack_once.py > gpurun_out/r87.log 2>&1 && \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:stack_kernel -s 3 -c 1 -o gpurun_out/r87_stack -f python tools/run_stack_once.py > gpurun_out/r87_ncu.log 2>&1
+tail -2 gpurun_out/r87_ncu.log
