@@ -813,7 +813,8 @@ static PnPlan pair_norm_plan(const loka_linear_args* a, int sms) {
   const int env = pair_norm_env();
   if (!a || env == 0 || !use_pair_kernel() || is_mx(a) || a->save_xhat || a->save_rstd) return pl;
   const bool bwd = a->bwd_xhat != nullptr;  // NEXT-1 norm backward: bf16 / f32 dz, no bias, 256-wide tiles
-  if (bwd && (!a->bwd_rstd || a->bias || is_fp8(a->y.dtype) || (a->bwd_xhat_ld * 2) % 16 || a->bwd_xhat_ld < a->N ||
+  if (bwd && (!a->bwd_rstd || a->bias || (is_fp8(a->y.dtype) && a->y.gran != LOKA_GRAN_BLK_1x128) ||
+              (a->bwd_xhat_ld * 2) % 16 || a->bwd_xhat_ld < a->N ||
               !aligned16(a->bwd_xhat)))
     return pl;
   if (a->a.gran != LOKA_GRAN_TENSOR && a->a.gran != LOKA_GRAN_ROW) return pl;
@@ -822,7 +823,9 @@ static PnPlan pair_norm_plan(const loka_linear_args* a, int sms) {
   if (a->norm != LOKA_NORM_LAYER && a->norm != LOKA_NORM_RMS && !(blk && a->norm_block == 256)) return pl;
   if (a->M <= 0 || a->N <= 0 || a->K <= 0 || a->N > 16384) return pl;
   const bool fp8_out = is_fp8(a->y.dtype);
-  if (fp8_out && (a->gamma || a->beta || a->act != LOKA_ACT_NONE)) return pl;  // row amax not monotone
+  // forward FP8 output: the row / granule amax comes through a monotone map (no gamma / beta / act);
+  // the backward's FP8 dz (1x128) takes its amax in an extra pass instead
+  if (fp8_out && !bwd && (a->gamma || a->beta || a->act != LOKA_ACT_NONE)) return pl;
   // 256-wide tiles with double-buffered accumulators by default: the epilogue (two TMEM passes and
   // the row-record exchange) runs under the next tile's MMAs; WIDE 512-column tiles (LOKA_PAIRNORM=512)
   // move 25% fewer operand bytes per FLOP but expose the whole epilogue (measured slower)

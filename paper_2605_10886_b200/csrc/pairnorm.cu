@@ -350,7 +350,9 @@ __global__ void __launch_bounds__(kPnThreads + (CASTX ? 32 * kPnCastWarps : 0), 
     const bool xs_stage = BWD && p.out_dtype == LOKA_BF16;  // xhat staged in smem (bf16 dz boxes match it)
     uint32_t xph = 0;
     const bool fold = !p.sb_row && p.bias == nullptr && !bwd;
-    const bool need_x = xchg && (NORM != LOKA_NORM_BLOCK_RMS || fp8_out);
+    // (BlockNorm exchanges only for the forward FP8 row amax; the backward's block sums are tile-local
+    // and its FP8 dz takes 1x128 granules)
+    const bool need_x = xchg && (NORM != LOKA_NORM_BLOCK_RMS || (fp8_out && !bwd));
     float4* xrec = reinterpret_cast<float4*>(p.xws);
     int nbox = 0;
     int mb, nb;
@@ -708,8 +710,29 @@ __global__ void __launch_bounds__(kPnThreads + (CASTX ? 32 * kPnCastWarps : 0), 
         }
       }
       if (tr) tr[2] = globaltimer_ns();
+      const float mgx_keep = amax;  // backward: mean(g xhat) (the forward never reads it)
+      // backward with FP8 dz (1x128 granules, TN = 256): this thread's 128 columns are one granule; an
+      // extra TMEM pass computes dz exactly as pass N will (the same non-contracted operations) and
+      // keeps max |dz| — the granule's scale must exist before the cast
+      float dz_amax = 0.f;
+      if constexpr (BWD) {
+        if (fp8_out) {
+          auto amax_chunk = [&](float (&y)[32], int c) {
+            const int cb = 32 * c;
+            if (!fold) dequant(y, cb);
+            float xv[32];
+            load_g(y, cb, xv);
+            const int nv = max(0, min(32, p.N - (col0 + cb)));
+#pragma unroll
+            for (int k = 0; k < 32; ++k)
+              if (k < nv) dz_amax = fmaxf(dz_amax, fabsf(__fmul_rn(rstd, __fsub_rn(__fsub_rn(y[k], c0), __fmul_rn(xv[k], amax)))));
+          };
+          stream_tmem(amax_chunk, false);
+        }
+      }
       float r_out = 1.f;
       if (fp8_out) {
+        if (bwd) amax = dz_amax;  // (amax carried mean(g xhat) so far; pass N gets it from mgx below)
         // 1x128 scales (TN = 256): this thread's 128 columns are one granule; its amax comes from the
         // thread's own y max / min of pass S through the same monotone map as the row amax
         if (TN == 256 && !bwd && p.y_blk)
@@ -730,7 +753,7 @@ __global__ void __launch_bounds__(kPnThreads + (CASTX ? 32 * kPnCastWarps : 0), 
       const float rs = __fmul_rn(sc, rstd);
       const float2 r2 = make_float2(rs, rs), c02 = make_float2(c0, c0);
       float amx = 0.f;
-      const float mgx = bwd ? amax : 0.f;
+      const float mgx = bwd ? mgx_keep : 0.f;
       auto out_chunk = [&](float (&y)[32], int c) {
         const int cb = 32 * c;
         if (!fold) dequant(y, cb);
@@ -738,7 +761,7 @@ __global__ void __launch_bounds__(kPnThreads + (CASTX ? 32 * kPnCastWarps : 0), 
           float xv[32];
           load_g(y, cb, xv);
 #pragma unroll
-          for (int k = 0; k < 32; ++k) y[k] = rstd * (y[k] - c0 - xv[k] * mgx);
+          for (int k = 0; k < 32; ++k) y[k] = __fmul_rn(rstd, __fsub_rn(__fsub_rn(y[k], c0), __fmul_rn(xv[k], mgx)));
         } else {
 #pragma unroll
         for (int k = 0; k < 32; k += 4) {

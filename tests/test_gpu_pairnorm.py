@@ -297,3 +297,38 @@ def test_fp8_output_1x128_only_on_the_fused_norm_route():
     with pytest.raises(lk.LokaError) as ei:
         lk.loka_fp8_linear_norm(xq, xs, wq, ws, norm="none", out_dtype="e4m3", y_gran="blk_1x128")
     assert ei.value.status == lk.ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("norm,N,act,affine", [("layer", 4096, "none", False), ("layer", 1024, "hardswish", True),
+                                               ("rms", 768, "none", True), ("block_rms", 512, "hardswish", False)])
+@pytest.mark.parametrize("od", ["e5m2", "e4m3"])
+def test_norm_backward_fp8_dz_1x128(norm, N, act, affine, od, monkeypatch):
+    """NEXT-1 norm backward with FP8 dz and 1x128 scales (the blockwise recipe's next dgrad operand),
+    fused: the granule amax from an extra TMEM pass that computes dz with the same operations as the
+    cast pass — codes + scales bit-exact vs the oracle's 1x128 quantize of the GPU's own pre-cast dz,
+    which is within 2e-3 of oracle.linear.norm_backward."""
+    monkeypatch.setenv("LOKA_PAIRNORM", "256")
+    M, K2 = 600, 384
+    aq, as_ = lk.loka_quantize(to_dev_padded(synth.grad(M, K2, 5) * 1024), "e5m2", "row")
+    bq, bs = lk.loka_quantize(to_dev_padded(synth.weight(N, K2, 6)), "e4m3", "row")
+    rng = np.random.default_rng(N + 1)
+    xh = torch.tensor(rng.normal(size=(M, N)), dtype=torch.bfloat16)
+    nb = N // 256
+    rstd = torch.tensor(rng.uniform(0.5, 2.0, size=(M, nb) if norm == "block_rms" else (M,)), dtype=torch.float32)
+    gamma = torch.tensor(1 + 0.2 * rng.normal(size=N), dtype=torch.float32) if affine else None
+    beta = torch.tensor(0.3 * rng.normal(size=N), dtype=torch.float32) if (affine and norm == "layer") else None
+    pre = torch.full((M, N), float("nan"), dtype=torch.float32, device=DEV)
+    y, ys = lk.loka_fp8_linear_norm(aq, as_, bq, bs, a_fmt="e5m2", norm=norm, act=act, out_dtype=od,
+                                    bwd_xhat=xh.to(DEV), bwd_rstd=rstd.to(DEV), direction="dgrad",
+                                    gamma=None if gamma is None else gamma.to(DEV),
+                                    beta=None if beta is None else beta.to(DEV), precast=pre, y_gran="blk_1x128")
+    torch.cuda.synchronize()
+    oq, os_ = oracle.quantize.quantize(f64(pre), od, "blk_1x128")
+    assert_scales_equal(ys, os_)
+    assert_bytes_equal(y, oq)
+    dh = oracle.linear.linear_norm(aq.cpu().numpy(), as_.cpu().numpy(), "e5m2", "row", bq.cpu().numpy(),
+                                   bs.cpu().numpy(), "e4m3", "row")
+    dz = oracle.linear.norm_backward(dh, xh.double().numpy(), rstd.double().numpy(), norm,
+                                     gamma=None if gamma is None else gamma.double().numpy(),
+                                     beta=None if beta is None else beta.double().numpy(), act=act)
+    assert guarded_rel_err(f64(pre), dz) <= TOL

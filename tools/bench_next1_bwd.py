@@ -47,15 +47,16 @@ def main():
         ds = torch.empty(M, dtype=torch.float32, device=dev)
         sh = stream.cuda_stream
         row = {"M": M, "N": N, "K": K2}
-        for od in ("bf16", "e5m2"):
+        for od in ("bf16", "e5m2", "e5m2_1x128"):
             keep = []
-            args, y, _ = lk.make_linear_args(dq, ds, wtq, wts, a_fmt="e5m2", norm="layer", out_dtype=od,
-                                             bwd_xhat=xh, bwd_rstd=rstd, direction="dgrad", keep=keep)
+            yg = "blk_1x128" if od.endswith("1x128") else "row"
+            args, y, _ = lk.make_linear_args(dq, ds, wtq, wts, a_fmt="e5m2", norm="layer", out_dtype=od[:4],
+                                             bwd_xhat=xh, bwd_rstd=rstd, direction="dgrad", keep=keep, y_gran=yg)
 
             wsb = torch.empty(max(1, lk.linear_workspace(args)), dtype=torch.uint8, device=dev)
             tiles = -(-M // 256) * -(-N // 256)
             row[f"path_{od}"] = ("CTA-pair engine, norm backward fused in its epilogue (pairnorm.cu)"
-                                 if od == "bf16" and tiles >= 74 else
+                                 if od in ("bf16", "e5m2_1x128") and (tiles >= 74 or od != "bf16") else
                                  "CTA-pair GEMM (FP32) + row-wise backward pass (FP8 dz needs the row amax)"
                                  if tiles >= 74 else "single-CTA fused epilogue (linear.cu)")
 
@@ -79,6 +80,7 @@ def main():
         row["fp8_bf16out_tflops"] = round(fl / row["fp8_bf16_ms"] / 1e9, 1)
         row["speedup_bf16out"] = round(row["bf16_ms"] / row["fp8_bf16_ms"], 3)
         row["speedup_e5m2out"] = round(row["bf16_ms"] / row["fp8_e5m2_ms"], 3)
+        row["speedup_e5m2out_1x128_fused"] = round(row["bf16_ms"] / row["fp8_e5m2_1x128_ms"], 3)
         res["cases"].append(row)
     _clk.__exit__()
     res["clocks"] = _clk.summary()

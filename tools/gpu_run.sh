@@ -1,5 +1,8 @@
 # scratch driver for one gpurun call (overwritten per experiment)
 mkdir -p gpurun_out
-timeout 300 python tools/run_stack_once.py > gpurun_out/r87.log 2>&1 && \
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:stack_kernel -s 3 -c 1 -o gpurun_out/r87_stack -f python tools/run_stack_once.py > gpurun_out/r87_ncu.log 2>&1
-tail -2 gpurun_out/r87_ncu.log
+timeout 900 python tools/bench_next1_bwd.py > gpurun_out/r89_bwd.json 2> gpurun_out/r89_bwd.err
+tail -2 gpurun_out/r89_bwd.err
+python -c "
+import json; d=json.loads(open('gpurun_out/r89_bwd.json').read().strip().splitlines()[-1])
+for c in d['cases']: print({k: v for k, v in c.items() if not k.startswith('path')})
+print(d['clocks'])"
